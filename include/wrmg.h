@@ -1,0 +1,189 @@
+/*
+ * wrmg.h — C ABI of the B200-native waveform-relaxation multigrid hot path
+ * (space-time finite elements, arXiv 2407.13997; citations are lines of the
+ * paper's LaTeX source, /root/reference/PAPER.md, and readings R# of DESIGN.md).
+ *
+ * Discretisation: continuous Lagrange P_k (k = 1..3) in space on the structured
+ * anti-diagonal triangulation of [0, nx h] x [0, ny h], upwind
+ * DG(q) (q = 0..3) in time on N uniform slabs (eq. dgintime),
+ * heat operator of eq. heatfem with diffusion kappa.
+ *
+ * Vectors.  Every vector argument is a caller-owned DEVICE pointer (e.g. a torch
+ * float64 CUDA tensor's data_ptr()) holding one value per lattice node and
+ * temporal DoF, waveform-major (R4):
+ *     v[(i * N + n) * (q + 1) + a],   i = J * (k*nx + 1) + I,
+ * i the canonical lattice node (all nodes, constrained ones included), n the
+ * slab, a the temporal node.  Its length is wrmg_layout_t.ndof.  Constrained
+ * (Dirichlet) DoFs are identity rows (R5).
+ *
+ * Streams and synchronisation.  Every call is enqueued on coeffs.stream (NULL =
+ * legacy default stream) of coeffs.device and returns without synchronising,
+ * except calls that return scalars to the host (wrmg_fgmres, wrmg_setup,
+ * wrmg_linearize), which synchronise the stream.  Not thread-safe: one context
+ * per (device, stream).
+ *
+ * Errors.  Every call returns a wrmg_status.  WRMG_E_SINGULAR carries the
+ * (level, patch, slab) of the failing pivot (wrmg_last_error).  On error the
+ * output buffers are unspecified.  Kernel-side failures are reported at the next
+ * synchronising call.  No call falls back to a CPU implementation.
+ */
+#ifndef WRMG_H
+#define WRMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct wrmg_ctx wrmg_ctx; /* opaque; owned by the library, freed by wrmg_destroy */
+
+typedef enum {
+  WRMG_OK = 0,
+  WRMG_E_INVALID = 1,       /* bad argument (null pointer, size, R <= 0, ...) */
+  WRMG_E_UNSUPPORTED = 2,   /* degree / problem / configuration not built */
+  WRMG_E_OOM = 3,           /* device allocation failed */
+  WRMG_E_SINGULAR = 4,      /* |pivot| < 1e-14 * max row norm in a patch or coarse block (R10) */
+  WRMG_E_BREAKDOWN = 5,     /* FGMRES: h_{j+1,j} < 1e-30 before convergence (R16) */
+  WRMG_E_NOT_CONVERGED = 6, /* FGMRES: maxit reached */
+  WRMG_E_CUDA = 7,          /* CUDA runtime error (message in wrmg_last_error) */
+  WRMG_E_NCCL = 8
+} wrmg_status;
+
+enum { WRMG_HEAT = 0, WRMG_NAVIER_STOKES = 1 };
+enum { WRMG_BC_DIRICHLET0 = 0, WRMG_BC_NEUMANN = 1, WRMG_BC_LID = 2 };
+enum { WRMG_W_POU = 0, WRMG_W_NONE = 1 };  /* scatter weights W_p = 1/mu (R11) or 1 */
+
+typedef struct {
+  int32_t gnx, gny;  /* global cells per side of the anti-diagonal lattice mesh */
+  int32_t x0, nx;    /* this rank's strip: first cell column and number of columns (x0 = 0, nx = gnx on 1 GPU) */
+  double h;          /* cell size; domain [0, gnx h] x [0, gny h] */
+  int32_t ncoarse;   /* coarsest level: coarsen while min(nx, ny) > ncoarse (R14; 0 -> 4) */
+} wrmg_mesh;
+
+typedef struct {
+  int32_t problem;      /* WRMG_HEAT (WRMG_NAVIER_STOKES: WRMG_E_UNSUPPORTED in this build) */
+  int32_t bc;           /* WRMG_BC_DIRICHLET0 (homogeneous Dirichlet on the whole boundary) */
+  double kappa;         /* diffusion coefficient (> 0) */
+  double reynolds;      /* Navier-Stokes only */
+  double lid_speed;     /* Navier-Stokes only */
+  int32_t weights;      /* WRMG_W_POU (default) | WRMG_W_NONE */
+  double omega_mg;      /* smoother damping inside the V-cycle (R15; 0 -> 1.0) */
+  int32_t nu_pre, nu_post; /* V(nu_pre, nu_post) (R15; 0,0 -> 1,1) */
+  int32_t factor_mode;  /* reserved (Navier-Stokes STORE / RECOMPUTE) */
+  int32_t device;       /* CUDA device ordinal */
+  void *stream;         /* cudaStream_t; NULL = default stream */
+  int32_t rank, nranks; /* strip partition (nranks = 1 in this build) */
+  const void *nccl_unique_id; /* reserved */
+} wrmg_coeffs;
+
+typedef struct {
+  int64_t nnode;        /* lattice nodes of the finest level owned by this rank */
+  int64_t nt;           /* temporal DoFs per node, N (q + 1) */
+  int64_t ndof;         /* vector length nnode * nt */
+  int64_t nfree_st;     /* free (unconstrained) space-time DoFs */
+  int32_t lx, ly;       /* lattice nodes per direction: k nx + 1, k ny + 1 */
+  int32_t nlevels;      /* multigrid levels (coarse + ... + fine) */
+  int32_t degree, q, nslabs;
+  int64_t npatch;       /* finest-level patches (R8) */
+  int32_t mp_max;       /* largest spatial patch size */
+  int32_t npatch_types; /* distinct finest-level patch blocks factored (translation classes) */
+  int64_t smooth_dof_updates_per_vcycle; /* sum over levels >= 1 of free space-time DoFs x (nu_pre + nu_post) */
+} wrmg_layout_t;
+
+/* Build the hierarchy on the device.  PAPER.md:351-360 (space-only coarsening),
+ * PAPER.md:381 (P = I (x) P_h, vertex-star patches).  Host: lattice maps, CSR
+ * patterns and patch tables (integer setup, H3).  Device kernels: spatial
+ * assembly (H1), patch blocks (H4), batched LU (H5), coarse factorisation.
+ * degree = k in {1,2,3}; q in {0,1,2,3}; nslabs = N >= 1; dt > 0.
+ * Synchronises.  *out receives the context (NULL on error). */
+wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, double dt,
+                       const wrmg_coeffs *coeffs, wrmg_ctx **out);
+
+/* Sizes of the finest level (host struct filled). */
+wrmg_status wrmg_layout(const wrmg_ctx *ctx, wrmg_layout_t *out);
+
+/* (Re)factorise every patch and coarse block for the operator linearised at
+ * `state` (device vector, NULL for the linear heat operator).  Heat: recomputes
+ * H1/H4/H5 on the device.  Synchronises; WRMG_E_SINGULAR on a failed pivot. */
+wrmg_status wrmg_linearize(wrmg_ctx *ctx, const double *state);
+
+/* b = (M (x) I_N (x) Mt) fhat on free rows, bc value on constrained rows
+ * (forcing term of eq. heatfem with f = sum fhat phi; R6).  fhat: ndof values. */
+wrmg_status wrmg_rhs(wrmg_ctx *ctx, const double *fhat, double *b);
+
+/* r = b - A u on the finest level (H6; eq. heatfem; constrained rows r = b - u).
+ * `nonlinear` is reserved (0).  r may not alias u or b. */
+wrmg_status wrmg_residual(wrmg_ctx *ctx, const double *u, const double *b, double *r, int32_t nonlinear);
+
+/* y = A x (Krylov matvec; constrained rows y = x). */
+wrmg_status wrmg_apply(wrmg_ctx *ctx, const double *x, double *y);
+
+/* nsweeps additive waveform-relaxation sweeps on the finest level, in place on u
+ * (H6 + H7 + H8, R9-R11):
+ *   r = b - A u;  for every patch p, for n = 0..N-1:  x_{p,n} = D_p^{-1}(r_{p,n} - L_p x_{p,n-1});
+ *   u += omega * sum_p R_p^T W_p x_p. */
+wrmg_status wrmg_smooth(wrmg_ctx *ctx, double *u, const double *b, int32_t nsweeps, double omega);
+
+/* z = B r: one V(nu_pre, nu_post) cycle from a zero initial guess (H9-H12;
+ * PAPER.md:361-366).  r must vanish on constrained rows (corrections, R5). */
+wrmg_status wrmg_vcycle(wrmg_ctx *ctx, const double *r, double *z);
+
+/* Restriction / prolongation between finest-level `level` (>= 1, counted from the
+ * coarsest = 0) and level-1 (H9, H10; PAPER.md:381 R = P^T, P = I (x) P_h).  The
+ * vectors have the layouts of the respective levels (wrmg_level_size). */
+wrmg_status wrmg_restrict(wrmg_ctx *ctx, int32_t level, const double *r_fine, double *r_coarse);
+wrmg_status wrmg_prolong_add(wrmg_ctx *ctx, int32_t level, const double *e_coarse, double *u_fine);
+/* Number of lattice nodes of a level (vector length = nodes * nt). */
+wrmg_status wrmg_level_size(const wrmg_ctx *ctx, int32_t level, int64_t *nnode);
+
+/* Right-preconditioned FGMRES(restart) with CGS2, x0 = 0 (H13; PAPER.md:361-366,
+ * R16).  Stops when |g_{j+1}| <= max(rtol ||b||, atol).  x receives the iterate,
+ * *iters the number of preconditioner applications, *relres the final true
+ * relative residual ||b - A x|| / ||b||.  Synchronises every Arnoldi step.
+ * Returns WRMG_OK, WRMG_E_BREAKDOWN or WRMG_E_NOT_CONVERGED (x still valid). */
+wrmg_status wrmg_fgmres(wrmg_ctx *ctx, const double *b, double *x, int32_t restart, int32_t maxit,
+                        double rtol, double atol, int32_t *iters, double *relres);
+
+/* Navier-Stokes Newton loop (H14): WRMG_E_UNSUPPORTED in this build. */
+wrmg_status wrmg_newton(wrmg_ctx *ctx, double *U, double rtol, int32_t maxit, int32_t *newton_its,
+                        int32_t *lin_its);
+
+/* Batched dense LU with partial pivoting (H5, R10) on caller device memory:
+ * A holds `batch` column-major m x m matrices (A + b*m*m), overwritten by the
+ * factors (unit-lower L below the diagonal, U on and above, LAPACK dgetrf
+ * layout); piv (batch*m int32) receives 0-based pivot rows; info (batch int32)
+ * receives 0 or 1 + the first singular column.  Synchronises.
+ * Returns WRMG_E_SINGULAR if any info != 0. */
+wrmg_status wrmg_batched_lu(const wrmg_ctx *ctx, double *A, int32_t m, int32_t batch, int32_t *piv,
+                            int32_t *info);
+
+/* Counter-based generator of R6 (splitmix64 finaliser) on the device:
+ * out[t] = U[-1,1) at canonical id first_id + t, t < count. */
+wrmg_status wrmg_fill_uniform(const wrmg_ctx *ctx, double *out, int64_t count, uint64_t first_id,
+                              uint64_t seed);
+
+/* Wait for all work enqueued on the context's stream; reports deferred kernel errors. */
+wrmg_status wrmg_sync(wrmg_ctx *ctx);
+
+/* Last error message (thread-local when ctx is NULL); level/patch/slab of a
+ * singular pivot when the last status was WRMG_E_SINGULAR (else -1). */
+const char *wrmg_last_error(const wrmg_ctx *ctx, int32_t *level, int32_t *patch, int32_t *slab);
+
+/* Free every device and host resource of the context. */
+void wrmg_destroy(wrmg_ctx *ctx);
+
+/* Host-only planning query (no device needed): sizes of the finest level and
+ * hierarchy for a configuration, for tests of the host setup logic (H3). */
+wrmg_status wrmg_plan(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs,
+                      wrmg_layout_t *out);
+
+/* Host-only: the finest-level patch table (H3, R8).  nodes receives npatch *
+ * mp_max int32 canonical node ids (-1 padded), sizes npatch int32 sizes; either
+ * may be NULL.  Buffers are host memory owned by the caller. */
+wrmg_status wrmg_plan_patches(const wrmg_mesh *mesh, int32_t degree, int32_t *nodes, int32_t *sizes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WRMG_H */

@@ -1,0 +1,217 @@
+"""ctypes marshalling for include/wrmg.h.  Names follow the C ABI."""
+import ctypes
+import os
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwrmg.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                      "there is no CPU fallback")
+lib = ctypes.CDLL(LIB_PATH)
+
+c_i32, c_i64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+
+STATUS = {0: "WRMG_OK", 1: "WRMG_E_INVALID", 2: "WRMG_E_UNSUPPORTED", 3: "WRMG_E_OOM", 4: "WRMG_E_SINGULAR",
+          5: "WRMG_E_BREAKDOWN", 6: "WRMG_E_NOT_CONVERGED", 7: "WRMG_E_CUDA", 8: "WRMG_E_NCCL"}
+
+
+class wrmg_mesh(ctypes.Structure):
+    _fields_ = [("gnx", c_i32), ("gny", c_i32), ("x0", c_i32), ("nx", c_i32), ("h", c_dbl), ("ncoarse", c_i32)]
+
+
+class wrmg_coeffs(ctypes.Structure):
+    _fields_ = [("problem", c_i32), ("bc", c_i32), ("kappa", c_dbl), ("reynolds", c_dbl), ("lid_speed", c_dbl),
+                ("weights", c_i32), ("omega_mg", c_dbl), ("nu_pre", c_i32), ("nu_post", c_i32),
+                ("factor_mode", c_i32), ("device", c_i32), ("stream", c_vp), ("rank", c_i32), ("nranks", c_i32),
+                ("nccl_unique_id", c_vp)]
+
+
+class wrmg_layout_t(ctypes.Structure):
+    _fields_ = [("nnode", c_i64), ("nt", c_i64), ("ndof", c_i64), ("nfree_st", c_i64), ("lx", c_i32),
+                ("ly", c_i32), ("nlevels", c_i32), ("degree", c_i32), ("q", c_i32), ("nslabs", c_i32),
+                ("npatch", c_i64), ("mp_max", c_i32), ("npatch_types", c_i32),
+                ("smooth_dof_updates_per_vcycle", c_i64)]
+
+
+_P = ctypes.POINTER
+_sig = {
+    "wrmg_setup": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, c_dbl, _P(wrmg_coeffs), _P(c_vp)]),
+    "wrmg_layout": (c_i32, [c_vp, _P(wrmg_layout_t)]),
+    "wrmg_linearize": (c_i32, [c_vp, c_vp]),
+    "wrmg_rhs": (c_i32, [c_vp, c_vp, c_vp]),
+    "wrmg_residual": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32]),
+    "wrmg_apply": (c_i32, [c_vp, c_vp, c_vp]),
+    "wrmg_smooth": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_dbl]),
+    "wrmg_vcycle": (c_i32, [c_vp, c_vp, c_vp]),
+    "wrmg_restrict": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
+    "wrmg_prolong_add": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
+    "wrmg_level_size": (c_i32, [c_vp, c_i32, _P(c_i64)]),
+    "wrmg_fgmres": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_dbl, c_dbl, _P(c_i32), _P(c_dbl)]),
+    "wrmg_newton": (c_i32, [c_vp, c_vp, c_dbl, c_i32, _P(c_i32), _P(c_i32)]),
+    "wrmg_batched_lu": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "wrmg_fill_uniform": (c_i32, [c_vp, c_vp, c_i64, ctypes.c_uint64, ctypes.c_uint64]),
+    "wrmg_sync": (c_i32, [c_vp]),
+    "wrmg_last_error": (ctypes.c_char_p, [c_vp, _P(c_i32), _P(c_i32), _P(c_i32)]),
+    "wrmg_destroy": (None, [c_vp]),
+    "wrmg_plan": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, _P(wrmg_layout_t)]),
+    "wrmg_plan_patches": (c_i32, [_P(wrmg_mesh), c_i32, c_vp, c_vp]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def exported_symbols():
+    return sorted(_sig)
+
+
+class WrmgError(RuntimeError):
+    def __init__(self, status, msg, where=None):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}" + (f" at {where}" if where else ""))
+        self.status = status
+        self.where = where
+
+
+def _check(st, ctx=None):
+    if st != 0:
+        lv, p, s = c_i32(), c_i32(), c_i32()
+        msg = lib.wrmg_last_error(ctx, ctypes.byref(lv), ctypes.byref(p), ctypes.byref(s))
+        where = (lv.value, p.value, s.value) if st == 4 else None
+        raise WrmgError(st, (msg or b"").decode(), where)
+
+
+def _ptr(t):
+    """Device pointer of a float64 / int32 CUDA tensor (contiguous)."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+        raise TypeError("expected a contiguous CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _mesh(nx, ny, h, ncoarse):
+    return wrmg_mesh(int(nx), int(ny), 0, int(nx), float(h), int(ncoarse))
+
+
+def wrmg_plan(nx, ny, h, degree, q, nslabs, ncoarse=4):
+    out = wrmg_layout_t()
+    _check(lib.wrmg_plan(ctypes.byref(_mesh(nx, ny, h, ncoarse)), degree, q, nslabs, ctypes.byref(out)))
+    return {f: getattr(out, f) for f, _ in wrmg_layout_t._fields_}
+
+
+def wrmg_plan_patches(nx, ny, h, degree):
+    lay = wrmg_plan(nx, ny, h, degree, 0, 1)
+    npatch, mp = lay["npatch"], lay["mp_max"]
+    nodes = np.empty((npatch, mp), dtype=np.int32)
+    sizes = np.empty(npatch, dtype=np.int32)
+    _check(lib.wrmg_plan_patches(ctypes.byref(_mesh(nx, ny, h, 4)), degree,
+                                 nodes.ctypes.data_as(c_vp), sizes.ctypes.data_as(c_vp)))
+    return nodes, sizes
+
+
+def wrmg_batched_lu(A, piv, info, ctx=None):
+    """A: (batch, m, m) float64 CUDA tensor holding column-major matrices (i.e. the
+    transposes, row-major); piv (batch, m) / info (batch,) int32 CUDA tensors."""
+    batch, m = A.shape[0], A.shape[1]
+    st = lib.wrmg_batched_lu(ctx, _ptr(A), m, batch, _ptr(piv), _ptr(info))
+    if st not in (0, 4):
+        _check(st)
+    return st
+
+
+def wrmg_fill_uniform(out, first_id=0, seed=0, ctx=None):
+    _check(lib.wrmg_fill_uniform(ctx, _ptr(out), out.numel(), int(first_id), int(seed)))
+
+
+class Context:
+    """One wrmg_ctx: the heat space-time hierarchy on one device/stream."""
+
+    def __init__(self, nx, ny=None, h=None, degree=1, q=0, nslabs=1, dt=1.0, kappa=1.0, omega_mg=1.0,
+                 nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None):
+        import torch
+        ny = nx if ny is None else ny
+        h = 1.0 / ny if h is None else h
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        self._mesh = _mesh(nx, ny, h, ncoarse)
+        co = wrmg_coeffs()
+        co.problem, co.bc, co.kappa = 0, 0, float(kappa)
+        co.weights = 0 if weights == "pou" else 1
+        co.omega_mg, co.nu_pre, co.nu_post = float(omega_mg), int(nu_pre), int(nu_post)
+        co.device, co.stream, co.rank, co.nranks = int(device), c_vp(stream), 0, 1
+        self._co = co
+        h_ = c_vp()
+        _check(lib.wrmg_setup(ctypes.byref(self._mesh), int(degree), int(q), int(nslabs), float(dt),
+                              ctypes.byref(co), ctypes.byref(h_)))
+        self._h = h_
+        lay = wrmg_layout_t()
+        _check(lib.wrmg_layout(self._h, ctypes.byref(lay)), self._h)
+        self.layout = {f: getattr(lay, f) for f, _ in wrmg_layout_t._fields_}
+        self.device = device
+
+    # --- helpers
+    def empty(self, level=None):
+        import torch
+        n = self.layout["ndof"] if level is None else self.level_size(level) * self.layout["nt"]
+        return torch.empty(n, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def zeros(self, level=None):
+        v = self.empty(level)
+        v.zero_()
+        return v
+
+    def level_size(self, level):
+        n = c_i64()
+        _check(lib.wrmg_level_size(self._h, int(level), ctypes.byref(n)), self._h)
+        return n.value
+
+    # --- C ABI
+    def linearize(self):
+        _check(lib.wrmg_linearize(self._h, None), self._h)
+
+    def rhs(self, fhat, b):
+        _check(lib.wrmg_rhs(self._h, _ptr(fhat), _ptr(b)), self._h)
+
+    def residual(self, u, b, r):
+        _check(lib.wrmg_residual(self._h, _ptr(u), _ptr(b), _ptr(r), 0), self._h)
+
+    def apply(self, x, y):
+        _check(lib.wrmg_apply(self._h, _ptr(x), _ptr(y)), self._h)
+
+    def smooth(self, u, b, nsweeps=1, omega=1.0):
+        _check(lib.wrmg_smooth(self._h, _ptr(u), _ptr(b), int(nsweeps), float(omega)), self._h)
+
+    def vcycle(self, r, z):
+        _check(lib.wrmg_vcycle(self._h, _ptr(r), _ptr(z)), self._h)
+
+    def restrict(self, level, rf, rc):
+        _check(lib.wrmg_restrict(self._h, int(level), _ptr(rf), _ptr(rc)), self._h)
+
+    def prolong_add(self, level, ec, uf):
+        _check(lib.wrmg_prolong_add(self._h, int(level), _ptr(ec), _ptr(uf)), self._h)
+
+    def fgmres(self, b, x, restart=30, maxit=200, rtol=1e-8, atol=0.0):
+        its, rel = c_i32(), c_dbl()
+        st = lib.wrmg_fgmres(self._h, _ptr(b), _ptr(x), int(restart), int(maxit), float(rtol), float(atol),
+                             ctypes.byref(its), ctypes.byref(rel))
+        if st not in (0, 5, 6):
+            _check(st, self._h)
+        return its.value, rel.value, STATUS[st]
+
+    def fill_uniform(self, out, first_id=0, seed=0):
+        _check(lib.wrmg_fill_uniform(self._h, _ptr(out), out.numel(), int(first_id), int(seed)), self._h)
+
+    def sync(self):
+        _check(lib.wrmg_sync(self._h), self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.wrmg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

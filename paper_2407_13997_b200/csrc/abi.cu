@@ -1,0 +1,702 @@
+// C ABI (include/wrmg.h): setup of the space-time hierarchy, the smoother,
+// V-cycle (H12) and FGMRES (H13) orchestration.  Every numerical step runs in
+// the kernels of kernels_*.cu; this file only allocates, uploads integer plans
+// and sequences launches on the context's stream.
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "plan.h"
+
+using namespace wrmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+  wrmg_status code;
+  std::string msg;
+};
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw Err{e_ == cudaErrorMemoryAllocation ? WRMG_E_OOM : WRMG_E_CUDA,                    \
+                std::string(#x) + ": " + cudaGetErrorString(e_)};                              \
+  } while (0)
+
+template <class T>
+T *dalloc(size_t n) {
+  void *p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return (T *)p;
+}
+
+template <class T>
+T *dupload(const std::vector<T> &v, cudaStream_t s) {
+  T *p = dalloc<T>(v.size());
+  if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+void dfree(void *p) {
+  if (p) cudaFree(p);
+}
+
+wrmg_status fail(wrmg_ctx *ctx, const Err &e) {
+  g_err = e.msg;
+  if (ctx) ctx->err = e.msg;
+  return e.code;
+}
+
+void check_launch() { CK(cudaGetLastError()); }
+
+void free_level(Level &L) {
+  for (void *p : {(void *)L.A.rowptr, (void *)L.A.col, (void *)L.A.val, (void *)L.A.val2, (void *)L.con,
+                  (void *)L.pnodes, (void *)L.ptype, (void *)L.wnode, (void *)L.type_rep, (void *)L.Dblk,
+                  (void *)L.Dinv, (void *)L.G, (void *)L.piv, (void *)L.info, (void *)L.P.rowptr, (void *)L.P.col,
+                  (void *)L.P.val, (void *)L.R.rowptr, (void *)L.R.col, (void *)L.R.val, (void *)L.vr, (void *)L.vz,
+                  (void *)L.vt})
+    dfree(p);
+}
+
+void validate(const wrmg_mesh *mesh, int degree, int q, int nslabs, double dt) {
+  if (!mesh) throw Err{WRMG_E_INVALID, "mesh is NULL"};
+  if (degree < 1 || degree > 3) throw Err{WRMG_E_UNSUPPORTED, "degree must be 1..3"};
+  if (q < 0 || q > 3) throw Err{WRMG_E_UNSUPPORTED, "q must be 0..3"};
+  if (nslabs < 1) throw Err{WRMG_E_INVALID, "nslabs must be >= 1"};
+  if (!(dt > 0)) throw Err{WRMG_E_INVALID, "dt must be > 0"};
+  if (mesh->gnx < 1 || mesh->gny < 1 || !(mesh->h > 0)) throw Err{WRMG_E_INVALID, "bad mesh size"};
+  if (mesh->x0 != 0 || (mesh->nx != 0 && mesh->nx != mesh->gnx))
+    throw Err{WRMG_E_UNSUPPORTED, "strip partitions (x0 != 0 or nx != gnx) are not built"};
+  int64_t L = (int64_t)(degree * mesh->gnx + 1) * (degree * mesh->gny + 1);
+  if (L > (int64_t)INT32_MAX / 8) throw Err{WRMG_E_UNSUPPORTED, "lattice too large for int32 node ids"};
+}
+
+// Numeric part of setup / linearisation: H1, H4, H5 on every level + coarse block.
+void factor_all(wrmg_ctx *c) {
+  cudaStream_t s = c->stream;
+  for (auto &L : c->lv) {
+    launch_assemble_spatial(L, c->k, c->ref_dev, c->co.kappa, s);
+    check_launch();
+    launch_patch_blocks(L, c->nq, c->tm, s);
+    check_launch();
+    const int m = c->nq * L.mp;
+    double *LU = dalloc<double>((size_t)L.ntypes * m * m);
+    CK(cudaMemcpyAsync(LU, L.Dblk, (size_t)L.ntypes * m * m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    launch_batched_lu(LU, m, L.ntypes, L.piv, L.info, s);
+    check_launch();
+    launch_inverse_and_G(L, LU, c->nq, s);
+    check_launch();
+    CK(cudaStreamSynchronize(s));
+    dfree(LU);
+  }
+  Coarse &C = c->coarse;
+  Level &L0 = c->lv[0];
+  launch_coarse_blocks(L0, C, c->nq, c->tm, s);
+  check_launch();
+  double *LU = dalloc<double>((size_t)C.m * C.m);
+  CK(cudaMemcpyAsync(LU, C.Dblk, (size_t)C.m * C.m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  launch_batched_lu(LU, C.m, 1, C.piv, C.info, s);
+  check_launch();
+  launch_coarse_inverse(C, LU, L0, c->nq, s);
+  check_launch();
+  CK(cudaStreamSynchronize(s));
+  dfree(LU);
+  // singular pivots (R10)
+  c->err_level = c->err_patch = c->err_slab = -1;
+  for (size_t l = 0; l < c->lv.size(); ++l) {
+    Level &L = c->lv[l];
+    std::vector<int32_t> info(L.ntypes);
+    CK(cudaMemcpy(info.data(), L.info, L.ntypes * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int t = 0; t < L.ntypes; ++t)
+      if (info[t]) {
+        c->err_level = (int)l;
+        c->err_patch = L.h_type_rep[t];
+        c->err_slab = -1;  // time-invariant block: every slab
+        throw Err{WRMG_E_SINGULAR, "singular patch block (level " + std::to_string(l) + ", patch " +
+                                       std::to_string(L.h_type_rep[t]) + ", column " + std::to_string(info[t]) + ")"};
+      }
+  }
+  int32_t ci = 0;
+  CK(cudaMemcpy(&ci, C.info, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (ci) {
+    c->err_level = 0;
+    c->err_patch = -1;
+    throw Err{WRMG_E_SINGULAR, "singular coarse block (column " + std::to_string(ci) + ")"};
+  }
+}
+
+int64_t ndof_level(const wrmg_ctx *c, int l) { return c->lv[l].nnode * c->nt; }
+
+// z = B r on level l (H12): V(nu_pre, nu_post), zero initial guess.
+void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
+  cudaStream_t s = c->stream;
+  Level &L = c->lv[l];
+  if (l == 0) {
+    launch_coarse_solve(c->coarse, L, c->q, c->N, r, z, s);
+    return;
+  }
+  const int64_t nd = ndof_level(c, l);
+  double *t = (l == (int)c->lv.size() - 1) ? c->tmp : L.vt;
+  const double om = c->co.omega_mg;
+  CK(cudaMemsetAsync(z, 0, nd * sizeof(double), s));
+  for (int it = 0; it < c->co.nu_pre; ++it) {
+    if (it == 0) {
+      launch_sweep(L, c->q, c->N, r, z, om, s);  // u = 0: residual is r itself
+    } else {
+      launch_residual(L, c->q, c->N, c->tm, z, r, t, false, s);
+      launch_sweep(L, c->q, c->N, t, z, om, s);
+    }
+  }
+  launch_residual(L, c->q, c->N, c->tm, z, r, t, c->co.nu_pre == 0, s);
+  Level &C = c->lv[l - 1];
+  launch_restrict(C, c->nt, t, C.vr, s);
+  vcycle_level(c, l - 1, C.vr, C.vz);
+  launch_prolong_add(C, c->nt, C.vz, z, s);
+  for (int it = 0; it < c->co.nu_post; ++it) {
+    launch_residual(L, c->q, c->N, c->tm, z, r, t, false, s);
+    launch_sweep(L, c->q, c->N, t, z, om, s);
+  }
+  check_launch();
+}
+
+double dot_host(wrmg_ctx *c, const double *a, const double *b, int64_t n) {
+  int nb = multidot_blocks(n);
+  const double *V[1] = {a};
+  launch_multidot(V, 1, b, n, c->red + 64, nb, c->stream);
+  launch_reduce_partials(c->red + 64, nb, 1, c->red, c->stream);
+  double out = 0;
+  CK(cudaMemcpyAsync(&out, c->red, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+wrmg_status wrmg_plan(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, wrmg_layout_t *out) {
+  try {
+    validate(mesh, degree, q, nslabs, 1.0);
+    if (!out) throw Err{WRMG_E_INVALID, "out is NULL"};
+    std::vector<int> nys;
+    int nc = mesh->ncoarse > 0 ? mesh->ncoarse : 4;
+    std::vector<int> nxs = level_sizes(mesh->gnx, mesh->gny, nc, &nys);
+    PlanLevel P;
+    plan_level(mesh->gnx, mesh->gny, mesh->h, degree, &P);
+    std::memset(out, 0, sizeof(*out));
+    out->nnode = P.nnode;
+    out->nt = (int64_t)nslabs * (q + 1);
+    out->ndof = P.nnode * out->nt;
+    out->nfree_st = P.nfree * out->nt;
+    out->lx = P.Lx;
+    out->ly = P.Ly;
+    out->nlevels = (int)nxs.size();
+    out->degree = degree;
+    out->q = q;
+    out->nslabs = nslabs;
+    out->npatch = P.npatch;
+    int mx = 0;
+    for (int32_t s : P.psize) mx = std::max(mx, (int)s);
+    out->mp_max = mx;
+    out->npatch_types = P.ntypes;
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(nullptr, e);
+  }
+}
+
+wrmg_status wrmg_plan_patches(const wrmg_mesh *mesh, int32_t degree, int32_t *nodes, int32_t *sizes) {
+  try {
+    validate(mesh, degree, 0, 1, 1.0);
+    PlanLevel P;
+    plan_level(mesh->gnx, mesh->gny, mesh->h, degree, &P);
+    int mx = 0;
+    for (int32_t s : P.psize) mx = std::max(mx, (int)s);
+    if (nodes)
+      for (int64_t p = 0; p < P.npatch; ++p)
+        for (int j = 0; j < mx; ++j) nodes[p * mx + j] = j < P.psize[p] ? P.pnodes[p * P.mp + j] : -1;
+    if (sizes)
+      for (int64_t p = 0; p < P.npatch; ++p) sizes[p] = P.psize[p];
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(nullptr, e);
+  }
+}
+
+wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, double dt,
+                       const wrmg_coeffs *coeffs, wrmg_ctx **out) {
+  wrmg_ctx *c = nullptr;
+  try {
+    if (!out) throw Err{WRMG_E_INVALID, "out is NULL"};
+    *out = nullptr;
+    validate(mesh, degree, q, nslabs, dt);
+    if (!coeffs) throw Err{WRMG_E_INVALID, "coeffs is NULL"};
+    if (coeffs->problem != WRMG_HEAT) throw Err{WRMG_E_UNSUPPORTED, "only WRMG_HEAT is built"};
+    if (coeffs->bc != WRMG_BC_DIRICHLET0) throw Err{WRMG_E_UNSUPPORTED, "only WRMG_BC_DIRICHLET0 is built"};
+    if (!(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
+    if (coeffs->nranks > 1) throw Err{WRMG_E_UNSUPPORTED, "multi-rank strips are not built"};
+    c = new wrmg_ctx();
+    c->mesh = *mesh;
+    if (c->mesh.nx == 0) c->mesh.nx = mesh->gnx;
+    if (c->mesh.ncoarse <= 0) c->mesh.ncoarse = 4;
+    c->co = *coeffs;
+    if (!(c->co.omega_mg > 0)) c->co.omega_mg = 1.0;
+    if (c->co.nu_pre <= 0 && c->co.nu_post <= 0) c->co.nu_pre = c->co.nu_post = 1;
+    c->k = degree;
+    c->q = q;
+    c->nq = q + 1;
+    c->N = nslabs;
+    c->nt = (int64_t)nslabs * c->nq;
+    c->dt = dt;
+    CK(cudaSetDevice(coeffs->device));
+    c->stream = (cudaStream_t)coeffs->stream;
+    cudaStream_t s = c->stream;
+    build_ref_element(degree, &c->ref);
+    build_temporal(q, dt, &c->tm);
+    for (int a = 0; a < c->nq; ++a)
+      for (int b = 0; b < c->nq; ++b) {
+        double want = (a == 0 && b == q) ? 1.0 : 0.0;
+        if (std::fabs(c->tm.E1[a * c->nq + b] - want) > 1e-14)
+          throw Err{WRMG_E_UNSUPPORTED, "E1 is not e_0 e_q^T (R2 temporal basis)"};
+      }
+    {
+      int nloc = c->ref.nloc;
+      std::vector<double> ref(2 * nloc * nloc);
+      std::memcpy(ref.data(), c->ref.M, nloc * nloc * sizeof(double));
+      std::memcpy(ref.data() + nloc * nloc, c->ref.K, nloc * nloc * sizeof(double));
+      c->ref_dev = dupload(ref, s);
+    }
+    std::vector<int> nys;
+    std::vector<int> nxs = level_sizes(mesh->gnx, mesh->gny, c->mesh.ncoarse, &nys);
+    const int nl = (int)nxs.size();
+    std::vector<PlanLevel> plans(nl);
+    c->lv.resize(nl);
+    for (int l = 0; l < nl; ++l) {
+      double h = mesh->h * (double)(mesh->gnx / nxs[l]);
+      plan_level(nxs[l], nys[l], h, degree, &plans[l]);
+      PlanLevel &P = plans[l];
+      Level &L = c->lv[l];
+      L.nx = P.nx;
+      L.ny = P.ny;
+      L.h = h;
+      L.Lx = P.Lx;
+      L.Ly = P.Ly;
+      L.nnode = P.nnode;
+      L.nfree = P.nfree;
+      L.A.nrow = P.nnode;
+      L.A.nnz = (int64_t)P.col.size();
+      L.A.rowptr = dupload(P.rowptr, s);
+      L.A.col = dupload(P.col, s);
+      L.A.val = dalloc<double>(P.col.size());
+      L.A.val2 = dalloc<double>(P.col.size());
+      L.h_con = P.con;
+      L.con = dupload(P.con, s);
+      L.npatch = P.npatch;
+      L.mp = P.mp;
+      L.ntypes = P.ntypes;
+      L.pnodes = dupload(P.pnodes, s);
+      L.ptype = dupload(P.ptype, s);
+      L.h_type_rep = P.type_rep;
+      L.type_rep = dupload(P.type_rep, s);
+      std::vector<double> w(P.nnode, 0.0);
+      for (int64_t i = 0; i < P.nnode; ++i)
+        if (P.mu[i] > 0) w[i] = (c->co.weights == WRMG_W_NONE) ? 1.0 : 1.0 / P.mu[i];
+      L.wnode = dupload(w, s);
+      int m = c->nq * L.mp;
+      L.Dblk = dalloc<double>((size_t)L.ntypes * m * m);
+      L.Dinv = dalloc<double>((size_t)L.ntypes * m * m);
+      L.G = dalloc<double>((size_t)L.ntypes * m * L.mp);
+      L.piv = dalloc<int32_t>((size_t)L.ntypes * m);
+      L.info = dalloc<int32_t>(L.ntypes);
+      if (l < nl - 1) {
+        L.vr = dalloc<double>(L.nnode * c->nt);
+        L.vz = dalloc<double>(L.nnode * c->nt);
+        L.vt = dalloc<double>(L.nnode * c->nt);
+      }
+      CK(cudaStreamSynchronize(s));  // host plan vectors die at scope end
+    }
+    for (int l = 1; l < nl; ++l) {
+      std::vector<int32_t> rp, ci, trp, tci;
+      std::vector<double> v, tv;
+      plan_interpolation(plans[l - 1], plans[l], degree, rp, ci, v);
+      transpose_csr(plans[l].nnode, plans[l - 1].nnode, rp, ci, v, trp, tci, tv);
+      Level &C = c->lv[l - 1];
+      C.P.nrow = plans[l].nnode;
+      C.P.nnz = (int64_t)ci.size();
+      C.P.rowptr = dupload(rp, s);
+      C.P.col = dupload(ci, s);
+      C.P.val = dupload(v, s);
+      C.R.nrow = plans[l - 1].nnode;
+      C.R.nnz = (int64_t)tci.size();
+      C.R.rowptr = dupload(trp, s);
+      C.R.col = dupload(tci, s);
+      C.R.val = dupload(tv, s);
+      CK(cudaStreamSynchronize(s));
+    }
+    {
+      Coarse &C = c->coarse;
+      std::vector<int32_t> nodes;
+      for (int64_t i = 0; i < plans[0].nnode; ++i)
+        if (!plans[0].con[i]) nodes.push_back((int32_t)i);
+      if (nodes.empty()) throw Err{WRMG_E_INVALID, "coarse level has no free node"};
+      C.nfree = (int64_t)nodes.size();
+      C.mp = (int)nodes.size();
+      C.m = c->nq * C.mp;
+      C.nodes = dupload(nodes, s);
+      C.Dblk = dalloc<double>((size_t)C.m * C.m);
+      C.DinvT = dalloc<double>((size_t)C.m * C.m);
+      C.GT = dalloc<double>((size_t)C.m * C.mp);
+      C.Gq = dalloc<double>((size_t)C.mp * C.mp);
+      C.Z = dalloc<double>((size_t)c->N * C.m);
+      C.Y = dalloc<double>((size_t)(c->N + 1) * C.mp);
+      C.piv = dalloc<int32_t>(C.m);
+      C.info = dalloc<int32_t>(1);
+    }
+    c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
+    c->red = dalloc<double>(64 + 64 * 148 * 4);
+    CK(cudaStreamSynchronize(s));
+    factor_all(c);
+    *out = c;
+    return WRMG_OK;
+  } catch (const Err &e) {
+    wrmg_status st = fail(c, e);
+    if (c) wrmg_destroy(c);
+    return st;
+  } catch (const std::bad_alloc &) {
+    if (c) wrmg_destroy(c);
+    g_err = "host allocation failed";
+    return WRMG_E_OOM;
+  }
+}
+
+wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
+  if (!c || !out) return WRMG_E_INVALID;
+  const Level &L = c->lv.back();
+  std::memset(out, 0, sizeof(*out));
+  out->nnode = L.nnode;
+  out->nt = c->nt;
+  out->ndof = L.nnode * c->nt;
+  out->nfree_st = L.nfree * c->nt;
+  out->lx = L.Lx;
+  out->ly = L.Ly;
+  out->nlevels = (int)c->lv.size();
+  out->degree = c->k;
+  out->q = c->q;
+  out->nslabs = c->N;
+  out->npatch = L.npatch;
+  out->mp_max = L.mp;
+  out->npatch_types = L.ntypes;
+  int64_t upd = 0;
+  for (size_t l = 1; l < c->lv.size(); ++l) upd += c->lv[l].nfree * c->nt * (c->co.nu_pre + c->co.nu_post);
+  out->smooth_dof_updates_per_vcycle = upd;
+  return WRMG_OK;
+}
+
+wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
+  if (!c) return WRMG_E_INVALID;
+  try {
+    if (state) throw Err{WRMG_E_UNSUPPORTED, "heat operator is linear: state must be NULL"};
+    factor_all(c);
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
+  if (!c || !fhat || !b) return WRMG_E_INVALID;
+  try {
+    launch_rhs(c->lv.back(), c->q, c->N, c->tm, fhat, b, c->stream);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double *r, int32_t nonlinear) {
+  if (!c || !u || !b || !r) return WRMG_E_INVALID;
+  if (nonlinear) return WRMG_E_UNSUPPORTED;
+  try {
+    launch_residual(c->lv.back(), c->q, c->N, c->tm, u, b, r, false, c->stream);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
+  if (!c || !x || !y) return WRMG_E_INVALID;
+  try {
+    // y = A x = 0 - (0 - A x): residual with b = 0 gives -A x; negate in place
+    const Level &L = c->lv.back();
+    const int64_t n = L.nnode * c->nt;
+    CK(cudaMemsetAsync(c->tmp, 0, n * sizeof(double), c->stream));
+    launch_residual(L, c->q, c->N, c->tm, x, c->tmp, y, false, c->stream);
+    launch_scale(y, y, -1.0, n, c->stream);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps, double omega) {
+  if (!c || !u || !b || nsweeps < 0) return WRMG_E_INVALID;
+  try {
+    Level &L = c->lv.back();
+    for (int s = 0; s < nsweeps; ++s) {
+      launch_residual(L, c->q, c->N, c->tm, u, b, c->tmp, false, c->stream);
+      launch_sweep(L, c->q, c->N, c->tmp, u, omega, c->stream);
+    }
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_vcycle(wrmg_ctx *c, const double *r, double *z) {
+  if (!c || !r || !z) return WRMG_E_INVALID;
+  try {
+    vcycle_level(c, (int)c->lv.size() - 1, r, z);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_level_size(const wrmg_ctx *c, int32_t level, int64_t *nnode) {
+  if (!c || !nnode || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  *nnode = c->lv[level].nnode;
+  return WRMG_OK;
+}
+
+wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *rc) {
+  if (!c || !rf || !rc || level < 1 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  try {
+    launch_restrict(c->lv[level - 1], c->nt, rf, rc, c->stream);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, double *uf) {
+  if (!c || !ec || !uf || level < 1 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  try {
+    launch_prolong_add(c->lv[level - 1], c->nt, ec, uf, c->stream);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
+                        double atol, int32_t *iters, double *relres) {
+  if (!c || !b || !x || restart < 1 || maxit < 1) return WRMG_E_INVALID;
+  try {
+    cudaStream_t s = c->stream;
+    const Level &L = c->lv.back();
+    const int64_t n = L.nnode * c->nt;
+    if (c->restart_alloc < restart) {
+      for (double *p : c->V) dfree(p);
+      for (double *p : c->Z) dfree(p);
+      c->V.clear();
+      c->Z.clear();
+      dfree(c->w);
+      for (int i = 0; i <= restart; ++i) c->V.push_back(dalloc<double>(n));
+      for (int i = 0; i < restart; ++i) c->Z.push_back(dalloc<double>(n));
+      c->w = dalloc<double>(n);
+      c->restart_alloc = restart;
+    }
+    double *red = c->red;            // [0, 64): results / coefficients
+    double *part = c->red + 64;      // partial sums
+    auto norm = [&](const double *v) { return std::sqrt(dot_host(c, v, v, n)); };
+    auto multidot = [&](int nv, const double *w, std::vector<double> &h) {
+      int nb = multidot_blocks(n);
+      std::vector<const double *> Vp(c->V.begin(), c->V.begin() + nv);
+      launch_multidot(Vp.data(), nv, w, n, part, nb, s);
+      launch_reduce_partials(part, nb, nv, red, s);
+      h.resize(nv);
+      CK(cudaMemcpyAsync(h.data(), red, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    };
+    CK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+    const double bnorm = norm(b);
+    const double target = std::max(rtol * bnorm, atol);
+    int its = 0;
+    wrmg_status status = WRMG_E_NOT_CONVERGED;
+    CK(cudaMemcpyAsync(c->tmp, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));  // r = b (x0 = 0)
+    double beta = bnorm;
+    bool done = beta <= target;
+    if (done) status = WRMG_OK;
+    std::vector<double> H((size_t)(restart + 1) * restart), cs(restart), sn(restart), g(restart + 1), h, h2, y;
+    while (!done && its < maxit) {
+      launch_scale(c->V[0], c->tmp, 1.0 / beta, n, s);
+      std::fill(H.begin(), H.end(), 0.0);
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int jend = 0;
+      for (int j = 0; j < restart; ++j) {
+        vcycle_level(c, (int)c->lv.size() - 1, c->V[j], c->Z[j]);
+        // w = A Z_j
+        CK(cudaMemsetAsync(c->w, 0, n * sizeof(double), s));
+        launch_residual(L, c->q, c->N, c->tm, c->Z[j], c->w, c->tmp, false, s);
+        launch_scale(c->w, c->tmp, -1.0, n, s);
+        // CGS2
+        multidot(j + 1, c->w, h);
+        launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+        multidot(j + 1, c->w, h2);
+        launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+        for (int i = 0; i <= j; ++i) h[i] += h2[i];
+        const double hn = norm(c->w);
+        std::vector<double> col(restart + 1, 0.0);
+        for (int i = 0; i <= j; ++i) col[i] = h[i];
+        col[j + 1] = hn;
+        for (int i = 0; i < j; ++i) {
+          double t = cs[i] * col[i] + sn[i] * col[i + 1];
+          col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+          col[i] = t;
+        }
+        const double d = std::hypot(col[j], col[j + 1]);
+        cs[j] = col[j] / d;
+        sn[j] = col[j + 1] / d;
+        col[j] = d;
+        col[j + 1] = 0.0;
+        g[j + 1] = -sn[j] * g[j];
+        g[j] = cs[j] * g[j];
+        for (int i = 0; i <= restart; ++i) H[(size_t)i * restart + j] = col[i];
+        ++its;
+        jend = j + 1;
+        if (hn < 1e-30) {
+          status = WRMG_E_BREAKDOWN;
+          done = true;
+          break;
+        }
+        launch_scale(c->V[j + 1], c->w, 1.0 / hn, n, s);
+        if (std::fabs(g[j + 1]) <= target) {
+          status = WRMG_OK;
+          done = true;
+          break;
+        }
+        if (its >= maxit) {
+          done = true;
+          break;
+        }
+      }
+      y.assign(jend, 0.0);
+      for (int i = jend - 1; i >= 0; --i) {
+        double acc = g[i];
+        for (int k2 = i + 1; k2 < jend; ++k2) acc -= H[(size_t)i * restart + k2] * y[k2];
+        y[i] = acc / H[(size_t)i * restart + i];
+      }
+      CK(cudaMemcpyAsync(red, y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, s));
+      launch_multiaxpy(x, c->Z.data(), red, jend, n, 1.0, s);
+      CK(cudaStreamSynchronize(s));
+      if (done) break;
+      launch_residual(L, c->q, c->N, c->tm, x, b, c->tmp, false, s);
+      beta = norm(c->tmp);
+      if (beta <= target) {
+        status = WRMG_OK;
+        break;
+      }
+    }
+    launch_residual(L, c->q, c->N, c->tm, x, b, c->tmp, false, s);
+    const double rn = norm(c->tmp);
+    if (iters) *iters = its;
+    if (relres) *relres = bnorm > 0 ? rn / bnorm : 0.0;
+    check_launch();
+    if (status != WRMG_OK) c->err = status == WRMG_E_BREAKDOWN ? "FGMRES breakdown" : "FGMRES: maxit reached";
+    return status;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_newton(wrmg_ctx *c, double *, double, int32_t, int32_t *, int32_t *) {
+  if (c) c->err = "Navier-Stokes Newton is not built";
+  g_err = "Navier-Stokes Newton is not built";
+  return WRMG_E_UNSUPPORTED;
+}
+
+wrmg_status wrmg_batched_lu(const wrmg_ctx *c, double *A, int32_t m, int32_t batch, int32_t *piv, int32_t *info) {
+  if (!A || !piv || !info || m < 1 || batch < 0) return WRMG_E_INVALID;
+  try {
+    cudaStream_t s = c ? c->stream : nullptr;
+    launch_batched_lu(A, m, batch, piv, info, s);
+    check_launch();
+    CK(cudaStreamSynchronize(s));
+    std::vector<int32_t> h(batch);
+    if (batch) CK(cudaMemcpy(h.data(), info, batch * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int32_t v : h)
+      if (v) {
+        g_err = "singular matrix in batched LU";
+        return WRMG_E_SINGULAR;
+      }
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(nullptr, e);
+  }
+}
+
+wrmg_status wrmg_fill_uniform(const wrmg_ctx *c, double *out, int64_t count, uint64_t first_id, uint64_t seed) {
+  if (!out || count < 0) return WRMG_E_INVALID;
+  try {
+    launch_fill_uniform(out, count, first_id, seed, c ? c->stream : nullptr);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(nullptr, e);
+  }
+}
+
+wrmg_status wrmg_sync(wrmg_ctx *c) {
+  if (!c) return WRMG_E_INVALID;
+  try {
+    CK(cudaStreamSynchronize(c->stream));
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+const char *wrmg_last_error(const wrmg_ctx *c, int32_t *level, int32_t *patch, int32_t *slab) {
+  if (level) *level = c ? c->err_level : -1;
+  if (patch) *patch = c ? c->err_patch : -1;
+  if (slab) *slab = c ? c->err_slab : -1;
+  if (c && !c->err.empty()) return c->err.c_str();
+  return g_err.c_str();
+}
+
+void wrmg_destroy(wrmg_ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto &L : c->lv) free_level(L);
+  Coarse &C = c->coarse;
+  for (void *p : {(void *)C.nodes, (void *)C.Dblk, (void *)C.DinvT, (void *)C.GT, (void *)C.Gq, (void *)C.Z,
+                  (void *)C.Y, (void *)C.piv, (void *)C.info})
+    dfree(p);
+  for (double *p : c->V) dfree(p);
+  for (double *p : c->Z) dfree(p);
+  dfree(c->w);
+  dfree(c->red);
+  dfree(c->tmp);
+  dfree(c->ref_dev);
+  delete c;
+}
+
+}  // extern "C"

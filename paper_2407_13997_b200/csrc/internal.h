@@ -1,0 +1,136 @@
+// Internal declarations of libwrmg (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/wrmg.h"
+
+namespace wrmg {
+
+constexpr int kMaxQ = 3;            // DG(q), q <= 3
+constexpr int kMaxK = 3;            // CG(k), k <= 3
+constexpr int kMaxLoc = 10;         // (k+1)(k+2)/2 for k = 3
+
+// ---------------------------------------------------------------- host math
+// Reference P_k element on T^ = {xi, eta >= 0, xi + eta <= 1} with nodes
+// (a/k, b/k); local index ordering: b outer, a inner (see host_fem.cu).
+struct RefElement {
+  int k = 0, nloc = 0;
+  int a[kMaxLoc], b[kMaxLoc];
+  double M[kMaxLoc * kMaxLoc];   // int phi_i phi_j over T^
+  double K[kMaxLoc * kMaxLoc];   // int grad phi_i . grad phi_j over T^
+};
+void build_ref_element(int k, RefElement *out);
+// Values of the reference basis at the point with k*lambda = (kl0, kl1, kl2)
+// (barycentric coordinates times k; exact rationals keep lattice zeros exact).
+void eval_basis_klambda(int k, double kl1, double kl2, double *vals);
+
+struct Temporal {
+  int q = 0, nq = 1;
+  double CE[(kMaxQ + 1) * (kMaxQ + 1)];  // C + E0, row a, column b
+  double Mt[(kMaxQ + 1) * (kMaxQ + 1)];  // dt int phi_a phi_b
+  double E1[(kMaxQ + 1) * (kMaxQ + 1)];  // phi_a(0) phi_b(1)
+};
+void build_temporal(int q, double dt, Temporal *out);
+
+// ---------------------------------------------------------------- device data
+struct DevCSR {
+  int64_t nrow = 0, nnz = 0;
+  int32_t *rowptr = nullptr, *col = nullptr;
+  double *val = nullptr, *val2 = nullptr;  // M and K (spatial) or P entries
+};
+
+struct Level {
+  int nx = 0, ny = 0;
+  double h = 0;
+  int Lx = 0, Ly = 0;
+  int64_t nnode = 0, nfree = 0;
+  DevCSR A;                         // spatial M (val) and kappa K (val2), all nodes
+  uint8_t *con = nullptr;           // constrained mask
+  std::vector<uint8_t> h_con;
+  // patches (vertex-star, R8)
+  int64_t npatch = 0;
+  int mp = 0;                       // padded spatial patch size (compile-time class)
+  int ntypes = 0;
+  int32_t *pnodes = nullptr;        // [npatch][mp], -1 pad
+  int32_t *ptype = nullptr;         // [npatch]
+  double *wnode = nullptr;          // 1/mu_i (or 1) per node, 0 on nodes in no patch
+  int32_t *type_rep = nullptr;      // representative patch of each type
+  double *Dblk = nullptr;           // [ntypes][m][m] assembled local blocks (column-major), m = nq*mp
+  double *Dinv = nullptr;           // [ntypes][m][m] row-major inverses
+  double *G = nullptr;              // [ntypes][m][mp] jump propagator Dinv[:, a=0] M_p
+  int32_t *piv = nullptr, *info = nullptr;
+  std::vector<int32_t> h_type_rep;
+  // transfer from this level to the next finer (stored on the coarse side)
+  DevCSR P;    // rows: fine nodes, cols: coarse nodes
+  DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)
+  // V-cycle work vectors (levels below the finest)
+  double *vr = nullptr, *vz = nullptr, *vt = nullptr;
+};
+
+struct Coarse {
+  int64_t nfree = 0;
+  int m = 0, mp = 0;
+  int32_t *nodes = nullptr;   // free coarse nodes (canonical order)
+  double *Dblk = nullptr;     // m x m, column-major
+  double *DinvT = nullptr;    // m x m, column-major inverse (Dinv^T row-major)
+  double *Gq = nullptr;       // mp x mp row-major: end-trace propagator
+  double *GT = nullptr;       // mp x m: G transposed (G[rho][j] at GT[j*m + rho])
+  double *Z = nullptr;        // N x m scratch
+  double *Y = nullptr;        // (N+1) x mp scratch
+  int32_t *piv = nullptr, *info = nullptr;
+};
+
+}  // namespace wrmg
+
+struct wrmg_ctx {
+  wrmg_mesh mesh{};
+  wrmg_coeffs co{};
+  int k = 1, q = 0, N = 1, nq = 1;
+  int64_t nt = 1;
+  double dt = 0;
+  cudaStream_t stream = nullptr;
+  wrmg::RefElement ref;
+  wrmg::Temporal tm;
+  std::vector<wrmg::Level> lv;  // 0 = coarsest
+  wrmg::Coarse coarse;
+  double *ref_dev = nullptr;    // reference M^, K^ on device
+  // FGMRES work space
+  int restart_alloc = 0;
+  std::vector<double *> V, Z;
+  double *w = nullptr, *red = nullptr, *red_host = nullptr;
+  double *tmp = nullptr;        // finest-level scratch (residual)
+  std::string err;
+  int err_level = -1, err_patch = -1, err_slab = -1;
+};
+
+namespace wrmg {
+// kernel launchers (kernels_*.cu)
+void launch_assemble_spatial(const Level &L, int k, const double *ref_dev, double kappa, cudaStream_t s);
+void launch_patch_blocks(const Level &L, int nq, const Temporal &tm, cudaStream_t s);
+void launch_batched_lu(double *A, int m, int batch, int32_t *piv, int32_t *info, cudaStream_t s);
+void launch_inverse_and_G(const Level &L, const double *LU, int nq, cudaStream_t s);
+void launch_coarse_blocks(const Level &L, Coarse &C, int nq, const Temporal &tm, cudaStream_t s);
+void launch_coarse_inverse(Coarse &C, const double *LU, const Level &L, int nq, cudaStream_t s);
+void launch_residual(const Level &L, int q, int N, const Temporal &tm, const double *u, const double *b,
+                     double *r, bool u_is_zero, cudaStream_t s);
+void launch_sweep(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s);
+void launch_restrict(const Level &coarse, int64_t nt, const double *rf, double *rc, cudaStream_t s);
+void launch_prolong_add(const Level &coarse, int64_t nt, const double *ec, double *uf, cudaStream_t s);
+void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const double *r, double *x,
+                         cudaStream_t s);
+void launch_rhs(const Level &L, int q, int N, const Temporal &tm, const double *fhat, double *b, cudaStream_t s);
+void launch_fill_uniform(double *out, int64_t count, uint64_t first, uint64_t seed, cudaStream_t s);
+// Krylov helpers
+void launch_multidot(const double *const *V, int nv, const double *w, int64_t n, double *partials, int nblk,
+                     cudaStream_t s);
+int multidot_blocks(int64_t n);
+void launch_reduce_partials(const double *partials, int nblk, int nv, double *out, cudaStream_t s);
+void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
+                      cudaStream_t s);
+void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s);
+}  // namespace wrmg

@@ -1,0 +1,30 @@
+// Host-side plan of one multigrid level (integer setup data).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "internal.h"
+
+namespace wrmg {
+
+struct PlanLevel {
+  int nx = 0, ny = 0, Lx = 0, Ly = 0;
+  double h = 0;
+  int64_t nnode = 0, nfree = 0;
+  std::vector<uint8_t> con;
+  std::vector<int32_t> rowptr, col;  // spatial sparsity (all nodes)
+  int mp = 0;                        // padded patch size
+  int64_t npatch = 0;
+  int ntypes = 0;
+  std::vector<int32_t> pnodes, psize, pvert, ptype, type_rep, mu;
+};
+
+void plan_level(int nx, int ny, double h, int k, PlanLevel *P);
+void plan_interpolation(const PlanLevel &C, const PlanLevel &F, int k, std::vector<int32_t> &rowptr,
+                        std::vector<int32_t> &col, std::vector<double> &val);
+void transpose_csr(int64_t nrow, int64_t ncol, const std::vector<int32_t> &rp, const std::vector<int32_t> &ci,
+                   const std::vector<double> &v, std::vector<int32_t> &trp, std::vector<int32_t> &tci,
+                   std::vector<double> &tv);
+std::vector<int> level_sizes(int gnx, int gny, int ncoarse, std::vector<int> *nys);
+
+}  // namespace wrmg

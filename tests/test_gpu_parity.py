@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same
+seeded inputs.  Tolerance (north_star, R23): relative 1e-10 in the
+2-norm and the max-norm per vector; identical FGMRES iteration counts."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import wrmg_inputs as wi
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _dev(x):
+    torch = _torch()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda:0")
+
+
+def _host(t):
+    _torch().cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def assert_parity(gpu, ref, tol=TOL, what=""):
+    gpu, ref = np.asarray(gpu), np.asarray(ref)
+    n2 = np.linalg.norm(ref)
+    ninf = np.max(np.abs(ref))
+    e2 = np.linalg.norm(gpu - ref) / n2
+    einf = np.max(np.abs(gpu - ref)) / ninf
+    assert e2 <= tol and einf <= tol, f"{what}: rel2 {e2:.3e} relinf {einf:.3e}"
+    return e2, einf
+
+
+def _ctx(n, k, q, N, **kw):
+    import paper_2407_13997_b200 as w
+    return w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N, **kw)
+
+
+def _prob(n, k, q, N, **kw):
+    from oracle import heat
+    return heat.unit_square_problem(n, k, q, N, 1.0 / N, **kw)
+
+
+CASES = [(16, 1, 0, 16), (8, 3, 1, 37), (6, 2, 1, 33), (5, 1, 2, 7), (4, 3, 0, 3), (7, 2, 3, 4)]
+
+
+def test_rng_bitwise():
+    torch = _torch()
+    import paper_2407_13997_b200 as w
+    out = torch.empty(100003, dtype=torch.float64, device="cuda:0")
+    w.wrmg_fill_uniform(out, first_id=12345, seed=3)
+    ref = wi.uniform_pm1(np.arange(100003, dtype=np.uint64) + np.uint64(12345), seed=3)
+    assert np.array_equal(_host(out), ref)
+
+
+@pytest.mark.parametrize("n,k,q,N", CASES)
+def test_rhs_and_residual(n, k, q, N):
+    p = _prob(n, k, q, N)
+    c = _ctx(n, k, q, N)
+    f = wi.spacetime_field(p.nnode, N, q, seed=0)
+    b_ref = p.rhs(f)
+    b = c.empty()
+    c.rhs(_dev(f), b)
+    assert_parity(_host(b), b_ref, what="rhs")
+    u_np = wi.spacetime_field(p.nnode, N, q, seed=1)
+    r = c.empty()
+    c.residual(_dev(u_np), _dev(b_ref), r)
+    assert_parity(_host(r), p.residual(u_np, b_ref), what="residual")
+    y = c.empty()
+    c.apply(_dev(u_np), y)
+    assert_parity(_host(y), p.A @ u_np, what="apply")
+
+
+@pytest.mark.parametrize("n,k,q,N", CASES)
+def test_smoother_sweeps(n, k, q, N):
+    from oracle import patches, smoother
+    p = _prob(n, k, q, N)
+    c = _ctx(n, k, q, N)
+    P, _ = patches.vertex_star_patches(p.mesh, k, p.constrained)
+    fac = smoother.PatchFactors(p, p.A, P)
+    wts = smoother.weights(P, p.nnode)
+    b = p.rhs(wi.spacetime_field(p.nnode, N, q, 0))
+    u0 = wi.spacetime_field(p.nnode, N, q, 2) * ~p.con_st
+    u_ref = u0.copy()
+    u = _dev(u0)
+    for sweep, om in enumerate((0.7, 1.0, 1.0)):
+        u_ref = smoother.wr_sweep(p, p.A, u_ref, b, fac, om, wts)
+        c.smooth(u, _dev(b), 1, om)
+        assert_parity(_host(u), u_ref, what=f"sweep {sweep}")
+
+
+def test_C1_protocol():
+    """BASELINE configs[0] (R28): P1/DG0 16x16, N=16; 10 sweeps omega=1 from 0,
+    compared after every sweep, then u += V(1,1)(b - A u)."""
+    from oracle import multigrid, smoother
+    n, k, q, N = 16, 1, 0, 16
+    H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
+    p = H.fine
+    c = _ctx(n, k, q, N)
+    f = wi.spacetime_field(p.nnode, N, q, 0)
+    b_ref = p.rhs(f)
+    b = c.empty()
+    c.rhs(_dev(f), b)
+    u_ref = np.zeros(p.ndof)
+    u = c.zeros()
+    L = H.levels[-1]
+    for s in range(10):
+        u_ref = smoother.wr_sweep(p, p.A, u_ref, b_ref, L.factors, 1.0, L.w)
+        c.smooth(u, b, 1, 1.0)
+        assert_parity(_host(u), u_ref, what=f"C1 sweep {s}")
+    r_ref = b_ref - p.A @ u_ref
+    u_ref = u_ref + multigrid.vcycle(H, r_ref)
+    r = c.empty()
+    z = c.empty()
+    c.residual(u, b, r)
+    c.vcycle(r, z)
+    u += z
+    assert_parity(_host(u), u_ref, what="C1 V-cycle")
+
+
+@pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 5), (8, 3, 1, 35), (16, 2, 1, 3), (8, 2, 2, 4)])
+def test_transfers(n, k, q, N):
+    from oracle import multigrid, transfer
+    H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
+    c = _ctx(n, k, q, N)
+    NT = N * (q + 1)
+    for l in range(1, len(H.levels)):
+        fp, cp = H.levels[l].prob, H.levels[l - 1].prob
+        rf = wi.spacetime_field(fp.nnode, N, q, 10 + l)
+        ec = wi.spacetime_field(cp.nnode, N, q, 20 + l) * ~cp.con_st
+        rc = c.empty(l - 1)
+        c.restrict(l, _dev(rf), rc)
+        assert_parity(_host(rc), transfer.restrict(H.P0[l], rf, NT), what=f"restrict {l}")
+        uf0 = wi.spacetime_field(fp.nnode, N, q, 30 + l)
+        uf = _dev(uf0)
+        c.prolong_add(l, _dev(ec), uf)
+        assert_parity(_host(uf), uf0 + transfer.prolong(H.P0[l], ec, NT), what=f"prolong {l}")
+
+
+@pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 16), (8, 3, 1, 34), (16, 2, 1, 6), (4, 2, 1, 9)])
+def test_vcycle(n, k, q, N):
+    from oracle import multigrid
+    H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
+    p = H.fine
+    c = _ctx(n, k, q, N)
+    assert c.layout["nlevels"] == len(H.levels)
+    r_np = p.rhs(wi.spacetime_field(p.nnode, N, q, 4))
+    z = c.empty()
+    c.vcycle(_dev(r_np), z)
+    assert_parity(_host(z), multigrid.vcycle(H, r_np), what="vcycle")
+
+
+@pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 16), (16, 3, 1, 16), (8, 2, 1, 40)])
+def test_fgmres(n, k, q, N):
+    from oracle import krylov, multigrid
+    H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
+    p = H.fine
+    b_np = p.rhs(wi.spacetime_field(p.nnode, N, q, 0))
+    x_ref, its_ref, hist, st = krylov.fgmres(lambda v: p.A @ v, lambda r: multigrid.vcycle(H, r), b_np,
+                                             restart=30, maxit=200, rtol=1e-8)
+    c = _ctx(n, k, q, N)
+    x = c.empty()
+    its, rel, status = c.fgmres(_dev(b_np), x, restart=30, maxit=200, rtol=1e-8)
+    assert status == "WRMG_OK" and st == "converged"
+    assert its == its_ref, (its, its_ref, hist[-3:])
+    assert rel <= 1e-8 * 1.01
+    assert_parity(_host(x), x_ref, tol=1e-9, what="fgmres iterate")
+
+
+def _colmajor(A):
+    return np.ascontiguousarray(np.transpose(A, (0, 2, 1)))
+
+
+@pytest.mark.parametrize("m,batch", [(2, 1), (38, 5), (78, 3), (162, 2), (250, 1)])
+def test_batched_lu_matches_lapack(m, batch):
+    torch = _torch()
+    import paper_2407_13997_b200 as w
+    rng = np.random.default_rng(m)
+    A = rng.standard_normal((batch, m, m))
+    if m == 2:
+        A[0] = [[0.0, 1.0], [1.0, 0.0]]  # requires a row interchange
+    dA = _dev(_colmajor(A))
+    piv = torch.empty((batch, m), dtype=torch.int32, device="cuda:0")
+    info = torch.empty(batch, dtype=torch.int32, device="cuda:0")
+    assert w.wrmg_batched_lu(dA, piv, info) == 0
+    LU = np.transpose(_host(dA), (0, 2, 1))
+    for b in range(batch):
+        lu, pv = sla.lu_factor(A[b])
+        assert np.array_equal(_host(piv)[b], pv)
+        assert np.max(np.abs(LU[b] - lu)) <= 1e-13 * max(1.0, np.max(np.abs(lu)))
+    assert np.all(_host(info) == 0)
+
+
+def test_batched_lu_singular():
+    torch = _torch()
+    import paper_2407_13997_b200 as w
+    A = np.array([[[1.0, 2.0, 3.0], [2.0, 4.0, 6.0], [0.0, 1.0, 1.0]]])
+    dA = _dev(_colmajor(A))
+    piv = torch.empty((1, 3), dtype=torch.int32, device="cuda:0")
+    info = torch.empty(1, dtype=torch.int32, device="cuda:0")
+    assert w.wrmg_batched_lu(dA, piv, info) == 4
+    assert _host(info)[0] == 3
