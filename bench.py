@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the WRMG hot path on B200 (contract: see DESIGN.md "Measurement").
+
+Workload (N=1): BASELINE.json configs[1] (C2): heat equation on the unit square,
+128x128 anti-diagonal mesh, P3 in space, DG1 in time, 128 slabs, dt = 1/128,
+kappa = 1, Dirichlet 0, f = seeded U[-1,1] nodal coefficients (R6);
+FGMRES(30) preconditioned by WRMG V(1,1) to 1e-8 relative residual, FP64.
+
+One step = one complete FGMRES-WRMG solve from x0 = 0 (every residual,
+smoother sweep on every level, restriction, prolongation, coarse solve and
+Krylov step of the solve).  metric value = smoother space-time DoF updates in
+the step (iterations x sum over smoothed levels of free DoFs x (nu_pre+nu_post))
+divided by the step time.  Vectors are 303 MB > 126 MB L2, so no L2 flush is
+needed between steps.
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py
+executes it) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "WR patch-smoother space-time DOF updates/s (FP64)"
+UNIT = "DoF-updates/s"
+CFG = dict(n=128, k=3, q=1, N=128, kappa=1.0, restart=30, rtol=1e-8)
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = p.get("hbm_gbs")
+    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    if not hbm:
+        hbm, hbm_src = 6650.0, "fallback (B200_PROFILING.md)"
+    # FP64: no measured entry; derived from unit counts and clocks:
+    # 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+    fp64 = 148 * 64 * 2 * 1.965e9 / 1e12
+    return hbm, hbm_src, fp64
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------- oracle
+def oracle_sample(n, N, repeats=1):
+    """Time the oracle (as it stands) on a bounded sample: the C2 discretisation
+    (P3 x DG1, kappa 1, FGMRES(30) + V(1,1) to 1e-8) on an n x n mesh with N slabs,
+    single host thread.  Returns (DoF-updates/s, seconds per solve, iterations)."""
+    from threadpoolctl import threadpool_limits
+
+    import wrmg_inputs as wi
+    from oracle import krylov, multigrid
+    with threadpool_limits(1):
+        H = multigrid.Hierarchy(n, n, 1.0 / n, CFG["k"], CFG["q"], N, 1.0 / N, kappa=CFG["kappa"])
+        p = H.fine
+        b = p.rhs(wi.spacetime_field(p.nnode, N, CFG["q"], 0))
+        upd_vc = sum(int(L.prob.free.sum()) * L.prob.NT * 2 for L in H.levels[1:])
+        times, its = [], 0
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            x, its, hist, st = krylov.fgmres(lambda v: p.A @ v, lambda r: multigrid.vcycle(H, r), b,
+                                             restart=CFG["restart"], rtol=CFG["rtol"])
+            times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return its * upd_vc / t, t, its, H, b, upd_vc
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    from threadpoolctl import threadpool_limits
+
+    from oracle import krylov, multigrid
+    n, N = 16, 32
+    import wrmg_inputs as wi
+    with threadpool_limits(1):
+        H = multigrid.Hierarchy(n, n, 1.0 / n, CFG["k"], CFG["q"], N, 1.0 / N, kappa=CFG["kappa"])
+        p = H.fine
+        b = p.rhs(wi.spacetime_field(p.nnode, N, CFG["q"], 0))
+        upd_vc = sum(int(L.prob.free.sum()) * L.prob.NT * 2 for L in H.levels[1:])
+        solve = lambda: krylov.fgmres(lambda v: p.A @ v, lambda r: multigrid.vcycle(H, r), b,
+                                      restart=CFG["restart"], rtol=CFG["rtol"])
+        for _ in range(args.warmup):
+            solve()
+        t0 = time.perf_counter()
+        tot = 0
+        for _ in range(args.steps):
+            x, its, hist, st = solve()
+            tot += its * upd_vc
+        el = time.perf_counter() - t0
+    v = tot / el
+    sample = (f"oracle FGMRES(30)+V(1,1) solve to 1e-8 of the C2 discretisation (P3 x DG1, kappa 1) on a "
+              f"{n}x{n} mesh with N={N} slabs per step, 1 host thread")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 (BASELINE configs[1]) bounded oracle sample", "mesh": n, "degree": 3,
+                       "q": 1, "nslabs": N},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------- GPU arm
+def run_gpu(args, ws, rank, local):
+    import torch
+
+    import paper_2407_13997_b200 as w
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    n, k, q, N = CFG["n"], CFG["k"], CFG["q"], CFG["N"]
+    stream = torch.cuda.current_stream()
+    ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N, kappa=CFG["kappa"], device=local,
+                    stream=stream.cuda_stream)
+    lay = ctx.layout
+    ndof = lay["ndof"]
+    fhat = ctx.empty()
+    ctx.fill_uniform(fhat, first_id=0, seed=0)  # R6 generator, canonical ids (weak: same problem per rank)
+    b = ctx.empty()
+    ctx.rhs(fhat, b)
+    x = ctx.empty()
+    upd_vc = lay["smooth_dof_updates_per_vcycle"]
+
+    def solve():
+        its, rel, st = ctx.fgmres(b, x, restart=CFG["restart"], maxit=200, rtol=CFG["rtol"])
+        if st != "WRMG_OK":
+            raise RuntimeError(f"FGMRES status {st}")
+        return its, rel
+
+    for _ in range(max(args.warmup, 0)):
+        solve()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ctx.profile(True)
+    launches0 = w.launch_count()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tot_upd, its_list, rels = 0, [], []
+    for _ in range(args.steps):
+        its, rel = solve()
+        tot_upd += its * upd_vc
+        its_list.append(its)
+        rels.append(rel)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms_total = e0.elapsed_time(e1)
+    launches = w.launch_count() - launches0
+    stats = ctx.kernel_stats()
+    ctx.profile(False)
+    clk = clocks.stop()
+    ms_total = max_over_ranks(ms_total, ws)
+    ms_step = ms_total / args.steps
+    value = ws * tot_upd / (ms_total / 1e3)
+
+    # dominant kernel (largest device-time share in the timed region)
+    hbm, hbm_src, fp64 = peaks()
+    tot_ms = sum(s["ms"] for s in stats.values())
+    (kname, klvl), ks = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = ks["ms"] / ks["launches"]
+    t_hbm = ks["bytes"] / ks["launches"] / (hbm * 1e9)
+    t_fp = ks["flops"] / ks["launches"] / (fp64 * 1e12)
+    if t_fp > t_hbm:
+        roof = {"bound": "alu", "achieved": ks["flops"] / ks["launches"] / (per_launch_ms / 1e3) / 1e12,
+                "peak": fp64, "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": ks["bytes"] / ks["launches"] / (per_launch_ms / 1e3) / 1e9,
+                "peak": hbm, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"{kname} (level {klvl} of {lay['nlevels']}, finest = {lay['nlevels'] - 1})"
+    roof["share_of_kernel_time"] = ks["ms"] / tot_ms if tot_ms else None
+    roof["peak_source"] = (hbm_src if roof["bound"] == "hbm" else
+                           "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (no measured FP64 peak)")
+    roof["hbm_achieved_GBs"] = ks["bytes"] / ks["launches"] / (per_launch_ms / 1e3) / 1e9
+    roof["fp64_achieved_TFs"] = ks["flops"] / ks["launches"] / (per_launch_ms / 1e3) / 1e12
+    per_kernel = {f"{a}@L{l}": {"launches": s["launches"], "ms": round(s["ms"], 4),
+                                "GBs": round(s["bytes"] / (s["ms"] / 1e3) / 1e9, 1) if s["ms"] > 0 else None,
+                                "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}
+                  for (a, l), s in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+
+    # V-cycle time and finest-level smoother sweep throughput (separately timed)
+    r = ctx.empty()
+    ctx.residual(x, b, r)
+    z = ctx.empty()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    for _ in range(10):
+        ctx.vcycle(b, z)
+    ev[1].record(stream)
+    u = ctx.zeros()
+    ev[2].record(stream)
+    for _ in range(10):
+        ctx.smooth(u, b, 1, 1.0)
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    vcycle_ms = ev[0].elapsed_time(ev[1]) / 10
+    sweep_ms = ev[2].elapsed_time(ev[3]) / 10
+
+    # end to end through the public API: pinned host b -> device, solve, x -> host
+    hb = b.detach().cpu().pin_memory()
+    hx = torch.empty_like(hb).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier(ws)
+    torch.cuda.synchronize()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    e2e_upd = 0
+    for _ in range(e2e_steps):
+        b.copy_(hb, non_blocking=True)
+        its, rel = solve()
+        hx.copy_(x, non_blocking=True)
+        e2e_upd += its * upd_vc
+    eb.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(ea.elapsed_time(eb), ws)
+    e2e = {"value": ws * e2e_upd / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": ndof * 8,
+           "d2h_bytes_per_step": ndof * 8}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 = BASELINE configs[1]: heat, unit square 128x128, P3 x DG1, N=128, "
+                                   "dt=1/128, kappa=1, Dirichlet 0, f ~ U[-1,1] seed 0; FGMRES(30)+WRMG V(1,1) "
+                                   "to 1e-8; one step = one full solve",
+                       "ndof": ndof, "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (303 MB vectors vs 126 MB L2); no flush"},
+            "fgmres_iterations": its_list[0], "final_relres": rels[-1],
+            "vcycle_ms": vcycle_ms, "smoother_sweep_ms": sweep_ms,
+            "smoother_sweep_dof_updates_per_s": lay["nfree_st"] / (sweep_ms / 1e3),
+            "roofline": roof, "per_kernel": per_kernel, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        v, t, its, *_ = oracle_sample(16, 128)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"oracle FGMRES(30)+V(1,1) to 1e-8, C2 discretisation (P3 x DG1, "
+                                          f"N=128) on a 16x16 mesh, 1 host thread, {its} iterations in {t:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wrmg", choices=["wrmg", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup(args) if args.impl == "wrmg" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_gpu(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

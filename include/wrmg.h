@@ -70,7 +70,8 @@ typedef struct {
   int32_t weights;      /* WRMG_W_POU (default) | WRMG_W_NONE */
   double omega_mg;      /* smoother damping inside the V-cycle (R15; 0 -> 1.0) */
   int32_t nu_pre, nu_post; /* V(nu_pre, nu_post) (R15; 0,0 -> 1,1) */
-  int32_t factor_mode;  /* reserved (Navier-Stokes STORE / RECOMPUTE) */
+  int32_t factor_mode;  /* 0 AUTO: heat patch solves Kronecker-diagonalised (kernels_kron.cu), N <= 256;
+                           1 LU: per-class LU factors (H5) applied by the split-form sweep */
   int32_t device;       /* CUDA device ordinal */
   void *stream;         /* cudaStream_t; NULL = default stream */
   int32_t rank, nranks; /* strip partition (nranks = 1 in this build) */
@@ -172,6 +173,26 @@ const char *wrmg_last_error(const wrmg_ctx *ctx, int32_t *level, int32_t *patch,
 
 /* Free every device and host resource of the context. */
 void wrmg_destroy(wrmg_ctx *ctx);
+
+/* Kernel timing.  wrmg_profile(ctx, 1) resets the counters and, until
+ * wrmg_profile(ctx, 0), records a CUDA event pair on the context's stream around
+ * every hot-path launch (classes below).  wrmg_kernel_stats synchronises and
+ * fills out[level * WRMG_K_COUNT + cls] for levels 0..nlevels-1 (level 0 =
+ * coarsest): launch count, summed device milliseconds, and the algorithmic
+ * bytes / flops of those launches ("Roofline accounting"). */
+enum { WRMG_K_RESIDUAL = 0, WRMG_K_SWEEP = 1, WRMG_K_RESTRICT = 2, WRMG_K_PROLONG = 3, WRMG_K_COARSE = 4,
+       WRMG_K_KRYLOV = 5, WRMG_K_COUNT = 6 };
+typedef struct {
+  int64_t launches;
+  double ms;
+  double bytes;
+  double flops;
+} wrmg_kernel_stat;
+wrmg_status wrmg_profile(wrmg_ctx *ctx, int32_t enable);
+wrmg_status wrmg_kernel_stats(wrmg_ctx *ctx, wrmg_kernel_stat *out);
+
+/* Number of kernels this library has launched in the process so far. */
+int64_t wrmg_launch_count(void);
 
 /* Host-only planning query (no device needed): sizes of the finest level and
  * hierarchy for a configuration, for tests of the host setup logic (H3). */

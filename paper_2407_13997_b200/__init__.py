@@ -10,6 +10,7 @@ from ._lib import (  # noqa: F401
     Context,
     WrmgError,
     exported_symbols,
+    launch_count,
     lib,
     wrmg_batched_lu,
     wrmg_fill_uniform,

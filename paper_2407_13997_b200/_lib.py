@@ -34,6 +34,12 @@ class wrmg_layout_t(ctypes.Structure):
                 ("smooth_dof_updates_per_vcycle", c_i64)]
 
 
+class wrmg_kernel_stat(ctypes.Structure):
+    _fields_ = [("launches", c_i64), ("ms", c_dbl), ("bytes", c_dbl), ("flops", c_dbl)]
+
+
+KERNEL_CLASSES = ["residual", "sweep", "restrict", "prolong", "coarse", "krylov"]
+
 _P = ctypes.POINTER
 _sig = {
     "wrmg_setup": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, c_dbl, _P(wrmg_coeffs), _P(c_vp)]),
@@ -56,11 +62,18 @@ _sig = {
     "wrmg_destroy": (None, [c_vp]),
     "wrmg_plan": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, _P(wrmg_layout_t)]),
     "wrmg_plan_patches": (c_i32, [_P(wrmg_mesh), c_i32, c_vp, c_vp]),
+    "wrmg_profile": (c_i32, [c_vp, c_i32]),
+    "wrmg_kernel_stats": (c_i32, [c_vp, c_vp]),
+    "wrmg_launch_count": (c_i64, []),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args
+
+
+def launch_count():
+    return lib.wrmg_launch_count()
 
 
 def exported_symbols():
@@ -128,7 +141,7 @@ class Context:
     """One wrmg_ctx: the heat space-time hierarchy on one device/stream."""
 
     def __init__(self, nx, ny=None, h=None, degree=1, q=0, nslabs=1, dt=1.0, kappa=1.0, omega_mg=1.0,
-                 nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None):
+                 nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None, factor_mode="auto"):
         import torch
         ny = nx if ny is None else ny
         h = 1.0 / ny if h is None else h
@@ -140,6 +153,7 @@ class Context:
         co.weights = 0 if weights == "pou" else 1
         co.omega_mg, co.nu_pre, co.nu_post = float(omega_mg), int(nu_pre), int(nu_post)
         co.device, co.stream, co.rank, co.nranks = int(device), c_vp(stream), 0, 1
+        co.factor_mode = {"auto": 0, "lu": 1}[factor_mode]
         self._co = co
         h_ = c_vp()
         _check(lib.wrmg_setup(ctypes.byref(self._mesh), int(degree), int(q), int(nslabs), float(dt),
@@ -201,6 +215,22 @@ class Context:
 
     def fill_uniform(self, out, first_id=0, seed=0):
         _check(lib.wrmg_fill_uniform(self._h, _ptr(out), out.numel(), int(first_id), int(seed)), self._h)
+
+    def profile(self, enable=True):
+        _check(lib.wrmg_profile(self._h, 1 if enable else 0), self._h)
+
+    def kernel_stats(self):
+        """{(class, level): dict(launches, ms, bytes, flops)} since profile(True)."""
+        nl = self.layout["nlevels"]
+        arr = (wrmg_kernel_stat * (nl * len(KERNEL_CLASSES)))()
+        _check(lib.wrmg_kernel_stats(self._h, ctypes.cast(arr, c_vp)), self._h)
+        out = {}
+        for l in range(nl):
+            for ci, name in enumerate(KERNEL_CLASSES):
+                st = arr[l * len(KERNEL_CLASSES) + ci]
+                if st.launches:
+                    out[(name, l)] = dict(launches=st.launches, ms=st.ms, bytes=st.bytes, flops=st.flops)
+        return out
 
     def sync(self):
         _check(lib.wrmg_sync(self._h), self._h)

@@ -13,6 +13,10 @@
 
 using namespace wrmg;
 
+namespace wrmg {
+int64_t g_launches = 0;
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -57,12 +61,64 @@ wrmg_status fail(wrmg_ctx *ctx, const Err &e) {
 
 void check_launch() { CK(cudaGetLastError()); }
 
+cudaEvent_t get_event(wrmg_ctx *c) {
+  if (!c->prof_pool.empty()) {
+    cudaEvent_t e = c->prof_pool.back();
+    c->prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  return e;
+}
+
+// Records a CUDA event pair around the launches issued in its scope (on the
+// context's stream) when profiling is on, with the launches' algorithmic cost.
+struct PScope {
+  wrmg_ctx *c;
+  int cls, lvl;
+  double bytes, flops;
+  cudaEvent_t a = nullptr, b = nullptr;
+  PScope(wrmg_ctx *c_, int cls_, int lvl_, double bytes_, double flops_)
+      : c(c_), cls(cls_), lvl(lvl_), bytes(bytes_), flops(flops_) {
+    if (c->prof_on) {
+      a = get_event(c);
+      b = get_event(c);
+      CK(cudaEventRecord(a, c->stream));
+    }
+  }
+  ~PScope() {
+    if (a) {
+      cudaEventRecord(b, c->stream);
+      c->prof_recs.push_back({cls, lvl, a, b, bytes, flops});
+    }
+  }
+};
+
+double residual_bytes(const wrmg_ctx *c, int l) { return 24.0 * c->lv[l].nnode * c->nt; }
+double residual_flops(const wrmg_ctx *c, int l) {
+  return 2.0 * (2 * c->nq + 1) * (double)c->lv[l].A.nnz * c->N;
+}
+double sweep_bytes(const wrmg_ctx *c, int l) { return 24.0 * c->lv[l].nfree * c->nt; }
+
+void prof_residual(wrmg_ctx *c, int l, const double *u, const double *b, double *r, bool uzero) {
+  PScope ps(c, WRMG_K_RESIDUAL, l, residual_bytes(c, l), uzero ? 0.0 : residual_flops(c, l));
+  launch_residual(c->lv[l], c->q, c->N, c->tm, u, b, r, uzero, c->stream);
+}
+
+void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
+  PScope ps(c, WRMG_K_SWEEP, l, sweep_bytes(c, l), c->sweep_flops[l]);
+  if (c->use_kron && launch_sweep_kron(c->lv[l], c->q, c->N, r, u, om, c->stream)) return;
+  launch_sweep(c->lv[l], c->q, c->N, r, u, om, c->stream);
+}
+
 void free_level(Level &L) {
   for (void *p : {(void *)L.A.rowptr, (void *)L.A.col, (void *)L.A.val, (void *)L.A.val2, (void *)L.con,
                   (void *)L.pnodes, (void *)L.ptype, (void *)L.wnode, (void *)L.type_rep, (void *)L.Dblk,
                   (void *)L.Dinv, (void *)L.G, (void *)L.piv, (void *)L.info, (void *)L.P.rowptr, (void *)L.P.col,
                   (void *)L.P.val, (void *)L.R.rowptr, (void *)L.R.col, (void *)L.R.val, (void *)L.vr, (void *)L.vz,
-                  (void *)L.vt})
+                  (void *)L.vt, (void *)L.kV, (void *)L.kVT, (void *)L.kS, (void *)L.ksig, (void *)L.cta_patch,
+                  (void *)L.cta_type, (void *)L.rcls})
     dfree(p);
 }
 
@@ -77,6 +133,40 @@ void validate(const wrmg_mesh *mesh, int degree, int q, int nslabs, double dt) {
     throw Err{WRMG_E_UNSUPPORTED, "strip partitions (x0 != 0 or nx != gnx) are not built"};
   int64_t L = (int64_t)(degree * mesh->gnx + 1) * (degree * mesh->gny + 1);
   if (L > (int64_t)INT32_MAX / 8) throw Err{WRMG_E_UNSUPPORTED, "lattice too large for int32 node ids"};
+}
+
+// Copy the residual stencil-class tables of a level to the host (kernel parameter).
+void gather_stencil(wrmg_ctx *c, Level &L) {
+  const int nc = (int)L.h_cls_rep.size();
+  L.stencil_ok = false;
+  if (nc == 0 || nc > kStencilMaxC) return;
+  int32_t *si = dalloc<int32_t>((size_t)2 * nc + 2 * nc * kStencilMaxE);
+  double *sd = dalloc<double>((size_t)2 * nc * kStencilMaxE);
+  CK(cudaMemcpyAsync(si, L.h_cls_rep.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+  launch_gather_classes(L, si, sd, c->stream);
+  check_launch();
+  std::vector<int32_t> hi((size_t)2 * nc + 2 * nc * kStencilMaxE);
+  std::vector<double> hd((size_t)2 * nc * kStencilMaxE);
+  CK(cudaMemcpyAsync(hi.data(), si, hi.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(hd.data(), sd, hd.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(si);
+  dfree(sd);
+  StencilTab &T = L.stencil;
+  std::memset(&T, 0, sizeof(T));
+  T.ncls = nc;
+  const int32_t *cnt = hi.data() + nc, *dI = cnt + nc, *dJ = dI + nc * kStencilMaxE;
+  for (int k2 = 0; k2 < nc; ++k2) {
+    if (cnt[k2] > kStencilMaxE) return;
+    T.cnt[k2] = cnt[k2];
+    for (int e = 0; e < cnt[k2]; ++e) {
+      T.dI[k2][e] = (int8_t)dI[k2 * kStencilMaxE + e];
+      T.dJ[k2][e] = (int8_t)dJ[k2 * kStencilMaxE + e];
+      T.m[k2][e] = hd[k2 * kStencilMaxE + e];
+      T.kk[k2][e] = hd[nc * kStencilMaxE + k2 * kStencilMaxE + e];
+    }
+  }
+  L.stencil_ok = true;
 }
 
 // Numeric part of setup / linearisation: H1, H4, H5 on every level + coarse block.
@@ -96,6 +186,14 @@ void factor_all(wrmg_ctx *c) {
     check_launch();
     CK(cudaStreamSynchronize(s));
     dfree(LU);
+    if (c->use_kron) {
+      double *scr = dalloc<double>((size_t)L.ntypes * 3 * L.mp * L.mp);
+      launch_kron_setup(L, c->nq, c->tm, scr, s);
+      check_launch();
+      CK(cudaStreamSynchronize(s));
+      dfree(scr);
+    }
+    gather_stencil(c, L);
   }
   Coarse &C = c->coarse;
   Level &L0 = c->lv[0];
@@ -109,6 +207,13 @@ void factor_all(wrmg_ctx *c) {
   check_launch();
   CK(cudaStreamSynchronize(s));
   dfree(LU);
+  if (c->use_kron) {
+    double *scr = dalloc<double>((size_t)3 * C.mp * C.mp);
+    launch_kron_setup_coarse(L0, C, c->nq, c->tm, scr, s);
+    check_launch();
+    CK(cudaStreamSynchronize(s));
+    dfree(scr);
+  }
   // singular pivots (R10)
   c->err_level = c->err_patch = c->err_slab = -1;
   for (size_t l = 0; l < c->lv.size(); ++l) {
@@ -140,7 +245,13 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
   cudaStream_t s = c->stream;
   Level &L = c->lv[l];
   if (l == 0) {
-    launch_coarse_solve(c->coarse, L, c->q, c->N, r, z, s);
+    const Coarse &C = c->coarse;
+    PScope ps(c, WRMG_K_COARSE, 0, 16.0 * C.nfree * c->nt + 8.0 * L.nnode * c->nt,
+              2.0 * c->N * ((double)C.m * C.m + (double)C.m * C.mp));
+    if (c->use_kron)
+      launch_coarse_solve_kron(C, L, c->q, c->N, r, z, s);
+    else
+      launch_coarse_solve(C, L, c->q, c->N, r, z, s);
     return;
   }
   const int64_t nd = ndof_level(c, l);
@@ -149,25 +260,32 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
   CK(cudaMemsetAsync(z, 0, nd * sizeof(double), s));
   for (int it = 0; it < c->co.nu_pre; ++it) {
     if (it == 0) {
-      launch_sweep(L, c->q, c->N, r, z, om, s);  // u = 0: residual is r itself
+      prof_sweep(c, l, r, z, om);  // u = 0: residual is r itself
     } else {
-      launch_residual(L, c->q, c->N, c->tm, z, r, t, false, s);
-      launch_sweep(L, c->q, c->N, t, z, om, s);
+      prof_residual(c, l, z, r, t, false);
+      prof_sweep(c, l, t, z, om);
     }
   }
-  launch_residual(L, c->q, c->N, c->tm, z, r, t, c->co.nu_pre == 0, s);
+  prof_residual(c, l, z, r, t, c->co.nu_pre == 0);
   Level &C = c->lv[l - 1];
-  launch_restrict(C, c->nt, t, C.vr, s);
+  {
+    PScope ps(c, WRMG_K_RESTRICT, l, 8.0 * (L.nnode + C.nnode) * c->nt, 2.0 * C.R.nnz * c->nt);
+    launch_restrict(C, c->nt, t, C.vr, s);
+  }
   vcycle_level(c, l - 1, C.vr, C.vz);
-  launch_prolong_add(C, c->nt, C.vz, z, s);
+  {
+    PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
+    launch_prolong_add(C, c->nt, C.vz, z, s);
+  }
   for (int it = 0; it < c->co.nu_post; ++it) {
-    launch_residual(L, c->q, c->N, c->tm, z, r, t, false, s);
-    launch_sweep(L, c->q, c->N, t, z, om, s);
+    prof_residual(c, l, z, r, t, false);
+    prof_sweep(c, l, t, z, om);
   }
   check_launch();
 }
 
 double dot_host(wrmg_ctx *c, const double *a, const double *b, int64_t n) {
+  PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 2.0 * n);
   int nb = multidot_blocks(n);
   const double *V[1] = {a};
   launch_multidot(V, 1, b, n, c->red + 64, nb, c->stream);
@@ -248,6 +366,9 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (c->mesh.nx == 0) c->mesh.nx = mesh->gnx;
     if (c->mesh.ncoarse <= 0) c->mesh.ncoarse = 4;
     c->co = *coeffs;
+    // factor_mode 0 (AUTO): Kronecker-diagonalised patch solves for the heat operator
+    // (N <= 256); 1 (LU): per-class LU factors and the split-form sweep
+    c->use_kron = coeffs->factor_mode == 0 && nslabs <= 256;
     if (!(c->co.omega_mg > 0)) c->co.omega_mg = 1.0;
     if (c->co.nu_pre <= 0 && c->co.nu_post <= 0) c->co.nu_pre = c->co.nu_post = 1;
     c->k = degree;
@@ -310,12 +431,33 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       for (int64_t i = 0; i < P.nnode; ++i)
         if (P.mu[i] > 0) w[i] = (c->co.weights == WRMG_W_NONE) ? 1.0 : 1.0 / P.mu[i];
       L.wnode = dupload(w, s);
+      {
+        double fl = 0.0;  // 2 m^2 + 2 m_p^2 per (patch, slab): LU solve + jump
+        for (int32_t ps : P.psize) fl += 2.0 * ((double)c->nq * ps) * ((double)c->nq * ps) + 2.0 * (double)ps * ps;
+        c->sweep_flops.push_back(fl * c->N);
+      }
       int m = c->nq * L.mp;
       L.Dblk = dalloc<double>((size_t)L.ntypes * m * m);
       L.Dinv = dalloc<double>((size_t)L.ntypes * m * m);
       L.G = dalloc<double>((size_t)L.ntypes * m * L.mp);
       L.piv = dalloc<int32_t>((size_t)L.ntypes * m);
       L.info = dalloc<int32_t>(L.ntypes);
+      L.rcls = dupload(P.rcls, s);
+      L.h_cls_rep = P.cls_rep;
+      if (c->use_kron) {
+        const int ld = (L.mp + 1) & ~1;
+        L.kV = dalloc<double>((size_t)L.ntypes * L.mp * ld);
+        L.kVT = dalloc<double>((size_t)L.ntypes * L.mp * ld);
+        L.kS = dalloc<double>((size_t)L.ntypes * L.mp * c->nq * c->nq);
+        L.ksig = dalloc<double>((size_t)L.ntypes * L.mp);
+        const int C = (c->N + 31) / 32;
+        L.kron_pp = std::max(1, 8 / C);
+        std::vector<int32_t> cp, ct;
+        plan_sweep_ctas(P, L.kron_pp, cp, ct);
+        L.kron_ncta = (int)ct.size();
+        L.cta_patch = dupload(cp, s);
+        L.cta_type = dupload(ct, s);
+      }
       if (l < nl - 1) {
         L.vr = dalloc<double>(L.nnode * c->nt);
         L.vz = dalloc<double>(L.nnode * c->nt);
@@ -359,6 +501,12 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       C.Y = dalloc<double>((size_t)(c->N + 1) * C.mp);
       C.piv = dalloc<int32_t>(C.m);
       C.info = dalloc<int32_t>(1);
+      if (c->use_kron) {
+        C.kV = dalloc<double>((size_t)C.mp * C.mp);
+        C.kVT = dalloc<double>((size_t)C.mp * C.mp);
+        C.kS = dalloc<double>((size_t)C.mp * c->nq * c->nq);
+        C.ksig = dalloc<double>((size_t)C.mp);
+      }
     }
     c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
     c->red = dalloc<double>(64 + 64 * 148 * 4);
@@ -426,7 +574,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
   if (!c || !u || !b || !r) return WRMG_E_INVALID;
   if (nonlinear) return WRMG_E_UNSUPPORTED;
   try {
-    launch_residual(c->lv.back(), c->q, c->N, c->tm, u, b, r, false, c->stream);
+    prof_residual(c, (int)c->lv.size() - 1, u, b, r, false);
     check_launch();
     return WRMG_OK;
   } catch (const Err &e) {
@@ -453,10 +601,10 @@ wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
 wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps, double omega) {
   if (!c || !u || !b || nsweeps < 0) return WRMG_E_INVALID;
   try {
-    Level &L = c->lv.back();
+    const int l = (int)c->lv.size() - 1;
     for (int s = 0; s < nsweeps; ++s) {
-      launch_residual(L, c->q, c->N, c->tm, u, b, c->tmp, false, c->stream);
-      launch_sweep(L, c->q, c->N, c->tmp, u, omega, c->stream);
+      prof_residual(c, l, u, b, c->tmp, false);
+      prof_sweep(c, l, c->tmp, u, omega);
     }
     check_launch();
     return WRMG_OK;
@@ -528,8 +676,11 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
     auto multidot = [&](int nv, const double *w, std::vector<double> &h) {
       int nb = multidot_blocks(n);
       std::vector<const double *> Vp(c->V.begin(), c->V.begin() + nv);
-      launch_multidot(Vp.data(), nv, w, n, part, nb, s);
-      launch_reduce_partials(part, nb, nv, red, s);
+      {
+        PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (nv + 1) * n, 2.0 * nv * n);
+        launch_multidot(Vp.data(), nv, w, n, part, nb, s);
+        launch_reduce_partials(part, nb, nv, red, s);
+      }
       h.resize(nv);
       CK(cudaMemcpyAsync(h.data(), red, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -545,7 +696,10 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
     if (done) status = WRMG_OK;
     std::vector<double> H((size_t)(restart + 1) * restart), cs(restart), sn(restart), g(restart + 1), h, h2, y;
     while (!done && its < maxit) {
-      launch_scale(c->V[0], c->tmp, 1.0 / beta, n, s);
+      {
+        PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 1.0 * n);
+        launch_scale(c->V[0], c->tmp, 1.0 / beta, n, s);
+      }
       std::fill(H.begin(), H.end(), 0.0);
       std::fill(g.begin(), g.end(), 0.0);
       g[0] = beta;
@@ -554,13 +708,22 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         vcycle_level(c, (int)c->lv.size() - 1, c->V[j], c->Z[j]);
         // w = A Z_j
         CK(cudaMemsetAsync(c->w, 0, n * sizeof(double), s));
-        launch_residual(L, c->q, c->N, c->tm, c->Z[j], c->w, c->tmp, false, s);
-        launch_scale(c->w, c->tmp, -1.0, n, s);
+        prof_residual(c, (int)c->lv.size() - 1, c->Z[j], c->w, c->tmp, false);
+        {
+          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 1.0 * n);
+          launch_scale(c->w, c->tmp, -1.0, n, s);
+        }
         // CGS2
         multidot(j + 1, c->w, h);
-        launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+        {
+          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 1) * n);
+          launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+        }
         multidot(j + 1, c->w, h2);
-        launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+        {
+          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 1) * n);
+          launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+        }
         for (int i = 0; i <= j; ++i) h[i] += h2[i];
         const double hn = norm(c->w);
         std::vector<double> col(restart + 1, 0.0);
@@ -586,7 +749,10 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           done = true;
           break;
         }
-        launch_scale(c->V[j + 1], c->w, 1.0 / hn, n, s);
+        {
+          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 1.0 * n);
+          launch_scale(c->V[j + 1], c->w, 1.0 / hn, n, s);
+        }
         if (std::fabs(g[j + 1]) <= target) {
           status = WRMG_OK;
           done = true;
@@ -604,17 +770,20 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         y[i] = acc / H[(size_t)i * restart + i];
       }
       CK(cudaMemcpyAsync(red, y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, s));
-      launch_multiaxpy(x, c->Z.data(), red, jend, n, 1.0, s);
+      {
+        PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (jend + 2) * n, 2.0 * jend * n);
+        launch_multiaxpy(x, c->Z.data(), red, jend, n, 1.0, s);
+      }
       CK(cudaStreamSynchronize(s));
       if (done) break;
-      launch_residual(L, c->q, c->N, c->tm, x, b, c->tmp, false, s);
+      prof_residual(c, (int)c->lv.size() - 1, x, b, c->tmp, false);
       beta = norm(c->tmp);
       if (beta <= target) {
         status = WRMG_OK;
         break;
       }
     }
-    launch_residual(L, c->q, c->N, c->tm, x, b, c->tmp, false, s);
+    prof_residual(c, (int)c->lv.size() - 1, x, b, c->tmp, false);
     const double rn = norm(c->tmp);
     if (iters) *iters = its;
     if (relres) *relres = bnorm > 0 ? rn / bnorm : 0.0;
@@ -625,6 +794,49 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
     return fail(c, e);
   }
 }
+
+wrmg_status wrmg_profile(wrmg_ctx *c, int32_t enable) {
+  if (!c) return WRMG_E_INVALID;
+  try {
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto &r : c->prof_recs) {
+      c->prof_pool.push_back(r.a);
+      c->prof_pool.push_back(r.b);
+    }
+    c->prof_recs.clear();
+    std::memset(c->stats, 0, sizeof(c->stats));
+    c->prof_on = enable != 0;
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
+  if (!c || !out) return WRMG_E_INVALID;
+  try {
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto &r : c->prof_recs) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      wrmg_kernel_stat &st = c->stats[r.cls][r.lvl];
+      st.launches += 1;
+      st.ms += ms;
+      st.bytes += r.bytes;
+      st.flops += r.flops;
+      c->prof_pool.push_back(r.a);
+      c->prof_pool.push_back(r.b);
+    }
+    c->prof_recs.clear();
+    for (size_t l = 0; l < c->lv.size(); ++l)
+      for (int k2 = 0; k2 < WRMG_K_COUNT; ++k2) out[l * WRMG_K_COUNT + k2] = c->stats[k2][l];
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+int64_t wrmg_launch_count(void) { return g_launches; }
 
 wrmg_status wrmg_newton(wrmg_ctx *c, double *, double, int32_t, int32_t *, int32_t *) {
   if (c) c->err = "Navier-Stokes Newton is not built";
@@ -688,7 +900,8 @@ void wrmg_destroy(wrmg_ctx *c) {
   for (auto &L : c->lv) free_level(L);
   Coarse &C = c->coarse;
   for (void *p : {(void *)C.nodes, (void *)C.Dblk, (void *)C.DinvT, (void *)C.GT, (void *)C.Gq, (void *)C.Z,
-                  (void *)C.Y, (void *)C.piv, (void *)C.info})
+                  (void *)C.Y, (void *)C.piv, (void *)C.info, (void *)C.kV, (void *)C.kVT, (void *)C.kS,
+                  (void *)C.ksig})
     dfree(p);
   for (double *p : c->V) dfree(p);
   for (double *p : c->Z) dfree(p);
@@ -696,6 +909,11 @@ void wrmg_destroy(wrmg_ctx *c) {
   dfree(c->red);
   dfree(c->tmp);
   dfree(c->ref_dev);
+  for (auto &r : c->prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : c->prof_pool) cudaEventDestroy(e);
   delete c;
 }
 

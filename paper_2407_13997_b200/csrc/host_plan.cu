@@ -105,6 +105,45 @@ void plan_level(int nx, int ny, double h, int k, PlanLevel *P) {
   P->npatch = (int64_t)P->psize.size();
   P->ntypes = (int)types.size();
   P->mu = mu;
+  // stencil classes of free rows: (I mod k, J mod k, which of the candidate cells exist)
+  std::map<std::vector<int32_t>, int> cls;
+  P->rcls.assign(nn, kRowConstrained);
+  P->cls_rep.clear();
+  for (int J = 0; J < Ly; ++J)
+    for (int I = 0; I < Lx; ++I) {
+      int64_t i = (int64_t)J * Lx + I;
+      if (P->con[i]) continue;
+      int ci[6], cj[6], t[6], la[6], lb[6];
+      int nc = cells_of_node(k, nx, ny, I, J, ci, cj, t, la, lb);
+      std::vector<int32_t> sig = {I % k, J % k};
+      for (int c = 0; c < nc; ++c) {
+        sig.push_back(ci[c] * k - I);
+        sig.push_back(cj[c] * k - J);
+        sig.push_back(t[c]);
+      }
+      auto it = cls.find(sig);
+      int id;
+      if (it == cls.end()) {
+        id = (int)cls.size();
+        cls.emplace(sig, id);
+        P->cls_rep.push_back((int32_t)i);
+      } else {
+        id = it->second;
+      }
+      P->rcls[i] = id < (int)kRowGeneric ? (uint8_t)id : kRowGeneric;
+    }
+}
+
+void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type) {
+  cta_patch.clear();
+  cta_type.clear();
+  std::vector<std::vector<int32_t>> by(P.ntypes);
+  for (int64_t p = 0; p < P.npatch; ++p) by[P.ptype[p]].push_back((int32_t)p);
+  for (int t = 0; t < P.ntypes; ++t)
+    for (size_t s = 0; s < by[t].size(); s += pp) {
+      cta_type.push_back(t);
+      for (int j = 0; j < pp; ++j) cta_patch.push_back(s + j < by[t].size() ? by[t][s + j] : -1);
+    }
 }
 
 // P_h from coarse (ncx x ncy, lattice Lxc) to fine (2ncx x 2ncy): row i (fine

@@ -37,6 +37,15 @@ struct Temporal {
 };
 void build_temporal(int q, double dt, Temporal *out);
 
+// Residual stencil classes (kernels_residual.cu), passed by value as a kernel parameter.
+constexpr int kStencilMaxC = 16, kStencilMaxE = 40;
+struct StencilTab {
+  int ncls;
+  int cnt[kStencilMaxC];
+  int8_t dI[kStencilMaxC][kStencilMaxE], dJ[kStencilMaxC][kStencilMaxE];
+  double m[kStencilMaxC][kStencilMaxE], kk[kStencilMaxC][kStencilMaxE];
+};
+
 // ---------------------------------------------------------------- device data
 struct DevCSR {
   int64_t nrow = 0, nnz = 0;
@@ -65,6 +74,15 @@ struct Level {
   double *G = nullptr;              // [ntypes][m][mp] jump propagator Dinv[:, a=0] M_p
   int32_t *piv = nullptr, *info = nullptr;
   std::vector<int32_t> h_type_rep;
+  // Kronecker-diagonalised sweep (kernels_kron.cu): per class V (mp x ld), V^T, S, sigma
+  double *kV = nullptr, *kVT = nullptr, *kS = nullptr, *ksig = nullptr;
+  int32_t *cta_patch = nullptr, *cta_type = nullptr;
+  int kron_pp = 1, kron_ncta = 0;
+  // residual stencil classes
+  uint8_t *rcls = nullptr;
+  std::vector<int32_t> h_cls_rep;
+  bool stencil_ok = false;
+  StencilTab stencil{};
   // transfer from this level to the next finer (stored on the coarse side)
   DevCSR P;    // rows: fine nodes, cols: coarse nodes
   DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)
@@ -80,6 +98,7 @@ struct Coarse {
   double *DinvT = nullptr;    // m x m, column-major inverse (Dinv^T row-major)
   double *Gq = nullptr;       // mp x mp row-major: end-trace propagator
   double *GT = nullptr;       // mp x m: G transposed (G[rho][j] at GT[j*m + rho])
+  double *kV = nullptr, *kVT = nullptr, *kS = nullptr, *ksig = nullptr;  // Kronecker coarse solve
   double *Z = nullptr;        // N x m scratch
   double *Y = nullptr;        // (N+1) x mp scratch
   int32_t *piv = nullptr, *info = nullptr;
@@ -104,11 +123,24 @@ struct wrmg_ctx {
   std::vector<double *> V, Z;
   double *w = nullptr, *red = nullptr, *red_host = nullptr;
   double *tmp = nullptr;        // finest-level scratch (residual)
+  bool use_kron = true;         // factor_mode AUTO: Kronecker-diagonalised heat patch solves
   std::string err;
   int err_level = -1, err_patch = -1, err_slab = -1;
+  // kernel timing (wrmg_profile / wrmg_kernel_stats)
+  struct ProfRec {
+    int cls, lvl;
+    cudaEvent_t a, b;
+    double bytes, flops;
+  };
+  bool prof_on = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> prof_pool;
+  wrmg_kernel_stat stats[WRMG_K_COUNT][16];
+  std::vector<double> sweep_flops;  // per level: algorithmic flops of one sweep
 };
 
 namespace wrmg {
+extern int64_t g_launches;  // kernels launched by this library (process-wide)
 // kernel launchers (kernels_*.cu)
 void launch_assemble_spatial(const Level &L, int k, const double *ref_dev, double kappa, cudaStream_t s);
 void launch_patch_blocks(const Level &L, int nq, const Temporal &tm, cudaStream_t s);
@@ -123,6 +155,14 @@ void launch_restrict(const Level &coarse, int64_t nt, const double *rf, double *
 void launch_prolong_add(const Level &coarse, int64_t nt, const double *ec, double *uf, cudaStream_t s);
 void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const double *r, double *x,
                          cudaStream_t s);
+void launch_kron_setup(const Level &L, int nq, const Temporal &tm, double *scratch, cudaStream_t s);
+void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal &tm, double *scratch, cudaStream_t s);
+bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s);
+void launch_coarse_solve_kron(const Coarse &C, const Level &L, int q, int N, const double *r, double *x,
+                              cudaStream_t s);
+void launch_gather_classes(const Level &L, int32_t *scratch_i, double *scratch_d, cudaStream_t s);
+bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const double *u, const double *b,
+                         double *r, cudaStream_t s);
 void launch_rhs(const Level &L, int q, int N, const Temporal &tm, const double *fhat, double *b, cudaStream_t s);
 void launch_fill_uniform(double *out, int64_t count, uint64_t first, uint64_t seed, cudaStream_t s);
 // Krylov helpers

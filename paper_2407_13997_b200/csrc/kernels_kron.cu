@@ -1,0 +1,488 @@
+// Kronecker-diagonalised waveform-relaxation patch solves (H7 + H8 for the
+// heat operator, and the coarse solve H11).
+//
+// The heat patch block is a Kronecker sum (tensor-product
+// space-time discretisation; eq. heatfem):
+//     D_p = (C + E0) (x) M_p + Mt (x) K_p,      L_p = -E1 (x) M_p,  E1 = e_0 e_q^T (R2),
+// with M_p, K_p symmetric and M_p positive definite.  With the generalised
+// eigenpairs K_p V = M_p V Lambda, V^T M_p V = I (computed once per patch
+// translation class, k_kron_setup), the patch space-time system decouples into
+// m_p independent temporal problems, one per spatial mode i:
+//     (C + E0 + lambda_i Mt) w_{n,i} = ghat_{n,i} + e_0 y_{n-1,i},
+//     ghat_n = (I (x) V^T) g_n,    x_n = (I (x) V) w_n,    y_{n,i} = w_{n,i}[q],
+// because V^T M_p V = I turns the jump carry M_p x_{n-1}[q] into y_{n-1}.  With
+// S_i = (C + E0 + lambda_i Mt)^{-1} and sigma_i = S_i[q][0], the end trace obeys
+// the scalar affine recurrence  y_{n,i} = (S_i ghat_{n,i})[q] + sigma_i y_{n-1,i},
+// solved for 32 slabs at once by a warp shuffle scan (lanes = slabs) and across
+// 32-slab chunks through shared memory (warps = chunks).  This is an exact
+// solve of A_p x = g (R9), the same operator the LU path factors; it differs
+// from the LU result only by rounding.  Per (patch, slab) it costs
+// 2 (q+1) m_p^2 + O((q+1)^2 m_p) FMAs instead of the LU solve's (q+1)^2 m_p^2 + m_p^2.
+#include <cfloat>
+
+#include "internal.h"
+
+namespace wrmg {
+namespace {
+
+struct TMk {
+  double CE[16], Mt[16];
+};
+
+__device__ __forceinline__ int csr_find_k(const int32_t *rowptr, const int32_t *col, int64_t i, int32_t j) {
+  int lo = rowptr[i], hi = rowptr[i + 1] - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int32_t c = col[mid];
+    if (c == j) return mid;
+    if (c < j) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return -1;
+}
+
+// One warp per class: generalised symmetric eigenproblem K v = lambda M v by
+// Cholesky M = L L^T, C = L^-1 K L^-T, cyclic Jacobi C = Q Lambda Q^T, V = L^-T Q;
+// then the per-mode temporal inverses S_i and multipliers sigma_i.
+// Outputs (stride mp, pad modes zero): V[t][j][i] (row j = patch node),
+// VT[t][i][j], S[t][i][nq*nq], sig[t][i].
+__global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                             const double *__restrict__ Mv, const double *__restrict__ Kv,
+                             const int32_t *__restrict__ nodes_all, const int32_t *__restrict__ rep, int mp, int nq,
+                             TMk tm, double *__restrict__ scratch, int ld, double *__restrict__ Vout,
+                             double *__restrict__ VTout, double *__restrict__ Sout, double *__restrict__ sigout,
+                             int32_t *__restrict__ info) {
+  const int t = blockIdx.x, lane = threadIdx.x;
+  const int32_t *nodes = nodes_all + (rep ? (int64_t)rep[t] * mp : 0);
+  int m = 0;
+  while (m < mp && nodes[m] >= 0) ++m;
+  double *A = scratch + (size_t)t * 3 * mp * mp;  // M -> L
+  double *B = A + (size_t)mp * mp;                // K -> X -> C
+  double *Q = B + (size_t)mp * mp;
+  for (int e = lane; e < m * m; e += 32) {
+    int i = e / m, j = e % m;
+    int pos = csr_find_k(rowptr, col, nodes[i], nodes[j]);
+    A[e] = pos >= 0 ? Mv[pos] : 0.0;
+    B[e] = pos >= 0 ? Kv[pos] : 0.0;
+    Q[e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  int bad = 0;
+  // Cholesky (lower, in place, row-major A[i*m+j], j <= i)
+  for (int j = 0; j < m; ++j) {
+    double d = A[j * m + j];
+    for (int p = 0; p < j; ++p) d -= A[j * m + p] * A[j * m + p];
+    if (!(d > 0.0)) bad = 1;
+    d = sqrt(fmax(d, 1e-300));
+    __syncwarp();
+    for (int i = j + 1 + lane; i < m; i += 32) {
+      double s = A[i * m + j];
+      for (int p = 0; p < j; ++p) s -= A[i * m + p] * A[j * m + p];
+      A[i * m + j] = s / d;
+    }
+    __syncwarp();
+    if (lane == 0) A[j * m + j] = d;
+    __syncwarp();
+  }
+  // X = L^-1 K (columns in parallel), then C = L^-1 X^T
+  for (int c = lane; c < m; c += 32)
+    for (int i = 0; i < m; ++i) {
+      double s = B[i * m + c];
+      for (int p = 0; p < i; ++p) s -= A[i * m + p] * B[p * m + c];
+      B[i * m + c] = s / A[i * m + i];
+    }
+  __syncwarp();
+  // transpose X in place, then apply L^-1 again (C = L^-1 X^T)
+  for (int e = lane; e < m * m; e += 32) {
+    int i = e / m, j = e % m;
+    if (i < j) {
+      double tmp = B[i * m + j];
+      B[i * m + j] = B[j * m + i];
+      B[j * m + i] = tmp;
+    }
+  }
+  __syncwarp();
+  for (int c = lane; c < m; c += 32)
+    for (int i = 0; i < m; ++i) {
+      double s = B[i * m + c];
+      for (int p = 0; p < i; ++p) s -= A[i * m + p] * B[p * m + c];
+      B[i * m + c] = s / A[i * m + i];
+    }
+  __syncwarp();
+  for (int e = lane; e < m * m; e += 32) {  // symmetrise
+    int i = e / m, j = e % m;
+    if (i < j) {
+      double s = 0.5 * (B[i * m + j] + B[j * m + i]);
+      B[i * m + j] = s;
+      B[j * m + i] = s;
+    }
+  }
+  __syncwarp();
+  // cyclic Jacobi
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (int e = lane; e < m * m; e += 32) {
+      int i = e / m, j = e % m;
+      if (i != j) off += B[e] * B[e];
+      else dia += B[e] * B[e];
+    }
+    for (int o = 16; o; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      dia += __shfl_xor_sync(0xffffffffu, dia, o);
+    }
+    if (off <= 1e-32 * dia) break;
+    for (int p = 0; p < m - 1; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = B[p * m + q];
+        if (fabs(apq) <= 1e-300) continue;
+        const double app = B[p * m + p], aqq = B[q * m + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+        __syncwarp();
+        for (int k2 = lane; k2 < m; k2 += 32) {  // columns p, q
+          double akp = B[k2 * m + p], akq = B[k2 * m + q];
+          B[k2 * m + p] = c * akp - s * akq;
+          B[k2 * m + q] = s * akp + c * akq;
+          double qkp = Q[k2 * m + p], qkq = Q[k2 * m + q];
+          Q[k2 * m + p] = c * qkp - s * qkq;
+          Q[k2 * m + q] = s * qkp + c * qkq;
+        }
+        __syncwarp();
+        for (int k2 = lane; k2 < m; k2 += 32) {  // rows p, q
+          double apk = B[p * m + k2], aqk = B[q * m + k2];
+          B[p * m + k2] = c * apk - s * aqk;
+          B[q * m + k2] = s * apk + c * aqk;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          B[p * m + q] = 0.0;
+          B[q * m + p] = 0.0;
+        }
+        __syncwarp();
+      }
+  }
+  // V = L^-T Q (columns in parallel): back substitution with L^T
+  double *Vt = Vout + (size_t)t * mp * ld, *VTt = VTout + (size_t)t * mp * ld;
+  for (int e = lane; e < mp * ld; e += 32) {
+    Vt[e] = 0.0;
+    VTt[e] = 0.0;
+  }
+  __syncwarp();
+  for (int c = lane; c < m; c += 32)
+    for (int i = m - 1; i >= 0; --i) {
+      double s = Q[i * m + c];
+      for (int p = i + 1; p < m; ++p) s -= A[p * m + i] * Q[p * m + c];
+      Q[i * m + c] = s / A[i * m + i];
+    }
+  __syncwarp();
+  for (int e = lane; e < m * m; e += 32) {
+    int j = e / m, i = e % m;  // node j, mode i
+    Vt[j * ld + i] = Q[e];
+    VTt[i * ld + j] = Q[e];
+  }
+  // per mode: S_i = (CE + lambda_i Mt)^-1 by Gauss-Jordan with partial pivoting
+  for (int i = lane; i < mp; i += 32) {
+    const double lam = i < m ? B[i * m + i] : 0.0;
+    double a[16], inv[16];
+    for (int r = 0; r < nq; ++r)
+      for (int c = 0; c < nq; ++c) {
+        a[r * nq + c] = tm.CE[r * nq + c] + lam * tm.Mt[r * nq + c];
+        inv[r * nq + c] = (r == c) ? 1.0 : 0.0;
+      }
+    for (int c = 0; c < nq; ++c) {
+      int pr = c;
+      for (int r = c + 1; r < nq; ++r)
+        if (fabs(a[r * nq + c]) > fabs(a[pr * nq + c])) pr = r;
+      for (int c2 = 0; c2 < nq; ++c2) {
+        double x = a[c * nq + c2]; a[c * nq + c2] = a[pr * nq + c2]; a[pr * nq + c2] = x;
+        x = inv[c * nq + c2]; inv[c * nq + c2] = inv[pr * nq + c2]; inv[pr * nq + c2] = x;
+      }
+      const double d = a[c * nq + c];
+      if (d == 0.0) bad = 1;
+      for (int c2 = 0; c2 < nq; ++c2) {
+        a[c * nq + c2] /= d;
+        inv[c * nq + c2] /= d;
+      }
+      for (int r = 0; r < nq; ++r)
+        if (r != c) {
+          const double f = a[r * nq + c];
+          for (int c2 = 0; c2 < nq; ++c2) {
+            a[r * nq + c2] -= f * a[c * nq + c2];
+            inv[r * nq + c2] -= f * inv[c * nq + c2];
+          }
+        }
+    }
+    for (int e = 0; e < nq * nq; ++e) Sout[((size_t)t * mp + i) * nq * nq + e] = inv[e];
+    sigout[(size_t)t * mp + i] = inv[(nq - 1) * nq + 0];
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) info[t] = bad;
+}
+
+// ------------------------------------------------------------------- sweep
+// CTA = PP patches of one class x C chunks of 32 slabs (warp w: patch w / C,
+// chunk w % C).  Lanes are slabs: gathers and scatters touch 32 (q+1)
+// contiguous doubles per patch node (waveform-major layout, R4).
+template <int NQ, int MP>
+__global__ void __launch_bounds__(256) k_sweep_kron(int N, int C, int PP, const int32_t *__restrict__ cta_patch,
+                                                    const int32_t *__restrict__ cta_type,
+                                                    const int32_t *__restrict__ pnodes,
+                                                    const double *__restrict__ Vg, const double *__restrict__ VTg,
+                                                    const double *__restrict__ Sg, const double *__restrict__ sigg,
+                                                    const double *__restrict__ wnode, double omega,
+                                                    const double *__restrict__ r, double *__restrict__ u) {
+  constexpr int MPS = (MP + 1) & ~1;  // even row stride: 16-byte aligned rows for LDS.128
+  extern __shared__ double sm[];
+  double *sV = sm;                  // MP*MPS  V[j][i]
+  double *sVT = sV + MP * MPS;      // MP*MPS  V^T[i][j]
+  double *sS = sVT + MP * MPS;      // MP*NQ*NQ
+  double *ssig = sS + MP * NQ * NQ; // MP
+  double *swt = ssig + MP;          // PP*MP
+  double *scar = swt + PP * MP;     // PP*C*MP chunk-end values
+  int *snode = reinterpret_cast<int *>(scar + PP * C * MP);  // PP*MP
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int cta = blockIdx.x, ty = cta_type[cta];
+  for (int e = tid; e < MP * MPS; e += blockDim.x) {
+    sV[e] = Vg[(size_t)ty * MP * MPS + e];
+    sVT[e] = VTg[(size_t)ty * MP * MPS + e];
+  }
+  for (int e = tid; e < MP * NQ * NQ; e += blockDim.x) sS[e] = Sg[(size_t)ty * MP * NQ * NQ + e];
+  for (int e = tid; e < MP; e += blockDim.x) ssig[e] = sigg[(size_t)ty * MP + e];
+  for (int e = tid; e < PP * MP; e += blockDim.x) {
+    const int pp = e / MP, j = e % MP;
+    const int p = cta_patch[(size_t)cta * PP + pp];
+    const int nd = p >= 0 ? pnodes[(size_t)p * MP + j] : -1;
+    snode[e] = nd;
+    swt[e] = nd >= 0 ? omega * wnode[nd] : 0.0;
+  }
+  __syncthreads();
+  const int pp = w / C, c = w % C;
+  const int *nodes = snode + pp * MP;
+  const int64_t NT = (int64_t)N * NQ;
+  const int n = c * 32 + lane;
+  const bool valid = n < N;
+  // 1. ghat = (I (x) V^T) g, one temporal node at a time
+  double t[NQ][MP];
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double g[MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) {
+      const int nd = nodes[j];
+      g[j] = (nd >= 0 && valid) ? __ldg(r + (int64_t)nd * NT + (int64_t)n * NQ + a) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < MP; ++i) t[a][i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < MP; ++j) {
+      const double2 *row = reinterpret_cast<const double2 *>(sV + j * MPS);
+#pragma unroll
+      for (int i2 = 0; i2 < MP / 2; ++i2) {
+        const double2 v = row[i2];
+        t[a][2 * i2] = fma(v.x, g[j], t[a][2 * i2]);
+        t[a][2 * i2 + 1] = fma(v.y, g[j], t[a][2 * i2 + 1]);
+      }
+      if constexpr (MP % 2) t[a][MP - 1] = fma(sV[j * MPS + MP - 1], g[j], t[a][MP - 1]);
+    }
+  }
+  // 2. per mode: t = S_i ghat, then the local scan of the end trace (carry-in 0)
+#pragma unroll
+  for (int i = 0; i < MP; ++i) {
+    double gh[NQ];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) gh[a] = t[a][i];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 < NQ; ++b2) s = fma(sS[(i * NQ + a) * NQ + b2], gh[b2], s);
+      t[a][i] = s;
+    }
+    double v = t[NQ - 1][i], p = ssig[i];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v = fma(p, o, v);
+      p *= p;
+    }
+    t[NQ - 1][i] = v;
+    if (lane == 31) scar[(pp * C + c) * MP + i] = v;
+  }
+  __syncthreads();
+  // 3. carry across chunks, end traces, full mode solutions, back-transform, scatter
+#pragma unroll
+  for (int i = 0; i < MP; ++i) {
+    const double sg = ssig[i];
+    double s32 = sg;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) s32 *= s32;
+    double Y = 0.0;
+    for (int c2 = 0; c2 < c; ++c2) Y = fma(s32, Y, scar[(pp * C + c2) * MP + i]);
+    double pw = 1.0, bs = sg;
+    int e = lane + 1;
+#pragma unroll
+    for (int bit = 0; bit < 6; ++bit) {
+      if (e & 1) pw *= bs;
+      bs *= bs;
+      e >>= 1;
+    }
+    const double y = fma(pw, Y, t[NQ - 1][i]);
+    double yp = __shfl_up_sync(0xffffffffu, y, 1);
+    if (lane == 0) yp = Y;
+#pragma unroll
+    for (int a = 0; a < NQ - 1; ++a) t[a][i] = fma(sS[(i * NQ + a) * NQ + 0], yp, t[a][i]);
+    t[NQ - 1][i] = y;
+  }
+  double *ub = u + (int64_t)n * NQ;
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double x[MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) x[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < MP; ++i) {
+      const double2 *row = reinterpret_cast<const double2 *>(sVT + i * MPS);
+#pragma unroll
+      for (int j2 = 0; j2 < MP / 2; ++j2) {
+        const double2 v = row[j2];
+        x[2 * j2] = fma(v.x, t[a][i], x[2 * j2]);
+        x[2 * j2 + 1] = fma(v.y, t[a][i], x[2 * j2 + 1]);
+      }
+      if constexpr (MP % 2) x[MP - 1] = fma(sVT[i * MPS + MP - 1], t[a][i], x[MP - 1]);
+    }
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < MP; ++j) {
+        const int nd = nodes[j];
+        if (nd >= 0) atomicAdd(ub + (int64_t)nd * NT + a, swt[pp * MP + j] * x[j]);
+      }
+    }
+  }
+}
+
+template <int NQ, int MP>
+void sweep_kron_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
+  const int C = (N + 31) / 32;
+  const int PP = L.kron_pp;
+  constexpr int MPS = (MP + 1) & ~1;
+  size_t smem = (size_t)(2 * MP * MPS + MP * NQ * NQ + MP + PP * MP + PP * C * MP) * sizeof(double) +
+                (size_t)PP * MP * sizeof(int);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_kron<NQ, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_sweep_kron<NQ, MP><<<L.kron_ncta, 32 * C * PP, smem, s>>>(N, C, PP, L.cta_patch, L.cta_type, L.pnodes, L.kV,
+                                                               L.kVT, L.kS, L.ksig, L.wnode, omega, r, u);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------- coarse (kron)
+// z-transform: T[n][a][i] = (S_i (V^T g_n)[:, i])[a] for every slab (block n).
+__global__ void __launch_bounds__(256) k_ckron_fwd(int mp, int nq, int64_t NT, const int32_t *__restrict__ nodes,
+                                                   const double *__restrict__ V, const double *__restrict__ S,
+                                                   const double *__restrict__ r, double *__restrict__ T) {
+  extern __shared__ double g[];  // nq * mp
+  const int n = blockIdx.x;
+  for (int e = threadIdx.x; e < nq * mp; e += blockDim.x) {
+    const int a = e / mp, j = e % mp;
+    g[e] = r[(int64_t)nodes[j] * NT + (int64_t)n * nq + a];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < mp; i += blockDim.x) {
+    double gh[4] = {0, 0, 0, 0};
+    for (int j = 0; j < mp; ++j) {
+      const double v = V[(int64_t)j * mp + i];
+      for (int a = 0; a < nq; ++a) gh[a] = fma(v, g[a * mp + j], gh[a]);
+    }
+    for (int a = 0; a < nq; ++a) {
+      double s = 0.0;
+      for (int b = 0; b < nq; ++b) s = fma(S[((int64_t)i * nq + a) * nq + b], gh[b], s);
+      T[((int64_t)n * nq + a) * mp + i] = s;
+    }
+  }
+}
+
+// per-mode recurrence over all slabs (one thread per mode)
+__global__ void k_ckron_scan(int N, int mp, int nq, const double *__restrict__ S, const double *__restrict__ sig,
+                             double *__restrict__ T) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= mp) return;
+  const double sg = sig[i];
+  double y = 0.0;
+  for (int n = 0; n < N; ++n) {
+    double *Tn = T + (int64_t)n * nq * mp;
+    const double yn = fma(sg, y, Tn[(nq - 1) * mp + i]);
+    for (int a = 0; a < nq - 1; ++a) Tn[a * mp + i] = fma(S[((int64_t)i * nq + a) * nq + 0], y, Tn[a * mp + i]);
+    Tn[(nq - 1) * mp + i] = yn;
+    y = yn;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ckron_bwd(int mp, int nq, int64_t NT, const int32_t *__restrict__ nodes,
+                                                   const double *__restrict__ VT, const double *__restrict__ T,
+                                                   double *__restrict__ x) {
+  extern __shared__ double w[];  // nq * mp
+  const int n = blockIdx.x;
+  for (int e = threadIdx.x; e < nq * mp; e += blockDim.x) w[e] = T[(int64_t)n * nq * mp + e];
+  __syncthreads();
+  for (int j = threadIdx.x; j < mp; j += blockDim.x) {
+    double xs[4] = {0, 0, 0, 0};
+    for (int i = 0; i < mp; ++i) {
+      const double v = VT[(int64_t)i * mp + j];
+      for (int a = 0; a < nq; ++a) xs[a] = fma(v, w[a * mp + i], xs[a]);
+    }
+    for (int a = 0; a < nq; ++a) x[(int64_t)nodes[j] * NT + (int64_t)n * nq + a] = xs[a];
+  }
+}
+
+TMk make_tmk(const Temporal &T) {
+  TMk t{};
+  for (int e = 0; e < T.nq * T.nq; ++e) {
+    t.CE[e] = T.CE[e];
+    t.Mt[e] = T.Mt[e];
+  }
+  return t;
+}
+
+}  // namespace
+
+void launch_kron_setup(const Level &L, int nq, const Temporal &tm, double *scratch, cudaStream_t s) {
+  k_kron_setup<<<L.ntypes, 32, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, L.pnodes, L.type_rep, L.mp, nq,
+                                       make_tmk(tm), scratch, (L.mp + 1) & ~1, L.kV, L.kVT, L.kS, L.ksig, L.info);
+  ++g_launches;
+}
+
+void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal &tm, double *scratch,
+                              cudaStream_t s) {
+  k_kron_setup<<<1, 32, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, C.nodes, nullptr, C.mp, nq, make_tmk(tm),
+                                scratch, C.mp, C.kV, C.kVT, C.kS, C.ksig, C.info);
+  ++g_launches;
+}
+
+bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s) {
+  const int nq = q + 1;
+#define WRMG_SK(NQ, MP) \
+  if (nq == NQ && L.mp == MP) { sweep_kron_launch<NQ, MP>(L, N, r, u, omega, s); return true; }
+  WRMG_SK(1, 1) WRMG_SK(2, 1) WRMG_SK(3, 1) WRMG_SK(4, 1)
+  WRMG_SK(1, 7) WRMG_SK(2, 7) WRMG_SK(3, 7) WRMG_SK(4, 7)
+  WRMG_SK(1, 19) WRMG_SK(2, 19) WRMG_SK(3, 19)
+#undef WRMG_SK
+  return false;
+}
+
+void launch_coarse_solve_kron(const Coarse &C, const Level &L, int q, int N, const double *r, double *x,
+                              cudaStream_t s) {
+  const int nq = q + 1;
+  const int64_t NT = (int64_t)N * nq;
+  cudaMemsetAsync(x, 0, L.nnode * NT * sizeof(double), s);
+  k_ckron_fwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kV, C.kS, r, C.Z);
+  ++g_launches;
+  k_ckron_scan<<<(C.mp + 127) / 128, 128, 0, s>>>(N, C.mp, nq, C.kS, C.ksig, C.Z);
+  ++g_launches;
+  k_ckron_bwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kVT, C.Z, x);
+  ++g_launches;
+}
+
+}  // namespace wrmg

@@ -83,7 +83,7 @@ void launch_multidot(const double *const *V, int nv, const double *w, int64_t n,
     int G = std::min(kGroup, nv - v0);
     for (int g = 0; g < G; ++g) P.p[g] = V[v0 + g];
     switch (G) {
-#define C(GG) case GG: k_multidot<GG><<<nblk, 256, 0, s>>>(P, w, n, partials, nv, v0); break;
+#define C(GG) case GG: k_multidot<GG><<<nblk, 256, 0, s>>>(P, w, n, partials, nv, v0); ++g_launches; break;
       C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
 #undef C
     }
@@ -91,7 +91,7 @@ void launch_multidot(const double *const *V, int nv, const double *w, int64_t n,
 }
 
 void launch_reduce_partials(const double *partials, int nblk, int nv, double *out, cudaStream_t s) {
-  k_reduce<<<nv, 32, 0, s>>>(partials, nblk, nv, out);
+  k_reduce<<<nv, 32, 0, s>>>(partials, nblk, nv, out); ++g_launches;
 }
 
 void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
@@ -101,7 +101,7 @@ void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev,
     int G = std::min(kGroup, nv - v0);
     for (int g = 0; g < G; ++g) P.p[g] = V[v0 + g];
     switch (G) {
-#define C(GG) case GG: k_multiaxpy<GG><<<grid_for(n), 256, 0, s>>>(w, P, coef_dev + v0, n, sign); break;
+#define C(GG) case GG: k_multiaxpy<GG><<<grid_for(n), 256, 0, s>>>(w, P, coef_dev + v0, n, sign); ++g_launches; break;
       C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
 #undef C
     }
@@ -109,7 +109,7 @@ void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev,
 }
 
 void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s) {
-  k_scale<<<grid_for(n), 256, 0, s>>>(dst, src, a, n);
+  k_scale<<<grid_for(n), 256, 0, s>>>(dst, src, a, n); ++g_launches;
 }
 
 }  // namespace wrmg

@@ -1,0 +1,193 @@
+// Space-time residual (H6) with stencil classes.
+//
+//   r_n = b_n - [(C+E0) (x) M + Mt (x) kappa K] u_n + (E1 (x) M) u_{n-1}     (eq. heatfem, R1-R3)
+//   constrained rows: r = b - u                                               (R5)
+//
+// Rows of the structured lattice whose surrounding cells are identical have
+// identical CSR rows (same neighbour offsets, same values): wrmg_setup groups
+// them into stencil classes (host_plan.cu) whose (offset, M, kappa K) tables
+// travel as a kernel parameter (constant bank, broadcast), so the hot loop reads
+// no indices and no matrix values from memory.  A CTA owns an 8x8 tile of rows
+// and walks the slabs in 32-slab chunks; each chunk of u (tile + k-wide halo)
+// is staged once in shared memory with cp.async.  Warp = one row x 32 slabs,
+// lane = slab: the jump term (M u)_{n-1}[q] is lane n-1's own accumulator,
+// passed with a shuffle; lane 0 takes lane 31's value of the previous chunk.
+#include "internal.h"
+
+namespace wrmg {
+namespace {
+
+constexpr int TR = 8;  // tile rows per direction
+
+struct TMr {
+  double CE[16], Mt[16];
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+template <int NQ>
+__global__ void __launch_bounds__(256) k_residual_cls(int k, int Lx, int Ly, int N,
+                                                      const uint8_t *__restrict__ rcls,
+                                                      const double *__restrict__ u, const double *__restrict__ b,
+                                                      double *__restrict__ r, TMr tm, const StencilTab T) {
+  extern __shared__ __align__(16) double su[];
+  __shared__ double prevq[TR * TR];
+  constexpr int W = 32 * NQ;  // doubles per staged node (one chunk)
+  const int64_t NT = (int64_t)N * NQ;
+  const int ntx = (Lx + TR - 1) / TR;
+  const int tx0 = (blockIdx.x % ntx) * TR, ty0 = (blockIdx.x / ntx) * TR;
+  const int RW = TR + 2 * k;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < TR * TR) prevq[tid] = 0.0;
+  const int nchunk = (N + 31) / 32;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int n0 = ch * 32;
+    const int nv = min(32, N - n0) * NQ;  // valid doubles per node in this chunk
+    __syncthreads();                      // previous chunk fully consumed
+    // stage u: 16-byte pieces (2 doubles); NQ*32 doubles per node
+    constexpr int PIECES = W / 2;
+    for (int e = tid; e < RW * RW * PIECES; e += blockDim.x) {
+      const int node = e / PIECES, pc = e % PIECES;
+      const int I = tx0 - k + node % RW, J = ty0 - k + node / RW;
+      double *dst = su + node * W + 2 * pc;
+      const bool in = I >= 0 && I < Lx && J >= 0 && J < Ly;
+      const double *src = in ? u + ((int64_t)J * Lx + I) * NT + (int64_t)n0 * NQ + 2 * pc : nullptr;
+      if (in && 2 * pc + 1 < nv && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        cp_async16(dst, src);
+      } else if (in && 2 * pc < nv) {
+        dst[0] = src[0];
+        dst[1] = (2 * pc + 1 < nv) ? src[1] : 0.0;
+      } else {
+        dst[0] = 0.0;
+        dst[1] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int n = n0 + lane;
+    const bool valid = n < N;
+    for (int rr = wid; rr < TR * TR; rr += 8) {
+      const int I = tx0 + rr % TR, J = ty0 + rr / TR;
+      if (I >= Lx || J >= Ly) continue;
+      const int64_t i = (int64_t)J * Lx + I;
+      const int64_t base = i * NT + (int64_t)n * NQ;
+      const double *own = su + ((J - ty0 + k) * RW + (I - tx0 + k)) * W + lane * NQ;
+      const int cls = rcls[i];
+      if (cls >= T.ncls) {  // constrained row (identity)
+        if (valid)
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) r[base + a] = b[base + a] - own[a];
+        continue;
+      }
+      double am[NQ], ak[NQ];
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) am[a] = ak[a] = 0.0;
+      const int cnt = T.cnt[cls];
+#pragma unroll 4
+      for (int e = 0; e < cnt; ++e) {
+        const double *ul = own + (T.dJ[cls][e] * RW + T.dI[cls][e]) * W;
+        const double mv = T.m[cls][e], kv = T.kk[cls][e];
+        if constexpr (NQ == 2) {
+          const double2 uv = *reinterpret_cast<const double2 *>(ul);
+          am[0] = fma(mv, uv.x, am[0]);
+          am[1] = fma(mv, uv.y, am[1]);
+          ak[0] = fma(kv, uv.x, ak[0]);
+          ak[1] = fma(kv, uv.y, ak[1]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) {
+            const double x = ul[a];
+            am[a] = fma(mv, x, am[a]);
+            ak[a] = fma(kv, x, ak[a]);
+          }
+        }
+      }
+      // jump: (M u)_{n-1}[q] is lane n-1's am[q]; lane 0 uses the previous chunk
+      double jm = __shfl_up_sync(0xffffffffu, am[NQ - 1], 1);
+      if (lane == 0) jm = prevq[rr];
+      const double last = __shfl_sync(0xffffffffu, am[NQ - 1], 31);
+      if (valid) {
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) {
+          double acc = b[base + a];
+#pragma unroll
+          for (int c = 0; c < NQ; ++c) acc -= tm.CE[a * NQ + c] * am[c] + tm.Mt[a * NQ + c] * ak[c];
+          if (a == 0 && n > 0) acc += jm;
+          r[base + a] = acc;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) prevq[rr] = last;
+    }
+  }
+}
+
+// Fill the class tables from the assembled CSR of each class's representative row.
+__global__ void k_gather_classes(int ncls, const int32_t *__restrict__ rep, int Lx, const int32_t *__restrict__ rowptr,
+                                 const int32_t *__restrict__ col, const double *__restrict__ Mv,
+                                 const double *__restrict__ Kv, int maxe, int32_t *__restrict__ cnt,
+                                 int32_t *__restrict__ dI, int32_t *__restrict__ dJ, double *__restrict__ m,
+                                 double *__restrict__ kk) {
+  const int c = blockIdx.x;
+  if (c >= ncls) return;
+  const int64_t i = rep[c];
+  const int e0 = rowptr[i], ne = rowptr[i + 1] - e0;
+  if (threadIdx.x == 0) cnt[c] = ne;
+  const int I = (int)(i % Lx), J = (int)(i / Lx);
+  for (int e = threadIdx.x; e < ne && e < maxe; e += blockDim.x) {
+    const int j = col[e0 + e];
+    dI[c * maxe + e] = j % Lx - I;
+    dJ[c * maxe + e] = j / Lx - J;
+    m[c * maxe + e] = Mv[e0 + e];
+    kk[c * maxe + e] = Kv[e0 + e];
+  }
+}
+
+}  // namespace
+
+void launch_gather_classes(const Level &L, int32_t *scratch_i, double *scratch_d, cudaStream_t s) {
+  const int nc = (int)L.h_cls_rep.size();
+  k_gather_classes<<<nc, 64, 0, s>>>(nc, scratch_i, L.Lx, L.A.rowptr, L.A.col, L.A.val, L.A.val2, kStencilMaxE,
+                                     scratch_i + nc, scratch_i + 2 * nc, scratch_i + 2 * nc + nc * kStencilMaxE,
+                                     scratch_d, scratch_d + nc * kStencilMaxE);
+  ++g_launches;
+}
+
+bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const double *u, const double *b,
+                         double *r, cudaStream_t s) {
+  if (!L.stencil_ok) return false;
+  const int k = (L.Lx - 1) / L.nx;
+  const int ntx = (L.Lx + TR - 1) / TR, nty = (L.Ly + TR - 1) / TR;
+  const int RW = TR + 2 * k;
+  TMr t{};
+  for (int e = 0; e < tm.nq * tm.nq; ++e) {
+    t.CE[e] = tm.CE[e];
+    t.Mt[e] = tm.Mt[e];
+  }
+  const size_t smem = (size_t)RW * RW * 32 * (q + 1) * sizeof(double);
+  if (smem > 200 * 1024) return false;
+#define WRMG_RC(NQ)                                                                                          \
+  {                                                                                                          \
+    static bool attr = false;                                                                                \
+    if (!attr) {                                                                                             \
+      cudaFuncSetAttribute(k_residual_cls<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);     \
+      attr = true;                                                                                           \
+    }                                                                                                        \
+    k_residual_cls<NQ><<<ntx * nty, 256, smem, s>>>(k, L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil);        \
+    ++g_launches;                                                                                            \
+    return true;                                                                                             \
+  }
+  switch (q) {
+    case 0: WRMG_RC(1);
+    case 1: WRMG_RC(2);
+    case 2: WRMG_RC(3);
+    default: WRMG_RC(4);
+  }
+#undef WRMG_RC
+}
+
+}  // namespace wrmg

@@ -277,12 +277,12 @@ void launch_assemble_spatial(const Level &L, int k, const double *ref_dev, doubl
   int nloc = (k + 1) * (k + 2) / 2;
   int blocks = (int)((L.nnode + 127) / 128);
   k_assemble<<<blocks, 128, 0, s>>>(k, L.nx, L.ny, L.Lx, L.nnode, L.h * L.h, kappa, L.A.rowptr, L.A.col, L.A.val,
-                                    L.A.val2, ref_dev, nloc);
+                                    L.A.val2, ref_dev, nloc); ++g_launches;
 }
 
 void launch_patch_blocks(const Level &L, int nq, const Temporal &tm, cudaStream_t s) {
   k_patch_blocks<<<L.ntypes, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, L.pnodes, L.type_rep, L.mp, nq,
-                                          make_tm(tm), L.Dblk);
+                                          make_tm(tm), L.Dblk); ++g_launches;
 }
 
 void launch_batched_lu(double *A, int m, int batch, int32_t *piv, int32_t *info, cudaStream_t s) {
@@ -294,32 +294,32 @@ void launch_batched_lu(double *A, int m, int batch, int32_t *piv, int32_t *info,
       cudaFuncSetAttribute(k_batched_lu<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
       attr = true;
     }
-    k_batched_lu<true><<<batch, 256, bytes, s>>>(A, m, piv, info);
+    k_batched_lu<true><<<batch, 256, bytes, s>>>(A, m, piv, info); ++g_launches;
   } else {
-    k_batched_lu<false><<<batch, 256, 0, s>>>(A, m, piv, info);
+    k_batched_lu<false><<<batch, 256, 0, s>>>(A, m, piv, info); ++g_launches;
   }
 }
 
 void launch_inverse_and_G(const Level &L, const double *LU, int nq, cudaStream_t s) {
   int m = nq * L.mp;
   dim3 grid((m + 127) / 128, L.ntypes);
-  k_lu_inverse<true><<<grid, 128, 0, s>>>(LU, L.piv, m, L.Dinv);
-  k_patch_G<<<L.ntypes, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.pnodes, L.type_rep, L.mp, nq, L.Dinv, L.G);
+  k_lu_inverse<true><<<grid, 128, 0, s>>>(LU, L.piv, m, L.Dinv); ++g_launches;
+  k_patch_G<<<L.ntypes, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.pnodes, L.type_rep, L.mp, nq, L.Dinv, L.G); ++g_launches;
 }
 
 void launch_coarse_blocks(const Level &L, Coarse &C, int nq, const Temporal &tm, cudaStream_t s) {
   int64_t mm = (int64_t)C.m * C.m;
   int blocks = (int)std::min<int64_t>((mm + 255) / 256, 4096);
   k_coarse_block<<<blocks, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, C.nodes, C.mp, nq, make_tm(tm),
-                                        C.Dblk);
+                                        C.Dblk); ++g_launches;
 }
 
 void launch_coarse_inverse(Coarse &C, const double *LU, const Level &L, int nq, cudaStream_t s) {
   dim3 grid((C.m + 127) / 128, 1);
-  k_lu_inverse<false><<<grid, 128, 0, s>>>(LU, C.piv, C.m, C.DinvT);
+  k_lu_inverse<false><<<grid, 128, 0, s>>>(LU, C.piv, C.m, C.DinvT); ++g_launches;
   int64_t n = (int64_t)C.m * C.mp;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
-  k_coarse_G<<<blocks, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, C.nodes, C.mp, nq, C.DinvT, C.GT, C.Gq);
+  k_coarse_G<<<blocks, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, C.nodes, C.mp, nq, C.DinvT, C.GT, C.Gq); ++g_launches;
 }
 
 }  // namespace wrmg

@@ -230,7 +230,7 @@ void sweep_launch(const Level &L, int N, const double *r, double *u, double omeg
   }
   int blocks = (int)((L.npatch + SW_WARPS - 1) / SW_WARPS);
   k_sweep<NQ, MP><<<blocks, 32 * SW_WARPS, smem, s>>>(L.npatch, N, L.pnodes, L.ptype, L.Dinv, L.G, L.wnode, omega,
-                                                      r, u);
+                                                      r, u); ++g_launches;
 }
 
 // ------------------------------------------------------------------ transfers
@@ -370,6 +370,7 @@ void launch_residual(const Level &L, int q, int N, const Temporal &tm, const dou
     cudaMemcpyAsync(r, b, L.nnode * NT * sizeof(double), cudaMemcpyDeviceToDevice, s);
     return;
   }
+  if (launch_residual_cls(L, q, N, tm, u, b, r, s)) return;
   const int k = (L.Lx - 1) / L.nx;
   const int ntx = (L.Lx + RT - 1) / RT, nty = (L.Ly + RT - 1) / RT;
   dim3 grid(ntx * nty, (N + RCS - 1) / RCS);
@@ -384,7 +385,7 @@ void launch_residual(const Level &L, int q, int N, const Temporal &tm, const dou
       attr = true;                                                                                              \
     }                                                                                                           \
     k_residual<NQ><<<grid, 256, smem, s>>>(k, L.Lx, L.Ly, N, L.A.rowptr, L.A.col, L.A.val, L.A.val2, L.con, u, b, \
-                                           r, t);                                                               \
+                                           r, t); ++g_launches;                                                               \
   }
   switch (q) {
     case 0: WRMG_RES(1); break;
@@ -407,19 +408,19 @@ void launch_sweep(const Level &L, int q, int N, const double *r, double *u, doub
 
 void launch_restrict(const Level &C, int64_t NT, const double *rf, double *rc, cudaStream_t s) {
   int64_t n = C.R.nrow * NT;
-  k_spmv_nt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C.R.nrow, NT, C.R.rowptr, C.R.col, C.R.val, rf, rc, 0);
+  k_spmv_nt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C.R.nrow, NT, C.R.rowptr, C.R.col, C.R.val, rf, rc, 0); ++g_launches;
 }
 
 void launch_prolong_add(const Level &C, int64_t NT, const double *ec, double *uf, cudaStream_t s) {
   int64_t n = C.P.nrow * NT;
-  k_spmv_nt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C.P.nrow, NT, C.P.rowptr, C.P.col, C.P.val, ec, uf, 1);
+  k_spmv_nt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C.P.nrow, NT, C.P.rowptr, C.P.col, C.P.val, ec, uf, 1); ++g_launches;
 }
 
 void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const double *r, double *x, cudaStream_t s) {
   const int nq = q + 1;
   const int64_t NT = (int64_t)N * nq;
   cudaMemsetAsync(x, 0, L.nnode * NT * sizeof(double), s);
-  k_coarse_z<<<N, 256, C.m * sizeof(double), s>>>(C.m, C.mp, nq, NT, C.nodes, C.DinvT, r, C.Z);
+  k_coarse_z<<<N, 256, C.m * sizeof(double), s>>>(C.m, C.mp, nq, NT, C.nodes, C.DinvT, r, C.Z); ++g_launches;
   size_t gq = (size_t)C.mp * C.mp * sizeof(double);
   int in_smem = (gq + 2 * C.mp * sizeof(double)) <= 200 * 1024;
   size_t smem = 2 * C.mp * sizeof(double) + (in_smem ? gq : 0);
@@ -428,8 +429,8 @@ void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const do
     cudaFuncSetAttribute(k_coarse_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     attr = true;
   }
-  k_coarse_rec<<<1, 1024, smem, s>>>(N, C.m, C.mp, nq, C.Z, C.Gq, C.Y, in_smem);
-  k_coarse_x<<<N, 256, 0, s>>>(C.m, C.mp, nq, NT, C.nodes, C.Z, C.GT, C.Y, x);
+  k_coarse_rec<<<1, 1024, smem, s>>>(N, C.m, C.mp, nq, C.Z, C.Gq, C.Y, in_smem); ++g_launches;
+  k_coarse_x<<<N, 256, 0, s>>>(C.m, C.mp, nq, NT, C.nodes, C.Z, C.GT, C.Y, x); ++g_launches;
 }
 
 void launch_rhs(const Level &L, int q, int N, const Temporal &tm, const double *f, double *b, cudaStream_t s) {
@@ -437,16 +438,16 @@ void launch_rhs(const Level &L, int q, int N, const Temporal &tm, const double *
   unsigned blocks = (unsigned)((n + 255) / 256);
   TMc t = make_tmc(tm);
   switch (q) {
-    case 0: k_rhs<1><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); break;
-    case 1: k_rhs<2><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); break;
-    case 2: k_rhs<3><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); break;
-    default: k_rhs<4><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); break;
+    case 0: k_rhs<1><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); ++g_launches; break;
+    case 1: k_rhs<2><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); ++g_launches; break;
+    case 2: k_rhs<3><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); ++g_launches; break;
+    default: k_rhs<4><<<blocks, 256, 0, s>>>(L.nnode, N, L.A.rowptr, L.A.col, L.A.val, L.con, f, b, t); ++g_launches; break;
   }
 }
 
 void launch_fill_uniform(double *out, int64_t count, uint64_t first, uint64_t seed, cudaStream_t s) {
   if (count <= 0) return;
-  k_fill_uniform<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(out, count, first, seed);
+  k_fill_uniform<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(out, count, first, seed); ++g_launches;
 }
 
 }  // namespace wrmg

@@ -17,7 +17,16 @@ struct PlanLevel {
   int64_t npatch = 0;
   int ntypes = 0;
   std::vector<int32_t> pnodes, psize, pvert, ptype, type_rep, mu;
+  // residual stencil classes: rows with identical geometry share (offsets, values)
+  std::vector<uint8_t> rcls;         // per row: class id, kRowConstrained, kRowGeneric
+  std::vector<int32_t> cls_rep;      // representative row per class
 };
+
+constexpr uint8_t kRowConstrained = 255;
+constexpr uint8_t kRowGeneric = 254;
+
+// Type-grouped CTA work list for the Kronecker sweep: ncta x pp patch ids (-1 pad).
+void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type);
 
 void plan_level(int nx, int ny, double h, int k, PlanLevel *P);
 void plan_interpolation(const PlanLevel &C, const PlanLevel &F, int k, std::vector<int32_t> &rowptr,

@@ -78,11 +78,15 @@ def test_rhs_and_residual(n, k, q, N):
     assert_parity(_host(y), p.A @ u_np, what="apply")
 
 
+MODES = ["auto", "lu"]
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("n,k,q,N", CASES)
-def test_smoother_sweeps(n, k, q, N):
+def test_smoother_sweeps(n, k, q, N, mode):
     from oracle import patches, smoother
     p = _prob(n, k, q, N)
-    c = _ctx(n, k, q, N)
+    c = _ctx(n, k, q, N, factor_mode=mode)
     P, _ = patches.vertex_star_patches(p.mesh, k, p.constrained)
     fac = smoother.PatchFactors(p, p.A, P)
     wts = smoother.weights(P, p.nnode)
@@ -144,12 +148,13 @@ def test_transfers(n, k, q, N):
         assert_parity(_host(uf), uf0 + transfer.prolong(H.P0[l], ec, NT), what=f"prolong {l}")
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 16), (8, 3, 1, 34), (16, 2, 1, 6), (4, 2, 1, 9)])
-def test_vcycle(n, k, q, N):
+def test_vcycle(n, k, q, N, mode):
     from oracle import multigrid
     H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
     p = H.fine
-    c = _ctx(n, k, q, N)
+    c = _ctx(n, k, q, N, factor_mode=mode)
     assert c.layout["nlevels"] == len(H.levels)
     r_np = p.rhs(wi.spacetime_field(p.nnode, N, q, 4))
     z = c.empty()
@@ -157,15 +162,16 @@ def test_vcycle(n, k, q, N):
     assert_parity(_host(z), multigrid.vcycle(H, r_np), what="vcycle")
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 16), (16, 3, 1, 16), (8, 2, 1, 40)])
-def test_fgmres(n, k, q, N):
+def test_fgmres(n, k, q, N, mode):
     from oracle import krylov, multigrid
     H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
     p = H.fine
     b_np = p.rhs(wi.spacetime_field(p.nnode, N, q, 0))
     x_ref, its_ref, hist, st = krylov.fgmres(lambda v: p.A @ v, lambda r: multigrid.vcycle(H, r), b_np,
                                              restart=30, maxit=200, rtol=1e-8)
-    c = _ctx(n, k, q, N)
+    c = _ctx(n, k, q, N, factor_mode=mode)
     x = c.empty()
     its, rel, status = c.fgmres(_dev(b_np), x, restart=30, maxit=200, rtol=1e-8)
     assert status == "WRMG_OK" and st == "converged"
