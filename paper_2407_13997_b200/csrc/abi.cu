@@ -156,12 +156,12 @@ void gather_stencil(wrmg_ctx *c, Level &L) {
   std::memset(&T, 0, sizeof(T));
   T.ncls = nc;
   const int32_t *cnt = hi.data() + nc, *dI = cnt + nc, *dJ = dI + nc * kStencilMaxE;
+  const int RW = 8 + 2 * c->k;  // residual tile (kernels_residual.cu) + k-wide halo
   for (int k2 = 0; k2 < nc; ++k2) {
-    if (cnt[k2] > kStencilMaxE) return;
-    T.cnt[k2] = cnt[k2];
+    if (((cnt[k2] + 3) & ~3) > kStencilMaxE) return;
+    T.cnt[k2] = (cnt[k2] + 3) & ~3;  // zero entries pad the loop to a multiple of 4
     for (int e = 0; e < cnt[k2]; ++e) {
-      T.dI[k2][e] = (int8_t)dI[k2 * kStencilMaxE + e];
-      T.dJ[k2][e] = (int8_t)dJ[k2 * kStencilMaxE + e];
+      T.off[k2][e] = (dJ[k2 * kStencilMaxE + e] * RW + dI[k2 * kStencilMaxE + e]) * 32 * c->nq;
       T.m[k2][e] = hd[k2 * kStencilMaxE + e];
       T.kk[k2][e] = hd[nc * kStencilMaxE + k2 * kStencilMaxE + e];
     }
@@ -585,12 +585,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
 wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
   if (!c || !x || !y) return WRMG_E_INVALID;
   try {
-    // y = A x = 0 - (0 - A x): residual with b = 0 gives -A x; negate in place
-    const Level &L = c->lv.back();
-    const int64_t n = L.nnode * c->nt;
-    CK(cudaMemsetAsync(c->tmp, 0, n * sizeof(double), c->stream));
-    launch_residual(L, c->q, c->N, c->tm, x, c->tmp, y, false, c->stream);
-    launch_scale(y, y, -1.0, n, c->stream);
+    prof_residual(c, (int)c->lv.size() - 1, x, nullptr, y, false);  // b = NULL: y = A x
     check_launch();
     return WRMG_OK;
   } catch (const Err &e) {
@@ -654,7 +649,7 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, doubl
 
 wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
                         double atol, int32_t *iters, double *relres) {
-  if (!c || !b || !x || restart < 1 || maxit < 1) return WRMG_E_INVALID;
+  if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1) return WRMG_E_INVALID;
   try {
     cudaStream_t s = c->stream;
     const Level &L = c->lv.back();
@@ -706,26 +701,29 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
       int jend = 0;
       for (int j = 0; j < restart; ++j) {
         vcycle_level(c, (int)c->lv.size() - 1, c->V[j], c->Z[j]);
-        // w = A Z_j
-        CK(cudaMemsetAsync(c->w, 0, n * sizeof(double), s));
-        prof_residual(c, (int)c->lv.size() - 1, c->Z[j], c->w, c->tmp, false);
-        {
-          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 1.0 * n);
-          launch_scale(c->w, c->tmp, -1.0, n, s);
-        }
-        // CGS2
+        // w = A Z_j (residual kernel in apply mode)
+        prof_residual(c, (int)c->lv.size() - 1, c->Z[j], nullptr, c->w, false);
+        // CGS2, fused: h = V^T w;  w -= V h & h2 = V^T w;  w -= V h2 & |w|^2
         multidot(j + 1, c->w, h);
         {
-          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 1) * n);
-          launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 4.0 * (j + 1) * n);
+          const int nb = multidot_blocks(n);
+          launch_cgs_update_dot(c->V.data(), j + 1, c->w, red, n, part, nb, s);
+          launch_reduce_partials(part, nb, j + 1, red + 32, s);
         }
-        multidot(j + 1, c->w, h2);
+        h2.resize(j + 1);
+        CK(cudaMemcpyAsync(h2.data(), red + 32, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        double hn2 = 0.0;
         {
-          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 1) * n);
-          launch_multiaxpy(c->w, c->V.data(), red, j + 1, n, -1.0, s);
+          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
+          const int nb = multidot_blocks(n);
+          launch_cgs_update_norm(c->V.data(), j + 1, c->w, red + 32, n, part, nb, s);
+          launch_reduce_partials(part, nb, 1, red + 63, s);
         }
+        CK(cudaMemcpyAsync(&hn2, red + 63, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         for (int i = 0; i <= j; ++i) h[i] += h2[i];
-        const double hn = norm(c->w);
+        const double hn = std::sqrt(hn2);
         std::vector<double> col(restart + 1, 0.0);
         for (int i = 0; i <= j; ++i) col[i] = h[i];
         col[j + 1] = hn;

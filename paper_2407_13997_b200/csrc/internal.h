@@ -42,7 +42,7 @@ constexpr int kStencilMaxC = 16, kStencilMaxE = 40;
 struct StencilTab {
   int ncls;
   int cnt[kStencilMaxC];
-  int8_t dI[kStencilMaxC][kStencilMaxE], dJ[kStencilMaxC][kStencilMaxE];
+  int32_t off[kStencilMaxC][kStencilMaxE];  // (dJ * RW + dI) * 32 (q+1): shared-memory offset in doubles
   double m[kStencilMaxC][kStencilMaxE], kk[kStencilMaxC][kStencilMaxE];
 };
 
@@ -169,6 +169,10 @@ void launch_fill_uniform(double *out, int64_t count, uint64_t first, uint64_t se
 void launch_multidot(const double *const *V, int nv, const double *w, int64_t n, double *partials, int nblk,
                      cudaStream_t s);
 int multidot_blocks(int64_t n);
+void launch_cgs_update_dot(const double *const *V, int nv, double *w, const double *coef, int64_t n,
+                           double *partials, int nblk, cudaStream_t s);
+void launch_cgs_update_norm(const double *const *V, int nv, double *w, const double *coef, int64_t n,
+                            double *partials, int nblk, cudaStream_t s);
 void launch_reduce_partials(const double *partials, int nblk, int nv, double *out, cudaStream_t s);
 void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
                       cudaStream_t s);

@@ -225,7 +225,7 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
 // chunk w % C).  Lanes are slabs: gathers and scatters touch 32 (q+1)
 // contiguous doubles per patch node (waveform-major layout, R4).
 template <int NQ, int MP>
-__global__ void __launch_bounds__(256) k_sweep_kron(int N, int C, int PP, const int32_t *__restrict__ cta_patch,
+__global__ void __launch_bounds__(256, 2) k_sweep_kron(int N, int C, int PP, const int32_t *__restrict__ cta_patch,
                                                     const int32_t *__restrict__ cta_type,
                                                     const int32_t *__restrict__ pnodes,
                                                     const double *__restrict__ Vg, const double *__restrict__ VTg,
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) k_sweep_kron(int N, int C, int PP, const 
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const double o = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane >= d) v = fma(p, o, v);
+      v = fma(lane >= d ? p : 0.0, o, v);
       p *= p;
     }
     t[NQ - 1][i] = v;
@@ -320,12 +320,11 @@ __global__ void __launch_bounds__(256) k_sweep_kron(int N, int C, int PP, const 
     double Y = 0.0;
     for (int c2 = 0; c2 < c; ++c2) Y = fma(s32, Y, scar[(pp * C + c2) * MP + i]);
     double pw = 1.0, bs = sg;
-    int e = lane + 1;
+    const int e = lane + 1;
 #pragma unroll
     for (int bit = 0; bit < 6; ++bit) {
-      if (e & 1) pw *= bs;
+      pw *= ((e >> bit) & 1) ? bs : 1.0;
       bs *= bs;
-      e >>= 1;
     }
     const double y = fma(pw, Y, t[NQ - 1][i]);
     double yp = __shfl_up_sync(0xffffffffu, y, 1);
@@ -404,19 +403,39 @@ __global__ void __launch_bounds__(256) k_ckron_fwd(int mp, int nq, int64_t NT, c
   }
 }
 
-// per-mode recurrence over all slabs (one thread per mode)
+// per-mode recurrence over all slabs: one warp per mode, lanes = slabs of a
+// 32-slab chunk (shuffle scan), chunks in order with the end trace carried.
 __global__ void k_ckron_scan(int N, int mp, int nq, const double *__restrict__ S, const double *__restrict__ sig,
                              double *__restrict__ T) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= mp) return;
   const double sg = sig[i];
-  double y = 0.0;
-  for (int n = 0; n < N; ++n) {
+  double pw = 1.0, bs = sg;
+#pragma unroll
+  for (int bit = 0; bit < 6; ++bit) {
+    pw *= (((lane + 1) >> bit) & 1) ? bs : 1.0;
+    bs *= bs;
+  }
+  double carry = 0.0;
+  for (int n0 = 0; n0 < N; n0 += 32) {
+    const int n = n0 + lane;
+    const bool valid = n < N;
     double *Tn = T + (int64_t)n * nq * mp;
-    const double yn = fma(sg, y, Tn[(nq - 1) * mp + i]);
-    for (int a = 0; a < nq - 1; ++a) Tn[a * mp + i] = fma(S[((int64_t)i * nq + a) * nq + 0], y, Tn[a * mp + i]);
-    Tn[(nq - 1) * mp + i] = yn;
-    y = yn;
+    double v = valid ? Tn[(nq - 1) * mp + i] : 0.0, p = sg;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, v, d);
+      v = fma(lane >= d ? p : 0.0, o, v);
+      p *= p;
+    }
+    const double y = fma(pw, carry, v);
+    double yp = __shfl_up_sync(0xffffffffu, y, 1);
+    if (lane == 0) yp = carry;
+    if (valid) {
+      for (int a = 0; a < nq - 1; ++a) Tn[a * mp + i] = fma(S[((int64_t)i * nq + a) * nq + 0], yp, Tn[a * mp + i]);
+      Tn[(nq - 1) * mp + i] = y;
+    }
+    carry = __shfl_sync(0xffffffffu, y, 31);
   }
 }
 
@@ -479,7 +498,7 @@ void launch_coarse_solve_kron(const Coarse &C, const Level &L, int q, int N, con
   cudaMemsetAsync(x, 0, L.nnode * NT * sizeof(double), s);
   k_ckron_fwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kV, C.kS, r, C.Z);
   ++g_launches;
-  k_ckron_scan<<<(C.mp + 127) / 128, 128, 0, s>>>(N, C.mp, nq, C.kS, C.ksig, C.Z);
+  k_ckron_scan<<<(C.mp + 3) / 4, 128, 0, s>>>(N, C.mp, nq, C.kS, C.ksig, C.Z);
   ++g_launches;
   k_ckron_bwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kVT, C.Z, x);
   ++g_launches;

@@ -1,68 +1,86 @@
-// FGMRES building blocks (H13): fused multi-vector dot products (one pass over
-// w for up to 8 basis vectors), deterministic two-stage reduction, fused
-// multi-AXPY, scaling.  Fixed grid and fixed reduction order -> bitwise
-// reproducible dots.
+// FGMRES building blocks (H13), fused so that one Arnoldi step of classical
+// Gram-Schmidt applied twice (CGS2, R16) streams the basis three times instead
+// of four:
+//   pass A:  h  = V^T w
+//   pass B:  w <- w - V h,   h2 = V^T w        (one read of V and w, one write of w)
+//   pass C:  w <- w - V h2,  |w|^2
+// Every kernel uses a fixed grid and a fixed two-stage reduction order, so dot
+// products are bitwise reproducible run to run.
 #include "internal.h"
 
 namespace wrmg {
 namespace {
 
 constexpr int kDotBlocks = 148 * 4;
-constexpr int kGroup = 8;
+constexpr int kMaxV = 32;
 
 struct Ptrs {
-  const double *p[kGroup];
+  const double *p[kMaxV];
 };
 
-template <int G>
-__global__ void __launch_bounds__(256) k_multidot(Ptrs V, const double *__restrict__ w, int64_t n,
-                                                  double *__restrict__ partials, int stride, int v0) {
-  double acc[G];
+// MODE 0: part[k] = sum_i V_k[i] w[i]
+// MODE 1: w <- w - sum_k c_k V_k;  part[k] = sum_i V_k[i] w_new[i]
+// MODE 2: w <- w - sum_k c_k V_k;  part[0] = sum_i w_new[i]^2
+// MODE 3: w <- w + sgn sum_k c_k V_k  (MODEs 1, 2 subtract: sgn = -1)
+template <int NV, int MODE>
+__global__ void __launch_bounds__(256) k_krylov(Ptrs V, int nv, double *__restrict__ w, const double *__restrict__ coef,
+                                                int64_t n, double *__restrict__ partials, int stride, double sgn) {
+  double acc[NV];
+  double c[NV];
 #pragma unroll
-  for (int g = 0; g < G; ++g) acc[g] = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double wv = __ldg(w + i);
-#pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = fma(__ldg(V.p[g] + i), wv, acc[g]);
+  for (int k = 0; k < NV; ++k) {
+    acc[k] = 0.0;
+    c[k] = (MODE != 0 && k < nv) ? sgn * coef[k] : 0.0;
   }
-  __shared__ double red[8][G];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double wi = w[i];
+    if (MODE != 0) {
+      double v[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[k] = k < nv ? __ldg(V.p[k] + i) : 0.0;
+      double s = wi;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s = fma(c[k], v[k], s);
+      wi = s;
+      w[i] = wi;
+      if (MODE == 1) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = fma(v[k], wi, acc[k]);
+      } else if (MODE == 2) {
+        acc[0] = fma(wi, wi, acc[0]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (k < nv) acc[k] = fma(__ldg(V.p[k] + i), wi, acc[k]);
+    }
+  }
+  if (MODE == 3) return;
+  constexpr int NR = (MODE == 2) ? 1 : NV;
+  __shared__ double red[8][NR];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    double v = acc[g];
+  for (int k = 0; k < NR; ++k) {
+    double v = acc[k];
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[wid][g] = v;
+    if (lane == 0) red[wid][k] = v;
   }
   __syncthreads();
-  if (threadIdx.x < G) {
+  const int nout = (MODE == 2) ? 1 : nv;
+  if (threadIdx.x < nout) {
     double s = 0.0;
     for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
-    partials[(int64_t)blockIdx.x * stride + v0 + threadIdx.x] = s;
+    partials[(int64_t)blockIdx.x * stride + threadIdx.x] = s;
   }
 }
 
 __global__ void k_reduce(const double *__restrict__ partials, int nblk, int nv, double *__restrict__ out) {
-  // one warp per output value, fixed order
   const int v = blockIdx.x;
   const int lane = threadIdx.x;
   double s = 0.0;
   for (int b = lane; b < nblk; b += 32) s += partials[(int64_t)b * nv + v];
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[v] = s;
-}
-
-template <int G>
-__global__ void __launch_bounds__(256) k_multiaxpy(double *__restrict__ w, Ptrs V, const double *__restrict__ coef,
-                                                   int64_t n, double sign) {
-  double c[G];
-#pragma unroll
-  for (int g = 0; g < G; ++g) c[g] = sign * coef[g];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double acc = w[i];
-#pragma unroll
-    for (int g = 0; g < G; ++g) acc = fma(c[g], __ldg(V.p[g] + i), acc);
-    w[i] = acc;
-  }
 }
 
 __global__ void k_scale(double *__restrict__ dst, const double *__restrict__ src, double a, int64_t n) {
@@ -72,44 +90,52 @@ __global__ void k_scale(double *__restrict__ dst, const double *__restrict__ src
 
 int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
 
+template <int MODE>
+void krylov_launch(const double *const *V, int nv, double *w, const double *coef, int64_t n, double *partials,
+                   int nblk, cudaStream_t s, double sgn = -1.0) {
+  Ptrs P{};
+  for (int k = 0; k < nv; ++k) P.p[k] = V[k];
+  const int stride = (MODE == 2) ? 1 : nv;
+  if (nv <= 4) k_krylov<4, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
+  else if (nv <= 8) k_krylov<8, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
+  else if (nv <= 16) k_krylov<16, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
+  else k_krylov<32, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
+  ++g_launches;
+}
+
 }  // namespace
 
 int multidot_blocks(int64_t n) { return (int)std::min<int64_t>(kDotBlocks, (n + 255) / 256); }
 
 void launch_multidot(const double *const *V, int nv, const double *w, int64_t n, double *partials, int nblk,
                      cudaStream_t s) {
-  for (int v0 = 0; v0 < nv; v0 += kGroup) {
-    Ptrs P{};
-    int G = std::min(kGroup, nv - v0);
-    for (int g = 0; g < G; ++g) P.p[g] = V[v0 + g];
-    switch (G) {
-#define C(GG) case GG: k_multidot<GG><<<nblk, 256, 0, s>>>(P, w, n, partials, nv, v0); ++g_launches; break;
-      C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
-#undef C
-    }
-  }
+  krylov_launch<0>(V, nv, const_cast<double *>(w), nullptr, n, partials, nblk, s);
+}
+
+void launch_cgs_update_dot(const double *const *V, int nv, double *w, const double *coef, int64_t n,
+                           double *partials, int nblk, cudaStream_t s) {
+  krylov_launch<1>(V, nv, w, coef, n, partials, nblk, s);
+}
+
+void launch_cgs_update_norm(const double *const *V, int nv, double *w, const double *coef, int64_t n,
+                            double *partials, int nblk, cudaStream_t s) {
+  krylov_launch<2>(V, nv, w, coef, n, partials, nblk, s);
 }
 
 void launch_reduce_partials(const double *partials, int nblk, int nv, double *out, cudaStream_t s) {
-  k_reduce<<<nv, 32, 0, s>>>(partials, nblk, nv, out); ++g_launches;
+  k_reduce<<<nv, 32, 0, s>>>(partials, nblk, nv, out);
+  ++g_launches;
 }
 
 void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
                       cudaStream_t s) {
-  for (int v0 = 0; v0 < nv; v0 += kGroup) {
-    Ptrs P{};
-    int G = std::min(kGroup, nv - v0);
-    for (int g = 0; g < G; ++g) P.p[g] = V[v0 + g];
-    switch (G) {
-#define C(GG) case GG: k_multiaxpy<GG><<<grid_for(n), 256, 0, s>>>(w, P, coef_dev + v0, n, sign); ++g_launches; break;
-      C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
-#undef C
-    }
-  }
+  // sign +1: w += V c (solution update); sign -1: w -= V c
+  krylov_launch<3>(V, nv, w, coef_dev, n, nullptr, grid_for(n), s, sign);
 }
 
 void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s) {
-  k_scale<<<grid_for(n), 256, 0, s>>>(dst, src, a, n); ++g_launches;
+  k_scale<<<grid_for(n), 256, 0, s>>>(dst, src, a, n);
+  ++g_launches;
 }
 
 }  // namespace wrmg

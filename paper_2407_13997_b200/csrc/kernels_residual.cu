@@ -12,6 +12,12 @@
 // is staged once in shared memory with cp.async.  Warp = one row x 32 slabs,
 // lane = slab: the jump term (M u)_{n-1}[q] is lane n-1's own accumulator,
 // passed with a shuffle; lane 0 takes lane 31's value of the previous chunk.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <tuple>
+
 #include "internal.h"
 
 namespace wrmg {
@@ -33,7 +39,7 @@ template <int NQ>
 __global__ void __launch_bounds__(256) k_residual_cls(int k, int Lx, int Ly, int N,
                                                       const uint8_t *__restrict__ rcls,
                                                       const double *__restrict__ u, const double *__restrict__ b,
-                                                      double *__restrict__ r, TMr tm, const StencilTab T) {
+                                                      double *__restrict__ r, TMr tm, const StencilTab T, int apply) {
   extern __shared__ __align__(16) double su[];
   __shared__ double prevq[TR * TR];
   constexpr int W = 32 * NQ;  // doubles per staged node (one chunk)
@@ -48,22 +54,24 @@ __global__ void __launch_bounds__(256) k_residual_cls(int k, int Lx, int Ly, int
     const int n0 = ch * 32;
     const int nv = min(32, N - n0) * NQ;  // valid doubles per node in this chunk
     __syncthreads();                      // previous chunk fully consumed
-    // stage u: 16-byte pieces (2 doubles); NQ*32 doubles per node
+    // stage u: one warp per node, 16-byte pieces (2 doubles), NQ*32 doubles per node
     constexpr int PIECES = W / 2;
-    for (int e = tid; e < RW * RW * PIECES; e += blockDim.x) {
-      const int node = e / PIECES, pc = e % PIECES;
+    for (int node = wid; node < RW * RW; node += 8) {
       const int I = tx0 - k + node % RW, J = ty0 - k + node / RW;
-      double *dst = su + node * W + 2 * pc;
       const bool in = I >= 0 && I < Lx && J >= 0 && J < Ly;
-      const double *src = in ? u + ((int64_t)J * Lx + I) * NT + (int64_t)n0 * NQ + 2 * pc : nullptr;
-      if (in && 2 * pc + 1 < nv && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-        cp_async16(dst, src);
-      } else if (in && 2 * pc < nv) {
-        dst[0] = src[0];
-        dst[1] = (2 * pc + 1 < nv) ? src[1] : 0.0;
-      } else {
-        dst[0] = 0.0;
-        dst[1] = 0.0;
+      const double *srcn = u + ((int64_t)J * Lx + I) * NT + (int64_t)n0 * NQ;
+      const bool al = in && ((reinterpret_cast<uintptr_t>(srcn) & 15) == 0);
+      for (int pc = lane; pc < PIECES; pc += 32) {
+        double *dst = su + node * W + 2 * pc;
+        if (al && 2 * pc + 1 < nv) {
+          cp_async16(dst, srcn + 2 * pc);
+        } else if (in && 2 * pc < nv) {
+          dst[0] = srcn[2 * pc];
+          dst[1] = (2 * pc + 1 < nv) ? srcn[2 * pc + 1] : 0.0;
+        } else {
+          dst[0] = 0.0;
+          dst[1] = 0.0;
+        }
       }
     }
     cp_async_wait_all();
@@ -77,19 +85,23 @@ __global__ void __launch_bounds__(256) k_residual_cls(int k, int Lx, int Ly, int
       const int64_t base = i * NT + (int64_t)n * NQ;
       const double *own = su + ((J - ty0 + k) * RW + (I - tx0 + k)) * W + lane * NQ;
       const int cls = rcls[i];
+      // issue the b loads first: their DRAM latency overlaps the stencil loop
+      double bv[NQ];
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) bv[a] = (valid && !apply) ? __ldg(b + base + a) : 0.0;
       if (cls >= T.ncls) {  // constrained row (identity)
         if (valid)
 #pragma unroll
-          for (int a = 0; a < NQ; ++a) r[base + a] = b[base + a] - own[a];
+          for (int a = 0; a < NQ; ++a) r[base + a] = apply ? own[a] : bv[a] - own[a];
         continue;
       }
       double am[NQ], ak[NQ];
 #pragma unroll
       for (int a = 0; a < NQ; ++a) am[a] = ak[a] = 0.0;
       const int cnt = T.cnt[cls];
-#pragma unroll 4
+#pragma unroll 8
       for (int e = 0; e < cnt; ++e) {
-        const double *ul = own + (T.dJ[cls][e] * RW + T.dI[cls][e]) * W;
+        const double *ul = own + T.off[cls][e];
         const double mv = T.m[cls][e], kv = T.kk[cls][e];
         if constexpr (NQ == 2) {
           const double2 uv = *reinterpret_cast<const double2 *>(ul);
@@ -113,17 +125,182 @@ __global__ void __launch_bounds__(256) k_residual_cls(int k, int Lx, int Ly, int
       if (valid) {
 #pragma unroll
         for (int a = 0; a < NQ; ++a) {
-          double acc = b[base + a];
+          double acc = bv[a];
 #pragma unroll
           for (int c = 0; c < NQ; ++c) acc -= tm.CE[a * NQ + c] * am[c] + tm.Mt[a * NQ + c] * ak[c];
           if (a == 0 && n > 0) acc += jm;
-          r[base + a] = acc;
+          r[base + a] = apply ? -acc : acc;  // apply: y = A u = -(0 - A u)
         }
       }
       __syncwarp();
       if (lane == 0) prevq[rr] = last;
     }
   }
+}
+
+
+// ---- TMA variant: the (tile + halo) x 32-slab box of u is one 3D tensor-map copy
+// (dims: time values, I, J), out-of-lattice halo and slabs beyond N zero-filled by
+// the TMA unit; completion through an mbarrier transaction count.
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(256, 2) k_residual_tma(const __grid_constant__ CUtensorMap umap, int k, int Lx,
+                                                         int Ly, int N, const uint8_t *__restrict__ rcls,
+                                                         const double *__restrict__ b, double *__restrict__ r, TMr tm,
+                                                         const StencilTab T, int apply) {
+  extern __shared__ __align__(128) double su[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double prevq[TR * TR];
+  constexpr int W = 32 * NQ;
+  const int64_t NT = (int64_t)N * NQ;
+  const int ntx = (Lx + TR - 1) / TR;
+  const int tx0 = (blockIdx.x % ntx) * TR, ty0 = (blockIdx.x / ntx) * TR;
+  const int RW = TR + 2 * k;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const unsigned bytes = (unsigned)(RW * RW * W * sizeof(double));
+  if (tid < TR * TR) prevq[tid] = 0.0;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int nchunk = (N + 31) / 32;
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int n0 = ch * 32;
+    if (ch) __syncthreads();  // the previous chunk is fully consumed
+    if (tid == 0) {
+      mbar_expect_tx(&bar, bytes);
+      tma_load_3d(su, &umap, n0 * NQ, tx0 - k, ty0 - k, &bar);
+    }
+    mbar_wait(&bar, ch & 1);
+    const int n = n0 + lane;
+    const bool valid = n < N;
+    for (int rr = wid; rr < TR * TR; rr += 8) {
+      const int I = tx0 + rr % TR, J = ty0 + rr / TR;
+      if (I >= Lx || J >= Ly) continue;
+      const int64_t i = (int64_t)J * Lx + I;
+      const int64_t base = i * NT + (int64_t)n * NQ;
+      const double *own = su + ((J - ty0 + k) * RW + (I - tx0 + k)) * W + lane * NQ;
+      const int cls = __shfl_sync(0xffffffffu, (int)rcls[i], 0);
+      double bv[NQ];
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) bv[a] = (valid && !apply) ? __ldg(b + base + a) : 0.0;
+      if (cls >= T.ncls) {  // constrained row (identity)
+        if (valid)
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) r[base + a] = apply ? own[a] : bv[a] - own[a];
+        continue;
+      }
+      double am[NQ], ak[NQ];
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) am[a] = ak[a] = 0.0;
+      const int cnt = T.cnt[cls];  // padded to a multiple of 4 with zero entries
+      for (int e0 = 0; e0 < cnt; e0 += 4) {
+#pragma unroll
+        for (int e = e0; e < e0 + 4; ++e) {
+          const double *ul = own + T.off[cls][e];
+          const double mv = T.m[cls][e], kv = T.kk[cls][e];
+          if constexpr (NQ == 2) {
+            const double2 uv = *reinterpret_cast<const double2 *>(ul);
+            am[0] = fma(mv, uv.x, am[0]);
+            am[1] = fma(mv, uv.y, am[1]);
+            ak[0] = fma(kv, uv.x, ak[0]);
+            ak[1] = fma(kv, uv.y, ak[1]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < NQ; ++a) {
+              const double x = ul[a];
+              am[a] = fma(mv, x, am[a]);
+              ak[a] = fma(kv, x, ak[a]);
+            }
+          }
+        }
+      }
+      double jm = __shfl_up_sync(0xffffffffu, am[NQ - 1], 1);
+      if (lane == 0) jm = prevq[rr];
+      const double last = __shfl_sync(0xffffffffu, am[NQ - 1], 31);
+      if (valid) {
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) {
+          double acc = bv[a];
+#pragma unroll
+          for (int c = 0; c < NQ; ++c) acc -= tm.CE[a * NQ + c] * am[c] + tm.Mt[a * NQ + c] * ak[c];
+          if (a == 0 && n > 0) acc += jm;
+          r[base + a] = apply ? -acc : acc;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) prevq[rr] = last;
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// Tensor map of a waveform-major vector: dims (NT, Lx, Ly), box (32 NQ, RW, RW).
+bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUtensorMap *out) {
+  static std::map<std::tuple<const double *, int64_t, int, int, int, int>, CUtensorMap> cache;
+  auto key = std::make_tuple(u, NT, Lx, Ly, boxT, RW);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  auto enc = get_encode();
+  if (!enc || (NT * 8) % 16 || (reinterpret_cast<uintptr_t>(u) & 15)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)NT, (cuuint64_t)Lx, (cuuint64_t)Ly};
+  cuuint64_t strides[2] = {(cuuint64_t)NT * 8, (cuuint64_t)NT * 8 * Lx};
+  cuuint32_t box[3] = {(cuuint32_t)boxT, (cuuint32_t)RW, (cuuint32_t)RW};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult rc = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(u), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return true;
 }
 
 // Fill the class tables from the assembled CSR of each class's representative row.
@@ -159,6 +336,7 @@ void launch_gather_classes(const Level &L, int32_t *scratch_i, double *scratch_d
 
 bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const double *u, const double *b,
                          double *r, cudaStream_t s) {
+  const int apply = b == nullptr;
   if (!L.stencil_ok) return false;
   const int k = (L.Lx - 1) / L.nx;
   const int ntx = (L.Lx + TR - 1) / TR, nty = (L.Ly + TR - 1) / TR;
@@ -170,6 +348,28 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
   }
   const size_t smem = (size_t)RW * RW * 32 * (q + 1) * sizeof(double);
   if (smem > 200 * 1024) return false;
+  CUtensorMap umap;
+  if (RW <= 256 && 32 * (q + 1) <= 256 && umap_for(u, (int64_t)N * (q + 1), L.Lx, L.Ly, 32 * (q + 1), RW, &umap)) {
+#define WRMG_RT(NQ)                                                                                          \
+    {                                                                                                        \
+      static bool attr = false;                                                                              \
+      if (!attr) {                                                                                           \
+        cudaFuncSetAttribute(k_residual_tma<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);   \
+        attr = true;                                                                                         \
+      }                                                                                                      \
+      k_residual_tma<NQ><<<ntx * nty, 256, smem, s>>>(umap, k, L.Lx, L.Ly, N, L.rcls, b, r, t, L.stencil,    \
+                                                      apply);                                                \
+      ++g_launches;                                                                                          \
+      return true;                                                                                           \
+    }
+    switch (q) {
+      case 0: WRMG_RT(1);
+      case 1: WRMG_RT(2);
+      case 2: WRMG_RT(3);
+      default: WRMG_RT(4);
+    }
+#undef WRMG_RT
+  }
 #define WRMG_RC(NQ)                                                                                          \
   {                                                                                                          \
     static bool attr = false;                                                                                \
@@ -177,7 +377,7 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
       cudaFuncSetAttribute(k_residual_cls<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);     \
       attr = true;                                                                                           \
     }                                                                                                        \
-    k_residual_cls<NQ><<<ntx * nty, 256, smem, s>>>(k, L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil);        \
+    k_residual_cls<NQ><<<ntx * nty, 256, smem, s>>>(k, L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply);        \
     ++g_launches;                                                                                            \
     return true;                                                                                             \
   }

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_residual(int k, int Lx, int Ly, int N, 
     if (con[i]) {
       const double *ul = su + ((J - ty0 + k) * RW + (I - tx0 + k)) * W + 1 + s * NQ;
 #pragma unroll
-      for (int a = 0; a < NQ; ++a) r[base + a] = b[base + a] - ul[a];
+      for (int a = 0; a < NQ; ++a) r[base + a] = b ? b[base + a] - ul[a] : ul[a];
       continue;
     }
     double am[NQ], ak[NQ], ap = 0.0;
@@ -95,11 +95,11 @@ __global__ void __launch_bounds__(256) k_residual(int k, int Lx, int Ly, int N, 
     }
 #pragma unroll
     for (int a = 0; a < NQ; ++a) {
-      double acc = b[base + a];
+      double acc = b ? b[base + a] : 0.0;
 #pragma unroll
       for (int c = 0; c < NQ; ++c) acc -= tm.CE[a * NQ + c] * am[c] + tm.Mt[a * NQ + c] * ak[c];
       if (a == 0 && n > 0) acc += ap;  // (E1 (x) M) u_{n-1}: E1 = e_0 e_q^T (R2)
-      r[base + a] = acc;
+      r[base + a] = b ? acc : -acc;    // b == NULL: y = A u
     }
   }
 }
@@ -235,9 +235,37 @@ void sweep_launch(const Level &L, int N, const double *r, double *u, double omeg
 
 // ------------------------------------------------------------------ transfers
 // H10: u_f += (P_h (x) I) e_c;  H9: r_c = (P_h^T (x) I) r_f.
-__global__ void k_spmv_nt(int64_t nrow, int64_t NT, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                          const double *__restrict__ v, const double *__restrict__ x, double *__restrict__ y,
-                          int accumulate) {
+template <bool ACC>
+__global__ void __launch_bounds__(256) k_spmv_nt(int64_t nrow, int64_t NT2, const int32_t *__restrict__ rp,
+                                                 const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                                 const double2 *__restrict__ x, double2 *__restrict__ y) {
+  // thread = (row, pair of consecutive time values); NT even (checked by the launcher)
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= nrow * NT2) return;
+  const int64_t i = idx / NT2, t = idx - i * NT2;
+  const int e0 = rp[i], e1 = rp[i + 1];
+  if (ACC && e0 == e1) return;
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+  for (int e = e0; e < e1; ++e) {
+    const double a = __ldg(v + e);
+    const double2 xv = __ldg(x + (int64_t)__ldg(ci + e) * NT2 + t);
+    acc.x = fma(a, xv.x, acc.x);
+    acc.y = fma(a, xv.y, acc.y);
+  }
+  if (ACC) {
+    double2 o = y[idx];
+    o.x += acc.x;
+    o.y += acc.y;
+    y[idx] = o;
+  } else {
+    y[idx] = acc;
+  }
+}
+
+__global__ void k_spmv_nt1(int64_t nrow, int64_t NT, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                           const double *__restrict__ v, const double *__restrict__ x, double *__restrict__ y,
+                           int accumulate) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= nrow * NT) return;
   int64_t i = idx / NT, t = idx - i * NT;
@@ -248,6 +276,22 @@ __global__ void k_spmv_nt(int64_t nrow, int64_t NT, const int32_t *__restrict__ 
   } else {
     y[idx] = acc;
   }
+}
+
+void spmv_nt(const DevCSR &A, int64_t NT, const double *x, double *y, bool acc, cudaStream_t s) {
+  if (NT % 2 == 0) {
+    const int64_t n = A.nrow * (NT / 2);
+    if (acc)
+      k_spmv_nt<true><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val,
+                                                                  (const double2 *)x, (double2 *)y);
+    else
+      k_spmv_nt<false><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val,
+                                                                   (const double2 *)x, (double2 *)y);
+  } else {
+    const int64_t n = A.nrow * NT;
+    k_spmv_nt1<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A.nrow, NT, A.rowptr, A.col, A.val, x, y, acc);
+  }
+  ++g_launches;
 }
 
 // ------------------------------------------------------------- coarse solve
@@ -367,7 +411,8 @@ void launch_residual(const Level &L, int q, int N, const Temporal &tm, const dou
                      bool u_is_zero, cudaStream_t s) {
   const int64_t NT = (int64_t)N * (q + 1);
   if (u_is_zero) {
-    cudaMemcpyAsync(r, b, L.nnode * NT * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (b) cudaMemcpyAsync(r, b, L.nnode * NT * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    else cudaMemsetAsync(r, 0, L.nnode * NT * sizeof(double), s);
     return;
   }
   if (launch_residual_cls(L, q, N, tm, u, b, r, s)) return;
@@ -407,13 +452,11 @@ void launch_sweep(const Level &L, int q, int N, const double *r, double *u, doub
 }
 
 void launch_restrict(const Level &C, int64_t NT, const double *rf, double *rc, cudaStream_t s) {
-  int64_t n = C.R.nrow * NT;
-  k_spmv_nt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C.R.nrow, NT, C.R.rowptr, C.R.col, C.R.val, rf, rc, 0); ++g_launches;
+  spmv_nt(C.R, NT, rf, rc, false, s);
 }
 
 void launch_prolong_add(const Level &C, int64_t NT, const double *ec, double *uf, cudaStream_t s) {
-  int64_t n = C.P.nrow * NT;
-  k_spmv_nt<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(C.P.nrow, NT, C.P.rowptr, C.P.col, C.P.val, ec, uf, 1); ++g_launches;
+  spmv_nt(C.P, NT, ec, uf, true, s);
 }
 
 void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const double *r, double *x, cudaStream_t s) {
