@@ -118,7 +118,8 @@ void free_level(Level &L) {
                   (void *)L.Dinv, (void *)L.G, (void *)L.piv, (void *)L.info, (void *)L.P.rowptr, (void *)L.P.col,
                   (void *)L.P.val, (void *)L.R.rowptr, (void *)L.R.col, (void *)L.R.val, (void *)L.vr, (void *)L.vz,
                   (void *)L.vt, (void *)L.kV, (void *)L.kVT, (void *)L.kS, (void *)L.ksig, (void *)L.cta_patch,
-                  (void *)L.cta_type, (void *)L.rcls})
+                  (void *)L.cta_type, (void *)L.rcls, (void *)L.cta_patch1, (void *)L.cta_type1,
+                  (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8})
     dfree(p);
 }
 
@@ -166,6 +167,13 @@ void gather_stencil(wrmg_ctx *c, Level &L) {
       T.kk[k2][e] = hd[nc * kStencilMaxE + k2 * kStencilMaxE + e];
     }
   }
+  std::vector<int64_t> go((size_t)kStencilMaxC * kStencilMaxE, 0);
+  for (int k2 = 0; k2 < nc; ++k2)
+    for (int e = 0; e < cnt[k2]; ++e)
+      go[k2 * kStencilMaxE + e] =
+          ((int64_t)dJ[k2 * kStencilMaxE + e] * L.Lx + dI[k2 * kStencilMaxE + e]) * c->nt;
+  if (!L.goff) L.goff = dalloc<int64_t>(go.size());
+  CK(cudaMemcpy(L.goff, go.data(), go.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   L.stencil_ok = true;
 }
 
@@ -457,6 +465,14 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         L.kron_ncta = (int)ct.size();
         L.cta_patch = dupload(cp, s);
         L.cta_type = dupload(ct, s);
+        plan_sweep_ctas(P, 1, cp, ct);
+        L.kron_ncta1 = (int)ct.size();
+        L.cta_patch1 = dupload(cp, s);
+        L.cta_type1 = dupload(ct, s);
+        plan_sweep_ctas(P, 8, cp, ct);
+        L.kron_ngrp8 = (int)ct.size();
+        L.grp_patch8 = dupload(cp, s);
+        L.grp_type8 = dupload(ct, s);
       }
       if (l < nl - 1) {
         L.vr = dalloc<double>(L.nnode * c->nt);

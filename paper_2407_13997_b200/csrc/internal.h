@@ -42,7 +42,7 @@ constexpr int kStencilMaxC = 16, kStencilMaxE = 40;
 struct StencilTab {
   int ncls;
   int cnt[kStencilMaxC];
-  int32_t off[kStencilMaxC][kStencilMaxE];  // (dJ * RW + dI) * 32 (q+1): shared-memory offset in doubles
+  int32_t off[kStencilMaxC][kStencilMaxE];   // (dJ * RW + dI) * 32 (q+1): smem offset (8x8 tiles, 32 slabs)
   double m[kStencilMaxC][kStencilMaxE], kk[kStencilMaxC][kStencilMaxE];
 };
 
@@ -78,11 +78,16 @@ struct Level {
   double *kV = nullptr, *kVT = nullptr, *kS = nullptr, *ksig = nullptr;
   int32_t *cta_patch = nullptr, *cta_type = nullptr;
   int kron_pp = 1, kron_ncta = 0;
+  int32_t *cta_patch1 = nullptr, *cta_type1 = nullptr;  // one patch per CTA (DMMA sweep)
+  int kron_ncta1 = 0;
+  int32_t *grp_patch8 = nullptr, *grp_type8 = nullptr;  // class-pure groups of 8 patches (DMMA sweep)
+  int kron_ngrp8 = 0;
   // residual stencil classes
   uint8_t *rcls = nullptr;
   std::vector<int32_t> h_cls_rep;
   bool stencil_ok = false;
   StencilTab stencil{};
+  int64_t *goff = nullptr;  // [kStencilMaxC][kStencilMaxE] global element offsets (dJ Lx + dI) NT
   // transfer from this level to the next finer (stored on the coarse side)
   DevCSR P;    // rows: fine nodes, cols: coarse nodes
   DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)

@@ -360,6 +360,232 @@ __global__ void __launch_bounds__(256, 2) k_sweep_kron(int N, int C, int PP, con
   }
 }
 
+
+// ------------------------------------------------------------ sweep (DMMA)
+// The two dense transforms of the Kronecker sweep, ghat = (I (x) V^T) g and
+// x = (I (x) V) w, are small GEMMs per (patch, 16-slab chunk):
+//     [modes x (slab, a)] = V^T [modes x nodes] * G [nodes x (slab, a)],
+// issued on the FP64 tensor cores (mma.sync.m8n8k4.f64; tcgen05 has no FP64
+// kind): one warp instruction = 256 FMAs instead of 32, which frees the issue
+// slots the DFMA version spends on shared-memory operand traffic.  Fragment
+// layout (verified by tools/dmma_layout.cu): a = A[l>>2][l&3], b = B[l&3][l>>2],
+// c[e] = C[l>>2][2(l&3)+e].  In the C layout a lane holds one mode and one slab
+// with both DG1 time values, so the per-mode 2x2 solve is lane-local and the end
+// trace scan runs over the 4 lanes of a quad and the 4 column tiles.  DG1 only.
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+
+// Warp = one patch, walking its slabs in 16-slab chunks with the end-trace
+// carry of every mode in registers (no inter-warp dependency, no barrier per
+// patch); CTA = 8 patches of one translation class sharing the class factors in
+// shared memory; persistent CTAs take patch groups in a strided order so the
+// active window stays spatially compact (L2 reuse of shared patch nodes).  The
+// gather of chunk c+1 (cp.async, zero-filled outside the lattice / horizon) is
+// in flight while chunk c is transformed, solved and scattered.
+template <int MP>
+__global__ void __launch_bounds__(256, 2) k_sweep_kron_mma(int N, int ld, int ngroups,
+                                                        const int32_t *__restrict__ grp_patch,
+                                                        const int32_t *__restrict__ grp_type,
+                                                        const int32_t *__restrict__ pnodes,
+                                                        const double *__restrict__ Vg, const double *__restrict__ Sg,
+                                                        const double *__restrict__ sigg,
+                                                        const double *__restrict__ wnode, double omega,
+                                                        const double *__restrict__ r, double *__restrict__ u) {
+  constexpr int NQ = 2;
+  constexpr int MT = (MP + 7) / 8;  // mode / node tiles of 8
+  constexpr int KF = (MP + 3) / 4;  // k-steps of 4 over nodes (fwd) and modes (bwd)
+  constexpr int P8 = 8 * MT;        // padded modes / nodes
+  constexpr int K4 = 4 * KF;        // rows of the gathered tile (nodes) and of W (modes)
+  constexpr int LDV = P8 + 1;
+  constexpr int LDG = 34;           // 32 (slab, a) columns + pad, 16-byte aligned rows
+  constexpr int WPC = 8;            // warps (patches) per CTA
+  extern __shared__ __align__(16) double sm[];
+  double *sV = sm;                     // P8 x LDV: V[node][mode], zero padded
+  double *sS = sV + P8 * LDV;          // P8 x 4: S_i (2x2)
+  double *ssig = sS + P8 * 4;          // P8 x 4: sigma, sigma^2, sigma^4, (unused)
+  double *sG = ssig + 4 * P8;          // WPC x 2 x K4 x LDG: gathered g, then W
+  const int tid = threadIdx.x, l = tid & 31, w = tid >> 5;
+  const int q4 = l & 3, g8 = l >> 2, qb = l & ~3;
+  const int64_t NT = (int64_t)N * NQ;
+  const int nch = (N + 15) / 16;
+  double *Gw = sG + w * 2 * K4 * LDG;
+  auto gather = [&](int p, int ch, double *G) {
+    const int n0 = 16 * ch;
+#pragma unroll
+    for (int t = 0; t < K4 / 2; ++t) {  // K4 rows x 16 pieces of 16 bytes
+      const int e = l + 32 * t, row = e >> 4, pc = e & 15;
+      const int nd = row < MP ? __ldg(pnodes + (size_t)p * MP + row) : -1;
+      const bool ok = nd >= 0 && n0 + pc < N;
+      const double *src = ok ? r + (int64_t)nd * NT + (int64_t)(n0 + pc) * NQ : r;
+      cp_async16_zfill(G + row * LDG + 2 * pc, src, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int cur_ty = -1;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int ty = grp_type[grp];
+    if (ty != cur_ty) {  // uniform across the CTA
+      __syncthreads();
+      for (int e = tid; e < P8 * P8; e += blockDim.x) {
+        const int j = e / P8, i = e - j * P8;
+        sV[j * LDV + i] = (j < MP && i < MP) ? Vg[((size_t)ty * MP + j) * ld + i] : 0.0;
+      }
+      for (int e = tid; e < P8 * 4; e += blockDim.x)
+        sS[e] = (e >> 2) < MP ? Sg[((size_t)ty * MP + (e >> 2)) * 4 + (e & 3)] : 0.0;
+      for (int i = tid; i < P8; i += blockDim.x) {
+        const double sg = i < MP ? sigg[(size_t)ty * MP + i] : 0.0, sg2 = sg * sg;
+        ssig[4 * i] = sg;
+        ssig[4 * i + 1] = sg2;
+        ssig[4 * i + 2] = sg2 * sg2;
+        ssig[4 * i + 3] = 0.0;
+      }
+      cur_ty = ty;
+      __syncthreads();
+    }
+    const int p = grp_patch[grp * WPC + w];
+    if (p < 0) continue;
+    // scatter targets of this lane: node 8mt + g8
+    int snd[MT];
+    double swj[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int j = 8 * mt + g8;
+      snd[mt] = j < MP ? __ldg(pnodes + (size_t)p * MP + j) : -1;
+      swj[mt] = snd[mt] >= 0 ? omega * __ldg(wnode + snd[mt]) : 0.0;
+    }
+    double Ycar[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) Ycar[mt] = 0.0;
+    gather(p, 0, Gw);
+    for (int ch = 0; ch < nch; ++ch) {
+      double *G = Gw + (ch & 1) * K4 * LDG;
+      if (ch + 1 < nch) {
+        gather(p, ch + 1, Gw + ((ch + 1) & 1) * K4 * LDG);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncwarp();
+      // 1. forward transform on the tensor cores: acc[mt][nt] = (V^T G)[8mt + g8][8nt + 2 q4 + e]
+      double acc[MT][4][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KF; ++kk) {
+        double bf[4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bf[nt] = G[(4 * kk + q4) * LDG + 8 * nt + g8];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double a = sV[(4 * kk + q4) * LDV + 8 * mt + g8];
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a, bf[nt]);
+        }
+      }
+      // 2. per mode: t = S_i ghat; end-trace scan over the quad's 4 slabs and the 4 column tiles,
+      //    carried in from the previous chunk; w = (t0 + S_i[0][0] y_{n-1}, y_n)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int i = 8 * mt + g8;
+        const double s00 = sS[i * 4 + 0], s01 = sS[i * 4 + 1], s10 = sS[i * 4 + 2], s11 = sS[i * 4 + 3];
+        const double sg = ssig[4 * i], sg2 = ssig[4 * i + 1], sg4 = ssig[4 * i + 2];
+        const double pw = q4 == 0 ? sg : q4 == 1 ? sg2 : q4 == 2 ? sg2 * sg : sg4;  // sg^(q4+1)
+        double Y = Ycar[mt];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const double g0 = acc[mt][nt][0], g1 = acc[mt][nt][1];
+          const double t0 = fma(s00, g0, s01 * g1);
+          double v = fma(s10, g0, s11 * g1);
+          double o = __shfl_up_sync(0xffffffffu, v, 1);
+          v = fma(q4 >= 1 ? sg : 0.0, o, v);
+          o = __shfl_up_sync(0xffffffffu, v, 2);
+          v = fma(q4 >= 2 ? sg2 : 0.0, o, v);
+          const double y = fma(pw, Y, v);
+          double yp = __shfl_up_sync(0xffffffffu, y, 1);
+          if (q4 == 0) yp = Y;
+          acc[mt][nt][0] = fma(s00, yp, t0);
+          acc[mt][nt][1] = y;
+          Y = __shfl_sync(0xffffffffu, y, qb | 3);
+        }
+        Ycar[mt] = Y;
+      }
+      // 3. W (modes < K4) -> this chunk's gather buffer, then the backward transform
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int i = 8 * mt + g8;
+        if (i < K4)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+            *reinterpret_cast<double2 *>(G + i * LDG + 8 * nt + 2 * q4) =
+                make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KF; ++kk) {
+        double bw[4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bw[nt] = G[(4 * kk + q4) * LDG + 8 * nt + g8];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double a = sV[(8 * mt + g8) * LDV + 4 * kk + q4];
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a, bw[nt]);
+        }
+      }
+      __syncwarp();  // W reads done before the buffer is refilled two chunks later
+      // 4. weighted additive scatter: lane holds node 8mt + g8, slab 16ch + 4nt + q4, both a
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int nd = snd[mt];
+        if (nd < 0) continue;
+        const double wj = swj[mt];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int n = 16 * ch + 4 * nt + q4;
+          if (n < N) {
+            double *dst = u + (int64_t)nd * NT + (int64_t)n * NQ;
+            atomicAdd(dst, wj * acc[mt][nt][0]);
+            atomicAdd(dst + 1, wj * acc[mt][nt][1]);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int MP>
+void sweep_kron_mma_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
+  constexpr int P8 = 8 * ((MP + 7) / 8);
+  constexpr int K4 = 4 * ((MP + 3) / 4);
+  const size_t smem = (size_t)(P8 * (P8 + 1) + P8 * 4 + 4 * P8 + 8 * 2 * K4 * 34) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_kron_mma<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  const int ngroups = L.kron_ngrp8;
+  const int grid = std::min(ngroups, 148 * 2);
+  k_sweep_kron_mma<MP><<<grid, 256, smem, s>>>(N, (L.mp + 1) & ~1, ngroups, L.grp_patch8, L.grp_type8, L.pnodes,
+                                               L.kV, L.kS, L.ksig, L.wnode, omega, r, u);
+  ++g_launches;
+}
+
 template <int NQ, int MP>
 void sweep_kron_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
   const int C = (N + 31) / 32;
@@ -482,6 +708,11 @@ void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal 
 
 bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s) {
   const int nq = q + 1;
+  if (nq == 2 && L.kron_ngrp8 > 0 && L.npatch >= 1000) {  // small levels: chunk-parallel kernel below
+    if (L.mp == 19) { sweep_kron_mma_launch<19>(L, N, r, u, omega, s); return true; }
+    if (L.mp == 7) { sweep_kron_mma_launch<7>(L, N, r, u, omega, s); return true; }
+    if (L.mp == 1) { sweep_kron_mma_launch<1>(L, N, r, u, omega, s); return true; }
+  }
 #define WRMG_SK(NQ, MP) \
   if (nq == NQ && L.mp == MP) { sweep_kron_launch<NQ, MP>(L, N, r, u, omega, s); return true; }
   WRMG_SK(1, 1) WRMG_SK(2, 1) WRMG_SK(3, 1) WRMG_SK(4, 1)

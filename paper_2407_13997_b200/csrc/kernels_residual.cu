@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(256, 2) k_residual_tma(const __grid_constant__
     const int n0 = ch * 32;
     if (ch) __syncthreads();  // the previous chunk is fully consumed
     if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       mbar_expect_tx(&bar, bytes);
       tma_load_3d(su, &umap, n0 * NQ, tx0 - k, ty0 - k, &bar);
     }
@@ -263,6 +264,83 @@ __global__ void __launch_bounds__(256, 2) k_residual_tma(const __grid_constant__
   }
 }
 
+
+// ---- L1 variant: no staging.  Warp = one row x 32 slabs (lane = slab); the
+// neighbour time histories are read straight from global memory (LDG.128,
+// L1-allocating).  A CTA walks an 8x8 tile of rows so the tile's neighbourhood
+// stays L1-resident; with no shared memory and ~40 registers an SM holds 64
+// warps, each with up to `cnt` independent loads in flight.
+template <int NQ>
+__global__ void __launch_bounds__(256) k_residual_l1(int Lx, int Ly, int N, const uint8_t *__restrict__ rcls,
+                                                     const double *__restrict__ u, const double *__restrict__ b,
+                                                     double *__restrict__ r, TMr tm, const StencilTab T, int apply,
+                                                     const int64_t *__restrict__ goff) {
+  const int64_t NT = (int64_t)N * NQ;
+  const int ntx = (Lx + TR - 1) / TR;
+  const int tx0 = (blockIdx.x % ntx) * TR, ty0 = (blockIdx.x / ntx) * TR;
+  const int n0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int n = n0 + lane;
+  const bool valid = n < N;
+  const int ns = valid ? n : N - 1;  // clamp loads of idle lanes
+  for (int rr = wid; rr < TR * TR; rr += 8) {
+    const int I = tx0 + rr % TR, J = ty0 + rr / TR;
+    if (I >= Lx || J >= Ly) continue;
+    const int64_t i = (int64_t)J * Lx + I;
+    const int64_t base = i * NT + (int64_t)ns * NQ;
+    const int cls = __ldg(rcls + i);
+    double bv[NQ];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) bv[a] = apply ? 0.0 : __ldg(b + base + a);
+    if (cls >= T.ncls) {
+      if (valid)
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) r[base + a] = apply ? __ldg(u + base + a) : bv[a] - __ldg(u + base + a);
+      continue;
+    }
+    double am[NQ], ak[NQ], ap = 0.0;
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) am[a] = ak[a] = 0.0;
+    const double *ub = u + base;
+    const int cnt = T.cnt[cls];
+    const int64_t *go = goff + cls * kStencilMaxE;
+    for (int e0 = 0; e0 < cnt; e0 += 4) {
+#pragma unroll
+      for (int e = e0; e < e0 + 4; ++e) {
+        const double *ul = ub + __ldg(go + e);
+        const double mv = T.m[cls][e], kv = T.kk[cls][e];
+        if constexpr (NQ == 2) {
+          const double2 uv = __ldg(reinterpret_cast<const double2 *>(ul));
+          am[0] = fma(mv, uv.x, am[0]);
+          am[1] = fma(mv, uv.y, am[1]);
+          ak[0] = fma(kv, uv.x, ak[0]);
+          ak[1] = fma(kv, uv.y, ak[1]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) {
+            const double x = __ldg(ul + a);
+            am[a] = fma(mv, x, am[a]);
+            ak[a] = fma(kv, x, ak[a]);
+          }
+        }
+        if (lane == 0 && n > 0) ap = fma(mv, __ldg(ul - 1), ap);  // (M u)_{n0-1}[q] for the chunk's first slab
+      }
+    }
+    double jm = __shfl_up_sync(0xffffffffu, am[NQ - 1], 1);
+    if (lane == 0) jm = ap;
+    if (valid) {
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) {
+        double acc = bv[a];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) acc -= tm.CE[a * NQ + c] * am[c] + tm.Mt[a * NQ + c] * ak[c];
+        if (a == 0 && n > 0) acc += jm;
+        r[base + a] = apply ? -acc : acc;
+      }
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -278,9 +356,10 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // Tensor map of a waveform-major vector: dims (NT, Lx, Ly), box (32 NQ, RW, RW).
-bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUtensorMap *out) {
-  static std::map<std::tuple<const double *, int64_t, int, int, int, int>, CUtensorMap> cache;
-  auto key = std::make_tuple(u, NT, Lx, Ly, boxT, RW);
+bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUtensorMap *out, int RWy = -1) {
+  if (RWy < 0) RWy = RW;
+  static std::map<std::tuple<const double *, int64_t, int, int, int, int, int>, CUtensorMap> cache;
+  auto key = std::make_tuple(u, NT, Lx, Ly, boxT, RW, RWy);
   auto it = cache.find(key);
   if (it != cache.end()) {
     *out = it->second;
@@ -290,7 +369,7 @@ bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUt
   if (!enc || (NT * 8) % 16 || (reinterpret_cast<uintptr_t>(u) & 15)) return false;
   cuuint64_t dims[3] = {(cuuint64_t)NT, (cuuint64_t)Lx, (cuuint64_t)Ly};
   cuuint64_t strides[2] = {(cuuint64_t)NT * 8, (cuuint64_t)NT * 8 * Lx};
-  cuuint32_t box[3] = {(cuuint32_t)boxT, (cuuint32_t)RW, (cuuint32_t)RW};
+  cuuint32_t box[3] = {(cuuint32_t)boxT, (cuuint32_t)RW, (cuuint32_t)RWy};
   cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap m;
   CUresult rc = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(u), dims, strides, box, es,
@@ -338,6 +417,23 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
                          double *r, cudaStream_t s) {
   const int apply = b == nullptr;
   if (!L.stencil_ok) return false;
+  if (L.goff && L.nnode < 50000) {  // small levels: no staging latency; large levels: TMA tiles below
+    TMr t{};
+    for (int e = 0; e < tm.nq * tm.nq; ++e) {
+      t.CE[e] = tm.CE[e];
+      t.Mt[e] = tm.Mt[e];
+    }
+    const int ntx = (L.Lx + TR - 1) / TR, nty = (L.Ly + TR - 1) / TR;
+    dim3 grid(ntx * nty, (N + 31) / 32);
+    switch (q) {
+      case 0: k_residual_l1<1><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
+      case 1: k_residual_l1<2><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
+      case 2: k_residual_l1<3><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
+      default: k_residual_l1<4><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
+    }
+    ++g_launches;
+    return true;
+  }
   const int k = (L.Lx - 1) / L.nx;
   const int ntx = (L.Lx + TR - 1) / TR, nty = (L.Ly + TR - 1) / TR;
   const int RW = TR + 2 * k;
