@@ -102,6 +102,17 @@ class HeatProblem:
             out[r_i] = b[row] - (np.ravel(mu) @ Tm[t] + self.kappa * (np.ravel(ku) @ Tk[t]))
         return out
 
+    def residual_node(self, i, u, b):
+        """All N (q+1) values of b - A u at spatial node i (Kronecker definition,
+        without forming A; for full-size sampled parity)."""
+        u2 = np.asarray(u, dtype=float).reshape(self.nnode, self.NT)
+        bi = np.asarray(b, dtype=float).reshape(self.nnode, self.NT)[i]
+        if self.constrained[i]:
+            return bi - u2[i]
+        mu = np.ravel(self.M.getrow(i) @ u2)
+        ku = np.ravel(self.K.getrow(i) @ u2)
+        return bi - (self.Tm @ mu + self.kappa * (self.Tk @ ku))
+
     def slab_indices(self, nodes, n):
         """Space-time indices of spatial nodes `nodes` in slab n, ordered
         (node-major, temporal node fastest)."""

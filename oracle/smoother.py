@@ -64,6 +64,35 @@ class PatchFactors:
         return x
 
 
+def patch_blocks_kron(prob, patch):
+    """D_{p,n} and L_{p,n} (same for every slab of the heat operator) from the
+    Kronecker definition of A (heat.py) restricted to the patch's free rows and
+    columns, without forming A: D = M_pp (x) (C+E0) + kappa K_pp (x) Mt,
+    L = -M_pp (x) E1 (node-major, temporal node fastest, like slab_indices).
+    Identical to A[I_p][:, I_p] for patches of free DoFs (R9); pinned by
+    tests/test_oracle_solver.py::test_patch_blocks_kron_equal_restriction."""
+    tm = prob.tm
+    Mpp = prob.M[patch][:, patch].toarray()
+    Kpp = prob.K[patch][:, patch].toarray()
+    D = np.kron(Mpp, tm.C + tm.E0) + prob.kappa * np.kron(Kpp, tm.Mt)
+    L = -np.kron(Mpp, tm.E1)
+    return D, L
+
+
+def patch_solve_kron(prob, patch, g):
+    """Forward substitution over slabs with the Kronecker-built blocks
+    (dense LAPACK LU per slab); g, x slab-major like patch_indices."""
+    D, L = patch_blocks_kron(prob, patch)
+    m = D.shape[0]
+    x = np.zeros_like(g)
+    for n in range(prob.N):
+        rhs = g[n * m:(n + 1) * m].copy()
+        if n > 0:
+            rhs -= L @ x[(n - 1) * m:n * m]
+        x[n * m:(n + 1) * m] = sla.lu_solve(sla.lu_factor(D), rhs)
+    return x
+
+
 def weights(patches, nnode, mode="pou"):
     if mode == "pou":
         mu = patchmod.multiplicity(patches, nnode)

@@ -109,3 +109,15 @@ def test_P13_manufactured_spatial_order(k):
     e2 = _manufactured_error(8, k, 2, 8, 0.1)
     order = np.log2(e1 / e2)
     assert order >= k + 1 - 0.2, order
+
+
+def test_residual_node_and_rows_match_explicit_A():
+    """The row-wise evaluators used for full-size sampled parity equal b - A u."""
+    p = heat.unit_square_problem(4, 3, 1, 5, 0.2)
+    u = wi.spacetime_field(p.nnode, 5, 1, seed=4)
+    b = wi.spacetime_field(p.nnode, 5, 1, seed=5)
+    r = p.residual(u, b).reshape(p.nnode, -1)
+    for i in (0, 7, 20, p.nnode // 2, p.nnode - 1):
+        assert np.allclose(p.residual_node(i, u, b), r[i], rtol=1e-13, atol=1e-14)
+    rows = np.array([3, 50, 77, p.ndof - 1])
+    assert np.allclose(p.residual_rows(rows, u, b), r.ravel()[rows], rtol=1e-13, atol=1e-14)

@@ -63,6 +63,21 @@ def test_P7_patch_march_equals_dense_solve():
         assert np.allclose(fac.solve(pi, g), np.linalg.solve(Ap, g), rtol=1e-11, atol=1e-12)
 
 
+def test_patch_blocks_kron_equal_restriction():
+    """The Kronecker-built patch blocks used at full size equal A[I_p][:, I_p]."""
+    for k, q in ((2, 1), (3, 2), (1, 0)):
+        p, b = _small_problem(n=4, k=k, q=q, N=3)
+        P, _ = patches.vertex_star_patches(p.mesh, k, p.constrained)
+        for pt in (P[0], P[len(P) // 2], P[-1]):
+            D, L = smoother.patch_blocks_kron(p, pt)
+            I1, I0 = p.slab_indices(pt, 1), p.slab_indices(pt, 0)
+            assert np.allclose(D, p.A[I1][:, I1].toarray(), rtol=0, atol=1e-15)
+            assert np.allclose(L, p.A[I1][:, I0].toarray(), rtol=0, atol=1e-15)
+            g = np.random.default_rng(0).standard_normal(pt.size * (q + 1) * p.N)
+            fac = smoother.PatchFactors(p, p.A, [pt])
+            assert np.allclose(smoother.patch_solve_kron(p, pt, g), fac.solve(0, g), rtol=1e-12, atol=1e-14)
+
+
 @pytest.mark.parametrize("k,q", [(1, 0), (2, 1), (3, 1)])
 def test_P8_single_patch_is_direct_solve(k, q):
     p, b = _small_problem(n=3, k=k, q=q)
