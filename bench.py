@@ -192,6 +192,72 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------------- GPU arm
+def run_c5(args, ws, rank, local):
+    """BASELINE configs[4] (C5), per GPU (weak reading R24): heat, P2 x DG1,
+    N = 256 (dt = 1/256, T = 1), 1024x1024 mesh, 20 stationary V(1,1) cycles
+    u <- u + V(b - A u) from u = 0 (one step = the 20 cycles)."""
+    import torch
+
+    import paper_2407_13997_b200 as w
+    torch.cuda.set_device(local)
+    n, k, q, N = 1024, 2, 1, 256
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N, device=local, stream=stream.cuda_stream)
+    setup_s = time.time() - t0
+    lay = ctx.layout
+    fhat = ctx.empty()
+    ctx.fill_uniform(fhat, 0, 0)
+    b = ctx.empty()
+    ctx.rhs(fhat, b)
+    del fhat
+    u, r, z = ctx.empty(), ctx.empty(), ctx.empty()
+    upd = lay["smooth_dof_updates_per_vcycle"]
+
+    def step():
+        u.zero_()
+        for _ in range(20):
+            ctx.residual(u, b, r)
+            ctx.vcycle(r, z)
+            u.add_(z)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ctx.profile(True)
+    l0 = w.launch_count()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    stats = ctx.kernel_stats()
+    clk = clocks.stop()
+    ctx.residual(u, b, r)
+    rel = float(torch.linalg.norm(r) / torch.linalg.norm(b))
+    per_kernel = {f"{a}@L{l}": {"launches": s["launches"], "ms": round(s["ms"], 3),
+                                "GBs": round(s["bytes"] / (s["ms"] / 1e3) / 1e9, 1) if s["ms"] > 0 else None,
+                                "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}
+                  for (a, l), s in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+    line = {"metric": METRIC, "value": ws * 20 * upd * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5 = BASELINE configs[4] per GPU: heat P2 x DG1, N=256, 1024x1024, 20 V(1,1)",
+                       "ndof": lay["ndof"], "levels": lay["nlevels"], "setup_s": round(setup_s, 2)},
+            "relres_after_20_vcycles": rel, "per_kernel": per_kernel, "clocks": clk,
+            "gpu_launches": w.launch_count() - l0}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
 def run_gpu(args, ws, rank, local):
     import torch
 
@@ -342,13 +408,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wrmg", choices=["wrmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="C2", choices=["C2", "C5"])
     args = ap.parse_args()
     ws, rank, local = dist_setup(args) if args.impl == "wrmg" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return
-    run_gpu(args, ws, rank, local)
+    if args.config == "C5":
+        run_c5(args, ws, rank, local)
+    else:
+        run_gpu(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
