@@ -164,3 +164,85 @@ def evaluate_basis(k, xi):
     xi = np.atleast_2d(xi)
     Vm = np.array([[x ** p * y ** s for (p, s) in mons] for (x, y) in xi])
     return Vm @ C
+
+
+# --------------------------------------------------------------------------
+# Mixed-degree integrals for Taylor-Hood (eq. nsfem).
+# Polynomials on T^ as dense coefficient arrays c[p, s] of xi^p eta^s.
+
+def basis_polys(k):
+    """List of (k+1, k+1) coefficient arrays of the P_k reference basis."""
+    C = lagrange_coefficients(k)
+    out = []
+    for i in range(C.shape[1]):
+        c = np.zeros((k + 1, k + 1))
+        for m, (p, s) in enumerate(monomials(k)):
+            c[p, s] = C[m, i]
+        out.append(c)
+    return out
+
+
+def poly_mul(a, b):
+    out = np.zeros((a.shape[0] + b.shape[0] - 1, a.shape[1] + b.shape[1] - 1))
+    for p in range(a.shape[0]):
+        for s in range(a.shape[1]):
+            if a[p, s] != 0.0:
+                out[p:p + b.shape[0], s:s + b.shape[1]] += a[p, s] * b
+    return out
+
+
+def poly_int(c):
+    tot = 0.0
+    for p in range(c.shape[0]):
+        for s in range(c.shape[1]):
+            if c[p, s] != 0.0:
+                tot += c[p, s] * mono_integral(p, s)
+    return tot
+
+
+def poly_dxi(c):
+    out = np.zeros_like(c)
+    out[:-1, :] = c[1:, :] * np.arange(1, c.shape[0])[:, None]
+    return out
+
+
+def poly_deta(c):
+    out = np.zeros_like(c)
+    out[:, :-1] = c[:, 1:] * np.arange(1, c.shape[1])[None, :]
+    return out
+
+
+def physical_grads(polys, Jac):
+    """(d/dx, d/dy) of each reference polynomial for x = v0 + Jac xi."""
+    Ji = np.linalg.inv(Jac)
+    out = []
+    for c in polys:
+        dx, dy = poly_dxi(c), poly_deta(c)
+        out.append((Ji[0, 0] * dx + Ji[1, 0] * dy, Ji[0, 1] * dx + Ji[1, 1] * dy))
+    return out
+
+
+def taylor_hood_element(ku, kp, verts):
+    """Element integrals on the physical triangle (all times |det Jac|):
+    Mv[i,j] = int v_i v_j, Kv[i,j] = int grad v_i . grad v_j          (velocity P_ku)
+    G[d][i,j] = int chi_j d_d v_i                                      (pressure P_kp)
+    To[d][i,l,j] = int v_i v_l d_d v_j                                 (convection)"""
+    v0, v1, v2 = np.asarray(verts, dtype=float)
+    Jac = np.column_stack([v1 - v0, v2 - v0])
+    det = abs(np.linalg.det(Jac))
+    vb, pb = basis_polys(ku), basis_polys(kp)
+    vg = physical_grads(vb, Jac)
+    nu, npn = len(vb), len(pb)
+    Mv = np.array([[poly_int(poly_mul(vb[i], vb[j])) for j in range(nu)] for i in range(nu)]) * det
+    Kv = np.array([[poly_int(poly_mul(vg[i][0], vg[j][0]) + 0.0) + poly_int(poly_mul(vg[i][1], vg[j][1]))
+                    for j in range(nu)] for i in range(nu)]) * det
+    G = np.array([[[poly_int(poly_mul(pb[j], vg[i][d])) for j in range(npn)] for i in range(nu)]
+                  for d in range(2)]) * det
+    To = np.zeros((2, nu, nu, nu))
+    for i in range(nu):
+        for l in range(nu):
+            vl = poly_mul(vb[i], vb[l])
+            for j in range(nu):
+                for d in range(2):
+                    To[d, i, l, j] = poly_int(poly_mul(vl, vg[j][d]))
+    return Mv * 1.0, Kv, G, To * det
