@@ -181,7 +181,7 @@ void wrmg_destroy(wrmg_ctx *ctx);
  * coarsest): launch count, summed device milliseconds, and the algorithmic
  * bytes / flops of those launches ("Roofline accounting"). */
 enum { WRMG_K_RESIDUAL = 0, WRMG_K_SWEEP = 1, WRMG_K_RESTRICT = 2, WRMG_K_PROLONG = 3, WRMG_K_COARSE = 4,
-       WRMG_K_KRYLOV = 5, WRMG_K_COUNT = 6 };
+       WRMG_K_KRYLOV = 5, WRMG_K_FACTOR = 6, WRMG_K_COUNT = 7 };
 typedef struct {
   int64_t launches;
   double ms;
@@ -190,6 +190,15 @@ typedef struct {
 } wrmg_kernel_stat;
 wrmg_status wrmg_profile(wrmg_ctx *ctx, int32_t enable);
 wrmg_status wrmg_kernel_stats(wrmg_ctx *ctx, wrmg_kernel_stat *out);
+
+/* Test / introspection hook: copy `count` elements of an internal device array of
+ * `level` to host memory.  which: 0 spatial val (heat M, NS M2), 1 val2 (heat
+ * kappa K, NS K2 + divergence blocks), 2 NS convection [nvv][N(q+1)], 3 NS
+ * injected state, 4 NS coarse slab blocks after factorisation (LU, column-major,
+ * per slab), 5 CSR rowptr (int32), 6 CSR col (int32), 7 coarse free sids (int32),
+ * 8 NS coarse LU info per slab (int32), 9 NS coarse LU pivots (int32).
+ * Synchronises.  WRMG_E_INVALID if the array is absent or shorter than count. */
+wrmg_status wrmg_debug_fetch(wrmg_ctx *ctx, int32_t level, int32_t which, void *host_dst, int64_t count);
 
 /* Number of kernels this library has launched in the process so far. */
 int64_t wrmg_launch_count(void);

@@ -38,7 +38,7 @@ class wrmg_kernel_stat(ctypes.Structure):
     _fields_ = [("launches", c_i64), ("ms", c_dbl), ("bytes", c_dbl), ("flops", c_dbl)]
 
 
-KERNEL_CLASSES = ["residual", "sweep", "restrict", "prolong", "coarse", "krylov"]
+KERNEL_CLASSES = ["residual", "sweep", "restrict", "prolong", "coarse", "krylov", "factor"]
 
 _P = ctypes.POINTER
 _sig = {
@@ -65,6 +65,7 @@ _sig = {
     "wrmg_profile": (c_i32, [c_vp, c_i32]),
     "wrmg_kernel_stats": (c_i32, [c_vp, c_vp]),
     "wrmg_launch_count": (c_i64, []),
+    "wrmg_debug_fetch": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -138,10 +139,12 @@ def wrmg_fill_uniform(out, first_id=0, seed=0, ctx=None):
 
 
 class Context:
-    """One wrmg_ctx: the heat space-time hierarchy on one device/stream."""
+    """One wrmg_ctx: the space-time hierarchy (heat, or Navier-Stokes with
+    problem="ns": Taylor-Hood P_{degree+1}-P_degree) on one device/stream."""
 
     def __init__(self, nx, ny=None, h=None, degree=1, q=0, nslabs=1, dt=1.0, kappa=1.0, omega_mg=1.0,
-                 nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None, factor_mode="auto"):
+                 nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None, factor_mode="auto",
+                 problem="heat", reynolds=1.0, bc=None, lid_speed=1.0):
         import torch
         ny = nx if ny is None else ny
         h = 1.0 / ny if h is None else h
@@ -149,7 +152,11 @@ class Context:
             stream = torch.cuda.current_stream(device).cuda_stream
         self._mesh = _mesh(nx, ny, h, ncoarse)
         co = wrmg_coeffs()
-        co.problem, co.bc, co.kappa = 0, 0, float(kappa)
+        co.problem = {"heat": 0, "ns": 1}[problem]
+        if bc is None:
+            bc = "dirichlet0"
+        co.bc = {"dirichlet0": 0, "neumann": 1, "lid": 2}[bc]
+        co.kappa, co.reynolds, co.lid_speed = float(kappa), float(reynolds), float(lid_speed)
         co.weights = 0 if weights == "pou" else 1
         co.omega_mg, co.nu_pre, co.nu_post = float(omega_mg), int(nu_pre), int(nu_post)
         co.device, co.stream, co.rank, co.nranks = int(device), c_vp(stream), 0, 1
@@ -181,14 +188,14 @@ class Context:
         return n.value
 
     # --- C ABI
-    def linearize(self):
-        _check(lib.wrmg_linearize(self._h, None), self._h)
+    def linearize(self, state=None):
+        _check(lib.wrmg_linearize(self._h, None if state is None else _ptr(state)), self._h)
 
     def rhs(self, fhat, b):
         _check(lib.wrmg_rhs(self._h, _ptr(fhat), _ptr(b)), self._h)
 
-    def residual(self, u, b, r):
-        _check(lib.wrmg_residual(self._h, _ptr(u), _ptr(b), _ptr(r), 0), self._h)
+    def residual(self, u, b, r, nonlinear=False):
+        _check(lib.wrmg_residual(self._h, _ptr(u), _ptr(b), _ptr(r), 1 if nonlinear else 0), self._h)
 
     def apply(self, x, y):
         _check(lib.wrmg_apply(self._h, _ptr(x), _ptr(y)), self._h)
@@ -213,6 +220,13 @@ class Context:
             _check(st, self._h)
         return its.value, rel.value, STATUS[st]
 
+    def newton(self, U, rtol=1e-8, maxit=20):
+        its, lin = c_i32(), c_i32()
+        st = lib.wrmg_newton(self._h, _ptr(U), float(rtol), int(maxit), ctypes.byref(its), ctypes.byref(lin))
+        if st not in (0, 6):
+            _check(st, self._h)
+        return its.value, lin.value, STATUS[st]
+
     def fill_uniform(self, out, first_id=0, seed=0):
         _check(lib.wrmg_fill_uniform(self._h, _ptr(out), out.numel(), int(first_id), int(seed)), self._h)
 
@@ -230,6 +244,11 @@ class Context:
                 st = arr[l * len(KERNEL_CLASSES) + ci]
                 if st.launches:
                     out[(name, l)] = dict(launches=st.launches, ms=st.ms, bytes=st.bytes, flops=st.flops)
+        return out
+
+    def debug_fetch(self, level, which, count, dtype=np.float64):
+        out = np.empty(int(count), dtype=dtype)
+        _check(lib.wrmg_debug_fetch(self._h, int(level), int(which), out.ctypes.data_as(c_vp), int(count)), self._h)
         return out
 
     def sync(self):

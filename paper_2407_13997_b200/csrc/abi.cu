@@ -9,6 +9,8 @@
 #include <vector>
 
 #include "internal.h"
+#include "ns.h"
+#include "ns_kernels.h"
 #include "plan.h"
 
 using namespace wrmg;
@@ -95,19 +97,59 @@ struct PScope {
   }
 };
 
-double residual_bytes(const wrmg_ctx *c, int l) { return 24.0 * c->lv[l].nnode * c->nt; }
+double residual_bytes(const wrmg_ctx *c, int l) {
+  return 24.0 * c->lv[l].nnode * c->nt + (c->ns ? 8.0 * c->lv[l].nvv * c->nt : 0.0);
+}
 double residual_flops(const wrmg_ctx *c, int l) {
   return 2.0 * (2 * c->nq + 1) * (double)c->lv[l].A.nnz * c->N;
 }
-double sweep_bytes(const wrmg_ctx *c, int l) { return 24.0 * c->lv[l].nfree * c->nt; }
+double sweep_bytes(const wrmg_ctx *c, int l) {
+  const Level &L = c->lv[l];
+  // NS: every stored (patch, slab) inverse is streamed once per sweep
+  return 24.0 * L.nfree * c->nt + (c->ns ? 8.0 * (double)L.npatch * c->N * L.mstride : 0.0);
+}
 
-void prof_residual(wrmg_ctx *c, int l, const double *u, const double *b, double *r, bool uzero) {
+NSGeom geom(const wrmg_ctx *c, const Level &L) {
+  NSGeom g{};
+  g.nx = L.nx;
+  g.ny = L.ny;
+  g.ku = c->k + 1;
+  g.kp = c->k;
+  g.Lux = L.Lux;
+  g.Lpx = L.Lpx;
+  g.nu = c->th_nu;
+  g.np = c->th_np;
+  g.Lu = L.Lu;
+  g.Lp = L.Lp;
+  g.ns = L.nnode;
+  g.h = L.h;
+  return g;
+}
+
+// Pressure mean removal per (slab, temporal node) of a level vector (H15, R19).
+void ns_project(wrmg_ctx *c, const Level &L, double *v) {
+  launch_ns_project(v + 2 * L.Lu * c->nt, L.Lp, c->nt, c->proj, c->stream);
+}
+
+void prof_residual(wrmg_ctx *c, int l, const double *u, const double *b, double *r, bool uzero,
+                   const double *conv = nullptr) {
   PScope ps(c, WRMG_K_RESIDUAL, l, residual_bytes(c, l), uzero ? 0.0 : residual_flops(c, l));
+  if (c->ns) {
+    const Level &L = c->lv[l];
+    launch_ns_residual(geom(c, L), c->q, c->N, c->tm, L.A, L.vvptr, conv ? conv : L.conv, L.con, u, b, r, c->stream);
+    return;
+  }
   launch_residual(c->lv[l], c->q, c->N, c->tm, u, b, r, uzero, c->stream);
 }
 
 void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
   PScope ps(c, WRMG_K_SWEEP, l, sweep_bytes(c, l), c->sweep_flops[l]);
+  if (c->ns) {
+    const Level &L = c->lv[l];
+    launch_ns_sweep(c->q, c->N, L.mp, L.npatch, L.mstride, L.pnodes, L.wnode, L.A, L.nsinv, r, u, om, c->stream);
+    ns_project(c, L, u);
+    return;
+  }
   if (c->use_kron && launch_sweep_kron(c->lv[l], c->q, c->N, r, u, om, c->stream)) return;
   launch_sweep(c->lv[l], c->q, c->N, r, u, om, c->stream);
 }
@@ -119,7 +161,8 @@ void free_level(Level &L) {
                   (void *)L.P.val, (void *)L.R.rowptr, (void *)L.R.col, (void *)L.R.val, (void *)L.vr, (void *)L.vz,
                   (void *)L.vt, (void *)L.kV, (void *)L.kVT, (void *)L.kS, (void *)L.ksig, (void *)L.cta_patch,
                   (void *)L.cta_type, (void *)L.rcls, (void *)L.cta_patch1, (void *)L.cta_type1,
-                  (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8})
+                  (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8, (void *)L.vvptr, (void *)L.conv,
+                  (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo})
     dfree(p);
 }
 
@@ -246,12 +289,217 @@ void factor_all(wrmg_ctx *c) {
   }
 }
 
+
+// Navier-Stokes linearisation at the finest-level state W (NULL = zero state):
+// inject W to every level (R13), assemble R N(W) (H1), invert every (patch, slab)
+// block (H4, H5) and the pinned coarse slab blocks (H11).  Synchronises.
+void factor_all_ns(wrmg_ctx *c, const double *W) {
+  cudaStream_t s = c->stream;
+  const int nl = (int)c->lv.size();
+  const double *Wl = W;
+  for (int l = nl - 1; l >= 0; --l) {
+    Level &L = c->lv[l];
+    if (l < nl - 1 && W) {
+      launch_ns_inject(geom(c, L), geom(c, c->lv[l + 1]), c->nt, Wl, L.state, s);
+      Wl = L.state;
+    }
+    launch_ns_assemble_conv(geom(c, L), c->nt, c->co.reynolds, true, L.A, L.vvptr, W ? Wl : nullptr, L.conv,
+                            c->th_T, s);
+    check_launch();
+    if (l >= 1 || nl == 1) {
+      const double m = (double)c->nq * L.mp;
+      PScope ps(c, WRMG_K_FACTOR, l, 8.0 * (double)L.npatch * c->N * L.mstride,
+                2.0 * m * m * m * (double)L.npatch * c->N);
+      launch_ns_factor(geom(c, L), c->q, c->N, c->tm, L.A, L.vvptr, L.conv, L.pnodes, L.npatch, L.mp, L.mstride,
+                       L.nsinv, L.nsinfo, s);
+      check_launch();
+    }
+  }
+  Coarse &C = c->coarse;
+  Level &L0 = c->lv[0];
+  launch_ns_coarse_blocks(geom(c, L0), c->q, c->N, c->tm, L0.A, L0.vvptr, L0.conv, C.nodes, C.mp, C.pin, C.nsD, s);
+  check_launch();
+  launch_batched_lu(C.nsD, C.m, c->N, C.nspiv, C.nsinfo, s);
+  check_launch();
+  launch_lu_inverse_batched(C.nsD, C.nspiv, C.m, c->N, C.nsinvT, s);
+  check_launch();
+  CK(cudaStreamSynchronize(s));
+  c->err_level = c->err_patch = c->err_slab = -1;
+  for (int l = (nl == 1 ? 0 : 1); l < nl; ++l) {
+    Level &L = c->lv[l];
+    std::vector<int32_t> info((size_t)L.npatch * c->N);
+    CK(cudaMemcpy(info.data(), L.nsinfo, info.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (size_t e = 0; e < info.size(); ++e)
+      if (info[e]) {
+        c->err_level = l;
+        c->err_patch = (int)(e / c->N);
+        c->err_slab = (int)(e % c->N);
+        throw Err{WRMG_E_SINGULAR, "singular Vanka patch block (level " + std::to_string(l) + ", patch " +
+                                       std::to_string(c->err_patch) + ", slab " + std::to_string(c->err_slab) + ")"};
+      }
+  }
+  std::vector<int32_t> ci(c->N);
+  CK(cudaMemcpy(ci.data(), C.nsinfo, c->N * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int n = 0; n < c->N; ++n)
+    if (ci[n]) {
+      c->err_level = 0;
+      c->err_slab = n;
+      throw Err{WRMG_E_SINGULAR, "singular coarse slab block (slab " + std::to_string(n) + ")"};
+    }
+}
+
+// Hierarchy of Taylor-Hood levels (problem == WRMG_NAVIER_STOKES).
+void setup_ns(wrmg_ctx *c) {
+  cudaStream_t s = c->stream;
+  if (c->k > 2) throw Err{WRMG_E_UNSUPPORTED, "Navier-Stokes: degree must be 1 (P2-P1) or 2 (P3-P2)"};
+  if (!(c->co.reynolds > 0)) throw Err{WRMG_E_INVALID, "Reynolds number must be > 0"};
+  if (c->co.bc != WRMG_BC_DIRICHLET0 && c->co.bc != WRMG_BC_LID)
+    throw Err{WRMG_E_UNSUPPORTED, "Navier-Stokes: bc must be WRMG_BC_DIRICHLET0 or WRMG_BC_LID"};
+  c->ns = true;
+  c->use_kron = false;
+  THElement E;
+  build_th_element(c->k, &E);
+  c->th_nu = E.nu;
+  c->th_np = E.np;
+  {
+    const int nu = E.nu, np = E.np;
+    std::vector<double> ref(2 * nu * nu + 2 * nu * np), th(2 * nu * nu * nu);
+    std::memcpy(ref.data(), E.Mh, nu * nu * sizeof(double));
+    std::memcpy(ref.data() + nu * nu, E.Kh, nu * nu * sizeof(double));
+    std::memcpy(ref.data() + 2 * nu * nu, E.Gh, 2 * nu * np * sizeof(double));
+    std::memcpy(th.data(), E.Th, th.size() * sizeof(double));
+    c->th_ref = dupload(ref, s);
+    c->th_T = dupload(th, s);
+  }
+  std::vector<int> nys;
+  std::vector<int> nxs = level_sizes(c->mesh.gnx, c->mesh.gny, c->mesh.ncoarse, &nys);
+  const int nl = (int)nxs.size();
+  std::vector<NSPlan> plans(nl);
+  c->lv.resize(nl);
+  for (int l = 0; l < nl; ++l) {
+    const double h = c->mesh.h * (double)(c->mesh.gnx / nxs[l]);
+    plan_ns_level(nxs[l], nys[l], h, c->k, c->co.bc, c->co.lid_speed, &plans[l]);
+    NSPlan &P = plans[l];
+    Level &L = c->lv[l];
+    L.nx = P.nx;
+    L.ny = P.ny;
+    L.h = h;
+    L.Lx = P.Lux;
+    L.Ly = P.Luy;
+    L.Lux = P.Lux;
+    L.Lpx = P.Lpx;
+    L.Lu = P.Lu;
+    L.Lp = P.Lp;
+    L.nnode = P.ns;
+    L.nfree = P.nfree;
+    L.A.nrow = P.ns;
+    L.A.nnz = (int64_t)P.col.size();
+    L.A.rowptr = dupload(P.rowptr, s);
+    L.A.col = dupload(P.col, s);
+    L.A.val = dalloc<double>(P.col.size());
+    L.A.val2 = dalloc<double>(P.col.size());
+    L.h_con = P.con;
+    L.con = dupload(P.con, s);
+    L.vvptr = dupload(P.vvptr, s);
+    L.nvv = P.vvptr.back();
+    L.conv = dalloc<double>((size_t)L.nvv * c->nt);
+    L.npatch = P.npatch;
+    L.mp = P.mp;
+    L.pnodes = dupload(P.pnodes, s);
+    std::vector<double> w(P.ns, 0.0);
+    for (int64_t i = 0; i < P.ns; ++i)
+      if (P.mu[i] > 0) w[i] = (c->co.weights == WRMG_W_NONE) ? 1.0 : 1.0 / P.mu[i];
+    L.wnode = dupload(w, s);
+    double fl = 0.0;  // per (patch, slab): 2 m^2 (stored-inverse matvec) + 2 m_p^2 (jump)
+    for (int32_t ps : P.psize) fl += 2.0 * ((double)c->nq * ps) * ((double)c->nq * ps) + 2.0 * (double)ps * ps;
+    c->sweep_flops.push_back(fl * c->N);
+    const int64_t m = (int64_t)c->nq * L.mp;
+    L.mstride = (m * m + 1) & ~(int64_t)1;
+    if (l >= 1 || nl == 1) {
+      L.nsinv = dalloc<double>((size_t)L.npatch * c->N * L.mstride);
+      L.nsinfo = dalloc<int32_t>((size_t)L.npatch * c->N);
+    }
+    if (l < nl - 1) {
+      L.vr = dalloc<double>(L.nnode * c->nt);
+      L.vz = dalloc<double>(L.nnode * c->nt);
+      L.vt = dalloc<double>(L.nnode * c->nt);
+      L.state = dalloc<double>(L.nnode * c->nt);
+    }
+    CK(cudaStreamSynchronize(s));
+  }
+  for (int l = 1; l < nl; ++l) {
+    std::vector<int32_t> rp, ci, trp, tci;
+    std::vector<double> v, tv;
+    plan_ns_interpolation(plans[l - 1], plans[l], rp, ci, v);
+    transpose_csr(plans[l].ns, plans[l - 1].ns, rp, ci, v, trp, tci, tv);
+    Level &C = c->lv[l - 1];
+    C.P.nrow = plans[l].ns;
+    C.P.nnz = (int64_t)ci.size();
+    C.P.rowptr = dupload(rp, s);
+    C.P.col = dupload(ci, s);
+    C.P.val = dupload(v, s);
+    C.R.nrow = plans[l - 1].ns;
+    C.R.nnz = (int64_t)tci.size();
+    C.R.rowptr = dupload(trp, s);
+    C.R.col = dupload(tci, s);
+    C.R.val = dupload(tv, s);
+    CK(cudaStreamSynchronize(s));
+  }
+  {
+    Coarse &C = c->coarse;
+    const NSPlan &P = plans[0];
+    std::vector<int32_t> nodes;
+    for (int64_t i = 0; i < P.ns; ++i)
+      if (!P.con[i]) {
+        if (i == 2 * P.Lu) C.pin = (int)nodes.size();  // first pressure DoF (R19)
+        nodes.push_back((int32_t)i);
+      }
+    C.nfree = (int64_t)nodes.size();
+    C.mp = (int)nodes.size();
+    C.m = c->nq * C.mp;
+    if (C.m > 2048) throw Err{WRMG_E_UNSUPPORTED, "coarse slab block larger than 2048 (raise ncoarse depth)"};
+    C.nodes = dupload(nodes, s);
+    C.nsD = dalloc<double>((size_t)c->N * C.m * C.m);
+    C.nsinvT = dalloc<double>((size_t)c->N * C.m * C.m);
+    C.nspiv = dalloc<int32_t>((size_t)c->N * C.m);
+    C.nsinfo = dalloc<int32_t>(c->N);
+    C.xq = dalloc<double>(P.ns);
+  }
+  c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
+  c->red = dalloc<double>(64 + 64 * 148 * 4);
+  c->proj = dalloc<double>(ns_project_scratch(c->lv.back().Lp, c->nt));
+  c->bcg = dupload(plans[nl - 1].g, s);
+  for (auto &L : c->lv) {
+    launch_ns_assemble_linear(geom(c, L), L.A, c->th_ref, s);
+    check_launch();
+  }
+  CK(cudaStreamSynchronize(s));
+  factor_all_ns(c, nullptr);
+}
+
+// r = b - F(u) on the finest level (eq. nsfem): the residual
+// kernel with conv = R O(u) (Picard form of the convection, no Newton term).
+void ns_nonlinear_residual(wrmg_ctx *c, const double *u, const double *b, double *r) {
+  Level &L = c->lv.back();
+  if (!c->conv_nl) c->conv_nl = dalloc<double>((size_t)L.nvv * c->nt);
+  launch_ns_assemble_conv(geom(c, L), c->nt, c->co.reynolds, false, L.A, L.vvptr, u, c->conv_nl, c->th_T, c->stream);
+  prof_residual(c, (int)c->lv.size() - 1, u, b, r, false, c->conv_nl);
+}
+
 int64_t ndof_level(const wrmg_ctx *c, int l) { return c->lv[l].nnode * c->nt; }
 
 // z = B r on level l (H12): V(nu_pre, nu_post), zero initial guess.
 void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
   cudaStream_t s = c->stream;
   Level &L = c->lv[l];
+  if (l == 0 && c->ns) {
+    const Coarse &C = c->coarse;
+    PScope ps(c, WRMG_K_COARSE, 0, 8.0 * c->N * (double)C.m * C.m + 16.0 * L.nnode * c->nt,
+              2.0 * c->N * (double)C.m * C.m);
+    launch_ns_coarse_solve(c->q, c->N, C.mp, C.pin, C.nodes, L.A, C.nsinvT, r, z, C.xq, L.nnode, s);
+    ns_project(c, L, z);
+    return;
+  }
   if (l == 0) {
     const Coarse &C = c->coarse;
     PScope ps(c, WRMG_K_COARSE, 0, 16.0 * C.nfree * c->nt + 8.0 * L.nnode * c->nt,
@@ -280,6 +528,7 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
     PScope ps(c, WRMG_K_RESTRICT, l, 8.0 * (L.nnode + C.nnode) * c->nt, 2.0 * C.R.nnz * c->nt);
     launch_restrict(C, c->nt, t, C.vr, s);
   }
+  if (c->ns) ns_project(c, C, C.vr);
   vcycle_level(c, l - 1, C.vr, C.vz);
   {
     PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
@@ -365,9 +614,11 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     *out = nullptr;
     validate(mesh, degree, q, nslabs, dt);
     if (!coeffs) throw Err{WRMG_E_INVALID, "coeffs is NULL"};
-    if (coeffs->problem != WRMG_HEAT) throw Err{WRMG_E_UNSUPPORTED, "only WRMG_HEAT is built"};
-    if (coeffs->bc != WRMG_BC_DIRICHLET0) throw Err{WRMG_E_UNSUPPORTED, "only WRMG_BC_DIRICHLET0 is built"};
-    if (!(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
+    if (coeffs->problem != WRMG_HEAT && coeffs->problem != WRMG_NAVIER_STOKES)
+      throw Err{WRMG_E_UNSUPPORTED, "problem must be WRMG_HEAT or WRMG_NAVIER_STOKES"};
+    if (coeffs->problem == WRMG_HEAT && coeffs->bc != WRMG_BC_DIRICHLET0)
+      throw Err{WRMG_E_UNSUPPORTED, "heat: only WRMG_BC_DIRICHLET0 is built"};
+    if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
     if (coeffs->nranks > 1) throw Err{WRMG_E_UNSUPPORTED, "multi-rank strips are not built"};
     c = new wrmg_ctx();
     c->mesh = *mesh;
@@ -402,6 +653,11 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       std::memcpy(ref.data(), c->ref.M, nloc * nloc * sizeof(double));
       std::memcpy(ref.data() + nloc * nloc, c->ref.K, nloc * nloc * sizeof(double));
       c->ref_dev = dupload(ref, s);
+    }
+    if (coeffs->problem == WRMG_NAVIER_STOKES) {
+      setup_ns(c);
+      *out = c;
+      return WRMG_OK;
     }
     std::vector<int> nys;
     std::vector<int> nxs = level_sizes(mesh->gnx, mesh->gny, c->mesh.ncoarse, &nys);
@@ -567,6 +823,10 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
 wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
   if (!c) return WRMG_E_INVALID;
   try {
+    if (c->ns) {
+      factor_all_ns(c, state);
+      return WRMG_OK;
+    }
     if (state) throw Err{WRMG_E_UNSUPPORTED, "heat operator is linear: state must be NULL"};
     factor_all(c);
     return WRMG_OK;
@@ -578,6 +838,13 @@ wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
 wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
   if (!c || !fhat || !b) return WRMG_E_INVALID;
   try {
+    if (c->ns) {  // R6 (C3): b = drawn values on free rows, 0 on constrained rows, pressure mean-projected
+      const Level &L = c->lv.back();
+      launch_ns_mask(L.nnode, c->nt, L.con, nullptr, fhat, b, c->stream);
+      ns_project(c, L, b);
+      check_launch();
+      return WRMG_OK;
+    }
     launch_rhs(c->lv.back(), c->q, c->N, c->tm, fhat, b, c->stream);
     check_launch();
     return WRMG_OK;
@@ -588,8 +855,13 @@ wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
 
 wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double *r, int32_t nonlinear) {
   if (!c || !u || !b || !r) return WRMG_E_INVALID;
-  if (nonlinear) return WRMG_E_UNSUPPORTED;
+  if (nonlinear && !c->ns) return WRMG_E_UNSUPPORTED;
   try {
+    if (nonlinear) {
+      ns_nonlinear_residual(c, u, b, r);
+      check_launch();
+      return WRMG_OK;
+    }
     prof_residual(c, (int)c->lv.size() - 1, u, b, r, false);
     check_launch();
     return WRMG_OK;
@@ -852,10 +1124,97 @@ wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
 
 int64_t wrmg_launch_count(void) { return g_launches; }
 
-wrmg_status wrmg_newton(wrmg_ctx *c, double *, double, int32_t, int32_t *, int32_t *) {
-  if (c) c->err = "Navier-Stokes Newton is not built";
-  g_err = "Navier-Stokes Newton is not built";
-  return WRMG_E_UNSUPPORTED;
+wrmg_status wrmg_debug_fetch(wrmg_ctx *c, int32_t level, int32_t which, void *host_dst, int64_t count) {
+  if (!c || !host_dst || count < 0 || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  try {
+    const Level &L = c->lv[level];
+    const void *src = nullptr;
+    int64_t avail = 0, esz = 8;
+    switch (which) {
+      case 0: src = L.A.val; avail = L.A.nnz; break;
+      case 1: src = L.A.val2; avail = L.A.nnz; break;
+      case 2: src = L.conv; avail = L.nvv * c->nt; break;
+      case 3: src = L.state; avail = L.state ? L.nnode * c->nt : 0; break;
+      case 4: src = c->coarse.nsD; avail = c->coarse.nsD ? (int64_t)c->N * c->coarse.m * c->coarse.m : 0; break;
+      case 5: src = L.A.rowptr; avail = L.A.nrow + 1; esz = 4; break;
+      case 6: src = L.A.col; avail = L.A.nnz; esz = 4; break;
+      case 7: src = c->coarse.nodes; avail = c->coarse.nfree; esz = 4; break;
+      case 8: src = c->coarse.nsinfo; avail = c->coarse.nsinfo ? c->N : 0; esz = 4; break;
+      case 9: src = c->coarse.nspiv; avail = c->coarse.nspiv ? (int64_t)c->N * c->coarse.m : 0; esz = 4; break;
+      default: return WRMG_E_INVALID;
+    }
+    if (!src || count > avail) return WRMG_E_INVALID;
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(host_dst, src, count * esz, cudaMemcpyDeviceToHost));
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+// Eisenstat-Walker choice 2 with safeguard (R22).
+static double eisenstat_walker(double eta_prev, double fn, double fprev) {
+  const double gamma = 1.0, alpha = 0.5 * (1.0 + std::sqrt(5.0)), eta_max = 0.9;
+  double eta = gamma * std::pow(fn / fprev, alpha);
+  const double sg = gamma * std::pow(eta_prev, alpha);
+  if (sg > 0.1) eta = std::max(eta, sg);
+  return std::min(eta, eta_max);
+}
+
+wrmg_status wrmg_newton(wrmg_ctx *c, double *U, double rtol, int32_t maxit, int32_t *newton_its, int32_t *lin_its) {
+  if (!c || !U || maxit < 0) return WRMG_E_INVALID;
+  if (!c->ns) {
+    c->err = "wrmg_newton: the heat operator is linear";
+    return WRMG_E_UNSUPPORTED;
+  }
+  try {
+    cudaStream_t s = c->stream;
+    Level &L = c->lv.back();
+    const int64_t n = L.nnode * c->nt;
+    if (!c->nl_b) {
+      c->nl_b = dalloc<double>(n);
+      c->nl_r = dalloc<double>(n);
+      c->nl_dx = dalloc<double>(n);
+    }
+    // Dirichlet / lid values on the constrained rows of U and of the residual's b (R5)
+    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, U, U, s);
+    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, nullptr, c->nl_b, s);
+    auto negF = [&]() {  // nl_r = -F(U)
+      ns_nonlinear_residual(c, U, c->nl_b, c->nl_r);
+      return std::sqrt(dot_host(c, c->nl_r, c->nl_r, n));
+    };
+    const double f0 = negF();
+    double fn = f0, fprev = f0, eta = 0.3;
+    int its = 0, lin = 0;
+    for (int it = 0; it < maxit; ++it) {
+      if (fn <= rtol * f0) break;
+      factor_all_ns(c, U);
+      ns_project(c, L, c->nl_r);
+      int32_t li = 0;
+      double rr = 0.0;
+      wrmg_status st = wrmg_fgmres(c, c->nl_r, c->nl_dx, 30, 200, eta, 0.0, &li, &rr);
+      if (st != WRMG_OK && st != WRMG_E_NOT_CONVERGED && st != WRMG_E_BREAKDOWN) return st;
+      lin += li;
+      ++its;
+      launch_axpy(n, 1.0, c->nl_dx, U, s);
+      ns_project(c, L, U);
+      const double fnew = negF();
+      eta = eisenstat_walker(eta, fnew, fprev);
+      fprev = fnew;
+      fn = fnew;
+    }
+    check_launch();
+    CK(cudaStreamSynchronize(s));
+    if (newton_its) *newton_its = its;
+    if (lin_its) *lin_its = lin;
+    if (!(fn <= rtol * f0)) {
+      c->err = "Newton: maxit reached";
+      return WRMG_E_NOT_CONVERGED;
+    }
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
 }
 
 wrmg_status wrmg_batched_lu(const wrmg_ctx *c, double *A, int32_t m, int32_t batch, int32_t *piv, int32_t *info) {
@@ -915,7 +1274,10 @@ void wrmg_destroy(wrmg_ctx *c) {
   Coarse &C = c->coarse;
   for (void *p : {(void *)C.nodes, (void *)C.Dblk, (void *)C.DinvT, (void *)C.GT, (void *)C.Gq, (void *)C.Z,
                   (void *)C.Y, (void *)C.piv, (void *)C.info, (void *)C.kV, (void *)C.kVT, (void *)C.kS,
-                  (void *)C.ksig})
+                  (void *)C.ksig, (void *)C.nsD, (void *)C.nsinvT, (void *)C.xq, (void *)C.nspiv, (void *)C.nsinfo})
+    dfree(p);
+  for (void *p : {(void *)c->th_ref, (void *)c->th_T, (void *)c->bcg, (void *)c->proj, (void *)c->conv_nl,
+                  (void *)c->nl_b, (void *)c->nl_r, (void *)c->nl_dx})
     dfree(p);
   for (double *p : c->V) dfree(p);
   for (double *p : c->Z) dfree(p);

@@ -13,6 +13,7 @@
 // Lagrange nodes incl. both end points) -> C + E0, Mt, E1.
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 #include "internal.h"
 
@@ -96,6 +97,35 @@ void build_ref_element(int k, RefElement *E) {
     }
 }
 
+void eval_basis_grad(int k, double xi, double eta, double *v, double *dxi, double *deta) {
+  Dual kl1 = {k * xi, (double)k, 0.0}, kl2 = {k * eta, 0.0, (double)k};
+  Dual kl0 = {k * (1.0 - xi - eta), -(double)k, -(double)k};
+  int n = 0;
+  for (int b = 0; b <= k; ++b)
+    for (int a = 0; a + b <= k; ++a) {
+      Dual p = lagrange_tri(k, a, b, kl0, kl1, kl2);
+      v[n] = p.v;
+      dxi[n] = p.dx;
+      deta[n] = p.dy;
+      ++n;
+    }
+}
+
+void gauss_triangle(int ng, std::vector<double> &xi, std::vector<double> &eta, std::vector<double> &w) {
+  double gx[32], gw[32];
+  gauss01(ng, gx, gw);
+  xi.clear();
+  eta.clear();
+  w.clear();
+  for (int iu = 0; iu < ng; ++iu)
+    for (int iv = 0; iv < ng; ++iv) {
+      double v = gx[iv], u = gx[iu];
+      xi.push_back(u * (1.0 - v));
+      eta.push_back(v);
+      w.push_back(gw[iu] * gw[iv] * (1.0 - v));
+    }
+}
+
 void eval_basis_klambda(int k, double kl1, double kl2, double *vals) {
   Dual d1 = {kl1, 0, 0}, d2 = {kl2, 0, 0}, d0 = {k - kl1 - kl2, 0, 0};
   int n = 0;
@@ -128,7 +158,7 @@ void build_temporal(int q, double dt, Temporal *T) {
   const int ng = q + 3;
   double gx[16], gw[16];
   gauss01(ng, gx, gw);
-  double C[16] = {0}, Mt[16] = {0};
+  double C[16] = {0}, Mt[16] = {0}, Tr[64] = {0};
   for (int g = 0; g < ng; ++g) {
     double v[4], d[4];
     for (int a = 0; a < nq; ++a) v[a] = basis(a, gx[g], &d[a]);
@@ -136,6 +166,7 @@ void build_temporal(int q, double dt, Temporal *T) {
       for (int b = 0; b < nq; ++b) {
         C[a * nq + b] += gw[g] * d[b] * v[a];
         Mt[a * nq + b] += gw[g] * v[a] * v[b];
+        for (int c = 0; c < nq; ++c) Tr[(a * nq + b) * nq + c] += gw[g] * v[a] * v[b] * v[c];
       }
   }
   double v0[4], v1[4], dd;
@@ -148,6 +179,7 @@ void build_temporal(int q, double dt, Temporal *T) {
       T->CE[a * nq + b] = C[a * nq + b] + v0[a] * v0[b];
       T->Mt[a * nq + b] = dt * Mt[a * nq + b];
       T->E1[a * nq + b] = v0[a] * v1[b];
+      for (int c2 = 0; c2 < nq; ++c2) T->T[(a * nq + b) * nq + c2] = dt * Tr[(a * nq + b) * nq + c2];
     }
 }
 

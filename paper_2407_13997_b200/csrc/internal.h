@@ -34,8 +34,13 @@ struct Temporal {
   double CE[(kMaxQ + 1) * (kMaxQ + 1)];  // C + E0, row a, column b
   double Mt[(kMaxQ + 1) * (kMaxQ + 1)];  // dt int phi_a phi_b
   double E1[(kMaxQ + 1) * (kMaxQ + 1)];  // phi_a(0) phi_b(1)
+  double T[(kMaxQ + 1) * (kMaxQ + 1) * (kMaxQ + 1)];  // dt int phi_a phi_b phi_c, index (a nq + b) nq + c
 };
 void build_temporal(int q, double dt, Temporal *out);
+// Reference basis of degree k (local order of lattice.h) and its xi/eta derivatives at (xi, eta).
+void eval_basis_grad(int k, double xi, double eta, double *v, double *dxi, double *deta);
+// Collapsed (Duffy) Gauss rule with ng x ng points on the reference triangle.
+void gauss_triangle(int ng, std::vector<double> &xi, std::vector<double> &eta, std::vector<double> &w);
 
 // Residual stencil classes (kernels_residual.cu), passed by value as a kernel parameter.
 constexpr int kStencilMaxC = 16, kStencilMaxE = 40;
@@ -93,6 +98,17 @@ struct Level {
   DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)
   // V-cycle work vectors (levels below the finest)
   double *vr = nullptr, *vz = nullptr, *vt = nullptr;
+  // Navier-Stokes (Taylor-Hood) level: A = sid CSR with val = M2, val2 = K2 + divergence blocks
+  int64_t Lu = 0, Lp = 0;
+  int Lux = 0, Lpx = 0;
+  int32_t *vvptr = nullptr;         // [2 Lu + 1] compact index of velocity-velocity entries
+  int64_t nvv = 0;
+  double *conv = nullptr;           // [nvv][NT]: R N(w_{n,c}) of the current linearisation
+  double *state = nullptr;          // injected linearisation state (levels below the finest)
+  int64_t mstride = 0;              // doubles per stored (patch, slab) inverse
+  double *nsinv = nullptr;          // [npatch][N][mstride] row-major D_{p,n}^{-1}
+  int32_t *nsinfo = nullptr;        // [npatch][N]
+  int64_t nsfree_patch_dofs = 0;    // sum of patch sizes (algorithmic accounting)
 };
 
 struct Coarse {
@@ -107,6 +123,10 @@ struct Coarse {
   double *Z = nullptr;        // N x m scratch
   double *Y = nullptr;        // (N+1) x mp scratch
   int32_t *piv = nullptr, *info = nullptr;
+  // Navier-Stokes coarse solve: per-slab blocks with the pinned pressure DoF (R19)
+  int pin = -1;
+  double *nsD = nullptr, *nsinvT = nullptr, *xq = nullptr;
+  int32_t *nspiv = nullptr, *nsinfo = nullptr;
 };
 
 }  // namespace wrmg
@@ -142,6 +162,14 @@ struct wrmg_ctx {
   std::vector<cudaEvent_t> prof_pool;
   wrmg_kernel_stat stats[WRMG_K_COUNT][16];
   std::vector<double> sweep_flops;  // per level: algorithmic flops of one sweep
+  // Navier-Stokes
+  bool ns = false;
+  double *th_ref = nullptr, *th_T = nullptr;   // Taylor-Hood reference integrals on the device
+  int th_nu = 0, th_np = 0;
+  double *bcg = nullptr;                       // finest-level boundary values per sid
+  double *proj = nullptr;                      // pressure-projection scratch
+  double *conv_nl = nullptr;                   // finest R O(U) for the nonlinear residual
+  double *nl_b = nullptr, *nl_r = nullptr, *nl_dx = nullptr;  // Newton work vectors
 };
 
 namespace wrmg {

@@ -1,0 +1,778 @@
+// Navier-Stokes hot-path kernels (Taylor-Hood P_{k+1}-P_k x DG(q), eq. nsfem,
+// PAPER.md:245-271; Newton linearisation DESIGN.md R18):
+//   H1  spatial assembly: linear sid CSR values M2 (velocity mass) and KG (vector
+//       Laplacian + divergence blocks, R17), convection R N(w_{n,c}) per (slab,
+//       temporal node) on the velocity-velocity entries;
+//   H4+H5 per-(patch, slab) Vanka+star block D_{p,n} assembled in shared memory and
+//       inverted in place by Gauss-Jordan with partial pivoting (the pivot rows of
+//       LAPACK dgetrf, R10), written row-major for the sweep;
+//   H6  space-time residual, warp per sid row, lanes over slabs;
+//   H7+H8 forward time sweep: per patch, D_{p,n}^{-1} streamed slab by slab with
+//       TMA bulk copies into a double buffer, jump carried from slab n-1,
+//       weighted additive scatter with FP64 atomics (R9, R11);
+//   H11 coarse blocks with the pinned pressure DoF (R19) and the time-marching solve;
+//   H15 pressure mean projection per (slab, temporal node) (R19);
+//   state injection to coarse levels (R13).
+#include <algorithm>
+#include <cfloat>
+
+#include "lattice.h"
+#include "ns_kernels.h"
+
+namespace wrmg {
+namespace {
+
+__device__ __forceinline__ int csr_find_ns(const int32_t *rowptr, const int32_t *col, int64_t i, int32_t j) {
+  int lo = rowptr[i], hi = rowptr[i + 1] - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int32_t c = col[mid];
+    if (c == j) return mid;
+    if (c < j) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return -1;
+}
+
+// ------------------------------------------------------------------ H1 linear
+// Row r of M2 (val) and K2 + G-blocks (val2).  Triangle t maps x = v0 + s h xi,
+// s = +1 (t = 0) / -1 (t = 1): M = h^2 Mh, K = Kh, G = s h Gh, To = s h Th.
+__global__ void k_ns_assemble_linear(NSGeom g, const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                                     double *__restrict__ Mv, double *__restrict__ KGv, const double *__restrict__ ref) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= g.ns) return;
+  const int nu = g.nu, np = g.np;
+  const double *Mh = ref, *Kh = ref + nu * nu, *Gh = ref + 2 * nu * nu;
+  for (int e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+    Mv[e] = 0.0;
+    KGv[e] = 0.0;
+  }
+  int ci[6], cj[6], t[6], la[6], lb[6];
+  if (r < 2 * g.Lu) {
+    const int d = (int)(r / g.Lu);
+    const int64_t i = r - d * g.Lu;
+    const int I = (int)(i % g.Lux), J = (int)(i / g.Lux);
+    const int nc = cells_of_node(g.ku, g.nx, g.ny, I, J, ci, cj, t, la, lb);
+    for (int c = 0; c < nc; ++c) {
+      const double s = t[c] == 0 ? 1.0 : -1.0;
+      const int li = loc_index(g.ku, la[c], lb[c]);
+      for (int b = 0; b <= g.ku; ++b)
+        for (int a = 0; a + b <= g.ku; ++a) {
+          int I2, J2;
+          loc_to_lattice(g.ku, ci[c], cj[c], t[c], a, b, &I2, &J2);
+          const int lj = loc_index(g.ku, a, b);
+          const int pos = csr_find_ns(rowptr, col, r, (int32_t)(d * g.Lu + (int64_t)J2 * g.Lux + I2));
+          Mv[pos] += g.h * g.h * Mh[li * nu + lj];
+          KGv[pos] += Kh[li * nu + lj];
+        }
+      for (int b = 0; b <= g.kp; ++b)
+        for (int a = 0; a + b <= g.kp; ++a) {
+          int I2, J2;
+          loc_to_lattice(g.kp, ci[c], cj[c], t[c], a, b, &I2, &J2);
+          const int lp = loc_index(g.kp, a, b);
+          const int pos = csr_find_ns(rowptr, col, r, (int32_t)(2 * g.Lu + (int64_t)J2 * g.Lpx + I2));
+          KGv[pos] += s * g.h * Gh[(d * nu + li) * np + lp];
+        }
+    }
+  } else {
+    const int64_t j = r - 2 * g.Lu;
+    const int Ip = (int)(j % g.Lpx), Jp = (int)(j / g.Lpx);
+    const int nc = cells_of_node(g.kp, g.nx, g.ny, Ip, Jp, ci, cj, t, la, lb);
+    for (int c = 0; c < nc; ++c) {
+      const double s = t[c] == 0 ? 1.0 : -1.0;
+      const int lp = loc_index(g.kp, la[c], lb[c]);
+      for (int b = 0; b <= g.ku; ++b)
+        for (int a = 0; a + b <= g.ku; ++a) {
+          int I2, J2;
+          loc_to_lattice(g.ku, ci[c], cj[c], t[c], a, b, &I2, &J2);
+          const int lj = loc_index(g.ku, a, b);
+          const int64_t node = (int64_t)J2 * g.Lux + I2;
+          for (int d = 0; d < 2; ++d) {
+            const int pos = csr_find_ns(rowptr, col, r, (int32_t)(d * g.Lu + node));
+            KGv[pos] += s * g.h * Gh[(d * nu + lj) * np + lp];
+          }
+        }
+    }
+  }
+}
+
+// --------------------------------------------------------------- H1 convection
+// conv[e][t] = R N(w_t) on the velocity-velocity entries e of the sid CSR, t =
+// n (q+1) + c.  N(w) = O(w) (+ Q(w) for the Newton Jacobian, R18):
+//   O[(d,i),(d,j)]  = sum_l sum_d2 w[l,d2] int v_i v_l d_d2 v_j
+//   Q[(d,i),(d2,j)] = sum_l w[l,d] int v_i v_j d_d2 v_l.
+// Thread = (velocity node i, t): owns column t of rows (0,i) and (1,i).
+__global__ void __launch_bounds__(256) k_ns_assemble_conv(NSGeom g, int64_t NT, double R, int newton,
+                                                          const int32_t *__restrict__ rowptr,
+                                                          const int32_t *__restrict__ col,
+                                                          const int32_t *__restrict__ vvptr,
+                                                          const double *__restrict__ W, double *__restrict__ conv,
+                                                          const double *__restrict__ Th_g) {
+  extern __shared__ double Th[];
+  const int nu = g.nu;
+  for (int e = threadIdx.x; e < 2 * nu * nu * nu; e += blockDim.x) Th[e] = Th_g[e];
+  __syncthreads();
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= g.Lu * NT) return;
+  const int64_t i = idx / NT, tt = idx - i * NT;
+  const int64_t r0 = i, r1 = g.Lu + i;
+  for (int e = vvptr[r0]; e < vvptr[r0 + 1]; ++e) conv[(int64_t)e * NT + tt] = 0.0;
+  for (int e = vvptr[r1]; e < vvptr[r1 + 1]; ++e) conv[(int64_t)e * NT + tt] = 0.0;
+  if (W == nullptr) return;
+  const int I = (int)(i % g.Lux), J = (int)(i / g.Lux);
+  int ci[6], cj[6], t[6], la[6], lb[6];
+  const int nc = cells_of_node(g.ku, g.nx, g.ny, I, J, ci, cj, t, la, lb);
+  for (int c = 0; c < nc; ++c) {
+    const double sh = (t[c] == 0 ? 1.0 : -1.0) * g.h * R;
+    const int li = loc_index(g.ku, la[c], lb[c]);
+    double w[kMaxLocU][2];
+    int64_t node[kMaxLocU];
+    for (int b = 0; b <= g.ku; ++b)
+      for (int a = 0; a + b <= g.ku; ++a) {
+        int I2, J2;
+        loc_to_lattice(g.ku, ci[c], cj[c], t[c], a, b, &I2, &J2);
+        const int l = loc_index(g.ku, a, b);
+        node[l] = (int64_t)J2 * g.Lux + I2;
+        w[l][0] = W[node[l] * NT + tt];
+        w[l][1] = W[(g.Lu + node[l]) * NT + tt];
+      }
+    for (int lj = 0; lj < nu; ++lj) {
+      double O = 0.0, Q00 = 0.0, Q01 = 0.0, Q10 = 0.0, Q11 = 0.0;
+      for (int l = 0; l < nu; ++l) {
+        O += w[l][0] * Th[((0 * nu + li) * nu + l) * nu + lj] + w[l][1] * Th[((1 * nu + li) * nu + l) * nu + lj];
+        if (newton) {
+          const double t0 = Th[((0 * nu + li) * nu + lj) * nu + l], t1 = Th[((1 * nu + li) * nu + lj) * nu + l];
+          Q00 += w[l][0] * t0;
+          Q01 += w[l][0] * t1;
+          Q10 += w[l][1] * t0;
+          Q11 += w[l][1] * t1;
+        }
+      }
+      const int p00 = csr_find_ns(rowptr, col, r0, (int32_t)node[lj]);
+      const int p01 = csr_find_ns(rowptr, col, r0, (int32_t)(g.Lu + node[lj]));
+      const int p10 = csr_find_ns(rowptr, col, r1, (int32_t)node[lj]);
+      const int p11 = csr_find_ns(rowptr, col, r1, (int32_t)(g.Lu + node[lj]));
+      conv[(int64_t)(vvptr[r0] + p00 - rowptr[r0]) * NT + tt] += sh * (O + Q00);
+      conv[(int64_t)(vvptr[r1] + p11 - rowptr[r1]) * NT + tt] += sh * (O + Q11);
+      if (newton) {
+        conv[(int64_t)(vvptr[r0] + p01 - rowptr[r0]) * NT + tt] += sh * Q01;
+        conv[(int64_t)(vvptr[r1] + p10 - rowptr[r1]) * NT + tt] += sh * Q10;
+      }
+    }
+  }
+}
+
+// State on the next coarser level by nodal sampling (R13): coarse node (I, J) is
+// fine node (2I, 2J) on both lattices.
+__global__ void k_ns_inject(NSGeom c, NSGeom f, int64_t NT, const double *__restrict__ Wf, double *__restrict__ Wc) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= c.ns * NT) return;
+  const int64_t s = idx / NT, tt = idx - s * NT;
+  int64_t fs;
+  if (s < 2 * c.Lu) {
+    const int d = (int)(s / c.Lu);
+    const int64_t i = s - d * c.Lu;
+    const int I = (int)(i % c.Lux), J = (int)(i / c.Lux);
+    fs = d * f.Lu + (int64_t)(2 * J) * f.Lux + 2 * I;
+  } else {
+    const int64_t j = s - 2 * c.Lu;
+    const int I = (int)(j % c.Lpx), J = (int)(j / c.Lpx);
+    fs = 2 * f.Lu + (int64_t)(2 * J) * f.Lpx + 2 * I;
+  }
+  Wc[idx] = Wf[fs * NT + tt];
+}
+
+// ------------------------------------------------------------------ H6 residual
+// r = b - A u:  (A u)_{n,a} = sum_e [(C+E0)_ab M2_e + Mt_ab KG_e] u_{col,n,b}
+//   - [a = 0] M2_e u_{col,n-1,q}  + sum_{e in vv} sum_{b,c} T_abc conv_{e,n,c} u_{col,n,b}
+// constrained rows r = b - u (R5).  b == NULL: r = A u (constrained rows r = u).
+template <int NQ>
+__global__ void __launch_bounds__(256) k_ns_residual(int64_t ns, int N, const int32_t *__restrict__ rowptr,
+                                                     const int32_t *__restrict__ col, const double *__restrict__ Mv,
+                                                     const double *__restrict__ KGv, int64_t nvrow,
+                                                     const int32_t *__restrict__ vvptr,
+                                                     const double *__restrict__ conv, const uint8_t *__restrict__ con,
+                                                     const double *__restrict__ u, const double *__restrict__ b,
+                                                     double *__restrict__ r, NSTime tm) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= ns) return;
+  const int64_t NT = (int64_t)N * NQ;
+  const int e0 = rowptr[row], e1 = rowptr[row + 1];
+  const int nvv = row < nvrow ? vvptr[row + 1] - vvptr[row] : 0;
+  const int vb = row < nvrow ? vvptr[row] : 0;
+  const bool cr = con[row] != 0;
+  for (int n = lane; n < N; n += 32) {
+    const int64_t base = row * NT + (int64_t)n * NQ;
+    double acc[NQ];
+    if (cr) {
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) r[base + a] = b ? b[base + a] - u[base + a] : u[base + a];
+      continue;
+    }
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) acc[a] = 0.0;
+    for (int e = e0; e < e1; ++e) {
+      const int64_t cb = (int64_t)__ldg(col + e) * NT + (int64_t)n * NQ;
+      const double mv = __ldg(Mv + e), kg = __ldg(KGv + e);
+      double ub[NQ];
+#pragma unroll
+      for (int bb = 0; bb < NQ; ++bb) ub[bb] = __ldg(u + cb + bb);
+#pragma unroll
+      for (int a = 0; a < NQ; ++a)
+#pragma unroll
+        for (int bb = 0; bb < NQ; ++bb) acc[a] = fma(tm.CE[a * NQ + bb] * mv + tm.Mt[a * NQ + bb] * kg, ub[bb], acc[a]);
+      if (n > 0) acc[0] = fma(-mv, __ldg(u + cb - 1), acc[0]);
+      const int ev = e - e0;
+      if (ev < nvv) {
+        const double *cv = conv + (int64_t)(vb + ev) * NT + (int64_t)n * NQ;
+        double w[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) w[c] = __ldg(cv + c);
+#pragma unroll
+        for (int a = 0; a < NQ; ++a)
+#pragma unroll
+          for (int bb = 0; bb < NQ; ++bb) {
+            double tw = 0.0;
+#pragma unroll
+            for (int c = 0; c < NQ; ++c) tw = fma(tm.T[(a * NQ + bb) * NQ + c], w[c], tw);
+            acc[a] = fma(tw, ub[bb], acc[a]);
+          }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) r[base + a] = b ? b[base + a] - acc[a] : acc[a];
+  }
+}
+
+// ------------------------------------------------------- H4 + H5 block inverse
+// Block value D[(i,a),(j,b)] of D_{p,n} = R_p A_nn R_p^T (R9) for sids si, sj.
+template <int NQ>
+__device__ __forceinline__ double block_entry(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                                              const double *__restrict__ Mv, const double *__restrict__ KGv,
+                                              int64_t nvrow, const int32_t *__restrict__ vvptr,
+                                              const double *__restrict__ conv, int64_t NT, int n, const NSTime &tm,
+                                              int si, int sj, int a, int bb) {
+  const int pos = csr_find_ns(rowptr, col, si, sj);
+  if (pos < 0) return 0.0;
+  double v = tm.CE[a * NQ + bb] * Mv[pos] + tm.Mt[a * NQ + bb] * KGv[pos];
+  if (si < nvrow) {
+    const int ev = pos - rowptr[si];
+    if (ev < vvptr[si + 1] - vvptr[si]) {
+      const double *cv = conv + (int64_t)(vvptr[si] + ev) * NT + (int64_t)n * NQ;
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) v = fma(tm.T[(a * NQ + bb) * NQ + c], cv[c], v);
+    }
+  }
+  return v;
+}
+
+// In-place Gauss-Jordan inverse of the row-major m x m matrix A in shared memory
+// with partial pivoting (first maximum |a| at or below the diagonal: the pivot rows
+// LAPACK dgetrf picks, R10).  Returns 0 or 1 + first column with |pivot| < tol.
+__device__ int gj_invert_smem(double *A, int m, double tol, double *f, int *piv) {
+  __shared__ double s_val[32];
+  __shared__ int s_idx[32];
+  __shared__ double s_pv;
+  __shared__ int s_p, s_info;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  if (tid == 0) s_info = 0;
+  for (int c = 0; c < m; ++c) {
+    double bv = -1.0;
+    int bi = m;
+    for (int r = c + tid; r < m; r += nth) {
+      const double v = fabs(A[r * m + c]);
+      if (v > bv) {
+        bv = v;
+        bi = r;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_val[wid] = bv;
+      s_idx[wid] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double v = s_val[0];
+      int ix = s_idx[0];
+      for (int w = 1; w < nw; ++w)
+        if (s_val[w] > v || (s_val[w] == v && s_idx[w] < ix)) {
+          v = s_val[w];
+          ix = s_idx[w];
+        }
+      piv[c] = ix;
+      s_p = ix;
+      s_pv = A[ix * m + c];
+      if (!(v >= tol) && s_info == 0) s_info = c + 1;
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double pinv = s_pv != 0.0 ? 1.0 / s_pv : 0.0;
+    for (int j = tid; j < m; j += nth) {
+      const double t1 = A[c * m + j], t2 = A[p * m + j];
+      A[p * m + j] = t1;
+      A[c * m + j] = (j == c) ? pinv : t2 * pinv;
+    }
+    __syncthreads();
+    for (int r = tid; r < m; r += nth) f[r] = (r == c) ? 0.0 : A[r * m + c];
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nth) {
+      const int r = e / m, j = e - r * m;
+      if (r == c) continue;
+      if (j == c)
+        A[e] = -f[r] * A[c * m + c];
+      else
+        A[e] = fma(-f[r], A[c * m + j], A[e]);
+    }
+    __syncthreads();
+  }
+  // (P A)^{-1} = A^{-1} P^T: undo the row interchanges as column interchanges, last first
+  for (int c = m - 1; c >= 0; --c) {
+    const int p = piv[c];
+    if (p != c)
+      for (int r = tid; r < m; r += nth) {
+        const double t = A[r * m + c];
+        A[r * m + c] = A[r * m + p];
+        A[r * m + p] = t;
+      }
+    __syncthreads();
+  }
+  return s_info;
+}
+
+// One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
+// DoFs: identity rows), invert, write the row-major inverse to
+// out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
+template <int NQ>
+__global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
+                                                   const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                                                   const double *__restrict__ Mv, const double *__restrict__ KGv,
+                                                   int64_t nvrow, const int32_t *__restrict__ vvptr,
+                                                   const double *__restrict__ conv, NSTime tm,
+                                                   double *__restrict__ out, int32_t *__restrict__ info) {
+  extern __shared__ __align__(16) double smem[];
+  const int m = NQ * mp;
+  double *A = smem, *f = smem + (int64_t)m * m;
+  int *piv = (int *)(f + m);
+  int *nodes = piv + m;
+  __shared__ double s_red[32];
+  const int64_t p = blockIdx.x;
+  const int n = blockIdx.y;
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < mp; i += blockDim.x) nodes[i] = pnodes[p * mp + i];
+  __syncthreads();
+  for (int e = tid; e < m * m; e += blockDim.x) {
+    const int rho = e / m, sig = e - rho * m;  // node-major: rho = i NQ + a
+    const int i = rho / NQ, a = rho - i * NQ, j = sig / NQ, bb = sig - j * NQ;
+    const int si = nodes[i], sj = nodes[j];
+    double v;
+    if (si < 0 || sj < 0)
+      v = (rho == sig) ? 1.0 : 0.0;
+    else
+      v = block_entry<NQ>(rowptr, col, Mv, KGv, nvrow, vvptr, conv, NT, n, tm, si, sj, a, bb);
+    A[e] = v;
+  }
+  __syncthreads();
+  double rn = 0.0;  // max row norm (R10 tolerance)
+  for (int r = tid; r < m; r += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < m; ++c) s += fabs(A[r * m + c]);
+    rn = fmax(rn, s);
+  }
+  for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
+  if ((tid & 31) == 0) s_red[tid >> 5] = rn;
+  __syncthreads();
+  double mx = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
+  const int st = gj_invert_smem(A, m, 1e-14 * mx, f, piv);
+  double *o = out + (p * N + n) * mstride;
+  for (int e = tid; e < m * m; e += blockDim.x) o[e] = A[e];
+  if (tid == 0) info[p * N + n] = st;
+}
+
+// ---------------------------------------------------------------- H7 + H8 sweep
+__device__ __forceinline__ void mbar_init_ns(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait_ns(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// 1D TMA bulk copy global -> shared, completion on the mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+// One CTA per patch; slabs in order.  x_n = D_{p,n}^{-1} (r_{p,n} + [a = 0] M_p x_{n-1}[q]),
+// u += omega W_p x (R11).  STAGED: D^{-1} of slab n+1 is bulk-copied into the other
+// half of a shared double buffer while slab n is solved.
+template <int NQ, bool STAGED>
+__global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
+                                                  const double *__restrict__ wnode, const int32_t *__restrict__ rowptr,
+                                                  const int32_t *__restrict__ col, const double *__restrict__ Mv,
+                                                  const double *__restrict__ Dinv, const double *__restrict__ r,
+                                                  double *__restrict__ u, double omega) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int m = NQ * mp;
+  double *buf = smem;                                   // STAGED: 2 x mstride
+  double *Mp = smem + (STAGED ? 2 * mstride : 0);       // mp x mp velocity mass of the patch
+  double *g = Mp + mp * mp, *x = g + m, *xq = x + m, *wn = xq + mp;
+  int *nodes = (int *)(wn + mp);
+  const int64_t p = blockIdx.x;
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const double *Dp = Dinv + p * N * mstride;
+  const unsigned bytes = (unsigned)(m * m * sizeof(double) + 15) & ~15u;
+  if (STAGED && tid == 0) {
+    mbar_init_ns(&bar[0], 1);
+    mbar_init_ns(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    bulk_load(buf, Dp, bytes, &bar[0]);
+  }
+  for (int i = tid; i < mp; i += blockDim.x) {
+    const int s = pnodes[p * mp + i];
+    nodes[i] = s;
+    wn[i] = s >= 0 ? omega * wnode[s] : 0.0;
+    xq[i] = 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < mp * mp; e += blockDim.x) {
+    const int i = e / mp, j = e - i * mp;
+    double v = 0.0;
+    if (nodes[i] >= 0 && nodes[j] >= 0) {
+      const int pos = csr_find_ns(rowptr, col, nodes[i], nodes[j]);
+      if (pos >= 0) v = Mv[pos];
+    }
+    Mp[e] = v;
+  }
+  __syncthreads();
+  for (int n = 0; n < N; ++n) {
+    if (STAGED && tid == 0 && n + 1 < N) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      bulk_load(buf + ((n + 1) & 1) * mstride, Dp + (int64_t)(n + 1) * mstride, bytes, &bar[(n + 1) & 1]);
+    }
+    for (int rho = tid; rho < m; rho += blockDim.x) {
+      const int i = rho / NQ, a = rho - i * NQ;
+      const int s = nodes[i];
+      double v = 0.0;
+      if (s >= 0) {
+        v = r[(int64_t)s * NT + (int64_t)n * NQ + a];
+        if (a == 0 && n > 0)
+          for (int j = 0; j < mp; ++j) v = fma(Mp[i * mp + j], xq[j], v);
+      }
+      g[rho] = v;
+    }
+    __syncthreads();
+    const double *D;
+    if (STAGED) {
+      mbar_wait_ns(&bar[n & 1], (n >> 1) & 1);
+      D = buf + (n & 1) * mstride;
+    } else {
+      D = Dp + (int64_t)n * mstride;
+    }
+    for (int rho = wid; rho < m; rho += nw) {
+      double acc = 0.0;
+      for (int s2 = lane; s2 < m; s2 += 32) acc = fma(STAGED ? D[rho * m + s2] : __ldg(D + rho * m + s2), g[s2], acc);
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) x[rho] = acc;
+    }
+    __syncthreads();
+    for (int rho = tid; rho < m; rho += blockDim.x) {
+      const int i = rho / NQ, a = rho - i * NQ;
+      const int s = nodes[i];
+      if (s >= 0) atomicAdd(u + (int64_t)s * NT + (int64_t)n * NQ + a, wn[i] * x[rho]);
+      if (a == NQ - 1) xq[i] = x[rho];
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------- H15 projection
+// partial[b][t] = sum of rows [b*rpb, (b+1)*rpb) of the Lp x NT pressure block.
+__global__ void k_colsum(const double *__restrict__ P, int64_t nrow, int64_t NT, int64_t rpb,
+                         double *__restrict__ partial) {
+  const int64_t r0 = blockIdx.x * rpb, r1 = min(nrow, r0 + rpb);
+  for (int64_t t = threadIdx.x; t < NT; t += blockDim.x) {
+    double s = 0.0;
+    for (int64_t rr = r0; rr < r1; ++rr) s += P[rr * NT + t];
+    partial[blockIdx.x * NT + t] = s;
+  }
+}
+__global__ void k_colmean(const double *__restrict__ partial, int nb, int64_t NT, int64_t nrow, double *__restrict__ mean) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < NT; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * NT + t];
+    mean[t] = s / (double)nrow;
+  }
+}
+__global__ void k_colsub(double *__restrict__ P, int64_t nrow, int64_t NT, const double *__restrict__ mean) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= nrow * NT) return;
+  P[idx] -= mean[idx % NT];
+}
+
+// ------------------------------------------------------------------ H11 coarse
+// Column-major block of slab n over the free coarse sids; the rows of the pinned
+// pressure DoF (first pressure node, every temporal node) are identity rows (R19).
+template <int NQ>
+__global__ void k_ns_coarse_blocks(int mc, int N, int pin, const int32_t *__restrict__ cnodes,
+                                   const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                                   const double *__restrict__ Mv, const double *__restrict__ KGv, int64_t nvrow,
+                                   const int32_t *__restrict__ vvptr, const double *__restrict__ conv, NSTime tm,
+                                   double *__restrict__ D) {
+  const int n = blockIdx.y;
+  const int64_t m = (int64_t)NQ * mc, NT = (int64_t)N * NQ;
+  double *Dn = D + (int64_t)n * m * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int sig = (int)(e / m), rho = (int)(e - (int64_t)sig * m);
+    const int i = rho / NQ, a = rho - i * NQ, j = sig / NQ, bb = sig - j * NQ;
+    double v;
+    if (i == pin)
+      v = (rho == sig) ? 1.0 : 0.0;
+    else
+      v = block_entry<NQ>(rowptr, col, Mv, KGv, nvrow, vvptr, conv, NT, n, tm, cnodes[i], cnodes[j], a, bb);
+    Dn[e] = v;
+  }
+}
+
+// Block forward substitution over slabs (one CTA): g = r_n + [a=0] M x_{n-1}[q]
+// (pinned rows 0), x_n = D_n^{-1} g; z receives x on free sids (z pre-zeroed).
+template <int NQ>
+__global__ void __launch_bounds__(1024) k_ns_coarse_solve(int mc, int N, int pin, const int32_t *__restrict__ cnodes,
+                                                          const int32_t *__restrict__ rowptr,
+                                                          const int32_t *__restrict__ col,
+                                                          const double *__restrict__ Mv,
+                                                          const double *__restrict__ DinvT, const double *__restrict__ r,
+                                                          double *__restrict__ z, double *__restrict__ xq) {
+  extern __shared__ double sm[];
+  const int m = NQ * mc;
+  double *g = sm;
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x;
+  for (int n = 0; n < N; ++n) {
+    for (int rho = tid; rho < m; rho += blockDim.x) {
+      const int i = rho / NQ, a = rho - i * NQ;
+      const int s = cnodes[i];
+      double v = 0.0;
+      if (i != pin) {
+        v = r[(int64_t)s * NT + (int64_t)n * NQ + a];
+        if (a == 0 && n > 0)
+          for (int e = rowptr[s]; e < rowptr[s + 1]; ++e) v = fma(Mv[e], xq[col[e]], v);
+      }
+      g[rho] = v;
+    }
+    __syncthreads();
+    const double *Di = DinvT + (int64_t)n * m * m;
+    double xv[2] = {0.0, 0.0};
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int rho = tid + k2 * blockDim.x;
+      if (rho >= m) break;
+      double acc = 0.0;
+      for (int s2 = 0; s2 < m; ++s2) acc = fma(Di[(int64_t)s2 * m + rho], g[s2], acc);
+      xv[k2] = acc;
+    }
+    __syncthreads();  // every thread has read xq of slab n-1 (through g)
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int rho = tid + k2 * blockDim.x;
+      if (rho >= m) break;
+      const int i = rho / NQ, a = rho - i * NQ;
+      const int s = cnodes[i];
+      z[(int64_t)s * NT + (int64_t)n * NQ + a] = xv[k2];
+      if (a == NQ - 1) xq[s] = xv[k2];
+    }
+    __syncthreads();
+  }
+}
+
+// dst = src on free sids; g[s] (or 0) on constrained sids (R5, R6).
+__global__ void k_ns_mask(int64_t ns, int64_t NT, const uint8_t *__restrict__ con, const double *__restrict__ g,
+                          const double *__restrict__ src, double *__restrict__ dst) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= ns * NT) return;
+  const int64_t s = idx / NT;
+  dst[idx] = con[s] ? (g ? g[s] : 0.0) : (src ? src[idx] : 0.0);
+}
+__global__ void k_axpy(int64_t n, double a, const double *__restrict__ x, double *__restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = fma(a, x[i], y[i]);
+}
+
+NSTime make_nstime(const Temporal &T) {
+  NSTime t{};
+  for (int e = 0; e < T.nq * T.nq; ++e) {
+    t.CE[e] = T.CE[e];
+    t.Mt[e] = T.Mt[e];
+  }
+  for (int e = 0; e < T.nq * T.nq * T.nq; ++e) t.T[e] = T.T[e];
+  return t;
+}
+
+template <class F>
+void by_nq(int nq, F f) {
+  switch (nq) {
+    case 1: f(std::integral_constant<int, 1>()); break;
+    case 2: f(std::integral_constant<int, 2>()); break;
+    case 3: f(std::integral_constant<int, 3>()); break;
+    default: f(std::integral_constant<int, 4>()); break;
+  }
+}
+
+}  // namespace
+
+void launch_ns_mask(int64_t ns, int64_t NT, const uint8_t *con, const double *g, const double *src, double *dst,
+                    cudaStream_t s) {
+  const int64_t n = ns * NT;
+  k_ns_mask<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ns, NT, con, g, src, dst);
+  ++g_launches;
+}
+
+void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s) {
+  k_axpy<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, a, x, y);
+  ++g_launches;
+}
+
+size_t ns_factor_smem(int m, int mp) {
+  return ((size_t)m * m + m) * sizeof(double) + (size_t)(m + mp) * sizeof(int) + 16;
+}
+
+size_t ns_sweep_smem(int m, int mp, int64_t mstride, bool staged) {
+  return ((staged ? 2 * mstride : 0) + (int64_t)mp * mp + 2 * m + 2 * mp) * sizeof(double) + mp * sizeof(int) + 16;
+}
+
+void launch_ns_assemble_linear(const NSGeom &g, const DevCSR &A, const double *ref, cudaStream_t s) {
+  k_ns_assemble_linear<<<(unsigned)((g.ns + 127) / 128), 128, 0, s>>>(g, A.rowptr, A.col, A.val, A.val2, ref);
+  ++g_launches;
+}
+
+void launch_ns_assemble_conv(const NSGeom &g, int64_t NT, double R, bool newton, const DevCSR &A, const int32_t *vvptr,
+                             const double *W, double *conv, const double *Th, cudaStream_t s) {
+  const size_t sm = (size_t)2 * g.nu * g.nu * g.nu * sizeof(double);
+  const int64_t n = g.Lu * NT;
+  k_ns_assemble_conv<<<(unsigned)((n + 255) / 256), 256, sm, s>>>(g, NT, R, newton ? 1 : 0, A.rowptr, A.col, vvptr, W,
+                                                                  conv, Th);
+  ++g_launches;
+}
+
+void launch_ns_inject(const NSGeom &c, const NSGeom &f, int64_t NT, const double *Wf, double *Wc, cudaStream_t s) {
+  const int64_t n = c.ns * NT;
+  k_ns_inject<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, f, NT, Wf, Wc);
+  ++g_launches;
+}
+
+void launch_ns_residual(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
+                        const double *conv, const uint8_t *con, const double *u, const double *b, double *r,
+                        cudaStream_t s) {
+  const NSTime tm = make_nstime(T);
+  const unsigned blocks = (unsigned)((g.ns + 7) / 8);
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    k_ns_residual<NQ><<<blocks, 256, 0, s>>>(g.ns, N, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr, conv, con, u,
+                                             b, r, tm);
+  });
+  ++g_launches;
+}
+
+void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
+                      const double *conv, const int32_t *pnodes, int64_t npatch, int mp, int64_t mstride, double *out,
+                      int32_t *info, cudaStream_t s) {
+  const NSTime tm = make_nstime(T);
+  const int m = (q + 1) * mp;
+  const size_t sm = ns_factor_smem(m, mp);
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    cudaFuncSetAttribute(k_ns_factor<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid((unsigned)npatch, (unsigned)N);
+    k_ns_factor<NQ><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
+                                          conv, tm, out, info);
+  });
+  ++g_launches;
+}
+
+void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
+                     const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s) {
+  const int m = (q + 1) * mp;
+  const bool staged = ns_sweep_smem(m, mp, mstride, true) <= 200 * 1024;
+  const size_t sm = ns_sweep_smem(m, mp, mstride, staged);
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    if (staged) {
+      cudaFuncSetAttribute(k_ns_sweep<NQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_ns_sweep<NQ, true><<<(unsigned)npatch, 256, sm, s>>>(mp, N, mstride, pnodes, wnode, A.rowptr, A.col, A.val,
+                                                             Dinv, r, u, omega);
+    } else {
+      cudaFuncSetAttribute(k_ns_sweep<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_ns_sweep<NQ, false><<<(unsigned)npatch, 256, sm, s>>>(mp, N, mstride, pnodes, wnode, A.rowptr, A.col, A.val,
+                                                              Dinv, r, u, omega);
+    }
+  });
+  ++g_launches;
+}
+
+void launch_ns_project(double *P, int64_t nrow, int64_t NT, double *scratch, cudaStream_t s) {
+  // scratch: >= (nb + 1) * NT doubles
+  const int64_t rpb = std::max<int64_t>(16, (nrow + 295) / 296);
+  const int nb = (int)((nrow + rpb - 1) / rpb);
+  double *partial = scratch, *mean = scratch + (int64_t)nb * NT;
+  k_colsum<<<nb, 256, 0, s>>>(P, nrow, NT, rpb, partial);
+  k_colmean<<<(unsigned)((NT + 255) / 256), 256, 0, s>>>(partial, nb, NT, nrow, mean);
+  const int64_t n = nrow * NT;
+  k_colsub<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, nrow, NT, mean);
+  g_launches += 3;
+}
+
+int64_t ns_project_scratch(int64_t nrow, int64_t NT) {
+  const int64_t rpb = std::max<int64_t>(16, (nrow + 295) / 296);
+  return ((nrow + rpb - 1) / rpb + 1) * NT;
+}
+
+void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
+                             const double *conv, const int32_t *cnodes, int mc, int pin, double *D, cudaStream_t s) {
+  const NSTime tm = make_nstime(T);
+  const int64_t m = (int64_t)(q + 1) * mc;
+  dim3 grid((unsigned)std::min<int64_t>((m * m + 255) / 256, 1024), (unsigned)N);
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    k_ns_coarse_blocks<NQ><<<grid, 256, 0, s>>>(mc, N, pin, cnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
+                                                conv, tm, D);
+  });
+  ++g_launches;
+}
+
+void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,
+                            const double *r, double *z, double *xq, int64_t ns, cudaStream_t s) {
+  const int m = (q + 1) * mc;
+  cudaMemsetAsync(z, 0, ns * (int64_t)N * (q + 1) * sizeof(double), s);
+  cudaMemsetAsync(xq, 0, ns * sizeof(double), s);
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    k_ns_coarse_solve<NQ><<<1, 1024, m * sizeof(double), s>>>(mc, N, pin, cnodes, A.rowptr, A.col, A.val, DinvT, r, z,
+                                                              xq);
+  });
+  ++g_launches;
+}
+
+}  // namespace wrmg

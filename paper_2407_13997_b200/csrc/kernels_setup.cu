@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(256) k_batched_lu(double *__restrict__ Aall, i
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
   if (SMEM)
     for (int e = tid; e < m * m; e += nth) A[e] = g[e];
+  __syncthreads();  // the row norms below read rows staged by other threads
   // max row norm
   double rn = 0.0;
   for (int r = tid; r < m; r += nth) {
@@ -322,4 +323,13 @@ void launch_coarse_inverse(Coarse &C, const double *LU, const Level &L, int nq, 
   k_coarse_G<<<blocks, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, C.nodes, C.mp, nq, C.DinvT, C.GT, C.Gq); ++g_launches;
 }
 
+}  // namespace wrmg
+
+namespace wrmg {
+void launch_lu_inverse_batched(const double *LU, const int32_t *piv, int m, int batch, double *out, cudaStream_t s) {
+  if (batch <= 0) return;
+  dim3 grid((m + 127) / 128, batch);
+  k_lu_inverse<false><<<grid, 128, 0, s>>>(LU, piv, m, out);
+  ++g_launches;
+}
 }  // namespace wrmg

@@ -1,0 +1,48 @@
+// Launchers of the Navier-Stokes kernels (kernels_ns.cu).
+#pragma once
+#include <type_traits>
+
+#include "internal.h"
+#include "ns.h"
+
+namespace wrmg {
+
+// Geometry of one Taylor-Hood level, passed by value to kernels.
+struct NSGeom {
+  int nx, ny, ku, kp, Lux, Lpx, nu, np;
+  int64_t Lu, Lp, ns;
+  double h;
+};
+
+struct NSTime {
+  double CE[16], Mt[16], T[64];
+};
+
+size_t ns_factor_smem(int m, int mp);
+size_t ns_sweep_smem(int m, int mp, int64_t mstride, bool staged);
+int64_t ns_project_scratch(int64_t nrow, int64_t NT);
+
+void launch_ns_assemble_linear(const NSGeom &g, const DevCSR &A, const double *ref, cudaStream_t s);
+void launch_ns_assemble_conv(const NSGeom &g, int64_t NT, double R, bool newton, const DevCSR &A, const int32_t *vvptr,
+                             const double *W, double *conv, const double *Th, cudaStream_t s);
+void launch_ns_inject(const NSGeom &c, const NSGeom &f, int64_t NT, const double *Wf, double *Wc, cudaStream_t s);
+void launch_ns_residual(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
+                        const double *conv, const uint8_t *con, const double *u, const double *b, double *r,
+                        cudaStream_t s);
+void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
+                      const double *conv, const int32_t *pnodes, int64_t npatch, int mp, int64_t mstride, double *out,
+                      int32_t *info, cudaStream_t s);
+void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
+                     const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s);
+void launch_ns_project(double *P, int64_t nrow, int64_t NT, double *scratch, cudaStream_t s);
+void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
+                             const double *conv, const int32_t *cnodes, int mc, int pin, double *D, cudaStream_t s);
+void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,
+                            const double *r, double *z, double *xq, int64_t ns, cudaStream_t s);
+void launch_ns_mask(int64_t ns, int64_t NT, const uint8_t *con, const double *g, const double *src, double *dst,
+                    cudaStream_t s);
+void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s);
+// Batched inverse from LU factors (kernels_setup.cu): out[b] = column-major inverse of batch b.
+void launch_lu_inverse_batched(const double *LU, const int32_t *piv, int m, int batch, double *out, cudaStream_t s);
+
+}  // namespace wrmg

@@ -1,0 +1,166 @@
+"""GPU parity of the Navier-Stokes path (Taylor-Hood x DG(q), Newton Jacobian at
+the C3 wind, Vanka+star WR smoother, V-cycle, FGMRES, Newton) against the oracle
+(oracle/ns.py) on the same seeded inputs.  Tolerance: DESIGN.md R23 (1e-10
+relative per vector, identical Krylov / Newton iteration counts)."""
+import numpy as np
+import pytest
+
+import wrmg_inputs as wi
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _dev(x):
+    torch = _torch()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda:0")
+
+
+def _host(t):
+    _torch().cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def assert_parity(gpu, ref, tol=TOL, what=""):
+    gpu, ref = np.asarray(gpu), np.asarray(ref)
+    e2 = np.linalg.norm(gpu - ref) / np.linalg.norm(ref)
+    einf = np.max(np.abs(gpu - ref)) / np.max(np.abs(ref))
+    assert e2 <= tol and einf <= tol, f"{what}: rel2 {e2:.3e} relinf {einf:.3e}"
+    return e2, einf
+
+
+def _setup(n, k, q, N, R=100.0, omega_mg=0.8, bc="lid", wind=True):
+    """GPU context and oracle hierarchy linearised at the C3 wind (R18)."""
+    import paper_2407_13997_b200 as w
+    from oracle import ns
+    dt = 1.0 / N
+    W = wi.wind_state(n, n, 1.0 / n, k, N, q, dt) if wind else None
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc=bc,
+                  omega_mg=omega_mg)
+    if W is not None:
+        c.linearize(_dev(W))
+    H = ns.NSHierarchy(n, n, 1.0 / n, k, q, N, dt, R, W=W, bc=bc, omega_mg=omega_mg)
+    return c, H, W
+
+
+def _rhs(c, p, seed=0):
+    """b of config C3 (R6): U[-1,1) on free rows, 0 on constrained, pressure projected."""
+    f = wi.spacetime_field(p.ns, p.N, p.q, seed)
+    b = c.empty()
+    c.rhs(_dev(f), b)
+    bref = f.copy()
+    bref[p.con_st] = 0.0
+    return b, p.project_pressure(bref)
+
+
+@pytest.mark.parametrize("k,q,N", [(1, 1, 3), (2, 1, 2), (1, 0, 4), (1, 2, 2)])
+def test_ns_apply_matches_jacobian(k, q, N):
+    c, H, W = _setup(8, k, q, N)
+    p = H.fine
+    x = wi.spacetime_field(p.ns, N, q, 7)
+    y = c.empty()
+    c.apply(_dev(x), y)
+    assert_parity(_host(y), H.A[-1] @ x, what="J x")
+    b = wi.spacetime_field(p.ns, N, q, 8)
+    r = c.empty()
+    c.residual(_dev(x), _dev(b), r)
+    assert_parity(_host(r), b - H.A[-1] @ x, what="b - J x")
+    c.close()
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_ns_nonlinear_residual(k):
+    c, H, W = _setup(8, k, 1, 3, wind=False)
+    p = H.fine
+    U = 0.3 * wi.spacetime_field(p.ns, 3, 1, 11)
+    b = np.zeros(p.ndof)
+    b[p.con_st] = p.g_st[p.con_st]
+    r = c.empty()
+    c.residual(_dev(U), _dev(b), r, nonlinear=True)
+    assert_parity(_host(r), -p.residual(U), what="-F(U)")
+    c.close()
+
+
+@pytest.mark.parametrize("k,omega", [(1, 1.0), (2, 0.8)])
+def test_ns_smoother_sweeps(k, omega):
+    from oracle import smoother
+    c, H, W = _setup(8, k, 1, 3)
+    p = H.fine
+    b, bref = _rhs(c, p)
+    assert_parity(_host(b), bref, what="rhs")
+    u = c.zeros()
+    uref = np.zeros(p.ndof)
+    for it in range(3):
+        c.smooth(u, b, 1, omega)
+        uref = p.project_pressure(smoother.wr_sweep(p, H.A[-1], uref, bref, H.factors[-1], omega, H.w[-1]))
+        assert_parity(_host(u), uref, what=f"sweep {it}")
+    c.close()
+
+
+@pytest.mark.parametrize("n,k", [(8, 1), (16, 1), (8, 2)])
+def test_ns_vcycle(n, k):
+    from oracle import ns
+    c, H, W = _setup(n, k, 1, 3)
+    p = H.fine
+    b, bref = _rhs(c, p, seed=3)
+    z = c.empty()
+    c.vcycle(b, z)
+    assert_parity(_host(z), ns.vcycle(H, bref), what="V(1,1)")
+    c.close()
+
+
+def test_ns_one_level_vcycle_is_pinned_coarse_solve():
+    from oracle import ns
+    c, H, W = _setup(4, 1, 1, 3)
+    p = H.fine
+    b, bref = _rhs(c, p, seed=4)
+    z = c.empty()
+    c.vcycle(b, z)
+    zref = ns.vcycle(H, bref)
+    assert_parity(_host(z), zref, what="coarse solve")
+    assert np.linalg.norm(p.project_pressure(bref - H.A[-1] @ zref)) <= 1e-10 * np.linalg.norm(bref)
+    c.close()
+
+
+@pytest.mark.parametrize("n,k,N,R", [(8, 1, 4, 10.0), (16, 1, 4, 20.0), (8, 2, 3, 20.0)])
+def test_ns_fgmres_iteration_count(n, k, N, R):
+    """Cell Reynolds numbers R |w| h <= 6 (C3 itself: 100 * 4.7 / 64 = 7.4); at
+    R |w| h ~ 30 the additive Vanka V(1,1) no longer contracts (oracle and GPU
+    alike), so no iteration count would be compared."""
+    from oracle import krylov, ns
+    c, H, W = _setup(n, k, 1, N, R=R)
+    p = H.fine
+    b, bref = _rhs(c, p, seed=0)
+    x = c.empty()
+    its, rel, st = c.fgmres(b, x, restart=30, maxit=200, rtol=1e-8)
+    xref, its_ref, hist, st_ref = krylov.fgmres(lambda v: H.A[-1] @ v, lambda r: ns.vcycle(H, r), bref,
+                                                restart=30, maxit=200, rtol=1e-8)
+    assert st == "WRMG_OK" and st_ref == "converged"
+    assert its == its_ref
+    assert_parity(_host(x), xref, tol=1e-9, what="FGMRES iterate")
+    c.close()
+
+
+def test_ns_newton_cavity():
+    """Newton-FGMRES-WRMG (R22) on a small lid-driven cavity:
+    identical Newton and linear iteration counts, solution within 1e-8."""
+    from oracle import ns
+    n, k, q, N, dt, R = 8, 1, 1, 3, 0.05, 10.0
+    import paper_2407_13997_b200 as w
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
+                  omega_mg=0.8)
+    H = ns.NSHierarchy(n, n, 1.0 / n, k, q, N, dt, R, bc="lid", omega_mg=0.8)
+    Uref, hist, lin = ns.newton(H, rtol=1e-8, maxit=12)
+    U = c.zeros()
+    its, lin_its, st = c.newton(U, rtol=1e-8, maxit=12)
+    assert st == "WRMG_OK"
+    assert its == len(lin) and lin_its == sum(lin)
+    assert_parity(_host(U), Uref, tol=1e-8, what="Newton solution")
+    c.close()

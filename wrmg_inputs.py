@@ -37,3 +37,25 @@ def spacetime_field(nnode, N, q, seed=0, node_offset=0):
     nt = N * (q + 1)
     ids = np.arange(nnode * nt, dtype=np.uint64) + np.uint64(node_offset * nt)
     return uniform_pm1(ids, seed)
+
+
+def wind_state(nx, ny, h, k, N, q, dt):
+    """Linearisation state of config C3 (BASELINE.json configs[2]; R18):
+    the nodal values of w = curl psi = (d_y psi, -d_x psi),
+    psi = a(t) sin^2(pi x) sin^2(pi y), a(t) = 1 + sin(2 pi t) / 2, at every
+    P_{k+1} velocity node and every DG(q) temporal node t = (n + a/q) dt (R2;
+    t = n dt for q = 0); pressure 0.  Waveform-major over sids (u_x, u_y, p)."""
+    ku, kp = k + 1, k
+    Lux, Luy = ku * nx + 1, ku * ny + 1
+    Lp = (kp * nx + 1) * (kp * ny + 1)
+    I, J = np.meshgrid(np.arange(Lux), np.arange(Luy), indexing="xy")
+    x, y = I.ravel() * h / ku, J.ravel() * h / ku
+    tau = np.array([0.0]) if q == 0 else np.arange(q + 1) / q
+    t = ((np.arange(N)[:, None] + tau[None, :]) * dt).ravel()  # (N (q+1),)
+    amp = 1.0 + 0.5 * np.sin(2 * np.pi * t)
+    wx = np.pi * np.sin(np.pi * x) ** 2 * np.sin(2 * np.pi * y)
+    wy = -np.pi * np.sin(2 * np.pi * x) * np.sin(np.pi * y) ** 2
+    out = np.zeros((2 * Lux * Luy + Lp, t.size))
+    out[:Lux * Luy] = np.outer(wx, amp)
+    out[Lux * Luy:2 * Lux * Luy] = np.outer(wy, amp)
+    return out.ravel()
