@@ -258,6 +258,112 @@ def run_c5(args, ws, rank, local):
     ctx.close()
 
 
+def run_c3(args, ws, rank, local):
+    """BASELINE configs[2] (C3): Oseen = one Newton linearisation of Navier-Stokes
+    (R18) at the wind w = curl psi, P2-P1 Taylor-Hood x DG1, 64x64, N = 64, T = 1
+    (R21), Re = 100, lid BCs, b ~ U[-1,1) on free rows (R6); omega_mg = 0.8
+    (R-omega-NS).  One step = the C3 protocol of SURVEY 8(d) with fixed work:
+    10 smoother sweeps (omega = 1), one V(1,1) on the residual, and one FGMRES(30)
+    restart cycle (30 preconditioned iterations); the additive Vanka V(1,1) does not
+    contract on this wind at Re = 100 (NS findings; the oracle agrees), so
+    a solve-to-tolerance step would not terminate.  The linearisation (assembly +
+    batched block inversion, H1/H4/H5) is timed apart."""
+    import numpy as np
+    import torch
+
+    import paper_2407_13997_b200 as w
+    import wrmg_inputs as wi
+    torch.cuda.set_device(local)
+    n, k, q, N, R, T = 64, 1, 1, 64, 100.0, 1.0
+    dt = T / N
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
+                    omega_mg=0.8, device=local, stream=stream.cuda_stream)
+    setup_s = time.time() - t0
+    lay = ctx.layout
+    W = torch.as_tensor(wi.wind_state(n, n, 1.0 / n, k, N, q, dt), device=f"cuda:{local}")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ctx.linearize(W)  # warm
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    ctx.linearize(W)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    lin_ms = ev[0].elapsed_time(ev[1])
+    f = ctx.empty()
+    ctx.fill_uniform(f, 0, 0)
+    b = ctx.empty()
+    ctx.rhs(f, b)
+    x = ctx.empty()
+    u, r, z = ctx.empty(), ctx.empty(), ctx.empty()
+    upd_vc = lay["smooth_dof_updates_per_vcycle"]
+    upd_sweep = lay["nfree_st"]
+
+    def solve():
+        u.zero_()
+        ctx.smooth(u, b, 10, 1.0)
+        ctx.residual(u, b, r)
+        ctx.vcycle(r, z)
+        its, rel, st = ctx.fgmres(b, x, restart=30, maxit=30, rtol=1e-8)
+        return its, rel, st
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ctx.profile(True)
+    l0 = w.launch_count()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    tot, its_l, st_l = 0, [], []
+    for _ in range(args.steps):
+        its, rel, st = solve()
+        tot += 10 * upd_sweep + (1 + its) * upd_vc
+        its_l.append(its)
+        st_l.append((st, rel))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    stats = ctx.kernel_stats()
+    ctx.profile(False)
+    clk = clocks.stop()
+    z = ctx.empty()
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev2[0].record(stream)
+    for _ in range(5):
+        ctx.vcycle(b, z)
+    ev2[1].record(stream)
+    u = ctx.zeros()
+    ev2[2].record(stream)
+    for _ in range(5):
+        ctx.smooth(u, b, 1, 1.0)
+    ev2[3].record(stream)
+    torch.cuda.synchronize()
+    per_kernel = {f"{a}@L{l}": {"launches": s["launches"], "ms": round(s["ms"], 3),
+                                "GBs": round(s["bytes"] / (s["ms"] / 1e3) / 1e9, 1) if s["ms"] > 0 else None,
+                                "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}
+                  for (a, l), s in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+    line = {"metric": METRIC, "value": ws * tot / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3 = BASELINE configs[2]: Oseen (Newton Jacobian at w = curl psi), P2-P1 x DG1, "
+                                   "64x64, N=64, T=1, Re=100, lid; step = 10 sweeps + V(1,1) + 30 FGMRES(30) "
+                                   "iterations, omega_mg 0.8",
+                       "ndof": lay["ndof"], "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
+                       "npatch": lay["npatch"], "mp_max": lay["mp_max"], "setup_s": round(setup_s, 2)},
+            "fgmres_iterations": its_l[0], "fgmres_status_relres": st_l[0], "linearize_ms": lin_ms,
+            "vcycle_ms": ev2[0].elapsed_time(ev2[1]) / 5, "smoother_sweep_ms": ev2[2].elapsed_time(ev2[3]) / 5,
+            "per_kernel": per_kernel, "clocks": clk, "gpu_launches": w.launch_count() - l0}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
 def run_gpu(args, ws, rank, local):
     import torch
 
@@ -408,7 +514,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wrmg", choices=["wrmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C2", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C5"])
     args = ap.parse_args()
     ws, rank, local = dist_setup(args) if args.impl == "wrmg" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
@@ -417,6 +523,8 @@ def main():
         return
     if args.config == "C5":
         run_c5(args, ws, rank, local)
+    elif args.config == "C3":
+        run_c3(args, ws, rank, local)
     else:
         run_gpu(args, ws, rank, local)
     if ws > 1:

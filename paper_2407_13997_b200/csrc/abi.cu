@@ -414,6 +414,9 @@ void setup_ns(wrmg_ctx *c) {
     for (int32_t ps : P.psize) fl += 2.0 * ((double)c->nq * ps) * ((double)c->nq * ps) + 2.0 * (double)ps * ps;
     c->sweep_flops.push_back(fl * c->N);
     const int64_t m = (int64_t)c->nq * L.mp;
+    if (m > 256 || ns_factor_smem((int)m, L.mp) > 227 * 1024)
+      throw Err{WRMG_E_UNSUPPORTED, "Vanka patch system of size " + std::to_string(m) +
+                                        " exceeds one CTA (shared-memory block inverse): lower q or degree"};
     L.mstride = (m * m + 1) & ~(int64_t)1;
     if (l >= 1 || nl == 1) {
       L.nsinv = dalloc<double>((size_t)L.npatch * c->N * L.mstride);

@@ -13,6 +13,8 @@
 //   H11 coarse blocks with the pinned pressure DoF (R19) and the time-marching solve;
 //   H15 pressure mean projection per (slab, temporal node) (R19);
 //   state injection to coarse levels (R13).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cfloat>
 
@@ -470,22 +472,25 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
     Mp[e] = v;
   }
   __syncthreads();
+  // thread rho < m owns row rho of the patch system (m <= blockDim, checked by the launcher);
+  // the r gather of slab n+1 is issued while slab n is solved
+  const int i_me = tid / NQ, a_me = tid - (tid / NQ) * NQ;
+  const bool own = tid < m && nodes[i_me < mp ? i_me : 0] >= 0 && i_me < mp;
+  const int64_t rbase = own ? (int64_t)nodes[i_me] * NT + a_me : 0;
+  double rcur = own ? __ldg(r + rbase) : 0.0;
   for (int n = 0; n < N; ++n) {
     if (STAGED && tid == 0 && n + 1 < N) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       bulk_load(buf + ((n + 1) & 1) * mstride, Dp + (int64_t)(n + 1) * mstride, bytes, &bar[(n + 1) & 1]);
     }
-    for (int rho = tid; rho < m; rho += blockDim.x) {
-      const int i = rho / NQ, a = rho - i * NQ;
-      const int s = nodes[i];
-      double v = 0.0;
-      if (s >= 0) {
-        v = r[(int64_t)s * NT + (int64_t)n * NQ + a];
-        if (a == 0 && n > 0)
-          for (int j = 0; j < mp; ++j) v = fma(Mp[i * mp + j], xq[j], v);
-      }
-      g[rho] = v;
+    const double rnext = (own && n + 1 < N) ? __ldg(r + rbase + (int64_t)(n + 1) * NQ) : 0.0;
+    if (tid < m) {
+      double v = rcur;
+      if (own && a_me == 0 && n > 0)  // jump: M_p x_{n-1}[q] (x still holds slab n-1)
+        for (int j = 0; j < mp; ++j) v = fma(Mp[i_me * mp + j], x[j * NQ + NQ - 1], v);
+      g[tid] = v;
     }
+    rcur = rnext;
     __syncthreads();
     const double *D;
     if (STAGED) {
@@ -501,13 +506,7 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
       if (lane == 0) x[rho] = acc;
     }
     __syncthreads();
-    for (int rho = tid; rho < m; rho += blockDim.x) {
-      const int i = rho / NQ, a = rho - i * NQ;
-      const int s = nodes[i];
-      if (s >= 0) atomicAdd(u + (int64_t)s * NT + (int64_t)n * NQ + a, wn[i] * x[rho]);
-      if (a == NQ - 1) xq[i] = x[rho];
-    }
-    __syncthreads();
+    if (own) atomicAdd(u + rbase + (int64_t)n * NQ, wn[i_me] * x[tid]);
   }
 }
 
@@ -605,6 +604,82 @@ __global__ void __launch_bounds__(1024) k_ns_coarse_solve(int mc, int N, int pin
       if (a == NQ - 1) xq[s] = xv[k2];
     }
     __syncthreads();
+  }
+}
+
+// Cluster variant: CS CTAs share the slab loop; CTA c owns rows [c RB, (c+1) RB)
+// of every D_n^{-1} (RB = ceil(m / CS)), every CTA forms the full g (the jump needs
+// the whole end trace, kept per sid in each CTA's shared memory and broadcast
+// through distributed shared memory), one cluster barrier per slab.
+template <int NQ, int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256)
+    k_ns_coarse_cluster(int mc, int N, int pin, int64_t ns, const int32_t *__restrict__ cnodes,
+                        const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                        const double *__restrict__ Mv, const double *__restrict__ DinvT,
+                        const double *__restrict__ r, double *__restrict__ z) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double sm[];
+  const int m = NQ * mc;
+  // xq: end trace per sid, double-buffered by slab parity (a CTA may publish slab n
+  // while another still reads slab n-1 for its g); 0 on constrained sids
+  double *g = sm, *xqb = sm + m;
+  __shared__ double part[8][33];
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x, rl = tid & 31, grp = tid >> 5;
+  const int rank = (int)cluster.block_rank();
+  const int RB = (m + CS - 1) / CS, r0 = rank * RB, r1 = min(m, r0 + RB);
+  for (int64_t s = tid; s < 2 * ns; s += blockDim.x) xqb[s] = 0.0;
+  cluster.sync();
+  for (int n = 0; n < N; ++n) {
+    const double *xq = xqb + ((n + 1) & 1) * ns;  // slab n-1
+    double *xo = xqb + (n & 1) * ns;              // slab n
+    for (int rho = tid; rho < m; rho += blockDim.x) {
+      const int i = rho / NQ, a = rho - i * NQ;
+      const int s = cnodes[i];
+      double v = 0.0;
+      if (i != pin) {
+        v = r[(int64_t)s * NT + (int64_t)n * NQ + a];
+        if (a == 0 && n > 0)
+          for (int e = rowptr[s]; e < rowptr[s + 1]; ++e) v = fma(Mv[e], xq[col[e]], v);
+      }
+      g[rho] = v;
+    }
+    __syncthreads();
+    const double *Di = DinvT + (int64_t)n * m * m;
+    for (int rb = r0; rb < r1; rb += 32) {
+      const int rho = rb + rl;
+      double acc = 0.0;
+      if (rho < r1) {
+        // 8 independent loads in flight per thread (the slab loop is latency-bound)
+        double a8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int s2 = grp;
+        for (; s2 + 56 < m; s2 += 64) {
+          double v[8];
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2) v[u2] = __ldg(Di + (int64_t)(s2 + 8 * u2) * m + rho);
+#pragma unroll
+          for (int u2 = 0; u2 < 8; ++u2) a8[u2] = fma(v[u2], g[s2 + 8 * u2], a8[u2]);
+        }
+        for (; s2 < m; s2 += 8) a8[0] = fma(__ldg(Di + (int64_t)s2 * m + rho), g[s2], a8[0]);
+#pragma unroll
+        for (int u2 = 0; u2 < 8; ++u2) acc += a8[u2];
+      }
+      part[grp][rl] = acc;
+      __syncthreads();
+      if (grp == 0 && rho < r1) {
+        double x = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) x += part[k2][rl];
+        const int i = rho / NQ, a = rho - i * NQ;
+        const int s = cnodes[i];
+        z[(int64_t)s * NT + (int64_t)n * NQ + a] = x;
+        if (a == NQ - 1)
+          for (int c = 0; c < CS; ++c) *cluster.map_shared_rank(xo + s, c) = x;
+      }
+      __syncthreads();
+    }
+    cluster.sync();
   }
 }
 
@@ -715,6 +790,7 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
 void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
                      const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s) {
   const int m = (q + 1) * mp;
+  // m <= 256 (one thread per patch row) is enforced by setup_ns
   const bool staged = ns_sweep_smem(m, mp, mstride, true) <= 200 * 1024;
   const size_t sm = ns_sweep_smem(m, mp, mstride, staged);
   by_nq(q + 1, [&](auto NQc) {
@@ -767,10 +843,16 @@ void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes
   const int m = (q + 1) * mc;
   cudaMemsetAsync(z, 0, ns * (int64_t)N * (q + 1) * sizeof(double), s);
   cudaMemsetAsync(xq, 0, ns * sizeof(double), s);
+  const size_t sm = (m + 2 * ns) * sizeof(double);
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
-    k_ns_coarse_solve<NQ><<<1, 1024, m * sizeof(double), s>>>(mc, N, pin, cnodes, A.rowptr, A.col, A.val, DinvT, r, z,
-                                                              xq);
+    if (sm <= 200 * 1024) {
+      cudaFuncSetAttribute(k_ns_coarse_cluster<NQ, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_ns_coarse_cluster<NQ, 8><<<8, 256, sm, s>>>(mc, N, pin, ns, cnodes, A.rowptr, A.col, A.val, DinvT, r, z);
+    } else {
+      k_ns_coarse_solve<NQ><<<1, 1024, m * sizeof(double), s>>>(mc, N, pin, cnodes, A.rowptr, A.col, A.val, DinvT, r,
+                                                                z, xq);
+    }
   });
   ++g_launches;
 }

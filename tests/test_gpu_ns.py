@@ -36,11 +36,11 @@ def assert_parity(gpu, ref, tol=TOL, what=""):
     return e2, einf
 
 
-def _setup(n, k, q, N, R=100.0, omega_mg=0.8, bc="lid", wind=True):
+def _setup(n, k, q, N, R=100.0, omega_mg=0.8, bc="lid", wind=True, T=1.0):
     """GPU context and oracle hierarchy linearised at the C3 wind (R18)."""
     import paper_2407_13997_b200 as w
     from oracle import ns
-    dt = 1.0 / N
+    dt = T / N
     W = wi.wind_state(n, n, 1.0 / n, k, N, q, dt) if wind else None
     c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc=bc,
                   omega_mg=omega_mg)
@@ -104,10 +104,10 @@ def test_ns_smoother_sweeps(k, omega):
     c.close()
 
 
-@pytest.mark.parametrize("n,k", [(8, 1), (16, 1), (8, 2)])
-def test_ns_vcycle(n, k):
+@pytest.mark.parametrize("n,k,N", [(8, 1, 3), (16, 1, 3), (8, 2, 3), (8, 1, 70)])
+def test_ns_vcycle(n, k, N):
     from oracle import ns
-    c, H, W = _setup(n, k, 1, 3)
+    c, H, W = _setup(n, k, 1, N, T=0.02 * N / 64)
     p = H.fine
     b, bref = _rhs(c, p, seed=3)
     z = c.empty()
@@ -129,13 +129,14 @@ def test_ns_one_level_vcycle_is_pinned_coarse_solve():
     c.close()
 
 
-@pytest.mark.parametrize("n,k,N,R", [(8, 1, 4, 10.0), (16, 1, 4, 20.0), (8, 2, 3, 20.0)])
-def test_ns_fgmres_iteration_count(n, k, N, R):
+@pytest.mark.parametrize("n,k,N,R,T", [(8, 1, 4, 10.0, 1.0), (16, 1, 4, 20.0, 1.0), (8, 2, 3, 20.0, 1.0),
+                                       (16, 1, 40, 10.0, 0.02 * 40 / 64)])
+def test_ns_fgmres_iteration_count(n, k, N, R, T):
     """Cell Reynolds numbers R |w| h <= 6 (C3 itself: 100 * 4.7 / 64 = 7.4); at
     R |w| h ~ 30 the additive Vanka V(1,1) no longer contracts (oracle and GPU
     alike), so no iteration count would be compared."""
     from oracle import krylov, ns
-    c, H, W = _setup(n, k, 1, N, R=R)
+    c, H, W = _setup(n, k, 1, N, R=R, T=T)
     p = H.fine
     b, bref = _rhs(c, p, seed=0)
     x = c.empty()
