@@ -405,8 +405,11 @@ __global__ void __launch_bounds__(256, 2) k_sweep_kron_mma(int N, int ld, int ng
   constexpr int KF = (MP + 3) / 4;  // k-steps of 4 over nodes (fwd) and modes (bwd)
   constexpr int P8 = 8 * MT;        // padded modes / nodes
   constexpr int K4 = 4 * KF;        // rows of the gathered tile (nodes) and of W (modes)
-  constexpr int LDV = P8 + 1;
-  constexpr int LDG = 34;           // 32 (slab, a) columns + pad, 16-byte aligned rows
+  // Padding chosen for conflict-free 64-bit fragment loads (a half-warp reads rows
+  // q4 = 0..3 x columns g8 = 0..3): row strides = 4 or 12 (mod 16) doubles put the
+  // four rows in disjoint bank groups.
+  constexpr int LDV = P8 + 4;
+  constexpr int LDG = 36;           // 32 (slab, a) columns + pad, 16-byte aligned rows
   constexpr int WPC = 8;            // warps (patches) per CTA
   extern __shared__ __align__(16) double sm[];
   double *sV = sm;                     // P8 x LDV: V[node][mode], zero padded
@@ -573,7 +576,7 @@ template <int MP>
 void sweep_kron_mma_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
   constexpr int P8 = 8 * ((MP + 7) / 8);
   constexpr int K4 = 4 * ((MP + 3) / 4);
-  const size_t smem = (size_t)(P8 * (P8 + 1) + P8 * 4 + 4 * P8 + 8 * 2 * K4 * 34) * sizeof(double);
+  const size_t smem = (size_t)(P8 * (P8 + 4) + P8 * 4 + 4 * P8 + 8 * 2 * K4 * 36) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sweep_kron_mma<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
