@@ -14,7 +14,7 @@ build/%.o: paper_2407_13997_b200/csrc/%.cu $(HDR)
 	$(NVCC) $(ARCH) $(FLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(OUT): $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -ldl
 
 clean:
 	rm -rf build $(OUT)

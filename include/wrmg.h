@@ -74,8 +74,11 @@ typedef struct {
                            1 LU: per-class LU factors (H5) applied by the split-form sweep */
   int32_t device;       /* CUDA device ordinal */
   void *stream;         /* cudaStream_t; NULL = default stream */
-  int32_t rank, nranks; /* strip partition (nranks = 1 in this build) */
-  const void *nccl_unique_id; /* reserved */
+  int32_t rank, nranks; /* strip partition across ranks (heat): rank r of nranks
+                           owns cell columns [mesh.x0, mesh.x0 + mesh.nx) with x0 = r * nx, nx * nranks = gnx */
+  const void *nccl_unique_id; /* nranks > 1: 128-byte ncclUniqueId from wrmg_nccl_unique_id on rank 0 */
+  void *loopback_hub;   /* nranks > 1 without NCCL: hub of wrmg_loopback_create, ranks = host threads of one
+                           process sharing one device (tests); NULL = NCCL */
 } wrmg_coeffs;
 
 typedef struct {
@@ -89,7 +92,11 @@ typedef struct {
   int64_t npatch;       /* finest-level patches (R8) */
   int32_t mp_max;       /* largest spatial patch size */
   int32_t npatch_types; /* distinct finest-level patch blocks factored (translation classes) */
-  int64_t smooth_dof_updates_per_vcycle; /* sum over levels >= 1 of free space-time DoFs x (nu_pre + nu_post) */
+  int64_t smooth_dof_updates_per_vcycle; /* sum over levels >= 1 of free space-time DoFs x (nu_pre + nu_post)
+                                            (owned DoFs on a strip) */
+  int32_t own0, own1;   /* owned lattice columns [own0, own1] of the local lattice (0, lx-1 on one rank) */
+  int32_t g0;           /* global lattice column of local column 0 */
+  int64_t nfree_owned_st; /* free space-time DoFs owned by this rank */
 } wrmg_layout_t;
 
 /* Build the hierarchy on the device.  PAPER.md:351-360 (space-only coarsening),
@@ -114,7 +121,9 @@ wrmg_status wrmg_linearize(wrmg_ctx *ctx, const double *state);
 wrmg_status wrmg_rhs(wrmg_ctx *ctx, const double *fhat, double *b);
 
 /* r = b - A u on the finest level (H6; eq. heatfem; constrained rows r = b - u).
- * `nonlinear` is reserved (0).  r may not alias u or b. */
+ * `nonlinear` (Navier-Stokes): r = b - F(u).  r may not alias u or b.
+ * Strips (nranks > 1): rows of owned columns are valid; the ghost columns of u
+ * are refreshed from the neighbours first (u is written there). */
 wrmg_status wrmg_residual(wrmg_ctx *ctx, const double *u, const double *b, double *r, int32_t nonlinear);
 
 /* y = A x (Krylov matvec; constrained rows y = x). */
@@ -127,7 +136,10 @@ wrmg_status wrmg_apply(wrmg_ctx *ctx, const double *x, double *y);
 wrmg_status wrmg_smooth(wrmg_ctx *ctx, double *u, const double *b, int32_t nsweeps, double omega);
 
 /* z = B r: one V(nu_pre, nu_post) cycle from a zero initial guess (H9-H12;
- * PAPER.md:361-366).  r must vanish on constrained rows (corrections, R5). */
+ * PAPER.md:361-366).  r must vanish on constrained rows (corrections, R5).
+ * Strips: r is read on owned columns (its ghost columns are overwritten); z is
+ * valid on owned and ghost columns; the coarsest level is solved replicated
+ * after an all-gather. */
 wrmg_status wrmg_vcycle(wrmg_ctx *ctx, const double *r, double *z);
 
 /* Restriction / prolongation between finest-level `level` (>= 1, counted from the
@@ -139,7 +151,7 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *ctx, int32_t level, const double *e_coars
 wrmg_status wrmg_level_size(const wrmg_ctx *ctx, int32_t level, int64_t *nnode);
 
 /* Right-preconditioned FGMRES(restart) with CGS2, x0 = 0 (H13; PAPER.md:361-366,
- * R16).  Stops when |g_{j+1}| <= max(rtol ||b||, atol).  x receives the iterate,
+ * R16).  Single rank only (strips: WRMG_E_UNSUPPORTED).  Stops when |g_{j+1}| <= max(rtol ||b||, atol).  x receives the iterate,
  * *iters the number of preconditioner applications, *relres the final true
  * relative residual ||b - A x|| / ||b||.  Synchronises every Arnoldi step.
  * Returns WRMG_OK, WRMG_E_BREAKDOWN or WRMG_E_NOT_CONVERGED (x still valid). */
@@ -200,6 +212,15 @@ wrmg_status wrmg_kernel_stats(wrmg_ctx *ctx, wrmg_kernel_stat *out);
  * Synchronises.  WRMG_E_INVALID if the array is absent or shorter than count. */
 wrmg_status wrmg_debug_fetch(wrmg_ctx *ctx, int32_t level, int32_t which, void *host_dst, int64_t count);
 
+/* Strip partition transports.  wrmg_nccl_unique_id writes a 128-byte NCCL unique
+ * id (call on rank 0, broadcast, pass as coeffs.nccl_unique_id on every rank).
+ * wrmg_loopback_create makes an in-process hub for nranks contexts driven by
+ * nranks host threads on one device (halo hand-over by host barrier + device
+ * copies); destroy it after every context using it. */
+wrmg_status wrmg_nccl_unique_id(void *out128);
+wrmg_status wrmg_loopback_create(int32_t nranks, void **hub);
+void wrmg_loopback_destroy(void *hub);
+
 /* Number of kernels this library has launched in the process so far. */
 int64_t wrmg_launch_count(void);
 
@@ -212,6 +233,15 @@ wrmg_status wrmg_plan(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t 
  * mp_max int32 canonical node ids (-1 padded), sizes npatch int32 sizes; either
  * may be NULL.  Buffers are host memory owned by the caller. */
 wrmg_status wrmg_plan_patches(const wrmg_mesh *mesh, int32_t degree, int32_t *nodes, int32_t *sizes);
+
+/* Host-only: the strip plan of one rank (mesh->x0, mesh->nx
+ * its cell columns).  info[16] = {G0, own0, own1, lg0, nlg, rg0, nrg, sl0, nsl,
+ * sr0, nsr, Lx, Ly, cx0, nxl, 0}: global column of local column 0, owned local
+ * columns, left / right ghost columns, columns sent left / right, local lattice
+ * size, local cells.  patch_vertex (may be NULL) receives the global vertex id
+ * J (gnx + 1) + I of each owned patch, *npatch their count. */
+wrmg_status wrmg_plan_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank, int32_t nranks, int32_t *info,
+                            int32_t *patch_vertex, int64_t *npatch);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,8 @@ CPU fallback: if the shared library is missing the import fails.
 from ._lib import (  # noqa: F401
     LIB_PATH,
     Context,
+    LoopbackHub,
+    nccl_unique_id,
     WrmgError,
     exported_symbols,
     launch_count,
@@ -16,4 +18,5 @@ from ._lib import (  # noqa: F401
     wrmg_fill_uniform,
     wrmg_plan,
     wrmg_plan_patches,
+    wrmg_plan_strip,
 )

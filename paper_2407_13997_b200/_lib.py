@@ -24,14 +24,15 @@ class wrmg_coeffs(ctypes.Structure):
     _fields_ = [("problem", c_i32), ("bc", c_i32), ("kappa", c_dbl), ("reynolds", c_dbl), ("lid_speed", c_dbl),
                 ("weights", c_i32), ("omega_mg", c_dbl), ("nu_pre", c_i32), ("nu_post", c_i32),
                 ("factor_mode", c_i32), ("device", c_i32), ("stream", c_vp), ("rank", c_i32), ("nranks", c_i32),
-                ("nccl_unique_id", c_vp)]
+                ("nccl_unique_id", c_vp), ("loopback_hub", c_vp)]
 
 
 class wrmg_layout_t(ctypes.Structure):
     _fields_ = [("nnode", c_i64), ("nt", c_i64), ("ndof", c_i64), ("nfree_st", c_i64), ("lx", c_i32),
                 ("ly", c_i32), ("nlevels", c_i32), ("degree", c_i32), ("q", c_i32), ("nslabs", c_i32),
                 ("npatch", c_i64), ("mp_max", c_i32), ("npatch_types", c_i32),
-                ("smooth_dof_updates_per_vcycle", c_i64)]
+                ("smooth_dof_updates_per_vcycle", c_i64), ("own0", c_i32), ("own1", c_i32), ("g0", c_i32),
+                ("nfree_owned_st", c_i64)]
 
 
 class wrmg_kernel_stat(ctypes.Structure):
@@ -66,6 +67,10 @@ _sig = {
     "wrmg_kernel_stats": (c_i32, [c_vp, c_vp]),
     "wrmg_launch_count": (c_i64, []),
     "wrmg_debug_fetch": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64]),
+    "wrmg_nccl_unique_id": (c_i32, [c_vp]),
+    "wrmg_plan_strip": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, c_vp, c_vp, _P(c_i64)]),
+    "wrmg_loopback_create": (c_i32, [c_i32, _P(c_vp)]),
+    "wrmg_loopback_destroy": (None, [c_vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(lib, _name)
@@ -104,8 +109,48 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _mesh(nx, ny, h, ncoarse):
-    return wrmg_mesh(int(nx), int(ny), 0, int(nx), float(h), int(ncoarse))
+def _mesh(nx, ny, h, ncoarse, x0=0, snx=None):
+    return wrmg_mesh(int(nx), int(ny), int(x0), int(nx if snx is None else snx), float(h), int(ncoarse))
+
+
+STRIP_INFO = ["G0", "own0", "own1", "lg0", "nlg", "rg0", "nrg", "sl0", "nsl", "sr0", "nsr", "Lx", "Ly", "cx0", "nxl"]
+
+
+def wrmg_plan_strip(gnx, gny, h, degree, rank, nranks):
+    """Host-only strip plan of one rank: (info dict, global vertex ids of its patches)."""
+    if gnx % nranks:
+        raise ValueError("gnx must be divisible by nranks")
+    snx = gnx // nranks
+    m = _mesh(gnx, gny, h, 4, rank * snx, snx)
+    info = np.zeros(16, dtype=np.int32)
+    n = c_i64()
+    _check(lib.wrmg_plan_strip(ctypes.byref(m), int(degree), int(rank), int(nranks), info.ctypes.data_as(c_vp),
+                               None, ctypes.byref(n)))
+    pv = np.zeros(max(n.value, 1), dtype=np.int32)
+    _check(lib.wrmg_plan_strip(ctypes.byref(m), int(degree), int(rank), int(nranks), info.ctypes.data_as(c_vp),
+                               pv.ctypes.data_as(c_vp), ctypes.byref(n)))
+    return dict(zip(STRIP_INFO, (int(x) for x in info))), pv[:n.value]
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0), as bytes."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.wrmg_nccl_unique_id(ctypes.cast(buf, c_vp)))
+    return buf.raw
+
+
+class LoopbackHub:
+    """In-process transport for nranks contexts driven by nranks host threads."""
+
+    def __init__(self, nranks):
+        h = c_vp()
+        _check(lib.wrmg_loopback_create(int(nranks), ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib.wrmg_loopback_destroy(self.handle)
+            self.handle = None
 
 
 def wrmg_plan(nx, ny, h, degree, q, nslabs, ncoarse=4):
@@ -144,13 +189,20 @@ class Context:
 
     def __init__(self, nx, ny=None, h=None, degree=1, q=0, nslabs=1, dt=1.0, kappa=1.0, omega_mg=1.0,
                  nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None, factor_mode="auto",
-                 problem="heat", reynolds=1.0, bc=None, lid_speed=1.0):
+                 problem="heat", reynolds=1.0, bc=None, lid_speed=1.0, rank=0, nranks=1, nccl_id=None,
+                 hub=None):
         import torch
         ny = nx if ny is None else ny
         h = 1.0 / ny if h is None else h
         if stream is None:
             stream = torch.cuda.current_stream(device).cuda_stream
-        self._mesh = _mesh(nx, ny, h, ncoarse)
+        if nranks > 1:
+            if nx % nranks:
+                raise ValueError("strips: nx must be divisible by nranks")
+            snx = nx // nranks
+            self._mesh = _mesh(nx, ny, h, ncoarse, rank * snx, snx)
+        else:
+            self._mesh = _mesh(nx, ny, h, ncoarse)
         co = wrmg_coeffs()
         co.problem = {"heat": 0, "ns": 1}[problem]
         if bc is None:
@@ -159,7 +211,13 @@ class Context:
         co.kappa, co.reynolds, co.lid_speed = float(kappa), float(reynolds), float(lid_speed)
         co.weights = 0 if weights == "pou" else 1
         co.omega_mg, co.nu_pre, co.nu_post = float(omega_mg), int(nu_pre), int(nu_post)
-        co.device, co.stream, co.rank, co.nranks = int(device), c_vp(stream), 0, 1
+        co.device, co.stream, co.rank, co.nranks = int(device), c_vp(stream), int(rank), int(nranks)
+        self._nccl_id = None
+        if nccl_id is not None:
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            co.nccl_unique_id = ctypes.cast(self._nccl_id, c_vp)
+        if hub is not None:
+            co.loopback_hub = hub.handle
         co.factor_mode = {"auto": 0, "lu": 1}[factor_mode]
         self._co = co
         h_ = c_vp()

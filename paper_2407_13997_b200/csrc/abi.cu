@@ -3,15 +3,18 @@
 // the kernels of kernels_*.cu; this file only allocates, uploads integer plans
 // and sequences launches on the context's stream.
 #include <cmath>
+#include <functional>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "internal.h"
 #include "ns.h"
 #include "ns_kernels.h"
 #include "plan.h"
+#include "strip.h"
 
 using namespace wrmg;
 
@@ -162,7 +165,8 @@ void free_level(Level &L) {
                   (void *)L.vt, (void *)L.kV, (void *)L.kVT, (void *)L.kS, (void *)L.ksig, (void *)L.cta_patch,
                   (void *)L.cta_type, (void *)L.rcls, (void *)L.cta_patch1, (void *)L.cta_type1,
                   (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8, (void *)L.vvptr, (void *)L.conv,
-                  (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo})
+                  (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo, (void *)L.hx[0], (void *)L.hx[1],
+                  (void *)L.hx[2], (void *)L.hx[3]})
     dfree(p);
 }
 
@@ -173,8 +177,7 @@ void validate(const wrmg_mesh *mesh, int degree, int q, int nslabs, double dt) {
   if (nslabs < 1) throw Err{WRMG_E_INVALID, "nslabs must be >= 1"};
   if (!(dt > 0)) throw Err{WRMG_E_INVALID, "dt must be > 0"};
   if (mesh->gnx < 1 || mesh->gny < 1 || !(mesh->h > 0)) throw Err{WRMG_E_INVALID, "bad mesh size"};
-  if (mesh->x0 != 0 || (mesh->nx != 0 && mesh->nx != mesh->gnx))
-    throw Err{WRMG_E_UNSUPPORTED, "strip partitions (x0 != 0 or nx != gnx) are not built"};
+  if (mesh->x0 < 0 || mesh->nx < 0 || mesh->x0 + mesh->nx > mesh->gnx) throw Err{WRMG_E_INVALID, "bad strip"};
   int64_t L = (int64_t)(degree * mesh->gnx + 1) * (degree * mesh->gny + 1);
   if (L > (int64_t)INT32_MAX / 8) throw Err{WRMG_E_UNSUPPORTED, "lattice too large for int32 node ids"};
 }
@@ -220,6 +223,84 @@ void gather_stencil(wrmg_ctx *c, Level &L) {
   L.stencil_ok = true;
 }
 
+
+// ------------------------------------------------------------ strip partition
+// Halo updates of a level vector (strip.h for the columns).
+void comm_call(wrmg_ctx *c, const std::function<void()> &f) {
+  try {
+    f();
+  } catch (const std::string &m) {
+    throw Err{WRMG_E_NCCL, m};
+  }
+}
+
+// ghosts <- owners (both sides)
+void halo_forward(wrmg_ctx *c, Level &L, double *v) {
+  const StripInfo &S = L.st;
+  cudaStream_t s = c->stream;
+  const size_t cnt = (size_t)L.Ly * c->k * c->nt;
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.sl0, S.nsl, L.hx[0], 0, s);
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.sr0, S.nsr, L.hx[2], 0, s);
+  comm_call(c, [&] { c->comm->exchange(L.hx[0], L.hx[1], S.nsl ? cnt : 0, L.hx[2], L.hx[3], S.nsr ? cnt : 0, s); });
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.lg0, S.nlg, L.hx[1], 1, s);
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.rg0, S.nrg, L.hx[3], 1, s);
+}
+
+// owners += ghosts of the neighbours (both sides)
+void halo_reverse_add(wrmg_ctx *c, Level &L, double *v) {
+  const StripInfo &S = L.st;
+  cudaStream_t s = c->stream;
+  const size_t cnt = (size_t)L.Ly * c->k * c->nt;
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.lg0, S.nlg, L.hx[0], 0, s);
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.rg0, S.nrg, L.hx[2], 0, s);
+  comm_call(c, [&] { c->comm->exchange(L.hx[0], L.hx[1], S.nlg ? cnt : 0, L.hx[2], L.hx[3], S.nrg ? cnt : 0, s); });
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.sl0, S.nsl, L.hx[1], 2, s);
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.sr0, S.nsr, L.hx[3], 2, s);
+}
+
+void zero_ghosts(wrmg_ctx *c, Level &L, double *v) {
+  const StripInfo &S = L.st;
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.lg0, S.nlg, nullptr, 3, c->stream);
+  launch_cols(v, L.Lx, L.Ly, c->nt, S.rg0, S.nrg, nullptr, 3, c->stream);
+}
+
+// One additive sweep on a strip: owned patches add into owned and right-ghost
+// columns; the ghost sums are returned to their owners, then ghosts refreshed.
+void sweep_strip(wrmg_ctx *c, int l, const double *r, double *u, double om) {
+  Level &L = c->lv[l];
+  zero_ghosts(c, L, u);
+  prof_sweep(c, l, r, u, om);
+  halo_reverse_add(c, L, u);
+  halo_forward(c, L, u);
+}
+
+// Coarsest level: all-gather the owned columns, replicated exact solve of the
+// global coarsest problem (H11), local window (owned + ghosts) back.
+void coarse_strip(wrmg_ctx *c, const double *r, double *z) {
+  Level &L0 = c->lv[0];
+  Level &G = c->gco;
+  const StripInfo &S = L0.st;
+  cudaStream_t s = c->stream;
+  const int k = c->k, nx0 = S.nx;
+  launch_cols(const_cast<double *>(r), L0.Lx, L0.Ly, c->nt, S.own0, S.own1 - S.own0 + 1, c->gsend, 0, s);
+  comm_call(c, [&] { c->comm->allgather(c->gsend, c->grecv, (size_t)c->gchunk, s); });
+  for (int q = 0; q < S.nranks; ++q) {
+    const int x0q = q * nx0;
+    const int g0 = q == 0 ? 0 : k * x0q + 1, g1 = k * (x0q + nx0);
+    launch_window(c->grecv + (int64_t)q * c->gchunk, g1 - g0 + 1, 0, c->gr, G.Lx, g0, G.Ly, g1 - g0 + 1, c->nt, s);
+  }
+  {
+    const Coarse &C = c->coarse;
+    PScope ps(c, WRMG_K_COARSE, 0, 16.0 * C.nfree * c->nt + 8.0 * G.nnode * c->nt,
+              2.0 * c->N * ((double)C.m * C.m + (double)C.m * C.mp));
+    if (c->use_kron)
+      launch_coarse_solve_kron(C, G, c->q, c->N, c->gr, c->gz, s);
+    else
+      launch_coarse_solve(C, G, c->q, c->N, c->gr, c->gz, s);
+  }
+  launch_window(c->gz, G.Lx, S.G0, z, L0.Lx, 0, L0.Ly, L0.Lx, c->nt, s);
+}
+
 // Numeric part of setup / linearisation: H1, H4, H5 on every level + coarse block.
 void factor_all(wrmg_ctx *c) {
   cudaStream_t s = c->stream;
@@ -247,7 +328,11 @@ void factor_all(wrmg_ctx *c) {
     gather_stencil(c, L);
   }
   Coarse &C = c->coarse;
-  Level &L0 = c->lv[0];
+  Level &L0 = c->strip ? c->gco : c->lv[0];  // strips: the replicated global coarsest level
+  if (c->strip) {
+    launch_assemble_spatial(L0, c->k, c->ref_dev, c->co.kappa, s);
+    check_launch();
+  }
   launch_coarse_blocks(L0, C, c->nq, c->tm, s);
   check_launch();
   double *LU = dalloc<double>((size_t)C.m * C.m);
@@ -418,6 +503,8 @@ void setup_ns(wrmg_ctx *c) {
       throw Err{WRMG_E_UNSUPPORTED, "Vanka patch system of size " + std::to_string(m) +
                                         " exceeds one CTA (shared-memory block inverse): lower q or degree"};
     L.mstride = (m * m + 1) & ~(int64_t)1;
+    L.st.own1 = L.Lx - 1;  // NS: single rank, whole lattice
+    L.nfree_owned = L.nfree;
     if (l >= 1 || nl == 1) {
       L.nsinv = dalloc<double>((size_t)L.npatch * c->N * L.mstride);
       L.nsinfo = dalloc<int32_t>((size_t)L.npatch * c->N);
@@ -492,7 +579,55 @@ void ns_nonlinear_residual(wrmg_ctx *c, const double *u, const double *b, double
 int64_t ndof_level(const wrmg_ctx *c, int l) { return c->lv[l].nnode * c->nt; }
 
 // z = B r on level l (H12): V(nu_pre, nu_post), zero initial guess.
+// V(nu_pre, nu_post) on a strip: r is valid on owned columns
+// (ghosts refreshed here), z leaves valid on owned and ghost columns.
+void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
+  cudaStream_t s = c->stream;
+  Level &L = c->lv[l];
+  if (l == 0) {
+    coarse_strip(c, r, z);
+    return;
+  }
+  const int64_t nd = L.nnode * c->nt;
+  double *t = (l == (int)c->lv.size() - 1) ? c->tmp : L.vt;
+  const double om = c->co.omega_mg;
+  halo_forward(c, L, const_cast<double *>(r));
+  CK(cudaMemsetAsync(z, 0, nd * sizeof(double), s));
+  for (int it = 0; it < c->co.nu_pre; ++it) {
+    if (it == 0) {
+      sweep_strip(c, l, r, z, om);
+    } else {
+      prof_residual(c, l, z, r, t, false);
+      halo_forward(c, L, t);
+      sweep_strip(c, l, t, z, om);
+    }
+  }
+  prof_residual(c, l, z, r, t, c->co.nu_pre == 0);
+  Level &C = c->lv[l - 1];
+  {
+    PScope ps(c, WRMG_K_RESTRICT, l, 8.0 * (L.nnode + C.nnode) * c->nt, 2.0 * C.R.nnz * c->nt);
+    launch_restrict(C, c->nt, t, C.vr, s);  // R = P^T over owned fine rows
+  }
+  halo_reverse_add(c, C, C.vr);
+  vcycle_strip(c, l - 1, C.vr, C.vz);
+  {
+    PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
+    launch_prolong_add(C, c->nt, C.vz, z, s);  // owned fine rows
+  }
+  halo_forward(c, L, z);
+  for (int it = 0; it < c->co.nu_post; ++it) {
+    prof_residual(c, l, z, r, t, false);
+    halo_forward(c, L, t);
+    sweep_strip(c, l, t, z, om);
+  }
+  check_launch();
+}
+
 void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
+  if (c->strip) {
+    vcycle_strip(c, l, r, z);
+    return;
+  }
   cudaStream_t s = c->stream;
   Level &L = c->lv[l];
   if (l == 0 && c->ns) {
@@ -609,6 +744,29 @@ wrmg_status wrmg_plan_patches(const wrmg_mesh *mesh, int32_t degree, int32_t *no
   }
 }
 
+wrmg_status wrmg_plan_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank, int32_t nranks, int32_t *info,
+                            int32_t *patch_vertex, int64_t *npatch) {
+  try {
+    validate(mesh, degree, 0, 1, 1.0);
+    if (!info || nranks < 1 || rank < 0 || rank >= nranks) throw Err{WRMG_E_INVALID, "bad strip query"};
+    PlanLevel P;
+    StripInfo S;
+    plan_strip_level(mesh->gnx, mesh->gny, mesh->x0, mesh->nx, mesh->h, degree, rank, nranks, &P, &S);
+    const int32_t v[16] = {S.G0, S.own0, S.own1, S.lg0, S.nlg, S.rg0, S.nrg, S.sl0, S.nsl, S.sr0, S.nsr, P.Lx, P.Ly,
+                           S.cx0, S.nxl, 0};
+    std::memcpy(info, v, sizeof(v));
+    if (npatch) *npatch = P.npatch;
+    if (patch_vertex)  // global vertex ids J (gnx + 1) + I
+      for (int64_t p = 0; p < P.npatch; ++p) {
+        const int vi = P.pvert[p] % (S.nxl + 1) + S.cx0, vj = P.pvert[p] / (S.nxl + 1);
+        patch_vertex[p] = vj * (mesh->gnx + 1) + vi;
+      }
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(nullptr, e);
+  }
+}
+
 wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, double dt,
                        const wrmg_coeffs *coeffs, wrmg_ctx **out) {
   wrmg_ctx *c = nullptr;
@@ -622,7 +780,8 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (coeffs->problem == WRMG_HEAT && coeffs->bc != WRMG_BC_DIRICHLET0)
       throw Err{WRMG_E_UNSUPPORTED, "heat: only WRMG_BC_DIRICHLET0 is built"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
-    if (coeffs->nranks > 1) throw Err{WRMG_E_UNSUPPORTED, "multi-rank strips are not built"};
+    if (coeffs->nranks > 1 && coeffs->problem != WRMG_HEAT)
+      throw Err{WRMG_E_UNSUPPORTED, "strip partitions are built for the heat operator only"};
     c = new wrmg_ctx();
     c->mesh = *mesh;
     if (c->mesh.nx == 0) c->mesh.nx = mesh->gnx;
@@ -667,11 +826,42 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     const int nl = (int)nxs.size();
     std::vector<PlanLevel> plans(nl);
     c->lv.resize(nl);
+    c->strip = coeffs->nranks > 1;
+    if (c->strip) {  // uniform strips x0 = rank * nx
+      const int P = coeffs->nranks, r = coeffs->rank;
+      if (r < 0 || r >= P || c->mesh.nx * P != mesh->gnx || c->mesh.x0 != r * c->mesh.nx)
+        throw Err{WRMG_E_INVALID, "strips: need nx * nranks = gnx and x0 = rank * nx"};
+      std::string e;
+      c->comm = coeffs->loopback_hub ? make_loop_comm(coeffs->loopback_hub, r, P, e)
+                                     : make_nccl_comm(coeffs->nccl_unique_id, r, P, e);
+      if (!c->comm) throw Err{WRMG_E_NCCL, e};
+    } else if (c->mesh.x0 != 0 || c->mesh.nx != mesh->gnx) {
+      throw Err{WRMG_E_INVALID, "a partial strip needs nranks > 1"};
+    }
     for (int l = 0; l < nl; ++l) {
       double h = mesh->h * (double)(mesh->gnx / nxs[l]);
-      plan_level(nxs[l], nys[l], h, degree, &plans[l]);
-      PlanLevel &P = plans[l];
       Level &L = c->lv[l];
+      if (c->strip) {
+        const int f = mesh->gnx / nxs[l];
+        if (c->mesh.nx % f || c->mesh.nx / f < 2)
+          throw Err{WRMG_E_UNSUPPORTED, "strips: a level's strip is narrower than 2 cells (raise ncoarse or nx)"};
+        plan_strip_level(nxs[l], nys[l], c->mesh.x0 / f, c->mesh.nx / f, h, degree, coeffs->rank, coeffs->nranks,
+                         &plans[l], &L.st);
+      } else {
+        plan_level(nxs[l], nys[l], h, degree, &plans[l]);
+        L.st = StripInfo{};
+        L.st.gnx = nxs[l];
+        L.st.nx = nxs[l];
+        L.st.nxl = nxs[l];
+        L.st.own1 = degree * nxs[l];
+      }
+      PlanLevel &P = plans[l];
+      {
+        int64_t nfo = 0;
+        for (int J = 0; J < P.Ly; ++J)
+          for (int I = L.st.own0; I <= L.st.own1; ++I) nfo += !P.con[(int64_t)J * P.Lx + I];
+        L.nfree_owned = nfo;
+      }
       L.nx = P.nx;
       L.ny = P.ny;
       L.h = h;
@@ -738,12 +928,17 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         L.vz = dalloc<double>(L.nnode * c->nt);
         L.vt = dalloc<double>(L.nnode * c->nt);
       }
+      if (c->strip)
+        for (int b = 0; b < 4; ++b) L.hx[b] = dalloc<double>((size_t)L.Ly * degree * c->nt);
       CK(cudaStreamSynchronize(s));  // host plan vectors die at scope end
     }
     for (int l = 1; l < nl; ++l) {
       std::vector<int32_t> rp, ci, trp, tci;
       std::vector<double> v, tv;
-      plan_interpolation(plans[l - 1], plans[l], degree, rp, ci, v);
+      if (c->strip)
+        plan_strip_interpolation(plans[l - 1], c->lv[l - 1].st, plans[l], c->lv[l].st, degree, nys[l], rp, ci, v);
+      else
+        plan_interpolation(plans[l - 1], plans[l], degree, rp, ci, v);
       transpose_csr(plans[l].nnode, plans[l - 1].nnode, rp, ci, v, trp, tci, tv);
       Level &C = c->lv[l - 1];
       C.P.nrow = plans[l].nnode;
@@ -758,11 +953,40 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       C.R.val = dupload(tv, s);
       CK(cudaStreamSynchronize(s));
     }
+    PlanLevel gplan;  // strips: the global coarsest level, replicated on every rank
+    if (c->strip) {
+      const double h0 = mesh->h * (double)(mesh->gnx / nxs[0]);
+      plan_level(nxs[0], nys[0], h0, degree, &gplan);
+      Level &G = c->gco;
+      G.nx = gplan.nx;
+      G.ny = gplan.ny;
+      G.h = h0;
+      G.Lx = gplan.Lx;
+      G.Ly = gplan.Ly;
+      G.nnode = gplan.nnode;
+      G.nfree = gplan.nfree;
+      G.A.nrow = gplan.nnode;
+      G.A.nnz = (int64_t)gplan.col.size();
+      G.A.rowptr = dupload(gplan.rowptr, s);
+      G.A.col = dupload(gplan.col, s);
+      G.A.val = dalloc<double>(gplan.col.size());
+      G.A.val2 = dalloc<double>(gplan.col.size());
+      G.h_con = gplan.con;
+      G.con = dupload(gplan.con, s);
+      c->gr = dalloc<double>(G.nnode * c->nt);
+      c->gz = dalloc<double>(G.nnode * c->nt);
+      c->gchunk = (int64_t)G.Ly * (degree * c->lv[0].st.nx + 1) * c->nt;
+      c->gsend = dalloc<double>(c->gchunk);
+      c->grecv = dalloc<double>(c->gchunk * coeffs->nranks);
+      CK(cudaMemsetAsync(c->gr, 0, G.nnode * c->nt * sizeof(double), s));
+      CK(cudaStreamSynchronize(s));
+    }
     {
+      const PlanLevel &CP = c->strip ? gplan : plans[0];
       Coarse &C = c->coarse;
       std::vector<int32_t> nodes;
-      for (int64_t i = 0; i < plans[0].nnode; ++i)
-        if (!plans[0].con[i]) nodes.push_back((int32_t)i);
+      for (int64_t i = 0; i < CP.nnode; ++i)
+        if (!CP.con[i]) nodes.push_back((int32_t)i);
       if (nodes.empty()) throw Err{WRMG_E_INVALID, "coarse level has no free node"};
       C.nfree = (int64_t)nodes.size();
       C.mp = (int)nodes.size();
@@ -820,6 +1044,15 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
   int64_t upd = 0;
   for (size_t l = 1; l < c->lv.size(); ++l) upd += c->lv[l].nfree * c->nt * (c->co.nu_pre + c->co.nu_post);
   out->smooth_dof_updates_per_vcycle = upd;
+  out->own0 = L.st.own0;
+  out->own1 = L.st.own1;
+  out->g0 = L.st.G0;
+  out->nfree_owned_st = L.nfree_owned * c->nt;
+  if (c->strip) {
+    upd = 0;
+    for (size_t l = 1; l < c->lv.size(); ++l) upd += c->lv[l].nfree_owned * c->nt * (c->co.nu_pre + c->co.nu_post);
+    out->smooth_dof_updates_per_vcycle = upd;
+  }
   return WRMG_OK;
 }
 
@@ -865,6 +1098,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
       check_launch();
       return WRMG_OK;
     }
+    if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(u));
     prof_residual(c, (int)c->lv.size() - 1, u, b, r, false);
     check_launch();
     return WRMG_OK;
@@ -876,6 +1110,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
 wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
   if (!c || !x || !y) return WRMG_E_INVALID;
   try {
+    if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(x));
     prof_residual(c, (int)c->lv.size() - 1, x, nullptr, y, false);  // b = NULL: y = A x
     check_launch();
     return WRMG_OK;
@@ -889,6 +1124,13 @@ wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps
   try {
     const int l = (int)c->lv.size() - 1;
     for (int s = 0; s < nsweeps; ++s) {
+      if (c->strip) {
+        halo_forward(c, c->lv[l], u);
+        prof_residual(c, l, u, b, c->tmp, false);
+        halo_forward(c, c->lv[l], c->tmp);
+        sweep_strip(c, l, c->tmp, u, omega);
+        continue;
+      }
       prof_residual(c, l, u, b, c->tmp, false);
       prof_sweep(c, l, c->tmp, u, omega);
     }
@@ -941,6 +1183,10 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, doubl
 wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
                         double atol, int32_t *iters, double *relres) {
   if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1) return WRMG_E_INVALID;
+  if (c->strip) {
+    c->err = "wrmg_fgmres: single rank only (strips run stationary V-cycles, C5)";
+    return WRMG_E_UNSUPPORTED;
+  }
   try {
     cudaStream_t s = c->stream;
     const Level &L = c->lv.back();
@@ -1127,6 +1373,24 @@ wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
 
 int64_t wrmg_launch_count(void) { return g_launches; }
 
+wrmg_status wrmg_nccl_unique_id(void *out128) {
+  if (!out128) return WRMG_E_INVALID;
+  std::string e;
+  if (!nccl_get_unique_id(out128, e)) {
+    g_err = e;
+    return WRMG_E_NCCL;
+  }
+  return WRMG_OK;
+}
+
+wrmg_status wrmg_loopback_create(int32_t nranks, void **hub) {
+  if (!hub || nranks < 1) return WRMG_E_INVALID;
+  *hub = loop_hub_create(nranks);
+  return WRMG_OK;
+}
+
+void wrmg_loopback_destroy(void *hub) { loop_hub_destroy(hub); }
+
 wrmg_status wrmg_debug_fetch(wrmg_ctx *c, int32_t level, int32_t which, void *host_dst, int64_t count) {
   if (!c || !host_dst || count < 0 || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
   try {
@@ -1274,6 +1538,9 @@ void wrmg_destroy(wrmg_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &L : c->lv) free_level(L);
+  free_level(c->gco);
+  for (void *p : {(void *)c->gr, (void *)c->gz, (void *)c->gsend, (void *)c->grecv}) dfree(p);
+  delete c->comm;
   Coarse &C = c->coarse;
   for (void *p : {(void *)C.nodes, (void *)C.Dblk, (void *)C.DinvT, (void *)C.GT, (void *)C.Gq, (void *)C.Z,
                   (void *)C.Y, (void *)C.piv, (void *)C.info, (void *)C.kV, (void *)C.kVT, (void *)C.kS,

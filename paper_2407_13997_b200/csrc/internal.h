@@ -51,6 +51,20 @@ struct StencilTab {
   double m[kStencilMaxC][kStencilMaxE], kk[kStencilMaxC][kStencilMaxE];
 };
 
+// Spatial strip of a level on this rank (host_strip.cu).
+struct StripInfo {
+  int rank = 0, nranks = 1;
+  int gnx = 0, x0 = 0, nx = 0;  // global cells, this rank's cell columns
+  int cx0 = 0, nxl = 0;         // local mesh: cells [cx0, cx0 + nxl)
+  int G0 = 0;                   // global node column of local column 0 (= k cx0)
+  int own0 = 0, own1 = 0;       // owned local columns [own0, own1] (inclusive)
+  int lg0 = 0, nlg = 0;         // left ghost local columns [lg0, lg0 + nlg)
+  int rg0 = 0, nrg = 0;         // right ghost local columns
+  int sl0 = 0, nsl = 0;         // columns sent to the left rank (its right ghosts)
+  int sr0 = 0, nsr = 0;         // columns sent to the right rank (its left ghosts)
+};
+struct Comm;
+
 // ---------------------------------------------------------------- device data
 struct DevCSR {
   int64_t nrow = 0, nnz = 0;
@@ -109,6 +123,10 @@ struct Level {
   double *nsinv = nullptr;          // [npatch][N][mstride] row-major D_{p,n}^{-1}
   int32_t *nsinfo = nullptr;        // [npatch][N]
   int64_t nsfree_patch_dofs = 0;    // sum of patch sizes (algorithmic accounting)
+  // strip partition (nranks > 1)
+  StripInfo st;
+  double *hx[4] = {nullptr, nullptr, nullptr, nullptr};  // halo send-left, recv-left, send-right, recv-right
+  int64_t nfree_owned = 0;
 };
 
 struct Coarse {
@@ -170,6 +188,12 @@ struct wrmg_ctx {
   double *proj = nullptr;                      // pressure-projection scratch
   double *conv_nl = nullptr;                   // finest R O(U) for the nonlinear residual
   double *nl_b = nullptr, *nl_r = nullptr, *nl_dx = nullptr;  // Newton work vectors
+  // strip partition (nranks > 1): transport, replicated global coarsest level
+  bool strip = false;
+  wrmg::Comm *comm = nullptr;
+  wrmg::Level gco;
+  double *gr = nullptr, *gz = nullptr, *gsend = nullptr, *grecv = nullptr;
+  int64_t gchunk = 0;
 };
 
 namespace wrmg {
@@ -210,4 +234,8 @@ void launch_reduce_partials(const double *partials, int nblk, int nv, double *ou
 void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
                       cudaStream_t s);
 void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s);
+// strip partition (kernels_strip.cu)
+void launch_cols(double *v, int Lx, int Ly, int64_t NT, int c0, int nc, double *buf, int mode, cudaStream_t s);
+void launch_window(const double *src, int Lxs, int sc0, double *dst, int Lxd, int dc0, int Ly, int nc, int64_t NT,
+                   cudaStream_t s);
 }  // namespace wrmg
