@@ -396,8 +396,11 @@ __global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstrid
   double mx = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
   const int st = gj_invert_smem(A, m, 1e-14 * mx, f, piv);
-  double *o = out + (p * N + n) * mstride;
-  for (int e = tid; e < m * m; e += blockDim.x) o[e] = A[e];
+  double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+  for (int e = tid; e < m * m; e += blockDim.x) {
+    const int sig = e / m, rho = e - sig * m;
+    o[e] = A[rho * m + sig];
+  }
   if (tid == 0) info[p * N + n] = st;
 }
 
@@ -442,8 +445,9 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
   const int m = NQ * mp;
   double *buf = smem;                                   // STAGED: 2 x mstride
   double *Mp = smem + (STAGED ? 2 * mstride : 0);       // mp x mp velocity mass of the patch
-  double *g = Mp + mp * mp, *x = g + m, *xq = x + m, *wn = xq + mp;
-  int *nodes = (int *)(wn + mp);
+  const int MR = (m + 31) & ~31, G = blockDim.x / MR;  // matvec: MR rows x G column groups
+  double *g = Mp + mp * mp, *x = g + m, *xq = x + m, *wn = xq + mp, *part = wn + mp;
+  int *nodes = (int *)(part + 256);
   const int64_t p = blockIdx.x;
   const int64_t NT = (int64_t)N * NQ;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
@@ -499,14 +503,24 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
     } else {
       D = Dp + (int64_t)n * mstride;
     }
-    for (int rho = wid; rho < m; rho += nw) {
+    // x = D^{-1} g with D^{-1} column-major: thread (rho, grp) sums columns
+    // sig = grp, grp + G, ... (consecutive rho -> consecutive banks), partials in smem
+    {
+      const int rho = tid % MR, grp = tid / MR;
       double acc = 0.0;
-      for (int s2 = lane; s2 < m; s2 += 32) acc = fma(STAGED ? D[rho * m + s2] : __ldg(D + rho * m + s2), g[s2], acc);
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) x[rho] = acc;
+      if (rho < m && grp < G)
+        for (int s2 = grp; s2 < m; s2 += G)
+          acc = fma(STAGED ? D[s2 * m + rho] : __ldg(D + (int64_t)s2 * m + rho), g[s2], acc);
+      if (grp < G) part[grp * MR + rho] = acc;
     }
     __syncthreads();
-    if (own) atomicAdd(u + rbase + (int64_t)n * NQ, wn[i_me] * x[tid]);
+    if (tid < m) {
+      double xv = 0.0;
+      for (int g2 = 0; g2 < G; ++g2) xv += part[g2 * MR + tid];
+      x[tid] = xv;
+      if (own) atomicAdd(u + rbase + (int64_t)n * NQ, wn[i_me] * xv);
+    }
+    __syncthreads();
   }
 }
 
@@ -735,7 +749,8 @@ size_t ns_factor_smem(int m, int mp) {
 }
 
 size_t ns_sweep_smem(int m, int mp, int64_t mstride, bool staged) {
-  return ((staged ? 2 * mstride : 0) + (int64_t)mp * mp + 2 * m + 2 * mp) * sizeof(double) + mp * sizeof(int) + 16;
+  return ((staged ? 2 * mstride : 0) + (int64_t)mp * mp + 2 * m + 2 * mp + 256) * sizeof(double) + mp * sizeof(int) +
+         16;
 }
 
 void launch_ns_assemble_linear(const NSGeom &g, const DevCSR &A, const double *ref, cudaStream_t s) {
