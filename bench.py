@@ -319,11 +319,15 @@ def run_c3(args, ws, rank, local):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ctx.linearize(W)  # warm
     torch.cuda.synchronize()
+    ctx.profile(True)
     ev[0].record(stream)
     ctx.linearize(W)
     ev[1].record(stream)
     torch.cuda.synchronize()
     lin_ms = ev[0].elapsed_time(ev[1])
+    lin_stats = {f"{a}@L{l}": {"ms": round(v["ms"], 3), "TFs": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 3)}
+                 for (a, l), v in ctx.kernel_stats().items()}
+    ctx.profile(False)
     f = ctx.empty()
     ctx.fill_uniform(f, 0, 0)
     b = ctx.empty()
@@ -390,6 +394,7 @@ def run_c3(args, ws, rank, local):
                        "ndof": lay["ndof"], "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
                        "npatch": lay["npatch"], "mp_max": lay["mp_max"], "setup_s": round(setup_s, 2)},
             "fgmres_iterations": its_l[0], "fgmres_status_relres": st_l[0], "linearize_ms": lin_ms,
+            "linearize_kernels": lin_stats,
             "vcycle_ms": ev2[0].elapsed_time(ev2[1]) / 5, "smoother_sweep_ms": ev2[2].elapsed_time(ev2[3]) / 5,
             "per_kernel": per_kernel, "clocks": clk, "gpu_launches": w.launch_count() - l0}
     if rank == 0:

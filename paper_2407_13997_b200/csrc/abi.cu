@@ -165,7 +165,8 @@ void free_level(Level &L) {
                   (void *)L.vt, (void *)L.kV, (void *)L.kVT, (void *)L.kS, (void *)L.ksig, (void *)L.cta_patch,
                   (void *)L.cta_type, (void *)L.rcls, (void *)L.cta_patch1, (void *)L.cta_type1,
                   (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8, (void *)L.vvptr, (void *)L.conv,
-                  (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo, (void *)L.hx[0], (void *)L.hx[1],
+                  (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo, (void *)L.ppos, (void *)L.pvv, (void *)L.hx[0],
+                  (void *)L.hx[1],
                   (void *)L.hx[2], (void *)L.hx[3]})
     dfree(p);
 }
@@ -396,7 +397,7 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
       PScope ps(c, WRMG_K_FACTOR, l, 8.0 * (double)L.npatch * c->N * L.mstride,
                 2.0 * m * m * m * (double)L.npatch * c->N);
       launch_ns_factor(geom(c, L), c->q, c->N, c->tm, L.A, L.vvptr, L.conv, L.pnodes, L.npatch, L.mp, L.mstride,
-                       L.nsinv, L.nsinfo, s);
+                       L.nsinv, L.nsinfo, L.ppos, L.pvv, s);
       check_launch();
     }
   }
@@ -508,6 +509,8 @@ void setup_ns(wrmg_ctx *c) {
     if (l >= 1 || nl == 1) {
       L.nsinv = dalloc<double>((size_t)L.npatch * c->N * L.mstride);
       L.nsinfo = dalloc<int32_t>((size_t)L.npatch * c->N);
+      L.ppos = dalloc<int32_t>((size_t)L.npatch * L.mp * L.mp);
+      L.pvv = dalloc<int32_t>((size_t)L.npatch * L.mp * L.mp);
     }
     if (l < nl - 1) {
       L.vr = dalloc<double>(L.nnode * c->nt);
@@ -547,6 +550,8 @@ void setup_ns(wrmg_ctx *c) {
     C.nfree = (int64_t)nodes.size();
     C.mp = (int)nodes.size();
     C.m = c->nq * C.mp;
+    C.nnzj = 0;
+    for (int32_t sd : nodes) C.nnzj += P.rowptr[sd + 1] - P.rowptr[sd];
     if (C.m > 2048) throw Err{WRMG_E_UNSUPPORTED, "coarse slab block larger than 2048 (raise ncoarse depth)"};
     C.nodes = dupload(nodes, s);
     C.nsD = dalloc<double>((size_t)c->N * C.m * C.m);
@@ -561,6 +566,7 @@ void setup_ns(wrmg_ctx *c) {
   c->bcg = dupload(plans[nl - 1].g, s);
   for (auto &L : c->lv) {
     launch_ns_assemble_linear(geom(c, L), L.A, c->th_ref, s);
+    if (L.ppos) launch_ns_patch_pos(geom(c, L), L.A, L.vvptr, L.pnodes, L.npatch, L.mp, L.ppos, L.pvv, s);
     check_launch();
   }
   CK(cudaStreamSynchronize(s));
@@ -634,7 +640,7 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
     const Coarse &C = c->coarse;
     PScope ps(c, WRMG_K_COARSE, 0, 8.0 * c->N * (double)C.m * C.m + 16.0 * L.nnode * c->nt,
               2.0 * c->N * (double)C.m * C.m);
-    launch_ns_coarse_solve(c->q, c->N, C.mp, C.pin, C.nodes, L.A, C.nsinvT, r, z, C.xq, L.nnode, s);
+    launch_ns_coarse_solve(c->q, c->N, C.mp, C.pin, C.nodes, L.A, C.nsinvT, r, z, C.xq, L.nnode, C.nnzj, s);
     ns_project(c, L, z);
     return;
   }

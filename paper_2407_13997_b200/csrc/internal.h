@@ -122,6 +122,7 @@ struct Level {
   int64_t mstride = 0;              // doubles per stored (patch, slab) inverse
   double *nsinv = nullptr;          // [npatch][N][mstride] row-major D_{p,n}^{-1}
   int32_t *nsinfo = nullptr;        // [npatch][N]
+  int32_t *ppos = nullptr, *pvv = nullptr;  // [npatch][mp][mp] CSR / convection index of each patch pair
   int64_t nsfree_patch_dofs = 0;    // sum of patch sizes (algorithmic accounting)
   // strip partition (nranks > 1)
   StripInfo st;
@@ -143,6 +144,7 @@ struct Coarse {
   int32_t *piv = nullptr, *info = nullptr;
   // Navier-Stokes coarse solve: per-slab blocks with the pinned pressure DoF (R19)
   int pin = -1;
+  int nnzj = 0;               // CSR entries of the free coarse rows (jump mass rows staged by the solve)
   double *nsD = nullptr, *nsinvT = nullptr, *xq = nullptr;
   int32_t *nspiv = nullptr, *nsinfo = nullptr;
 };

@@ -247,6 +247,44 @@ __global__ void __launch_bounds__(256) k_ns_residual(int64_t ns, int N, const in
   }
 }
 
+// Per patch, the CSR positions of every (i, j) node pair of D_p (the sparsity is
+// the same for every slab and linearisation): ppos = entry of the sid CSR or -1,
+// pvv = the pair's index in the convection storage or -1 (pressure rows / columns).
+__global__ void k_ns_patch_pos(int mp, const int32_t *__restrict__ pnodes, const int32_t *__restrict__ rowptr,
+                               const int32_t *__restrict__ col, int64_t nvrow, const int32_t *__restrict__ vvptr,
+                               int32_t *__restrict__ ppos, int32_t *__restrict__ pvv) {
+  const int64_t p = blockIdx.x;
+  for (int e = threadIdx.x; e < mp * mp; e += blockDim.x) {
+    const int i = e / mp, j = e - i * mp;
+    const int si = pnodes[p * mp + i], sj = pnodes[p * mp + j];
+    int pos = -1, vv = -1;
+    if (si >= 0 && sj >= 0) {
+      pos = csr_find_ns(rowptr, col, si, sj);
+      if (pos >= 0 && si < nvrow) {
+        const int ev = pos - rowptr[si];
+        if (ev < vvptr[si + 1] - vvptr[si]) vv = vvptr[si] + ev;
+      }
+    }
+    ppos[p * mp * mp + e] = pos;
+    pvv[p * mp * mp + e] = vv;
+  }
+}
+
+// Block value from the precomputed pair tables (no searches): the same value as block_entry.
+template <int NQ>
+__device__ __forceinline__ double block_entry_tab(int pos, int vv, const double *__restrict__ Mv,
+                                                  const double *__restrict__ KGv, const double *__restrict__ conv,
+                                                  int64_t NT, int n, const NSTime &tm, int a, int bb) {
+  if (pos < 0) return 0.0;
+  double v = tm.CE[a * NQ + bb] * __ldg(Mv + pos) + tm.Mt[a * NQ + bb] * __ldg(KGv + pos);
+  if (vv >= 0) {
+    const double *cv = conv + (int64_t)vv * NT + (int64_t)n * NQ;
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) v = fma(tm.T[(a * NQ + bb) * NQ + c], __ldg(cv + c), v);
+  }
+  return v;
+}
+
 // ------------------------------------------------------- H4 + H5 block inverse
 // Block value D[(i,a),(j,b)] of D_{p,n} = R_p A_nn R_p^T (R9) for sids si, sj.
 template <int NQ>
@@ -359,7 +397,8 @@ __global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstrid
                                                    const double *__restrict__ Mv, const double *__restrict__ KGv,
                                                    int64_t nvrow, const int32_t *__restrict__ vvptr,
                                                    const double *__restrict__ conv, NSTime tm,
-                                                   double *__restrict__ out, int32_t *__restrict__ info) {
+                                                   double *__restrict__ out, int32_t *__restrict__ info,
+                                                   const int32_t *__restrict__ ppos, const int32_t *__restrict__ pvv) {
   extern __shared__ __align__(16) double smem[];
   const int m = NQ * mp;
   double *A = smem, *f = smem + (int64_t)m * m;
@@ -377,10 +416,12 @@ __global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstrid
     const int i = rho / NQ, a = rho - i * NQ, j = sig / NQ, bb = sig - j * NQ;
     const int si = nodes[i], sj = nodes[j];
     double v;
-    if (si < 0 || sj < 0)
+    if (si < 0 || sj < 0) {
       v = (rho == sig) ? 1.0 : 0.0;
-    else
-      v = block_entry<NQ>(rowptr, col, Mv, KGv, nvrow, vvptr, conv, NT, n, tm, si, sj, a, bb);
+    } else {
+      const int64_t pe = (p * mp + i) * mp + j;
+      v = block_entry_tab<NQ>(__ldg(ppos + pe), __ldg(pvv + pe), Mv, KGv, conv, NT, n, tm, a, bb);
+    }
     A[e] = v;
   }
   __syncthreads();
@@ -402,6 +443,189 @@ __global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstrid
     o[e] = A[rho * m + sig];
   }
   if (tid == 0) info[p * N + n] = st;
+}
+
+// Register-tiled variant (m <= 80): thread t owns the TR x TC tile (t / NTC, t % NTC)
+// of D_{p,n} in registers for the whole Gauss-Jordan; per column: (A) column c
+// published, (B) pivot chosen by warp 0 (first maximum |a| among rows >= c, the
+// dgetrf choice, R10), (C) the scaled pivot row and the displaced row c published;
+// the update applies the interchange implicitly.  The column interchanges that
+// undo the row pivoting become a permutation of the output columns; the inverse
+// is written column-major for the sweep.
+template <int NQ, int TR, int TC, int NTR, int NTC>
+__global__ void __launch_bounds__(256) k_ns_factor_reg(int mp, int N, int64_t mstride,
+                                                       const int32_t *__restrict__ pnodes,
+                                                       const double *__restrict__ Mv, const double *__restrict__ KGv,
+                                                       const double *__restrict__ conv, NSTime tm,
+                                                       double *__restrict__ out, int32_t *__restrict__ info,
+                                                       const int32_t *__restrict__ ppos,
+                                                       const int32_t *__restrict__ pvv) {
+  constexpr int MRP = TR * NTR, MCP = TC * NTC;
+  __shared__ double colv[MRP], prow[MCP], rowc[MCP];
+  __shared__ int nodes[MRP / NQ + 1], perm[MCP];
+  __shared__ double s_red[8];
+  __shared__ double s_pv, s_tol;
+  __shared__ int s_p, s_info;
+  const int m = NQ * mp;
+  const int64_t p = blockIdx.x;
+  const int n = blockIdx.y;
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool act = tid < NTR * NTC;
+  const int tr = act ? tid / NTC : 0, tc = act ? tid % NTC : 0;
+  const int R0 = tr * TR, C0 = tc * TC;
+  for (int i = tid; i < mp; i += blockDim.x) nodes[i] = pnodes[p * mp + i];
+  if (tid == 0) s_info = 0;
+  __syncthreads();
+  double A[TR][TC];
+#pragma unroll
+  for (int a = 0; a < TR; ++a)
+#pragma unroll
+    for (int b = 0; b < TC; ++b) {
+      const int rho = R0 + a, sig = C0 + b;
+      double v = 0.0;
+      if (act && rho < m && sig < m) {
+        const int i = rho / NQ, aa = rho - i * NQ, j = sig / NQ, bb = sig - j * NQ;
+        if (nodes[i] < 0 || nodes[j] < 0) {
+          v = (rho == sig) ? 1.0 : 0.0;
+        } else {
+          const int64_t e = (p * mp + i) * mp + j;
+          v = block_entry_tab<NQ>(__ldg(ppos + e), __ldg(pvv + e), Mv, KGv, conv, NT, n, tm, aa, bb);
+        }
+      }
+      A[a][b] = v;
+    }
+  // R10 tolerance: 1e-14 x max row sum of |D|
+  {
+    __shared__ double rsum[MRP][NTC + 1];
+    if (act)
+#pragma unroll
+      for (int a = 0; a < TR; ++a) {
+        double t = 0.0;
+#pragma unroll
+        for (int b = 0; b < TC; ++b) t += fabs(A[a][b]);
+        rsum[R0 + a][tc] = t;
+      }
+    __syncthreads();
+    double mx = 0.0;
+    for (int r = tid; r < m; r += blockDim.x) {
+      double t = 0.0;
+      for (int b = 0; b < NTC; ++b) t += rsum[r][b];
+      mx = fmax(mx, t);
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) s_red[tid >> 5] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, s_red[w]);
+      s_tol = 1e-14 * v;
+    }
+  }
+  if (act && C0 == 0)
+#pragma unroll
+    for (int a = 0; a < TR; ++a) colv[R0 + a] = A[a][0];
+  __syncthreads();  // (A)
+  for (int c = 0; c < m; ++c) {
+    if (tid < 32) {  // (B) pivot: first maximum |a| over rows c .. m-1
+      double bv = -1.0;
+      int bi = m;
+      for (int r = c + lane; r < m; r += 32) {
+        const double v = fabs(colv[r]);
+        if (v > bv) {
+          bv = v;
+          bi = r;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        s_pv = colv[bi];
+        perm[c] = bi;
+        if (!(bv >= s_tol) && s_info == 0) s_info = c + 1;
+      }
+    }
+    __syncthreads();
+    const int pr = s_p;
+    const double pinv = s_pv != 0.0 ? 1.0 / s_pv : 0.0;
+    const double fp = colv[c];  // multiplier of the displaced row c (it lands on row p)
+    double fr[TR];              // read before (C): colv is rewritten after the update
+#pragma unroll
+    for (int a = 0; a < TR; ++a) fr[a] = colv[R0 + a];
+    // (C) new row c = old row p / pivot (column c <- 1 / pivot); old row c kept for row p
+    if (act && pr >= R0 && pr < R0 + TR)
+#pragma unroll
+      for (int a = 0; a < TR; ++a)
+        if (R0 + a == pr)
+#pragma unroll
+          for (int b = 0; b < TC; ++b) prow[C0 + b] = (C0 + b == c) ? pinv : A[a][b] * pinv;
+    if (act && c >= R0 && c < R0 + TR)
+#pragma unroll
+      for (int a = 0; a < TR; ++a)
+        if (R0 + a == c)
+#pragma unroll
+          for (int b = 0; b < TC; ++b) rowc[C0 + b] = A[a][b];
+    __syncthreads();  // (C)
+    if (act) {
+#pragma unroll
+      for (int a = 0; a < TR; ++a) {
+        const int r = R0 + a;
+        if (r == c) {
+#pragma unroll
+          for (int b = 0; b < TC; ++b) A[a][b] = prow[C0 + b];
+        } else {
+          const bool isp = (r == pr);
+          const double f = isp ? fp : fr[a];
+#pragma unroll
+          for (int b = 0; b < TC; ++b) {
+            const double old = isp ? rowc[C0 + b] : A[a][b];
+            A[a][b] = (C0 + b == c) ? -f * pinv : fma(-f, prow[C0 + b], old);
+          }
+        }
+      }
+      if (c + 1 < m && c + 1 >= C0 && c + 1 < C0 + TC)  // publish column c + 1
+#pragma unroll
+        for (int b = 0; b < TC; ++b)
+          if (C0 + b == c + 1)
+#pragma unroll
+            for (int a = 0; a < TR; ++a) colv[R0 + a] = A[a][b];
+    }
+    __syncthreads();  // (A)
+  }
+  // (P A)^{-1} = A^{-1} P^T: arr[pos] = work column at final position pos; dstc = arr^-1
+  __shared__ int arr[MCP], dstc[MCP];
+  if (tid == 0) {
+    for (int j = 0; j < m; ++j) arr[j] = j;
+    for (int c = m - 1; c >= 0; --c) {
+      const int pc = perm[c];
+      if (pc != c) {
+        const int t = arr[c];
+        arr[c] = arr[pc];
+        arr[pc] = t;
+      }
+    }
+    for (int j = 0; j < m; ++j) dstc[arr[j]] = j;
+  }
+  __syncthreads();
+  double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+  if (act)
+#pragma unroll
+    for (int b = 0; b < TC; ++b) {
+      const int sig = C0 + b;
+      if (sig >= m) continue;
+      const int dst = dstc[sig];
+#pragma unroll
+      for (int a = 0; a < TR; ++a)
+        if (R0 + a < m) o[(int64_t)dst * m + R0 + a] = A[a][b];
+    }
+  if (tid == 0) info[p * N + n] = s_info;
 }
 
 // ---------------------------------------------------------------- H7 + H8 sweep
@@ -630,32 +854,60 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256)
     k_ns_coarse_cluster(int mc, int N, int pin, int64_t ns, const int32_t *__restrict__ cnodes,
                         const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
                         const double *__restrict__ Mv, const double *__restrict__ DinvT,
-                        const double *__restrict__ r, double *__restrict__ z) {
+                        const double *__restrict__ r, double *__restrict__ z, int nnzj) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ double sm[];
   const int m = NQ * mc;
   // xq: end trace per sid, double-buffered by slab parity (a CTA may publish slab n
-  // while another still reads slab n-1 for its g); 0 on constrained sids
-  double *g = sm, *xqb = sm + m;
+  // while another still reads slab n-1 for its g); 0 on constrained sids.
+  // The mass rows of the jump are staged once in shared memory (jp / jc / jv).
+  double *g = sm, *xqb = sm + m, *jv = xqb + 2 * ns;
+  int *jc = reinterpret_cast<int *>(jv + nnzj), *jp = jc + nnzj;
   __shared__ double part[8][33];
   const int64_t NT = (int64_t)N * NQ;
   const int tid = threadIdx.x, rl = tid & 31, grp = tid >> 5;
   const int rank = (int)cluster.block_rank();
   const int RB = (m + CS - 1) / CS, r0 = rank * RB, r1 = min(m, r0 + RB);
   for (int64_t s = tid; s < 2 * ns; s += blockDim.x) xqb[s] = 0.0;
+  if (tid == 0) {
+    int acc = 0;
+    for (int i = 0; i < mc; ++i) {
+      jp[i] = acc;
+      acc += rowptr[cnodes[i] + 1] - rowptr[cnodes[i]];
+    }
+    jp[mc] = acc;
+  }
+  __syncthreads();
+  for (int i = grp; i < mc; i += blockDim.x >> 5) {
+    const int s = cnodes[i], e0 = rowptr[s], ne = rowptr[s + 1] - e0;
+    for (int e = rl; e < ne; e += 32) {
+      jc[jp[i] + e] = col[e0 + e];
+      jv[jp[i] + e] = Mv[e0 + e];
+    }
+  }
+  // r of slab 0 (thread rho < m; m <= 2 * blockDim checked by the launcher)
+  double rn[2] = {0.0, 0.0};
+  for (int k2 = 0; k2 < 2; ++k2) {
+    const int rho = tid + k2 * blockDim.x;
+    if (rho < m) {
+      const int i = rho / NQ, a = rho - i * NQ;
+      if (i != pin) rn[k2] = __ldg(r + (int64_t)cnodes[i] * NT + a);
+    }
+  }
   cluster.sync();
   for (int n = 0; n < N; ++n) {
     const double *xq = xqb + ((n + 1) & 1) * ns;  // slab n-1
     double *xo = xqb + (n & 1) * ns;              // slab n
-    for (int rho = tid; rho < m; rho += blockDim.x) {
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int rho = tid + k2 * blockDim.x;
+      if (rho >= m) break;
       const int i = rho / NQ, a = rho - i * NQ;
-      const int s = cnodes[i];
-      double v = 0.0;
+      double v = rn[k2];
       if (i != pin) {
-        v = r[(int64_t)s * NT + (int64_t)n * NQ + a];
+        if (n + 1 < N) rn[k2] = __ldg(r + (int64_t)cnodes[i] * NT + (int64_t)(n + 1) * NQ + a);  // next slab
         if (a == 0 && n > 0)
-          for (int e = rowptr[s]; e < rowptr[s + 1]; ++e) v = fma(Mv[e], xq[col[e]], v);
+          for (int e = jp[i]; e < jp[i + 1]; ++e) v = fma(jv[e], xq[jc[e]], v);
       }
       g[rho] = v;
     }
@@ -786,18 +1038,34 @@ void launch_ns_residual(const NSGeom &g, int q, int N, const Temporal &T, const 
   ++g_launches;
 }
 
+void launch_ns_patch_pos(const NSGeom &g, const DevCSR &A, const int32_t *vvptr, const int32_t *pnodes, int64_t npatch,
+                         int mp, int32_t *ppos, int32_t *pvv, cudaStream_t s) {
+  if (npatch <= 0) return;
+  k_ns_patch_pos<<<(unsigned)npatch, 256, 0, s>>>(mp, pnodes, A.rowptr, A.col, 2 * g.Lu, vvptr, ppos, pvv);
+  ++g_launches;
+}
+
 void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                       const double *conv, const int32_t *pnodes, int64_t npatch, int mp, int64_t mstride, double *out,
-                      int32_t *info, cudaStream_t s) {
+                      int32_t *info, const int32_t *ppos, const int32_t *pvv, cudaStream_t s) {
   const NSTime tm = make_nstime(T);
   const int m = (q + 1) * mp;
   const size_t sm = ns_factor_smem(m, mp);
+  dim3 grid((unsigned)npatch, (unsigned)N);
+  if (m <= 80) {  // register-tiled Gauss-Jordan (4 x 8 tiles, 20 x 10 threads)
+    by_nq(q + 1, [&](auto NQc) {
+      constexpr int NQ = decltype(NQc)::value;
+      k_ns_factor_reg<NQ, 4, 8, 20, 10><<<grid, 256, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out,
+                                                             info, ppos, pvv);
+    });
+    ++g_launches;
+    return;
+  }
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
     cudaFuncSetAttribute(k_ns_factor<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((unsigned)npatch, (unsigned)N);
     k_ns_factor<NQ><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
-                                          conv, tm, out, info);
+                                          conv, tm, out, info, ppos, pvv);
   });
   ++g_launches;
 }
@@ -854,16 +1122,17 @@ void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, c
 }
 
 void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,
-                            const double *r, double *z, double *xq, int64_t ns, cudaStream_t s) {
+                            const double *r, double *z, double *xq, int64_t ns, int nnzj, cudaStream_t s) {
   const int m = (q + 1) * mc;
   cudaMemsetAsync(z, 0, ns * (int64_t)N * (q + 1) * sizeof(double), s);
   cudaMemsetAsync(xq, 0, ns * sizeof(double), s);
-  const size_t sm = (m + 2 * ns) * sizeof(double);
+  const size_t sm = (m + 2 * ns + nnzj) * sizeof(double) + (nnzj + mc + 1) * sizeof(int);
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
-    if (sm <= 200 * 1024) {
+    if (sm <= 200 * 1024 && m <= 512) {
       cudaFuncSetAttribute(k_ns_coarse_cluster<NQ, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_ns_coarse_cluster<NQ, 8><<<8, 256, sm, s>>>(mc, N, pin, ns, cnodes, A.rowptr, A.col, A.val, DinvT, r, z);
+      k_ns_coarse_cluster<NQ, 8><<<8, 256, sm, s>>>(mc, N, pin, ns, cnodes, A.rowptr, A.col, A.val, DinvT, r, z,
+                                                     nnzj);
     } else {
       k_ns_coarse_solve<NQ><<<1, 1024, m * sizeof(double), s>>>(mc, N, pin, cnodes, A.rowptr, A.col, A.val, DinvT, r,
                                                                 z, xq);

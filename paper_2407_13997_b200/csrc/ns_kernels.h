@@ -31,14 +31,16 @@ void launch_ns_residual(const NSGeom &g, int q, int N, const Temporal &T, const 
                         cudaStream_t s);
 void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                       const double *conv, const int32_t *pnodes, int64_t npatch, int mp, int64_t mstride, double *out,
-                      int32_t *info, cudaStream_t s);
+                      int32_t *info, const int32_t *ppos, const int32_t *pvv, cudaStream_t s);
+void launch_ns_patch_pos(const NSGeom &g, const DevCSR &A, const int32_t *vvptr, const int32_t *pnodes, int64_t npatch,
+                         int mp, int32_t *ppos, int32_t *pvv, cudaStream_t s);
 void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
                      const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s);
 void launch_ns_project(double *P, int64_t nrow, int64_t NT, double *scratch, cudaStream_t s);
 void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                              const double *conv, const int32_t *cnodes, int mc, int pin, double *D, cudaStream_t s);
 void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,
-                            const double *r, double *z, double *xq, int64_t ns, cudaStream_t s);
+                            const double *r, double *z, double *xq, int64_t ns, int nnzj, cudaStream_t s);
 void launch_ns_mask(int64_t ns, int64_t NT, const uint8_t *con, const double *g, const double *src, double *dst,
                     cudaStream_t s);
 void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s);
