@@ -628,6 +628,168 @@ __global__ void __launch_bounds__(256) k_ns_factor_reg(int mp, int N, int64_t ms
   if (tid == 0) info[p * N + n] = s_info;
 }
 
+// Row-per-thread Gauss-Jordan (m <= MMAX): thread r holds row r of D_{p,n} in
+// registers.  Step c: the unused row with the largest |a[c]| (first such row on
+// ties: partial pivoting, R10) is scaled and broadcast through shared memory,
+// every other row eliminates column c in place (implicit pivoting: no row moves).
+// With p_c the pivot row of step c, the in-place result X gives
+//     D^{-1}[c][p_k] = X[p_c][k],
+// written column-major for the sweep.  Two barriers per step, no dynamic register
+// indexing (a[c] is picked by a predicated select over the unrolled row).
+template <int NQ, int MMAX, int NTH>
+__global__ void __launch_bounds__(NTH) k_ns_factor_row(int mp, int N, int64_t mstride,
+                                                        const int32_t *__restrict__ pnodes,
+                                                        const double *__restrict__ Mv,
+                                                        const double *__restrict__ KGv,
+                                                        const double *__restrict__ conv, NSTime tm,
+                                                        double *__restrict__ out, int32_t *__restrict__ info,
+                                                        const int32_t *__restrict__ ppos,
+                                                        const int32_t *__restrict__ pvv) {
+  __shared__ __align__(16) double prow[MMAX];
+  __shared__ int nodes[MMAX / NQ + 1], pcs[MMAX];
+  __shared__ double s_wv[NTH / 32];
+  __shared__ int s_wi[NTH / 32];
+  __shared__ double s_tol;
+  __shared__ int s_p, s_info;
+  const int m = NQ * mp;
+  const int64_t p = blockIdx.x;
+  const int n = blockIdx.y;
+  const int64_t NT = (int64_t)N * NQ;
+  const int r = threadIdx.x, lane = r & 31, w = r >> 5;
+  constexpr int NW = NTH / 32;
+  for (int i = r; i < mp; i += NTH) nodes[i] = pnodes[p * mp + i];
+  if (r == 0) s_info = 0;
+  __syncthreads();
+  const bool live = r < m;
+  double a[MMAX];
+  {
+    const int i = r / NQ, ar = r - (r / NQ) * NQ;
+    const bool rowpad = !live || nodes[live ? i : 0] < 0;
+#pragma unroll
+    for (int j = 0; j < MMAX; ++j) {
+      double v = 0.0;
+      if (live && j < m) {
+        const int jn = j / NQ, bb = j - jn * NQ;
+        if (rowpad || nodes[jn] < 0) {
+          v = (r == j) ? 1.0 : 0.0;
+        } else {
+          const int64_t e = (p * mp + i) * mp + jn;
+          v = block_entry_tab<NQ>(__ldg(ppos + e), __ldg(pvv + e), Mv, KGv, conv, NT, n, tm, ar, bb);
+        }
+      }
+      a[j] = v;
+    }
+  }
+  {  // R10 tolerance: 1e-14 x max row sum
+    double rs = 0.0;
+#pragma unroll
+    for (int j = 0; j < MMAX; ++j) rs += fabs(a[j]);
+    for (int o = 16; o; o >>= 1) rs = fmax(rs, __shfl_xor_sync(0xffffffffu, rs, o));
+    if (lane == 0) s_wv[w] = rs;
+    __syncthreads();
+    if (r == 0) {
+      double mx = 0.0;
+      for (int k = 0; k < NW; ++k) mx = fmax(mx, s_wv[k]);
+      s_tol = 1e-14 * mx;
+    }
+    __syncthreads();
+  }
+  bool used = !live;
+  int mystep = -1;
+  // Steps in blocks of 8 columns: inside a block the column index is static, the
+  // block index cb is a runtime loop (compact code).  The block's 8 columns live in
+  // blk[] (extracted / written back by selects over cb); the full-row update also
+  // touches the stale copy a[cb][.], which the write-back overwrites.
+  constexpr int NB = MMAX / 8;
+  const int nb = (m + 7) / 8;
+  for (int cb = 0; cb < nb; ++cb) {
+    double blk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double v = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 < NB; ++b2) v = (b2 == cb) ? a[b2 * 8 + k] : v;
+      blk[k] = v;
+    }
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {  // runtime step loop: the body (~400 instructions) stays in the I-cache
+      const int c = cb * 8 + k;
+      if (c < m) {
+        double ac = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) ac = (k2 == k) ? blk[k2] : ac;
+        double bv = used ? -1.0 : fabs(ac);
+        int bi = used ? NTH : r;
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          s_wv[w] = bv;
+          s_wi[w] = bi;
+        }
+        __syncthreads();
+        if (r == 0) {
+          double v = s_wv[0];
+          int ix = s_wi[0];
+          for (int k2 = 1; k2 < NW; ++k2)
+            if (s_wv[k2] > v || (s_wv[k2] == v && s_wi[k2] < ix)) {
+              v = s_wv[k2];
+              ix = s_wi[k2];
+            }
+          s_p = ix;
+          pcs[c] = ix;
+          if (!(v >= s_tol) && s_info == 0) s_info = c + 1;
+        }
+        __syncthreads();
+        const int pr = s_p;
+        if (r == pr) {  // pivot row: column c <- 1, then scale (column c becomes 1 / pivot)
+          const double pinv = ac != 0.0 ? 1.0 / ac : 0.0;
+#pragma unroll
+          for (int j = 0; j < MMAX; ++j) a[j] *= pinv;
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) blk[k2] = (k2 == k) ? pinv : blk[k2] * pinv;
+#pragma unroll
+          for (int j = 0; j < MMAX; j += 2) *reinterpret_cast<double2 *>(prow + j) = make_double2(a[j], a[j + 1]);
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) prow[cb * 8 + k2] = blk[k2];  // the block's true values
+          used = true;
+          mystep = c;
+        }
+        __syncthreads();
+        if (r != pr && live) {
+          const double f = ac;
+#pragma unroll
+          for (int j = 0; j < MMAX; j += 2) {
+            const double2 pv = *reinterpret_cast<const double2 *>(prow + j);
+            a[j] = fma(-f, pv.x, a[j]);
+            a[j + 1] = fma(-f, pv.y, a[j + 1]);
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) blk[k2] = (k2 == k) ? -f * prow[c] : fma(-f, prow[cb * 8 + k2], blk[k2]);
+        }
+        // prow is rewritten only after the next step's first barrier
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int b2 = 0; b2 < NB; ++b2)
+        if (b2 == cb) a[b2 * 8 + k] = blk[k];
+  }
+  __syncthreads();
+  double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+  if (live)
+#pragma unroll
+    for (int k = 0; k < MMAX; ++k)
+      if (k < m) o[(int64_t)pcs[k] * m + mystep] = a[k];
+  if (r == 0) info[p * N + n] = s_info;
+}
+
 // ---------------------------------------------------------------- H7 + H8 sweep
 __device__ __forceinline__ void mbar_init_ns(uint64_t *bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
@@ -1052,6 +1214,20 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
   const int m = (q + 1) * mp;
   const size_t sm = ns_factor_smem(m, mp);
   dim3 grid((unsigned)npatch, (unsigned)N);
+  // row-per-thread register Gauss-Jordan, fully unrolled (instantiated for DG0 / DG1 patch sizes only:
+  // each instance is ~7k straight-line DFMAs)
+  if (q == 0 && m <= 64) {
+    k_ns_factor_row<1, 64, 64><<<grid, 64, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos,
+                                                   pvv);
+    ++g_launches;
+    return;
+  }
+  if (q == 1 && m <= 80) {
+    k_ns_factor_row<2, 80, 96><<<grid, 96, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos,
+                                                   pvv);
+    ++g_launches;
+    return;
+  }
   if (m <= 80) {  // register-tiled Gauss-Jordan (4 x 8 tiles, 20 x 10 threads)
     by_nq(q + 1, [&](auto NQc) {
       constexpr int NQ = decltype(NQc)::value;
