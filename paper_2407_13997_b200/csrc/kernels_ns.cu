@@ -214,34 +214,53 @@ __global__ void __launch_bounds__(256) k_ns_residual(int64_t ns, int N, const in
     }
 #pragma unroll
     for (int a = 0; a < NQ; ++a) acc[a] = 0.0;
-    for (int e = e0; e < e1; ++e) {
-      const int64_t cb = (int64_t)__ldg(col + e) * NT + (int64_t)n * NQ;
-      const double mv = __ldg(Mv + e), kg = __ldg(KGv + e);
-      double ub[NQ];
+    // entries in batches of U with every load of a batch issued before its FMAs
+    // (velocity-velocity entries first: they carry the convection values)
+    constexpr int U = 4;
+    auto batch = [&](int e, int cnt, bool hasconv) {
+      int64_t cb[U];
+      double mv[U], kg[U], ub[U][NQ], um[U], w[U][NQ];
 #pragma unroll
-      for (int bb = 0; bb < NQ; ++bb) ub[bb] = __ldg(u + cb + bb);
+      for (int k = 0; k < U; ++k) {
+        const int ek = k < cnt ? e + k : e;
+        cb[k] = (int64_t)__ldg(col + ek) * NT + (int64_t)n * NQ;
+        mv[k] = k < cnt ? __ldg(Mv + ek) : 0.0;
+        kg[k] = k < cnt ? __ldg(KGv + ek) : 0.0;
+      }
 #pragma unroll
-      for (int a = 0; a < NQ; ++a)
+      for (int k = 0; k < U; ++k) {
 #pragma unroll
-        for (int bb = 0; bb < NQ; ++bb) acc[a] = fma(tm.CE[a * NQ + bb] * mv + tm.Mt[a * NQ + bb] * kg, ub[bb], acc[a]);
-      if (n > 0) acc[0] = fma(-mv, __ldg(u + cb - 1), acc[0]);
-      const int ev = e - e0;
-      if (ev < nvv) {
-        const double *cv = conv + (int64_t)(vb + ev) * NT + (int64_t)n * NQ;
-        double w[NQ];
+        for (int bb = 0; bb < NQ; ++bb) ub[k][bb] = __ldg(u + cb[k] + bb);
+        um[k] = n > 0 ? __ldg(u + cb[k] - 1) : 0.0;
+        if (hasconv) {
+          const double *cv = conv + (int64_t)(vb + (k < cnt ? e + k : e) - e0) * NT + (int64_t)n * NQ;
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) w[c] = __ldg(cv + c);
+          for (int c = 0; c < NQ; ++c) w[k][c] = k < cnt ? __ldg(cv + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
 #pragma unroll
         for (int a = 0; a < NQ; ++a)
 #pragma unroll
-          for (int bb = 0; bb < NQ; ++bb) {
-            double tw = 0.0;
+          for (int bb = 0; bb < NQ; ++bb)
+            acc[a] = fma(tm.CE[a * NQ + bb] * mv[k] + tm.Mt[a * NQ + bb] * kg[k], ub[k][bb], acc[a]);
+        acc[0] = fma(-mv[k], um[k], acc[0]);
+        if (hasconv)
 #pragma unroll
-            for (int c = 0; c < NQ; ++c) tw = fma(tm.T[(a * NQ + bb) * NQ + c], w[c], tw);
-            acc[a] = fma(tw, ub[bb], acc[a]);
-          }
+          for (int a = 0; a < NQ; ++a)
+#pragma unroll
+            for (int bb = 0; bb < NQ; ++bb) {
+              double tw = 0.0;
+#pragma unroll
+              for (int c = 0; c < NQ; ++c) tw = fma(tm.T[(a * NQ + bb) * NQ + c], w[k][c], tw);
+              acc[a] = fma(tw, ub[k][bb], acc[a]);
+            }
       }
-    }
+    };
+    const int ev1 = e0 + nvv;
+    for (int e = e0; e < ev1; e += U) batch(e, min(U, ev1 - e), true);
+    for (int e = ev1; e < e1; e += U) batch(e, min(U, e1 - e), false);
 #pragma unroll
     for (int a = 0; a < NQ; ++a) r[base + a] = b ? b[base + a] - acc[a] : acc[a];
   }
