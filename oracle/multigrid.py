@@ -27,7 +27,8 @@ class Level:
 
 class Hierarchy:
     def __init__(self, nx, ny, h, k, q, N, dt, kappa=1.0, n_coarse=4, omega_mg=1.0,
-                 nu_pre=1, nu_post=1, weight_mode="pou", bc="dirichlet"):
+                 nu_pre=1, nu_post=1, weight_mode="pou", bc="dirichlet", smoother_kind="damped", cheb_steps=50,
+                 cheb_seed=7):
         meshes = [Mesh(nx, ny, h)]
         while min(meshes[-1].nx, meshes[-1].ny) > n_coarse:
             m = meshes[-1]
@@ -42,6 +43,11 @@ class Hierarchy:
             P = transfer.interpolation(cp.mesh, fp.mesh, k)
             self.P0.append(transfer.correction_interpolation(P, fp.constrained, cp.constrained))
         self.omega_mg, self.nu_pre, self.nu_post = omega_mg, nu_pre, nu_post
+        self.smoother_kind = smoother_kind
+        self.lam = [None] * len(self.levels)
+        if smoother_kind == "chebyshev":
+            for l in range(1, len(self.levels)):
+                self.lam[l] = estimate_lambda(self.levels[l], cheb_steps, cheb_seed)
 
     @property
     def fine(self):
@@ -71,21 +77,84 @@ class CoarseSolver:
         return x
 
 
+def relaxation(L, r):
+    """B r: one additive WR sweep from zero with unit damping."""
+    p = L.prob
+    return smoother.wr_sweep(p, p.A, np.zeros_like(r), r, L.factors, 1.0, L.w)
+
+
+def estimate_lambda(L, steps=50, seed=7):
+    """Largest eigenvalue estimate of the relaxation-preconditioned operator B A
+    (PAPER.md:366-371: "50 steps of relaxation-preconditioned GMRES").  Reading
+    (DESIGN.md R-cheb): `steps` Arnoldi steps (classical Gram-Schmidt twice) on B A
+    from the seeded vector U[-1,1) at the canonical ids (generator of R6, `seed`,
+    constrained rows 0), and the estimate is the largest singular value of the
+    (steps+1) x steps Hessenberg -- the quantity PETSc's Chebyshev eigenvalue
+    estimate uses."""
+    import wrmg_inputs as wi
+    p = L.prob
+    v = wi.uniform_pm1(np.arange(p.ndof, dtype=np.uint64), seed)
+    v[np.repeat(p.constrained, p.NT)] = 0.0
+    V = [v / np.linalg.norm(v)]
+    Hm = np.zeros((steps + 1, steps))
+    for j in range(steps):
+        w = relaxation(L, p.A @ V[j])
+        Vm = np.array(V)
+        h = Vm @ w
+        w = w - Vm.T @ h
+        h2 = Vm @ w
+        w = w - Vm.T @ h2
+        Hm[:j + 1, j] = h + h2
+        Hm[j + 1, j] = np.linalg.norm(w)
+        V.append(w / Hm[j + 1, j])
+    return float(np.linalg.svd(Hm, compute_uv=False).max())
+
+
+def chebyshev(L, u, b, lam, nu):
+    """nu steps of Chebyshev iteration for B A x = B b on the interval
+    [0.25 lam, 1.05 lam], three-term recurrence:
+        theta = (b+a)/2, delta = (b-a)/2, sigma = theta/delta, rho_0 = 1/sigma,
+        d_0 = B r_0 / theta,  d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k / delta) B r_k,
+        rho_k = 1 / (2 sigma - rho_{k-1}),  x_{k+1} = x_k + d_k."""
+    A = L.prob.A
+    lo, hi = 0.25 * lam, 1.05 * lam
+    theta, delta = 0.5 * (hi + lo), 0.5 * (hi - lo)
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    d = relaxation(L, b - A @ u) / theta
+    u = u + d
+    for _ in range(1, nu):
+        rn = 1.0 / (2.0 * sigma - rho)
+        d = rn * rho * d + (2.0 * rn / delta) * relaxation(L, b - A @ u)
+        rho = rn
+        u = u + d
+    return u
+
+
 def vcycle(H, r, l=None):
-    """z = B r with zero initial guess (PAPER.md:361-366 V-cycle preconditioner)."""
+    """z = B r with zero initial guess (PAPER.md:361-366 V-cycle preconditioner);
+    smoothing is nu damped additive WR sweeps (R15) or, with smoother_kind =
+    "chebyshev", nu Chebyshev-accelerated steps."""
     if l is None:
         l = len(H.levels) - 1
     L = H.levels[l]
     prob = L.prob
     if l == 0:
         return H.coarse(r)
+    cheb = H.smoother_kind == "chebyshev"
     u = np.zeros_like(r)
-    for _ in range(H.nu_pre):
-        u = smoother.wr_sweep(prob, prob.A, u, r, L.factors, H.omega_mg, L.w)
+    if cheb:
+        u = chebyshev(L, u, r, H.lam[l], H.nu_pre)
+    else:
+        for _ in range(H.nu_pre):
+            u = smoother.wr_sweep(prob, prob.A, u, r, L.factors, H.omega_mg, L.w)
     res = r - prob.A @ u
     rc = transfer.restrict(H.P0[l], res, prob.NT)
     ec = vcycle(H, rc, l - 1)
     u = u + transfer.prolong(H.P0[l], ec, prob.NT)
-    for _ in range(H.nu_post):
-        u = smoother.wr_sweep(prob, prob.A, u, r, L.factors, H.omega_mg, L.w)
+    if cheb:
+        u = chebyshev(L, u, r, H.lam[l], H.nu_post)
+    else:
+        for _ in range(H.nu_post):
+            u = smoother.wr_sweep(prob, prob.A, u, r, L.factors, H.omega_mg, L.w)
     return u

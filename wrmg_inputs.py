@@ -59,3 +59,12 @@ def wind_state(nx, ny, h, k, N, q, dt):
     out[:Lux * Luy] = np.outer(wx, amp)
     out[Lux * Luy:2 * Lux * Luy] = np.outer(wy, amp)
     return out.ravel()
+
+
+def paper_heat_u0(nx, ny, h, k):
+    """Initial state of the paper's heat runs: the nodal values
+    of u0(x, y) = sin(pi x) + cos(2 pi y) on the P_k lattice, canonical order."""
+    Lx, Ly = k * nx + 1, k * ny + 1
+    I, J = np.meshgrid(np.arange(Lx), np.arange(Ly), indexing="xy")
+    x, y = I.ravel() * h / k, J.ravel() * h / k
+    return np.sin(np.pi * x) + np.cos(2 * np.pi * y)
