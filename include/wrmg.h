@@ -63,7 +63,8 @@ typedef struct {
 
 typedef struct {
   int32_t problem;      /* WRMG_HEAT (WRMG_NAVIER_STOKES: WRMG_E_UNSUPPORTED in this build) */
-  int32_t bc;           /* WRMG_BC_DIRICHLET0 (homogeneous Dirichlet on the whole boundary) */
+  int32_t bc;           /* heat: WRMG_BC_DIRICHLET0 (homogeneous Dirichlet on the whole boundary) or
+                           WRMG_BC_NEUMANN (homogeneous Neumann, no constrained DoF; single rank) */
   double kappa;         /* diffusion coefficient (> 0) */
   double reynolds;      /* Navier-Stokes only */
   double lid_speed;     /* Navier-Stokes only */
@@ -79,7 +80,13 @@ typedef struct {
   const void *nccl_unique_id; /* nranks > 1: 128-byte ncclUniqueId from wrmg_nccl_unique_id on rank 0 */
   void *loopback_hub;   /* nranks > 1 without NCCL: hub of wrmg_loopback_create, ranks = host threads of one
                            process sharing one device (tests); NULL = NCCL */
+  int32_t smoother;     /* WRMG_SMOOTH_DAMPED (default: nu damped additive sweeps, R15) |
+                           WRMG_SMOOTH_CHEBYSHEV (heat: nu Chebyshev-accelerated steps on [0.25 lam, 1.05 lam],
+                           lam from cheb_steps Arnoldi steps on B A, DESIGN.md R-cheb) */
+  int32_t cheb_steps;   /* Arnoldi steps of the lambda estimate (0 -> 50, <= 63) */
+  uint64_t cheb_seed;   /* seed of the Arnoldi start vector (R6 generator at canonical ids) */
 } wrmg_coeffs;
+enum { WRMG_SMOOTH_DAMPED = 0, WRMG_SMOOTH_CHEBYSHEV = 1 };
 
 typedef struct {
   int64_t nnode;        /* lattice nodes of the finest level owned by this rank */
@@ -119,6 +126,15 @@ wrmg_status wrmg_linearize(wrmg_ctx *ctx, const double *state);
 /* b = (M (x) I_N (x) Mt) fhat on free rows, bc value on constrained rows
  * (forcing term of eq. heatfem with f = sum fhat phi; R6).  fhat: ndof values. */
 wrmg_status wrmg_rhs(wrmg_ctx *ctx, const double *fhat, double *b);
+
+/* b += the initial-state term of eq. dgintime (Y_0^- = y_0, R7): on every free row
+ * i and temporal node a of slab 0, phi_a(0) (M u0)_i.  u0: nnode nodal values
+ * (device).  Heat only. */
+wrmg_status wrmg_rhs_initial(wrmg_ctx *ctx, const double *u0, double *b);
+
+/* Largest-eigenvalue estimates of the Chebyshev smoother (R-cheb), level >= 1
+ * (0 for the coarsest / damped smoothing).  Host output. */
+wrmg_status wrmg_cheb_lambda(const wrmg_ctx *ctx, int32_t level, double *lam);
 
 /* r = b - A u on the finest level (H6; eq. heatfem; constrained rows r = b - u).
  * `nonlinear` (Navier-Stokes): r = b - F(u).  r may not alias u or b.

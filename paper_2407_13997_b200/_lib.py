@@ -24,7 +24,8 @@ class wrmg_coeffs(ctypes.Structure):
     _fields_ = [("problem", c_i32), ("bc", c_i32), ("kappa", c_dbl), ("reynolds", c_dbl), ("lid_speed", c_dbl),
                 ("weights", c_i32), ("omega_mg", c_dbl), ("nu_pre", c_i32), ("nu_post", c_i32),
                 ("factor_mode", c_i32), ("device", c_i32), ("stream", c_vp), ("rank", c_i32), ("nranks", c_i32),
-                ("nccl_unique_id", c_vp), ("loopback_hub", c_vp)]
+                ("nccl_unique_id", c_vp), ("loopback_hub", c_vp), ("smoother", c_i32), ("cheb_steps", c_i32),
+                ("cheb_seed", ctypes.c_uint64)]
 
 
 class wrmg_layout_t(ctypes.Structure):
@@ -47,6 +48,8 @@ _sig = {
     "wrmg_layout": (c_i32, [c_vp, _P(wrmg_layout_t)]),
     "wrmg_linearize": (c_i32, [c_vp, c_vp]),
     "wrmg_rhs": (c_i32, [c_vp, c_vp, c_vp]),
+    "wrmg_rhs_initial": (c_i32, [c_vp, c_vp, c_vp]),
+    "wrmg_cheb_lambda": (c_i32, [c_vp, c_i32, _P(c_dbl)]),
     "wrmg_residual": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32]),
     "wrmg_apply": (c_i32, [c_vp, c_vp, c_vp]),
     "wrmg_smooth": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_dbl]),
@@ -190,7 +193,7 @@ class Context:
     def __init__(self, nx, ny=None, h=None, degree=1, q=0, nslabs=1, dt=1.0, kappa=1.0, omega_mg=1.0,
                  nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None, factor_mode="auto",
                  problem="heat", reynolds=1.0, bc=None, lid_speed=1.0, rank=0, nranks=1, nccl_id=None,
-                 hub=None):
+                 hub=None, smoother="damped", cheb_steps=50, cheb_seed=7):
         import torch
         ny = nx if ny is None else ny
         h = 1.0 / ny if h is None else h
@@ -218,6 +221,8 @@ class Context:
             co.nccl_unique_id = ctypes.cast(self._nccl_id, c_vp)
         if hub is not None:
             co.loopback_hub = hub.handle
+        co.smoother = {"damped": 0, "chebyshev": 1}[smoother]
+        co.cheb_steps, co.cheb_seed = int(cheb_steps), int(cheb_seed)
         co.factor_mode = {"auto": 0, "lu": 1}[factor_mode]
         self._co = co
         h_ = c_vp()
@@ -251,6 +256,14 @@ class Context:
 
     def rhs(self, fhat, b):
         _check(lib.wrmg_rhs(self._h, _ptr(fhat), _ptr(b)), self._h)
+
+    def rhs_initial(self, u0, b):
+        _check(lib.wrmg_rhs_initial(self._h, _ptr(u0), _ptr(b)), self._h)
+
+    def cheb_lambda(self, level):
+        v = c_dbl()
+        _check(lib.wrmg_cheb_lambda(self._h, int(level), ctypes.byref(v)), self._h)
+        return v.value
 
     def residual(self, u, b, r, nonlinear=False):
         _check(lib.wrmg_residual(self._h, _ptr(u), _ptr(b), _ptr(r), 1 if nonlinear else 0), self._h)

@@ -585,6 +585,144 @@ void ns_nonlinear_residual(wrmg_ctx *c, const double *u, const double *b, double
 int64_t ndof_level(const wrmg_ctx *c, int l) { return c->lv[l].nnode * c->nt; }
 
 // z = B r on level l (H12): V(nu_pre, nu_post), zero initial guess.
+// ------------------------------------------------------------ Chebyshev
+// Largest singular value of the row-major (m+1) x m Hessenberg: eigenvalues of
+// the symmetric H^T H by cyclic Jacobi (DESIGN.md R-cheb).
+double hess_sigma_max(const std::vector<double> &H, int m) {
+  std::vector<double> S((size_t)m * m, 0.0);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double t = 0.0;
+      for (int k2 = 0; k2 <= m; ++k2) t += H[(size_t)k2 * m + i] * H[(size_t)k2 * m + j];
+      S[(size_t)i * m + j] = t;
+    }
+  double nrm = 0.0;
+  for (double v : S) nrm += v * v;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < m; ++i)
+      for (int j = i + 1; j < m; ++j) off += S[(size_t)i * m + j] * S[(size_t)i * m + j];
+    if (off <= 1e-32 * nrm) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = S[(size_t)p * m + q];
+        if (apq == 0.0) continue;
+        const double th = (S[(size_t)q * m + q] - S[(size_t)p * m + p]) / (2.0 * apq);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k2 = 0; k2 < m; ++k2) {  // columns p, q
+          const double a = S[(size_t)k2 * m + p], b = S[(size_t)k2 * m + q];
+          S[(size_t)k2 * m + p] = cs * a - sn * b;
+          S[(size_t)k2 * m + q] = sn * a + cs * b;
+        }
+        for (int k2 = 0; k2 < m; ++k2) {  // rows p, q
+          const double a = S[(size_t)p * m + k2], b = S[(size_t)q * m + k2];
+          S[(size_t)p * m + k2] = cs * a - sn * b;
+          S[(size_t)q * m + k2] = sn * a + cs * b;
+        }
+      }
+  }
+  double mx = 0.0;
+  for (int i = 0; i < m; ++i) mx = std::max(mx, S[(size_t)i * m + i]);
+  return std::sqrt(mx);
+}
+
+void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om);
+
+// lam_l: `steps` Arnoldi steps (CGS2) on B A from the seeded start vector, B one
+// undamped sweep from zero (DESIGN.md R-cheb).
+double estimate_lambda(wrmg_ctx *c, int l) {
+  cudaStream_t s = c->stream;
+  Level &L = c->lv[l];
+  const int64_t n = L.nnode * c->nt;
+  const int steps = c->co.cheb_steps;
+  std::vector<double *> V(steps + 1);
+  for (auto &v : V) v = dalloc<double>(n);
+  double *w = dalloc<double>(n), *t = dalloc<double>(n);
+  auto dot = [&](const double *a, const double *b) {
+    const int nb = multidot_blocks(n);
+    const double *Vp[1] = {a};
+    launch_multidot(Vp, 1, b, n, c->red + 64, nb, s);
+    launch_reduce_partials(c->red + 64, nb, 1, c->red, s);
+    double out = 0;
+    CK(cudaMemcpyAsync(&out, c->red, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return out;
+  };
+  // h = V[0..nv)^T w in chunks of 32 vectors
+  auto multidot = [&](int nv, std::vector<double> &h) {
+    h.assign(nv, 0.0);
+    for (int c0 = 0; c0 < nv; c0 += 32) {
+      const int k2 = std::min(32, nv - c0);
+      const int nb = multidot_blocks(n);
+      launch_multidot(V.data() + c0, k2, w, n, c->red + 64, nb, s);
+      launch_reduce_partials(c->red + 64, nb, k2, c->red, s);
+      CK(cudaMemcpyAsync(h.data() + c0, c->red, k2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+  };
+  auto subtract = [&](int nv, const std::vector<double> &h) {  // w -= V h
+    for (int c0 = 0; c0 < nv; c0 += 32) {
+      const int k2 = std::min(32, nv - c0);
+      CK(cudaMemcpyAsync(c->red, h.data() + c0, k2 * sizeof(double), cudaMemcpyHostToDevice, s));
+      launch_multiaxpy(w, V.data() + c0, c->red, k2, n, -1.0, s);
+    }
+  };
+  launch_fill_uniform(V[0], n, 0, c->co.cheb_seed, s);
+  launch_ns_mask(L.nnode, c->nt, L.con, nullptr, V[0], V[0], s);  // constrained rows 0
+  launch_scale(V[0], V[0], 1.0 / std::sqrt(dot(V[0], V[0])), n, s);
+  std::vector<double> H((size_t)(steps + 1) * steps, 0.0), h, h2;
+  for (int j = 0; j < steps; ++j) {
+    prof_residual(c, l, V[j], nullptr, t, false);  // t = A v_j
+    CK(cudaMemsetAsync(w, 0, n * sizeof(double), s));
+    prof_sweep(c, l, t, w, 1.0);                    // w = B A v_j
+    multidot(j + 1, h);
+    subtract(j + 1, h);
+    multidot(j + 1, h2);
+    subtract(j + 1, h2);
+    const double hn = std::sqrt(dot(w, w));
+    for (int i = 0; i <= j; ++i) H[(size_t)i * steps + j] = h[i] + h2[i];
+    H[(size_t)(j + 1) * steps + j] = hn;
+    if (hn <= 0.0) break;
+    launch_scale(V[j + 1], w, 1.0 / hn, n, s);
+  }
+  CK(cudaStreamSynchronize(s));
+  for (auto v : V) dfree(v);
+  dfree(w);
+  dfree(t);
+  return hess_sigma_max(H, steps);
+}
+
+// nu Chebyshev steps for B A x = B b on [0.25 lam, 1.05 lam]:
+// d_0 = B r_0 / theta, d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k / delta) B r_k, x += d_k.
+void cheb_smooth(wrmg_ctx *c, int l, const double *b, double *u, bool u_zero, int nu) {
+  cudaStream_t s = c->stream;
+  Level &L = c->lv[l];
+  const int64_t n = L.nnode * c->nt;
+  double *t = (l == (int)c->lv.size() - 1) ? c->tmp : L.vt;
+  double *d = c->cd[l], *br = c->cbr[l];
+  const double lam = c->lam[l], lo = 0.25 * lam, hi = 1.05 * lam;
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  for (int k2 = 0; k2 < nu; ++k2) {
+    const double *res = b;
+    if (k2 > 0 || !u_zero) {
+      prof_residual(c, l, u, b, t, false);
+      res = t;
+    }
+    CK(cudaMemsetAsync(br, 0, n * sizeof(double), s));
+    prof_sweep(c, l, res, br, 1.0);
+    double c1 = 0.0, c2 = 1.0 / theta;
+    if (k2 > 0) {
+      const double rn = 1.0 / (2.0 * sigma - rho);
+      c1 = rn * rho;
+      c2 = 2.0 * rn / delta;
+      rho = rn;
+    }
+    launch_cheb_update(n, c1, c2, br, d, u, s);
+  }
+}
+
 // V(nu_pre, nu_post) on a strip: r is valid on owned columns
 // (ghosts refreshed here), z leaves valid on owned and ghost columns.
 void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
@@ -658,12 +796,16 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
   double *t = (l == (int)c->lv.size() - 1) ? c->tmp : L.vt;
   const double om = c->co.omega_mg;
   CK(cudaMemsetAsync(z, 0, nd * sizeof(double), s));
-  for (int it = 0; it < c->co.nu_pre; ++it) {
-    if (it == 0) {
-      prof_sweep(c, l, r, z, om);  // u = 0: residual is r itself
-    } else {
-      prof_residual(c, l, z, r, t, false);
-      prof_sweep(c, l, t, z, om);
+  if (c->cheb) {
+    cheb_smooth(c, l, r, z, true, c->co.nu_pre);
+  } else {
+    for (int it = 0; it < c->co.nu_pre; ++it) {
+      if (it == 0) {
+        prof_sweep(c, l, r, z, om);  // u = 0: residual is r itself
+      } else {
+        prof_residual(c, l, z, r, t, false);
+        prof_sweep(c, l, t, z, om);
+      }
     }
   }
   prof_residual(c, l, z, r, t, c->co.nu_pre == 0);
@@ -678,9 +820,13 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
     PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
     launch_prolong_add(C, c->nt, C.vz, z, s);
   }
-  for (int it = 0; it < c->co.nu_post; ++it) {
-    prof_residual(c, l, z, r, t, false);
-    prof_sweep(c, l, t, z, om);
+  if (c->cheb) {
+    cheb_smooth(c, l, r, z, false, c->co.nu_post);
+  } else {
+    for (int it = 0; it < c->co.nu_post; ++it) {
+      prof_residual(c, l, z, r, t, false);
+      prof_sweep(c, l, t, z, om);
+    }
   }
   check_launch();
 }
@@ -783,8 +929,13 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (!coeffs) throw Err{WRMG_E_INVALID, "coeffs is NULL"};
     if (coeffs->problem != WRMG_HEAT && coeffs->problem != WRMG_NAVIER_STOKES)
       throw Err{WRMG_E_UNSUPPORTED, "problem must be WRMG_HEAT or WRMG_NAVIER_STOKES"};
-    if (coeffs->problem == WRMG_HEAT && coeffs->bc != WRMG_BC_DIRICHLET0)
-      throw Err{WRMG_E_UNSUPPORTED, "heat: only WRMG_BC_DIRICHLET0 is built"};
+    if (coeffs->problem == WRMG_HEAT && coeffs->bc != WRMG_BC_DIRICHLET0 && coeffs->bc != WRMG_BC_NEUMANN)
+      throw Err{WRMG_E_UNSUPPORTED, "heat: bc must be WRMG_BC_DIRICHLET0 or WRMG_BC_NEUMANN"};
+    if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV &&
+        (coeffs->problem != WRMG_HEAT || coeffs->nranks > 1 || coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
+      throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: heat, single rank, cheb_steps <= 63"};
+    if (coeffs->bc == WRMG_BC_NEUMANN && coeffs->nranks > 1)
+      throw Err{WRMG_E_UNSUPPORTED, "Neumann boundaries on strips are not built"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
     if (coeffs->nranks > 1 && coeffs->problem != WRMG_HEAT)
       throw Err{WRMG_E_UNSUPPORTED, "strip partitions are built for the heat operator only"};
@@ -854,7 +1005,7 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         plan_strip_level(nxs[l], nys[l], c->mesh.x0 / f, c->mesh.nx / f, h, degree, coeffs->rank, coeffs->nranks,
                          &plans[l], &L.st);
       } else {
-        plan_level(nxs[l], nys[l], h, degree, &plans[l]);
+        plan_level(nxs[l], nys[l], h, degree, &plans[l], coeffs->bc == WRMG_BC_NEUMANN);
         L.st = StripInfo{};
         L.st.gnx = nxs[l];
         L.st.nx = nxs[l];
@@ -1017,6 +1168,18 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     c->red = dalloc<double>(64 + 64 * 148 * 4);
     CK(cudaStreamSynchronize(s));
     factor_all(c);
+    c->cheb = coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV;
+    if (c->cheb) {
+      if (c->co.cheb_steps == 0) c->co.cheb_steps = 50;
+      c->lam.assign(nl, 0.0);
+      c->cd.assign(nl, nullptr);
+      c->cbr.assign(nl, nullptr);
+      for (int l = 1; l < nl; ++l) {
+        c->cd[l] = dalloc<double>(c->lv[l].nnode * c->nt);
+        c->cbr[l] = dalloc<double>(c->lv[l].nnode * c->nt);
+        c->lam[l] = estimate_lambda(c, l);
+      }
+    }
     *out = c;
     return WRMG_OK;
   } catch (const Err &e) {
@@ -1093,6 +1256,24 @@ wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
   } catch (const Err &e) {
     return fail(c, e);
   }
+}
+
+wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
+  if (!c || !u0 || !b) return WRMG_E_INVALID;
+  if (c->ns) return WRMG_E_UNSUPPORTED;
+  try {
+    launch_rhs_initial(c->lv.back(), c->nq, c->nt, c->tm.phi0, u0, b, c->stream);
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_cheb_lambda(const wrmg_ctx *c, int32_t level, double *lam) {
+  if (!c || !lam || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  *lam = c->cheb ? c->lam[level] : 0.0;
+  return WRMG_OK;
 }
 
 wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double *r, int32_t nonlinear) {
@@ -1545,6 +1726,8 @@ void wrmg_destroy(wrmg_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &L : c->lv) free_level(L);
   free_level(c->gco);
+  for (double *p : c->cd) dfree(p);
+  for (double *p : c->cbr) dfree(p);
   for (void *p : {(void *)c->gr, (void *)c->gz, (void *)c->gsend, (void *)c->grecv}) dfree(p);
   delete c->comm;
   Coarse &C = c->coarse;

@@ -174,6 +174,7 @@ void build_temporal(int q, double dt, Temporal *T) {
     v0[a] = basis(a, 0.0, &dd);
     v1[a] = basis(a, 1.0, &dd);
   }
+  for (int a = 0; a < nq; ++a) T->phi0[a] = v0[a];
   for (int a = 0; a < nq; ++a)
     for (int b = 0; b < nq; ++b) {
       T->CE[a * nq + b] = C[a * nq + b] + v0[a] * v0[b];

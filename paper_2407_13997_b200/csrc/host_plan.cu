@@ -12,7 +12,7 @@
 
 namespace wrmg {
 
-void plan_level(int nx, int ny, double h, int k, PlanLevel *P) {
+void plan_level(int nx, int ny, double h, int k, PlanLevel *P, bool neumann) {
   P->nx = nx;
   P->ny = ny;
   P->h = h;
@@ -26,7 +26,7 @@ void plan_level(int nx, int ny, double h, int k, PlanLevel *P) {
   int64_t nfree = 0;
   for (int J = 0; J < Ly; ++J)
     for (int I = 0; I < Lx; ++I) {
-      bool c = (I == 0 || J == 0 || I == Lx - 1 || J == Ly - 1);
+      bool c = !neumann && (I == 0 || J == 0 || I == Lx - 1 || J == Ly - 1);  // Neumann: no constrained DoF
       P->con[(int64_t)J * Lx + I] = c;
       nfree += !c;
     }
@@ -82,11 +82,21 @@ void plan_level(int nx, int ny, double h, int k, PlanLevel *P) {
     int64_t p = (int64_t)P->psize.size();
     int vi = v % (nx + 1), vj = v / (nx + 1);
     std::vector<int32_t> sig;
-    sig.reserve(2 * s.size());
+    sig.reserve(2 * s.size() + 20);
     for (int32_t i : s) {
       sig.push_back((int32_t)(i % Lx) - k * vi);
       sig.push_back((int32_t)(i / Lx) - k * vj);
       mu[i] += 1;
+    }
+    {  // the cells of the star enter the block too (P1 stars are one node; Neumann boundary stars differ)
+      int ci[6], cj[6], t[6], la[6], lb[6];
+      const int nc = cells_of_node(k, nx, ny, k * vi, k * vj, ci, cj, t, la, lb);
+      sig.push_back(-1000 - nc);
+      for (int c = 0; c < nc; ++c) {
+        sig.push_back(ci[c] - vi);
+        sig.push_back(cj[c] - vj);
+        sig.push_back(t[c]);
+      }
     }
     auto it = types.find(sig);
     int ty;

@@ -35,6 +35,7 @@ struct Temporal {
   double Mt[(kMaxQ + 1) * (kMaxQ + 1)];  // dt int phi_a phi_b
   double E1[(kMaxQ + 1) * (kMaxQ + 1)];  // phi_a(0) phi_b(1)
   double T[(kMaxQ + 1) * (kMaxQ + 1) * (kMaxQ + 1)];  // dt int phi_a phi_b phi_c, index (a nq + b) nq + c
+  double phi0[kMaxQ + 1];                             // phi_a(0)
 };
 void build_temporal(int q, double dt, Temporal *out);
 // Reference basis of degree k (local order of lattice.h) and its xi/eta derivatives at (xi, eta).
@@ -196,6 +197,10 @@ struct wrmg_ctx {
   wrmg::Level gco;
   double *gr = nullptr, *gz = nullptr, *gsend = nullptr, *grecv = nullptr;
   int64_t gchunk = 0;
+  // Chebyshev-accelerated smoothing (WRMG_SMOOTH_CHEBYSHEV): lambda per level, direction / B r vectors
+  bool cheb = false;
+  std::vector<double> lam;
+  std::vector<double *> cd, cbr;
 };
 
 namespace wrmg {
@@ -236,6 +241,10 @@ void launch_reduce_partials(const double *partials, int nblk, int nv, double *ou
 void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
                       cudaStream_t s);
 void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s);
+// Chebyshev smoothing / initial state (kernels_cheb.cu)
+void launch_cheb_update(int64_t n, double c1, double c2, const double *br, double *d, double *u, cudaStream_t s);
+void launch_rhs_initial(const Level &L, int nq, int64_t NT, const double *phi0, const double *u0, double *b,
+                        cudaStream_t s);
 // strip partition (kernels_strip.cu)
 void launch_cols(double *v, int Lx, int Ly, int64_t NT, int c0, int nc, double *buf, int mode, cudaStream_t s);
 void launch_window(const double *src, int Lxs, int sc0, double *dst, int Lxd, int dc0, int Ly, int nc, int64_t NT,

@@ -46,12 +46,21 @@ __device__ __forceinline__ int csr_find_k(const int32_t *rowptr, const int32_t *
 // then the per-mode temporal inverses S_i and multipliers sigma_i.
 // Outputs (stride mp, pad modes zero): V[t][j][i] (row j = patch node),
 // VT[t][i][j], S[t][i][nq*nq], sig[t][i].
-__global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+template <int NT>
+__global__ void __launch_bounds__(NT) k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
                              const double *__restrict__ Mv, const double *__restrict__ Kv,
                              const int32_t *__restrict__ nodes_all, const int32_t *__restrict__ rep, int mp, int nq,
                              TMk tm, double *__restrict__ scratch, int ld, double *__restrict__ Vout,
                              double *__restrict__ VTout, double *__restrict__ Sout, double *__restrict__ sigout,
                              int32_t *__restrict__ info) {
+  // NT threads per class: one warp for the patch classes, a whole CTA for the
+  // (single, large) coarsest level
+#define KSYNC() \
+  do {                              \
+    if (NT == 32) __syncwarp();     \
+    else __syncthreads();           \
+  } while (0)
+  __shared__ double red_off[NT / 32], red_dia[NT / 32];
   const int t = blockIdx.x, lane = threadIdx.x;
   const int32_t *nodes = nodes_all + (rep ? (int64_t)rep[t] * mp : 0);
   int m = 0;
@@ -59,14 +68,14 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
   double *A = scratch + (size_t)t * 3 * mp * mp;  // M -> L
   double *B = A + (size_t)mp * mp;                // K -> X -> C
   double *Q = B + (size_t)mp * mp;
-  for (int e = lane; e < m * m; e += 32) {
+  for (int e = lane; e < m * m; e += NT) {
     int i = e / m, j = e % m;
     int pos = csr_find_k(rowptr, col, nodes[i], nodes[j]);
     A[e] = pos >= 0 ? Mv[pos] : 0.0;
     B[e] = pos >= 0 ? Kv[pos] : 0.0;
     Q[e] = (i == j) ? 1.0 : 0.0;
   }
-  __syncwarp();
+  KSYNC();
   int bad = 0;
   // Cholesky (lower, in place, row-major A[i*m+j], j <= i)
   for (int j = 0; j < m; ++j) {
@@ -74,26 +83,26 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
     for (int p = 0; p < j; ++p) d -= A[j * m + p] * A[j * m + p];
     if (!(d > 0.0)) bad = 1;
     d = sqrt(fmax(d, 1e-300));
-    __syncwarp();
-    for (int i = j + 1 + lane; i < m; i += 32) {
+    KSYNC();
+    for (int i = j + 1 + lane; i < m; i += NT) {
       double s = A[i * m + j];
       for (int p = 0; p < j; ++p) s -= A[i * m + p] * A[j * m + p];
       A[i * m + j] = s / d;
     }
-    __syncwarp();
+    KSYNC();
     if (lane == 0) A[j * m + j] = d;
-    __syncwarp();
+    KSYNC();
   }
   // X = L^-1 K (columns in parallel), then C = L^-1 X^T
-  for (int c = lane; c < m; c += 32)
+  for (int c = lane; c < m; c += NT)
     for (int i = 0; i < m; ++i) {
       double s = B[i * m + c];
       for (int p = 0; p < i; ++p) s -= A[i * m + p] * B[p * m + c];
       B[i * m + c] = s / A[i * m + i];
     }
-  __syncwarp();
+  KSYNC();
   // transpose X in place, then apply L^-1 again (C = L^-1 X^T)
-  for (int e = lane; e < m * m; e += 32) {
+  for (int e = lane; e < m * m; e += NT) {
     int i = e / m, j = e % m;
     if (i < j) {
       double tmp = B[i * m + j];
@@ -101,15 +110,15 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
       B[j * m + i] = tmp;
     }
   }
-  __syncwarp();
-  for (int c = lane; c < m; c += 32)
+  KSYNC();
+  for (int c = lane; c < m; c += NT)
     for (int i = 0; i < m; ++i) {
       double s = B[i * m + c];
       for (int p = 0; p < i; ++p) s -= A[i * m + p] * B[p * m + c];
       B[i * m + c] = s / A[i * m + i];
     }
-  __syncwarp();
-  for (int e = lane; e < m * m; e += 32) {  // symmetrise
+  KSYNC();
+  for (int e = lane; e < m * m; e += NT) {  // symmetrise
     int i = e / m, j = e % m;
     if (i < j) {
       double s = 0.5 * (B[i * m + j] + B[j * m + i]);
@@ -117,11 +126,11 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
       B[j * m + i] = s;
     }
   }
-  __syncwarp();
+  KSYNC();
   // cyclic Jacobi
   for (int sweep = 0; sweep < 60; ++sweep) {
     double off = 0.0, dia = 0.0;
-    for (int e = lane; e < m * m; e += 32) {
+    for (int e = lane; e < m * m; e += NT) {
       int i = e / m, j = e % m;
       if (i != j) off += B[e] * B[e];
       else dia += B[e] * B[e];
@@ -129,6 +138,20 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
     for (int o = 16; o; o >>= 1) {
       off += __shfl_xor_sync(0xffffffffu, off, o);
       dia += __shfl_xor_sync(0xffffffffu, dia, o);
+    }
+    if (NT > 32) {
+      if ((lane & 31) == 0) {
+        red_off[lane >> 5] = off;
+        red_dia[lane >> 5] = dia;
+      }
+      __syncthreads();
+      off = 0.0;
+      dia = 0.0;
+      for (int w = 0; w < NT / 32; ++w) {
+        off += red_off[w];
+        dia += red_dia[w];
+      }
+      __syncthreads();
     }
     if (off <= 1e-32 * dia) break;
     for (int p = 0; p < m - 1; ++p)
@@ -139,8 +162,8 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
         const double theta = (aqq - app) / (2.0 * apq);
         const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
         const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
-        __syncwarp();
-        for (int k2 = lane; k2 < m; k2 += 32) {  // columns p, q
+        KSYNC();
+        for (int k2 = lane; k2 < m; k2 += NT) {  // columns p, q
           double akp = B[k2 * m + p], akq = B[k2 * m + q];
           B[k2 * m + p] = c * akp - s * akq;
           B[k2 * m + q] = s * akp + c * akq;
@@ -148,41 +171,41 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
           Q[k2 * m + p] = c * qkp - s * qkq;
           Q[k2 * m + q] = s * qkp + c * qkq;
         }
-        __syncwarp();
-        for (int k2 = lane; k2 < m; k2 += 32) {  // rows p, q
+        KSYNC();
+        for (int k2 = lane; k2 < m; k2 += NT) {  // rows p, q
           double apk = B[p * m + k2], aqk = B[q * m + k2];
           B[p * m + k2] = c * apk - s * aqk;
           B[q * m + k2] = s * apk + c * aqk;
         }
-        __syncwarp();
+        KSYNC();
         if (lane == 0) {
           B[p * m + q] = 0.0;
           B[q * m + p] = 0.0;
         }
-        __syncwarp();
+        KSYNC();
       }
   }
   // V = L^-T Q (columns in parallel): back substitution with L^T
   double *Vt = Vout + (size_t)t * mp * ld, *VTt = VTout + (size_t)t * mp * ld;
-  for (int e = lane; e < mp * ld; e += 32) {
+  for (int e = lane; e < mp * ld; e += NT) {
     Vt[e] = 0.0;
     VTt[e] = 0.0;
   }
-  __syncwarp();
-  for (int c = lane; c < m; c += 32)
+  KSYNC();
+  for (int c = lane; c < m; c += NT)
     for (int i = m - 1; i >= 0; --i) {
       double s = Q[i * m + c];
       for (int p = i + 1; p < m; ++p) s -= A[p * m + i] * Q[p * m + c];
       Q[i * m + c] = s / A[i * m + i];
     }
-  __syncwarp();
-  for (int e = lane; e < m * m; e += 32) {
+  KSYNC();
+  for (int e = lane; e < m * m; e += NT) {
     int j = e / m, i = e % m;  // node j, mode i
     Vt[j * ld + i] = Q[e];
     VTt[i * ld + j] = Q[e];
   }
   // per mode: S_i = (CE + lambda_i Mt)^-1 by Gauss-Jordan with partial pivoting
-  for (int i = lane; i < mp; i += 32) {
+  for (int i = lane; i < mp; i += NT) {
     const double lam = i < m ? B[i * m + i] : 0.0;
     double a[16], inv[16];
     for (int r = 0; r < nq; ++r)
@@ -216,8 +239,12 @@ __global__ void k_kron_setup(const int32_t *__restrict__ rowptr, const int32_t *
     for (int e = 0; e < nq * nq; ++e) Sout[((size_t)t * mp + i) * nq * nq + e] = inv[e];
     sigout[(size_t)t * mp + i] = inv[(nq - 1) * nq + 0];
   }
-  bad = __any_sync(0xffffffffu, bad);
+  if (NT == 32)
+    bad = __any_sync(0xffffffffu, bad);
+  else
+    bad = __syncthreads_or(bad);
   if (lane == 0) info[t] = bad;
+#undef KSYNC
 }
 
 // ------------------------------------------------------------------- sweep
@@ -697,14 +724,15 @@ TMk make_tmk(const Temporal &T) {
 }  // namespace
 
 void launch_kron_setup(const Level &L, int nq, const Temporal &tm, double *scratch, cudaStream_t s) {
-  k_kron_setup<<<L.ntypes, 32, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, L.pnodes, L.type_rep, L.mp, nq,
+  k_kron_setup<32><<<L.ntypes, 32, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, L.pnodes, L.type_rep, L.mp, nq,
                                        make_tmk(tm), scratch, (L.mp + 1) & ~1, L.kV, L.kVT, L.kS, L.ksig, L.info);
   ++g_launches;
 }
 
 void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal &tm, double *scratch,
                               cudaStream_t s) {
-  k_kron_setup<<<1, 32, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, C.nodes, nullptr, C.mp, nq, make_tmk(tm),
+  k_kron_setup<1024><<<1, 1024, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, L.A.val2, C.nodes, nullptr, C.mp, nq,
+                                         make_tmk(tm),
                                 scratch, C.mp, C.kV, C.kVT, C.kS, C.ksig, C.info);
   ++g_launches;
 }

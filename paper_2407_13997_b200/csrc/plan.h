@@ -28,7 +28,7 @@ constexpr uint8_t kRowGeneric = 254;
 // Type-grouped CTA work list for the Kronecker sweep: ncta x pp patch ids (-1 pad).
 void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type);
 
-void plan_level(int nx, int ny, double h, int k, PlanLevel *P);
+void plan_level(int nx, int ny, double h, int k, PlanLevel *P, bool neumann = false);
 void plan_interpolation(const PlanLevel &C, const PlanLevel &F, int k, std::vector<int32_t> &rowptr,
                         std::vector<int32_t> &col, std::vector<double> &val);
 void transpose_csr(int64_t nrow, int64_t ncol, const std::vector<int32_t> &rp, const std::vector<int32_t> &ci,

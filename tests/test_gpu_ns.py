@@ -149,11 +149,13 @@ def test_ns_fgmres_iteration_count(n, k, N, R, T):
     c.close()
 
 
-def test_ns_newton_cavity():
-    """Newton-FGMRES-WRMG (R22) on a small lid-driven cavity:
-    identical Newton and linear iteration counts, solution within 1e-8."""
+@pytest.mark.parametrize("k", [1, 2])
+def test_ns_newton_cavity(k):
+    """Newton-FGMRES-WRMG (R22) on a small lid-driven cavity,
+    P2-P1 and P3-P2 (C4's pair) x DG1: identical Newton and linear iteration
+    counts, solution within 1e-8."""
     from oracle import ns
-    n, k, q, N, dt, R = 8, 1, 1, 3, 0.05, 10.0
+    n, q, N, dt, R = 8, 1, 3, 0.05, 10.0
     import paper_2407_13997_b200 as w
     c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
                   omega_mg=0.8)
