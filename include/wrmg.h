@@ -81,8 +81,9 @@ typedef struct {
   void *loopback_hub;   /* nranks > 1 without NCCL: hub of wrmg_loopback_create, ranks = host threads of one
                            process sharing one device (tests); NULL = NCCL */
   int32_t smoother;     /* WRMG_SMOOTH_DAMPED (default: nu damped additive sweeps, R15) |
-                           WRMG_SMOOTH_CHEBYSHEV (heat: nu Chebyshev-accelerated steps on [0.25 lam, 1.05 lam],
-                           lam from cheb_steps Arnoldi steps on B A, DESIGN.md R-cheb) */
+                           WRMG_SMOOTH_CHEBYSHEV (nu Chebyshev-accelerated steps on [0.25 lam, 1.05 lam], lam from
+                           cheb_steps Arnoldi steps on B A per level -- re-estimated by every Navier-Stokes
+                           linearisation, DESIGN.md R-cheb; single rank) */
   int32_t cheb_steps;   /* Arnoldi steps of the lambda estimate (0 -> 50, <= 63) */
   uint64_t cheb_seed;   /* seed of the Arnoldi start vector (R6 generator at canonical ids) */
 } wrmg_coeffs;

@@ -278,9 +278,13 @@ def inject(fine, coarse, U):
 
 
 class NSHierarchy:
-    """Levels coarse -> fine; operators = Jacobians at the injected state W."""
+    """Levels coarse -> fine; operators = Jacobians at the injected state W.
+    smoother_kind = "chebyshev": nu_pre / nu_post Chebyshev-accelerated relaxation
+    steps (DESIGN.md R-cheb) with lambda re-estimated at every
+    linearisation; weight_mode "none" = unweighted additive patches."""
 
-    def __init__(self, nx, ny, h, k, q, N, dt, R, W=None, bc="lid", n_coarse=4, omega_mg=1.0, newton=True):
+    def __init__(self, nx, ny, h, k, q, N, dt, R, W=None, bc="lid", n_coarse=4, omega_mg=1.0, newton=True,
+                 smoother_kind="damped", nu_pre=1, nu_post=1, weight_mode="pou", cheb_steps=50, cheb_seed=7):
         meshes = [Mesh(nx, ny, h)]
         while min(meshes[-1].nx, meshes[-1].ny) > n_coarse:
             m = meshes[-1]
@@ -289,6 +293,8 @@ class NSHierarchy:
         self.probs = [NSProblem(m, k, q, N, dt, R, bc=bc) for m in meshes]
         self.omega_mg = omega_mg
         self.newton = newton
+        self.smoother_kind, self.nu_pre, self.nu_post = smoother_kind, nu_pre, nu_post
+        self.weight_mode, self.cheb_steps, self.cheb_seed = weight_mode, cheb_steps, cheb_seed
         self.P0 = [None]
         for l in range(1, len(self.probs)):
             c, f = self.probs[l - 1], self.probs[l]
@@ -316,11 +322,15 @@ class NSHierarchy:
             if l > 0:
                 patches, _ = vanka_star_patches(p)
                 self.factors.append(smoother.PatchFactors(p, A, patches))
-                self.w.append(smoother.weights(patches, p.ns))
+                self.w.append(smoother.weights(patches, p.ns, self.weight_mode))
             else:
                 self.factors.append(None)
                 self.w.append(None)
         self.coarse = PinnedCoarse(self.probs[0], self.A[0])
+        self.lam = [None] * len(self.probs)
+        if self.smoother_kind == "chebyshev":
+            for l in range(1, len(self.probs)):
+                self.lam[l] = ns_estimate_lambda(self, l)
 
 
 class PinnedCoarse:
@@ -359,21 +369,75 @@ class PinnedCoarse:
         return self.prob.project_pressure(x)
 
 
+def ns_relaxation(H, l, r):
+    """B r: one undamped additive Vanka+star sweep from zero, pressure projected (R19)."""
+    p = H.probs[l]
+    return p.project_pressure(smoother.wr_sweep(p, H.A[l], np.zeros_like(r), r, H.factors[l], 1.0, H.w[l]))
+
+
+def ns_estimate_lambda(H, l):
+    """Largest singular value of the Arnoldi (CGS2) Hessenberg of B A (DESIGN.md
+    R-cheb), start vector = the R6 generator at canonical ids with constrained
+    rows 0 (as for heat, multigrid.estimate_lambda)."""
+    import wrmg_inputs as wi
+    p, A, steps = H.probs[l], H.A[l], H.cheb_steps
+    v = wi.uniform_pm1(np.arange(p.ndof, dtype=np.uint64), H.cheb_seed)
+    v[p.con_st] = 0.0
+    V = [v / np.linalg.norm(v)]
+    Hm = np.zeros((steps + 1, steps))
+    for j in range(steps):
+        w = ns_relaxation(H, l, A @ V[j])
+        Vm = np.array(V)
+        h = Vm @ w
+        w = w - Vm.T @ h
+        h2 = Vm @ w
+        w = w - Vm.T @ h2
+        Hm[:j + 1, j] = h + h2
+        Hm[j + 1, j] = np.linalg.norm(w)
+        V.append(w / Hm[j + 1, j])
+    return float(np.linalg.svd(Hm, compute_uv=False).max())
+
+
+def ns_chebyshev(H, l, u, b, nu):
+    """nu Chebyshev steps on [0.25 lam, 1.05 lam], as
+    multigrid.chebyshev with the Navier-Stokes relaxation."""
+    A, lam = H.A[l], H.lam[l]
+    lo, hi = 0.25 * lam, 1.05 * lam
+    theta, delta = 0.5 * (hi + lo), 0.5 * (hi - lo)
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    d = ns_relaxation(H, l, b - A @ u) / theta
+    u = u + d
+    for _ in range(1, nu):
+        rn = 1.0 / (2.0 * sigma - rho)
+        d = rn * rho * d + (2.0 * rn / delta) * ns_relaxation(H, l, b - A @ u)
+        rho = rn
+        u = u + d
+    return u
+
+
 def vcycle(H, r, l=None):
     """V(1,1) with the additive Vanka+star waveform smoother; pressure projected
-    after every smoother application and on the cycle output (R19)."""
+    after every smoother application and on the cycle output (R19).  With
+    smoother_kind = "chebyshev": V(nu_pre, nu_post) Chebyshev-accelerated."""
     if l is None:
         l = len(H.probs) - 1
     p = H.probs[l]
     if l == 0:
         return H.coarse(r)
     A = H.A[l]
-    u = smoother.wr_sweep(p, A, np.zeros_like(r), r, H.factors[l], H.omega_mg, H.w[l])
-    u = p.project_pressure(u)
+    cheb = H.smoother_kind == "chebyshev"
+    if cheb:
+        u = ns_chebyshev(H, l, np.zeros_like(r), r, H.nu_pre)
+    else:
+        u = smoother.wr_sweep(p, A, np.zeros_like(r), r, H.factors[l], H.omega_mg, H.w[l])
+        u = p.project_pressure(u)
     res = r - A @ u
     rc = transfer.restrict(H.P0[l], res, p.NT)
     ec = vcycle(H, H.probs[l - 1].project_pressure(rc), l - 1)
     u = u + transfer.prolong(H.P0[l], ec, p.NT)
+    if cheb:
+        return ns_chebyshev(H, l, u, r, H.nu_post)
     u = smoother.wr_sweep(p, A, u, r, H.factors[l], H.omega_mg, H.w[l])
     return p.project_pressure(u)
 

@@ -376,6 +376,8 @@ void factor_all(wrmg_ctx *c) {
 }
 
 
+double estimate_lambda(wrmg_ctx *c, int l);
+
 // Navier-Stokes linearisation at the finest-level state W (NULL = zero state):
 // inject W to every level (R13), assemble R N(W) (H1), invert every (patch, slab)
 // block (H4, H5) and the pinned coarse slab blocks (H11).  Synchronises.
@@ -432,6 +434,8 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
       c->err_slab = n;
       throw Err{WRMG_E_SINGULAR, "singular coarse slab block (slab " + std::to_string(n) + ")"};
     }
+  if (c->cheb)  // the relaxed operator changed: new Chebyshev intervals (R-cheb)
+    for (int l = 1; l < nl; ++l) c->lam[l] = estimate_lambda(c, l);
 }
 
 // Hierarchy of Taylor-Hood levels (problem == WRMG_NAVIER_STOKES).
@@ -570,6 +574,17 @@ void setup_ns(wrmg_ctx *c) {
     check_launch();
   }
   CK(cudaStreamSynchronize(s));
+  c->cheb = c->co.smoother == WRMG_SMOOTH_CHEBYSHEV;
+  if (c->cheb) {
+    if (c->co.cheb_steps == 0) c->co.cheb_steps = 50;
+    c->lam.assign(nl, 0.0);
+    c->cd.assign(nl, nullptr);
+    c->cbr.assign(nl, nullptr);
+    for (int l = 1; l < nl; ++l) {
+      c->cd[l] = dalloc<double>(c->lv[l].nnode * c->nt);
+      c->cbr[l] = dalloc<double>(c->lv[l].nnode * c->nt);
+    }
+  }
   factor_all_ns(c, nullptr);
 }
 
@@ -932,8 +947,8 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (coeffs->problem == WRMG_HEAT && coeffs->bc != WRMG_BC_DIRICHLET0 && coeffs->bc != WRMG_BC_NEUMANN)
       throw Err{WRMG_E_UNSUPPORTED, "heat: bc must be WRMG_BC_DIRICHLET0 or WRMG_BC_NEUMANN"};
     if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV &&
-        (coeffs->problem != WRMG_HEAT || coeffs->nranks > 1 || coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
-      throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: heat, single rank, cheb_steps <= 63"};
+        (coeffs->nranks > 1 || coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
+      throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: single rank, cheb_steps <= 63"};
     if (coeffs->bc == WRMG_BC_NEUMANN && coeffs->nranks > 1)
       throw Err{WRMG_E_UNSUPPORTED, "Neumann boundaries on strips are not built"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};

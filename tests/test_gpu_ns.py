@@ -167,3 +167,36 @@ def test_ns_newton_cavity(k):
     assert its == len(lin) and lin_its == sum(lin)
     assert_parity(_host(U), Uref, tol=1e-8, what="Newton solution")
     c.close()
+
+
+def test_ns_chebyshev_vcycle_and_newton():
+    """Chebyshev-accelerated V(2,2) on the Vanka+star smoother (PAPER.md:366-379,
+    R-cheb; unweighted patches) for the lid-driven cavity: lambda per level
+    (re-estimated at every linearisation), one cycle, and Newton-FGMRES-WRMG
+    with identical Newton and linear counts."""
+    import paper_2407_13997_b200 as w
+    from oracle import ns
+    n, k, q, N, dt, R = 8, 1, 1, 4, 0.001, 10.0
+    kw = dict(bc="lid")
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, weights="none",
+                  nu_pre=2, nu_post=2, smoother="chebyshev", **kw)
+    H = ns.NSHierarchy(n, n, 1.0 / n, k, q, N, dt, R, smoother_kind="chebyshev", nu_pre=2, nu_post=2,
+                       weight_mode="none", **kw)
+    for l in range(1, len(H.probs)):
+        assert abs(c.cheb_lambda(l) - H.lam[l]) <= 1e-10 * H.lam[l]
+    p = H.fine
+    f = wi.spacetime_field(p.ns, N, q, 5)
+    b = c.empty()
+    c.rhs(_dev(f), b)
+    bref = f.copy()
+    bref[p.con_st] = 0.0
+    bref = p.project_pressure(bref)
+    z = c.empty()
+    c.vcycle(b, z)
+    assert_parity(_host(z), ns.vcycle(H, bref), what="Chebyshev V(2,2)")
+    Uref, hist, lin = ns.newton(H, rtol=1e-8, maxit=12)
+    U = c.zeros()
+    its, lin_its, st = c.newton(U, rtol=1e-8, maxit=12)
+    assert st == "WRMG_OK" and its == len(lin) and lin_its == sum(lin)
+    assert_parity(_host(U), Uref, tol=1e-8, what="Newton solution")
+    c.close()
