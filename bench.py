@@ -130,6 +130,32 @@ def barrier(ws):
         dist.barrier()
 
 
+def ncu_traffic(kclass):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the finest-level launch of
+    the kernel behind a timing class, from the committed `ncu --set full` summary
+    of the C2 bench (profiles/r01_v15_c2_ncu.txt); (None, None) if absent."""
+    import re
+    names = {"residual": "k_residual_tma", "sweep": "k_sweep_kron_mma", "krylov": "k_krylov"}
+    path = os.path.join(ROOT, "profiles", "r01_v15_c2_ncu.txt")
+    if kclass not in names or not os.path.exists(path):
+        return None, None
+    best = None
+    for block in open(path).read().split("## ")[1:]:
+        if names[kclass] not in block.splitlines()[0]:
+            continue
+        vals = {}
+        for key in ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"):
+            m = re.search(key + r"\s+([0-9.]+)\s+(\w+)", block)
+            if m:
+                scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "us": 1.0, "ms": 1e3}.get(m.group(2), 1.0)
+                vals[key] = float(m.group(1)) * scale
+        if len(vals) == 3 and (best is None or vals["gpu__time_duration.sum"] > best[0]):
+            best = (vals["gpu__time_duration.sum"], vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
+    if best is None:
+        return None, None
+    return best[1], "profiles/r01_v15_c2_ncu.txt (ncu --set full, finest-level launch)"
+
+
 # --------------------------------------------------------------------- oracle
 def oracle_sample(n, N, repeats=1):
     """Time the oracle (as it stands) on a bounded sample: the C2 discretisation
@@ -471,7 +497,7 @@ def run_gpu(args, ws, rank, local):
         roof = {"bound": "hbm", "achieved": ks["bytes"] / ks["launches"] / (per_launch_ms / 1e3) / 1e9,
                 "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(kname)
     roof["kernel"] = f"{kname} (level {klvl} of {lay['nlevels']}, finest = {lay['nlevels'] - 1})"
     roof["share_of_kernel_time"] = ks["ms"] / tot_ms if tot_ms else None
     roof["peak_source"] = (hbm_src if roof["bound"] == "hbm" else
