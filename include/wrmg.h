@@ -251,6 +251,11 @@ wrmg_status wrmg_plan(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t 
  * may be NULL.  Buffers are host memory owned by the caller. */
 wrmg_status wrmg_plan_patches(const wrmg_mesh *mesh, int32_t degree, int32_t *nodes, int32_t *sizes);
 
+/* Host-only test hook: eigenvalues (wr + i wi) of the n x n row-major upper
+ * Hessenberg H by the Francis double-shift QR iteration used for the Chebyshev
+ * eigenvalue estimate (R-cheb).  WRMG_E_NOT_CONVERGED if the iteration fails. */
+wrmg_status wrmg_hessenberg_eig(const double *H, int32_t n, double *wr, double *wi);
+
 /* Host-only: the strip plan of one rank (mesh->x0, mesh->nx
  * its cell columns).  info[16] = {G0, own0, own1, lg0, nlg, rg0, nrg, sl0, nsl,
  * sr0, nsr, Lx, Ly, cx0, nxl, 0}: global column of local column 0, owned local

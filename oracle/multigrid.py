@@ -88,9 +88,8 @@ def estimate_lambda(L, steps=50, seed=7):
     (PAPER.md:366-371: "50 steps of relaxation-preconditioned GMRES").  Reading
     (DESIGN.md R-cheb): `steps` Arnoldi steps (classical Gram-Schmidt twice) on B A
     from the seeded vector U[-1,1) at the canonical ids (generator of R6, `seed`,
-    constrained rows 0), and the estimate is the largest singular value of the
-    (steps+1) x steps Hessenberg -- the quantity PETSc's Chebyshev eigenvalue
-    estimate uses."""
+    constrained rows 0), and the estimate is the largest modulus among the Ritz
+    values (eigenvalues of the square steps x steps Hessenberg)."""
     import wrmg_inputs as wi
     p = L.prob
     v = wi.uniform_pm1(np.arange(p.ndof, dtype=np.uint64), seed)
@@ -107,7 +106,7 @@ def estimate_lambda(L, steps=50, seed=7):
         Hm[:j + 1, j] = h + h2
         Hm[j + 1, j] = np.linalg.norm(w)
         V.append(w / Hm[j + 1, j])
-    return float(np.linalg.svd(Hm, compute_uv=False).max())
+    return float(np.abs(np.linalg.eigvals(Hm[:steps, :steps])).max())
 
 
 def chebyshev(L, u, b, lam, nu):

@@ -376,7 +376,7 @@ def ns_relaxation(H, l, r):
 
 
 def ns_estimate_lambda(H, l):
-    """Largest singular value of the Arnoldi (CGS2) Hessenberg of B A (DESIGN.md
+    """Largest |Ritz value| of the Arnoldi (CGS2) Hessenberg of B A (DESIGN.md
     R-cheb), start vector = the R6 generator at canonical ids with constrained
     rows 0 (as for heat, multigrid.estimate_lambda)."""
     import wrmg_inputs as wi
@@ -395,7 +395,7 @@ def ns_estimate_lambda(H, l):
         Hm[:j + 1, j] = h + h2
         Hm[j + 1, j] = np.linalg.norm(w)
         V.append(w / Hm[j + 1, j])
-    return float(np.linalg.svd(Hm, compute_uv=False).max())
+    return float(np.abs(np.linalg.eigvals(Hm[:steps, :steps])).max())
 
 
 def ns_chebyshev(H, l, u, b, nu):

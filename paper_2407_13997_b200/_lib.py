@@ -71,6 +71,7 @@ _sig = {
     "wrmg_launch_count": (c_i64, []),
     "wrmg_debug_fetch": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64]),
     "wrmg_nccl_unique_id": (c_i32, [c_vp]),
+    "wrmg_hessenberg_eig": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
     "wrmg_plan_strip": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, c_vp, c_vp, _P(c_i64)]),
     "wrmg_loopback_create": (c_i32, [c_i32, _P(c_vp)]),
     "wrmg_loopback_destroy": (None, [c_vp]),

@@ -20,6 +20,7 @@ using namespace wrmg;
 
 namespace wrmg {
 int64_t g_launches = 0;
+bool hessenberg_eigenvalues(std::vector<double> &a, int n, std::vector<double> &wr, std::vector<double> &wi);
 }
 
 namespace {
@@ -601,51 +602,11 @@ int64_t ndof_level(const wrmg_ctx *c, int l) { return c->lv[l].nnode * c->nt; }
 
 // z = B r on level l (H12): V(nu_pre, nu_post), zero initial guess.
 // ------------------------------------------------------------ Chebyshev
-// Largest singular value of the row-major (m+1) x m Hessenberg: eigenvalues of
-// the symmetric H^T H by cyclic Jacobi (DESIGN.md R-cheb).
-double hess_sigma_max(const std::vector<double> &H, int m) {
-  std::vector<double> S((size_t)m * m, 0.0);
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < m; ++j) {
-      double t = 0.0;
-      for (int k2 = 0; k2 <= m; ++k2) t += H[(size_t)k2 * m + i] * H[(size_t)k2 * m + j];
-      S[(size_t)i * m + j] = t;
-    }
-  double nrm = 0.0;
-  for (double v : S) nrm += v * v;
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0;
-    for (int i = 0; i < m; ++i)
-      for (int j = i + 1; j < m; ++j) off += S[(size_t)i * m + j] * S[(size_t)i * m + j];
-    if (off <= 1e-32 * nrm) break;
-    for (int p = 0; p < m; ++p)
-      for (int q = p + 1; q < m; ++q) {
-        const double apq = S[(size_t)p * m + q];
-        if (apq == 0.0) continue;
-        const double th = (S[(size_t)q * m + q] - S[(size_t)p * m + p]) / (2.0 * apq);
-        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
-        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
-        for (int k2 = 0; k2 < m; ++k2) {  // columns p, q
-          const double a = S[(size_t)k2 * m + p], b = S[(size_t)k2 * m + q];
-          S[(size_t)k2 * m + p] = cs * a - sn * b;
-          S[(size_t)k2 * m + q] = sn * a + cs * b;
-        }
-        for (int k2 = 0; k2 < m; ++k2) {  // rows p, q
-          const double a = S[(size_t)p * m + k2], b = S[(size_t)q * m + k2];
-          S[(size_t)p * m + k2] = cs * a - sn * b;
-          S[(size_t)q * m + k2] = sn * a + cs * b;
-        }
-      }
-  }
-  double mx = 0.0;
-  for (int i = 0; i < m; ++i) mx = std::max(mx, S[(size_t)i * m + i]);
-  return std::sqrt(mx);
-}
-
 void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om);
 
 // lam_l: `steps` Arnoldi steps (CGS2) on B A from the seeded start vector, B one
-// undamped sweep from zero (DESIGN.md R-cheb).
+// undamped sweep from zero; the estimate is the largest |Ritz value| (PAPER.md:366-371:
+// "estimate the largest eigenvalue"; DESIGN.md R-cheb).
 double estimate_lambda(wrmg_ctx *c, int l) {
   cudaStream_t s = c->stream;
   Level &L = c->lv[l];
@@ -705,7 +666,12 @@ double estimate_lambda(wrmg_ctx *c, int l) {
   for (auto v : V) dfree(v);
   dfree(w);
   dfree(t);
-  return hess_sigma_max(H, steps);
+  // largest |Ritz value|: eigenvalues of the square Hessenberg (R-cheb)
+  std::vector<double> Hs(H.begin(), H.begin() + (size_t)steps * steps), wr, wi;
+  if (!hessenberg_eigenvalues(Hs, steps, wr, wi)) throw Err{WRMG_E_NOT_CONVERGED, "Ritz values did not converge"};
+  double mx = 0.0;
+  for (int i = 0; i < steps; ++i) mx = std::max(mx, std::hypot(wr[i], wi[i]));
+  return mx;
 }
 
 // nu Chebyshev steps for B A x = B b on [0.25 lam, 1.05 lam]:
@@ -1574,6 +1540,17 @@ wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
 }
 
 int64_t wrmg_launch_count(void) { return g_launches; }
+
+wrmg_status wrmg_hessenberg_eig(const double *H, int32_t n, double *wr, double *wi) {
+  if (!H || !wr || !wi || n < 1) return WRMG_E_INVALID;
+  std::vector<double> a(H, H + (size_t)n * n), r, i;
+  if (!hessenberg_eigenvalues(a, n, r, i)) return WRMG_E_NOT_CONVERGED;
+  for (int k = 0; k < n; ++k) {
+    wr[k] = r[k];
+    wi[k] = i[k];
+  }
+  return WRMG_OK;
+}
 
 wrmg_status wrmg_nccl_unique_id(void *out128) {
   if (!out128) return WRMG_E_INVALID;

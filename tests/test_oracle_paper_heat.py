@@ -49,9 +49,8 @@ def test_chebyshev_degree_one_is_optimally_damped_relaxation():
 
 
 def test_lambda_estimate_bounds_the_relaxed_operator():
-    """The Arnoldi estimate is a Ritz-type value of B A: below the 2-norm of B A
-    (power-iteration upper bound from below) and above the largest eigenvalue
-    modulus of the Hessenberg (singular values dominate eigenvalues)."""
+    """The Arnoldi estimate is a Ritz value of B A: of the size of the power-
+    iteration growth rate of B A (which converges to the spectral radius)."""
     H, p, b = paper_problem(1, 1, 1, steps=20)
     L, lam = H.levels[-1], H.lam[-1]
     rng = np.random.default_rng(0)
