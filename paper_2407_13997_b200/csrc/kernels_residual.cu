@@ -353,167 +353,6 @@ __global__ void __launch_bounds__(256) k_residual_l1(int Lx, int Ly, int N, cons
   }
 }
 
-// ---- persistent, double-buffered TMA variant: one CTA (16 warps) per SM walks
-// its (tile, 32-slab chunk) items in order; the TMA copy of item i+1 lands in the
-// other shared-memory stage while item i is computed, and the b loads of a warp's
-// rows are issued before the stage wait, so neither DRAM nor TMA latency sits on
-// the critical path of the stencil loop.
-template <int NQ>
-__global__ void __launch_bounds__(512, 1) k_residual_pipe(const __grid_constant__ CUtensorMap umap, int k, int Lx,
-                                                          int Ly, int N, const uint8_t *__restrict__ rcls,
-                                                          const double *__restrict__ b, double *__restrict__ r,
-                                                          TMr tm, const StencilTab T, int apply, int ntiles) {
-  extern __shared__ __align__(128) double su[];
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double prevq[TR * TR];
-  // class tables in shared memory: warp-uniform broadcast loads instead of
-  // dynamically indexed constant-bank loads (LDC) in the stencil loop
-  __shared__ __align__(16) double2 smk[kStencilMaxC * kStencilMaxE];
-  __shared__ int soff[kStencilMaxC * kStencilMaxE];
-  __shared__ int scnt[kStencilMaxC];
-  constexpr int W = 32 * NQ;
-  constexpr int RPW = TR * TR / 16;  // rows per warp
-  const int64_t NT = (int64_t)N * NQ;
-  const int ntx = (Lx + TR - 1) / TR;
-  const int RW = TR + 2 * k;
-  const int64_t stage = (int64_t)RW * RW * W;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const unsigned bytes = (unsigned)(stage * sizeof(double));
-  const int nchunk = (N + 31) / 32;
-  const int mytiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int nitems = mytiles * nchunk;
-  auto issue = [&](int it, int st) {
-    const int tile = blockIdx.x + (it / nchunk) * gridDim.x, ch = it % nchunk;
-    const int tx0 = (tile % ntx) * TR, ty0 = (tile / ntx) * TR;
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_expect_tx(&bar[st], bytes);
-    tma_load_3d(su + st * stage, &umap, ch * 32 * NQ, tx0 - k, ty0 - k, &bar[st]);
-  };
-  for (int e = tid; e < T.ncls * kStencilMaxE; e += blockDim.x) {
-    const int c = e / kStencilMaxE, x = e - c * kStencilMaxE;
-    smk[e] = make_double2(T.m[c][x], T.kk[c][x]);
-    soff[e] = T.off[c][x];
-  }
-  for (int c = tid; c < T.ncls; c += blockDim.x) scnt[c] = T.cnt[c];
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    if (nitems > 0) issue(0, 0);
-  }
-  __syncthreads();
-  for (int it = 0; it < nitems; ++it) {
-    const int st = it & 1;
-    if (tid == 0 && it + 1 < nitems) issue(it + 1, st ^ 1);  // stage st^1 was released by the barrier below
-    const int tile = blockIdx.x + (it / nchunk) * gridDim.x, ch = it % nchunk;
-    const int tx0 = (tile % ntx) * TR, ty0 = (tile / ntx) * TR;
-    if (ch == 0) {
-      if (tid < TR * TR) prevq[tid] = 0.0;
-      __syncthreads();
-    }
-    const int n = ch * 32 + lane;
-    const bool valid = n < N;
-    double bpre[RPW][NQ];
-    int cpre[RPW];
-#pragma unroll
-    for (int j = 0; j < RPW; ++j) {
-      const int rr = wid + 16 * j;
-      const int I = tx0 + rr % TR, J = ty0 + rr / TR;
-      const bool in = I < Lx && J < Ly;
-      const int64_t base = ((int64_t)J * Lx + I) * NT + (int64_t)n * NQ;
-      cpre[j] = in ? (int)__ldg(rcls + (int64_t)J * Lx + I) : 0;
-#pragma unroll
-      for (int a = 0; a < NQ; ++a) bpre[j][a] = (in && valid && !apply) ? __ldg(b + base + a) : 0.0;
-    }
-    mbar_wait(&bar[st], (it >> 1) & 1);
-    const double *sb = su + st * stage;
-    // two rows per pass: their stencil loops are interleaved (independent shared
-    // loads in flight); zero-padded table entries let both run to the larger count
-#pragma unroll
-    for (int j = 0; j < RPW; j += 2) {
-      int rrv[2], clsv[2], cntv[2];
-      bool inr[2];
-      const double *ownv[2];
-      int64_t basev[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rr = wid + 16 * (j + h);
-        const int I = tx0 + rr % TR, J = ty0 + rr / TR;
-        rrv[h] = rr;
-        inr[h] = I < Lx && J < Ly;
-        basev[h] = ((int64_t)J * Lx + I) * NT + (int64_t)n * NQ;
-        ownv[h] = sb + ((J - ty0 + k) * RW + (I - tx0 + k)) * W + lane * NQ;
-        const int c = cpre[j + h];
-        clsv[h] = (inr[h] && c < T.ncls) ? c : -1;
-        cntv[h] = clsv[h] >= 0 ? scnt[clsv[h]] : 0;
-        if (inr[h] && clsv[h] < 0 && valid)  // constrained row (identity)
-#pragma unroll
-          for (int a2 = 0; a2 < NQ; ++a2)
-            r[basev[h] + a2] = apply ? ownv[h][a2] : bpre[j + h][a2] - ownv[h][a2];
-      }
-      double am[2][NQ], ak[2][NQ];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int a2 = 0; a2 < NQ; ++a2) am[h][a2] = ak[h][a2] = 0.0;
-      const int cmax = max(cntv[0], cntv[1]);
-      const double2 *mk0 = smk + max(clsv[0], 0) * kStencilMaxE, *mk1 = smk + max(clsv[1], 0) * kStencilMaxE;
-      const int *of0 = soff + max(clsv[0], 0) * kStencilMaxE, *of1 = soff + max(clsv[1], 0) * kStencilMaxE;
-      const bool z0 = clsv[0] < 0, z1 = clsv[1] < 0;
-      for (int e0 = 0; e0 < cmax; e0 += 4) {
-#pragma unroll
-        for (int e = e0; e < e0 + 4; ++e) {
-          const double2 w0 = z0 ? make_double2(0.0, 0.0) : mk0[e];
-          const double2 w1 = z1 ? make_double2(0.0, 0.0) : mk1[e];
-          const double *u0 = ownv[0] + (z0 ? 0 : of0[e]);
-          const double *u1 = ownv[1] + (z1 ? 0 : of1[e]);
-          if constexpr (NQ == 2) {
-            const double2 x0 = *reinterpret_cast<const double2 *>(u0);
-            const double2 x1 = *reinterpret_cast<const double2 *>(u1);
-            am[0][0] = fma(w0.x, x0.x, am[0][0]);
-            am[0][1] = fma(w0.x, x0.y, am[0][1]);
-            ak[0][0] = fma(w0.y, x0.x, ak[0][0]);
-            ak[0][1] = fma(w0.y, x0.y, ak[0][1]);
-            am[1][0] = fma(w1.x, x1.x, am[1][0]);
-            am[1][1] = fma(w1.x, x1.y, am[1][1]);
-            ak[1][0] = fma(w1.y, x1.x, ak[1][0]);
-            ak[1][1] = fma(w1.y, x1.y, ak[1][1]);
-          } else {
-#pragma unroll
-            for (int a2 = 0; a2 < NQ; ++a2) {
-              const double x0 = u0[a2], x1 = u1[a2];
-              am[0][a2] = fma(w0.x, x0, am[0][a2]);
-              ak[0][a2] = fma(w0.y, x0, ak[0][a2]);
-              am[1][a2] = fma(w1.x, x1, am[1][a2]);
-              ak[1][a2] = fma(w1.y, x1, ak[1][a2]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double jm = __shfl_up_sync(0xffffffffu, am[h][NQ - 1], 1);
-        if (lane == 0) jm = prevq[rrv[h]];
-        const double last = __shfl_sync(0xffffffffu, am[h][NQ - 1], 31);
-        if (valid && clsv[h] >= 0) {
-#pragma unroll
-          for (int a2 = 0; a2 < NQ; ++a2) {
-            double acc = bpre[j + h][a2];
-#pragma unroll
-            for (int c = 0; c < NQ; ++c) acc -= tm.CE[a2 * NQ + c] * am[h][c] + tm.Mt[a2 * NQ + c] * ak[h][c];
-            if (a2 == 0 && n > 0) acc += jm;
-            r[basev[h] + a2] = apply ? -acc : acc;
-          }
-        }
-        __syncwarp();
-        if (lane == 0 && clsv[h] >= 0) prevq[rrv[h]] = last;
-      }
-    }
-    __syncthreads();  // stage st consumed; prevq of this chunk published
-  }
-}
-
-constexpr bool kResidualPipe = false;  // persistent 1-CTA/SM variant (slower on C2: 403 vs ~390 us)
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -620,33 +459,6 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
   if (smem > 200 * 1024) return false;
   const size_t tab = (size_t)L.stencil.ncls * kStencilMaxE * (sizeof(double2) + sizeof(int));
   CUtensorMap umap;
-  if (kResidualPipe && 2 * smem <= 210 * 1024 && RW <= 256 && 32 * (q + 1) <= 256 &&
-      umap_for(u, (int64_t)N * (q + 1), L.Lx, L.Ly, 32 * (q + 1), RW, &umap)) {
-    const int ntiles = ntx * nty;
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(ntiles, nsm);
-#define WRMG_RP(NQ)                                                                                          \
-    {                                                                                                        \
-      static bool attr = false;                                                                              \
-      if (!attr) {                                                                                           \
-        cudaFuncSetAttribute(k_residual_pipe<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);  \
-        attr = true;                                                                                         \
-      }                                                                                                      \
-      k_residual_pipe<NQ><<<grid, 512, 2 * smem, s>>>(umap, k, L.Lx, L.Ly, N, L.rcls, b, r, t, L.stencil,    \
-                                                       apply, ntiles);                                       \
-      ++g_launches;                                                                                          \
-      return true;                                                                                           \
-    }
-    switch (q) {
-      case 0: WRMG_RP(1);
-      case 1: WRMG_RP(2);
-      case 2: WRMG_RP(3);
-      default: WRMG_RP(4);
-    }
-#undef WRMG_RP
-  }
   if (RW <= 256 && 32 * (q + 1) <= 256 && umap_for(u, (int64_t)N * (q + 1), L.Lx, L.Ly, 32 * (q + 1), RW, &umap)) {
 #define WRMG_RT(NQ)                                                                                          \
     {                                                                                                        \
