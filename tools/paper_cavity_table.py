@@ -28,7 +28,8 @@ def main():
             for R in (1.0, 10.0, 100.0):
                 t0 = time.time()
                 c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=T / N, ncoarse=10, problem="ns",
-                              reynolds=R, bc="lid", weights="none", nu_pre=2, nu_post=2, smoother="chebyshev")
+                              reynolds=R, bc="lid", weights=os.environ.get("WRMG_WEIGHTS", "none"), nu_pre=2,
+                              nu_post=2, smoother="chebyshev")
                 U = c.zeros()
                 torch.cuda.synchronize()
                 t1 = time.time()
