@@ -90,3 +90,11 @@ def test_strip_plans_and_halo_over_gloo(world, snx, gny, k):
     assert len(allv) == len(set(allv.tolist()))
     assert sorted(allv.tolist()) == sorted(int(v) for v in verts)
 
+
+
+def test_nccl_transport_loads_and_creates_unique_ids():
+    """The NCCL transport of the strips (comm.cu) opens libnccl.so.2 at run time;
+    rank 0's unique id is 128 bytes and differs between calls (no device needed)."""
+    import paper_2407_13997_b200 as w
+    a, b = w.nccl_unique_id(), w.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b and any(a)
