@@ -666,10 +666,10 @@ __global__ void __launch_bounds__(NTH) k_ns_factor_row(int mp, int N, int64_t ms
                                                         const int32_t *__restrict__ pvv) {
   __shared__ __align__(16) double prow[MMAX];
   __shared__ int nodes[MMAX / NQ + 1], pcs[MMAX];
-  __shared__ double s_wv[NTH / 32];
-  __shared__ int s_wi[NTH / 32];
-  __shared__ double s_tol;
-  __shared__ int s_p, s_info;
+  __shared__ double s_wv[2 * (NTH / 32)];
+  __shared__ int s_wi[2 * (NTH / 32)];
+  __shared__ double s_tol, s_pv;
+  __shared__ int s_info;
   const int m = NQ * mp;
   const int64_t p = blockIdx.x;
   const int n = blockIdx.y;
@@ -747,49 +747,55 @@ __global__ void __launch_bounds__(NTH) k_ns_factor_row(int mp, int N, int64_t ms
             bi = oi;
           }
         }
+        // per-warp maxima; every thread combines them itself (no second barrier).
+        // Double-buffered by step parity: a fast warp may publish step c+1 while a
+        // slow one still reads step c.
         if (lane == 0) {
-          s_wv[w] = bv;
-          s_wi[w] = bi;
+          s_wv[(c & 1) * NW + w] = bv;
+          s_wi[(c & 1) * NW + w] = bi;
         }
         __syncthreads();
+        double pv = s_wv[(c & 1) * NW];
+        int pr = s_wi[(c & 1) * NW];
+#pragma unroll
+        for (int k2 = 1; k2 < NW; ++k2) {
+          const double v2 = s_wv[(c & 1) * NW + k2];
+          const int i2 = s_wi[(c & 1) * NW + k2];
+          if (v2 > pv || (v2 == pv && i2 < pr)) {
+            pv = v2;
+            pr = i2;
+          }
+        }
         if (r == 0) {
-          double v = s_wv[0];
-          int ix = s_wi[0];
-          for (int k2 = 1; k2 < NW; ++k2)
-            if (s_wv[k2] > v || (s_wv[k2] == v && s_wi[k2] < ix)) {
-              v = s_wv[k2];
-              ix = s_wi[k2];
-            }
-          s_p = ix;
-          pcs[c] = ix;
-          if (!(v >= s_tol) && s_info == 0) s_info = c + 1;
+          pcs[c] = pr;
+          if (!(pv >= s_tol) && s_info == 0) s_info = c + 1;
+        }
+        if (r == pr) {  // publish the raw pivot row (block columns from blk) and the pivot
+#pragma unroll
+          for (int j = 0; j < MMAX; j += 2) *reinterpret_cast<double2 *>(prow + j) = make_double2(a[j], a[j + 1]);
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) prow[cb * 8 + k2] = blk[k2];
+          s_pv = ac;
         }
         __syncthreads();
-        const int pr = s_p;
+        const double piv = s_pv, pinv = piv != 0.0 ? 1.0 / piv : 0.0;
         if (r == pr) {  // pivot row: column c <- 1, then scale (column c becomes 1 / pivot)
-          const double pinv = ac != 0.0 ? 1.0 / ac : 0.0;
 #pragma unroll
           for (int j = 0; j < MMAX; ++j) a[j] *= pinv;
 #pragma unroll
           for (int k2 = 0; k2 < 8; ++k2) blk[k2] = (k2 == k) ? pinv : blk[k2] * pinv;
-#pragma unroll
-          for (int j = 0; j < MMAX; j += 2) *reinterpret_cast<double2 *>(prow + j) = make_double2(a[j], a[j + 1]);
-#pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2) prow[cb * 8 + k2] = blk[k2];  // the block's true values
           used = true;
           mystep = c;
-        }
-        __syncthreads();
-        if (r != pr && live) {
-          const double f = ac;
+        } else if (live) {  // eliminate with the raw pivot row: f / pivot folded into the multiplier
+          const double fs = ac * pinv;
 #pragma unroll
           for (int j = 0; j < MMAX; j += 2) {
-            const double2 pv = *reinterpret_cast<const double2 *>(prow + j);
-            a[j] = fma(-f, pv.x, a[j]);
-            a[j + 1] = fma(-f, pv.y, a[j + 1]);
+            const double2 pw = *reinterpret_cast<const double2 *>(prow + j);
+            a[j] = fma(-fs, pw.x, a[j]);
+            a[j + 1] = fma(-fs, pw.y, a[j + 1]);
           }
 #pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2) blk[k2] = (k2 == k) ? -f * prow[c] : fma(-f, prow[cb * 8 + k2], blk[k2]);
+          for (int k2 = 0; k2 < 8; ++k2) blk[k2] = (k2 == k) ? -fs : fma(-fs, prow[cb * 8 + k2], blk[k2]);
         }
         // prow is rewritten only after the next step's first barrier
       }
