@@ -91,3 +91,19 @@ def test_newton_cavity_converges_quadratically():
     U, hist, lin = ns.newton(H, rtol=1e-8, maxit=12)
     assert hist[-1] <= 1e-8 * hist[0]
     assert len(hist) <= 8
+
+
+def test_ns_chebyshev_degree_one_is_damped_vanka():
+    """Chebyshev with nu = 1 is one Vanka+star sweep damped
+    by 1 / theta, theta = 0.65 lam, followed by the pressure projection (R19)."""
+    from oracle import smoother
+    H = ns.NSHierarchy(4, 4, 0.25, 1, 1, 2, 0.01, 10.0, bc="lid", smoother_kind="chebyshev", nu_pre=1,
+                       nu_post=1, weight_mode="none", n_coarse=2, cheb_steps=12)
+    l = len(H.probs) - 1
+    p = H.probs[l]
+    b = wi.spacetime_field(p.ns, 2, 1, 9)
+    b[p.con_st] = 0.0
+    x1 = ns.ns_chebyshev(H, l, np.zeros(p.ndof), b, 1)
+    ref = p.project_pressure(smoother.wr_sweep(p, H.A[l], np.zeros(p.ndof), b, H.factors[l],
+                                               1.0 / (0.65 * H.lam[l]), H.w[l]))
+    assert np.allclose(x1, ref, rtol=1e-12, atol=1e-15)
