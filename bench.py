@@ -136,7 +136,7 @@ def ncu_traffic(kclass):
     of the C2 bench (profiles/r01_v15_c2_ncu.txt); (None, None) if absent."""
     import re
     names = {"residual": "k_residual_tma", "sweep": "k_sweep_kron_mma", "krylov": "k_krylov"}
-    path = os.path.join(ROOT, "profiles", "r01_v15_c2_ncu.txt")
+    path = os.path.join(ROOT, "profiles", "r01_final_c2_ncu.txt")
     if kclass not in names or not os.path.exists(path):
         return None, None
     best = None
@@ -153,7 +153,7 @@ def ncu_traffic(kclass):
             best = (vals["gpu__time_duration.sum"], vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
     if best is None:
         return None, None
-    return best[1], "profiles/r01_v15_c2_ncu.txt (ncu --set full, finest-level launch)"
+    return best[1], "profiles/r01_final_c2_ncu.txt (ncu --set full, finest-level launch)"
 
 
 # --------------------------------------------------------------------- oracle
