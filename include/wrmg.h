@@ -129,8 +129,9 @@ wrmg_status wrmg_linearize(wrmg_ctx *ctx, const double *state);
 wrmg_status wrmg_rhs(wrmg_ctx *ctx, const double *fhat, double *b);
 
 /* b += the initial-state term of eq. dgintime (Y_0^- = y_0, R7): on every free row
- * i and temporal node a of slab 0, phi_a(0) (M u0)_i.  u0: nnode nodal values
- * (device).  Heat only. */
+ * i and temporal node a of slab 0, phi_a(0) (M u0)_i, M the spatial mass (heat) or
+ * the velocity mass M2 (Navier-Stokes; the jump acts on velocity only).  u0:
+ * nnode (heat) / sid (NS) nodal values on the device. */
 wrmg_status wrmg_rhs_initial(wrmg_ctx *ctx, const double *u0, double *b);
 
 /* Largest-eigenvalue estimates of the Chebyshev smoother (R-cheb), level >= 1
@@ -175,9 +176,18 @@ wrmg_status wrmg_level_size(const wrmg_ctx *ctx, int32_t level, int64_t *nnode);
 wrmg_status wrmg_fgmres(wrmg_ctx *ctx, const double *b, double *x, int32_t restart, int32_t maxit,
                         double rtol, double atol, int32_t *iters, double *relres);
 
-/* Navier-Stokes Newton loop (H14): WRMG_E_UNSUPPORTED in this build. */
+/* Navier-Stokes Newton-FGMRES-WRMG (H14, R22): solves F(U) = 0
+ * from U (constrained rows set to the boundary values), relinearising every
+ * level and refactorising every (patch, slab) block at each step, FGMRES(30)
+ * with Eisenstat-Walker forcing (eta_0 = 0.3), until ||F|| <= rtol ||F(U_0)||.
+ * *newton_its = linear solves, *lin_its = total FGMRES iterations.
+ * WRMG_E_NOT_CONVERGED after maxit steps (U holds the last iterate). */
 wrmg_status wrmg_newton(wrmg_ctx *ctx, double *U, double rtol, int32_t maxit, int32_t *newton_its,
                         int32_t *lin_its);
+/* As wrmg_newton for F(U) = rhs (rhs on free rows, NULL = 0): e.g. the
+ * initial-state term of wrmg_rhs_initial for one slab of a timestepping run. */
+wrmg_status wrmg_newton_rhs(wrmg_ctx *ctx, double *U, const double *rhs, double rtol, int32_t maxit,
+                            int32_t *newton_its, int32_t *lin_its);
 
 /* Batched dense LU with partial pivoting (H5, R10) on caller device memory:
  * A holds `batch` column-major m x m matrices (A + b*m*m), overwritten by the

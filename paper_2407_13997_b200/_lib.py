@@ -59,6 +59,7 @@ _sig = {
     "wrmg_level_size": (c_i32, [c_vp, c_i32, _P(c_i64)]),
     "wrmg_fgmres": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_dbl, c_dbl, _P(c_i32), _P(c_dbl)]),
     "wrmg_newton": (c_i32, [c_vp, c_vp, c_dbl, c_i32, _P(c_i32), _P(c_i32)]),
+    "wrmg_newton_rhs": (c_i32, [c_vp, c_vp, c_vp, c_dbl, c_i32, _P(c_i32), _P(c_i32)]),
     "wrmg_batched_lu": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "wrmg_fill_uniform": (c_i32, [c_vp, c_vp, c_i64, ctypes.c_uint64, ctypes.c_uint64]),
     "wrmg_sync": (c_i32, [c_vp]),
@@ -292,9 +293,10 @@ class Context:
             _check(st, self._h)
         return its.value, rel.value, STATUS[st]
 
-    def newton(self, U, rtol=1e-8, maxit=20):
+    def newton(self, U, rtol=1e-8, maxit=20, rhs=None):
         its, lin = c_i32(), c_i32()
-        st = lib.wrmg_newton(self._h, _ptr(U), float(rtol), int(maxit), ctypes.byref(its), ctypes.byref(lin))
+        st = lib.wrmg_newton_rhs(self._h, _ptr(U), None if rhs is None else _ptr(rhs), float(rtol), int(maxit),
+                                 ctypes.byref(its), ctypes.byref(lin))
         if st not in (0, 6):
             _check(st, self._h)
         return its.value, lin.value, STATUS[st]

@@ -1241,7 +1241,6 @@ wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
 
 wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
   if (!c || !u0 || !b) return WRMG_E_INVALID;
-  if (c->ns) return WRMG_E_UNSUPPORTED;
   try {
     launch_rhs_initial(c->lv.back(), c->nq, c->nt, c->tm.phi0, u0, b, c->stream);
     check_launch();
@@ -1608,6 +1607,11 @@ static double eisenstat_walker(double eta_prev, double fn, double fprev) {
 }
 
 wrmg_status wrmg_newton(wrmg_ctx *c, double *U, double rtol, int32_t maxit, int32_t *newton_its, int32_t *lin_its) {
+  return wrmg_newton_rhs(c, U, nullptr, rtol, maxit, newton_its, lin_its);
+}
+
+wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rtol, int32_t maxit, int32_t *newton_its,
+                            int32_t *lin_its) {
   if (!c || !U || maxit < 0) return WRMG_E_INVALID;
   if (!c->ns) {
     c->err = "wrmg_newton: the heat operator is linear";
@@ -1624,7 +1628,7 @@ wrmg_status wrmg_newton(wrmg_ctx *c, double *U, double rtol, int32_t maxit, int3
     }
     // Dirichlet / lid values on the constrained rows of U and of the residual's b (R5)
     launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, U, U, s);
-    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, nullptr, c->nl_b, s);
+    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, rhs, c->nl_b, s);  // F(U) = rhs on free rows, U = g on constrained
     auto negF = [&]() {  // nl_r = -F(U)
       ns_nonlinear_residual(c, U, c->nl_b, c->nl_r);
       return std::sqrt(dot_host(c, c->nl_r, c->nl_r, n));

@@ -200,3 +200,29 @@ def test_ns_chebyshev_vcycle_and_newton():
     assert st == "WRMG_OK" and its == len(lin) and lin_its == sum(lin)
     assert_parity(_host(U), Uref, tol=1e-8, what="Newton solution")
     c.close()
+
+
+def test_ns_newton_with_initial_state():
+    """Newton with the initial-state term (R7; wrmg_rhs_initial + wrmg_newton_rhs):
+    one slab started from a nonzero velocity, as one step of the timestepping
+    comparison; counts and solution equal the oracle's."""
+    import paper_2407_13997_b200 as w
+    from oracle import ns
+    n, k, q, N, dt, R = 8, 1, 0, 1, 0.001, 10.0
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
+                  weights="none", nu_pre=2, nu_post=2, smoother="chebyshev")
+    H = ns.NSHierarchy(n, n, 1.0 / n, k, q, N, dt, R, bc="lid", smoother_kind="chebyshev", nu_pre=2, nu_post=2,
+                       weight_mode="none")
+    p = H.fine
+    u0 = np.zeros(p.ns)
+    x, y = p.vel_xy[:, 0], p.vel_xy[:, 1]
+    u0[:p.Lu] = np.sin(np.pi * x) * np.sin(np.pi * y) ** 2
+    u0[p.Lu:2 * p.Lu] = -np.sin(np.pi * x) ** 2 * np.sin(np.pi * y)
+    Uref, hist, lin = ns.newton(H, rtol=1e-8, maxit=12, u0=u0)
+    rhs = c.zeros()
+    c.rhs_initial(_dev(u0), rhs)
+    U = c.zeros()
+    its, lin_its, st = c.newton(U, rtol=1e-8, maxit=12, rhs=rhs)
+    assert st == "WRMG_OK" and its == len(lin) and lin_its == sum(lin)
+    assert_parity(_host(U), Uref, tol=1e-8, what="Newton with u0")
+    c.close()
