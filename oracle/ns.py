@@ -224,6 +224,48 @@ class NSProblem:
         F[self.con_st] = U[self.con_st] - self.g_st[self.con_st]
         return F
 
+    def jacobian_residual_rows(self, rows, x, b, W, newton=True):
+        """(b - J(W) x) on the given sids for every (slab, temporal node), evaluated
+        row by row from the element integrals (no global space-time matrix): the
+        linear rows of M2, K2 + G (eq. nsfem), the jump
+        -E1 (x) M2 (R1), and R sum_{b,c} T_abc (N(w_{n,c}) x_{n,b}) with N = O (+ Q)
+        (R18) summed over the cells that contain the row's node.  Constrained rows:
+        b - x (R5).  Returns an array (len(rows), N, q+1)."""
+        nq, N, tm, Lu = self.q + 1, self.N, self.tm, self.Lu
+        X, Bv, Wv = self.field_view(x), self.field_view(b), self.field_view(W)
+        L2 = (self.K2 + self.Gb).tocsr()
+        out = np.zeros((len(rows), N, nq))
+        for ir, r in enumerate(rows):
+            r = int(r)
+            if self.constrained[r]:
+                out[ir] = Bv[r] - X[r]
+                continue
+            mrow, lrow = self.M2.getrow(r), L2.getrow(r)
+            Mx = np.einsum("j,jnb->nb", mrow.data, X[mrow.indices]) if mrow.nnz else np.zeros((N, nq))
+            Lx = np.einsum("j,jnb->nb", lrow.data, X[lrow.indices]) if lrow.nnz else np.zeros((N, nq))
+            acc = Mx @ (tm.C + tm.E0).T + Lx @ tm.Mt.T  # acc[n, a] = sum_b CE_ab Mx[n,b] + Mt_ab Lx[n,b]
+            acc[1:, 0] -= Mx[:-1, nq - 1]               # jump: -(E1 M x_{n-1})_a, E1 = e_0 e_q^T (R2)
+            if r < 2 * Lu:  # convection rows
+                d, i = divmod(r, Lu)
+                Nx = np.zeros((N, nq, nq))  # Nx[n, c, b] = (N(w_{n,c}) x_{n,b})_r
+                for dv, dp, To in self.elems:
+                    loc = np.nonzero(dv == i)[0]
+                    if loc.size == 0:
+                        continue
+                    li = int(loc[0])
+                    wl = np.stack([Wv[dv], Wv[Lu + dv]], axis=-1)       # (nloc, N, nq, 2)
+                    xl = np.stack([X[dv], X[Lu + dv]], axis=-1)         # (nloc, N, nq, 2)
+                    # O: sum_l sum_d2 w[l,d2] To[d2, li, l, j] x_d[j]
+                    Ow = np.einsum("lncd,dlj->ncj", wl, To[:, li])     # (N, nq, nloc)
+                    Nx += np.einsum("ncj,jnb->ncb", Ow, xl[..., d])
+                    if newton:  # Q: sum_l w[l,d] To[d2, li, j, l] x_d2[j]
+                        for d2 in range(2):
+                            Qw = np.einsum("lnc,jl->ncj", wl[..., d], To[d2, li])
+                            Nx += np.einsum("ncj,jnb->ncb", Qw, xl[..., d2])
+                acc += self.R * np.einsum("abc,ncb->na", tm.T, Nx)
+            out[ir] = Bv[r] - acc
+        return out
+
     def project_pressure(self, U):
         """Remove the mean of the pressure nodal values per (slab, temporal node) (R19)."""
         V = np.array(self.field_view(U), copy=True)

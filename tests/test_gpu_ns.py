@@ -226,3 +226,35 @@ def test_ns_newton_with_initial_state():
     assert st == "WRMG_OK" and its == len(lin) and lin_its == sum(lin)
     assert_parity(_host(U), Uref, tol=1e-8, what="Newton with u0")
     c.close()
+
+
+def test_C3_fullsize_sampled_jacobian_rows():
+    """C3 at its full size (BASELINE configs[2]: 64x64 P2-P1 x DG1, N = 64, Re = 100,
+    Newton Jacobian at the wind, lid): b - J x from the GPU residual kernel, in the
+    bench's launch configuration, against the oracle's row-by-row element
+    evaluation on sampled velocity and pressure rows (every slab and temporal node)."""
+    import paper_2407_13997_b200 as w
+    from oracle import mesh as omesh
+    from oracle import ns
+    n, k, q, N, R = 64, 1, 1, 64, 100.0
+    dt = 1.0 / N
+    W = wi.wind_state(n, n, 1.0 / n, k, N, q, dt)
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
+                  omega_mg=0.8)
+    c.linearize(_dev(W))
+    p = ns.NSProblem(omesh.unit_square(n), k, q, N, dt, R, bc="lid")
+    x = wi.spacetime_field(p.ns, N, q, 21)
+    b = wi.spacetime_field(p.ns, N, q, 22)
+    r = c.empty()
+    c.residual(_dev(x), _dev(b), r)
+    got = _host(r).reshape(p.ns, N, q + 1)
+    rng = np.random.default_rng(0)
+    Lu, Lux = p.Lu, 2 * n + 1
+    picks = [Lux + 1, 2 * Lux + 2, (Lux // 2) * Lux + Lux // 2, Lu - Lux - 2, Lu + Lux + 1, Lu + 3 * Lux + 5,
+             2 * Lu, 2 * Lu + 66, 2 * Lu + p.Lp - 1]
+    picks += list(rng.integers(0, p.ns, 20))
+    ref = p.jacobian_residual_rows(picks, x, b, W)
+    for ir, s_ in enumerate(picks):
+        e = np.max(np.abs(got[s_] - ref[ir])) / max(np.max(np.abs(ref[ir])), 1e-300)
+        assert e <= 1e-10, (s_, e)
+    c.close()

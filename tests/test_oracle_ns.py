@@ -107,3 +107,16 @@ def test_ns_chebyshev_degree_one_is_damped_vanka():
     ref = p.project_pressure(smoother.wr_sweep(p, H.A[l], np.zeros(p.ndof), b, H.factors[l],
                                                1.0 / (0.65 * H.lam[l]), H.w[l]))
     assert np.allclose(x1, ref, rtol=1e-12, atol=1e-15)
+
+
+def test_jacobian_residual_rows_equal_assembled_operator():
+    """Row-by-row element evaluation of b - J(W) x (used for the full-size C3
+    parity) equals the explicitly assembled space-time Jacobian."""
+    p = ns.NSProblem(mesh.unit_square(4), 1, 1, 3, 0.1, R=50.0)
+    W = 0.5 * wi.spacetime_field(p.ns, 3, 1, 4)
+    x = wi.spacetime_field(p.ns, 3, 1, 5)
+    b = wi.spacetime_field(p.ns, 3, 1, 6)
+    ref = (b - p.jacobian(W) @ x).reshape(p.ns, 3, 2)
+    rows = np.arange(p.ns)
+    got = p.jacobian_residual_rows(rows, x, b, W)
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
