@@ -134,6 +134,16 @@ wrmg_status wrmg_rhs(wrmg_ctx *ctx, const double *fhat, double *b);
  * nnode (heat) / sid (NS) nodal values on the device. */
 wrmg_status wrmg_rhs_initial(wrmg_ctx *ctx, const double *u0, double *b);
 
+/* Navier-Stokes: time-dependent Dirichlet data (R5, R28).  g: device or
+ * host vector of ndof values in the solution layout; only its constrained rows
+ * (boundary velocity DoFs, every slab and temporal node) are read, and
+ * wrmg_newton / wrmg_newton_rhs then impose U = g there instead of the setup's
+ * per-sid values (bc, lid_speed).  Copied (the caller keeps ownership);
+ * g = NULL restores the setup's values.  Synchronises.  Heat contexts:
+ * WRMG_E_UNSUPPORTED.  Used for the Chorin problem, whose
+ * exact velocity decays in time on the boundary. */
+wrmg_status wrmg_set_boundary_values(wrmg_ctx *ctx, const double *g);
+
 /* Largest-eigenvalue estimates of the Chebyshev smoother (R-cheb), level >= 1
  * (0 for the coarsest / damped smoothing).  Host output. */
 wrmg_status wrmg_cheb_lambda(const wrmg_ctx *ctx, int32_t level, double *lam);

@@ -112,6 +112,15 @@ class NSProblem:
         self.vel_xy = xy
         self.p_xy = meshmod.node_coords(mesh, self.kp)
 
+    def set_boundary_data(self, G):
+        """Time-dependent Dirichlet data (R5, R28): the constrained
+        entries of the space-time vector G (solution layout) replace the per-sid
+        boundary values; Newton starts from this lift."""
+        G = np.asarray(G, dtype=float).reshape(-1)
+        if G.size != self.ndof:
+            raise ValueError("boundary data must have ndof entries")
+        self.g_st = np.where(self.con_st, G, 0.0)
+
     # ---------------------------------------------------------------- helpers
     @property
     def ndof(self):
@@ -519,3 +528,49 @@ def newton(H, rtol=1e-8, maxit=20, eta0=0.3, restart=30, u0=None):
         eta = eisenstat_walker(eta, fn, fprev)
         fprev = fn
     return U, hist, lin
+
+
+# ------------------------------------------------------- error functional
+def triangle_rule(npts):
+    """Collapsed (Duffy) Gauss-Legendre rule on the reference triangle
+    {xi, eta >= 0, xi + eta <= 1}: xi = u, eta = v (1 - u), weight (1 - u);
+    exact for polynomials of degree <= 2 npts - 2.  Returns (points (n, 2), weights)."""
+    g, w = np.polynomial.legendre.leggauss(npts)
+    g, w = 0.5 * (g + 1.0), 0.5 * w
+    U, V = np.meshgrid(g, g, indexing="ij")
+    WU, WV = np.meshgrid(w, w, indexing="ij")
+    pts = np.stack([U.ravel(), (V * (1.0 - U)).ravel()], axis=1)
+    return pts, (WU * WV * (1.0 - U)).ravel()
+
+
+def velocity_l2_error(prob, U, exact, nspace=6, ntime=None):
+    """Space-time L2 norm of the velocity error (Table
+    tab:chorin:mg_errors):  ( sum_n int_{I_n} int_Omega |u_h - u|^2 )^(1/2),
+    u_h = sum_i sum_a U[(d,i), n, a] v_i(x) phi_a((t - t_n)/dt) on slab n, by the
+    collapsed Gauss rule per triangle (nspace^2 points) and Gauss-Legendre in time
+    (ntime points, default q + 4).  exact(x, y, t) -> (ux, uy), broadcasting.
+    Post-processing for tests; not part of the solver."""
+    ku, mesh, N, q, dt = prob.ku, prob.mesh, prob.N, prob.q, prob.dt
+    ntime = q + 4 if ntime is None else ntime
+    xi, wx = triangle_rule(nspace)
+    B = fem.evaluate_basis(ku, xi)                        # (nqp, nloc)
+    gt, wt = np.polynomial.legendre.leggauss(ntime)
+    gt, wt = 0.5 * (gt + 1.0), 0.5 * wt
+    Tb = prob.tm.eval(gt)                                 # (ntime, q+1)
+    dofs = fem.cell_dofs(mesh, ku)                        # (ncell, nloc)
+    V = prob.field_view(U)
+    vx = mesh.vertices[mesh.cells]                        # (ncell, 3, 2)
+    J1, J2 = vx[:, 1] - vx[:, 0], vx[:, 2] - vx[:, 0]
+    det = np.abs(J1[:, 0] * J2[:, 1] - J1[:, 1] * J2[:, 0])   # (ncell,)
+    X = vx[:, None, 0, :] + xi[None, :, 0:1] * J1[:, None, :] + xi[None, :, 1:2] * J2[:, None, :]
+    tot = 0.0
+    for n in range(N):
+        t = (n + gt) * dt
+        ex = exact(X[:, :, 0:1], X[:, :, 1:2], t[None, None, :])       # each (ncell, nqp, ntime)
+        err = 0.0
+        for comp in (0, 1):
+            coef = V[comp * prob.Lu + dofs, n, :]                    # (ncell, nloc, q+1)
+            uh = np.einsum("ql,cla,ta->cqt", B, coef, Tb)
+            err = err + (uh - ex[comp]) ** 2
+        tot += dt * np.einsum("c,q,t,cqt->", det, wx, wt, err)
+    return float(np.sqrt(tot))

@@ -50,6 +50,7 @@ _sig = {
     "wrmg_rhs": (c_i32, [c_vp, c_vp, c_vp]),
     "wrmg_rhs_initial": (c_i32, [c_vp, c_vp, c_vp]),
     "wrmg_cheb_lambda": (c_i32, [c_vp, c_i32, _P(c_dbl)]),
+    "wrmg_set_boundary_values": (c_i32, [c_vp, c_vp]),
     "wrmg_residual": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32]),
     "wrmg_apply": (c_i32, [c_vp, c_vp, c_vp]),
     "wrmg_smooth": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_dbl]),
@@ -261,6 +262,10 @@ class Context:
 
     def rhs_initial(self, u0, b):
         _check(lib.wrmg_rhs_initial(self._h, _ptr(u0), _ptr(b)), self._h)
+
+    def set_boundary_values(self, g):
+        """Time-dependent Dirichlet data for Newton (NS; None restores the setup's)."""
+        _check(lib.wrmg_set_boundary_values(self._h, None if g is None else _ptr(g)), self._h)
 
     def cheb_lambda(self, level):
         v = c_dbl()

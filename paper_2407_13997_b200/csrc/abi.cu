@@ -1250,6 +1250,28 @@ wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
   }
 }
 
+wrmg_status wrmg_set_boundary_values(wrmg_ctx *c, const double *g) {
+  if (!c) return WRMG_E_INVALID;
+  if (!c->ns) {
+    c->err = "wrmg_set_boundary_values: Navier-Stokes contexts only";
+    return WRMG_E_UNSUPPORTED;
+  }
+  try {
+    const int64_t n = c->lv.back().nnode * c->nt;
+    if (!g) {
+      if (c->bcg_st) CK(cudaFree(c->bcg_st));
+      c->bcg_st = nullptr;
+      return WRMG_OK;
+    }
+    if (!c->bcg_st) c->bcg_st = dalloc<double>(n);
+    CK(cudaMemcpyAsync(c->bcg_st, g, n * sizeof(double), cudaMemcpyDefault, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
 wrmg_status wrmg_cheb_lambda(const wrmg_ctx *c, int32_t level, double *lam) {
   if (!c || !lam || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
   *lam = c->cheb ? c->lam[level] : 0.0;
@@ -1627,8 +1649,8 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
       c->nl_dx = dalloc<double>(n);
     }
     // Dirichlet / lid values on the constrained rows of U and of the residual's b (R5)
-    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, U, U, s);
-    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, rhs, c->nl_b, s);  // F(U) = rhs on free rows, U = g on constrained
+    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, U, U, s, c->bcg_st);
+    launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, rhs, c->nl_b, s, c->bcg_st);  // F(U) = rhs on free rows, U = g on constrained
     auto negF = [&]() {  // nl_r = -F(U)
       ns_nonlinear_residual(c, U, c->nl_b, c->nl_r);
       return std::sqrt(dot_host(c, c->nl_r, c->nl_r, n));
@@ -1731,7 +1753,7 @@ void wrmg_destroy(wrmg_ctx *c) {
                   (void *)C.Y, (void *)C.piv, (void *)C.info, (void *)C.kV, (void *)C.kVT, (void *)C.kS,
                   (void *)C.ksig, (void *)C.nsD, (void *)C.nsinvT, (void *)C.xq, (void *)C.nspiv, (void *)C.nsinfo})
     dfree(p);
-  for (void *p : {(void *)c->th_ref, (void *)c->th_T, (void *)c->bcg, (void *)c->proj, (void *)c->conv_nl,
+  for (void *p : {(void *)c->th_ref, (void *)c->th_T, (void *)c->bcg, (void *)c->bcg_st, (void *)c->proj, (void *)c->conv_nl,
                   (void *)c->nl_b, (void *)c->nl_r, (void *)c->nl_dx})
     dfree(p);
   for (double *p : c->V) dfree(p);

@@ -188,6 +188,7 @@ struct wrmg_ctx {
   double *th_ref = nullptr, *th_T = nullptr;   // Taylor-Hood reference integrals on the device
   int th_nu = 0, th_np = 0;
   double *bcg = nullptr;                       // finest-level boundary values per sid
+  double *bcg_st = nullptr;                    // wrmg_set_boundary_values: per space-time DoF (NULL: bcg)
   double *proj = nullptr;                      // pressure-projection scratch
   double *conv_nl = nullptr;                   // finest R O(U) for the nonlinear residual
   double *nl_b = nullptr, *nl_r = nullptr, *nl_dx = nullptr;  // Newton work vectors

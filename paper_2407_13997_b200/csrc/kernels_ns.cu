@@ -1137,12 +1137,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256)
 }
 
 // dst = src on free sids; g[s] (or 0) on constrained sids (R5, R6).
+// dst = boundary value on constrained sids (gst: per space-time DoF, else g: per
+// sid, else 0), src (or 0) on free sids
 __global__ void k_ns_mask(int64_t ns, int64_t NT, const uint8_t *__restrict__ con, const double *__restrict__ g,
-                          const double *__restrict__ src, double *__restrict__ dst) {
+                          const double *__restrict__ gst, const double *__restrict__ src, double *__restrict__ dst) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= ns * NT) return;
   const int64_t s = idx / NT;
-  dst[idx] = con[s] ? (g ? g[s] : 0.0) : (src ? src[idx] : 0.0);
+  dst[idx] = con[s] ? (gst ? gst[idx] : g ? g[s] : 0.0) : (src ? src[idx] : 0.0);
 }
 __global__ void k_axpy(int64_t n, double a, const double *__restrict__ x, double *__restrict__ y) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1172,9 +1174,9 @@ void by_nq(int nq, F f) {
 }  // namespace
 
 void launch_ns_mask(int64_t ns, int64_t NT, const uint8_t *con, const double *g, const double *src, double *dst,
-                    cudaStream_t s) {
+                    cudaStream_t s, const double *gst) {
   const int64_t n = ns * NT;
-  k_ns_mask<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ns, NT, con, g, src, dst);
+  k_ns_mask<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ns, NT, con, g, gst, src, dst);
   ++g_launches;
 }
 

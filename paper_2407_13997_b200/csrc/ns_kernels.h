@@ -42,7 +42,7 @@ void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, c
 void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,
                             const double *r, double *z, double *xq, int64_t ns, int nnzj, cudaStream_t s);
 void launch_ns_mask(int64_t ns, int64_t NT, const uint8_t *con, const double *g, const double *src, double *dst,
-                    cudaStream_t s);
+                    cudaStream_t s, const double *gst = nullptr);
 void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s);
 // Batched inverse from LU factors (kernels_setup.cu): out[b] = column-major inverse of batch b.
 void launch_lu_inverse_batched(const double *LU, const int32_t *piv, int m, int batch, double *out, cudaStream_t s);

@@ -1,0 +1,125 @@
+"""The paper's Chorin problem on the
+GPU: Newton-FGMRES-WRMG with Chebyshev V(2,2) on unweighted Vanka+star patches,
+the exact velocity as time-dependent Dirichlet data (wrmg_set_boundary_values,
+DESIGN.md R28) and as the initial state (wrmg_rhs_initial).  Parity with the
+oracle at 8x8; the space-time velocity error (oracle's post-processing
+functional) against Table tab:chorin:mg_errors at the paper's Mref = 3.
+
+WRMG_PAPER_TABLES=1 adds the whole spatial-degree-1 column of the table
+(test_paper_chorin_table, ~3.5 min; JSON lines to $WRMG_TABLE_OUT if set): every
+error within 8 % of the printed one (measured: 2-8 % below it), the printed
+1.77e-3 at temporal 1, N = 10 read as 1.77e-4 (R28)."""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import wrmg_inputs as wi
+from wrmg_testutil import read_golden
+
+pytestmark = pytest.mark.gpu
+
+T_END, REYNOLDS = 0.1, 10.0
+
+
+def _torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _dev(x):
+    torch = _torch()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda:0")
+
+
+def _host(t):
+    _torch().cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def _gpu_chorin(n, k, q, N, ncoarse):
+    import paper_2407_13997_b200 as w
+    dt = T_END / N
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, ncoarse=ncoarse, problem="ns",
+                  reynolds=REYNOLDS, bc="dirichlet0", weights="none", nu_pre=2, nu_post=2, smoother="chebyshev")
+    c.set_boundary_values(_dev(wi.chorin_boundary_data(n, n, 1.0 / n, k, N, q, dt)))
+    b = c.zeros()
+    c.rhs_initial(_dev(wi.chorin_u0(n, n, 1.0 / n, k)), b)
+    U = c.zeros()
+    its, lin, st = c.newton(U, rtol=1e-8, maxit=20, rhs=b)
+    out = _host(U)
+    c.close()
+    return out, its, lin, st
+
+
+def _printed():
+    tab = {}
+    for row in read_golden("paper_chorin_errors.txt"):
+        tab[(int(row[0]), int(row[1]), int(row[2]))] = float(row[3])
+    return tab
+
+
+def test_chorin_newton_parity():
+    """GPU Newton on the Chorin problem = oracle Newton: identical Newton and total
+    FGMRES counts, solution within 1e-8, and the same velocity error."""
+    from oracle import ns
+    n, k, q, N = 8, 1, 1, 4
+    dt = T_END / N
+    H = ns.NSHierarchy(n, n, 1.0 / n, k, q, N, dt, REYNOLDS, bc="dirichlet0", smoother_kind="chebyshev",
+                       nu_pre=2, nu_post=2, weight_mode="none")
+    H.fine.set_boundary_data(wi.chorin_boundary_data(n, n, 1.0 / n, k, N, q, dt))
+    Uref, hist, lin = ns.newton(H, rtol=1e-8, maxit=20, u0=wi.chorin_u0(n, n, 1.0 / n, k))
+    U, its, lin_its, st = _gpu_chorin(n, k, q, N, 4)
+    assert st == "WRMG_OK"
+    assert its == len(lin) and lin_its == sum(lin), (its, lin_its, lin)
+    e = np.linalg.norm(U - Uref) / np.linalg.norm(Uref)
+    assert e <= 1e-8, e
+    err_gpu = ns.velocity_l2_error(H.fine, U, wi.chorin_velocity)
+    err_ref = ns.velocity_l2_error(H.fine, Uref, wi.chorin_velocity)
+    assert abs(err_gpu - err_ref) <= 1e-8 * err_ref
+
+
+def _paper_case(k, q, N, Mref=3):
+    from oracle import ns, mesh
+    n = 10 * 2 ** Mref
+    t0 = time.time()
+    U, its, lin, st = _gpu_chorin(n, k, q, N, 10)
+    t1 = time.time()
+    p = ns.NSProblem(mesh.unit_square(n), k, q, N, T_END / N, REYNOLDS, bc="dirichlet0")
+    err = ns.velocity_l2_error(p, U, wi.chorin_velocity)
+    return {"Mref": Mref, "spatial_degree": k, "temporal": q, "N": N, "error": err,
+            "printed": _printed().get((k, q, N)), "newton": its, "linear": lin, "status": st,
+            "ndof": int(U.size), "setup_plus_solve_s": round(t1 - t0, 2)}
+
+
+def test_paper_chorin_error_q0_N10():
+    """Mref = 3, P2-P1 x DG0, N = 10: the printed error 6.51e-3 (R28:
+    within 5 %, the printed precision plus the reading of the boundary data) in at
+    most the printed 5 Newton steps."""
+    r = _paper_case(1, 0, 10)
+    print(json.dumps(r))
+    assert r["status"] == "WRMG_OK" and r["newton"] <= 5
+    assert abs(r["error"] / r["printed"] - 1.0) <= 0.05, r
+
+
+@pytest.mark.skipif(os.environ.get("WRMG_PAPER_TABLES") != "1", reason="set WRMG_PAPER_TABLES=1")
+def test_paper_chorin_table():
+    out = os.environ.get("WRMG_TABLE_OUT")
+    rows = []
+    for q in (0, 1):
+        for N in (10, 20, 40):
+            r = _paper_case(1, q, N)
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            if out:
+                with open(out, "a") as f:
+                    f.write(json.dumps(r) + "\n")
+    assert all(r["status"] == "WRMG_OK" for r in rows)
+    for r in rows:
+        printed = r["printed"]
+        if (r["temporal"], r["N"]) == (1, 10):
+            printed = 1.77e-4  # R28: the printed 1.77e-3 contradicts the stated 1/N^2 column (4.60e-5 at N = 20)
+        assert abs(r["error"] / printed - 1.0) <= 0.08, r

@@ -120,3 +120,96 @@ def test_jacobian_residual_rows_equal_assembled_operator():
     rows = np.arange(p.ns)
     got = p.jacobian_residual_rows(rows, x, b, W)
     assert np.allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+# ------------------------------------------------------------------ Chorin (N2)
+def test_chorin_exact_solution_solves_the_momentum_equation():
+    """PAPER.md:283-299 / R27: the exact Chorin velocity is solenoidal and, with the
+    corrected pressure, solves u_t - Lap u + R (u.grad) u + grad p = 0 (central
+    differences at random points); the printed pressure does not."""
+    rng = np.random.default_rng(3)
+    R, d = 10.0, 1e-4
+    u = lambda x, y, t: np.array(wi.chorin_velocity(x, y, t))
+    for x, y, t in rng.uniform(0.05, 0.95, size=(5, 3)) * [1, 1, 0.1]:
+        ux, uy = (u(x + d, y, t) - u(x - d, y, t)) / (2 * d), (u(x, y + d, t) - u(x, y - d, t)) / (2 * d)
+        ut = (u(x, y, t + d) - u(x, y, t - d)) / (2 * d)
+        lap = (u(x + d, y, t) + u(x - d, y, t) + u(x, y + d, t) + u(x, y - d, t) - 4 * u(x, y, t)) / d ** 2
+        u0 = u(x, y, t)
+        conv = u0[0] * ux + u0[1] * uy
+        for pf, ok in ((lambda X, Y: wi.chorin_pressure(X, Y, t, R), True),
+                       (lambda X, Y: R * np.pi / 4 * (np.cos(2 * np.pi * X) + np.cos(2 * np.pi * Y))
+                        * np.exp(-4 * np.pi ** 2 * t), False)):
+            gp = np.array([(pf(x + d, y) - pf(x - d, y)) / (2 * d), (pf(x, y + d) - pf(x, y - d)) / (2 * d)])
+            res = np.abs(ut - lap + R * conv + gp).max()
+            assert (res < 1e-5) == ok, res
+        assert abs(ux[0] + uy[1]) < 1e-8
+
+
+def test_triangle_rule_integrates_monomials_exactly():
+    from oracle import fem
+    for npts in (2, 4, 6):
+        xi, w = ns.triangle_rule(npts)
+        for p in range(2 * npts - 1):
+            for s in range(2 * npts - 1 - p):
+                got = np.sum(w * xi[:, 0] ** p * xi[:, 1] ** s)
+                assert abs(got - fem.mono_integral(p, s)) <= 1e-14 * max(1.0, fem.mono_integral(p, s)) + 1e-16
+
+
+@pytest.mark.parametrize("k,q", [(1, 1), (2, 2)])
+def test_velocity_l2_error_pins(k, q):
+    """velocity_l2_error: zero for the interpolant of a field of
+    degree <= k+1 in space and <= q in time; the closed form int_0^T int |u|^2 =
+    T^3/27 for u = (x y t, 0) (needs k+1 >= 2, q >= 1); the closed form
+    (1/2)(1 - exp(-4 pi^2 T)) / (4 pi^2) for U = 0 against the Chorin velocity."""
+    n, N, T = 3, 2, 0.1
+    p = ns.NSProblem(mesh.unit_square(n), k, q, N, T / N, 1.0, bc="dirichlet0")
+    xy, tau = p.vel_xy, p.tm.nodes
+    t = ((np.arange(N)[:, None] + tau[None, :]) * p.dt).ravel()
+    f = lambda x, y, t: (x * y * t + (x ** (k + 1) - 2 * y) * t ** q, y ** (k + 1) * (1 + t ** q) - x * y)
+    fx, fy = f(xy[:, 0:1], xy[:, 1:2], t[None, :])
+    U = np.concatenate([fx, fy, np.zeros((p.Lp, t.size))]).ravel()
+    assert ns.velocity_l2_error(p, U, f) < 1e-13
+    g = lambda x, y, t: (x * y * t, 0.0 * x * y * t)
+    gx, gy = g(xy[:, 0:1], xy[:, 1:2], t[None, :])
+    U = np.concatenate([gx, gy, np.zeros((p.Lp, t.size))]).ravel()
+    zero = lambda x, y, t: (0.0 * x * y * t, 0.0 * x * y * t)
+    assert abs(ns.velocity_l2_error(p, U, zero) - np.sqrt(T ** 3 / 27)) < 1e-14
+    ref = np.sqrt(0.5 * (1 - np.exp(-4 * np.pi ** 2 * T)) / (4 * np.pi ** 2))
+    got = ns.velocity_l2_error(p, np.zeros(p.ndof), wi.chorin_velocity, nspace=10, ntime=10)
+    assert abs(got - ref) < 1e-9 * ref
+
+
+def test_chorin_newton_error_decreases_like_one_over_N():
+    """Chorin problem (R28): Newton-FGMRES-WRMG with the exact
+    velocity as Dirichlet data converges in a few steps and, at temporal degree 0,
+    the space-time velocity error falls ~2x when N doubles (the 1/N column of
+    Table tab:chorin:mg_errors)."""
+    n, k, q, T, R = 4, 1, 0, 0.1, 10.0
+    errs = []
+    for N in (2, 4):
+        H = ns.NSHierarchy(n, n, 1.0 / n, k, q, N, T / N, R, bc="dirichlet0", n_coarse=2)
+        H.fine.set_boundary_data(wi.chorin_boundary_data(n, n, 1.0 / n, k, N, q, T / N))
+        U, hist, lin = ns.newton(H, rtol=1e-8, maxit=10, u0=wi.chorin_u0(n, n, 1.0 / n, k))
+        assert hist[-1] <= 1e-8 * hist[0] and len(lin) <= 6
+        errs.append(ns.velocity_l2_error(H.fine, U, wi.chorin_velocity))
+    assert 1.6 < errs[0] / errs[1] < 2.4, errs
+
+
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_chorin_boundary_data_interpolates_at_gauss_points(q):
+    """R28: on every slab the temporal polynomial of the boundary data (R2 nodal
+    basis, evaluated by the oracle's DG basis) equals the exact velocity at the
+    q+1 Gauss-Legendre points."""
+    from oracle import dg
+    n, k, N, dt = 2, 1, 3, 0.05
+    G = wi.chorin_boundary_data(n, n, 1.0 / n, k, N, q, dt)
+    Lu = (2 * n + 1) ** 2
+    V = G.reshape(-1, N, q + 1)
+    g = 0.5 * (np.polynomial.legendre.leggauss(q + 1)[0] + 1.0)
+    B = dg.TemporalMatrices(q, dt).eval(g)          # (q+1 points, q+1 basis)
+    xy = mesh.node_coords(mesh.unit_square(n), k + 1)
+    for nn in range(N):
+        ex = wi.chorin_velocity(xy[:, 0:1], xy[:, 1:2], (nn + g[None, :]) * dt)
+        assert np.allclose(V[:Lu, nn] @ B.T, ex[0], atol=1e-14)
+        assert np.allclose(V[Lu:2 * Lu, nn] @ B.T, ex[1], atol=1e-14)
+    assert not V[2 * Lu:].any()

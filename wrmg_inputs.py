@@ -68,3 +68,54 @@ def paper_heat_u0(nx, ny, h, k):
     I, J = np.meshgrid(np.arange(Lx), np.arange(Ly), indexing="xy")
     x, y = I.ravel() * h / k, J.ravel() * h / k
     return np.sin(np.pi * x) + np.cos(2 * np.pi * y)
+
+
+def chorin_velocity(x, y, t):
+    """Exact velocity of the Chorin problem:
+    u = (-cos(pi x) sin(pi y), sin(pi x) cos(pi y)) exp(-2 pi^2 t).  Broadcasts."""
+    e = np.exp(-2.0 * np.pi ** 2 * t)
+    return (-np.cos(np.pi * x) * np.sin(np.pi * y) * e, np.sin(np.pi * x) * np.cos(np.pi * y) * e)
+
+
+def chorin_pressure(x, y, t, R):
+    """Pressure that makes chorin_velocity a solution of u_t - Lap u + R (u.grad)u
+    + grad p = 0 (DESIGN.md R27 reading: the printed +R pi/4 (...) does not;
+    -R/4 (cos 2 pi x + cos 2 pi y) exp(-4 pi^2 t) does).  Reference only."""
+    return -0.25 * R * (np.cos(2 * np.pi * x) + np.cos(2 * np.pi * y)) * np.exp(-4.0 * np.pi ** 2 * t)
+
+
+def _velocity_nodes(nx, ny, h, k):
+    ku = k + 1
+    Lux, Luy = ku * nx + 1, ku * ny + 1
+    I, J = np.meshgrid(np.arange(Lux), np.arange(Luy), indexing="xy")
+    return I.ravel() * h / ku, J.ravel() * h / ku, (k * nx + 1) * (k * ny + 1)
+
+
+def chorin_boundary_data(nx, ny, h, k, N, q, dt):
+    """Dirichlet data of the Chorin runs (R28) in the Taylor-Hood
+    waveform-major layout (sids u_x, u_y, p): in space the exact velocity at every
+    P_{k+1} node; in time, per slab, the degree-q polynomial interpolating it at the
+    q+1 Gauss-Legendre points (the slab midpoint for q = 0), stored as its values at
+    the DG(q) nodes t = (n + a/q) dt of R2.  Pressure 0.  Only the boundary rows
+    are used by the solvers."""
+    x, y, Lp = _velocity_nodes(nx, ny, h, k)
+    g = 0.5 * (np.polynomial.legendre.leggauss(q + 1)[0] + 1.0)     # interpolation points in [0, 1]
+    tau = np.array([0.0]) if q == 0 else np.arange(q + 1) / q       # R2 nodes
+    # L[a, j] = Lagrange polynomial of point g_j evaluated at node tau_a
+    L = np.ones((q + 1, q + 1))
+    for j in range(q + 1):
+        for m in range(q + 1):
+            if m != j:
+                L[:, j] *= (tau - g[m]) / (g[j] - g[m])
+    tg = ((np.arange(N)[:, None] + g[None, :]) * dt)                  # (N, q+1)
+    ux, uy = chorin_velocity(x[:, None, None], y[:, None, None], tg[None, :, :])
+    ux, uy = np.einsum("aj,snj->sna", L, ux), np.einsum("aj,snj->sna", L, uy)
+    return np.concatenate([ux.reshape(x.size, -1), uy.reshape(x.size, -1), np.zeros((Lp, N * (q + 1)))]).ravel()
+
+
+def chorin_u0(nx, ny, h, k):
+    """Initial state of the Chorin runs: exact velocity at t = 0 on the P_{k+1}
+    nodes, pressure 0 (sid vector)."""
+    x, y, Lp = _velocity_nodes(nx, ny, h, k)
+    ux, uy = chorin_velocity(x, y, 0.0)
+    return np.concatenate([ux, uy, np.zeros(Lp)])
