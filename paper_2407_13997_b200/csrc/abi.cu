@@ -339,10 +339,20 @@ void factor_all(wrmg_ctx *c) {
   check_launch();
   double *LU = dalloc<double>((size_t)C.m * C.m);
   CK(cudaMemcpyAsync(LU, C.Dblk, (size_t)C.m * C.m * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  launch_batched_lu(LU, C.m, 1, C.piv, C.info, s);
-  check_launch();
-  launch_coarse_inverse(C, LU, L0, c->nq, s);
-  check_launch();
+  if (C.m >= kGJMinM) {  // blocked Gauss-Jordan inverse (kernels_gj.cu)
+    double *scr = dalloc<double>(gj_scratch_doubles(C.m, 1));
+    launch_gj_inverse_batched(LU, C.m, 1, C.piv, C.info, C.DinvT, scr, s);
+    check_launch();
+    launch_coarse_G(C, L0, c->nq, s);
+    check_launch();
+    CK(cudaStreamSynchronize(s));
+    dfree(scr);
+  } else {
+    launch_batched_lu(LU, C.m, 1, C.piv, C.info, s);
+    check_launch();
+    launch_coarse_inverse(C, LU, L0, c->nq, s);
+    check_launch();
+  }
   CK(cudaStreamSynchronize(s));
   dfree(LU);
   if (c->use_kron) {
@@ -408,10 +418,21 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
   Level &L0 = c->lv[0];
   launch_ns_coarse_blocks(geom(c, L0), c->q, c->N, c->tm, L0.A, L0.vvptr, L0.conv, C.nodes, C.mp, C.pin, C.nsD, s);
   check_launch();
-  launch_batched_lu(C.nsD, C.m, c->N, C.nspiv, C.nsinfo, s);
-  check_launch();
-  launch_lu_inverse_batched(C.nsD, C.nspiv, C.m, c->N, C.nsinvT, s);
-  check_launch();
+  {
+    PScope ps(c, WRMG_K_FACTOR, 0, 16.0 * (double)c->N * C.m * C.m, 2.0 * (double)C.m * C.m * C.m * c->N);
+    if (C.m >= kGJMinM) {
+      double *scr = dalloc<double>(gj_scratch_doubles(C.m, c->N));
+      launch_gj_inverse_batched(C.nsD, C.m, c->N, C.nspiv, C.nsinfo, C.nsinvT, scr, s);
+      check_launch();
+      CK(cudaStreamSynchronize(s));
+      dfree(scr);
+    } else {
+      launch_batched_lu(C.nsD, C.m, c->N, C.nspiv, C.nsinfo, s);
+      check_launch();
+      launch_lu_inverse_batched(C.nsD, C.nspiv, C.m, c->N, C.nsinvT, s);
+      check_launch();
+    }
+  }
   CK(cudaStreamSynchronize(s));
   c->err_level = c->err_patch = c->err_slab = -1;
   for (int l = (nl == 1 ? 0 : 1); l < nl; ++l) {

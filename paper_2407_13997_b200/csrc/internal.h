@@ -209,6 +209,7 @@ extern int64_t g_launches;  // kernels launched by this library (process-wide)
 // kernel launchers (kernels_*.cu)
 void launch_assemble_spatial(const Level &L, int k, const double *ref_dev, double kappa, cudaStream_t s);
 void launch_patch_blocks(const Level &L, int nq, const Temporal &tm, cudaStream_t s);
+void launch_coarse_G(Coarse &C, const Level &L, int nq, cudaStream_t s);  // GT, Gq from DinvT
 void launch_batched_lu(double *A, int m, int batch, int32_t *piv, int32_t *info, cudaStream_t s);
 void launch_inverse_and_G(const Level &L, const double *LU, int nq, cudaStream_t s);
 void launch_coarse_blocks(const Level &L, Coarse &C, int nq, const Temporal &tm, cudaStream_t s);

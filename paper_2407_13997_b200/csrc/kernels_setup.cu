@@ -318,6 +318,10 @@ void launch_coarse_blocks(const Level &L, Coarse &C, int nq, const Temporal &tm,
 void launch_coarse_inverse(Coarse &C, const double *LU, const Level &L, int nq, cudaStream_t s) {
   dim3 grid((C.m + 127) / 128, 1);
   k_lu_inverse<false><<<grid, 128, 0, s>>>(LU, C.piv, C.m, C.DinvT); ++g_launches;
+  launch_coarse_G(C, L, nq, s);
+}
+
+void launch_coarse_G(Coarse &C, const Level &L, int nq, cudaStream_t s) {
   int64_t n = (int64_t)C.m * C.mp;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
   k_coarse_G<<<blocks, 256, 0, s>>>(L.A.rowptr, L.A.col, L.A.val, C.nodes, C.mp, nq, C.DinvT, C.GT, C.Gq); ++g_launches;

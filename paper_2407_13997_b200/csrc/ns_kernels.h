@@ -45,6 +45,14 @@ void launch_ns_mask(int64_t ns, int64_t NT, const uint8_t *con, const double *g,
                     cudaStream_t s, const double *gst = nullptr);
 void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s);
 // Batched inverse from LU factors (kernels_setup.cu): out[b] = column-major inverse of batch b.
+// Blocked Gauss-Jordan inverses (kernels_gj.cu) for large blocks: A (batch
+// column-major m x m, destroyed), piv (batch x m), info (batch: 0 or 1 + first
+// singular column), out (batch column-major inverses), scratch of
+// gj_scratch_doubles(m, batch) doubles.
+constexpr int kGJMinM = 192;  // below this the CTA-per-matrix LU + inverse is used
+size_t gj_scratch_doubles(int m, int batch);
+void launch_gj_inverse_batched(double *A, int m, int batch, int32_t *piv, int32_t *info, double *out,
+                               double *scratch, cudaStream_t s);
 void launch_lu_inverse_batched(const double *LU, const int32_t *piv, int m, int batch, double *out, cudaStream_t s);
 
 }  // namespace wrmg

@@ -116,9 +116,12 @@ def test_ns_vcycle(n, k, N):
     c.close()
 
 
-def test_ns_one_level_vcycle_is_pinned_coarse_solve():
+@pytest.mark.parametrize("n,k,q,N", [(4, 1, 1, 3), (4, 2, 1, 3), (4, 2, 0, 5), (2, 1, 0, 3)])
+def test_ns_one_level_vcycle_is_pinned_coarse_solve(n, k, q, N):
+    """Coarse slab blocks of m = 27 (CTA LU) and 246 / 323 / 646 (blocked
+    Gauss-Jordan, kernels_gj.cu)."""
     from oracle import ns
-    c, H, W = _setup(4, 1, 1, 3)
+    c, H, W = _setup(n, k, q, N)
     p = H.fine
     b, bref = _rhs(c, p, seed=4)
     z = c.empty()

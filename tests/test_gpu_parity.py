@@ -162,6 +162,27 @@ def test_vcycle(n, k, q, N, mode):
     assert_parity(_host(z), multigrid.vcycle(H, r_np), what="vcycle")
 
 
+@pytest.mark.parametrize("n,k,q,N", [(8, 3, 1, 5), (6, 2, 3, 3), (10, 1, 0, 4)])
+def test_one_level_coarse_solve_large_blocks(n, k, q, N):
+    """H11 with a single level (ncoarse = n): the V-cycle is the exact time-marching
+    coarse solve; slab blocks of m = 1058 / 484 / 81 use the blocked Gauss-Jordan
+    inverse (kernels_gj.cu, m >= 192) or the CTA LU.  Checked against the oracle's
+    V-cycle and against A z = r (spsolve-free residual check)."""
+    from oracle import multigrid
+    import paper_2407_13997_b200 as w
+    H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N, n_coarse=n)
+    p = H.fine
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N, ncoarse=n)
+    assert c.layout["nlevels"] == 1 == len(H.levels)
+    r_np = p.rhs(wi.spacetime_field(p.nnode, N, q, 6))
+    z = c.empty()
+    c.vcycle(_dev(r_np), z)
+    zg = _host(z)
+    assert_parity(zg, multigrid.vcycle(H, r_np), what="one-level vcycle")
+    assert np.linalg.norm(p.A @ zg - r_np) <= 1e-11 * np.linalg.norm(r_np)
+    c.close()
+
+
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 16), (16, 3, 1, 16), (8, 2, 1, 40)])
 def test_fgmres(n, k, q, N, mode):
