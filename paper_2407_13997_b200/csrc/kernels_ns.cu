@@ -326,92 +326,151 @@ __device__ __forceinline__ double block_entry(const int32_t *__restrict__ rowptr
   return v;
 }
 
-// In-place Gauss-Jordan inverse of the row-major m x m matrix A in shared memory
-// with partial pivoting (first maximum |a| at or below the diagonal: the pivot rows
-// LAPACK dgetrf picks, R10).  Returns 0 or 1 + first column with |pivot| < tol.
-__device__ int gj_invert_smem(double *A, int m, double tol, double *f, int *piv) {
+// In-place blocked Gauss-Jordan inverse of the row-major m x m matrix A in shared
+// memory with partial pivoting (first maximum |a| at or below the diagonal: the
+// pivot rows LAPACK dgetrf picks, R10).  Panels of GJB columns: (1) Gauss-Jordan on
+// the panel columns with whole-row interchanges; the panel becomes
+// [P11^{-1}; -A_O P11^{-1}] (pivot rows / other rows); (2) X = the pivot rows of the
+// other columns; (3) rank-GJB update A[:, j] = [0; A_O[:, j]] + Panel X[:, j] by 4x4
+// register tiles (the 2 m^3 flops; shared-memory traffic / GJB of the column-at-a-
+// time form).  The row interchanges are undone as an output column permutation:
+// idx[c] = the column of A holding column c of the inverse.  Returns 0 or 1 + the
+// first column with |pivot| < tol.
+constexpr int GJB = 8;
+__device__ int gj_invert_smem(double *A, int m, double tol, double *X, int *piv, int *idx) {
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ double s_pv;
   __shared__ int s_p, s_info;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
   if (tid == 0) s_info = 0;
-  for (int c = 0; c < m; ++c) {
-    double bv = -1.0;
-    int bi = m;
-    for (int r = c + tid; r < m; r += nth) {
-      const double v = fabs(A[r * m + c]);
-      if (v > bv) {
-        bv = v;
-        bi = r;
-      }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      s_val[wid] = bv;
-      s_idx[wid] = bi;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double v = s_val[0];
-      int ix = s_idx[0];
-      for (int w = 1; w < nw; ++w)
-        if (s_val[w] > v || (s_val[w] == v && s_idx[w] < ix)) {
-          v = s_val[w];
-          ix = s_idx[w];
+  const int ntr = (m + 3) / 4;
+  for (int k0 = 0; k0 < m; k0 += GJB) {
+    const int nb = min(GJB, m - k0), k1 = k0 + nb;
+    for (int c = k0; c < k1; ++c) {
+      double bv = -1.0;
+      int bi = m;
+      for (int r = c + tid; r < m; r += nth) {
+        const double v = fabs(A[r * m + c]);
+        if (v > bv) {
+          bv = v;
+          bi = r;
         }
-      piv[c] = ix;
-      s_p = ix;
-      s_pv = A[ix * m + c];
-      if (!(v >= tol) && s_info == 0) s_info = c + 1;
-    }
-    __syncthreads();
-    const int p = s_p;
-    const double pinv = s_pv != 0.0 ? 1.0 / s_pv : 0.0;
-    for (int j = tid; j < m; j += nth) {
-      const double t1 = A[c * m + j], t2 = A[p * m + j];
-      A[p * m + j] = t1;
-      A[c * m + j] = (j == c) ? pinv : t2 * pinv;
-    }
-    __syncthreads();
-    for (int r = tid; r < m; r += nth) f[r] = (r == c) ? 0.0 : A[r * m + c];
-    __syncthreads();
-    for (int e = tid; e < m * m; e += nth) {
-      const int r = e / m, j = e - r * m;
-      if (r == c) continue;
-      if (j == c)
-        A[e] = -f[r] * A[c * m + c];
-      else
-        A[e] = fma(-f[r], A[c * m + j], A[e]);
-    }
-    __syncthreads();
-  }
-  // (P A)^{-1} = A^{-1} P^T: undo the row interchanges as column interchanges, last first
-  for (int c = m - 1; c >= 0; --c) {
-    const int p = piv[c];
-    if (p != c)
-      for (int r = tid; r < m; r += nth) {
-        const double t = A[r * m + c];
-        A[r * m + c] = A[r * m + p];
-        A[r * m + p] = t;
       }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_val[wid] = bv;
+        s_idx[wid] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double v = s_val[0];
+        int ix = s_idx[0];
+        for (int w = 1; w < nw; ++w)
+          if (s_val[w] > v || (s_val[w] == v && s_idx[w] < ix)) {
+            v = s_val[w];
+            ix = s_idx[w];
+          }
+        piv[c] = ix;
+        s_p = ix;
+        s_pv = A[ix * m + c];
+        if (!(v >= tol) && s_info == 0) s_info = c + 1;
+      }
+      __syncthreads();
+      const int p = s_p;
+      const double pinv = s_pv != 0.0 ? 1.0 / s_pv : 0.0;
+      // whole-row interchange c <-> p; row c scaled on the panel columns
+      for (int j = tid; j < m; j += nth) {
+        const double t1 = A[c * m + j], t2 = A[p * m + j];
+        A[p * m + j] = t1;
+        A[c * m + j] = (j >= k0 && j < k1) ? ((j == c) ? pinv : t2 * pinv) : t2;
+      }
+      __syncthreads();
+      // panel rank-1 step on the other rows: A[r][j] -= f_r row_c[j], column c = -f_r / pivot
+      for (int e = tid; e < m * nb; e += nth) {
+        const int r = e / nb, j = k0 + (e - r * nb);
+        if (r == c) continue;
+        const double fr = A[r * m + c];
+        if (j != c) A[r * m + j] = fma(-fr, A[c * m + j], A[r * m + j]);
+      }
+      __syncthreads();
+      for (int r = tid; r < m; r += nth)
+        if (r != c) A[r * m + c] = -A[r * m + c] * A[c * m + c];
+      __syncthreads();
+    }
+    // X = pivot rows of the other columns
+    for (int e = tid; e < nb * m; e += nth) {
+      const int t = e / m, j = e - t * m;
+      X[e] = (j >= k0 && j < k1) ? 0.0 : A[(k0 + t) * m + j];
+    }
+    __syncthreads();
+    // A[:, j] = [0 on pivot rows; A] + Panel X   (columns outside the panel).
+    // Warp item = 4 rows x 64 columns, lane = columns (lane, lane + 32): the row-major
+    // A and X accesses are consecutive across lanes, the panel values broadcast.
+    {
+      const int ncb = (m + 63) / 64, items = ntr * ncb;
+      for (int it = wid; it < items; it += nw) {
+        const int r0 = (it / ncb) * 4, jb = (it % ncb) * 64;
+        int jj[2];
+        bool wr[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          jj[b] = jb + lane + 32 * b;
+          wr[b] = jj[b] < m && (jj[b] < k0 || jj[b] >= k1);
+        }
+        double acc[4][2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int r = r0 + a;
+            acc[a][b] = (wr[b] && r < m && (r < k0 || r >= k1)) ? A[r * m + jj[b]] : 0.0;
+          }
+        for (int t = 0; t < nb; ++t) {
+          double pv[4], xv[2];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) pv[a] = (r0 + a < m) ? A[(r0 + a) * m + k0 + t] : 0.0;
+#pragma unroll
+          for (int b = 0; b < 2; ++b) xv[b] = jj[b] < m ? X[t * m + jj[b]] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) acc[a][b] = fma(pv[a], xv[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            if (wr[b] && r0 + a < m) A[(r0 + a) * m + jj[b]] = acc[a][b];
+      }
+    }
     __syncthreads();
   }
+  // (P A)^{-1} = A^{-1} P^T: columns interchanged (c, piv[c]) for c = m-1 .. 0
+  if (tid == 0) {
+    for (int c = 0; c < m; ++c) idx[c] = c;
+    for (int c = m - 1; c >= 0; --c) {
+      const int p = piv[c], t = idx[c];
+      idx[c] = idx[p];
+      idx[p] = t;
+    }
+  }
+  __syncthreads();
   return s_info;
 }
 
 // One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
 // DoFs: identity rows), invert, write the row-major inverse to
 // out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
-template <int NQ>
-__global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
+template <int NQ, int NTH>
+__global__ void __launch_bounds__(NTH) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
                                                    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
                                                    const double *__restrict__ Mv, const double *__restrict__ KGv,
                                                    int64_t nvrow, const int32_t *__restrict__ vvptr,
@@ -420,9 +479,10 @@ __global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstrid
                                                    const int32_t *__restrict__ ppos, const int32_t *__restrict__ pvv) {
   extern __shared__ __align__(16) double smem[];
   const int m = NQ * mp;
-  double *A = smem, *f = smem + (int64_t)m * m;
-  int *piv = (int *)(f + m);
-  int *nodes = piv + m;
+  double *A = smem, *X = smem + (int64_t)m * m;  // X: GJB x m
+  int *piv = (int *)(X + GJB * m);
+  int *idx = piv + m;
+  int *nodes = idx + m;
   __shared__ double s_red[32];
   const int64_t p = blockIdx.x;
   const int n = blockIdx.y;
@@ -455,11 +515,11 @@ __global__ void __launch_bounds__(256) k_ns_factor(int mp, int N, int64_t mstrid
   __syncthreads();
   double mx = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
-  const int st = gj_invert_smem(A, m, 1e-14 * mx, f, piv);
+  const int st = gj_invert_smem(A, m, 1e-14 * mx, X, piv, idx);
   double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
   for (int e = tid; e < m * m; e += blockDim.x) {
     const int sig = e / m, rho = e - sig * m;
-    o[e] = A[rho * m + sig];
+    o[e] = A[rho * m + idx[sig]];
   }
   if (tid == 0) info[p * N + n] = st;
 }
@@ -935,6 +995,101 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
   }
 }
 
+// Large blocks (m x m too big for a shared double buffer, e.g. P3-P2 x DG1,
+// m = 162): D^{-1} of each slab streamed in chunks of CW columns (contiguous in
+// the column-major layout) through a ring of R shared slots by 1-D TMA bulk
+// copies; the ring runs ahead across slab boundaries (D_{p,n+1} does not depend
+// on x_n), so the stream never drains inside a patch.  Thread rho < m owns row rho.
+template <int NQ>
+__global__ void __launch_bounds__(256) k_ns_sweep_chunked(int mp, int N, int64_t mstride, int CW, int R,
+                                                          const int32_t *__restrict__ pnodes,
+                                                          const double *__restrict__ wnode,
+                                                          const int32_t *__restrict__ rowptr,
+                                                          const int32_t *__restrict__ col,
+                                                          const double *__restrict__ Mv,
+                                                          const double *__restrict__ Dinv, const double *__restrict__ r,
+                                                          double *__restrict__ u, double omega) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bar[8];
+  const int m = NQ * mp;
+  const int64_t slot = (int64_t)CW * m;                 // doubles per ring slot
+  double *ring = smem;                                  // R x slot
+  double *Mp = smem + R * slot;                         // mp x mp velocity mass of the patch
+  double *g = Mp + mp * mp, *x = g + m, *wn = x + m;
+  int *nodes = (int *)(wn + mp);
+  const int64_t p = blockIdx.x;
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x;
+  const double *Dp = Dinv + p * N * mstride;
+  const int nch = (m + CW - 1) / CW;
+  const int64_t total = (int64_t)N * nch;
+  auto issue = [&](int64_t t) {  // chunk t = (slab n, chunk c) into slot t % R
+    const int64_t n = t / nch;
+    const int c = (int)(t - n * nch);
+    const int cols = min(CW, m - c * CW);
+    const unsigned bytes = (unsigned)((int64_t)cols * m * sizeof(double) + 15) & ~15u;
+    bulk_load(ring + (t % R) * slot, Dp + n * mstride + (int64_t)c * CW * m, bytes, &bar[t % R]);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < R; ++k) mbar_init_ns(&bar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int64_t t = 0; t < R && t < total; ++t) issue(t);
+  }
+  for (int i = tid; i < mp; i += blockDim.x) {
+    const int sn = pnodes[p * mp + i];
+    nodes[i] = sn;
+    wn[i] = sn >= 0 ? omega * wnode[sn] : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < mp * mp; e += blockDim.x) {
+    const int i = e / mp, j = e - i * mp;
+    double v = 0.0;
+    if (nodes[i] >= 0 && nodes[j] >= 0) {
+      const int pos = csr_find_ns(rowptr, col, nodes[i], nodes[j]);
+      if (pos >= 0) v = Mv[pos];
+    }
+    Mp[e] = v;
+  }
+  for (int i = tid; i < m; i += blockDim.x) x[i] = 0.0;
+  __syncthreads();
+  const int i_me = tid / NQ, a_me = tid - (tid / NQ) * NQ;
+  const bool own = tid < m && i_me < mp && nodes[i_me] >= 0;
+  const int64_t rbase = own ? (int64_t)nodes[i_me] * NT + a_me : 0;
+  double rcur = own ? __ldg(r + rbase) : 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double rnext = (own && n + 1 < N) ? __ldg(r + rbase + (int64_t)(n + 1) * NQ) : 0.0;
+    if (tid < m) {
+      double v = rcur;
+      if (own && a_me == 0 && n > 0)  // jump: M_p x_{n-1}[q]
+        for (int j = 0; j < mp; ++j) v = fma(Mp[i_me * mp + j], x[j * NQ + NQ - 1], v);
+      g[tid] = v;
+    }
+    rcur = rnext;
+    __syncthreads();
+    double acc = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      const int64_t t = (int64_t)n * nch + c;
+      mbar_wait_ns(&bar[t % R], (unsigned)((t / R) & 1));
+      const double *D = ring + (t % R) * slot;
+      const int cols = min(CW, m - c * CW);
+      if (tid < m) {
+        const double *gc = g + c * CW;
+        for (int j = 0; j < cols; ++j) acc = fma(D[j * m + tid], gc[j], acc);
+      }
+      __syncthreads();  // slot consumed by every thread
+      if (tid == 0 && t + R < total) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(t + R);
+      }
+    }
+    if (tid < m) {
+      x[tid] = acc;
+      if (own) atomicAdd(u + rbase + (int64_t)n * NQ, wn[i_me] * acc);
+    }
+    __syncthreads();
+  }
+}
+
 // --------------------------------------------------------------- H15 projection
 // partial[b][t] = sum of rows [b*rpb, (b+1)*rpb) of the Lp x NT pressure block.
 __global__ void k_colsum(const double *__restrict__ P, int64_t nrow, int64_t NT, int64_t rpb,
@@ -1186,7 +1341,7 @@ void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s
 }
 
 size_t ns_factor_smem(int m, int mp) {
-  return ((size_t)m * m + m) * sizeof(double) + (size_t)(m + mp) * sizeof(int) + 16;
+  return ((size_t)m * m + (size_t)GJB * m) * sizeof(double) + (size_t)(2 * m + mp) * sizeof(int) + 16;
 }
 
 size_t ns_sweep_smem(int m, int mp, int64_t mstride, bool staged) {
@@ -1266,8 +1421,8 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
   }
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
-    cudaFuncSetAttribute(k_ns_factor<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_ns_factor<NQ><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
+    cudaFuncSetAttribute(k_ns_factor<NQ, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_ns_factor<NQ, 256><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
                                           conv, tm, out, info, ppos, pvv);
   });
   ++g_launches;
@@ -1279,6 +1434,25 @@ void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, cons
   // m <= 256 (one thread per patch row) is enforced by setup_ns
   const bool staged = ns_sweep_smem(m, mp, mstride, true) <= 200 * 1024;
   const size_t sm = ns_sweep_smem(m, mp, mstride, staged);
+  if (!staged) {  // chunked ring: two CTAs per SM when it fits, else one with a deeper ring
+    const size_t fixed = ((size_t)mp * mp + 2 * m + mp) * sizeof(double) + mp * sizeof(int) + 64;
+    int CW = 16, R = 2;
+    while (CW > 4 && fixed + (size_t)R * CW * m * sizeof(double) > 110 * 1024) CW /= 2;
+    if (fixed + (size_t)R * CW * m * sizeof(double) > 110 * 1024) {
+      CW = 32;
+      R = 3;
+      while (CW > 4 && fixed + (size_t)R * CW * m * sizeof(double) > 220 * 1024) CW /= 2;
+    }
+    const size_t smc = fixed + (size_t)R * CW * m * sizeof(double);
+    by_nq(q + 1, [&](auto NQc) {
+      constexpr int NQ = decltype(NQc)::value;
+      cudaFuncSetAttribute(k_ns_sweep_chunked<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+      k_ns_sweep_chunked<NQ><<<(unsigned)npatch, 256, smc, s>>>(mp, N, mstride, CW, R, pnodes, wnode, A.rowptr,
+                                                                A.col, A.val, Dinv, r, u, omega);
+    });
+    ++g_launches;
+    return;
+  }
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
     if (staged) {
