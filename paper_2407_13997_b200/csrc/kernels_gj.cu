@@ -46,23 +46,31 @@ __global__ void __launch_bounds__(1024) k_gj_tol(const double *__restrict__ Aall
   }
 }
 
+// Panel kernel: the m x nb panel (contiguous in the column-major layout) is staged
+// in shared memory, eliminated there, and written back; thread 0 also records the
+// panel's row interchanges as one composite map (rows dst[l] <- src[l], l < cnt)
+// for the other columns.
 __global__ void __launch_bounds__(GJ_PTH) k_gj_panel(double *__restrict__ Aall, int m, int k0, int nb,
                                                       int32_t *__restrict__ pivall, int32_t *__restrict__ info,
-                                                      const double *__restrict__ tol) {
+                                                      const double *__restrict__ tol, int32_t *__restrict__ rmap) {
+  extern __shared__ __align__(16) double P[];  // P[jj * m + i] = A[i][k0 + jj]
   __shared__ double s_val[32];
   __shared__ int s_idx[32];
   __shared__ double s_row[GJ_NB];
-  __shared__ double s_d;
   __shared__ int s_p;
-  double *A = Aall + (int64_t)blockIdx.x * m * m;
+  double *A = Aall + (int64_t)blockIdx.x * m * m + (int64_t)k0 * m;
   int32_t *piv = pivall + (int64_t)blockIdx.x * m;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int tot = m * nb;
+  for (int e = tid; e < tot; e += blockDim.x) P[e] = A[e];
+  __syncthreads();
   for (int t = 0; t < nb; ++t) {
     const int k = k0 + t;
+    const double *pk = P + t * m;
     double bv = -1.0;
     int bi = m;
     for (int r = k + tid; r < m; r += blockDim.x) {
-      const double v = fabs(A[(int64_t)k * m + r]);
+      const double v = fabs(pk[r]);
       if (v > bv) {
         bv = v;
         bi = r;
@@ -95,60 +103,82 @@ __global__ void __launch_bounds__(GJ_PTH) k_gj_panel(double *__restrict__ Aall, 
     }
     __syncthreads();
     const int p = s_p;
-    if (tid < nb && p != k) {  // swap rows k, p in the panel columns
-      double *cj = A + (int64_t)(k0 + tid) * m;
-      const double tmp = cj[k];
-      cj[k] = cj[p];
-      cj[p] = tmp;
-    }
-    __syncthreads();
-    if (tid == 0) s_d = A[(int64_t)k * m + k];
-    __syncthreads();
-    const double d = s_d;
+    const double d = P[t * m + p];  // pivot value (row p before the interchange)
     const double dinv = d != 0.0 ? 1.0 / d : 0.0;
-    if (tid < nb) {  // scaled pivot row (panel columns)
-      const double v = A[(int64_t)(k0 + tid) * m + k] * dinv;
-      s_row[tid] = v;
+    if (tid < nb) {  // interchange rows k, p of the panel; scaled pivot row
+      double *cj = P + tid * m;
+      const double a = cj[p];
+      cj[p] = cj[k];
+      cj[k] = a;
+      s_row[tid] = a * dinv;
     }
     __syncthreads();
-    // other rows: A[i][j] -= A[i][k] * row_k[j]   (j != k in the panel)
-    const int64_t tot = (int64_t)m * nb;
-    for (int64_t e = tid; e < tot; e += blockDim.x) {
-      const int i = (int)(e % m), jj = (int)(e / m);
-      if (i == k || k0 + jj == k) continue;
-      A[(int64_t)(k0 + jj) * m + i] -= A[(int64_t)k * m + i] * s_row[jj];
+    // other rows: A[i][j] -= A[i][k] row_k[j]   (j != k in the panel)
+    for (int e = tid; e < tot; e += blockDim.x) {
+      const int jj = e / m, i = e - jj * m;
+      if (i == k || jj == t) continue;
+      P[e] = fma(-pk[i], s_row[jj], P[e]);
     }
     __syncthreads();
-    // pivot row and pivot column
-    if (tid < nb && k0 + tid != k) A[(int64_t)(k0 + tid) * m + k] = s_row[tid];
-    for (int i = tid; i < m; i += blockDim.x)
-      A[(int64_t)k * m + i] = (i == k) ? dinv : -A[(int64_t)k * m + i] * dinv;
+    if (tid < nb && tid != t) P[tid * m + k] = s_row[tid];
+    for (int i = tid; i < m; i += blockDim.x) P[t * m + i] = (i == k) ? dinv : -pk[i] * dinv;
     __syncthreads();
+  }
+  for (int e = tid; e < tot; e += blockDim.x) A[e] = P[e];
+  if (tid == 0) {  // composite row map of the panel's interchanges
+    int32_t *mp = rmap + (int64_t)blockIdx.x * (4 * GJ_NB + 1);
+    int dst[2 * GJ_NB], src[2 * GJ_NB], cnt = 0;
+    auto slot = [&](int r) {
+      for (int l = 0; l < cnt; ++l)
+        if (dst[l] == r) return l;
+      dst[cnt] = r;
+      src[cnt] = r;
+      return cnt++;
+    };
+    for (int t = 0; t < nb; ++t) {
+      const int k = k0 + t, pr = piv[k];
+      if (pr == k) continue;
+      const int a = slot(k), b = slot(pr);
+      const int tmp = src[a];
+      src[a] = src[b];
+      src[b] = tmp;
+    }
+    mp[0] = cnt;
+    for (int l = 0; l < cnt; ++l) {
+      mp[1 + 2 * l] = dst[l];
+      mp[2 + 2 * l] = src[l];
+    }
   }
 }
 
-// One thread per column outside the panel: the panel's row swaps, then X = the
-// pivot rows (nb x m, row-major per matrix) and zero them in A.
-__global__ void k_gj_swap_x(double *__restrict__ Aall, int m, int k0, int nb, const int32_t *__restrict__ pivall,
+// Warp per column outside the panel: the panel's row interchanges (composite map,
+// all loads before any store), then X = the pivot rows (nb x m per matrix), zeroed in A.
+__global__ void k_gj_swap_x(double *__restrict__ Aall, int m, int k0, int nb, const int32_t *__restrict__ rmap,
                             double *__restrict__ Xall) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= m) return;
   double *X = Xall + (int64_t)blockIdx.y * GJ_NB * m;
   if (j >= k0 && j < k0 + nb) {
-    for (int t = 0; t < nb; ++t) X[(int64_t)t * m + j] = 0.0;
+    for (int t = lane; t < nb; t += 32) X[(int64_t)t * m + j] = 0.0;
     return;
   }
   double *cj = Aall + (int64_t)blockIdx.y * m * m + (int64_t)j * m;
-  const int32_t *piv = pivall + (int64_t)blockIdx.y * m;
-  for (int t = 0; t < nb; ++t) {
-    const int k = k0 + t, p = piv[k];
-    if (p != k) {
-      const double tmp = cj[k];
-      cj[k] = cj[p];
-      cj[p] = tmp;
-    }
+  const int32_t *mp = rmap + (int64_t)blockIdx.y * (4 * GJ_NB + 1);
+  const int cnt = mp[0];
+  double v[2];
+  int dr[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int l = lane + 32 * h;
+    dr[h] = l < cnt ? mp[1 + 2 * l] : -1;
+    v[h] = l < cnt ? cj[mp[2 + 2 * l]] : 0.0;
   }
-  for (int t = 0; t < nb; ++t) {
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (dr[h] >= 0) cj[dr[h]] = v[h];
+  __syncwarp();
+  for (int t = lane; t < nb; t += 32) {
     X[(int64_t)t * m + j] = cj[k0 + t];
     cj[k0 + t] = 0.0;
   }
@@ -217,23 +247,24 @@ __global__ void k_gj_colidx(const int32_t *__restrict__ pivall, int m, int32_t *
   }
 }
 
+// grid (m columns, batch): out[:, c] = A[:, idx[c]]
 __global__ void k_gj_unpermute(const double *__restrict__ Aall, int m, const int32_t *__restrict__ idxall,
                                double *__restrict__ outall) {
   const int64_t mm = (int64_t)m * m;
-  const double *A = Aall + blockIdx.y * mm;
+  const int c = blockIdx.x;
   const int32_t *idx = idxall + (int64_t)blockIdx.y * m;
-  double *out = outall + blockIdx.y * mm;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mm; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e / m), r = (int)(e % m);
-    out[e] = A[(int64_t)idx[c] * m + r];
-  }
+  const double *src = Aall + blockIdx.y * mm + (int64_t)idx[c] * m;
+  double *dst = outall + blockIdx.y * mm + (int64_t)c * m;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) dst[r] = src[r];
 }
 
 }  // namespace
 
 size_t gj_scratch_doubles(int m, int batch) {
-  // X panels (batch x NB x m) + tolerances (batch) + column index (batch x m int32, as doubles)
-  return (size_t)batch * GJ_NB * m + (size_t)batch + ((size_t)batch * m + 1) / 2;
+  // X panels (batch x NB x m) + tolerances (batch) + column index (batch x m int32) + row maps
+  // (batch x (4 NB + 1) int32), the int32 parts counted in doubles
+  return (size_t)batch * GJ_NB * m + (size_t)batch + ((size_t)batch * m + 1) / 2 +
+         ((size_t)batch * (4 * GJ_NB + 1) + 1) / 2 + 1;
 }
 
 void launch_gj_inverse_batched(double *A, int m, int batch, int32_t *piv, int32_t *info, double *out,
@@ -242,19 +273,26 @@ void launch_gj_inverse_batched(double *A, int m, int batch, int32_t *piv, int32_
   double *X = scratch;
   double *tol = X + (size_t)batch * GJ_NB * m;
   int32_t *idx = reinterpret_cast<int32_t *>(tol + batch);
+  int32_t *rmap = idx + (size_t)batch * m;
   k_gj_tol<<<batch, 1024, 0, s>>>(A, m, tol, info);
   ++g_launches;
+  // panel width: the m x nb panel must fit in shared memory
+  const int NBP = std::max(1, std::min(GJ_NB, (int)((220 * 1024) / (sizeof(double) * (size_t)m))));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gj_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 221 * 1024);
+    attr = true;
+  }
   const int nt = (m + GJ_T - 1) / GJ_T;
-  for (int k0 = 0; k0 < m; k0 += GJ_NB) {
-    const int nb = std::min(GJ_NB, m - k0);
-    k_gj_panel<<<batch, GJ_PTH, 0, s>>>(A, m, k0, nb, piv, info, tol);
-    k_gj_swap_x<<<dim3((m + 127) / 128, batch), 128, 0, s>>>(A, m, k0, nb, piv, X);
+  for (int k0 = 0; k0 < m; k0 += NBP) {
+    const int nb = std::min(NBP, m - k0);
+    k_gj_panel<<<batch, GJ_PTH, (size_t)m * nb * sizeof(double), s>>>(A, m, k0, nb, piv, info, tol, rmap);
+    k_gj_swap_x<<<dim3((m + 7) / 8, batch), 256, 0, s>>>(A, m, k0, nb, rmap, X);
     k_gj_update<<<dim3(nt, nt, batch), 256, 0, s>>>(A, m, k0, nb, X);
     g_launches += 3;
   }
   k_gj_colidx<<<batch, 32, 0, s>>>(piv, m, idx);
-  const int64_t mm = (int64_t)m * m;
-  k_gj_unpermute<<<dim3((unsigned)std::min<int64_t>((mm + 255) / 256, 4096), batch), 256, 0, s>>>(A, m, idx, out);
+  k_gj_unpermute<<<dim3((unsigned)m, batch), 256, 0, s>>>(A, m, idx, out);
   g_launches += 2;
 }
 

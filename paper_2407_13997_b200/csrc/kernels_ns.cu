@@ -394,9 +394,9 @@ __device__ int gj_invert_smem(double *A, int m, double tol, double *X, int *piv,
       }
       __syncthreads();
       // panel rank-1 step on the other rows: A[r][j] -= f_r row_c[j], column c = -f_r / pivot
-      for (int e = tid; e < m * nb; e += nth) {
-        const int r = e / nb, j = k0 + (e - r * nb);
-        if (r == c) continue;
+      for (int e = tid; e < m * GJB; e += nth) {
+        const int r = e / GJB, jj = e % GJB, j = k0 + jj;
+        if (r == c || jj >= nb) continue;
         const double fr = A[r * m + c];
         if (j != c) A[r * m + j] = fma(-fr, A[c * m + j], A[r * m + j]);
       }
