@@ -179,9 +179,13 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *ctx, int32_t level, const double *e_coars
 wrmg_status wrmg_level_size(const wrmg_ctx *ctx, int32_t level, int64_t *nnode);
 
 /* Right-preconditioned FGMRES(restart) with CGS2, x0 = 0 (H13; PAPER.md:361-366,
- * R16).  Single rank only (strips: WRMG_E_UNSUPPORTED).  Stops when |g_{j+1}| <= max(rtol ||b||, atol).  x receives the iterate,
+ * R16).  Stops when |g_{j+1}| <= max(rtol ||b||, atol).  x receives the iterate,
  * *iters the number of preconditioner applications, *relres the final true
  * relative residual ||b - A x|| / ||b||.  Synchronises every Arnoldi step.
+ * Strips (nranks > 1): collective - every rank calls it with its local b and x;
+ * b is read on owned columns, x is valid on owned and ghost columns; dot products
+ * run over owned rows and are summed across ranks (all-gather of the per-rank
+ * partial results, added in rank order, so every rank takes identical decisions).
  * Returns WRMG_OK, WRMG_E_BREAKDOWN or WRMG_E_NOT_CONVERGED (x still valid). */
 wrmg_status wrmg_fgmres(wrmg_ctx *ctx, const double *b, double *x, int32_t restart, int32_t maxit,
                         double rtol, double atol, int32_t *iters, double *relres);

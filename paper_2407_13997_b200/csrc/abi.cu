@@ -833,6 +833,30 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
   check_launch();
 }
 
+// Host copy of nv reduction results at dev (<= 64).  Strips: every rank's values
+// are all-gathered and summed in rank order, so all ranks hold bitwise-identical
+// global sums (and take identical host-side decisions).
+void reduce_to_host(wrmg_ctx *c, const double *dev, int nv, double *host) {
+  cudaStream_t s = c->stream;
+  if (!c->strip || c->comm->nranks == 1) {
+    CK(cudaMemcpyAsync(host, dev, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  const int P = c->comm->nranks;
+  if (!c->gred) c->gred = dalloc<double>((size_t)P * 64);
+  comm_call(c, [&] { c->comm->allgather(dev, c->gred, (size_t)nv, s); });
+  std::vector<double> all((size_t)P * nv);
+  CK(cudaMemcpyAsync(all.data(), c->gred, all.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < nv; ++i) {
+    double t = 0.0;
+    for (int q = 0; q < P; ++q) t += all[(size_t)q * nv + i];
+    host[i] = t;
+  }
+}
+
+// Global dot product (owned rows: strips pass vectors with zeroed ghost columns).
 double dot_host(wrmg_ctx *c, const double *a, const double *b, int64_t n) {
   PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 2.0 * n);
   int nb = multidot_blocks(n);
@@ -840,8 +864,7 @@ double dot_host(wrmg_ctx *c, const double *a, const double *b, int64_t n) {
   launch_multidot(V, 1, b, n, c->red + 64, nb, c->stream);
   launch_reduce_partials(c->red + 64, nb, 1, c->red, c->stream);
   double out = 0;
-  CK(cudaMemcpyAsync(&out, c->red, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  reduce_to_host(c, c->red, 1, &out);
   return out;
 }
 
@@ -1393,13 +1416,10 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, doubl
 wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
                         double atol, int32_t *iters, double *relres) {
   if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1) return WRMG_E_INVALID;
-  if (c->strip) {
-    c->err = "wrmg_fgmres: single rank only (strips run stationary V-cycles, C5)";
-    return WRMG_E_UNSUPPORTED;
-  }
   try {
     cudaStream_t s = c->stream;
-    const Level &L = c->lv.back();
+    Level &L = c->lv.back();
+    const bool strip = c->strip;
     const int64_t n = L.nnode * c->nt;
     if (c->restart_alloc < restart) {
       for (double *p : c->V) dfree(p);
@@ -1424,16 +1444,25 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         launch_reduce_partials(part, nb, nv, red, s);
       }
       h.resize(nv);
-      CK(cudaMemcpyAsync(h.data(), red, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      reduce_to_host(c, red, nv, h.data());
+      if (strip)  // the CGS update consumes the global coefficients
+        CK(cudaMemcpyAsync(red, h.data(), nv * sizeof(double), cudaMemcpyHostToDevice, s));
     };
     CK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
-    const double bnorm = norm(b);
-    const double target = std::max(rtol * bnorm, atol);
+    // strips: norms and dots over owned rows (ghost columns of the Krylov vectors are zero)
+    const double bnorm = strip ? 0.0 : norm(b);
+    double bnorm_g = bnorm;
+    if (strip) {
+      CK(cudaMemcpyAsync(c->tmp, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      zero_ghosts(c, L, c->tmp);
+      bnorm_g = norm(c->tmp);
+    }
+    const double target = std::max(rtol * bnorm_g, atol);
     int its = 0;
     wrmg_status status = WRMG_E_NOT_CONVERGED;
     CK(cudaMemcpyAsync(c->tmp, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));  // r = b (x0 = 0)
-    double beta = bnorm;
+    if (strip) zero_ghosts(c, L, c->tmp);
+    double beta = strip ? norm(c->tmp) : bnorm;
     bool done = beta <= target;
     if (done) status = WRMG_OK;
     std::vector<double> H((size_t)(restart + 1) * restart), cs(restart), sn(restart), g(restart + 1), h, h2, y;
@@ -1447,9 +1476,11 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
       g[0] = beta;
       int jend = 0;
       for (int j = 0; j < restart; ++j) {
-        vcycle_level(c, (int)c->lv.size() - 1, c->V[j], c->Z[j]);
+        vcycle_level(c, (int)c->lv.size() - 1, c->V[j], c->Z[j]);  // strips: z valid on owned + ghost columns
+        if (strip) zero_ghosts(c, L, c->V[j]);  // the cycle refreshed V_j's ghosts; dots count owned rows only
         // w = A Z_j (residual kernel in apply mode)
         prof_residual(c, (int)c->lv.size() - 1, c->Z[j], nullptr, c->w, false);
+        if (strip) zero_ghosts(c, L, c->w);
         // CGS2, fused: h = V^T w;  w -= V h & h2 = V^T w;  w -= V h2 & |w|^2
         multidot(j + 1, c->w, h);
         {
@@ -1459,7 +1490,12 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           launch_reduce_partials(part, nb, j + 1, red + 32, s);
         }
         h2.resize(j + 1);
-        CK(cudaMemcpyAsync(h2.data(), red + 32, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (strip) {
+          reduce_to_host(c, red + 32, j + 1, h2.data());
+          CK(cudaMemcpyAsync(red + 32, h2.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, s));
+        } else {
+          CK(cudaMemcpyAsync(h2.data(), red + 32, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
         double hn2 = 0.0;
         {
           PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
@@ -1467,8 +1503,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           launch_cgs_update_norm(c->V.data(), j + 1, c->w, red + 32, n, part, nb, s);
           launch_reduce_partials(part, nb, 1, red + 63, s);
         }
-        CK(cudaMemcpyAsync(&hn2, red + 63, sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        reduce_to_host(c, red + 63, 1, &hn2);
         for (int i = 0; i <= j; ++i) h[i] += h2[i];
         const double hn = std::sqrt(hn2);
         std::vector<double> col(restart + 1, 0.0);
@@ -1521,17 +1556,21 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
       }
       CK(cudaStreamSynchronize(s));
       if (done) break;
+      if (strip) halo_forward(c, L, x);
       prof_residual(c, (int)c->lv.size() - 1, x, b, c->tmp, false);
+      if (strip) zero_ghosts(c, L, c->tmp);
       beta = norm(c->tmp);
       if (beta <= target) {
         status = WRMG_OK;
         break;
       }
     }
+    if (strip) halo_forward(c, L, x);
     prof_residual(c, (int)c->lv.size() - 1, x, b, c->tmp, false);
+    if (strip) zero_ghosts(c, L, c->tmp);
     const double rn = norm(c->tmp);
     if (iters) *iters = its;
-    if (relres) *relres = bnorm > 0 ? rn / bnorm : 0.0;
+    if (relres) *relres = bnorm_g > 0 ? rn / bnorm_g : 0.0;
     check_launch();
     if (status != WRMG_OK) c->err = status == WRMG_E_BREAKDOWN ? "FGMRES breakdown" : "FGMRES: maxit reached";
     return status;
@@ -1774,7 +1813,7 @@ void wrmg_destroy(wrmg_ctx *c) {
                   (void *)C.Y, (void *)C.piv, (void *)C.info, (void *)C.kV, (void *)C.kVT, (void *)C.kS,
                   (void *)C.ksig, (void *)C.nsD, (void *)C.nsinvT, (void *)C.xq, (void *)C.nspiv, (void *)C.nsinfo})
     dfree(p);
-  for (void *p : {(void *)c->th_ref, (void *)c->th_T, (void *)c->bcg, (void *)c->bcg_st, (void *)c->proj, (void *)c->conv_nl,
+  for (void *p : {(void *)c->th_ref, (void *)c->th_T, (void *)c->bcg, (void *)c->bcg_st, (void *)c->gred, (void *)c->proj, (void *)c->conv_nl,
                   (void *)c->nl_b, (void *)c->nl_r, (void *)c->nl_dx})
     dfree(p);
   for (double *p : c->V) dfree(p);

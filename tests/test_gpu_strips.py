@@ -99,3 +99,54 @@ def test_strips_match_global(P, snx, ny, k, q, N, nc):
         full = np.concatenate([a for _, a in sorted(pieces, key=lambda x: x[0])], axis=1)
         e = np.linalg.norm(full - ref[key]) / np.linalg.norm(ref[key])
         assert e <= 1e-12, f"{key}: rel {e:.3e}"
+
+
+@pytest.mark.parametrize("P,snx,ny,k,q,N,nc", [(2, 8, 8, 2, 1, 6, 2), (4, 4, 8, 1, 0, 5, 4), (3, 8, 16, 3, 1, 4, 4)])
+def test_strips_fgmres_match_global(P, snx, ny, k, q, N, nc):
+    """FGMRES(30)-WRMG across strips (H13 with cross-rank dot products): the same
+    iteration count as the single-rank solve and the owned columns of x equal to
+    1e-9 (the sums run in a different order)."""
+    import torch
+    import paper_2407_13997_b200 as w
+    gnx = P * snx
+    h = 1.0 / ny
+    dt = 1.0 / N
+    g = w.Context(gnx, ny, h, degree=k, q=q, nslabs=N, dt=dt, ncoarse=nc)
+    gl = g.layout
+    f = wi.spacetime_field(gl["nnode"], N, q, 9)
+    bg = g.empty()
+    g.rhs(torch.as_tensor(f, device="cuda:0"), bg)
+    xg = g.empty()
+    its_g, rel_g, st_g = g.fgmres(bg, xg, restart=30, maxit=100, rtol=1e-10)
+    torch.cuda.synchronize()
+    Lxg, NT = gl["lx"], gl["nt"]
+    ref = xg.cpu().numpy().reshape(gl["ly"], Lxg, NT)
+    g.close()
+    assert st_g == "WRMG_OK"
+    hub = w.LoopbackHub(P)
+
+    def rank_fn(r):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            c = w.Context(gnx, ny, h, degree=k, q=q, nslabs=N, dt=dt, ncoarse=nc, rank=r, nranks=P, hub=hub,
+                          stream=st.cuda_stream)
+            lay = c.layout
+            Lx = lay["lx"]
+            fl = f.reshape(gl["ly"], Lxg, NT)[:, lay["g0"]:lay["g0"] + Lx, :].copy()
+            b = c.empty()
+            c.rhs(torch.as_tensor(fl.reshape(-1), device="cuda:0"), b)
+            x = c.empty()
+            its, rel, status = c.fgmres(b, x, restart=30, maxit=100, rtol=1e-10)
+            st.synchronize()
+            res = (its, rel, status, _owned(c, x))
+            c.close()
+            return res
+
+    outs = _run_ranks(P, rank_fn)
+    hub.close()
+    for its, rel, status, _ in outs:
+        assert status == "WRMG_OK" and its == its_g, (its, its_g)
+        assert rel == outs[0][1]  # identical on every rank
+    full = np.concatenate([a for (a, c0) in sorted((o[3] for o in outs), key=lambda x: x[1])], axis=1)
+    e = np.linalg.norm(full - ref) / np.linalg.norm(ref)
+    assert e <= 1e-9, f"x: rel {e:.3e}"
