@@ -833,22 +833,39 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
   check_launch();
 }
 
+// Small transfers of the Krylov loop through mapped pinned memory and a copy
+// kernel on the context's stream: they never queue behind bulk copies that other
+// streams (e.g. a serving loop's next input) keep on the copy engines.
+double *hmap(wrmg_ctx *c) {
+  if (!c->hmap) CK(cudaHostAlloc((void **)&c->hmap, 2048 * sizeof(double), cudaHostAllocMapped));
+  return c->hmap;
+}
+void small_d2h(wrmg_ctx *c, const double *dev, double *host, int nv) {  // synchronises
+  double *hm = hmap(c);
+  launch_scale(hm, dev, 1.0, nv, c->stream);
+  CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(host, hm, nv * sizeof(double));
+}
+void small_h2d(wrmg_ctx *c, const double *host, double *dev, int nv) {  // caller synchronises before reuse
+  double *hm = hmap(c) + 1024;
+  std::memcpy(hm, host, nv * sizeof(double));
+  launch_scale(dev, hm, 1.0, nv, c->stream);
+}
+
 // Host copy of nv reduction results at dev (<= 64).  Strips: every rank's values
 // are all-gathered and summed in rank order, so all ranks hold bitwise-identical
 // global sums (and take identical host-side decisions).
 void reduce_to_host(wrmg_ctx *c, const double *dev, int nv, double *host) {
   cudaStream_t s = c->stream;
   if (!c->strip || c->comm->nranks == 1) {
-    CK(cudaMemcpyAsync(host, dev, nv * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    small_d2h(c, dev, host, nv);
     return;
   }
   const int P = c->comm->nranks;
   if (!c->gred) c->gred = dalloc<double>((size_t)P * 64);
   comm_call(c, [&] { c->comm->allgather(dev, c->gred, (size_t)nv, s); });
   std::vector<double> all((size_t)P * nv);
-  CK(cudaMemcpyAsync(all.data(), c->gred, all.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  small_d2h(c, c->gred, all.data(), (int)all.size());
   for (int i = 0; i < nv; ++i) {
     double t = 0.0;
     for (int q = 0; q < P; ++q) t += all[(size_t)q * nv + i];
@@ -1446,7 +1463,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
       h.resize(nv);
       reduce_to_host(c, red, nv, h.data());
       if (strip)  // the CGS update consumes the global coefficients
-        CK(cudaMemcpyAsync(red, h.data(), nv * sizeof(double), cudaMemcpyHostToDevice, s));
+        small_h2d(c, h.data(), red, nv);
     };
     CK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
     // strips: norms and dots over owned rows (ghost columns of the Krylov vectors are zero)
@@ -1492,9 +1509,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         h2.resize(j + 1);
         if (strip) {
           reduce_to_host(c, red + 32, j + 1, h2.data());
-          CK(cudaMemcpyAsync(red + 32, h2.data(), (j + 1) * sizeof(double), cudaMemcpyHostToDevice, s));
-        } else {
-          CK(cudaMemcpyAsync(h2.data(), red + 32, (j + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+          small_h2d(c, h2.data(), red + 32, j + 1);
         }
         double hn2 = 0.0;
         {
@@ -1503,7 +1518,14 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           launch_cgs_update_norm(c->V.data(), j + 1, c->w, red + 32, n, part, nb, s);
           launch_reduce_partials(part, nb, 1, red + 63, s);
         }
-        reduce_to_host(c, red + 63, 1, &hn2);
+        if (strip) {
+          reduce_to_host(c, red + 63, 1, &hn2);
+        } else {  // h2 and |w|^2 in one small read
+          double tmp2[33];
+          small_d2h(c, red + 32, tmp2, 32);
+          for (int i = 0; i <= j; ++i) h2[i] = tmp2[i];
+          hn2 = tmp2[31];
+        }
         for (int i = 0; i <= j; ++i) h[i] += h2[i];
         const double hn = std::sqrt(hn2);
         std::vector<double> col(restart + 1, 0.0);
@@ -1549,7 +1571,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         for (int k2 = i + 1; k2 < jend; ++k2) acc -= H[(size_t)i * restart + k2] * y[k2];
         y[i] = acc / H[(size_t)i * restart + i];
       }
-      CK(cudaMemcpyAsync(red, y.data(), jend * sizeof(double), cudaMemcpyHostToDevice, s));
+      small_h2d(c, y.data(), red, jend);
       {
         PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (jend + 2) * n, 2.0 * jend * n);
         launch_multiaxpy(x, c->Z.data(), red, jend, n, 1.0, s);
@@ -1802,6 +1824,8 @@ const char *wrmg_last_error(const wrmg_ctx *c, int32_t *level, int32_t *patch, i
 void wrmg_destroy(wrmg_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->hmap) cudaFreeHost(c->hmap);
+  c->hmap = nullptr;
   for (auto &L : c->lv) free_level(L);
   free_level(c->gco);
   for (double *p : c->cd) dfree(p);

@@ -168,6 +168,7 @@ struct wrmg_ctx {
   int restart_alloc = 0;
   std::vector<double *> V, Z;
   double *w = nullptr, *red = nullptr, *red_host = nullptr;
+  double *hmap = nullptr;  // mapped pinned host buffer (2 x 1024 doubles): small Krylov results without the copy engines
   double *gred = nullptr;  // strips: all ranks' reduction results (nranks x 64), for wrmg_fgmres
   double *tmp = nullptr;        // finest-level scratch (residual)
   bool use_kron = true;         // factor_mode AUTO: Kronecker-diagonalised heat patch solves
