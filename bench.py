@@ -133,7 +133,7 @@ def barrier(ws):
 def ncu_traffic(kclass):
     """dram__bytes_read.sum + dram__bytes_write.sum of the finest-level launch of
     the kernel behind a timing class, from the committed `ncu --set full` summary
-    of the C2 bench (profiles/r01_v15_c2_ncu.txt); (None, None) if absent."""
+    of the C2 bench (profiles/r01_final_c2_ncu.txt); (None, None) if absent."""
     import re
     names = {"residual": "k_residual_tma", "sweep": "k_sweep_kron_mma", "krylov": "k_krylov"}
     path = os.path.join(ROOT, "profiles", "r01_final_c2_ncu.txt")

@@ -99,3 +99,35 @@ def test_abi_rejects_bad_arguments():
     with pytest.raises(w.WrmgError) as e:
         w.Context(4, 4, 0.25, degree=1, q=0, nslabs=2, dt=0.5, problem="ns", reynolds=0.0)
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("n,k,q,N", [(80, 3, 1, 70), (112, 2, 0, 100), (80, 3, 1, 64), (80, 3, 2, 65)])
+def test_large_level_residual_ragged_chunks(n, k, q, N):
+    """Residual rows on lattices large enough for the TMA-tiled kernels (>= 50000
+    nodes), with N around multiples of the 32-slab chunk
+    (ragged last chunk, chunk boundaries; N (q+1) odd takes the cp.async variant): sampled rows
+    (corner, boundary-adjacent, interior; every slab) against the oracle's row
+    formula, in residual and apply mode."""
+    import torch
+    import paper_2407_13997_b200 as w
+    from oracle import heat
+    p = heat.unit_square_problem(n, k, q, N, 1.0 / N, build_matrix=False)
+    ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N)
+    assert p.nnode >= 50000
+    u = wi.spacetime_field(p.nnode, N, q, seed=3)
+    b = p.rhs(wi.spacetime_field(p.nnode, N, q, seed=4))
+    dev = lambda a: torch.as_tensor(a, dtype=torch.float64, device="cuda:0")
+    r, y = ctx.empty(), ctx.empty()
+    ctx.residual(dev(u), dev(b), r)
+    ctx.apply(dev(u), y)
+    torch.cuda.synchronize()
+    rg, yg = r.cpu().numpy().reshape(p.nnode, -1), y.cpu().numpy().reshape(p.nnode, -1)
+    L = k * n + 1
+    zero = np.zeros_like(b)
+    for I, J in [(0, 0), (1, 1), (2, 1), (k, k), (L // 2, L // 2 + 1), (L - 2, L - 2), (L - 1, 5), (7, L - 2)]:
+        i = J * L + I
+        ref = p.residual_node(i, u, b)
+        assert np.max(np.abs(rg[i] - ref)) <= 1e-10 * max(np.max(np.abs(ref)), 1e-300), (I, J)
+        refy = -p.residual_node(i, u, zero)
+        assert np.max(np.abs(yg[i] - refy)) <= 1e-10 * max(np.max(np.abs(refy)), 1e-300), (I, J)
+    ctx.close()
