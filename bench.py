@@ -130,13 +130,13 @@ def barrier(ws):
         dist.barrier()
 
 
-def ncu_traffic(kclass):
+def ncu_traffic(kclass, path=None, names=None):
     """dram__bytes_read.sum + dram__bytes_write.sum of the finest-level launch of
-    the kernel behind a timing class, from the committed `ncu --set full` summary
-    of the C2 bench (profiles/r01_final_c2_ncu.txt); (None, None) if absent."""
+    the kernel behind a timing class, from a committed `ncu --set full` summary
+    (default: the C2 bench's profiles/r01_final_c2_ncu.txt); (None, None) if absent."""
     import re
-    names = {"residual": "k_residual_tma", "sweep": "k_sweep_kron_mma", "krylov": "k_krylov"}
-    path = os.path.join(ROOT, "profiles", "r01_final_c2_ncu.txt")
+    names = names or {"residual": "k_residual_tma", "sweep": "k_sweep_kron_mma", "krylov": "k_krylov"}
+    path = path or os.path.join(ROOT, "profiles", "r01_final_c2_ncu.txt")
     if kclass not in names or not os.path.exists(path):
         return None, None
     best = None
@@ -153,7 +153,7 @@ def ncu_traffic(kclass):
             best = (vals["gpu__time_duration.sum"], vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
     if best is None:
         return None, None
-    return best[1], "profiles/r01_final_c2_ncu.txt (ncu --set full, finest-level launch)"
+    return best[1], os.path.relpath(path, ROOT) + " (ncu --set full, finest-level launch)"
 
 
 # --------------------------------------------------------------------- oracle
@@ -218,6 +218,28 @@ def run_reference(args, ws, rank):
 
 
 # ---------------------------------------------------------------------- GPU arm
+def top_roofline(stats, ncu_path=None, ncu_names=None):
+    """Roofline object for the timing class with the largest device time (C3, C5
+    lines): achieved algorithmic bytes (or flops) per launch over its measured
+    per-launch time, against the measured HBM peak or the derived FP64 peak,
+    whichever bounds it."""
+    hbm, hbm_src, fp64 = peaks()
+    tot = sum(s["ms"] for s in stats.values())
+    (a, l), st = max(stats.items(), key=lambda kv: kv[1]["ms"])
+    t = st["ms"] / st["launches"] / 1e3
+    gbs, tfs = st["bytes"] / st["launches"] / t / 1e9, st["flops"] / st["launches"] / t / 1e12
+    alu = st["flops"] / (fp64 * 1e12) > st["bytes"] / (hbm * 1e9)
+    traffic, src = (None, None)
+    if ncu_path:
+        traffic, src = ncu_traffic(a, os.path.join(ROOT, "profiles", ncu_path), ncu_names)
+    return {"bound": "alu" if alu else "hbm", "achieved": tfs if alu else gbs,
+            "peak": fp64 if alu else hbm, "unit": "TFLOP/s" if alu else "GB/s",
+            "frac": (tfs / fp64) if alu else (gbs / hbm), "traffic": traffic, "traffic_source": src,
+            "kernel": f"{a}@L{l}",
+            "share_of_kernel_time": st["ms"] / tot if tot else None,
+            "peak_source": hbm_src if not alu else "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
+
+
 def run_c5(args, ws, rank, local):
     """BASELINE configs[4] (C5), per GPU (weak reading R24): heat, P2 x DG1,
     N = 256 (dt = 1/256, T = 1), 1024x1024 mesh, 20 stationary V(1,1) cycles
@@ -310,7 +332,7 @@ def run_c5(args, ws, rank, local):
                        "ndof_per_gpu": lay["ndof"], "levels": lay["nlevels"], "setup_s": round(setup_s, 2),
                        "parallelism": f"{ws} spatial strips, NCCL halo per operator" if ws > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (17 GB vectors); no flush"},
-            "relres_after_20_vcycles": rel, "per_kernel": per_kernel, "clocks": clk,
+            "relres_after_20_vcycles": rel, "roofline": top_roofline(stats), "per_kernel": per_kernel, "clocks": clk,
             "gpu_launches": w.launch_count() - l0}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -422,6 +444,8 @@ def run_c3(args, ws, rank, local):
             "fgmres_iterations": its_l[0], "fgmres_status_relres": st_l[0], "linearize_ms": lin_ms,
             "linearize_kernels": lin_stats,
             "vcycle_ms": ev2[0].elapsed_time(ev2[1]) / 5, "smoother_sweep_ms": ev2[2].elapsed_time(ev2[3]) / 5,
+            "roofline": top_roofline(stats, "r01_final_c3_ncu.txt",
+                                     {"sweep": "k_ns_sweep", "residual": "k_ns_residual"}),
             "per_kernel": per_kernel, "clocks": clk, "gpu_launches": w.launch_count() - l0}
     if rank == 0:
         print(json.dumps(line), flush=True)
