@@ -433,6 +433,8 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
       check_launch();
     }
   }
+  launch_ns_coarse_H(c->q, c->N, C.mp, C.pin, C.nodes, C.sid2c, L0.A, C.nsinvT, C.nsH, C.nsG, s);
+  check_launch();
   CK(cudaStreamSynchronize(s));
   c->err_level = c->err_patch = c->err_slab = -1;
   for (int l = (nl == 1 ? 0 : 1); l < nl; ++l) {
@@ -585,6 +587,13 @@ void setup_ns(wrmg_ctx *c) {
     C.nspiv = dalloc<int32_t>((size_t)c->N * C.m);
     C.nsinfo = dalloc<int32_t>(c->N);
     C.xq = dalloc<double>(P.ns);
+    std::vector<int32_t> s2c(P.ns, -1);
+    for (size_t i = 0; i < nodes.size(); ++i) s2c[nodes[i]] = (int32_t)i;
+    C.sid2c = dupload(s2c, s);
+    C.nsH = dalloc<double>((size_t)c->N * C.mp * C.m);
+    C.nsG = dalloc<double>((size_t)c->N * C.mp * C.mp);
+    C.nsZ = dalloc<double>((size_t)c->N * C.m);
+    C.nsY = dalloc<double>((size_t)c->N * C.mp);
   }
   c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
   c->red = dalloc<double>(64 + 64 * 148 * 4);
@@ -780,7 +789,15 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
     const Coarse &C = c->coarse;
     PScope ps(c, WRMG_K_COARSE, 0, 8.0 * c->N * (double)C.m * C.m + 16.0 * L.nnode * c->nt,
               2.0 * c->N * (double)C.m * C.m);
-    launch_ns_coarse_solve(c->q, c->N, C.mp, C.pin, C.nodes, L.A, C.nsinvT, r, z, C.xq, L.nnode, C.nnzj, s);
+    static const bool march = [] {  // WRMG_NS_COARSE_MARCH=1: the slab-by-slab cluster march (A/B)
+      const char *e = getenv("WRMG_NS_COARSE_MARCH");
+      return e && e[0] == '1';
+    }();
+    if (march)
+      launch_ns_coarse_solve(c->q, c->N, C.mp, C.pin, C.nodes, L.A, C.nsinvT, r, z, C.xq, L.nnode, C.nnzj, s);
+    else
+      launch_ns_coarse_solve_pint(c->q, c->N, C.mp, C.pin, C.nodes, C.nsinvT, C.nsH, C.nsG, C.nsZ, C.nsY, r, z,
+                                  L.nnode, s);
     ns_project(c, L, z);
     return;
   }
@@ -1835,7 +1852,8 @@ void wrmg_destroy(wrmg_ctx *c) {
   Coarse &C = c->coarse;
   for (void *p : {(void *)C.nodes, (void *)C.Dblk, (void *)C.DinvT, (void *)C.GT, (void *)C.Gq, (void *)C.Z,
                   (void *)C.Y, (void *)C.piv, (void *)C.info, (void *)C.kV, (void *)C.kVT, (void *)C.kS,
-                  (void *)C.ksig, (void *)C.nsD, (void *)C.nsinvT, (void *)C.xq, (void *)C.nspiv, (void *)C.nsinfo})
+                  (void *)C.ksig, (void *)C.nsD, (void *)C.nsinvT, (void *)C.xq, (void *)C.nspiv, (void *)C.nsinfo,
+                  (void *)C.nsH, (void *)C.nsG, (void *)C.nsZ, (void *)C.nsY, (void *)C.sid2c})
     dfree(p);
   for (void *p : {(void *)c->th_ref, (void *)c->th_T, (void *)c->bcg, (void *)c->bcg_st, (void *)c->gred, (void *)c->proj, (void *)c->conv_nl,
                   (void *)c->nl_b, (void *)c->nl_r, (void *)c->nl_dx})

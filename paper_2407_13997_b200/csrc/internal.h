@@ -148,6 +148,11 @@ struct Coarse {
   int nnzj = 0;               // CSR entries of the free coarse rows (jump mass rows staged by the solve)
   double *nsD = nullptr, *nsinvT = nullptr, *xq = nullptr;
   int32_t *nspiv = nullptr, *nsinfo = nullptr;
+  // parallel-in-time form of the NS coarse march (only the velocity end trace
+  // propagates): H_n = D_n^{-1} E (m x mp per slab, column-major), G_n = its a = q
+  // rows (mp x mp, column-major), scratch z_n = D_n^{-1} r_n (N x m), y_n (N x mp)
+  double *nsH = nullptr, *nsG = nullptr, *nsZ = nullptr, *nsY = nullptr;
+  int32_t *sid2c = nullptr;   // sid -> coarse free index or -1
 };
 
 }  // namespace wrmg

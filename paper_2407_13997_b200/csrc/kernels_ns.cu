@@ -1187,6 +1187,121 @@ __global__ void __launch_bounds__(1024) k_ns_coarse_solve(int mc, int N, int pin
   }
 }
 
+// ---- Parallel-in-time coarse march.  With E the jump (rows (i, a=0) of free sid i:
+// E[(i,0), j] = M[s_i, s_j], pinned row 0) and y_n = x_n[a = q] (per free sid):
+//   x_n = D_n^{-1} r_n + H_n y_{n-1},  H_n = D_n^{-1} E,   y_n = x_n[q] = z_n[q] + G_n y_{n-1}
+// (G_n = the a = q rows of H_n).  H_n and G_n are formed once per linearisation;
+// a solve is then two slab-parallel GEMV passes around an mp-sized recurrence.
+// H[(n mp + j) m + rho] = sum_{e in row(s_j)} M_e D_n^{-1}[rho][(idx(col_e), 0)]  (M symmetric)
+template <int NQ>
+__global__ void k_ns_coarse_H(int mc, int N, int pin, const int32_t *__restrict__ cnodes,
+                              const int32_t *__restrict__ sid2c, const int32_t *__restrict__ rowptr,
+                              const int32_t *__restrict__ col, const double *__restrict__ Mv,
+                              const double *__restrict__ DinvT, double *__restrict__ H, double *__restrict__ G) {
+  const int m = NQ * mc;
+  const int rho = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, n = blockIdx.z;
+  if (rho >= m) return;
+  const double *Di = DinvT + (int64_t)n * m * m;
+  const int sj = cnodes[j];
+  double acc = 0.0;
+  for (int e = rowptr[sj]; e < rowptr[sj + 1]; ++e) {
+    const int i = sid2c[col[e]];
+    if (i >= 0 && i != pin) acc = fma(Mv[e], Di[(int64_t)(i * NQ) * m + rho], acc);
+  }
+  H[((int64_t)n * mc + j) * m + rho] = acc;
+  if (rho % NQ == NQ - 1) G[((int64_t)n * mc + j) * mc + rho / NQ] = acc;
+}
+
+// z_n = D_n^{-1} r_n (pinned row of r taken as 0): CTA = (slab, 32 rows), warp w
+// sums columns w, w + 8, ...; out[n m + rho].  With H (K3) the CTA adds H_n y_{n-1}
+// and scatters x_n to the sid layout.
+template <int NQ, bool FINAL>
+__global__ void __launch_bounds__(256) k_ns_coarse_pass(int mc, int N, int pin, const int32_t *__restrict__ cnodes,
+                                                        const double *__restrict__ DinvT,
+                                                        const double *__restrict__ r, double *__restrict__ Z,
+                                                        const double *__restrict__ H, const double *__restrict__ Y,
+                                                        double *__restrict__ z) {
+  extern __shared__ double gsh[];  // m (pass 1) or mc (pass 2)
+  __shared__ double part[8][33];
+  const int m = NQ * mc, n = blockIdx.x, rb = blockIdx.y * 32;
+  const int tid = threadIdx.x, rl = tid & 31, w = tid >> 5;
+  const int64_t NT = (int64_t)N * NQ;
+  double acc = 0.0;
+  const int rho = rb + rl;
+  if (!FINAL) {
+    for (int s2 = tid; s2 < m; s2 += blockDim.x) {
+      const int i = s2 / NQ, a = s2 - i * NQ;
+      gsh[s2] = (i != pin) ? __ldg(r + (int64_t)cnodes[i] * NT + (int64_t)n * NQ + a) : 0.0;
+    }
+    __syncthreads();
+    if (rho < m) {
+      const double *Di = DinvT + (int64_t)n * m * m;
+      for (int s2 = w; s2 < m; s2 += 8) acc = fma(__ldg(Di + (int64_t)s2 * m + rho), gsh[s2], acc);
+    }
+  } else {
+    if (n > 0) {
+      for (int j = tid; j < mc; j += blockDim.x) gsh[j] = Y[(int64_t)(n - 1) * mc + j];
+      __syncthreads();
+      if (rho < m) {
+        const double *Hn = H + (int64_t)n * mc * m;
+        for (int j = w; j < mc; j += 8) acc = fma(__ldg(Hn + (int64_t)j * m + rho), gsh[j], acc);
+      }
+    }
+  }
+  part[w][rl] = acc;
+  __syncthreads();
+  if (w == 0 && rho < m) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][rl];
+    if (!FINAL) {
+      Z[(int64_t)n * m + rho] = t;
+    } else {
+      const int i = rho / NQ, a = rho - i * NQ;
+      z[(int64_t)cnodes[i] * NT + (int64_t)n * NQ + a] = Z[(int64_t)n * m + rho] + t;
+    }
+  }
+}
+
+// y_n = z_n[q] + G_n y_{n-1} (y_{-1} = 0), one CTA of 1024 threads: thread (row
+// jj = t % 128 + 128 k, column group t / 128 of 8); y double-buffered by slab
+// parity, two barriers per slab; Y[n mp + jj].
+template <int NQ>
+__global__ void __launch_bounds__(1024) k_ns_coarse_yrec(int mc, int N, const double *__restrict__ Z,
+                                                         const double *__restrict__ G, double *__restrict__ Y) {
+  extern __shared__ double sh[];  // y (2 mc) + partials (8 mc)
+  double *yb = sh, *pp = sh + 2 * mc;
+  const int m = NQ * mc, tid = threadIdx.x, rr = tid & 127, cg8 = tid >> 7;
+  for (int j = tid; j < 2 * mc; j += blockDim.x) yb[j] = 0.0;
+  __syncthreads();
+  for (int n = 0; n < N; ++n) {
+    const double *Gn = G + (int64_t)n * mc * mc;
+    const double *yp = yb + ((n + 1) & 1) * mc;
+    double *yn = yb + (n & 1) * mc;
+    for (int jj = rr; jj < mc; jj += 128) {
+      double a0 = 0.0, a1 = 0.0;
+      if (n > 0) {
+        int j = cg8;
+        for (; j + 8 < mc; j += 16) {
+          a0 = fma(__ldg(Gn + (int64_t)j * mc + jj), yp[j], a0);
+          a1 = fma(__ldg(Gn + (int64_t)(j + 8) * mc + jj), yp[j + 8], a1);
+        }
+        if (j < mc) a0 = fma(__ldg(Gn + (int64_t)j * mc + jj), yp[j], a0);
+      }
+      pp[cg8 * mc + jj] = a0 + a1;
+    }
+    __syncthreads();
+    for (int jj = tid; jj < mc; jj += blockDim.x) {
+      double v = Z[(int64_t)n * m + jj * NQ + NQ - 1];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v += pp[k * mc + jj];
+      yn[jj] = v;
+      Y[(int64_t)n * mc + jj] = v;
+    }
+    __syncthreads();
+  }
+}
+
 // Cluster variant: CS CTAs share the slab loop; CTA c owns rows [c RB, (c+1) RB)
 // of every D_n^{-1} (RB = ceil(m / CS)), every CTA forms the full g (the jump needs
 // the whole end trace, kept per sid in each CTA's shared memory and broadcast
@@ -1496,6 +1611,38 @@ void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, c
                                                 conv, tm, D);
   });
   ++g_launches;
+}
+
+void launch_ns_coarse_H(int q, int N, int mc, int pin, const int32_t *cnodes, const int32_t *sid2c, const DevCSR &A,
+                        const double *DinvT, double *H, double *G, cudaStream_t s) {
+  const int m = (q + 1) * mc;
+  dim3 grid((unsigned)((m + 127) / 128), (unsigned)mc, (unsigned)N);
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    k_ns_coarse_H<NQ><<<grid, 128, 0, s>>>(mc, N, pin, cnodes, sid2c, A.rowptr, A.col, A.val, DinvT, H, G);
+  });
+  ++g_launches;
+}
+
+void launch_ns_coarse_solve_pint(int q, int N, int mc, int pin, const int32_t *cnodes, const double *DinvT,
+                                 const double *H, const double *G, double *Zs, double *Ys, const double *r, double *z,
+                                 int64_t ns, cudaStream_t s) {
+  const int m = (q + 1) * mc;
+  cudaMemsetAsync(z, 0, ns * (int64_t)N * (q + 1) * sizeof(double), s);
+  dim3 grid((unsigned)N, (unsigned)((m + 31) / 32));
+  by_nq(q + 1, [&](auto NQc) {
+    constexpr int NQ = decltype(NQc)::value;
+    k_ns_coarse_pass<NQ, false><<<grid, 256, m * sizeof(double), s>>>(mc, N, pin, cnodes, DinvT, r, Zs, nullptr,
+                                                                      nullptr, nullptr);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_ns_coarse_yrec<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_ns_coarse_yrec<NQ><<<1, 1024, 10 * mc * sizeof(double), s>>>(mc, N, Zs, G, Ys);
+    k_ns_coarse_pass<NQ, true><<<grid, 256, mc * sizeof(double), s>>>(mc, N, pin, cnodes, DinvT, r, Zs, H, Ys, z);
+  });
+  g_launches += 3;
 }
 
 void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,

@@ -53,6 +53,11 @@ constexpr int kGJMinM = 192;  // below this the CTA-per-matrix LU + inverse is u
 size_t gj_scratch_doubles(int m, int batch);
 void launch_gj_inverse_batched(double *A, int m, int batch, int32_t *piv, int32_t *info, double *out,
                                double *scratch, cudaStream_t s);
+void launch_ns_coarse_H(int q, int N, int mc, int pin, const int32_t *cnodes, const int32_t *sid2c, const DevCSR &A,
+                        const double *DinvT, double *H, double *G, cudaStream_t s);
+void launch_ns_coarse_solve_pint(int q, int N, int mc, int pin, const int32_t *cnodes, const double *DinvT,
+                                 const double *H, const double *G, double *Zs, double *Ys, const double *r, double *z,
+                                 int64_t ns, cudaStream_t s);
 void launch_lu_inverse_batched(const double *LU, const int32_t *piv, int m, int batch, double *out, cudaStream_t s);
 
 }  // namespace wrmg
