@@ -89,6 +89,8 @@ def test_abi_rejects_bad_arguments():
     assert lib.wrmg_fgmres(c._h, None, None, 0, 1, 1e-8, 0.0, None, None) == 1  # restart < 1
     assert lib.wrmg_newton(c._h, ctypes.c_void_p(1), 1e-8, 3, None, None) == 2  # heat is linear
     assert lib.wrmg_level_size(c._h, 99, ctypes.byref(ctypes.c_int64())) == 1
+    assert lib.wrmg_set_boundary_values(c._h, None) == 2  # heat: Dirichlet data is the setup's
+    assert lib.wrmg_set_boundary_values(None, None) == 1
     c.close()
     with pytest.raises(w.WrmgError) as e:
         w.Context(4, 4, 0.25, degree=4, q=0, nslabs=2, dt=0.5)
@@ -99,6 +101,12 @@ def test_abi_rejects_bad_arguments():
     with pytest.raises(w.WrmgError) as e:
         w.Context(4, 4, 0.25, degree=1, q=0, nslabs=2, dt=0.5, problem="ns", reynolds=0.0)
     assert e.value.status == 1
+    # NS: boundary data set, then restored with NULL
+    import torch
+    cn = w.Context(4, 4, 0.25, degree=1, q=0, nslabs=2, dt=0.5, problem="ns", reynolds=1.0, bc="dirichlet0")
+    cn.set_boundary_values(torch.zeros(cn.layout["ndof"], dtype=torch.float64, device="cuda:0"))
+    cn.set_boundary_values(None)
+    cn.close()
 
 
 @pytest.mark.parametrize("n,k,q,N", [(80, 3, 1, 70), (112, 2, 0, 100), (80, 3, 1, 64), (80, 3, 2, 65)])
