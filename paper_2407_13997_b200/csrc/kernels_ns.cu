@@ -337,72 +337,77 @@ __device__ __forceinline__ double block_entry(const int32_t *__restrict__ rowptr
 // idx[c] = the column of A holding column c of the inverse.  Returns 0 or 1 + the
 // first column with |pivot| < tol.
 constexpr int GJB = 8;
+__device__ __forceinline__ void dmma_ns(double &c0, double &c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
 __device__ int gj_invert_smem(double *A, int m, double tol, double *X, int *piv, int *idx) {
-  __shared__ double s_val[32];
+  __shared__ double s_val[32], s_sv[32];
   __shared__ int s_idx[32];
-  __shared__ double s_pv;
-  __shared__ int s_p, s_info;
+  __shared__ int s_info;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
   if (tid == 0) s_info = 0;
-  const int ntr = (m + 3) / 4;
+  __syncthreads();
   for (int k0 = 0; k0 < m; k0 += GJB) {
     const int nb = min(GJB, m - k0), k1 = k0 + nb;
     for (int c = k0; c < k1; ++c) {
-      double bv = -1.0;
+      // (1) argmax |A[r][c]|, r >= c (first maximum), with its signed value
+      double bv = -1.0, bs = 0.0;
       int bi = m;
       for (int r = c + tid; r < m; r += nth) {
-        const double v = fabs(A[r * m + c]);
+        const double sv = A[r * m + c], v = fabs(sv);
         if (v > bv) {
           bv = v;
+          bs = sv;
           bi = r;
         }
       }
       for (int o = 16; o; o >>= 1) {
         const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > bv || (ov == bv && oi < bi)) {
           bv = ov;
+          bs = os;
           bi = oi;
         }
       }
       if (lane == 0) {
         s_val[wid] = bv;
+        s_sv[wid] = bs;
         s_idx[wid] = bi;
       }
       __syncthreads();
+      // (2) every thread combines the warp maxima; whole-row interchange c <-> p, row c
+      // scaled on the panel columns
+      double v = s_val[0], pv = s_sv[0];
+      int p = s_idx[0];
+      for (int w = 1; w < nw; ++w)
+        if (s_val[w] > v || (s_val[w] == v && s_idx[w] < p)) {
+          v = s_val[w];
+          pv = s_sv[w];
+          p = s_idx[w];
+        }
       if (tid == 0) {
-        double v = s_val[0];
-        int ix = s_idx[0];
-        for (int w = 1; w < nw; ++w)
-          if (s_val[w] > v || (s_val[w] == v && s_idx[w] < ix)) {
-            v = s_val[w];
-            ix = s_idx[w];
-          }
-        piv[c] = ix;
-        s_p = ix;
-        s_pv = A[ix * m + c];
+        piv[c] = p;
         if (!(v >= tol) && s_info == 0) s_info = c + 1;
       }
-      __syncthreads();
-      const int p = s_p;
-      const double pinv = s_pv != 0.0 ? 1.0 / s_pv : 0.0;
-      // whole-row interchange c <-> p; row c scaled on the panel columns
+      const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
       for (int j = tid; j < m; j += nth) {
         const double t1 = A[c * m + j], t2 = A[p * m + j];
         A[p * m + j] = t1;
         A[c * m + j] = (j >= k0 && j < k1) ? ((j == c) ? pinv : t2 * pinv) : t2;
       }
       __syncthreads();
-      // panel rank-1 step on the other rows: A[r][j] -= f_r row_c[j], column c = -f_r / pivot
-      for (int e = tid; e < m * GJB; e += nth) {
-        const int r = e / GJB, jj = e % GJB, j = k0 + jj;
-        if (r == c || jj >= nb) continue;
+      // (3) thread per row: panel rank-1 step and the pivot column, -f_r / pivot
+      for (int r = tid; r < m; r += nth) {
+        if (r == c) continue;
         const double fr = A[r * m + c];
-        if (j != c) A[r * m + j] = fma(-fr, A[c * m + j], A[r * m + j]);
+        for (int j = k0; j < k1; ++j)
+          if (j != c) A[r * m + j] = fma(-fr, A[c * m + j], A[r * m + j]);
+        A[r * m + c] = -fr * pinv;
       }
-      __syncthreads();
-      for (int r = tid; r < m; r += nth)
-        if (r != c) A[r * m + c] = -A[r * m + c] * A[c * m + c];
       __syncthreads();
     }
     // X = pivot rows of the other columns
@@ -411,44 +416,37 @@ __device__ int gj_invert_smem(double *A, int m, double tol, double *X, int *piv,
       X[e] = (j >= k0 && j < k1) ? 0.0 : A[(k0 + t) * m + j];
     }
     __syncthreads();
-    // A[:, j] = [0 on pivot rows; A] + Panel X   (columns outside the panel).
-    // Warp item = 4 rows x 64 columns, lane = columns (lane, lane + 32): the row-major
-    // A and X accesses are consecutive across lanes, the panel values broadcast.
+    // A[:, j] = [0 on pivot rows; A] + Panel X   (columns outside the panel), on the
+    // FP64 tensor cores: warp item = one 8 x 8 output tile, two mma.m8n8k4 (k = the
+    // 8 panel columns).  Fragments (tools/dmma_layout.cu): a = P[l>>2][l&3],
+    // b = X[l&3][l>>2], c[e] = C[l>>2][2(l&3)+e]; the panel is exactly tile column k0/8.
     {
-      const int ncb = (m + 63) / 64, items = ntr * ncb;
-      for (int it = wid; it < items; it += nw) {
-        const int r0 = (it / ncb) * 4, jb = (it % ncb) * 64;
-        int jj[2];
-        bool wr[2];
+      const int nt8 = (m + 7) / 8, pt = k0 / 8;
+      const int lr = lane >> 2, lc = lane & 3;
+      for (int it = wid; it < nt8 * nt8; it += nw) {
+        const int tr = it / nt8, tc = it - tr * nt8;
+        if (tc == pt) continue;
+        const int R = tr * 8 + lr;
+        const bool rok = R < m, rpiv = R >= k0 && R < k1;
+        double c[2];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          jj[b] = jb + lane + 32 * b;
-          wr[b] = jj[b] < m && (jj[b] < k0 || jj[b] >= k1);
+        for (int e = 0; e < 2; ++e) {
+          const int J = tc * 8 + 2 * lc + e;
+          c[e] = (rok && !rpiv && J < m) ? A[R * m + J] : 0.0;
         }
-        double acc[4][2];
+        const int Jb = tc * 8 + lr;
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b) {
-            const int r = r0 + a;
-            acc[a][b] = (wr[b] && r < m && (r < k0 || r >= k1)) ? A[r * m + jj[b]] : 0.0;
-          }
-        for (int t = 0; t < nb; ++t) {
-          double pv[4], xv[2];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) pv[a] = (r0 + a < m) ? A[(r0 + a) * m + k0 + t] : 0.0;
-#pragma unroll
-          for (int b = 0; b < 2; ++b) xv[b] = jj[b] < m ? X[t * m + jj[b]] : 0.0;
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 2; ++b) acc[a][b] = fma(pv[a], xv[b], acc[a][b]);
+        for (int h = 0; h < 2; ++h) {
+          const int t = 4 * h + lc;
+          const double a = (rok && t < nb) ? A[R * m + k0 + t] : 0.0;
+          const double b = (t < nb && Jb < m) ? X[t * m + Jb] : 0.0;
+          dmma_ns(c[0], c[1], a, b);
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-            if (wr[b] && r0 + a < m) A[(r0 + a) * m + jj[b]] = acc[a][b];
+        for (int e = 0; e < 2; ++e) {
+          const int J = tc * 8 + 2 * lc + e;
+          if (rok && J < m) A[R * m + J] = c[e];
+        }
       }
     }
     __syncthreads();
@@ -490,18 +488,55 @@ __global__ void __launch_bounds__(NTH) k_ns_factor(int mp, int N, int64_t mstrid
   const int tid = threadIdx.x;
   for (int i = tid; i < mp; i += blockDim.x) nodes[i] = pnodes[p * mp + i];
   __syncthreads();
-  for (int e = tid; e < m * m; e += blockDim.x) {
-    const int rho = e / m, sig = e - rho * m;  // node-major: rho = i NQ + a
-    const int i = rho / NQ, a = rho - i * NQ, j = sig / NQ, bb = sig - j * NQ;
-    const int si = nodes[i], sj = nodes[j];
-    double v;
-    if (si < 0 || sj < 0) {
-      v = (rho == sig) ? 1.0 : 0.0;
-    } else {
-      const int64_t pe = (p * mp + i) * mp + j;
-      v = block_entry_tab<NQ>(__ldg(ppos + pe), __ldg(pvv + pe), Mv, KGv, conv, NT, n, tm, a, bb);
+  // thread per node pair (i, j): the pair's CSR position, mass / stiffness values
+  // and convection values are loaded once for its NQ x NQ entries (node-major:
+  // rho = i NQ + a, sig = j NQ + bb); two pairs per iteration for more loads in flight
+  const int npair = mp * mp;
+  for (int e0 = tid; e0 < npair; e0 += 2 * blockDim.x) {
+    int pos[2], vv[2], ii[2], jj[2];
+    bool pad[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = e0 + h * blockDim.x;
+      const bool ok = e < npair;
+      ii[h] = ok ? e / mp : 0;
+      jj[h] = ok ? e - ii[h] * mp : 0;
+      pad[h] = !ok || nodes[ii[h]] < 0 || nodes[jj[h]] < 0;
+      const int64_t pe = (p * mp + ii[h]) * mp + jj[h];
+      pos[h] = (!pad[h]) ? __ldg(ppos + pe) : -1;
+      vv[h] = (!pad[h]) ? __ldg(pvv + pe) : -1;
     }
-    A[e] = v;
+    double mv[2], kg[2], cv[2][NQ];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mv[h] = pos[h] >= 0 ? __ldg(Mv + pos[h]) : 0.0;
+      kg[h] = pos[h] >= 0 ? __ldg(KGv + pos[h]) : 0.0;
+      const double *cp = conv + (int64_t)(vv[h] >= 0 ? vv[h] : 0) * NT + (int64_t)n * NQ;
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) cv[h][c] = (pos[h] >= 0 && vv[h] >= 0) ? __ldg(cp + c) : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (e0 + h * blockDim.x >= npair) continue;
+#pragma unroll
+      for (int a = 0; a < NQ; ++a)
+#pragma unroll
+        for (int bb = 0; bb < NQ; ++bb) {
+          const int rho = ii[h] * NQ + a, sig = jj[h] * NQ + bb;
+          double v;
+          if (pad[h]) {
+            v = (rho == sig) ? 1.0 : 0.0;
+          } else if (pos[h] < 0) {
+            v = 0.0;
+          } else {
+            v = tm.CE[a * NQ + bb] * mv[h] + tm.Mt[a * NQ + bb] * kg[h];
+            if (vv[h] >= 0)
+#pragma unroll
+              for (int c = 0; c < NQ; ++c) v = fma(tm.T[(a * NQ + bb) * NQ + c], cv[h][c], v);
+          }
+          A[rho * m + sig] = v;
+        }
+    }
   }
   __syncthreads();
   double rn = 0.0;  // max row norm (R10 tolerance)
