@@ -1548,19 +1548,26 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
   dim3 grid((unsigned)npatch, (unsigned)N);
   // row-per-thread register Gauss-Jordan, fully unrolled (instantiated for DG0 / DG1 patch sizes only:
   // each instance is ~7k straight-line DFMAs)
-  if (q == 0 && m <= 64) {
+  // The shared-memory blocked kernel (gj_invert_smem: DMMA tile updates, 2.5 TF/s at
+  // m = 78) is the default for every m; WRMG_NS_FACTOR_REG=1 selects the register
+  // Gauss-Jordan kernels below for m <= 80 (1.9 TF/s at m = 78; A/B).
+  static const bool force_smem = [] {
+    const char *e = getenv("WRMG_NS_FACTOR_REG");
+    return !(e && e[0] == '1');
+  }();
+  if (!force_smem && q == 0 && m <= 64) {
     k_ns_factor_row<1, 64, 64><<<grid, 64, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos,
                                                    pvv);
     ++g_launches;
     return;
   }
-  if (q == 1 && m <= 80) {
+  if (!force_smem && q == 1 && m <= 80) {
     k_ns_factor_row<2, 80, 96><<<grid, 96, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos,
                                                    pvv);
     ++g_launches;
     return;
   }
-  if (m <= 80) {  // register-tiled Gauss-Jordan (4 x 8 tiles, 20 x 10 threads)
+  if (!force_smem && m <= 80) {  // register-tiled Gauss-Jordan (4 x 8 tiles, 20 x 10 threads)
     by_nq(q + 1, [&](auto NQc) {
       constexpr int NQ = decltype(NQc)::value;
       k_ns_factor_reg<NQ, 4, 8, 20, 10><<<grid, 256, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out,
