@@ -11,7 +11,7 @@ python tools/ncu_summary.py launches gpurun_out/f_c2_launches.csv > gpurun_out/f
 ncu --set full --clock-control none --import-source on -k regex:"k_residual_tma|k_sweep_kron_mma|k_krylov" -c 4 -o gpurun_out/f_c2_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 python tools/ncu_summary.py report gpurun_out/f_c2_full.ncu-rep > gpurun_out/f_c2_ncu.txt
 # C3: the finest-level launch of each top NS kernel (factor at setup, then the sweep and residual)
-ncu --set full --clock-control none -k regex:"k_ns_factor_row" -c 1 -o gpurun_out/f_c3_factor -f python bench.py --config C3 --steps 1 --warmup 0 > /dev/null 2>&1
+ncu --set full --clock-control none -k regex:"k_ns_factor" -c 1 -o gpurun_out/f_c3_factor -f python bench.py --config C3 --steps 1 --warmup 0 > /dev/null 2>&1
 ncu --set full --clock-control none -k regex:"k_ns_sweep" -c 1 -o gpurun_out/f_c3_sweep -f python bench.py --config C3 --steps 1 --warmup 0 > /dev/null 2>&1
 ncu --set full --clock-control none -k regex:"k_ns_residual" -c 1 -o gpurun_out/f_c3_resid -f python bench.py --config C3 --steps 1 --warmup 0 > /dev/null 2>&1
 python tools/ncu_summary.py report gpurun_out/f_c3_factor.ncu-rep gpurun_out/f_c3_sweep.ncu-rep gpurun_out/f_c3_resid.ncu-rep > gpurun_out/f_c3_ncu.txt
