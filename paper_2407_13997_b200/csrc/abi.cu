@@ -1479,8 +1479,6 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
       }
       h.resize(nv);
       reduce_to_host(c, red, nv, h.data());
-      if (strip)  // the CGS update consumes the global coefficients
-        small_h2d(c, h.data(), red, nv);
     };
     CK(cudaMemsetAsync(x, 0, n * sizeof(double), s));
     // strips: norms and dots over owned rows (ghost columns of the Krylov vectors are zero)
@@ -1500,11 +1498,14 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
     bool done = beta <= target;
     if (done) status = WRMG_OK;
     std::vector<double> H((size_t)(restart + 1) * restart), cs(restart), sn(restart), g(restart + 1), h, h2, y;
+    // Lazily scaled basis: the stored V_i' and Z_i' = B V_i' carry a host scale sc_i
+    // (V_i = sc_i V_i', sc_i = 1 / |V_i'|), so no pass over the vectors normalises
+    // them: the new basis vector is the orthogonalised w itself (buffer swap) and
+    // the scales enter the CGS coefficients, the Hessenberg entries and y.
+    std::vector<double> sc(restart + 1, 0.0), coef(32);
     while (!done && its < maxit) {
-      {
-        PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 1.0 * n);
-        launch_scale(c->V[0], c->tmp, 1.0 / beta, n, s);
-      }
+      std::swap(c->V[0], c->tmp);  // V_0' = r, sc_0 = 1 / beta
+      sc[0] = 1.0 / beta;
       std::fill(H.begin(), H.end(), 0.0);
       std::fill(g.begin(), g.end(), 0.0);
       g[0] = beta;
@@ -1516,7 +1517,14 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         prof_residual(c, (int)c->lv.size() - 1, c->Z[j], nullptr, c->w, false);
         if (strip) zero_ghosts(c, L, c->w);
         // CGS2, fused: h = V^T w;  w -= V h & h2 = V^T w;  w -= V h2 & |w|^2
+        // (w' = A Z_j', the true w = sc_j w': h_i = sc_i sc_j <V_i', w'>, and
+        // w -= sum h_i V_i  <=>  w' -= sum sc_i^2 <V_i', w'> V_i')
         multidot(j + 1, c->w, h);
+        for (int i = 0; i <= j; ++i) {
+          coef[i] = sc[i] * sc[i] * h[i];
+          h[i] *= sc[i] * sc[j];
+        }
+        small_h2d(c, coef.data(), red, j + 1);
         {
           PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 4.0 * (j + 1) * n);
           const int nb = multidot_blocks(n);
@@ -1524,27 +1532,21 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           launch_reduce_partials(part, nb, j + 1, red + 32, s);
         }
         h2.resize(j + 1);
-        if (strip) {
-          reduce_to_host(c, red + 32, j + 1, h2.data());
-          small_h2d(c, h2.data(), red + 32, j + 1);
+        reduce_to_host(c, red + 32, j + 1, h2.data());
+        for (int i = 0; i <= j; ++i) {
+          coef[i] = sc[i] * sc[i] * h2[i];
+          h[i] += sc[i] * sc[j] * h2[i];
         }
-        double hn2 = 0.0;
+        small_h2d(c, coef.data(), red + 32, j + 1);
+        double wn2 = 0.0;
         {
           PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
           const int nb = multidot_blocks(n);
           launch_cgs_update_norm(c->V.data(), j + 1, c->w, red + 32, n, part, nb, s);
           launch_reduce_partials(part, nb, 1, red + 63, s);
         }
-        if (strip) {
-          reduce_to_host(c, red + 63, 1, &hn2);
-        } else {  // h2 and |w|^2 in one small read
-          double tmp2[33];
-          small_d2h(c, red + 32, tmp2, 32);
-          for (int i = 0; i <= j; ++i) h2[i] = tmp2[i];
-          hn2 = tmp2[31];
-        }
-        for (int i = 0; i <= j; ++i) h[i] += h2[i];
-        const double hn = std::sqrt(hn2);
+        reduce_to_host(c, red + 63, 1, &wn2);
+        const double hn = sc[j] * std::sqrt(wn2);
         std::vector<double> col(restart + 1, 0.0);
         for (int i = 0; i <= j; ++i) col[i] = h[i];
         col[j + 1] = hn;
@@ -1568,10 +1570,8 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           done = true;
           break;
         }
-        {
-          PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 16.0 * n, 1.0 * n);
-          launch_scale(c->V[j + 1], c->w, 1.0 / hn, n, s);
-        }
+        std::swap(c->V[j + 1], c->w);  // V_{j+1}' = w', sc_{j+1} = 1 / |w'|
+        sc[j + 1] = 1.0 / std::sqrt(wn2);
         if (std::fabs(g[j + 1]) <= target) {
           status = WRMG_OK;
           done = true;
@@ -1588,6 +1588,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         for (int k2 = i + 1; k2 < jend; ++k2) acc -= H[(size_t)i * restart + k2] * y[k2];
         y[i] = acc / H[(size_t)i * restart + i];
       }
+      for (int i = 0; i < jend; ++i) y[i] *= sc[i];  // x += sum y_i Z_i = sum (y_i sc_i) Z_i'
       small_h2d(c, y.data(), red, jend);
       {
         PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (jend + 2) * n, 2.0 * jend * n);
