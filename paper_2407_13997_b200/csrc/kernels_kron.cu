@@ -659,6 +659,98 @@ __global__ void __launch_bounds__(256) k_ckron_fwd(int mp, int nq, int64_t NT, c
   }
 }
 
+// Variants for mp <= 128 and compile-time NQ: thread (i = t % 128, half = t / 128)
+// sums half of the j range with 4 independent loads in flight; halves combined in
+// shared memory.  The generic kernels above keep one thread per mode and a serial
+// j loop (latency-bound on the V loads: ~55 us per call at C2's 121 coarse modes).
+template <int NQ>
+__global__ void __launch_bounds__(256) k_ckron_fwd2(int mp, int64_t NT, const int32_t *__restrict__ nodes,
+                                                    const double *__restrict__ V, const double *__restrict__ S,
+                                                    const double *__restrict__ r, double *__restrict__ T) {
+  extern __shared__ double g[];  // NQ * mp + 2 * NQ * 128
+  double *ph = g + NQ * mp;
+  const int n = blockIdx.x, tid = threadIdx.x, i = tid & 127, half = tid >> 7;
+  for (int e = tid; e < NQ * mp; e += blockDim.x) {
+    const int a = e / mp, j = e - a * mp;
+    g[e] = r[(int64_t)nodes[j] * NT + (int64_t)n * NQ + a];
+  }
+  __syncthreads();
+  double gh[NQ];
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) gh[a] = 0.0;
+  if (i < mp) {
+    const int j0 = half * ((mp + 1) / 2), j1 = min(mp, j0 + (mp + 1) / 2);
+    int j = j0;
+    for (; j + 4 <= j1; j += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(V + (int64_t)(j + u) * mp + i);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) gh[a] = fma(v[u], g[a * mp + j + u], gh[a]);
+    }
+    for (; j < j1; ++j) {
+      const double v = __ldg(V + (int64_t)j * mp + i);
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) gh[a] = fma(v, g[a * mp + j], gh[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) ph[(half * NQ + a) * 128 + i] = gh[a];
+  __syncthreads();
+  if (half == 0 && i < mp) {
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) gh[a] = ph[a * 128 + i] + ph[(NQ + a) * 128 + i];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double sum = 0.0;
+#pragma unroll
+      for (int b = 0; b < NQ; ++b) sum = fma(S[((int64_t)i * NQ + a) * NQ + b], gh[b], sum);
+      T[((int64_t)n * NQ + a) * mp + i] = sum;
+    }
+  }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(256) k_ckron_bwd2(int mp, int64_t NT, const int32_t *__restrict__ nodes,
+                                                    const double *__restrict__ VT, const double *__restrict__ T,
+                                                    double *__restrict__ x) {
+  extern __shared__ double w[];  // NQ * mp + 2 * NQ * 128
+  double *ph = w + NQ * mp;
+  const int n = blockIdx.x, tid = threadIdx.x, j = tid & 127, half = tid >> 7;
+  for (int e = tid; e < NQ * mp; e += blockDim.x) w[e] = T[(int64_t)n * NQ * mp + e];
+  __syncthreads();
+  double xs[NQ];
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) xs[a] = 0.0;
+  if (j < mp) {
+    const int i0 = half * ((mp + 1) / 2), i1 = min(mp, i0 + (mp + 1) / 2);
+    int i = i0;
+    for (; i + 4 <= i1; i += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldg(VT + (int64_t)(i + u) * mp + j);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) xs[a] = fma(v[u], w[a * mp + i + u], xs[a]);
+    }
+    for (; i < i1; ++i) {
+      const double v = __ldg(VT + (int64_t)i * mp + j);
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) xs[a] = fma(v, w[a * mp + i], xs[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) ph[(half * NQ + a) * 128 + j] = xs[a];
+  __syncthreads();
+  if (half == 0 && j < mp)
+#pragma unroll
+    for (int a = 0; a < NQ; ++a)
+      x[(int64_t)nodes[j] * NT + (int64_t)n * NQ + a] = ph[a * 128 + j] + ph[(NQ + a) * 128 + j];
+}
+
 // per-mode recurrence over all slabs: one warp per mode, lanes = slabs of a
 // 32-slab chunk (shuffle scan), chunks in order with the end trace carried.
 __global__ void k_ckron_scan(int N, int mp, int nq, const double *__restrict__ S, const double *__restrict__ sig,
@@ -758,11 +850,34 @@ void launch_coarse_solve_kron(const Coarse &C, const Level &L, int q, int N, con
   const int nq = q + 1;
   const int64_t NT = (int64_t)N * nq;
   cudaMemsetAsync(x, 0, L.nnode * NT * sizeof(double), s);
-  k_ckron_fwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kV, C.kS, r, C.Z);
+  const size_t sm2 = (size_t)(nq * C.mp + 2 * nq * 128) * sizeof(double);
+  const bool two = C.mp <= 128;
+#define WRMG_CK(NQ, KER, ...)                                                 \
+  case NQ: KER<NQ><<<N, 256, sm2, s>>>(__VA_ARGS__); break;
+  if (two) {
+    switch (nq) {
+      WRMG_CK(1, k_ckron_fwd2, C.mp, NT, C.nodes, C.kV, C.kS, r, C.Z)
+      WRMG_CK(2, k_ckron_fwd2, C.mp, NT, C.nodes, C.kV, C.kS, r, C.Z)
+      WRMG_CK(3, k_ckron_fwd2, C.mp, NT, C.nodes, C.kV, C.kS, r, C.Z)
+      default: k_ckron_fwd2<4><<<N, 256, sm2, s>>>(C.mp, NT, C.nodes, C.kV, C.kS, r, C.Z); break;
+    }
+  } else {
+    k_ckron_fwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kV, C.kS, r, C.Z);
+  }
   ++g_launches;
   k_ckron_scan<<<(C.mp + 3) / 4, 128, 0, s>>>(N, C.mp, nq, C.kS, C.ksig, C.Z);
   ++g_launches;
-  k_ckron_bwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kVT, C.Z, x);
+  if (two) {
+    switch (nq) {
+      WRMG_CK(1, k_ckron_bwd2, C.mp, NT, C.nodes, C.kVT, C.Z, x)
+      WRMG_CK(2, k_ckron_bwd2, C.mp, NT, C.nodes, C.kVT, C.Z, x)
+      WRMG_CK(3, k_ckron_bwd2, C.mp, NT, C.nodes, C.kVT, C.Z, x)
+      default: k_ckron_bwd2<4><<<N, 256, sm2, s>>>(C.mp, NT, C.nodes, C.kVT, C.Z, x); break;
+    }
+  } else {
+    k_ckron_bwd<<<N, 256, nq * C.mp * sizeof(double), s>>>(C.mp, nq, NT, C.nodes, C.kVT, C.Z, x);
+  }
+#undef WRMG_CK
   ++g_launches;
 }
 
