@@ -282,21 +282,21 @@ __global__ void __launch_bounds__(256, 2) k_residual_tma(const __grid_constant__
 // L1-allocating).  A CTA walks an 8x8 tile of rows so the tile's neighbourhood
 // stays L1-resident; with no shared memory and ~40 registers an SM holds 64
 // warps, each with up to `cnt` independent loads in flight.
-template <int NQ>
+template <int NQ, int TRL>
 __global__ void __launch_bounds__(256) k_residual_l1(int Lx, int Ly, int N, const uint8_t *__restrict__ rcls,
                                                      const double *__restrict__ u, const double *__restrict__ b,
                                                      double *__restrict__ r, TMr tm, const StencilTab T, int apply,
                                                      const int64_t *__restrict__ goff) {
   const int64_t NT = (int64_t)N * NQ;
-  const int ntx = (Lx + TR - 1) / TR;
-  const int tx0 = (blockIdx.x % ntx) * TR, ty0 = (blockIdx.x / ntx) * TR;
+  const int ntx = (Lx + TRL - 1) / TRL;
+  const int tx0 = (blockIdx.x % ntx) * TRL, ty0 = (blockIdx.x / ntx) * TRL;
   const int n0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n = n0 + lane;
   const bool valid = n < N;
   const int ns = valid ? n : N - 1;  // clamp loads of idle lanes
-  for (int rr = wid; rr < TR * TR; rr += 8) {
-    const int I = tx0 + rr % TR, J = ty0 + rr / TR;
+  for (int rr = wid; rr < TRL * TRL; rr += 8) {
+    const int I = tx0 + rr % TRL, J = ty0 + rr / TRL;
     if (I >= Lx || J >= Ly) continue;
     const int64_t i = (int64_t)J * Lx + I;
     const int64_t base = i * NT + (int64_t)ns * NQ;
@@ -436,14 +436,25 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
       t.CE[e] = tm.CE[e];
       t.Mt[e] = tm.Mt[e];
     }
-    const int ntx = (L.Lx + TR - 1) / TR, nty = (L.Ly + TR - 1) / TR;
-    dim3 grid(ntx * nty, (N + 31) / 32);
+    // 8x8-row tiles, or 4x4 when that leaves fewer than 4 CTAs per SM (the
+    // coarsest levels are latency-bound: more, shorter CTAs)
+    const int nchunk = (N + 31) / 32;
+    const bool small = (int64_t)((L.Lx + TR - 1) / TR) * ((L.Ly + TR - 1) / TR) * nchunk < 4 * 148;
+    const int tr = small ? 4 : TR;
+    const int ntx = (L.Lx + tr - 1) / tr, nty = (L.Ly + tr - 1) / tr;
+    dim3 grid(ntx * nty, nchunk);
+#define WRMG_RL(NQ)                                                                                             \
+  if (small)                                                                                                   \
+    k_residual_l1<NQ, 4><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff);      \
+  else                                                                                                         \
+    k_residual_l1<NQ, TR><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff);
     switch (q) {
-      case 0: k_residual_l1<1><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
-      case 1: k_residual_l1<2><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
-      case 2: k_residual_l1<3><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
-      default: k_residual_l1<4><<<grid, 256, 0, s>>>(L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply, L.goff); break;
+      case 0: WRMG_RL(1) break;
+      case 1: WRMG_RL(2) break;
+      case 2: WRMG_RL(3) break;
+      default: WRMG_RL(4) break;
     }
+#undef WRMG_RL
     ++g_launches;
     return true;
   }
