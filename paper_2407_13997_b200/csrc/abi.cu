@@ -1124,9 +1124,16 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         L.kS = dalloc<double>((size_t)L.ntypes * L.mp * c->nq * c->nq);
         L.ksig = dalloc<double>((size_t)L.ntypes * L.mp);
         const int C = (c->N + 31) / 32;
-        L.kron_pp = std::max(1, 8 / C);
+        // patches per CTA: 8 warps' worth, or 1 when that leaves fewer than 2 CTAs per SM
+        // (coarse levels are latency-bound)
+        int pp = std::max(1, 8 / C);
         std::vector<int32_t> cp, ct;
-        plan_sweep_ctas(P, L.kron_pp, cp, ct);
+        plan_sweep_ctas(P, pp, cp, ct);
+        if (pp > 1 && (int)ct.size() < 2 * 148) {
+          pp = 1;
+          plan_sweep_ctas(P, pp, cp, ct);
+        }
+        L.kron_pp = pp;
         L.kron_ncta = (int)ct.size();
         L.cta_patch = dupload(cp, s);
         L.cta_type = dupload(ct, s);
