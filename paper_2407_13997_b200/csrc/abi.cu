@@ -4,6 +4,9 @@
 // and sequences launches on the context's stream.
 #include <cmath>
 #include <functional>
+#include <mutex>
+#include <map>
+#include <utility>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -19,7 +22,35 @@
 using namespace wrmg;
 
 namespace wrmg {
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
+
+int num_sms() {
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  if (dev >= 64) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+void smem_optin(const void *kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, int> done;  // (kernel, device) -> largest opt-in so far
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int &have = done[std::make_pair(kernel, dev)];
+  if (bytes > have && cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+    have = bytes;
+}
 bool hessenberg_eigenvalues(std::vector<double> &a, int n, std::vector<double> &wr, std::vector<double> &wi);
 }
 
@@ -596,7 +627,7 @@ void setup_ns(wrmg_ctx *c) {
     C.nsY = dalloc<double>((size_t)c->N * C.mp);
   }
   c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
-  c->red = dalloc<double>(64 + 64 * 148 * 4);
+  c->red = dalloc<double>(64 + 64 * kDotBlocksMax);
   c->proj = dalloc<double>(ns_project_scratch(c->lv.back().Lp, c->nt));
   c->bcg = dupload(plans[nl - 1].g, s);
   for (auto &L : c->lv) {
@@ -854,17 +885,23 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
 // kernel on the context's stream: they never queue behind bulk copies that other
 // streams (e.g. a serving loop's next input) keep on the copy engines.
 double *hmap(wrmg_ctx *c) {
-  if (!c->hmap) CK(cudaHostAlloc((void **)&c->hmap, 2048 * sizeof(double), cudaHostAllocMapped));
+  if (!c->hmap) {
+    const int P = c->comm ? c->comm->nranks : 1;
+    c->hmap_cap = std::max(1024, 64 * P);
+    CK(cudaHostAlloc((void **)&c->hmap, 2 * (size_t)c->hmap_cap * sizeof(double), cudaHostAllocMapped));
+  }
   return c->hmap;
 }
 void small_d2h(wrmg_ctx *c, const double *dev, double *host, int nv) {  // synchronises
   double *hm = hmap(c);
+  if (nv > c->hmap_cap) throw Err{WRMG_E_INVALID, "small_d2h: transfer larger than the mapped buffer"};
   launch_scale(hm, dev, 1.0, nv, c->stream);
   CK(cudaStreamSynchronize(c->stream));
   std::memcpy(host, hm, nv * sizeof(double));
 }
 void small_h2d(wrmg_ctx *c, const double *host, double *dev, int nv) {  // caller synchronises before reuse
-  double *hm = hmap(c) + 1024;
+  double *hm = hmap(c) + c->hmap_cap;
+  if (nv > c->hmap_cap) throw Err{WRMG_E_INVALID, "small_h2d: transfer larger than the mapped buffer"};
   std::memcpy(hm, host, nv * sizeof(double));
   launch_scale(dev, hm, 1.0, nv, c->stream);
 }
@@ -901,6 +938,24 @@ double dot_host(wrmg_ctx *c, const double *a, const double *b, int64_t n) {
   reduce_to_host(c, c->red, 1, &out);
   return out;
 }
+
+// Every exported entry point runs on the context's device and restores the
+// caller's current device on return (wrmg_setup used to leave the
+// calling thread on coeffs.device and later calls used whatever was current).
+struct DevGuard {
+  int prev = -1, dev = -1;
+  explicit DevGuard(int d) : dev(d) {
+    if (dev < 0 || cudaGetDevice(&prev) != cudaSuccess) {
+      dev = -1;
+      return;
+    }
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  explicit DevGuard(const wrmg_ctx *c) : DevGuard(c ? c->co.device : -1) {}
+  ~DevGuard() {
+    if (dev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
 
 }  // namespace
 
@@ -981,6 +1036,7 @@ wrmg_status wrmg_plan_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank,
 wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, double dt,
                        const wrmg_coeffs *coeffs, wrmg_ctx **out) {
   wrmg_ctx *c = nullptr;
+  DevGuard dg_(coeffs ? coeffs->device : -1);
   try {
     if (!out) throw Err{WRMG_E_INVALID, "out is NULL"};
     *out = nullptr;
@@ -1129,7 +1185,7 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         int pp = std::max(1, 8 / C);
         std::vector<int32_t> cp, ct;
         plan_sweep_ctas(P, pp, cp, ct);
-        if (pp > 1 && (int)ct.size() < 2 * 148) {
+        if (pp > 1 && (int)ct.size() < 2 * num_sms()) {
           pp = 1;
           plan_sweep_ctas(P, pp, cp, ct);
         }
@@ -1231,7 +1287,7 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       }
     }
     c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
-    c->red = dalloc<double>(64 + 64 * 148 * 4);
+    c->red = dalloc<double>(64 + 64 * kDotBlocksMax);
     CK(cudaStreamSynchronize(s));
     factor_all(c);
     c->cheb = coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV;
@@ -1293,6 +1349,7 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
 
 wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
   if (!c) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     if (c->ns) {
       factor_all_ns(c, state);
@@ -1308,6 +1365,7 @@ wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
 
 wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
   if (!c || !fhat || !b) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     if (c->ns) {  // R6 (C3): b = drawn values on free rows, 0 on constrained rows, pressure mean-projected
       const Level &L = c->lv.back();
@@ -1326,6 +1384,7 @@ wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
 
 wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
   if (!c || !u0 || !b) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     launch_rhs_initial(c->lv.back(), c->nq, c->nt, c->tm.phi0, u0, b, c->stream);
     check_launch();
@@ -1341,6 +1400,7 @@ wrmg_status wrmg_set_boundary_values(wrmg_ctx *c, const double *g) {
     c->err = "wrmg_set_boundary_values: Navier-Stokes contexts only";
     return WRMG_E_UNSUPPORTED;
   }
+  DevGuard dg_(c);
   try {
     const int64_t n = c->lv.back().nnode * c->nt;
     if (!g) {
@@ -1366,6 +1426,7 @@ wrmg_status wrmg_cheb_lambda(const wrmg_ctx *c, int32_t level, double *lam) {
 wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double *r, int32_t nonlinear) {
   if (!c || !u || !b || !r) return WRMG_E_INVALID;
   if (nonlinear && !c->ns) return WRMG_E_UNSUPPORTED;
+  DevGuard dg_(c);
   try {
     if (nonlinear) {
       ns_nonlinear_residual(c, u, b, r);
@@ -1383,6 +1444,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
 
 wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
   if (!c || !x || !y) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(x));
     prof_residual(c, (int)c->lv.size() - 1, x, nullptr, y, false);  // b = NULL: y = A x
@@ -1395,6 +1457,7 @@ wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
 
 wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps, double omega) {
   if (!c || !u || !b || nsweeps < 0) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     const int l = (int)c->lv.size() - 1;
     for (int s = 0; s < nsweeps; ++s) {
@@ -1417,6 +1480,7 @@ wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps
 
 wrmg_status wrmg_vcycle(wrmg_ctx *c, const double *r, double *z) {
   if (!c || !r || !z) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     vcycle_level(c, (int)c->lv.size() - 1, r, z);
     check_launch();
@@ -1434,6 +1498,7 @@ wrmg_status wrmg_level_size(const wrmg_ctx *c, int32_t level, int64_t *nnode) {
 
 wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *rc) {
   if (!c || !rf || !rc || level < 1 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     launch_restrict(c->lv[level - 1], c->nt, rf, rc, c->stream);
     check_launch();
@@ -1445,6 +1510,7 @@ wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *
 
 wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, double *uf) {
   if (!c || !ec || !uf || level < 1 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     launch_prolong_add(c->lv[level - 1], c->nt, ec, uf, c->stream);
     check_launch();
@@ -1457,6 +1523,7 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, doubl
 wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
                         double atol, int32_t *iters, double *relres) {
   if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     cudaStream_t s = c->stream;
     Level &L = c->lv.back();
@@ -1628,6 +1695,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
 
 wrmg_status wrmg_profile(wrmg_ctx *c, int32_t enable) {
   if (!c) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     CK(cudaStreamSynchronize(c->stream));
     for (auto &r : c->prof_recs) {
@@ -1645,6 +1713,7 @@ wrmg_status wrmg_profile(wrmg_ctx *c, int32_t enable) {
 
 wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
   if (!c || !out) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     CK(cudaStreamSynchronize(c->stream));
     for (auto &r : c->prof_recs) {
@@ -1667,7 +1736,7 @@ wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
   }
 }
 
-int64_t wrmg_launch_count(void) { return g_launches; }
+int64_t wrmg_launch_count(void) { return g_launches.load(); }
 
 wrmg_status wrmg_hessenberg_eig(const double *H, int32_t n, double *wr, double *wi) {
   if (!H || !wr || !wi || n < 1) return WRMG_E_INVALID;
@@ -1700,6 +1769,7 @@ void wrmg_loopback_destroy(void *hub) { loop_hub_destroy(hub); }
 
 wrmg_status wrmg_debug_fetch(wrmg_ctx *c, int32_t level, int32_t which, void *host_dst, int64_t count) {
   if (!c || !host_dst || count < 0 || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     const Level &L = c->lv[level];
     const void *src = nullptr;
@@ -1746,6 +1816,7 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
     c->err = "wrmg_newton: the heat operator is linear";
     return WRMG_E_UNSUPPORTED;
   }
+  DevGuard dg_(c);
   try {
     cudaStream_t s = c->stream;
     Level &L = c->lv.back();
@@ -1798,6 +1869,7 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
 
 wrmg_status wrmg_batched_lu(const wrmg_ctx *c, double *A, int32_t m, int32_t batch, int32_t *piv, int32_t *info) {
   if (!A || !piv || !info || m < 1 || batch < 0) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     cudaStream_t s = c ? c->stream : nullptr;
     launch_batched_lu(A, m, batch, piv, info, s);
@@ -1818,6 +1890,7 @@ wrmg_status wrmg_batched_lu(const wrmg_ctx *c, double *A, int32_t m, int32_t bat
 
 wrmg_status wrmg_fill_uniform(const wrmg_ctx *c, double *out, int64_t count, uint64_t first_id, uint64_t seed) {
   if (!out || count < 0) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     launch_fill_uniform(out, count, first_id, seed, c ? c->stream : nullptr);
     check_launch();
@@ -1829,6 +1902,7 @@ wrmg_status wrmg_fill_uniform(const wrmg_ctx *c, double *out, int64_t count, uin
 
 wrmg_status wrmg_sync(wrmg_ctx *c) {
   if (!c) return WRMG_E_INVALID;
+  DevGuard dg_(c);
   try {
     CK(cudaStreamSynchronize(c->stream));
     check_launch();
@@ -1848,6 +1922,7 @@ const char *wrmg_last_error(const wrmg_ctx *c, int32_t *level, int32_t *patch, i
 
 void wrmg_destroy(wrmg_ctx *c) {
   if (!c) return;
+  DevGuard dg_(c);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->hmap) cudaFreeHost(c->hmap);
   c->hmap = nullptr;

@@ -1,7 +1,9 @@
 // Internal declarations of libwrmg (not part of the C ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -173,7 +175,8 @@ struct wrmg_ctx {
   int restart_alloc = 0;
   std::vector<double *> V, Z;
   double *w = nullptr, *red = nullptr, *red_host = nullptr;
-  double *hmap = nullptr;  // mapped pinned host buffer (2 x 1024 doubles): small Krylov results without the copy engines
+  double *hmap = nullptr;  // mapped pinned host buffer (2 x hmap_cap doubles): small Krylov results without the copy engines
+  int hmap_cap = 0;        // doubles per direction: max(1024, 64 nranks)
   double *gred = nullptr;  // strips: all ranks' reduction results (nranks x 64), for wrmg_fgmres
   double *tmp = nullptr;        // finest-level scratch (residual)
   bool use_kron = true;         // factor_mode AUTO: Kronecker-diagonalised heat patch solves
@@ -212,7 +215,17 @@ struct wrmg_ctx {
 };
 
 namespace wrmg {
-extern int64_t g_launches;  // kernels launched by this library (process-wide)
+extern std::atomic<int64_t> g_launches;  // kernels launched by this library (process-wide)
+// Streaming multiprocessors of the current device (cached per device; 148 on B200).
+int num_sms();
+// Dynamic shared-memory opt-in (cudaFuncAttributeMaxDynamicSharedMemorySize) of a
+// kernel on the current device, set once per (kernel, device) under a lock.
+void smem_optin(const void *kernel, int bytes);
+// Upper bound of the Krylov reduction blocks (multidot_blocks <= kDotBlocksMax).
+constexpr int kDotBlocksMax = 1024;
+// TMA tensor map of a waveform-major level vector: dims (NT, Lx, Ly), box (boxT, RW, RWy)
+// (kernels_residual.cu; cached, thread-safe).  false if TMA cannot describe it.
+bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUtensorMap *out, int RWy = -1);
 // kernel launchers (kernels_*.cu)
 void launch_assemble_spatial(const Level &L, int k, const double *ref_dev, double kappa, cudaStream_t s);
 void launch_patch_blocks(const Level &L, int nq, const Temporal &tm, cudaStream_t s);

@@ -34,7 +34,7 @@ __global__ void k_rhs_initial(int64_t nnode, int nq, int64_t NT, Phi0 phi, const
 }  // namespace
 
 void launch_cheb_update(int64_t n, double c1, double c2, const double *br, double *d, double *u, cudaStream_t s) {
-  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   k_cheb_update<<<grid, 256, 0, s>>>(n, c1, c2, br, d, u);
   ++g_launches;
 }

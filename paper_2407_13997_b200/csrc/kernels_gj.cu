@@ -278,11 +278,7 @@ void launch_gj_inverse_batched(double *A, int m, int batch, int32_t *piv, int32_
   ++g_launches;
   // panel width: the m x nb panel must fit in shared memory
   const int NBP = std::max(1, std::min(GJ_NB, (int)((220 * 1024) / (sizeof(double) * (size_t)m))));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gj_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 221 * 1024);
-    attr = true;
-  }
+  smem_optin((const void *)k_gj_panel, 221 * 1024);
   const int nt = (m + GJ_T - 1) / GJ_T;
   for (int k0 = 0; k0 < m; k0 += NBP) {
     const int nb = std::min(NBP, m - k0);

@@ -604,13 +604,9 @@ void sweep_kron_mma_launch(const Level &L, int N, const double *r, double *u, do
   constexpr int P8 = 8 * ((MP + 7) / 8);
   constexpr int K4 = 4 * ((MP + 3) / 4);
   const size_t smem = (size_t)(P8 * (P8 + 4) + P8 * 4 + 4 * P8 + 8 * 2 * K4 * 36) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep_kron_mma<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
+  smem_optin((const void *)k_sweep_kron_mma<MP>, 220 * 1024);
   const int ngroups = L.kron_ngrp8;
-  const int grid = std::min(ngroups, 148 * 2);
+  const int grid = std::min(ngroups, num_sms() * 2);
   k_sweep_kron_mma<MP><<<grid, 256, smem, s>>>(N, (L.mp + 1) & ~1, ngroups, L.grp_patch8, L.grp_type8, L.pnodes,
                                                L.kV, L.kS, L.ksig, L.wnode, omega, r, u);
   ++g_launches;
@@ -623,11 +619,7 @@ void sweep_kron_launch(const Level &L, int N, const double *r, double *u, double
   constexpr int MPS = (MP + 1) & ~1;
   size_t smem = (size_t)(2 * MP * MPS + MP * NQ * NQ + MP + PP * MP + PP * C * MP) * sizeof(double) +
                 (size_t)PP * MP * sizeof(int);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep_kron<NQ, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void *)k_sweep_kron<NQ, MP>, 200 * 1024);
   k_sweep_kron<NQ, MP><<<L.kron_ncta, 32 * C * PP, smem, s>>>(N, C, PP, L.cta_patch, L.cta_type, L.pnodes, L.kV,
                                                                L.kVT, L.kS, L.ksig, L.wnode, omega, r, u);
   ++g_launches;

@@ -11,7 +11,6 @@
 namespace wrmg {
 namespace {
 
-constexpr int kDotBlocks = 148 * 4;
 constexpr int kMaxV = 32;
 
 struct Ptrs {
@@ -88,7 +87,7 @@ __global__ void k_scale(double *__restrict__ dst, const double *__restrict__ src
     dst[i] = a * src[i];
 }
 
-int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 8); }
+int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8); }
 
 template <int MODE>
 void krylov_launch(const double *const *V, int nv, double *w, const double *coef, int64_t n, double *partials,
@@ -105,7 +104,7 @@ void krylov_launch(const double *const *V, int nv, double *w, const double *coef
 
 }  // namespace
 
-int multidot_blocks(int64_t n) { return (int)std::min<int64_t>(kDotBlocks, (n + 255) / 256); }
+int multidot_blocks(int64_t n) { return (int)std::min<int64_t>(std::min(4 * num_sms(), kDotBlocksMax), (n + 255) / 256); }
 
 void launch_multidot(const double *const *V, int nv, const double *w, int64_t n, double *partials, int nblk,
                      cudaStream_t s) {

@@ -1578,7 +1578,7 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
   }
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
-    cudaFuncSetAttribute(k_ns_factor<NQ, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    smem_optin((const void *)k_ns_factor<NQ, 256>, (int)sm);
     k_ns_factor<NQ, 256><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
                                           conv, tm, out, info, ppos, pvv);
   });
@@ -1603,7 +1603,7 @@ void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, cons
     const size_t smc = fixed + (size_t)R * CW * m * sizeof(double);
     by_nq(q + 1, [&](auto NQc) {
       constexpr int NQ = decltype(NQc)::value;
-      cudaFuncSetAttribute(k_ns_sweep_chunked<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+      smem_optin((const void *)k_ns_sweep_chunked<NQ>, (int)smc);
       k_ns_sweep_chunked<NQ><<<(unsigned)npatch, 256, smc, s>>>(mp, N, mstride, CW, R, pnodes, wnode, A.rowptr,
                                                                 A.col, A.val, Dinv, r, u, omega);
     });
@@ -1613,11 +1613,11 @@ void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, cons
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
     if (staged) {
-      cudaFuncSetAttribute(k_ns_sweep<NQ, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      smem_optin((const void *)k_ns_sweep<NQ, true>, (int)sm);
       k_ns_sweep<NQ, true><<<(unsigned)npatch, 256, sm, s>>>(mp, N, mstride, pnodes, wnode, A.rowptr, A.col, A.val,
                                                              Dinv, r, u, omega);
     } else {
-      cudaFuncSetAttribute(k_ns_sweep<NQ, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      smem_optin((const void *)k_ns_sweep<NQ, false>, (int)sm);
       k_ns_sweep<NQ, false><<<(unsigned)npatch, 256, sm, s>>>(mp, N, mstride, pnodes, wnode, A.rowptr, A.col, A.val,
                                                               Dinv, r, u, omega);
     }
@@ -1676,11 +1676,7 @@ void launch_ns_coarse_solve_pint(int q, int N, int mc, int pin, const int32_t *c
     constexpr int NQ = decltype(NQc)::value;
     k_ns_coarse_pass<NQ, false><<<grid, 256, m * sizeof(double), s>>>(mc, N, pin, cnodes, DinvT, r, Zs, nullptr,
                                                                       nullptr, nullptr);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_ns_coarse_yrec<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
+    smem_optin((const void *)k_ns_coarse_yrec<NQ>, 200 * 1024);
     k_ns_coarse_yrec<NQ><<<1, 1024, 10 * mc * sizeof(double), s>>>(mc, N, Zs, G, Ys);
     k_ns_coarse_pass<NQ, true><<<grid, 256, mc * sizeof(double), s>>>(mc, N, pin, cnodes, DinvT, r, Zs, H, Ys, z);
   });
@@ -1696,7 +1692,7 @@ void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
     if (sm <= 200 * 1024 && m <= 512) {
-      cudaFuncSetAttribute(k_ns_coarse_cluster<NQ, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      smem_optin((const void *)k_ns_coarse_cluster<NQ, 8>, (int)sm);
       k_ns_coarse_cluster<NQ, 8><<<8, 256, sm, s>>>(mc, N, pin, ns, cnodes, A.rowptr, A.col, A.val, DinvT, r, z,
                                                      nnzj);
     } else {

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <tuple>
 
 #include "internal.h"
@@ -356,23 +357,28 @@ __global__ void __launch_bounds__(256) k_residual_l1(int Lx, int Ly, int N, cons
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
-  }
+  });
   return fn;
 }
 
-// Tensor map of a waveform-major vector: dims (NT, Lx, Ly), box (32 NQ, RW, RW).
-bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUtensorMap *out, int RWy = -1) {
+}  // namespace
+
+// Tensor map of a waveform-major vector: dims (NT, Lx, Ly), box (boxT, RW, RWy).
+// Encoded maps are cached per (pointer, shape, box) under a lock: strips run
+// several contexts as host threads of one process (loopback transport).
+bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUtensorMap *out, int RWy) {
   if (RWy < 0) RWy = RW;
+  static std::mutex mu;
   static std::map<std::tuple<const double *, int64_t, int, int, int, int, int>, CUtensorMap> cache;
   auto key = std::make_tuple(u, NT, Lx, Ly, boxT, RW, RWy);
+  std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
     *out = it->second;
@@ -394,6 +400,8 @@ bool umap_for(const double *u, int64_t NT, int Lx, int Ly, int boxT, int RW, CUt
   *out = m;
   return true;
 }
+
+namespace {
 
 // Fill the class tables from the assembled CSR of each class's representative row.
 __global__ void k_gather_classes(int ncls, const int32_t *__restrict__ rep, int Lx, const int32_t *__restrict__ rowptr,
@@ -439,7 +447,7 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
     // 8x8-row tiles, or 4x4 when that leaves fewer than 4 CTAs per SM (the
     // coarsest levels are latency-bound: more, shorter CTAs)
     const int nchunk = (N + 31) / 32;
-    const bool small = (int64_t)((L.Lx + TR - 1) / TR) * ((L.Ly + TR - 1) / TR) * nchunk < 4 * 148;
+    const bool small = (int64_t)((L.Lx + TR - 1) / TR) * ((L.Ly + TR - 1) / TR) * nchunk < 4 * num_sms();
     const int tr = small ? 4 : TR;
     const int ntx = (L.Lx + tr - 1) / tr, nty = (L.Ly + tr - 1) / tr;
     dim3 grid(ntx * nty, nchunk);
@@ -473,11 +481,7 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
   if (RW <= 256 && 32 * (q + 1) <= 256 && umap_for(u, (int64_t)N * (q + 1), L.Lx, L.Ly, 32 * (q + 1), RW, &umap)) {
 #define WRMG_RT(NQ)                                                                                          \
     {                                                                                                        \
-      static bool attr = false;                                                                              \
-      if (!attr) {                                                                                           \
-        cudaFuncSetAttribute(k_residual_tma<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);   \
-        attr = true;                                                                                         \
-      }                                                                                                      \
+      smem_optin((const void *)k_residual_tma<NQ>, 200 * 1024);                                                                                                      \
       k_residual_tma<NQ><<<ntx * nty, 256, smem + tab, s>>>(umap, k, L.Lx, L.Ly, N, L.rcls, b, r, t,          \
                                                             L.stencil,                                       \
                                                       apply);                                                \
@@ -494,11 +498,7 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
   }
 #define WRMG_RC(NQ)                                                                                          \
   {                                                                                                          \
-    static bool attr = false;                                                                                \
-    if (!attr) {                                                                                             \
-      cudaFuncSetAttribute(k_residual_cls<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);     \
-      attr = true;                                                                                           \
-    }                                                                                                        \
+    smem_optin((const void *)k_residual_cls<NQ>, 200 * 1024);                                                                                                        \
     k_residual_cls<NQ><<<ntx * nty, 256, smem, s>>>(k, L.Lx, L.Ly, N, L.rcls, u, b, r, t, L.stencil, apply);        \
     ++g_launches;                                                                                            \
     return true;                                                                                             \

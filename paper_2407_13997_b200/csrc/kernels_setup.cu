@@ -290,11 +290,7 @@ void launch_batched_lu(double *A, int m, int batch, int32_t *piv, int32_t *info,
   if (batch <= 0) return;
   size_t bytes = (size_t)m * m * sizeof(double);
   if (bytes <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_batched_lu<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-      attr = true;
-    }
+    smem_optin((const void *)k_batched_lu<true>, 210 * 1024);
     k_batched_lu<true><<<batch, 256, bytes, s>>>(A, m, piv, info); ++g_launches;
   } else {
     k_batched_lu<false><<<batch, 256, 0, s>>>(A, m, piv, info); ++g_launches;

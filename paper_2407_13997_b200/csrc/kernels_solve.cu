@@ -223,11 +223,7 @@ template <int NQ, int MP>
 void sweep_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
   constexpr int M = NQ * MP;
   size_t smem = (size_t)SW_WARPS * (M * 33 + 33 * MP + MP) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sweep<NQ, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void *)k_sweep<NQ, MP>, (int)smem);
   int blocks = (int)((L.npatch + SW_WARPS - 1) / SW_WARPS);
   k_sweep<NQ, MP><<<blocks, 32 * SW_WARPS, smem, s>>>(L.npatch, N, L.pnodes, L.ptype, L.Dinv, L.G, L.wnode, omega,
                                                       r, u); ++g_launches;
@@ -424,11 +420,7 @@ void launch_residual(const Level &L, int q, int N, const Temporal &tm, const dou
   TMc t = make_tmc(tm);
 #define WRMG_RES(NQ)                                                                                            \
   {                                                                                                             \
-    static bool attr = false;                                                                                   \
-    if (!attr) {                                                                                                \
-      cudaFuncSetAttribute(k_residual<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);            \
-      attr = true;                                                                                              \
-    }                                                                                                           \
+    smem_optin((const void *)k_residual<NQ>, 200 * 1024);                                                                                                           \
     k_residual<NQ><<<grid, 256, smem, s>>>(k, L.Lx, L.Ly, N, L.A.rowptr, L.A.col, L.A.val, L.A.val2, L.con, u, b, \
                                            r, t); ++g_launches;                                                               \
   }
@@ -467,11 +459,7 @@ void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const do
   size_t gq = (size_t)C.mp * C.mp * sizeof(double);
   int in_smem = (gq + 2 * C.mp * sizeof(double)) <= 200 * 1024;
   size_t smem = 2 * C.mp * sizeof(double) + (in_smem ? gq : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_coarse_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    attr = true;
-  }
+  smem_optin((const void *)k_coarse_rec, 210 * 1024);
   k_coarse_rec<<<1, 1024, smem, s>>>(N, C.m, C.mp, nq, C.Z, C.Gq, C.Y, in_smem); ++g_launches;
   k_coarse_x<<<N, 256, 0, s>>>(C.m, C.mp, nq, NT, C.nodes, C.Z, C.GT, C.Y, x); ++g_launches;
 }

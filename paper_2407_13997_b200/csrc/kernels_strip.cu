@@ -37,7 +37,7 @@ __global__ void k_window(const double *__restrict__ src, int Lxs, int sc0, doubl
   }
 }
 
-unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16); }
 
 }  // namespace
 
