@@ -2,7 +2,10 @@
 // V-cycle (H12) and FGMRES (H13) orchestration.  Every numerical step runs in
 // the kernels of kernels_*.cu; this file only allocates, uploads integer plans
 // and sequences launches on the context's stream.
+#include <algorithm>
+#include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <mutex>
 #include <map>
@@ -18,6 +21,7 @@
 #include "ns_kernels.h"
 #include "plan.h"
 #include "strip.h"
+#include "sym.h"
 
 using namespace wrmg;
 
@@ -185,7 +189,12 @@ void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
     ns_project(c, L, u);
     return;
   }
-  if (c->use_kron && launch_sweep_kron(c->lv[l], c->q, c->N, r, u, om, c->stream)) return;
+  if (c->use_kron) {
+    const Level &L = c->lv[l];
+    const bool sym = launch_sweep_sym(L, c->k, c->q, c->N, r, u, om, c->stream);
+    if (sym && L.kron_ngrp8 == 0 && L.kron_ncta == 0) return;  // every patch is in the symmetric class
+    if (launch_sweep_kron(L, c->q, c->N, r, u, om, c->stream)) return;
+  }
   launch_sweep(c->lv[l], c->q, c->N, r, u, om, c->stream);
 }
 
@@ -199,7 +208,7 @@ void free_level(Level &L) {
                   (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8, (void *)L.vvptr, (void *)L.conv,
                   (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo, (void *)L.ppos, (void *)L.pvv, (void *)L.hx[0],
                   (void *)L.hx[1],
-                  (void *)L.hx[2], (void *)L.hx[3]})
+                  (void *)L.hx[2], (void *)L.hx[3], (void *)L.gen_rows, (void *)L.sym_nodes})
     dfree(p);
 }
 
@@ -254,6 +263,18 @@ void gather_stencil(wrmg_ctx *c, Level &L) {
   if (!L.goff) L.goff = dalloc<int64_t>(go.size());
   CK(cudaMemcpy(L.goff, go.data(), go.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   L.stencil_ok = true;
+  // macro-block residual: interior classes per row type, fix-up list of the other rows
+  std::vector<int32_t> vc(cnt, cnt + nc), vI(dI, dI + nc * kStencilMaxE), vJ(dJ, dJ + nc * kStencilMaxE), gen;
+  std::vector<double> vm(hd.begin(), hd.begin() + nc * kStencilMaxE), vk(hd.begin() + nc * kStencilMaxE, hd.end());
+  L.mac_ok = plan_residual_mac(L, c->k, vc, vI, vJ, vm, vk, gen);
+  dfree(L.gen_rows);
+  L.gen_rows = nullptr;
+  L.ngen_rows = 0;
+  if (L.mac_ok && !gen.empty()) {
+    L.gen_rows = dalloc<int32_t>(gen.size());
+    CK(cudaMemcpy(L.gen_rows, gen.data(), gen.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    L.ngen_rows = (int64_t)gen.size();
+  }
 }
 
 
@@ -334,6 +355,34 @@ void coarse_strip(wrmg_ctx *c, const double *r, double *z) {
   launch_window(c->gz, G.Lx, S.G0, z, L0.Lx, 0, L0.Ly, L0.Lx, c->nt, s);
 }
 
+bool sym_disabled() {  // WRMG_SWEEP_SYM=0: every class through kernels_kron.cu (A/B)
+  const char *e = getenv("WRMG_SWEEP_SYM");
+  return e && e[0] == '0';
+}
+
+// Symmetry-reduced sweep coefficients of the interior class from the assembled M, kappa K.
+void sym_setup(wrmg_ctx *c, Level &L) {
+  const int mps = (int)std::lround(std::sqrt((double)L.sym_pos.size()));
+  int64_t lo = INT64_MAX, hi = -1;
+  for (int64_t e : L.sym_pos)
+    if (e >= 0) {
+      lo = std::min(lo, e);
+      hi = std::max(hi, e);
+    }
+  if (hi < 0) throw Err{WRMG_E_INVALID, "symmetric patch block has no entries"};
+  std::vector<double> mv(hi - lo + 1), kv(hi - lo + 1);
+  CK(cudaMemcpy(mv.data(), L.A.val + lo, mv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(kv.data(), L.A.val2 + lo, kv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> Mp((size_t)mps * mps, 0.0), Kp((size_t)mps * mps, 0.0);
+  for (size_t e = 0; e < L.sym_pos.size(); ++e)
+    if (L.sym_pos[e] >= 0) {
+      Mp[e] = mv[L.sym_pos[e] - lo];
+      Kp[e] = kv[L.sym_pos[e] - lo];
+    }
+  if (!sym_factor(c->k, Mp.data(), Kp.data(), c->tm, &L.symtab))
+    throw Err{WRMG_E_SINGULAR, "symmetry-reduced patch factorisation failed"};
+}
+
 // Numeric part of setup / linearisation: H1, H4, H5 on every level + coarse block.
 void factor_all(wrmg_ctx *c) {
   cudaStream_t s = c->stream;
@@ -358,8 +407,10 @@ void factor_all(wrmg_ctx *c) {
       CK(cudaStreamSynchronize(s));
       dfree(scr);
     }
+    if (L.sym_ok) sym_setup(c, L);
     gather_stencil(c, L);
   }
+  if (c->sub) return;  // the replicated hierarchy factored its own levels and coarse solve
   Coarse &C = c->coarse;
   Level &L0 = c->strip ? c->gco : c->lv[0];  // strips: the replicated global coarsest level
   if (c->strip) {
@@ -767,10 +818,33 @@ void cheb_smooth(wrmg_ctx *c, int l, const double *b, double *u, bool u_zero, in
 
 // V(nu_pre, nu_post) on a strip: r is valid on owned columns
 // (ghosts refreshed here), z leaves valid on owned and ghost columns.
+void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z);
+
+// Below the coarsest partitioned level: the restriction of the owned fine rows into
+// the replicated level (partial sums), all-reduced in rank order; the replicated
+// V-cycle (c->sub, identical on every rank); prolongation to the owned fine rows.
+void sub_cycle(wrmg_ctx *c, const double *t, double *z) {
+  cudaStream_t s = c->stream;
+  wrmg_ctx *S = c->sub;
+  const Level &T = S->lv.back();
+  const int64_t ng = T.nnode * c->nt;
+  {
+    PScope ps(c, WRMG_K_RESTRICT, 0, 8.0 * (c->lv[0].nnode + T.nnode) * c->nt, 2.0 * c->xfer.R.nnz * c->nt);
+    launch_restrict(c->xfer, c->nt, t, c->sub_part, s);
+  }
+  comm_call(c, [&] { c->comm->allgather(c->sub_part, c->sub_all, (size_t)ng, s); });
+  launch_sum_chunks(c->sub_all, c->comm->nranks, ng, c->sub_r, s);
+  vcycle_level(S, (int)S->lv.size() - 1, c->sub_r, c->sub_z);
+  {
+    PScope ps(c, WRMG_K_PROLONG, 0, 8.0 * (2 * c->lv[0].nnode + T.nnode) * c->nt, 2.0 * c->xfer.P.nnz * c->nt);
+    launch_prolong_add(c->xfer, c->nt, c->sub_z, z, s);
+  }
+}
+
 void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
   cudaStream_t s = c->stream;
   Level &L = c->lv[l];
-  if (l == 0) {
+  if (l == 0 && !c->sub) {
     coarse_strip(c, r, z);
     return;
   }
@@ -789,16 +863,20 @@ void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
     }
   }
   prof_residual(c, l, z, r, t, c->co.nu_pre == 0);
-  Level &C = c->lv[l - 1];
-  {
-    PScope ps(c, WRMG_K_RESTRICT, l, 8.0 * (L.nnode + C.nnode) * c->nt, 2.0 * C.R.nnz * c->nt);
-    launch_restrict(C, c->nt, t, C.vr, s);  // R = P^T over owned fine rows
-  }
-  halo_reverse_add(c, C, C.vr);
-  vcycle_strip(c, l - 1, C.vr, C.vz);
-  {
-    PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
-    launch_prolong_add(C, c->nt, C.vz, z, s);  // owned fine rows
+  if (l == 0) {
+    sub_cycle(c, t, z);
+  } else {
+    Level &C = c->lv[l - 1];
+    {
+      PScope ps(c, WRMG_K_RESTRICT, l, 8.0 * (L.nnode + C.nnode) * c->nt, 2.0 * C.R.nnz * c->nt);
+      launch_restrict(C, c->nt, t, C.vr, s);  // R = P^T over owned fine rows
+    }
+    halo_reverse_add(c, C, C.vr);
+    vcycle_strip(c, l - 1, C.vr, C.vz);
+    {
+      PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
+      launch_prolong_add(C, c->nt, C.vz, z, s);  // owned fine rows
+    }
   }
   halo_forward(c, L, z);
   for (int it = 0; it < c->co.nu_post; ++it) {
@@ -1049,8 +1127,6 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV &&
         (coeffs->nranks > 1 || coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
       throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: single rank, cheb_steps <= 63"};
-    if (coeffs->bc == WRMG_BC_NEUMANN && coeffs->nranks > 1)
-      throw Err{WRMG_E_UNSUPPORTED, "Neumann boundaries on strips are not built"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
     if (coeffs->nranks > 1 && coeffs->problem != WRMG_HEAT)
       throw Err{WRMG_E_UNSUPPORTED, "strip partitions are built for the heat operator only"};
@@ -1095,10 +1171,40 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     }
     std::vector<int> nys;
     std::vector<int> nxs = level_sizes(mesh->gnx, mesh->gny, c->mesh.ncoarse, &nys);
+    c->strip = coeffs->nranks > 1;
+    const bool neumann = coeffs->bc == WRMG_BC_NEUMANN;
+    // strips: levels whose strip is narrower than 2 cells are agglomerated -- they run
+    // replicated on every rank as a complete single-rank hierarchy (c->sub) below the
+    // coarsest partitioned level
+    int lrep = 0;
+    if (c->strip)
+      for (int l = 0; l < (int)nxs.size(); ++l) {
+        const int f = mesh->gnx / nxs[l];
+        if (c->mesh.nx % f || c->mesh.nx / f < 2) lrep = l + 1;
+      }
+    if (lrep >= (int)nxs.size())
+      throw Err{WRMG_E_UNSUPPORTED, "strips: the finest level's strip is narrower than 2 cells"};
+    if (lrep > 0) {
+      wrmg_mesh sm{};
+      sm.gnx = nxs[lrep - 1];
+      sm.gny = nys[lrep - 1];
+      sm.x0 = 0;
+      sm.nx = sm.gnx;
+      sm.h = mesh->h * (double)(mesh->gnx / nxs[lrep - 1]);
+      sm.ncoarse = c->mesh.ncoarse;
+      wrmg_coeffs sc = *coeffs;
+      sc.rank = 0;
+      sc.nranks = 1;
+      sc.loopback_hub = nullptr;
+      sc.nccl_unique_id = nullptr;
+      const wrmg_status st = wrmg_setup(&sm, degree, q, nslabs, dt, &sc, &c->sub);
+      if (st != WRMG_OK) throw Err{st, std::string("replicated coarse hierarchy: ") + wrmg_last_error(nullptr, 0, 0, 0)};
+      nxs.erase(nxs.begin(), nxs.begin() + lrep);
+      nys.erase(nys.begin(), nys.begin() + lrep);
+    }
     const int nl = (int)nxs.size();
     std::vector<PlanLevel> plans(nl);
     c->lv.resize(nl);
-    c->strip = coeffs->nranks > 1;
     if (c->strip) {  // uniform strips x0 = rank * nx
       const int P = coeffs->nranks, r = coeffs->rank;
       if (r < 0 || r >= P || c->mesh.nx * P != mesh->gnx || c->mesh.x0 != r * c->mesh.nx)
@@ -1115,12 +1221,10 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       Level &L = c->lv[l];
       if (c->strip) {
         const int f = mesh->gnx / nxs[l];
-        if (c->mesh.nx % f || c->mesh.nx / f < 2)
-          throw Err{WRMG_E_UNSUPPORTED, "strips: a level's strip is narrower than 2 cells (raise ncoarse or nx)"};
         plan_strip_level(nxs[l], nys[l], c->mesh.x0 / f, c->mesh.nx / f, h, degree, coeffs->rank, coeffs->nranks,
-                         &plans[l], &L.st);
+                         &plans[l], &L.st, neumann);
       } else {
-        plan_level(nxs[l], nys[l], h, degree, &plans[l], coeffs->bc == WRMG_BC_NEUMANN);
+        plan_level(nxs[l], nys[l], h, degree, &plans[l], neumann);
         L.st = StripInfo{};
         L.st.gnx = nxs[l];
         L.st.nx = nxs[l];
@@ -1160,11 +1264,6 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       for (int64_t i = 0; i < P.nnode; ++i)
         if (P.mu[i] > 0) w[i] = (c->co.weights == WRMG_W_NONE) ? 1.0 : 1.0 / P.mu[i];
       L.wnode = dupload(w, s);
-      {
-        double fl = 0.0;  // 2 m^2 + 2 m_p^2 per (patch, slab): LU solve + jump
-        for (int32_t ps : P.psize) fl += 2.0 * ((double)c->nq * ps) * ((double)c->nq * ps) + 2.0 * (double)ps * ps;
-        c->sweep_flops.push_back(fl * c->N);
-      }
       int m = c->nq * L.mp;
       L.Dblk = dalloc<double>((size_t)L.ntypes * m * m);
       L.Dinv = dalloc<double>((size_t)L.ntypes * m * m);
@@ -1172,7 +1271,39 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       L.piv = dalloc<int32_t>((size_t)L.ntypes * m);
       L.info = dalloc<int32_t>(L.ntypes);
       L.rcls = dupload(P.rcls, s);
+      L.h_rcls = P.rcls;
       L.h_cls_rep = P.cls_rep;
+      if (c->use_kron && c->nq <= (degree == 3 ? 3 : 4) && degree >= 2 && P.npatch >= 1000 && !sym_disabled()) {
+        // symmetry-reduced sweep for the interior vertex-star class (host_sym.cu): the most frequent class
+        std::vector<int64_t> cnt(P.ntypes, 0);
+        for (int64_t p = 0; p < P.npatch; ++p) ++cnt[P.ptype[p]];
+        const int cls = (int)(std::max_element(cnt.begin(), cnt.end()) - cnt.begin());
+        std::vector<int32_t> perm;
+        int counts[3];
+        if (plan_sym_class(P, degree, cls, perm, counts)) {
+          std::vector<int32_t> sn;
+          sn.reserve((size_t)cnt[cls] * perm.size());
+          for (int64_t p = 0; p < P.npatch; ++p)
+            if (P.ptype[p] == cls)
+              for (int32_t sl : perm) sn.push_back(P.pnodes[p * P.mp + sl]);
+          L.sym_ok = true;
+          L.sym_cls = cls;
+          L.nsym = cnt[cls];
+          L.sym_nodes = dupload(sn, s);
+          // CSR positions of the representative patch block (values read at factor time)
+          const int64_t rep = P.type_rep[cls];
+          const int mps = (int)perm.size();
+          L.sym_pos.assign((size_t)mps * mps, -1);
+          for (int a2 = 0; a2 < mps; ++a2) {
+            const int32_t i = P.pnodes[rep * P.mp + perm[a2]];
+            for (int b2 = 0; b2 < mps; ++b2) {
+              const int32_t j = P.pnodes[rep * P.mp + perm[b2]];
+              for (int32_t e = P.rowptr[i]; e < P.rowptr[i + 1]; ++e)
+                if (P.col[e] == j) L.sym_pos[(size_t)a2 * mps + b2] = e;
+            }
+          }
+        }
+      }
       if (c->use_kron) {
         const int ld = (L.mp + 1) & ~1;
         L.kV = dalloc<double>((size_t)L.ntypes * L.mp * ld);
@@ -1183,24 +1314,43 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         // patches per CTA: 8 warps' worth, or 1 when that leaves fewer than 2 CTAs per SM
         // (coarse levels are latency-bound)
         int pp = std::max(1, 8 / C);
+        const int ex = L.sym_ok ? L.sym_cls : -1;  // the symmetric class runs in kernels_sweep_sym.cu
         std::vector<int32_t> cp, ct;
-        plan_sweep_ctas(P, pp, cp, ct);
+        plan_sweep_ctas(P, pp, cp, ct, ex);
         if (pp > 1 && (int)ct.size() < 2 * num_sms()) {
           pp = 1;
-          plan_sweep_ctas(P, pp, cp, ct);
+          plan_sweep_ctas(P, pp, cp, ct, ex);
         }
         L.kron_pp = pp;
         L.kron_ncta = (int)ct.size();
         L.cta_patch = dupload(cp, s);
         L.cta_type = dupload(ct, s);
-        plan_sweep_ctas(P, 1, cp, ct);
+        plan_sweep_ctas(P, 1, cp, ct, ex);
         L.kron_ncta1 = (int)ct.size();
         L.cta_patch1 = dupload(cp, s);
         L.cta_type1 = dupload(ct, s);
-        plan_sweep_ctas(P, 8, cp, ct);
+        plan_sweep_ctas(P, 8, cp, ct, ex);
         L.kron_ngrp8 = (int)ct.size();
         L.grp_patch8 = dupload(cp, s);
         L.grp_type8 = dupload(ct, s);
+      }
+      {
+        // algorithmic flops of one sweep, per (patch, slab), of the solve the path runs:
+        //   LU mode: 2 m^2 + 2 m_p^2 (LU solve + jump);
+        //   Kronecker: 2 (2 (q+1) m_p^2 + m_p (q+1)^2) (two transforms + per-mode DG(q) solves);
+        //   symmetric class: 2 (2 (q+1) sum_chi d_chi^2 + m_p (q+1)^2) (host_sym.cu blocks)
+        const double nq = c->nq, s2 = degree == 3 ? 99.0 : 15.0;
+        double fl = 0.0;
+        for (int64_t p = 0; p < P.npatch; ++p) {
+          const double ps = P.psize[p];
+          if (!c->use_kron)
+            fl += 2.0 * (nq * ps) * (nq * ps) + 2.0 * ps * ps;
+          else if (L.sym_ok && P.ptype[p] == L.sym_cls)
+            fl += 2.0 * (2.0 * nq * s2 + ps * nq * nq);
+          else
+            fl += 2.0 * (2.0 * nq * ps * ps + ps * nq * nq);
+        }
+        c->sweep_flops.push_back(fl * c->N);
       }
       if (l < nl - 1) {
         L.vr = dalloc<double>(L.nnode * c->nt);
@@ -1215,7 +1365,8 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       std::vector<int32_t> rp, ci, trp, tci;
       std::vector<double> v, tv;
       if (c->strip)
-        plan_strip_interpolation(plans[l - 1], c->lv[l - 1].st, plans[l], c->lv[l].st, degree, nys[l], rp, ci, v);
+        plan_strip_interpolation(plans[l - 1], c->lv[l - 1].st, plans[l], c->lv[l].st, degree, nys[l], rp, ci, v,
+                                 neumann);
       else
         plan_interpolation(plans[l - 1], plans[l], degree, rp, ci, v);
       transpose_csr(plans[l].nnode, plans[l - 1].nnode, rp, ci, v, trp, tci, tv);
@@ -1232,10 +1383,40 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       C.R.val = dupload(tv, s);
       CK(cudaStreamSynchronize(s));
     }
+    if (c->sub) {  // hand-over between the coarsest partitioned level and the replicated hierarchy
+      const Level &T = c->sub->lv.back();
+      PlanLevel gc;
+      plan_level(T.nx, T.ny, T.h, degree, &gc, neumann);
+      StripInfo whole{};
+      whole.gnx = T.nx;
+      whole.nx = T.nx;
+      whole.nxl = T.nx;
+      std::vector<int32_t> rp, ci, trp, tci;
+      std::vector<double> v, tv;
+      plan_strip_interpolation(gc, whole, plans[0], c->lv[0].st, degree, nys[0], rp, ci, v, neumann);
+      transpose_csr(plans[0].nnode, gc.nnode, rp, ci, v, trp, tci, tv);
+      Level &X = c->xfer;
+      X.P.nrow = plans[0].nnode;
+      X.P.nnz = (int64_t)ci.size();
+      X.P.rowptr = dupload(rp, s);
+      X.P.col = dupload(ci, s);
+      X.P.val = dupload(v, s);
+      X.R.nrow = gc.nnode;
+      X.R.nnz = (int64_t)tci.size();
+      X.R.rowptr = dupload(trp, s);
+      X.R.col = dupload(tci, s);
+      X.R.val = dupload(tv, s);
+      const int64_t ng = gc.nnode * c->nt;
+      c->sub_r = dalloc<double>(ng);
+      c->sub_z = dalloc<double>(ng);
+      c->sub_part = dalloc<double>(ng);
+      c->sub_all = dalloc<double>(ng * coeffs->nranks);
+      CK(cudaStreamSynchronize(s));
+    }
     PlanLevel gplan;  // strips: the global coarsest level, replicated on every rank
-    if (c->strip) {
+    if (c->strip && !c->sub) {
       const double h0 = mesh->h * (double)(mesh->gnx / nxs[0]);
-      plan_level(nxs[0], nys[0], h0, degree, &gplan);
+      plan_level(nxs[0], nys[0], h0, degree, &gplan, neumann);
       Level &G = c->gco;
       G.nx = gplan.nx;
       G.ny = gplan.ny;
@@ -1260,7 +1441,7 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       CK(cudaMemsetAsync(c->gr, 0, G.nnode * c->nt * sizeof(double), s));
       CK(cudaStreamSynchronize(s));
     }
-    {
+    if (!c->sub) {
       const PlanLevel &CP = c->strip ? gplan : plans[0];
       Coarse &C = c->coarse;
       std::vector<int32_t> nodes;
@@ -1339,9 +1520,18 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
   out->own1 = L.st.own1;
   out->g0 = L.st.G0;
   out->nfree_owned_st = L.nfree_owned * c->nt;
-  if (c->strip) {
+  if (c->strip) {  // owned rows; the replicated levels (c->sub) are counted once, on rank 0
     upd = 0;
-    for (size_t l = 1; l < c->lv.size(); ++l) upd += c->lv[l].nfree_owned * c->nt * (c->co.nu_pre + c->co.nu_post);
+    for (size_t l = c->sub ? 0 : 1; l < c->lv.size(); ++l)
+      upd += c->lv[l].nfree_owned * c->nt * (c->co.nu_pre + c->co.nu_post);
+    if (c->sub) {
+      out->nlevels += (int)c->sub->lv.size();
+      if (c->co.rank == 0) {
+        wrmg_layout_t sl;
+        wrmg_layout(c->sub, &sl);
+        upd += sl.smooth_dof_updates_per_vcycle;
+      }
+    }
     out->smooth_dof_updates_per_vcycle = upd;
   }
   return WRMG_OK;
@@ -1928,6 +2118,9 @@ void wrmg_destroy(wrmg_ctx *c) {
   c->hmap = nullptr;
   for (auto &L : c->lv) free_level(L);
   free_level(c->gco);
+  free_level(c->xfer);
+  for (void *p : {(void *)c->sub_r, (void *)c->sub_z, (void *)c->sub_part, (void *)c->sub_all}) dfree(p);
+  if (c->sub) wrmg_destroy(c->sub);
   for (double *p : c->cd) dfree(p);
   for (double *p : c->cbr) dfree(p);
   for (void *p : {(void *)c->gr, (void *)c->gz, (void *)c->gsend, (void *)c->grecv}) dfree(p);

@@ -144,12 +144,14 @@ void plan_level(int nx, int ny, double h, int k, PlanLevel *P, bool neumann) {
     }
 }
 
-void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type) {
+void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type,
+                     int exclude) {
   cta_patch.clear();
   cta_type.clear();
   std::vector<std::vector<int32_t>> by(P.ntypes);
   for (int64_t p = 0; p < P.npatch; ++p) by[P.ptype[p]].push_back((int32_t)p);
   for (int t = 0; t < P.ntypes; ++t)
+    if (t != exclude)
     for (size_t s = 0; s < by[t].size(); s += pp) {
       cta_type.push_back(t);
       for (int j = 0; j < pp; ++j) cta_patch.push_back(s + j < by[t].size() ? by[t][s + j] : -1);

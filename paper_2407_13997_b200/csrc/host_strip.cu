@@ -9,7 +9,7 @@
 namespace wrmg {
 
 void plan_strip_level(int gnx, int gny, int x0, int nx, double h, int k, int rank, int nranks, PlanLevel *P,
-                      StripInfo *S) {
+                      StripInfo *S, bool neumann) {
   StripInfo &s = *S;
   s = StripInfo{};
   s.rank = rank;
@@ -35,7 +35,7 @@ void plan_strip_level(int gnx, int gny, int x0, int nx, double h, int k, int ran
     s.nsr = k;
     s.sr0 = k * (x0 + nx) - k + 1 - s.G0;
   }
-  plan_level(s.nxl, gny, h, k, P);
+  plan_level(s.nxl, gny, h, k, P, neumann);
   // keep the patches of owned vertices only; renumber the translation classes
   const int vlo = (rank == 0 ? 0 : x0 + 1) - s.cx0, vhi = x0 + nx - s.cx0;
   const int nvx = s.nxl + 1;
@@ -71,7 +71,7 @@ void plan_strip_level(int gnx, int gny, int x0, int nx, double h, int k, int ran
 
 void plan_strip_interpolation(const PlanLevel &C, const StripInfo &Sc, const PlanLevel &F, const StripInfo &Sf, int k,
                               int gny_f, std::vector<int32_t> &rowptr, std::vector<int32_t> &col,
-                              std::vector<double> &val) {
+                              std::vector<double> &val, bool neumann) {
   rowptr.assign(F.nnode + 1, 0);
   col.clear();
   val.clear();
@@ -84,7 +84,7 @@ void plan_strip_interpolation(const PlanLevel &C, const StripInfo &Sc, const Pla
       const int64_t i = (int64_t)J * F.Lx + I;
       const int Ig = I + Sf.G0;
       const bool owned = I >= Sf.own0 && I <= Sf.own1;
-      const bool gcon = Ig == 0 || Ig == gLxf - 1 || J == 0 || J == gLy - 1;  // global Dirichlet boundary (R5)
+      const bool gcon = !neumann && (Ig == 0 || Ig == gLxf - 1 || J == 0 || J == gLy - 1);  // Dirichlet (R5)
       if (owned && !gcon) {
         const int ci = std::min(Ig / twok, gncx - 1), cj = std::min(J / twok, gncy - 1);
         const int ra = Ig - twok * ci, rb = J - twok * cj;
@@ -104,7 +104,7 @@ void plan_strip_interpolation(const PlanLevel &C, const StripInfo &Sc, const Pla
             int I2, J2;
             loc_to_lattice(k, ci, cj, t, a, b, &I2, &J2);  // global coarse lattice
             const int gLxc = k * gncx + 1, gLyc = k * gncy + 1;
-            if (I2 == 0 || I2 == gLxc - 1 || J2 == 0 || J2 == gLyc - 1) continue;  // constrained coarse column
+            if (!neumann && (I2 == 0 || I2 == gLxc - 1 || J2 == 0 || J2 == gLyc - 1)) continue;  // constrained
             const int Il = I2 - Sc.G0;
             ent.push_back({J2 * C.Lx + Il, v});
           }

@@ -54,6 +54,27 @@ struct StencilTab {
   double m[kStencilMaxC][kStencilMaxE], kk[kStencilMaxC][kStencilMaxE];
 };
 
+// Macro-block residual (kernels_residual_mac.cu): interior coefficients of every
+// row type (I mod k, J mod k) in the entry order of residual_mac_gen.h, and the
+// stencil class that holds them.
+constexpr int kMacMaxEntries = 153;  // P3: 9 row types, 153 stencil entries
+struct MacCoef {
+  double m[kMacMaxEntries], k[kMacMaxEntries];
+};
+struct MacTab {
+  MacCoef C;
+  int32_t canon[9];
+};
+
+// Symmetry-reduced patch solve of the interior vertex-star class (host_sym.cu,
+// kernels_sweep_sym.cu): character blocks V_chi, per-mode DG(q) inverses.
+constexpr int kSymMaxMP = 19;
+struct SymTab {
+  double V[7 * 7 + 3 * 3 + 4 * 4 + 5 * 5];
+  double S[kSymMaxMP * 16];
+  double sig[kSymMaxMP];
+};
+
 // Spatial strip of a level on this rank (host_strip.cu).
 struct StripInfo {
   int rank = 0, nranks = 1;
@@ -110,6 +131,18 @@ struct Level {
   bool stencil_ok = false;
   StencilTab stencil{};
   int64_t *goff = nullptr;  // [kStencilMaxC][kStencilMaxE] global element offsets (dJ Lx + dI) NT
+  std::vector<uint8_t> h_rcls;      // host copy of rcls
+  bool mac_ok = false;              // macro-block residual available on this level
+  MacTab mac{};
+  int32_t *gen_rows = nullptr;      // rows outside the interior classes (fix-up after the macro kernel)
+  int64_t ngen_rows = 0;
+  // symmetry-reduced sweep of the interior patch class (the kron work lists then hold the other classes)
+  bool sym_ok = false;
+  int sym_cls = -1;
+  int64_t nsym = 0;
+  int32_t *sym_nodes = nullptr;     // [nsym][mp] patch nodes in host_sym.cu slot order
+  std::vector<int64_t> sym_pos;     // [mp][mp] CSR positions of the representative's block (-1: none)
+  SymTab symtab{};
   // transfer from this level to the next finer (stored on the coarse side)
   DevCSR P;    // rows: fine nodes, cols: coarse nodes
   DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)
@@ -206,6 +239,12 @@ struct wrmg_ctx {
   bool strip = false;
   wrmg::Comm *comm = nullptr;
   wrmg::Level gco;
+  // strips whose coarse levels are narrower than 2 cells per rank: those levels run
+  // replicated as a single-rank hierarchy; xfer holds P / R between the coarsest
+  // partitioned level (owned rows) and the replicated finest level (global ids)
+  wrmg_ctx *sub = nullptr;
+  wrmg::Level xfer;
+  double *sub_r = nullptr, *sub_z = nullptr, *sub_part = nullptr, *sub_all = nullptr;
   double *gr = nullptr, *gz = nullptr, *gsend = nullptr, *grecv = nullptr;
   int64_t gchunk = 0;
   // Chebyshev-accelerated smoothing (WRMG_SMOOTH_CHEBYSHEV): lambda per level, direction / B r vectors
@@ -243,10 +282,17 @@ void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const do
                          cudaStream_t s);
 void launch_kron_setup(const Level &L, int nq, const Temporal &tm, double *scratch, cudaStream_t s);
 void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal &tm, double *scratch, cudaStream_t s);
+bool launch_sweep_sym(const Level &L, int k, int q, int N, const double *r, double *u, double omega,
+                      cudaStream_t s);
 bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s);
 void launch_coarse_solve_kron(const Coarse &C, const Level &L, int q, int N, const double *r, double *x,
                               cudaStream_t s);
 void launch_gather_classes(const Level &L, int32_t *scratch_i, double *scratch_d, cudaStream_t s);
+bool launch_residual_mac(const Level &L, int k, int q, int N, const Temporal &tm, const double *u, const double *b,
+                         double *r, cudaStream_t s);
+bool plan_residual_mac(Level &L, int k, const std::vector<int32_t> &cnt, const std::vector<int32_t> &dI,
+                       const std::vector<int32_t> &dJ, const std::vector<double> &m, const std::vector<double> &kk,
+                       std::vector<int32_t> &gen_rows);
 bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const double *u, const double *b,
                          double *r, cudaStream_t s);
 void launch_rhs(const Level &L, int q, int N, const Temporal &tm, const double *fhat, double *b, cudaStream_t s);
@@ -269,6 +315,7 @@ void launch_rhs_initial(const Level &L, int nq, int64_t NT, const double *phi0, 
                         cudaStream_t s);
 // strip partition (kernels_strip.cu)
 void launch_cols(double *v, int Lx, int Ly, int64_t NT, int c0, int nc, double *buf, int mode, cudaStream_t s);
+void launch_sum_chunks(const double *all, int nchunks, int64_t n, double *out, cudaStream_t s);
 void launch_window(const double *src, int Lxs, int sc0, double *dst, int Lxd, int dc0, int Ly, int nc, int64_t NT,
                    cudaStream_t s);
 }  // namespace wrmg

@@ -411,8 +411,9 @@ void launch_residual(const Level &L, int q, int N, const Temporal &tm, const dou
     else cudaMemsetAsync(r, 0, L.nnode * NT * sizeof(double), s);
     return;
   }
-  if (launch_residual_cls(L, q, N, tm, u, b, r, s)) return;
   const int k = (L.Lx - 1) / L.nx;
+  if (L.nnode >= 50000 && launch_residual_mac(L, k, q, N, tm, u, b, r, s)) return;
+  if (launch_residual_cls(L, q, N, tm, u, b, r, s)) return;
   const int ntx = (L.Lx + RT - 1) / RT, nty = (L.Ly + RT - 1) / RT;
   dim3 grid(ntx * nty, (N + RCS - 1) / RCS);
   const int RW = RT + 2 * k;

@@ -37,6 +37,16 @@ __global__ void k_window(const double *__restrict__ src, int Lxs, int sc0, doubl
   }
 }
 
+// out[e] = sum_q all[q n + e], q = 0 .. nchunks-1 in order (rank-order all-reduce:
+// every rank forms bitwise-identical sums)
+__global__ void k_sum_chunks(const double *__restrict__ all, int nchunks, int64_t n, double *__restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < nchunks; ++q) s += all[(int64_t)q * n + e];
+    out[e] = s;
+  }
+}
+
 unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16); }
 
 }  // namespace
@@ -53,6 +63,11 @@ void launch_window(const double *src, int Lxs, int sc0, double *dst, int Lxd, in
   if (nc <= 0) return;
   const int64_t n = (int64_t)Ly * nc * NT;
   k_window<<<grid_for(n), 256, 0, s>>>(src, Lxs, sc0, dst, Lxd, dc0, Ly, nc, NT);
+  ++g_launches;
+}
+
+void launch_sum_chunks(const double *all, int nchunks, int64_t n, double *out, cudaStream_t s) {
+  k_sum_chunks<<<grid_for(n), 256, 0, s>>>(all, nchunks, n, out);
   ++g_launches;
 }
 

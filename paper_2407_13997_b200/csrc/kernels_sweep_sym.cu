@@ -1,0 +1,251 @@
+// Waveform-relaxation patch sweep (H7 + H8) for the interior vertex-star class
+// in the symmetry-adapted Kronecker basis (host_sym.cu derives it):
+//
+//   g   = R_p r_n                       gather, slot order of host_sym.cu
+//   y   = U^T g                         orbit sums / differences (adds only)
+//   gh  = diag(V_chi)^T y               four small blocks: sum d_chi^2 FMAs (P3: 99, not 361)
+//   per mode i: t = S_i gh_i, end trace y_{n,i} = t[q] + sigma_i y_{n-1,i} (scan over slabs),
+//               w = t + S_i[:, 0] y_{n-1,i} (a < q),  w[q] = y_{n,i}       (kernels_kron.cu)
+//   x   = U diag(V_chi) w
+//   u  += omega W_p x                   FP64 atomics (weighted additive scatter, R11)
+//
+// Warp = one patch, lane = one slab of a 32-slab chunk holding its NQ values; the
+// warp walks the chunks in order, the end-trace carry of every mode kept in shared
+// memory; one character block at a time is live in registers besides y.  The
+// block coefficients are kernel parameters (constant bank operands).  Patches of the
+// other (boundary) classes go through kernels_kron.cu on their own work lists.
+#include "internal.h"
+#include "sym.h"
+
+namespace wrmg {
+namespace {
+
+template <int K>
+struct SymShape;
+template <>
+struct SymShape<2> {
+  static constexpr int N1 = 1, N2 = 1, N3 = 0;
+};
+template <>
+struct SymShape<3> {
+  static constexpr int N1 = 3, N2 = 2, N3 = 1;
+};
+
+template <int K>
+struct Sh {
+  static constexpr int N1 = SymShape<K>::N1, N2 = SymShape<K>::N2, N3 = SymShape<K>::N3;
+  static constexpr int MP = 1 + 4 * N1 + 2 * N2 + 2 * N3;
+  static constexpr int D0 = 1 + N1 + N2 + N3, D1 = N1, D2 = N1 + N3, D3 = N1 + N2;
+  static constexpr int B0 = 0, B1 = D0, B2 = D0 + D1, B3 = D0 + D1 + D2;
+  static constexpr int V0 = 0, V1 = D0 * D0, V2 = V1 + D1 * D1, V3 = V2 + D2 * D2;
+  static constexpr int T1 = 1, T2 = 1 + 4 * N1, T3 = 1 + 4 * N1 + 2 * N2;  // first slot of each orbit type
+};
+
+constexpr double kR = 0.70710678118654752440;  // 1/sqrt(2)
+
+// y = U^T g (slot order -> block coordinates)
+template <int K>
+__device__ __forceinline__ void sym_fwd(const double (&g)[Sh<K>::MP], double (&y)[Sh<K>::MP]) {
+  using S = Sh<K>;
+  y[S::B0] = g[0];
+#pragma unroll
+  for (int o = 0; o < S::N1; ++o) {
+    const double x0 = g[S::T1 + 4 * o], x1 = g[S::T1 + 4 * o + 1], x2 = g[S::T1 + 4 * o + 2],
+                 x3 = g[S::T1 + 4 * o + 3];
+    const double s01 = x0 + x1, d01 = x0 - x1, s23 = x2 + x3, d23 = x2 - x3;
+    y[S::B0 + 1 + o] = 0.5 * (s01 + s23);
+    y[S::B1 + o] = 0.5 * (s01 - s23);
+    y[S::B2 + o] = 0.5 * (d01 + d23);
+    y[S::B3 + o] = 0.5 * (d01 - d23);
+  }
+#pragma unroll
+  for (int o = 0; o < S::N2; ++o) {
+    const double x0 = g[S::T2 + 2 * o], x1 = g[S::T2 + 2 * o + 1];
+    y[S::B0 + 1 + S::N1 + o] = kR * (x0 + x1);
+    y[S::B3 + S::N1 + o] = kR * (x0 - x1);
+  }
+#pragma unroll
+  for (int o = 0; o < S::N3; ++o) {
+    const double x0 = g[S::T3 + 2 * o], x1 = g[S::T3 + 2 * o + 1];
+    y[S::B0 + 1 + S::N1 + S::N2 + o] = kR * (x0 + x1);
+    y[S::B2 + S::N1 + o] = kR * (x0 - x1);
+  }
+}
+
+// x = U y (block coordinates -> slot order)
+template <int K>
+__device__ __forceinline__ void sym_bwd(const double (&y)[Sh<K>::MP], double (&x)[Sh<K>::MP]) {
+  using S = Sh<K>;
+  x[0] = y[S::B0];
+#pragma unroll
+  for (int o = 0; o < S::N1; ++o) {
+    const double a = y[S::B0 + 1 + o], b = y[S::B1 + o], c = y[S::B2 + o], d = y[S::B3 + o];
+    const double ab = a + b, amb = a - b, cd = c + d, cmd = c - d;
+    x[S::T1 + 4 * o] = 0.5 * (ab + cd);
+    x[S::T1 + 4 * o + 1] = 0.5 * (ab - cd);
+    x[S::T1 + 4 * o + 2] = 0.5 * (amb + cmd);
+    x[S::T1 + 4 * o + 3] = 0.5 * (amb - cmd);
+  }
+#pragma unroll
+  for (int o = 0; o < S::N2; ++o) {
+    const double a = y[S::B0 + 1 + S::N1 + o], d = y[S::B3 + S::N1 + o];
+    x[S::T2 + 2 * o] = kR * (a + d);
+    x[S::T2 + 2 * o + 1] = kR * (a - d);
+  }
+#pragma unroll
+  for (int o = 0; o < S::N3; ++o) {
+    const double a = y[S::B0 + 1 + S::N1 + S::N2 + o], c = y[S::B2 + S::N1 + o];
+    x[S::T3 + 2 * o] = kR * (a + c);
+    x[S::T3 + 2 * o + 1] = kR * (a - c);
+  }
+}
+
+// One character block of the transformed patch solve, for all NQ temporal nodes:
+//   gh = V_chi^T y_chi;  per mode i of the block: t = S_i gh, end-trace scan, carry;
+//   y_chi <- V_chi w   (in place: y_chi is dead once gh is formed)
+template <int D, int B, int VO, int MODE0, int NQ, int MP>
+__device__ __forceinline__ void sym_block(const SymTab &P, double (&y)[NQ][MP], double *ycar, int lane) {
+  double t[NQ][D];
+#pragma unroll
+  for (int a = 0; a < NQ; ++a)
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(P.V[VO + j * D + i], y[a][B + j], s);
+      t[a][i] = s;
+    }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const int md = MODE0 + i;
+    double gh[NQ];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) gh[a] = t[a][i];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 < NQ; ++b2) s = fma(P.S[md * 16 + a * NQ + b2], gh[b2], s);
+      t[a][i] = s;
+    }
+    const double sg = P.sig[md];
+    double v = t[NQ - 1][i], pp = sg;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, v, d);
+      v = fma(lane >= d ? pp : 0.0, o, v);
+      pp *= pp;
+    }
+    double pw = 1.0, bs = sg;  // sigma^(lane + 1)
+#pragma unroll
+    for (int bit = 0; bit < 6; ++bit) {
+      pw *= (((lane + 1) >> bit) & 1) ? bs : 1.0;
+      bs *= bs;
+    }
+    const double yc = ycar[md];
+    const double yn = fma(pw, yc, v);
+    double yp = __shfl_up_sync(0xffffffffu, yn, 1);
+    if (lane == 0) yp = yc;
+#pragma unroll
+    for (int a = 0; a < NQ - 1; ++a) t[a][i] = fma(P.S[md * 16 + a * NQ + 0], yp, t[a][i]);
+    t[NQ - 1][i] = yn;
+    const double last = __shfl_sync(0xffffffffu, yn, 31);
+    __syncwarp();
+    if (lane == 0) ycar[md] = last;
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; ++a)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) s = fma(P.V[VO + j * D + i], t[a][i], s);
+      y[a][B + j] = s;
+    }
+}
+
+template <int K, int NQ>
+__global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, const int32_t *__restrict__ pnodes,
+                                                      const __grid_constant__ SymTab P,
+                                                      const double *__restrict__ wnode, double omega,
+                                                      const double *__restrict__ r, double *__restrict__ u) {
+  using S = Sh<K>;
+  constexpr int MP = S::MP;
+  constexpr int WPC = 4;
+  __shared__ int snode[WPC][MP];
+  __shared__ double swt[WPC][MP];
+  __shared__ double sycar[WPC][MP];  // end trace of every mode at the previous chunk's last slab
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t NT = (int64_t)N * NQ;
+  const int nch = (N + 31) / 32;
+  for (int64_t p = (int64_t)blockIdx.x * WPC + w; p < npatch; p += (int64_t)gridDim.x * WPC) {
+    __syncwarp();
+    if (lane < MP) {
+      const int nd = __ldg(pnodes + p * MP + lane);
+      snode[w][lane] = nd;
+      swt[w][lane] = omega * __ldg(wnode + nd);
+      sycar[w][lane] = 0.0;
+    }
+    __syncwarp();
+    for (int ch = 0; ch < nch; ++ch) {
+      const int n = 32 * ch + lane;
+      const bool valid = n < N;
+      double y[NQ][MP];
+      {  // gather (slot order) and y = U^T g
+        double g[NQ][MP];
+#pragma unroll
+        for (int j = 0; j < MP; ++j) {
+          const double *src = r + (int64_t)snode[w][j] * NT + (int64_t)n * NQ;
+          if constexpr (NQ == 2) {
+            const double2 v = valid ? __ldg(reinterpret_cast<const double2 *>(src)) : make_double2(0.0, 0.0);
+            g[0][j] = v.x;
+            g[1][j] = v.y;
+          } else {
+#pragma unroll
+            for (int a = 0; a < NQ; ++a) g[a][j] = valid ? __ldg(src + a) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) sym_fwd<K>(g[a], y[a]);
+      }
+      sym_block<S::D0, S::B0, S::V0, S::B0, NQ, MP>(P, y, sycar[w], lane);
+      sym_block<S::D1, S::B1, S::V1, S::B1, NQ, MP>(P, y, sycar[w], lane);
+      sym_block<S::D2, S::B2, S::V2, S::B2, NQ, MP>(P, y, sycar[w], lane);
+      sym_block<S::D3, S::B3, S::V3, S::B3, NQ, MP>(P, y, sycar[w], lane);
+      // x = U y and the weighted additive scatter
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) {
+        double x[MP];
+        sym_bwd<K>(y[a], x);
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < MP; ++j)
+            atomicAdd(u + (int64_t)snode[w][j] * NT + (int64_t)n * NQ + a, swt[w][j] * x[j]);
+        }
+      }
+    }
+  }
+}
+
+template <int K, int NQ>
+void sym_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
+  const int64_t nblk = (L.nsym + 3) / 4;
+  const int grid = (int)std::min<int64_t>(nblk, (int64_t)6 * num_sms());
+  k_sweep_sym<K, NQ><<<grid, 128, 0, s>>>(N, L.nsym, L.sym_nodes, L.symtab, L.wnode, omega, r, u);
+  ++g_launches;
+}
+
+}  // namespace
+
+bool launch_sweep_sym(const Level &L, int k, int q, int N, const double *r, double *u, double omega,
+                      cudaStream_t s) {
+  if (!L.sym_ok || L.nsym == 0) return false;
+#define WRMG_SYM(KK_, NQ_) \
+  if (k == KK_ && q + 1 == NQ_) { sym_launch<KK_, NQ_>(L, N, r, u, omega, s); return true; }
+  WRMG_SYM(2, 1) WRMG_SYM(2, 2) WRMG_SYM(2, 3) WRMG_SYM(2, 4)
+  WRMG_SYM(3, 1) WRMG_SYM(3, 2) WRMG_SYM(3, 3)
+#undef WRMG_SYM
+  return false;
+}
+
+}  // namespace wrmg

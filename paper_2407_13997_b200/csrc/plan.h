@@ -26,7 +26,9 @@ constexpr uint8_t kRowConstrained = 255;
 constexpr uint8_t kRowGeneric = 254;
 
 // Type-grouped CTA work list for the Kronecker sweep: ncta x pp patch ids (-1 pad).
-void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type);
+// Patches of class `exclude` (>= 0) are left out (they run in the symmetry-reduced sweep).
+void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type,
+                     int exclude = -1);
 
 void plan_level(int nx, int ny, double h, int k, PlanLevel *P, bool neumann = false);
 void plan_interpolation(const PlanLevel &C, const PlanLevel &F, int k, std::vector<int32_t> &rowptr,

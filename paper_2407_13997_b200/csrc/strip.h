@@ -28,12 +28,13 @@ namespace wrmg {
 // Plan one level's strip: the local PlanLevel (patches restricted to owned vertices,
 // translation classes renumbered) and the column bookkeeping.
 void plan_strip_level(int gnx, int gny, int x0, int nx, double h, int k, int rank, int nranks, PlanLevel *P,
-                      StripInfo *S);
+                      StripInfo *S, bool neumann = false);
 
 // P_h (correction form, R5, R12) with rows only for owned fine nodes; columns are
-// local coarse lattice indices.
+// local coarse lattice indices (Sc = a whole-lattice strip with G0 = 0: global ids,
+// used for the hand-over to the replicated coarse levels).
 void plan_strip_interpolation(const PlanLevel &C, const StripInfo &Sc, const PlanLevel &F, const StripInfo &Sf, int k,
                               int gny_f, std::vector<int32_t> &rowptr, std::vector<int32_t> &col,
-                              std::vector<double> &val);
+                              std::vector<double> &val, bool neumann = false);
 
 }  // namespace wrmg

@@ -60,12 +60,13 @@ def test_dmma_sweep_vcycle_fgmres(n, k, N, nc, mp):
     c.close()
 
 
-@pytest.mark.parametrize("k,q", [(1, 0), (2, 2)])
-def test_multi_patch_cta_sweep(k, q):
+def test_multi_patch_cta_sweep():
+    """P1 x DG0 on 50x50 (2401 single-node patches, one 32-slab chunk): PP = 8 patches
+    per CTA in k_sweep_kron, every entry of three sweeps."""
     from oracle import patches, smoother
     from oracle import heat
     import paper_2407_13997_b200 as w
-    n, N = 50, 4
+    n, k, q, N = 50, 1, 0, 4
     p = heat.unit_square_problem(n, k, q, N, 1.0 / N)
     c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N)
     P, _ = patches.vertex_star_patches(p.mesh, k, p.constrained)
@@ -80,3 +81,59 @@ def test_multi_patch_cta_sweep(k, q):
         c.smooth(u, _dev(b), 1, om)
         assert_parity(_host(u), u_ref, tol=TOL, what=f"sweep {s}")
     c.close()
+
+
+def _sampled_sweep_check(n, k, q, N, nodes_ij, omega=0.9):
+    """One sweep from a random state on an n x n mesh; the update at the sampled
+    nodes against omega * sum_{p ni i} x_p[i] / mu_i, x_p = the oracle's exact patch
+    space-time solve (Kronecker-built blocks, per-slab LAPACK LU)."""
+    from oracle import heat, smoother
+    from oracle import patches as pm
+    import paper_2407_13997_b200 as w
+    p = heat.unit_square_problem(n, k, q, N, 1.0 / N, build_matrix=False)
+    c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N)
+    P, _ = pm.vertex_star_patches(p.mesh, k, p.constrained)
+    b = wi.spacetime_field(p.nnode, N, q, seed=3)
+    u0 = wi.spacetime_field(p.nnode, N, q, seed=4) * np.repeat(p.free, p.NT)
+    ug = _dev(u0)
+    c.smooth(ug, _dev(b), 1, omega)
+    du = (_host(ug) - u0).reshape(p.nnode, -1)
+    mu = pm.multiplicity(P, p.nnode)
+    L = k * n + 1
+    nq = q + 1
+    rn = {}
+
+    def rnode(j):
+        if j not in rn:
+            rn[j] = p.residual_node(j, u0, b).reshape(N, nq)
+        return rn[j]
+
+    worst = 0.0
+    for I, J in nodes_ij:
+        i = J * L + I
+        if not p.free[i]:
+            continue
+        acc = np.zeros(p.NT)
+        for pt in P:
+            if i not in pt:
+                continue
+            g = np.concatenate([np.stack([rnode(j)[s] for j in pt]).ravel() for s in range(N)])
+            x = smoother.patch_solve_kron(p, pt, g).reshape(N, pt.size, nq)
+            acc += omega * x[:, list(pt).index(i), :].ravel() / mu[i]
+        worst = max(worst, np.max(np.abs(du[i] - acc)) / np.max(np.abs(acc)))
+    c.close()
+    return worst
+
+
+@pytest.mark.parametrize("n,k,q,N", [(40, 3, 0, 37), (40, 3, 2, 6), (40, 3, 1, 20), (36, 2, 0, 33),
+                                     (36, 2, 2, 4), (36, 2, 3, 5), (48, 2, 1, 3)])
+def test_symmetric_sweep_sampled(n, k, q, N):
+    """Levels with >= 1000 patches run the interior class through the symmetry-reduced
+    sweep (kernels_sweep_sym.cu) and the boundary classes through kernels_kron.cu;
+    sampled nodes cover the vertex, edge and cell-interior types of both, the corners
+    and the lattice edges."""
+    L = k * n + 1
+    m = L // 2
+    nodes = [(1, 1), (2, 1), (1, 2), (k, k), (k + 1, k), (2 * k, 1), (m, m), (m + 1, m), (m, m + 1),
+             (m + 1, m + 2), (m + 2, m + 2), (L - 2, L - 2), (L - 2, m), (m, 1), (3 * k + 1, 2 * k + 2)]
+    assert _sampled_sweep_check(n, k, q, N, nodes) <= 1e-10

@@ -38,16 +38,21 @@ def _owned(ctx, v):
     return a[:, lay["own0"]:lay["own1"] + 1, :], lay["g0"] + lay["own0"]
 
 
-@pytest.mark.parametrize("P,snx,ny,k,q,N,nc", [(2, 8, 8, 2, 1, 6, 2), (4, 4, 8, 1, 0, 5, 4), (2, 8, 16, 3, 1, 3, 4),
-                                             (3, 8, 8, 2, 1, 40, 2)])
-def test_strips_match_global(P, snx, ny, k, q, N, nc):
+@pytest.mark.parametrize("P,snx,ny,k,q,N,nc,bc", [(2, 8, 8, 2, 1, 6, 2, "dirichlet0"), (4, 4, 8, 1, 0, 5, 4, "dirichlet0"),
+                                                (2, 8, 16, 3, 1, 3, 4, "dirichlet0"), (3, 8, 8, 2, 1, 40, 2, "dirichlet0"),
+                                                # agglomerated coarse levels (strips narrower than 2 cells)
+                                                (4, 4, 16, 2, 1, 6, 2, "dirichlet0"), (8, 4, 32, 3, 1, 4, 4, "dirichlet0"),
+                                                (4, 2, 8, 1, 1, 33, 2, "dirichlet0"),
+                                                # Neumann boundaries (the paper's heat runs)
+                                                (2, 8, 8, 2, 1, 6, 2, "neumann"), (4, 4, 16, 3, 0, 5, 4, "neumann")])
+def test_strips_match_global(P, snx, ny, k, q, N, nc, bc):
     import torch
     import paper_2407_13997_b200 as w
     gnx = P * snx
     h = 1.0 / ny
     dt = 1.0 / N
     # global single-rank reference on the same device
-    g = w.Context(gnx, ny, h, degree=k, q=q, nslabs=N, dt=dt, ncoarse=nc)
+    g = w.Context(gnx, ny, h, degree=k, q=q, nslabs=N, dt=dt, ncoarse=nc, bc=bc)
     gl = g.layout
     f = wi.spacetime_field(gl["nnode"], N, q, 5)
     fd = torch.as_tensor(f, device="cuda:0")
@@ -69,7 +74,7 @@ def test_strips_match_global(P, snx, ny, k, q, N, nc):
         st = torch.cuda.Stream()
         with torch.cuda.stream(st):
             c = w.Context(gnx, ny, h, degree=k, q=q, nslabs=N, dt=dt, ncoarse=nc, rank=r, nranks=P, hub=hub,
-                          stream=st.cuda_stream)
+                          stream=st.cuda_stream, bc=bc)
             lay = c.layout
             # f on the local lattice from the global generator (local column c <-> global g0 + c)
             Lx = lay["lx"]
@@ -101,7 +106,10 @@ def test_strips_match_global(P, snx, ny, k, q, N, nc):
         assert e <= 1e-12, f"{key}: rel {e:.3e}"
 
 
-@pytest.mark.parametrize("P,snx,ny,k,q,N,nc", [(2, 8, 8, 2, 1, 6, 2), (4, 4, 8, 1, 0, 5, 4), (3, 8, 16, 3, 1, 4, 4)])
+@pytest.mark.parametrize("P,snx,ny,k,q,N,nc", [(2, 8, 8, 2, 1, 6, 2), (4, 4, 8, 1, 0, 5, 4), (3, 8, 16, 3, 1, 4, 4),
+                                             # C2-shaped hierarchy (P3 x DG1, coarsest 4 x 4) split 4 and 8 ways:
+                                             # the 4^2 and 8^2 levels run replicated
+                                             (4, 8, 32, 3, 1, 16, 4), (8, 4, 32, 3, 1, 16, 4)])
 def test_strips_fgmres_match_global(P, snx, ny, k, q, N, nc):
     """FGMRES(30)-WRMG across strips (H13 with cross-rank dot products): the same
     iteration count as the single-rank solve and the owned columns of x equal to

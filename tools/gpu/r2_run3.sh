@@ -1,0 +1,3 @@
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/atomic_probe tools/atomic_probe.cu && /tmp/atomic_probe > gpurun_out/r2_atomic_probe.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_residual_mac.py tests/test_gpu_fullsize.py -x -q -p no:cacheprovider > gpurun_out/r2_t3.log 2>&1; echo rc=$? >> gpurun_out/r2_t3.log
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_b3.json 2> gpurun_out/r2_b3.err
