@@ -17,6 +17,7 @@
 
 #include "comm.h"
 #include "internal.h"
+#include "lattice.h"
 #include "ns.h"
 #include "ns_kernels.h"
 #include "plan.h"
@@ -208,7 +209,8 @@ void free_level(Level &L) {
                   (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8, (void *)L.vvptr, (void *)L.conv,
                   (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo, (void *)L.ppos, (void *)L.pvv, (void *)L.hx[0],
                   (void *)L.hx[1],
-                  (void *)L.hx[2], (void *)L.hx[3], (void *)L.gen_rows, (void *)L.sym_nodes})
+                  (void *)L.hx[2], (void *)L.hx[3], (void *)L.gen_rows, (void *)L.sym_nodes,
+                  (void *)L.tile_patch, (void *)L.sym_single, (void *)L.tgeo_dev})
     dfree(p);
 }
 
@@ -359,6 +361,88 @@ bool sym_disabled() {  // WRMG_SWEEP_SYM=0: every class through kernels_kron.cu 
   const char *e = getenv("WRMG_SWEEP_SYM");
   return e && e[0] == '0';
 }
+bool tiles_disabled() {  // WRMG_SWEEP_TILES=0: symmetric patches one per warp with atomics only (A/B)
+  const char *e = getenv("WRMG_SWEEP_TILES");
+  return e && e[0] == '0';
+}
+
+// 2 x 2 tiles of symmetric-class patches (even vertex coordinates) for the tiled
+// sweep; every tile must have the representative's union geometry, else the tiled
+// form is not used on this level.
+void plan_sym_tiles(const PlanLevel &P, int k, int cls, int mp, const std::vector<int32_t> &sn, Level &L,
+                    cudaStream_t s) {
+  const int nvx = P.nx + 1;
+  std::vector<int32_t> at((size_t)nvx * (P.ny + 1), -1);  // vertex -> index in the symmetric list
+  {
+    int32_t q = 0;
+    for (int64_t p = 0; p < P.npatch; ++p)
+      if (P.ptype[p] == cls) at[P.pvert[p]] = q++;
+  }
+  std::vector<int32_t> tiles, single;
+  std::vector<uint8_t> used(L.nsym, 0);
+  TileGeom G{};
+  bool have = false, ok = !tiles_disabled();
+  for (int vj = 0; ok && vj + 1 <= P.ny; vj += 2)
+    for (int vi = 0; ok && vi + 1 <= P.nx; vi += 2) {
+      const int32_t q[4] = {at[vj * nvx + vi], at[vj * nvx + vi + 1], at[(vj + 1) * nvx + vi],
+                            at[(vj + 1) * nvx + vi + 1]};
+      if (q[0] < 0 || q[1] < 0 || q[2] < 0 || q[3] < 0) continue;
+      const int64_t base = (int64_t)k * vj * P.Lx + k * vi;
+      TileGeom T{};
+      for (int w = 0; w < 4; ++w)
+        for (int j = 0; j < mp; ++j) {
+          const int32_t o = (int32_t)(sn[(size_t)q[w] * mp + j] - base);
+          int u = 0;
+          while (u < T.nu && T.off[u] != o) ++u;
+          if (u == T.nu) {
+            if (T.nu == kTileMaxU) { ok = false; break; }
+            T.off[T.nu++] = o;
+          }
+          if (T.cnt[u] == 4) { ok = false; break; }
+          T.src[u][T.cnt[u]++] = (int16_t)(w * mp + j);
+        }
+      if (!ok) break;
+      if (!have) {
+        for (int u = 0; u < T.nu; ++u) {  // interior: the node's entity vertices all lie in the tile
+          const int64_t g = base + T.off[u];
+          int ei[3], ej[3];
+          const int ne = entity_vertices(k, (int)(g % P.Lx), (int)(g / P.Lx), ei, ej);
+          bool in = true;
+          for (int e = 0; e < ne; ++e) in = in && ei[e] >= vi && ei[e] <= vi + 1 && ej[e] >= vj && ej[e] <= vj + 1;
+          T.interior[u] = in;
+        }
+        G = T;
+        have = true;
+      } else {
+        bool same = T.nu == G.nu;
+        for (int u = 0; same && u < T.nu; ++u) {
+          same = T.off[u] == G.off[u] && T.cnt[u] == G.cnt[u];
+          for (int e = 0; same && e < T.cnt[u]; ++e) same = T.src[u][e] == G.src[u][e];
+        }
+        if (!same) { ok = false; break; }
+      }
+      for (int w = 0; w < 4; ++w) {
+        tiles.push_back(q[w]);
+        used[q[w]] = 1;
+      }
+    }
+  if (!ok || !have) {
+    tiles.clear();
+    std::fill(used.begin(), used.end(), 0);
+  }
+  for (int64_t q = 0; q < L.nsym; ++q)
+    if (!used[q]) single.push_back((int32_t)q);
+  L.ntile = (int64_t)tiles.size() / 4;
+  L.nsingle = (int64_t)single.size();
+  L.tgeo = (ok && have) ? G : TileGeom{};
+  if (L.ntile) {
+    L.tile_patch = dupload(tiles, s);
+    L.tgeo_dev = dupload(std::vector<TileGeom>{L.tgeo}, s);
+  }
+  if (L.nsingle) L.sym_single = dupload(single, s);
+}
+
+
 
 // Symmetry-reduced sweep coefficients of the interior class from the assembled M, kappa K.
 void sym_setup(wrmg_ctx *c, Level &L) {
@@ -1290,6 +1374,7 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
           L.sym_cls = cls;
           L.nsym = cnt[cls];
           L.sym_nodes = dupload(sn, s);
+          plan_sym_tiles(P, degree, cls, (int)perm.size(), sn, L, s);
           // CSR positions of the representative patch block (values read at factor time)
           const int64_t rep = P.type_rep[cls];
           const int mps = (int)perm.size();

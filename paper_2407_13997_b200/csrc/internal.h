@@ -75,6 +75,19 @@ struct SymTab {
   double sig[kSymMaxMP];
 };
 
+// 2 x 2 vertex tiles of the symmetric class (kernels_sweep_sym.cu, tiled form): the
+// union of the four patches' nodes (relative lattice offsets from the tile's first
+// vertex node), which of them no patch outside the tile touches (plain
+// read-modify-write instead of atomics), and the (patch, slot) pairs feeding each.
+constexpr int kTileMaxU = 64;
+struct TileGeom {
+  int nu = 0;
+  int32_t off[kTileMaxU];
+  uint8_t interior[kTileMaxU];
+  uint8_t cnt[kTileMaxU];
+  int16_t src[kTileMaxU][4];  // w * MP + slot
+};
+
 // Spatial strip of a level on this rank (host_strip.cu).
 struct StripInfo {
   int rank = 0, nranks = 1;
@@ -143,6 +156,11 @@ struct Level {
   int32_t *sym_nodes = nullptr;     // [nsym][mp] patch nodes in host_sym.cu slot order
   std::vector<int64_t> sym_pos;     // [mp][mp] CSR positions of the representative's block (-1: none)
   SymTab symtab{};
+  int64_t ntile = 0, nsingle = 0;
+  int32_t *tile_patch = nullptr;    // [ntile][4] indices into sym_nodes (tile vertices (0,0),(1,0),(0,1),(1,1))
+  int32_t *sym_single = nullptr;    // sym patches outside complete tiles
+  TileGeom tgeo{};
+  TileGeom *tgeo_dev = nullptr;
   // transfer from this level to the next finer (stored on the coarse side)
   DevCSR P;    // rows: fine nodes, cols: coarse nodes
   DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)

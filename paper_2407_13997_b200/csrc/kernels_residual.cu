@@ -477,11 +477,12 @@ bool launch_residual_cls(const Level &L, int q, int N, const Temporal &tm, const
   const size_t smem = (size_t)RW * RW * 32 * (q + 1) * sizeof(double);
   if (smem > 200 * 1024) return false;
   const size_t tab = (size_t)L.stencil.ncls * kStencilMaxE * (sizeof(double2) + sizeof(int));
+  const bool tma_fits = smem + tab <= 220 * 1024;  // u tile + class tables in dynamic shared memory
   CUtensorMap umap;
-  if (RW <= 256 && 32 * (q + 1) <= 256 && umap_for(u, (int64_t)N * (q + 1), L.Lx, L.Ly, 32 * (q + 1), RW, &umap)) {
+  if (tma_fits && RW <= 256 && 32 * (q + 1) <= 256 && umap_for(u, (int64_t)N * (q + 1), L.Lx, L.Ly, 32 * (q + 1), RW, &umap)) {
 #define WRMG_RT(NQ)                                                                                          \
     {                                                                                                        \
-      smem_optin((const void *)k_residual_tma<NQ>, 200 * 1024);                                                                                                      \
+      smem_optin((const void *)k_residual_tma<NQ>, (int)(smem + tab));                                                                                                      \
       k_residual_tma<NQ><<<ntx * nty, 256, smem + tab, s>>>(umap, k, L.Lx, L.Ly, N, L.rcls, b, r, t,          \
                                                             L.stencil,                                       \
                                                       apply);                                                \

@@ -34,6 +34,33 @@
 #include <string>
 
 #include "internal.h"
+
+namespace wrmg {
+// value types of the L1 macro kernel (NQ doubles per lane) and their FMA, declared
+// before the generated accumulation code that calls vfma
+struct V3 {
+  double x, y, z;
+};
+struct V4 {
+  double2 a, b;
+};
+__device__ __forceinline__ void vfma(double &acc, double c, const double &v) { acc = fma(c, v, acc); }
+__device__ __forceinline__ void vfma(double2 &acc, double c, const double2 &v) {
+  acc.x = fma(c, v.x, acc.x);
+  acc.y = fma(c, v.y, acc.y);
+}
+__device__ __forceinline__ void vfma(V3 &acc, double c, const V3 &v) {
+  acc.x = fma(c, v.x, acc.x);
+  acc.y = fma(c, v.y, acc.y);
+  acc.z = fma(c, v.z, acc.z);
+}
+__device__ __forceinline__ void vfma(V4 &acc, double c, const V4 &v) {
+  vfma(acc.a, c, v.a);
+  vfma(acc.b, c, v.b);
+}
+
+}  // namespace wrmg
+
 #include "residual_mac_gen.h"
 
 namespace wrmg {
@@ -79,150 +106,6 @@ __device__ __forceinline__ void mac_accum(const double *g0, const double *g1, co
   if constexpr (K == 1) mac_accum_k1<RWX, VPC>(g0, g1, g2, C, am, ak);
   else if constexpr (K == 2) mac_accum_k2<RWX, VPC>(g0, g1, g2, C, am, ak);
   else mac_accum_k3<RWX, VPC>(g0, g1, g2, C, am, ak);
-}
-
-template <int K, int NQ, int MX, int R>
-__global__ void __launch_bounds__(32 * MX) k_residual_mac(const __grid_constant__ CUtensorMap umap,
-                                                          const __grid_constant__ MacArgs P, int Lx, int Ly,
-                                                          int64_t NT, int nstrips, int nmy, int JS,
-                                                          const uint8_t *__restrict__ rcls,
-                                                          const double *__restrict__ b, double *__restrict__ r,
-                                                          int apply) {
-  constexpr int VPC = NQ * (32 / NQ);  // time values per chunk (lanes >= VPC idle)
-  constexpr int SPC = VPC / NQ;        // slabs per chunk
-  constexpr int RWX = K * MX + 2 * K;  // staged window width (nodes)
-  constexpr int GROUP = K * RWX * VPC; // doubles per group of K node lines
-  constexpr int KK = K * K;
-  constexpr int LA = R - 3;            // macro rows of TMA lookahead
-  extern __shared__ __align__(128) double ring[];
-  __shared__ __align__(8) uint64_t full[R];
-  double *prevq = ring + R * GROUP;  // [2][MX][JS][KK]: (M u)_{last slab}[q] of the previous chunk (by parity)
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int strip = blockIdx.x % nstrips, seg = blockIdx.x / nstrips;
-  const int j0 = seg * JS, ns = min(nmy, j0 + JS) - j0;  // macro rows of this segment
-  const int x0 = K * MX * strip;                           // first node column of the strip
-  const int im = MX * strip + w;                           // this warp's macro column
-  const int ngrp = ns + 2;                                 // line groups per chunk (halo groups included)
-  const int nch = (int)((NT + VPC - 1) / VPC);
-  const int nsteps = nch * ns;
-  if (ns <= 0) return;
-  // lane constants: temporal node a of this lane; its column of (CE, Mt) (the lane's
-  // contribution to every output a2 of its slab) or, for NQ = 3, its row
-  const int al = lane % NQ, lbase = lane - al;
-  double cea[NQ], mta[NQ];
-#pragma unroll
-  for (int c2 = 0; c2 < NQ; ++c2) {
-    cea[c2] = (NQ & (NQ - 1)) ? P.CE[al * NQ + c2] : P.CE[c2 * NQ + al];
-    mta[c2] = (NQ & (NQ - 1)) ? P.Mt[al * NQ + c2] : P.Mt[c2 * NQ + al];
-  }
-  if (tid == 0) {
-    for (int z = 0; z < R; ++z) mbar_init(&full[z], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  for (int e = tid; e < 2 * MX * JS * KK; e += blockDim.x) prevq[e] = 0.0;
-  __syncthreads();
-  constexpr unsigned kBytes = (unsigned)(GROUP * sizeof(double));
-  auto issue = [&](int F) {
-    const int c = F / ngrp, g = F - c * ngrp, z = F % R;
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_expect_tx(&full[z], kBytes);
-    tma_load_3d(ring + (size_t)z * GROUP, &umap, c * VPC, x0 - K, K * (j0 + g - 1), &full[z]);
-  };
-  int issued = 0;  // groups issued so far (thread 0's bookkeeping)
-  const bool active = im * K < Lx;
-  // b and the row classes of a step, loaded one step ahead (software pipelined)
-  auto load_b = [&](int st, double (&bvv)[KK], int &rcv) {
-    const int cs = st / ns, jms = j0 + (st - cs * ns);
-    const int64_t tgs = (int64_t)cs * VPC + lane;
-    const bool vs = lane < VPC && tgs < NT;
-    rcv = 0xFF;
-    if (lane < KK) {
-      const int X = K * im + lane % K, Y = K * jms + lane / K;
-      rcv = (X < Lx && Y < Ly) ? (int)__ldg(rcls + (int64_t)Y * Lx + X) : 0x100;
-    }
-#pragma unroll
-    for (int t = 0; t < KK; ++t) {
-      const int X = K * im + t % K, Y = K * jms + t / K;
-      bvv[t] = (vs && !apply && X < Lx && Y < Ly) ? __ldg(b + ((int64_t)Y * Lx + X) * NT + tgs) : 0.0;
-    }
-  };
-  double bv[KK];
-  int rc = 0xFF;
-  if (active) load_b(0, bv, rc);
-  for (int s = 0; s < nsteps; ++s) {
-    const int c = s / ns, jj = s - c * ns, jm = j0 + jj;
-    const int lo = c * ngrp + jj;  // first of the three groups of this step
-    if (tid == 0) {  // keep the ring up to LA steps ahead, as far as free slots allow
-      const int st = min(nsteps - 1, s + LA);
-      const int hi = (st / ns) * ngrp + (st - (st / ns) * ns) + 2;
-      while (issued <= hi && issued - R < lo) issue(issued++);
-    }
-    const int64_t tg = (int64_t)c * VPC + lane;
-    const bool valid = lane < VPC && tg < NT;
-    double bn[KK];
-    int rcn = 0xFF;
-    if (active && s + 1 < nsteps) load_b(s + 1, bn, rcn);
-#pragma unroll
-    for (int g = 0; g < 3; ++g) mbar_wait(&full[(lo + g) % R], (unsigned)(((lo + g) / R) & 1));
-    if (active) {
-      const double *gp[3];
-#pragma unroll
-      for (int g = 0; g < 3; ++g) gp[g] = ring + (size_t)((lo + g) % R) * GROUP + (K * w) * VPC + lane;
-      double am[KK], ak[KK];
-#pragma unroll
-      for (int t = 0; t < KK; ++t) am[t] = ak[t] = 0.0;
-      mac_accum<K, VPC, RWX>(gp[0], gp[1], gp[2], P.C, am, ak);
-      const int n = c * SPC + lane / NQ;
-      const double *pqr = prevq + (((size_t)(c & 1) * MX + w) * JS + jj) * KK;
-      double *pqw = prevq + (((size_t)((c + 1) & 1) * MX + w) * JS + jj) * KK;
-#pragma unroll
-      for (int t = 0; t < KK; ++t) {
-        const int cls = __shfl_sync(0xffffffffu, rc, t);
-        if (cls > 0xFF) continue;  // outside the lattice
-        const int X = K * im + t % K, Y = K * jm + t / K;
-        // upwind jump (M u)_{n-1}[q]: lane - 1's value, lane 0 the previous chunk's last
-        double jmv = __shfl_up_sync(0xffffffffu, am[t], 1);
-        if (lane == 0) jmv = pqr[t];
-        if (lane == VPC - 1) pqw[t] = am[t];
-        double acc;
-        if constexpr ((NQ & (NQ - 1)) == 0) {
-          // reduce-scatter of the lanes' contributions over the NQ lanes of a slab
-          double p[NQ];
-#pragma unroll
-          for (int a2 = 0; a2 < NQ; ++a2) p[a2] = fma(cea[a2], am[t], mta[a2] * ak[t]);
-#pragma unroll
-          for (int mm = NQ / 2; mm >= 1; mm >>= 1) {
-#pragma unroll
-            for (int j = 0; j < mm; ++j) {
-              const bool hi = al & mm;
-              const double send = hi ? p[j] : p[j + mm], keep = hi ? p[j + mm] : p[j];
-              p[j] = keep + __shfl_xor_sync(0xffffffffu, send, mm);
-            }
-          }
-          acc = bv[t] - p[0];
-        } else {
-          acc = bv[t];
-#pragma unroll
-          for (int c2 = 0; c2 < NQ; ++c2) {
-            const double mc = __shfl_sync(0xffffffffu, am[t], (lbase + c2) & 31);
-            const double kc = __shfl_sync(0xffffffffu, ak[t], (lbase + c2) & 31);
-            acc -= cea[c2] * mc + mta[c2] * kc;
-          }
-        }
-        if (al == 0 && n > 0) acc += jmv;
-        double val = apply ? -acc : acc;  // apply: y = A u = -(0 - A u)
-        if (cls == 0xFF) {
-          const double own = gp[1][((t / K) * RWX + K + t % K) * VPC];
-          val = apply ? own : bv[t] - own;
-        }
-        if (valid) r[((int64_t)Y * Lx + X) * NT + tg] = val;
-      }
-    }
-    __syncthreads();  // every warp is done with this step's groups before their slots are refilled
-#pragma unroll
-    for (int t = 0; t < KK; ++t) bv[t] = bn[t];
-    rc = rcn;
-  }
 }
 
 // Rows that are not interior-class (boundary rows with truncated stencils, strip-local
@@ -275,10 +158,335 @@ __global__ void __launch_bounds__(256) k_residual_rows(int64_t nrows, const int3
   }
 }
 
+// ---- L1 form: no staging.  Warp = one macro block x 32 slabs (lane = slab, its NQ
+// values in registers: one vector load per union node and lane, every coefficient
+// feeds NQ FMAs, the DG(q) combination is lane-local); the warp walks the 32-slab
+// chunks of its macro in order, the jump carry (M u)_{last slab}[q] of every row in
+// registers.  Neighbour values come through L1: the warps of a CTA take adjacent
+// macros, so the halo lines they share are read once per SM.
+template <int NQ>
+struct VT;
+template <>
+struct VT<1> {
+  using T = double;
+  static __device__ __forceinline__ T ld(const double *p) { return __ldg(p); }
+  static __device__ __forceinline__ T zero() { return 0.0; }
+  static __device__ __forceinline__ double get(const T &v, int) { return v; }
+  static __device__ __forceinline__ void st(double *p, const double (&o)[1]) { *p = o[0]; }
+};
+template <>
+struct VT<2> {
+  using T = double2;
+  static __device__ __forceinline__ T ld(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
+  static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
+  static __device__ __forceinline__ double get(const T &v, int a) { return a ? v.y : v.x; }
+  static __device__ __forceinline__ void st(double *p, const double (&o)[2]) {
+    *reinterpret_cast<double2 *>(p) = make_double2(o[0], o[1]);
+  }
+};
+template <>
+struct VT<3> {
+  using T = V3;
+  static __device__ __forceinline__ T ld(const double *p) { return V3{__ldg(p), __ldg(p + 1), __ldg(p + 2)}; }
+  static __device__ __forceinline__ T zero() { return V3{0.0, 0.0, 0.0}; }
+  static __device__ __forceinline__ double get(const T &v, int a) { return a == 0 ? v.x : a == 1 ? v.y : v.z; }
+  static __device__ __forceinline__ void st(double *p, const double (&o)[3]) {
+    p[0] = o[0];
+    p[1] = o[1];
+    p[2] = o[2];
+  }
+};
+template <>
+struct VT<4> {
+  using T = V4;
+  static __device__ __forceinline__ T ld(const double *p) {
+    return V4{__ldg(reinterpret_cast<const double2 *>(p)), __ldg(reinterpret_cast<const double2 *>(p + 2))};
+  }
+  static __device__ __forceinline__ T zero() { return V4{make_double2(0.0, 0.0), make_double2(0.0, 0.0)}; }
+  static __device__ __forceinline__ double get(const T &v, int a) {
+    return a == 0 ? v.a.x : a == 1 ? v.a.y : a == 2 ? v.b.x : v.b.y;
+  }
+  static __device__ __forceinline__ void st(double *p, const double (&o)[4]) {
+    *reinterpret_cast<double2 *>(p) = make_double2(o[0], o[1]);
+    *reinterpret_cast<double2 *>(p + 2) = make_double2(o[2], o[3]);
+  }
+};
+// rows of macro line b = 0 (part 0) or b >= 1 (part 1); K = 1 has a single part
+template <int K, class LD, class V>
+__device__ __forceinline__ void mac_accum_ld_part(int part, const LD &ld, const MacCoef &C, V (&am)[K * K],
+                                                  V (&ak)[K * K]) {
+  if constexpr (K == 1) mac_accum_ld_k1(ld, C, am, ak);
+  else if constexpr (K == 2) {
+    if (part == 0) mac_accum_ld_k2_p0(ld, C, am, ak);
+    else mac_accum_ld_k2_p1(ld, C, am, ak);
+  } else {
+    if (part == 0) mac_accum_ld_k3_p0(ld, C, am, ak);
+    else mac_accum_ld_k3_p1(ld, C, am, ak);
+  }
+}
+
+template <int K, class LD, class V>
+__device__ __forceinline__ void mac_accum_ld(const LD &ld, const MacCoef &C, V (&am)[K * K], V (&ak)[K * K]) {
+  if constexpr (K == 1) mac_accum_ld_k1(ld, C, am, ak);
+  else if constexpr (K == 2) mac_accum_ld_k2(ld, C, am, ak);
+  else mac_accum_ld_k3(ld, C, am, ak);
+}
+
+// one macro block, all time chunks; GUARD: the 3k x 3k window leaves the lattice
+template <int K, int NQ, bool GUARD>
+__device__ __forceinline__ void mac_l1_block(const MacArgs &P, int Lx, int Ly, int N, int X0, int Y0, int rc,
+                                             const double *__restrict__ u, const double *__restrict__ b,
+                                             double *__restrict__ r, int apply, int lane) {
+  using W = VT<NQ>;
+  using V = typename W::T;
+  constexpr int KK = K * K;
+  const int64_t NT = (int64_t)N * NQ;
+  const int64_t LxNT = (int64_t)Lx * NT;
+  const int nch = (N + 31) / 32;
+  double prev[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) prev[t] = 0.0;
+  // window origin (X0 - K, Y0 - K); window node (yl, xl) at element offset yl Lx NT + xl NT
+  const double *wbase = u + (int64_t)(Y0 - K) * LxNT + (int64_t)(X0 - K) * NT;
+  for (int c = 0; c < nch; ++c) {
+    const int n = 32 * c + lane;
+    const bool valid = n < N;
+    const int64_t so = (int64_t)(valid ? n : N - 1) * NQ;
+    const double *wl = wbase + so;
+    auto ld = [&](int yl, int xl) -> V {
+      if (GUARD) {
+        const int X = X0 - K + xl, Y = Y0 - K + yl;
+        if (X < 0 || Y < 0 || X >= Lx || Y >= Ly) return W::zero();
+      }
+      return W::ld(wl + (yl * LxNT + xl * NT));
+    };
+    V am[KK], ak[KK];
+#pragma unroll
+    for (int t = 0; t < KK; ++t) am[t] = ak[t] = W::zero();
+    mac_accum_ld<K>(ld, P.C, am, ak);
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      const int cls = __shfl_sync(0xffffffffu, rc, t);
+      const double lastq = W::get(am[t], NQ - 1);
+      double jmv = __shfl_up_sync(0xffffffffu, lastq, 1);
+      if (lane == 0) jmv = prev[t];
+      prev[t] = __shfl_sync(0xffffffffu, lastq, 31);
+      const int64_t ro = (int64_t)(Y0 + t / K) * LxNT + (int64_t)(X0 + t % K) * NT + so;
+      const bool inl = cls <= 0xFF;  // the row exists (partial macros at the far lattice edges)
+      const V bv = (apply || !inl) ? W::zero() : W::ld(b + ro);
+      double o[NQ];
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) {
+        double acc = W::get(bv, a);
+#pragma unroll
+        for (int c2 = 0; c2 < NQ; ++c2)
+          acc -= P.CE[a * NQ + c2] * W::get(am[t], c2) + P.Mt[a * NQ + c2] * W::get(ak[t], c2);
+        if (a == 0 && n > 0) acc += jmv;
+        o[a] = apply ? -acc : acc;
+      }
+      if (cls == 0xFF) {  // constrained row: identity
+        const V own = W::ld(u + ro);
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) o[a] = apply ? W::get(own, a) : W::get(bv, a) - W::get(own, a);
+      }
+      if (valid && inl) W::st(r + ro, o);
+    }
+  }
+}
+
+template <int K, int NQ>
+__global__ void __launch_bounds__(128, K == 3 ? 3 : 4) k_residual_mac_l1(const __grid_constant__ MacArgs P, int Lx,
+                                                                         int Ly, int N, int nmx, int64_t nmac,
+                                                                         const uint8_t *__restrict__ rcls,
+                                                                         const double *__restrict__ u,
+                                                                         const double *__restrict__ b,
+                                                                         double *__restrict__ r, int apply) {
+  constexpr int KK = K * K;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t mi = w0; mi < nmac; mi += nw) {
+    const int im = (int)(mi % nmx), jm = (int)(mi / nmx);
+    const int X0 = K * im, Y0 = K * jm;
+    int rc = 0x100;
+    if (lane < KK) {
+      const int X = X0 + lane % K, Y = Y0 + lane / K;
+      if (X < Lx && Y < Ly) rc = __ldg(rcls + (int64_t)Y * Lx + X);
+    }
+    if (X0 < K || Y0 < K || X0 + 2 * K > Lx || Y0 + 2 * K > Ly)
+      mac_l1_block<K, NQ, true>(P, Lx, Ly, N, X0, Y0, rc, u, b, r, apply, lane);
+    else
+      mac_l1_block<K, NQ, false>(P, Lx, Ly, N, X0, Y0, rc, u, b, r, apply, lane);
+  }
+}
+
+template <int K, int NQ>
+bool mac_l1_launch(const Level &L, int N, const MacArgs &P, const double *u, const double *b, double *r, int apply,
+                   cudaStream_t s) {
+  const int nmx = (L.Lx + K - 1) / K, nmy = (L.Ly + K - 1) / K;
+  const int64_t nmac = (int64_t)nmx * nmy;
+  const int64_t blocks = (nmac + 3) / 4;
+  const int grid = (int)std::min<int64_t>(blocks, (int64_t)(K == 3 ? 3 : 4) * num_sms());
+  k_residual_mac_l1<K, NQ><<<grid, 128, 0, s>>>(P, L.Lx, L.Ly, N, nmx, nmac, L.rcls, u, b, r, apply);
+  ++g_launches;
+  return true;
+}
+
+// ---- TMA form.  Warp = two adjacent macro blocks x 16 slabs (lane = (macro h, slab):
+// half-warp h, its NQ values in registers); CTA = MX macro columns x JS macro rows,
+// walking 16-slab chunks (outer) and macro rows (inner); u arrives in groups of k
+// node lines x (k MX + 2k) nodes x 16 slabs through a ring of R TMA boxes (one
+// mbarrier per slot), R - 3 macro rows ahead.  Each union value is one LDS of NQ
+// doubles from the staged window; the coefficients are constant-bank operands,
+// each feeding NQ FMAs.
+// One macro-row step of k_residual_mac for the rows [T0, T1) of the half-warp's macro
+// (PART: compile-time row set, so only its accumulators are live).
+template <int K, int NQ, int MX, int R, int PART>
+__device__ __forceinline__ void mac_step(const MacArgs &P, double *ring, uint64_t *full, double *prevq, int Lx,
+                                         int Ly, int64_t NT, int JS, const uint8_t *__restrict__ rcls,
+                                         const double *__restrict__ b, double *__restrict__ r, int apply, int c,
+                                         int jj, int jm, int lo, int im, int mloc, int sl, int N, bool active) {
+  using W = VT<NQ>;
+  using V = typename W::T;
+  constexpr int SPC = 16;
+  constexpr int VPC = SPC * NQ;
+  constexpr int RWX = K * MX + 2 * K;
+  constexpr int GROUP = K * RWX * VPC;
+  constexpr int KK = K * K;
+  constexpr int T0 = (K == 1 || PART == 0) ? 0 : K, T1 = (K == 1 || PART == 1) ? KK : K;
+  const int n = c * SPC + sl;
+  const bool valid = n < N;
+  const int64_t tg = (int64_t)(valid ? n : N - 1) * NQ;
+    // row classes (lane t of each half: row t) and b, issued before the wait
+    int rc = 0x100;
+    if (active && sl < KK) {
+      const int X = K * im + sl % K, Y = K * jm + sl / K;
+      if (X < Lx && Y < Ly) rc = __ldg(rcls + (int64_t)Y * Lx + X);
+    }
+    V bv[KK];
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      const int X = K * im + t % K, Y = K * jm + t / K;
+      bv[t] = (t >= T0 && t < T1 && active && !apply && X < Lx && Y < Ly)
+                  ? W::ld(b + ((int64_t)Y * Lx + X) * NT + tg)
+                  : W::zero();
+    }
+#pragma unroll
+    for (int g = 0; g < 3; ++g) mbar_wait(&full[(lo + g) % R], (unsigned)(((lo + g) / R) & 1));
+    {
+      const double *gp[3];
+#pragma unroll
+      for (int g = 0; g < 3; ++g) gp[g] = ring + (size_t)((lo + g) % R) * GROUP + (K * mloc) * VPC + sl * NQ;
+      auto ld = [&](int yl, int xl) -> V {  // window line yl = dy + K, column xl = dx + K
+        const double *p = gp[yl / K] + ((yl % K) * RWX + xl) * VPC;
+        if constexpr (NQ == 2) return *reinterpret_cast<const double2 *>(p);
+        else if constexpr (NQ == 1) return *p;
+        else return W::ld(p);
+      };
+      V am[KK], ak[KK];
+#pragma unroll
+      for (int t = 0; t < KK; ++t) am[t] = ak[t] = W::zero();
+      mac_accum_ld_part<K>(PART, ld, P.C, am, ak);
+      const double *pqr = prevq + (((size_t)(c & 1) * MX + mloc) * JS + jj) * KK;
+      double *pqw = prevq + (((size_t)((c + 1) & 1) * MX + mloc) * JS + jj) * KK;
+#pragma unroll
+      for (int t = 0; t < KK; ++t) {
+        if (t < T0 || t >= T1) continue;  // compile time: the other part's rows
+        const int cls = __shfl_sync(0xffffffffu, rc, t, 16);
+        const double lastq = W::get(am[t], NQ - 1);
+        double jmv = __shfl_up_sync(0xffffffffu, lastq, 1, 16);
+        if (sl == 0) jmv = pqr[t];
+        if (sl == SPC - 1) pqw[t] = lastq;
+        double o[NQ];
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) {
+          double acc = W::get(bv[t], a);
+#pragma unroll
+          for (int c2 = 0; c2 < NQ; ++c2)
+            acc -= P.CE[a * NQ + c2] * W::get(am[t], c2) + P.Mt[a * NQ + c2] * W::get(ak[t], c2);
+          if (a == 0 && n > 0) acc += jmv;
+          o[a] = apply ? -acc : acc;
+        }
+        if (cls == 0xFF) {  // constrained row: identity
+          const V own = ld(t / K + K, t % K + K);
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) o[a] = apply ? W::get(own, a) : W::get(bv[t], a) - W::get(own, a);
+        }
+        const int X = K * im + t % K, Y = K * jm + t / K;
+        if (active && valid && cls <= 0xFF) W::st(r + ((int64_t)Y * Lx + X) * NT + tg, o);
+      }
+    }
+}
+
+template <int K, int NQ, int MX, int R>
+__global__ void __launch_bounds__(16 * MX * (K > 1 ? 2 : 1)) k_residual_mac(const __grid_constant__ CUtensorMap umap,
+                                                          const __grid_constant__ MacArgs P, int Lx, int Ly,
+                                                          int64_t NT, int nstrips, int nmy, int JS,
+                                                          const uint8_t *__restrict__ rcls,
+                                                          const double *__restrict__ b, double *__restrict__ r,
+                                                          int apply) {
+  using W = VT<NQ>;
+  using V = typename W::T;
+  constexpr int SPC = 16;              // slabs per chunk
+  constexpr int VPC = SPC * NQ;        // values per node and chunk
+  constexpr int RWX = K * MX + 2 * K;  // staged window width (nodes)
+  constexpr int GROUP = K * RWX * VPC; // doubles per group of K node lines
+  constexpr int KK = K * K;
+  constexpr int LA = R - 3;            // macro rows of TMA lookahead
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[R];
+  double *prevq = ring + R * GROUP;  // [2][MX][JS][KK]: (M u)_{last slab}[q] of the previous chunk (by parity)
+  constexpr int NPART = K > 1 ? 2 : 1;  // warps per macro pair: rows of line b = 0 / lines b >= 1
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int part = w % NPART, pw = w / NPART;
+  const int h = lane >> 4, sl = lane & 15;
+  const int strip = blockIdx.x % nstrips, seg = blockIdx.x / nstrips;
+  const int j0 = seg * JS, ns = min(nmy, j0 + JS) - j0;  // macro rows of this segment
+  const int x0 = K * MX * strip;                           // first node column of the strip
+  const int mloc = 2 * pw + h;                             // this half-warp's macro within the strip
+  const int im = MX * strip + mloc;
+  const int ngrp = ns + 2;                                 // line groups per chunk (halo groups included)
+  const int N = (int)(NT / NQ);
+  const int nch = (N + SPC - 1) / SPC;
+  const int nsteps = nch * ns;
+  if (ns <= 0) return;
+  if (tid == 0) {
+    for (int z = 0; z < R; ++z) mbar_init(&full[z], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int e = tid; e < 2 * MX * JS * KK; e += blockDim.x) prevq[e] = 0.0;
+  __syncthreads();
+  constexpr unsigned kBytes = (unsigned)(GROUP * sizeof(double));
+  auto issue = [&](int F) {
+    const int c = F / ngrp, g = F - c * ngrp, z = F % R;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect_tx(&full[z], kBytes);
+    tma_load_3d(ring + (size_t)z * GROUP, &umap, c * VPC, x0 - K, K * (j0 + g - 1), &full[z]);
+  };
+  int issued = 0;  // groups issued so far (thread 0's bookkeeping)
+  const bool active = im * K < Lx;
+  for (int s = 0; s < nsteps; ++s) {
+    const int c = s / ns, jj = s - c * ns, jm = j0 + jj;
+    const int lo = c * ngrp + jj;  // first of the three groups of this step
+    if (tid == 0) {  // keep the ring up to LA macro rows ahead, as far as free slots allow
+      const int st = min(nsteps - 1, s + LA);
+      const int hi = (st / ns) * ngrp + (st - (st / ns) * ns) + 2;
+      while (issued <= hi && issued - R < lo) issue(issued++);
+    }
+    if (part == 0)
+      mac_step<K, NQ, MX, R, 0>(P, ring, full, prevq, Lx, Ly, NT, JS, rcls, b, r, apply, c, jj, jm, lo, im, mloc, sl, N,
+                                active);
+    else
+      mac_step<K, NQ, MX, R, 1>(P, ring, full, prevq, Lx, Ly, NT, JS, rcls, b, r, apply, c, jj, jm, lo, im, mloc, sl, N,
+                                active);
+    __syncthreads();  // every warp is done with this step's groups before their slots are refilled
+  }
+}
+
 template <int K, int NQ, int MX, int R>
 bool mac_launch(const Level &L, int N, const MacArgs &P, const double *u, const double *b, double *r, int apply,
                 cudaStream_t s) {
-  constexpr int VPC = NQ * (32 / NQ);
+  constexpr int VPC = 16 * NQ;
   constexpr int RWX = K * MX + 2 * K;
   const int64_t NT = (int64_t)N * NQ;
   CUtensorMap umap;
@@ -291,9 +499,9 @@ bool mac_launch(const Level &L, int N, const MacArgs &P, const double *u, const 
   const int JS = (nmy + nseg - 1) / nseg;
   nseg = (nmy + JS - 1) / JS;
   const size_t smem = ((size_t)R * K * RWX * VPC + (size_t)2 * MX * JS * K * K) * sizeof(double);
-  if (smem > 220 * 1024) return false;
+  if (smem > 200 * 1024) return false;
   smem_optin((const void *)k_residual_mac<K, NQ, MX, R>, (int)smem);
-  k_residual_mac<K, NQ, MX, R><<<nstrips * nseg, 32 * MX, smem, s>>>(umap, P, L.Lx, L.Ly, NT, nstrips, nmy, JS,
+  k_residual_mac<K, NQ, MX, R><<<nstrips * nseg, 16 * MX * (K > 1 ? 2 : 1), smem, s>>>(umap, P, L.Lx, L.Ly, NT, nstrips, nmy, JS,
                                                                         L.rcls, b, r, apply);
   ++g_launches;
   return true;
@@ -326,12 +534,26 @@ bool launch_residual_mac(const Level &L, int k, int q, int N, const Temporal &tm
     P.Mt[e] = tm.Mt[e];
   }
   bool ok = false;
-#define WRMG_MAC(KK_, NQ_, MX_, R_)                                   \
+  static const bool l1 = [] {  // WRMG_RESIDUAL=macl1: the L1 macro kernel (A/B)
+    const char *e = getenv("WRMG_RESIDUAL");
+    return e && std::string(e) == "macl1";
+  }();
+  if (!l1) {
+#define WRMG_MAC(KK_, NQ_, MX_, R_) \
   if (k == KK_ && q + 1 == NQ_) ok = mac_launch<KK_, NQ_, MX_, R_>(L, N, P, u, b, r, apply, s);
-  WRMG_MAC(1, 1, 8, 12) WRMG_MAC(1, 2, 8, 12) WRMG_MAC(1, 3, 8, 12) WRMG_MAC(1, 4, 8, 12)
-  WRMG_MAC(2, 1, 8, 8) WRMG_MAC(2, 2, 8, 8) WRMG_MAC(2, 3, 8, 8) WRMG_MAC(2, 4, 8, 8)
-  WRMG_MAC(3, 1, 4, 7) WRMG_MAC(3, 2, 4, 7) WRMG_MAC(3, 3, 4, 7) WRMG_MAC(3, 4, 4, 7)
+    WRMG_MAC(1, 1, 16, 8) WRMG_MAC(1, 2, 16, 8) WRMG_MAC(1, 3, 16, 8) WRMG_MAC(1, 4, 16, 8)
+    WRMG_MAC(2, 1, 8, 5) WRMG_MAC(2, 2, 8, 5) WRMG_MAC(2, 3, 8, 5) WRMG_MAC(2, 4, 8, 4)
+    WRMG_MAC(3, 1, 8, 4) WRMG_MAC(3, 2, 8, 4)
 #undef WRMG_MAC
+  }
+  if (!ok) {
+#define WRMG_MACL1(KK_, NQ_) \
+  if (k == KK_ && q + 1 == NQ_) ok = mac_l1_launch<KK_, NQ_>(L, N, P, u, b, r, apply, s);
+    WRMG_MACL1(1, 1) WRMG_MACL1(1, 2) WRMG_MACL1(1, 3) WRMG_MACL1(1, 4)
+    WRMG_MACL1(2, 1) WRMG_MACL1(2, 2) WRMG_MACL1(2, 3) WRMG_MACL1(2, 4)
+    WRMG_MACL1(3, 1) WRMG_MACL1(3, 2) WRMG_MACL1(3, 3)
+#undef WRMG_MACL1
+  }
   if (!ok) return false;
   if (L.ngen_rows > 0) {
     switch (q) {

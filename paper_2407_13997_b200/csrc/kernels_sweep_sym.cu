@@ -164,13 +164,53 @@ __device__ __forceinline__ void sym_block(const SymTab &P, double (&y)[NQ][MP], 
     }
 }
 
+// One patch x one 32-slab chunk: gather, y = U^T g, the four character blocks
+// (end-trace carry in ycar), x = U y, handed to emit(a, x[slot]) one temporal node
+// at a time (short live ranges).
+template <int K, int NQ, class EMIT>
+__device__ __forceinline__ void sym_patch_chunk(const SymTab &P, const int *snode, double *ycar, int n, bool valid,
+                                                int64_t NT, const double *__restrict__ r, int lane,
+                                                const EMIT &emit) {
+  using S = Sh<K>;
+  constexpr int MP = S::MP;
+  double y[NQ][MP];
+  {  // gather (slot order) and y = U^T g
+    double g[NQ][MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) {
+      const double *src = r + (int64_t)snode[j] * NT + (int64_t)n * NQ;
+      if constexpr (NQ == 2) {
+        const double2 v = valid ? __ldg(reinterpret_cast<const double2 *>(src)) : make_double2(0.0, 0.0);
+        g[0][j] = v.x;
+        g[1][j] = v.y;
+      } else {
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) g[a][j] = valid ? __ldg(src + a) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) sym_fwd<K>(g[a], y[a]);
+  }
+  sym_block<S::D0, S::B0, S::V0, S::B0, NQ, MP>(P, y, ycar, lane);
+  sym_block<S::D1, S::B1, S::V1, S::B1, NQ, MP>(P, y, ycar, lane);
+  sym_block<S::D2, S::B2, S::V2, S::B2, NQ, MP>(P, y, ycar, lane);
+  sym_block<S::D3, S::B3, S::V3, S::B3, NQ, MP>(P, y, ycar, lane);
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double x[MP];
+    sym_bwd<K>(y[a], x);
+    emit(a, x);
+  }
+}
+
+// Patches one per warp, FP64 atomics for the weighted additive scatter.
 template <int K, int NQ>
-__global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, const int32_t *__restrict__ pnodes,
+__global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, const int32_t *__restrict__ list,
+                                                      const int32_t *__restrict__ pnodes,
                                                       const __grid_constant__ SymTab P,
                                                       const double *__restrict__ wnode, double omega,
                                                       const double *__restrict__ r, double *__restrict__ u) {
-  using S = Sh<K>;
-  constexpr int MP = S::MP;
+  constexpr int MP = Sh<K>::MP;
   constexpr int WPC = 4;
   __shared__ int snode[WPC][MP];
   __shared__ double swt[WPC][MP];
@@ -178,7 +218,8 @@ __global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, con
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t NT = (int64_t)N * NQ;
   const int nch = (N + 31) / 32;
-  for (int64_t p = (int64_t)blockIdx.x * WPC + w; p < npatch; p += (int64_t)gridDim.x * WPC) {
+  for (int64_t i = (int64_t)blockIdx.x * WPC + w; i < npatch; i += (int64_t)gridDim.x * WPC) {
+    const int64_t p = list ? list[i] : i;
     __syncwarp();
     if (lane < MP) {
       const int nd = __ldg(pnodes + p * MP + lane);
@@ -190,49 +231,110 @@ __global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, con
     for (int ch = 0; ch < nch; ++ch) {
       const int n = 32 * ch + lane;
       const bool valid = n < N;
-      double y[NQ][MP];
-      {  // gather (slot order) and y = U^T g
-        double g[NQ][MP];
-#pragma unroll
-        for (int j = 0; j < MP; ++j) {
-          const double *src = r + (int64_t)snode[w][j] * NT + (int64_t)n * NQ;
-          if constexpr (NQ == 2) {
-            const double2 v = valid ? __ldg(reinterpret_cast<const double2 *>(src)) : make_double2(0.0, 0.0);
-            g[0][j] = v.x;
-            g[1][j] = v.y;
-          } else {
-#pragma unroll
-            for (int a = 0; a < NQ; ++a) g[a][j] = valid ? __ldg(src + a) : 0.0;
-          }
-        }
-#pragma unroll
-        for (int a = 0; a < NQ; ++a) sym_fwd<K>(g[a], y[a]);
-      }
-      sym_block<S::D0, S::B0, S::V0, S::B0, NQ, MP>(P, y, sycar[w], lane);
-      sym_block<S::D1, S::B1, S::V1, S::B1, NQ, MP>(P, y, sycar[w], lane);
-      sym_block<S::D2, S::B2, S::V2, S::B2, NQ, MP>(P, y, sycar[w], lane);
-      sym_block<S::D3, S::B3, S::V3, S::B3, NQ, MP>(P, y, sycar[w], lane);
-      // x = U y and the weighted additive scatter
-#pragma unroll
-      for (int a = 0; a < NQ; ++a) {
-        double x[MP];
-        sym_bwd<K>(y[a], x);
+      sym_patch_chunk<K, NQ>(P, snode[w], sycar[w], n, valid, NT, r, lane, [&](int a, const double(&x)[MP]) {
         if (valid) {
 #pragma unroll
           for (int j = 0; j < MP; ++j)
             atomicAdd(u + (int64_t)snode[w][j] * NT + (int64_t)n * NQ + a, swt[w][j] * x[j]);
         }
+      });
+    }
+  }
+}
+
+// 2 x 2 vertex tiles (CTA = 4 warps = 4 patches): the patches' corrections meet in
+// shared memory, each union node of the tile is written once per chunk as 32 NQ
+// contiguous doubles -- plain read-modify-write for nodes no other tile touches,
+// FP64 atomics for the tile's boundary nodes (k = 3: 42 atomic + 16 plain node
+// updates instead of 76 atomic ones).
+template <int K, int NQ>
+__global__ void __launch_bounds__(128, 3) k_sweep_sym_tile(int N, int64_t ntile, const int32_t *__restrict__ tiles,
+                                                           const int32_t *__restrict__ pnodes,
+                                                           const __grid_constant__ SymTab P,
+                                                           const TileGeom *__restrict__ Tg,
+                                                           const double *__restrict__ wnode, double omega,
+                                                           const double *__restrict__ r, double *__restrict__ u) {
+  constexpr int MP = Sh<K>::MP;
+  constexpr int VC = 32 * NQ;  // doubles per node and chunk
+  __shared__ int snode[4][MP];
+  __shared__ double sycar[4][MP];
+  __shared__ int32_t toff[kTileMaxU];
+  __shared__ int16_t tsrc[kTileMaxU][4];
+  __shared__ uint8_t tcnt[kTileMaxU], tint[kTileMaxU];
+  extern __shared__ __align__(16) double acc_dyn[];  // [4][MP][VC]
+  double(*acc)[MP][VC] = reinterpret_cast<double(*)[MP][VC]>(acc_dyn);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t NT = (int64_t)N * NQ;
+  const int nch = (N + 31) / 32;
+  const int nu = Tg->nu;
+  for (int e = threadIdx.x; e < nu; e += blockDim.x) {  // tile geometry into shared memory
+    toff[e] = Tg->off[e];
+    tcnt[e] = Tg->cnt[e];
+    tint[e] = Tg->interior[e];
+    for (int q = 0; q < 4; ++q) tsrc[e][q] = Tg->src[e][q];
+  }
+  for (int64_t tl = blockIdx.x; tl < ntile; tl += gridDim.x) {
+    __syncthreads();
+    const int64_t p = tiles[tl * 4 + w];
+    if (lane < MP) {
+      snode[w][lane] = __ldg(pnodes + p * MP + lane);
+      sycar[w][lane] = 0.0;
+    }
+    __syncthreads();
+    // tile base node: the node of union offset 0 relative position, from patch 0's first slot
+    const int64_t base = (int64_t)snode[0][tsrc[0][0] % MP] - toff[0];
+    for (int ch = 0; ch < nch; ++ch) {
+      const int n = 32 * ch + lane;
+      const bool valid = n < N;
+      sym_patch_chunk<K, NQ>(P, snode[w], sycar[w], n, valid, NT, r, lane, [&](int a, const double(&x)[MP]) {
+#pragma unroll
+        for (int j = 0; j < MP; ++j) acc[w][j][lane * NQ + a] = x[j];
+      });
+      __syncthreads();
+      const int64_t t0 = (int64_t)ch * VC;  // first time value of the chunk
+      for (int uu = w; uu < nu; uu += 4) {
+        const int64_t node = base + toff[uu];
+        const double wt = omega * __ldg(wnode + node);
+        const int cnt = tcnt[uu];
+        const bool inner = tint[uu];
+        double *dst = u + node * NT + t0;
+#pragma unroll
+        for (int e = 0; e < NQ; ++e) {
+          const int idx = lane + 32 * e;
+          double v = 0.0;
+          for (int q = 0; q < cnt; ++q) {
+            const int sw = tsrc[uu][q];
+            v += acc[sw / MP][sw % MP][idx];
+          }
+          if (t0 + idx < NT) {
+            if (inner) dst[idx] += wt * v;
+            else atomicAdd(dst + idx, wt * v);
+          }
+        }
       }
+      __syncthreads();
     }
   }
 }
 
 template <int K, int NQ>
 void sym_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
-  const int64_t nblk = (L.nsym + 3) / 4;
-  const int grid = (int)std::min<int64_t>(nblk, (int64_t)6 * num_sms());
-  k_sweep_sym<K, NQ><<<grid, 128, 0, s>>>(N, L.nsym, L.sym_nodes, L.symtab, L.wnode, omega, r, u);
-  ++g_launches;
+  if (L.ntile > 0) {
+    const int grid = (int)std::min<int64_t>(L.ntile, (int64_t)6 * num_sms());
+    const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
+    smem_optin((const void *)k_sweep_sym_tile<K, NQ>, smem);
+    k_sweep_sym_tile<K, NQ><<<grid, 128, smem, s>>>(N, L.ntile, L.tile_patch, L.sym_nodes, L.symtab, L.tgeo_dev, L.wnode,
+                                                  omega, r, u);
+    ++g_launches;
+  }
+  const int64_t np = L.ntile > 0 ? L.nsingle : L.nsym;
+  if (np > 0) {
+    const int64_t nblk = (np + 3) / 4;
+    const int grid = (int)std::min<int64_t>(nblk, (int64_t)6 * num_sms());
+    k_sweep_sym<K, NQ><<<grid, 128, 0, s>>>(N, np, L.ntile > 0 ? L.sym_single : nullptr, L.sym_nodes, L.symtab,
+                                            L.wnode, omega, r, u);
+    ++g_launches;
+  }
 }
 
 }  // namespace

@@ -15,6 +15,33 @@ __device__ __forceinline__ long long hashpos(long long w) {  // spread warps ove
   return (long long)(z % (unsigned long long)((kN - 64) / 64)) * 64;
 }
 
+// bulk reduction (TMA): each warp stages 64 doubles (512 B) in shared memory and one lane
+// issues cp.reduce.async.bulk .add.f64 of the whole segment (UBLKRED), double-buffered
+__global__ void kbulk(double *u, long long nwarp_ops) {
+  __shared__ __align__(128) double buf[8][2][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  int it = 0;
+  for (long long wi = w0; wi < nwarp_ops; wi += nw, ++it) {
+    const long long base = hashpos(wi);
+    double *b = buf[w][it & 1];
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+    b[2 * lane] = 1.0;
+    b[2 * lane + 1] = 1.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], 512;" ::"l"(u + base),
+                   "r"((unsigned)__cvta_generic_to_shared(b))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int MODE>
 __global__ void k(double *u, long long nwarp_ops) {
   const int lane = threadIdx.x & 31;
@@ -46,13 +73,15 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const long long nwarp_ops = kOps / 64;  // 64 element updates per warp iteration
-  const char *names[3] = {"red_f64_stride16B(sweep pattern)", "red_f64_contiguous", "ld_add_st_rmw"};
-  for (int mode = 0; mode < 3; ++mode)
+  const char *names[4] = {"red_f64_stride16B(sweep pattern)", "red_f64_contiguous", "ld_add_st_rmw",
+                          "bulk_reduce_512B(UBLKRED)"};
+  for (int mode = 0; mode < 4; ++mode)
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
       if (mode == 0) k<0><<<148 * 8, 256>>>(u, nwarp_ops);
       if (mode == 1) k<1><<<148 * 8, 256>>>(u, nwarp_ops);
       if (mode == 2) k<2><<<148 * 8, 256>>>(u, nwarp_ops);
+      if (mode == 3) kbulk<<<148 * 8, 256>>>(u, nwarp_ops);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;

@@ -86,6 +86,40 @@ def emit(k, out):
         out.append("  }")
     out.append("}")
     out.append("")
+    # L1 variant: values through a loader functor ld(line, column) of the (3k lines) x (3k columns)
+    # window around the macro (line = dy + k, column = dx + k), any value type V with vfma
+    out.append("template <class LD, class Coef, class V>")
+    out.append(f"__device__ __forceinline__ void mac_accum_ld_k{k}(const LD &ld, const Coef &C, "
+               f"V (&am)[{k * k}], V (&ak)[{k * k}]) {{")
+    for (x, y) in order:
+        out.append(f"  {{ const V v = ld({y + k}, {x + k});")
+        for (t, idx) in users[(x, y)]:
+            out.append(f"    vfma(am[{t}], C.m[{idx}], v); vfma(ak[{t}], C.k[{idx}], v);")
+        out.append("  }")
+    out.append("}")
+    out.append("")
+    # row-split variant: part 0 = the rows of macro line b = 0, part 1 = lines b >= 1 (two
+    # warps share a macro block; each loads only the union of its own rows' stencils)
+    if k > 1:
+        for part in (0, 1):
+            rows = [t for t, (a, b) in enumerate(types) if (b == 0) == (part == 0)]
+            sub = {}
+            for t in rows:
+                a, b = types[t]
+                for e, (dx, dy) in enumerate(st[t]):
+                    sub.setdefault((a + dx, b + dy), []).append((t, base[t] + e))
+            sorder = sorted(sub, key=lambda p: (p[1], p[0]))
+            out.append(f"// part {part}: rows {rows}, {len(sorder)} distinct nodes")
+            out.append("template <class LD, class Coef, class V>")
+            out.append(f"__device__ __forceinline__ void mac_accum_ld_k{k}_p{part}(const LD &ld, const Coef &C, "
+                       f"V (&am)[{k * k}], V (&ak)[{k * k}]) {{")
+            for (x, y) in sorder:
+                out.append(f"  {{ const V v = ld({y + k}, {x + k});")
+                for (t, idx) in sub[(x, y)]:
+                    out.append(f"    vfma(am[{t}], C.m[{idx}], v); vfma(ak[{t}], C.k[{idx}], v);")
+                out.append("  }")
+            out.append("}")
+            out.append("")
 
 
 def main():
