@@ -469,7 +469,7 @@ def run_gpu(args, ws, rank, local):
         dist.broadcast(idt, 0)
         kw = dict(rank=rank, nranks=ws, nccl_id=bytes(idt.cpu().numpy().tobytes()))
     ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N, kappa=CFG["kappa"], device=local,
-                    stream=stream.cuda_stream, **kw)
+                    stream=stream.cuda_stream, scatter=args.scatter, **kw)
     lay = ctx.layout
     ndof = lay["ndof"]
     fhat = ctx.empty()
@@ -644,7 +644,8 @@ def run_gpu(args, ws, rank, local):
                        "ndof": ndof, "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
                        "parallelism": (f"{ws} spatial strips of the one C2 problem (NCCL halos; levels narrower "
                                        f"than 2 cells per strip replicated)") if ws > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 (303 MB vectors vs 126 MB L2); no flush"},
+                       "l2": "inputs larger than L2 (303 MB vectors vs 126 MB L2); no flush",
+                       "scatter": args.scatter},
             "fgmres_iterations": its_list[0], "final_relres": rels[-1],
             "vcycle_ms": vcycle_ms, "smoother_sweep_ms": sweep_ms,
             "smoother_sweep_dof_updates_per_s": lay["nfree_st"] / (sweep_ms / 1e3),
@@ -669,6 +670,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C5"])
     ap.add_argument("--c5-n", type=int, default=1024, help="C5 cells per side per GPU (1024 = the config)")
+    ap.add_argument("--scatter", default="atomic", choices=["atomic", "colour"],
+                    help="weighted additive scatter of the heat sweep (H8): FP64 atomics or coloured passes")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args) if args.impl == "wrmg" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)

@@ -86,8 +86,14 @@ typedef struct {
                            linearisation, DESIGN.md R-cheb; single rank) */
   int32_t cheb_steps;   /* Arnoldi steps of the lambda estimate (0 -> 50, <= 63) */
   uint64_t cheb_seed;   /* seed of the Arnoldi start vector (R6 generator at canonical ids) */
+  int32_t scatter;      /* weighted additive scatter (H8) of the heat sweep in factor_mode AUTO:
+                           WRMG_SCATTER_ATOMIC (default; FP64 atomics, order of the <= mu_max additions per
+                           value unspecified) | WRMG_SCATTER_COLOUR (three passes, one per vertex colour
+                           (i - j) mod 3 -- patches of one colour share no DoF -- so every value receives one
+                           addition per pass in a fixed order: bitwise reproducible) */
 } wrmg_coeffs;
 enum { WRMG_SMOOTH_DAMPED = 0, WRMG_SMOOTH_CHEBYSHEV = 1 };
+enum { WRMG_SCATTER_ATOMIC = 0, WRMG_SCATTER_COLOUR = 1 };
 
 typedef struct {
   int64_t nnode;        /* lattice nodes of the finest level owned by this rank */

@@ -190,6 +190,15 @@ void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
     ns_project(c, L, u);
     return;
   }
+  if (c->use_kron && c->lv[l].coloured) {  // one pass per vertex colour: one addition per value and pass
+    const Level &L = c->lv[l];
+    for (int cc = 0; cc < 3; ++cc) {
+      launch_sweep_sym(L, c->k, c->q, c->N, r, u, om, c->stream, &L.col[cc]);
+      if (!launch_sweep_kron(L, c->q, c->N, r, u, om, c->stream, &L.col[cc]))
+        throw Err{WRMG_E_UNSUPPORTED, "coloured scatter: no Kronecker sweep for this level"};
+    }
+    return;
+  }
   if (c->use_kron) {
     const Level &L = c->lv[l];
     const bool sym = launch_sweep_sym(L, c->k, c->q, c->N, r, u, om, c->stream);
@@ -212,6 +221,10 @@ void free_level(Level &L) {
                   (void *)L.hx[2], (void *)L.hx[3], (void *)L.gen_rows, (void *)L.sym_nodes,
                   (void *)L.tile_patch, (void *)L.sym_single, (void *)L.tgeo_dev})
     dfree(p);
+  for (auto &S : L.col)
+    for (void *p : {(void *)S.cta_patch, (void *)S.cta_type, (void *)S.grp_patch8, (void *)S.grp_type8,
+                    (void *)S.sym_list})
+      dfree(p);
 }
 
 void validate(const wrmg_mesh *mesh, int degree, int q, int nslabs, double dt) {
@@ -361,9 +374,9 @@ bool sym_disabled() {  // WRMG_SWEEP_SYM=0: every class through kernels_kron.cu 
   const char *e = getenv("WRMG_SWEEP_SYM");
   return e && e[0] == '0';
 }
-bool tiles_disabled() {  // WRMG_SWEEP_TILES=0: symmetric patches one per warp with atomics only (A/B)
+bool tiles_disabled() {  // WRMG_SWEEP_TILES=1: the 2 x 2 tiled symmetric sweep (measured slower)
   const char *e = getenv("WRMG_SWEEP_TILES");
-  return e && e[0] == '0';
+  return !(e && e[0] == '1');
 }
 
 // 2 x 2 tiles of symmetric-class patches (even vertex coordinates) for the tiled
@@ -1418,6 +1431,41 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         L.kron_ngrp8 = (int)ct.size();
         L.grp_patch8 = dupload(cp, s);
         L.grp_type8 = dupload(ct, s);
+        if (coeffs->scatter == WRMG_SCATTER_COLOUR) {  // per-colour work lists (deterministic scatter)
+          std::vector<uint8_t> pc(P.npatch);
+          for (int64_t p = 0; p < P.npatch; ++p) {
+            const int vi = P.pvert[p] % (P.nx + 1) + L.st.cx0, vj = P.pvert[p] / (P.nx + 1);
+            pc[p] = (uint8_t)(((vi - vj) % 3 + 3) % 3);
+          }
+          for (int cc = 0; cc < 3; ++cc) {
+            SweepLists &S = L.col[cc];
+            plan_sweep_ctas(P, pp, cp, ct, ex, &pc, cc);
+            S.pp = pp;
+            S.ncta = (int)ct.size();
+            if (S.ncta) {
+              S.cta_patch = dupload(cp, s);
+              S.cta_type = dupload(ct, s);
+            }
+            plan_sweep_ctas(P, 8, cp, ct, ex, &pc, cc);
+            S.ngrp8 = (int)ct.size();
+            if (S.ngrp8) {
+              S.grp_patch8 = dupload(cp, s);
+              S.grp_type8 = dupload(ct, s);
+            }
+            if (L.sym_ok) {
+              std::vector<int32_t> sl;
+              int32_t qi = 0;
+              for (int64_t p = 0; p < P.npatch; ++p)
+                if (P.ptype[p] == L.sym_cls) {
+                  if (pc[p] == cc) sl.push_back(qi);
+                  ++qi;
+                }
+              S.nsym = (int64_t)sl.size();
+              if (S.nsym) S.sym_list = dupload(sl, s);
+            }
+          }
+          L.coloured = true;
+        }
       }
       {
         // algorithmic flops of one sweep, per (patch, slab), of the solve the path runs:

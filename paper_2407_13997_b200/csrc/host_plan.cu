@@ -145,11 +145,12 @@ void plan_level(int nx, int ny, double h, int k, PlanLevel *P, bool neumann) {
 }
 
 void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type,
-                     int exclude) {
+                     int exclude, const std::vector<uint8_t> *colour, int want) {
   cta_patch.clear();
   cta_type.clear();
   std::vector<std::vector<int32_t>> by(P.ntypes);
-  for (int64_t p = 0; p < P.npatch; ++p) by[P.ptype[p]].push_back((int32_t)p);
+  for (int64_t p = 0; p < P.npatch; ++p)
+    if (!colour || (*colour)[p] == want) by[P.ptype[p]].push_back((int32_t)p);
   for (int t = 0; t < P.ntypes; ++t)
     if (t != exclude)
     for (size_t s = 0; s < by[t].size(); s += pp) {

@@ -88,6 +88,18 @@ struct TileGeom {
   int16_t src[kTileMaxU][4];  // w * MP + slot
 };
 
+// Work lists of one sweep pass (coloured scatter: one per vertex colour (i - j) mod 3,
+// whose patches share no node, so each value receives one addition per pass and the
+// sweep is bitwise deterministic).
+struct SweepLists {
+  int ncta = 0, pp = 1;
+  int32_t *cta_patch = nullptr, *cta_type = nullptr;   // k_sweep_kron
+  int ngrp8 = 0;
+  int32_t *grp_patch8 = nullptr, *grp_type8 = nullptr; // k_sweep_kron_mma
+  int64_t nsym = 0;
+  int32_t *sym_list = nullptr;                          // k_sweep_sym (indices into sym_nodes)
+};
+
 // Spatial strip of a level on this rank (host_strip.cu).
 struct StripInfo {
   int rank = 0, nranks = 1;
@@ -161,6 +173,8 @@ struct Level {
   int32_t *sym_single = nullptr;    // sym patches outside complete tiles
   TileGeom tgeo{};
   TileGeom *tgeo_dev = nullptr;
+  bool coloured = false;            // WRMG_SCATTER_COLOUR: per-colour work lists below
+  SweepLists col[3];
   // transfer from this level to the next finer (stored on the coarse side)
   DevCSR P;    // rows: fine nodes, cols: coarse nodes
   DevCSR R;    // rows: coarse nodes, cols: fine nodes (R = P^T, same doubles)
@@ -301,8 +315,9 @@ void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const do
 void launch_kron_setup(const Level &L, int nq, const Temporal &tm, double *scratch, cudaStream_t s);
 void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal &tm, double *scratch, cudaStream_t s);
 bool launch_sweep_sym(const Level &L, int k, int q, int N, const double *r, double *u, double omega,
-                      cudaStream_t s);
-bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s);
+                      cudaStream_t s, const SweepLists *sl = nullptr);
+bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s,
+                       const SweepLists *sl = nullptr);
 void launch_coarse_solve_kron(const Coarse &C, const Level &L, int q, int N, const double *r, double *x,
                               cudaStream_t s);
 void launch_gather_classes(const Level &L, int32_t *scratch_i, double *scratch_d, cudaStream_t s);

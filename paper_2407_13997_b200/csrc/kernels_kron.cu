@@ -600,27 +600,27 @@ __global__ void __launch_bounds__(256, 2) k_sweep_kron_mma(int N, int ld, int ng
 }
 
 template <int MP>
-void sweep_kron_mma_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
+void sweep_kron_mma_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s,
+                           int ngroups, const int32_t *grp_patch, const int32_t *grp_type) {
   constexpr int P8 = 8 * ((MP + 7) / 8);
   constexpr int K4 = 4 * ((MP + 3) / 4);
   const size_t smem = (size_t)(P8 * (P8 + 4) + P8 * 4 + 4 * P8 + 8 * 2 * K4 * 36) * sizeof(double);
   smem_optin((const void *)k_sweep_kron_mma<MP>, 220 * 1024);
-  const int ngroups = L.kron_ngrp8;
   const int grid = std::min(ngroups, num_sms() * 2);
-  k_sweep_kron_mma<MP><<<grid, 256, smem, s>>>(N, (L.mp + 1) & ~1, ngroups, L.grp_patch8, L.grp_type8, L.pnodes,
+  k_sweep_kron_mma<MP><<<grid, 256, smem, s>>>(N, (L.mp + 1) & ~1, ngroups, grp_patch, grp_type, L.pnodes,
                                                L.kV, L.kS, L.ksig, L.wnode, omega, r, u);
   ++g_launches;
 }
 
 template <int NQ, int MP>
-void sweep_kron_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s) {
+void sweep_kron_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s, int ncta,
+                       int PP, const int32_t *cta_patch, const int32_t *cta_type) {
   const int C = (N + 31) / 32;
-  const int PP = L.kron_pp;
   constexpr int MPS = (MP + 1) & ~1;
   size_t smem = (size_t)(2 * MP * MPS + MP * NQ * NQ + MP + PP * MP + PP * C * MP) * sizeof(double) +
                 (size_t)PP * MP * sizeof(int);
   smem_optin((const void *)k_sweep_kron<NQ, MP>, 200 * 1024);
-  k_sweep_kron<NQ, MP><<<L.kron_ncta, 32 * C * PP, smem, s>>>(N, C, PP, L.cta_patch, L.cta_type, L.pnodes, L.kV,
+  k_sweep_kron<NQ, MP><<<ncta, 32 * C * PP, smem, s>>>(N, C, PP, cta_patch, cta_type, L.pnodes, L.kV,
                                                                L.kVT, L.kS, L.ksig, L.wnode, omega, r, u);
   ++g_launches;
 }
@@ -821,15 +821,27 @@ void launch_kron_setup_coarse(const Level &L, Coarse &C, int nq, const Temporal 
   ++g_launches;
 }
 
-bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s) {
+bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u, double omega, cudaStream_t s,
+                       const SweepLists *sl) {
   const int nq = q + 1;
-  if (nq == 2 && L.kron_ngrp8 > 0 && L.npatch >= 1000) {  // small levels: chunk-parallel kernel below
-    if (L.mp == 19) { sweep_kron_mma_launch<19>(L, N, r, u, omega, s); return true; }
-    if (L.mp == 7) { sweep_kron_mma_launch<7>(L, N, r, u, omega, s); return true; }
-    if (L.mp == 1) { sweep_kron_mma_launch<1>(L, N, r, u, omega, s); return true; }
+  const int ngrp8 = sl ? sl->ngrp8 : L.kron_ngrp8, ncta = sl ? sl->ncta : L.kron_ncta;
+  const int pp = sl ? sl->pp : L.kron_pp;
+  const int32_t *gp = sl ? sl->grp_patch8 : L.grp_patch8, *gt = sl ? sl->grp_type8 : L.grp_type8;
+  const int32_t *cp = sl ? sl->cta_patch : L.cta_patch, *ct = sl ? sl->cta_type : L.cta_type;
+  if (nq == 2 && L.npatch >= 1000) {  // small levels: chunk-parallel kernel below
+    if (L.mp == 19 || L.mp == 7 || L.mp == 1) {
+      if (ngrp8 == 0) return true;  // nothing in this list
+      if (L.mp == 19) sweep_kron_mma_launch<19>(L, N, r, u, omega, s, ngrp8, gp, gt);
+      if (L.mp == 7) sweep_kron_mma_launch<7>(L, N, r, u, omega, s, ngrp8, gp, gt);
+      if (L.mp == 1) sweep_kron_mma_launch<1>(L, N, r, u, omega, s, ngrp8, gp, gt);
+      return true;
+    }
   }
-#define WRMG_SK(NQ, MP) \
-  if (nq == NQ && L.mp == MP) { sweep_kron_launch<NQ, MP>(L, N, r, u, omega, s); return true; }
+#define WRMG_SK(NQ, MP)                                                    \
+  if (nq == NQ && L.mp == MP) {                                            \
+    if (ncta > 0) sweep_kron_launch<NQ, MP>(L, N, r, u, omega, s, ncta, pp, cp, ct); \
+    return true;                                                           \
+  }
   WRMG_SK(1, 1) WRMG_SK(2, 1) WRMG_SK(3, 1) WRMG_SK(4, 1)
   WRMG_SK(1, 7) WRMG_SK(2, 7) WRMG_SK(3, 7) WRMG_SK(4, 7)
   WRMG_SK(1, 19) WRMG_SK(2, 19) WRMG_SK(3, 19)

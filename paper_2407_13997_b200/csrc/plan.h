@@ -27,8 +27,9 @@ constexpr uint8_t kRowGeneric = 254;
 
 // Type-grouped CTA work list for the Kronecker sweep: ncta x pp patch ids (-1 pad).
 // Patches of class `exclude` (>= 0) are left out (they run in the symmetry-reduced sweep).
+// colour: only patches whose (*colour)[p] == want.
 void plan_sweep_ctas(const PlanLevel &P, int pp, std::vector<int32_t> &cta_patch, std::vector<int32_t> &cta_type,
-                     int exclude = -1);
+                     int exclude = -1, const std::vector<uint8_t> *colour = nullptr, int want = -1);
 
 void plan_level(int nx, int ny, double h, int k, PlanLevel *P, bool neumann = false);
 void plan_interpolation(const PlanLevel &C, const PlanLevel &F, int k, std::vector<int32_t> &rowptr,
