@@ -135,8 +135,8 @@ def ncu_traffic(kclass, path=None, names=None):
     the kernel behind a timing class, from a committed `ncu --set full` summary
     (default: the C2 bench's profiles/r01_final_c2_ncu.txt); (None, None) if absent."""
     import re
-    names = names or {"residual": "k_residual_tma", "sweep": "k_sweep_kron_mma", "krylov": "k_krylov"}
-    path = path or os.path.join(ROOT, "profiles", "r01_final_c2_ncu.txt")
+    names = names or {"residual": "k_residual_mac", "sweep": "k_sweep_sym", "krylov": "k_krylov"}
+    path = path or os.path.join(ROOT, "profiles", "r02_c2_ncu.txt")
     if kclass not in names or not os.path.exists(path):
         return None, None
     best = None
@@ -452,6 +452,98 @@ def run_c3(args, ws, rank, local):
     ctx.close()
 
 
+def run_c4(args, ws, rank, local):
+    """BASELINE configs[3] (C4) shape on one B200: Navier-Stokes lid-driven cavity, P3-P2
+    Taylor-Hood x DG1, 128x128 mesh, dt = 1/128, Re = 1000, linearised at the zero state
+    + lid lift (the first Newton step, R26), N = args.c4_n slabs: the stored (patch, slab)
+    block inverses of the full 128-slab horizon are 447 GB, N = 32 is the
+    largest slab count whose ~150 GB fit one GPU.  Step = fixed work: 10 Vanka+star
+    sweeps (omega 1) + one residual + one V(1,1) on a seeded RHS (omega_mg 0.8); the
+    linearisation (assembly + batched block inversion on every level) is timed apart."""
+    import torch
+
+    import paper_2407_13997_b200 as w
+    torch.cuda.set_device(local)
+    n, k, q, N, R = 128, 2, 1, args.c4_n, 1000.0
+    dt = 1.0 / 128
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
+                    omega_mg=0.8, device=local, stream=stream.cuda_stream)
+    setup_s = time.time() - t0
+    lay = ctx.layout
+    NT = lay["nt"]
+    ku = k + 1
+    Lux = ku * n + 1
+    Lu = Lux * Lux
+    W = torch.zeros(lay["ndof"], dtype=torch.float64, device=f"cuda:{local}")
+    top = W.view(-1, NT)[(Lux - 1) * Lux + 1:(Lux - 1) * Lux + Lux - 1]  # u_x on the lid, corners excluded
+    top.fill_(1.0)
+    assert (Lux - 1) * Lux + Lux - 1 <= Lu
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ctx.profile(True)
+    ev[0].record(stream)
+    ctx.linearize(W)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    lin_ms = ev[0].elapsed_time(ev[1])
+    lin_stats = {f"{a}@L{l}": {"ms": round(v["ms"], 3), "TFs": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 3)}
+                 for (a, l), v in ctx.kernel_stats().items()}
+    ctx.profile(False)
+    f = ctx.empty()
+    ctx.fill_uniform(f, 0, 0)
+    b = ctx.empty()
+    ctx.rhs(f, b)
+    del f
+    u, r, z = ctx.empty(), ctx.empty(), ctx.empty()
+    upd_vc = lay["smooth_dof_updates_per_vcycle"]
+    upd_sweep = lay["nfree_st"]
+
+    def step():
+        u.zero_()
+        ctx.smooth(u, b, 10, 1.0)
+        ctx.residual(u, b, r)
+        ctx.vcycle(r, z)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ctx.profile(True)
+    l0 = w.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    stats = ctx.kernel_stats()
+    ctx.profile(False)
+    clk = clocks.stop()
+    per_kernel = {f"{a}@L{l}": {"launches": s["launches"], "ms": round(s["ms"], 3),
+                                "GBs": round(s["bytes"] / (s["ms"] / 1e3) / 1e9, 1) if s["ms"] > 0 else None,
+                                "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}
+                  for (a, l), s in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
+    tot = args.steps * (10 * upd_sweep + upd_vc)
+    line = {"metric": METRIC, "value": tot / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C4 shape = BASELINE configs[3] at full mesh: NS cavity P3-P2 x DG1, 128x128, "
+                                   f"dt=1/128, Re=1000, linearised at the lid lift; N={N} slabs (C4's 128 slabs "
+                                   f"need 447 GB of stored block inverses); step = 10 sweeps + residual + V(1,1)",
+                       "ndof": lay["ndof"], "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
+                       "npatch": lay["npatch"], "mp_max": lay["mp_max"], "setup_s": round(setup_s, 2)},
+            "linearize_ms": lin_ms, "linearize_kernels": lin_stats,
+            "roofline": top_roofline(stats), "per_kernel": per_kernel, "clocks": clk,
+            "gpu_launches": w.launch_count() - l0}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
 def run_gpu(args, ws, rank, local):
     import torch
 
@@ -668,7 +760,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wrmg", choices=["wrmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--c4-n", type=int, default=32, help="C4 slabs on one GPU (32: largest whose inverses fit)")
     ap.add_argument("--c5-n", type=int, default=1024, help="C5 cells per side per GPU (1024 = the config)")
     ap.add_argument("--scatter", default="atomic", choices=["atomic", "colour"],
                     help="weighted additive scatter of the heat sweep (H8): FP64 atomics or coloured passes")
@@ -682,6 +775,8 @@ def main():
         run_c5(args, ws, rank, local)
     elif args.config == "C3":
         run_c3(args, ws, rank, local)
+    elif args.config == "C4":
+        run_c4(args, ws, rank, local)
     else:
         run_gpu(args, ws, rank, local)
     if ws > 1:

@@ -1900,9 +1900,11 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
     // them: the new basis vector is the orthogonalised w itself (buffer swap) and
     // the scales enter the CGS coefficients, the Hessenberg entries and y.
     std::vector<double> sc(restart + 1, 0.0), coef(32);
+    if (!strip && !c->kry) c->kry = dalloc<double>(256);
     while (!done && its < maxit) {
       std::swap(c->V[0], c->tmp);  // V_0' = r, sc_0 = 1 / beta
       sc[0] = 1.0 / beta;
+      if (!strip) small_h2d(c, &sc[0], c->kry, 1);
       std::fill(H.begin(), H.end(), 0.0);
       std::fill(g.begin(), g.end(), 0.0);
       g[0] = beta;
@@ -1916,6 +1918,33 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         // CGS2, fused: h = V^T w;  w -= V h & h2 = V^T w;  w -= V h2 & |w|^2
         // (w' = A Z_j', the true w = sc_j w': h_i = sc_i sc_j <V_i', w'>, and
         // w -= sum h_i V_i  <=>  w' -= sum sc_i^2 <V_i', w'> V_i')
+        double wn2 = 0.0;
+        if (!strip) {  // coefficients on the device: one host read per Arnoldi step
+          const int nb = multidot_blocks(n);
+          std::vector<const double *> Vp(c->V.begin(), c->V.begin() + j + 1);
+          {
+            PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 2) * n, 2.0 * (j + 1) * n);
+            launch_multidot(Vp.data(), j + 1, c->w, n, part, nb, s);
+            launch_reduce_partials(part, nb, j + 1, c->kry + 32, s);
+          }
+          launch_cgs_step(c->kry, j, 0, s);
+          {
+            PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 4.0 * (j + 1) * n);
+            launch_cgs_update_dot(c->V.data(), j + 1, c->w, c->kry + 64, n, part, nb, s);
+            launch_reduce_partials(part, nb, j + 1, c->kry + 96, s);
+          }
+          launch_cgs_step(c->kry, j, 1, s);
+          {
+            PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
+            launch_cgs_update_norm(c->V.data(), j + 1, c->w, c->kry + 128, n, part, nb, s);
+            launch_reduce_partials(part, nb, 1, c->kry + 192, s);
+          }
+          launch_cgs_step(c->kry, j, 2, s);
+          std::vector<double> out(j + 2);
+          small_d2h(c, c->kry + 200, out.data(), j + 2);
+          h.assign(out.begin(), out.begin() + j + 1);
+          wn2 = out[j + 1];
+        } else {
         multidot(j + 1, c->w, h);
         for (int i = 0; i <= j; ++i) {
           coef[i] = sc[i] * sc[i] * h[i];
@@ -1935,7 +1964,6 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           h[i] += sc[i] * sc[j] * h2[i];
         }
         small_h2d(c, coef.data(), red + 32, j + 1);
-        double wn2 = 0.0;
         {
           PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
           const int nb = multidot_blocks(n);
@@ -1943,6 +1971,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           launch_reduce_partials(part, nb, 1, red + 63, s);
         }
         reduce_to_host(c, red + 63, 1, &wn2);
+        }
         const double hn = sc[j] * std::sqrt(wn2);
         std::vector<double> col(restart + 1, 0.0);
         for (int i = 0; i <= j; ++i) col[i] = h[i];
@@ -2271,6 +2300,7 @@ void wrmg_destroy(wrmg_ctx *c) {
   for (double *p : c->Z) dfree(p);
   dfree(c->w);
   dfree(c->red);
+  dfree(c->kry);
   dfree(c->tmp);
   dfree(c->ref_dev);
   for (auto &r : c->prof_recs) {

@@ -240,6 +240,7 @@ struct wrmg_ctx {
   int restart_alloc = 0;
   std::vector<double *> V, Z;
   double *w = nullptr, *red = nullptr, *red_host = nullptr;
+  double *kry = nullptr;   // device-side CGS2 coefficients of the single-rank FGMRES (kernels_krylov.cu)
   double *hmap = nullptr;  // mapped pinned host buffer (2 x hmap_cap doubles): small Krylov results without the copy engines
   int hmap_cap = 0;        // doubles per direction: max(1024, 64 nranks)
   double *gred = nullptr;  // strips: all ranks' reduction results (nranks x 64), for wrmg_fgmres
@@ -342,6 +343,7 @@ void launch_reduce_partials(const double *partials, int nblk, int nv, double *ou
 void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev, int nv, int64_t n, double sign,
                       cudaStream_t s);
 void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s);
+void launch_cgs_step(double *kry, int j, int stage, cudaStream_t s);
 // Chebyshev smoothing / initial state (kernels_cheb.cu)
 void launch_cheb_update(int64_t n, double c1, double c2, const double *br, double *d, double *u, cudaStream_t s);
 void launch_rhs_initial(const Level &L, int nq, int64_t NT, const double *phi0, const double *u0, double *b,

@@ -82,6 +82,31 @@ __global__ void k_reduce(const double *__restrict__ partials, int nblk, int nv, 
   if (lane == 0) out[v] = s;
 }
 
+// Device-side CGS2 coefficients of FGMRES step j with the lazily scaled basis (single
+// rank: no host round trip inside the Arnoldi step).  kry layout (doubles):
+//   [0, 32) sc_i   [32, 64) h_i = <V_i', w'>   [64, 96) sc_i^2 h_i   [96, 128) h2_i
+//   [128, 160) sc_i^2 h2_i   [160, 192) Hessenberg column   [192] |w'|^2   [200, 233) out
+// stage 0 (after pass A): coef A, column = sc_i sc_j h_i; stage 1 (after pass B): coef B,
+// column += sc_i sc_j h2_i; stage 2 (after pass C): sc_{j+1} = 1 / |w'|, out = (column, |w'|^2).
+// The products are rounded one at a time (__dmul_rn), as the host computes them.
+__global__ void k_cgs_step(double *__restrict__ kry, int j, int stage) {
+  const int i = threadIdx.x;
+  double *sc = kry, *h = kry + 32, *ca = kry + 64, *h2 = kry + 96, *cb = kry + 128, *col = kry + 160;
+  if (stage == 0 && i <= j) {
+    ca[i] = __dmul_rn(__dmul_rn(sc[i], sc[i]), h[i]);
+    col[i] = __dmul_rn(__dmul_rn(sc[i], sc[j]), h[i]);
+  } else if (stage == 1 && i <= j) {
+    cb[i] = __dmul_rn(__dmul_rn(sc[i], sc[i]), h2[i]);
+    col[i] = __dadd_rn(col[i], __dmul_rn(__dmul_rn(sc[i], sc[j]), h2[i]));
+  } else if (stage == 2) {
+    if (i <= j) kry[200 + i] = col[i];
+    if (i == 0) {
+      kry[200 + j + 1] = kry[192];
+      if (j + 1 < 32) sc[j + 1] = 1.0 / sqrt(kry[192]);
+    }
+  }
+}
+
 __global__ void k_scale(double *__restrict__ dst, const double *__restrict__ src, double a, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = a * src[i];
@@ -130,6 +155,11 @@ void launch_multiaxpy(double *w, const double *const *V, const double *coef_dev,
                       cudaStream_t s) {
   // sign +1: w += V c (solution update); sign -1: w -= V c
   krylov_launch<3>(V, nv, w, coef_dev, n, nullptr, grid_for(n), s, sign);
+}
+
+void launch_cgs_step(double *kry, int j, int stage, cudaStream_t s) {
+  k_cgs_step<<<1, 32, 0, s>>>(kry, j, stage);
+  ++g_launches;
 }
 
 void launch_scale(double *dst, const double *src, double a, int64_t n, cudaStream_t s) {

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, con
   __shared__ int snode[WPC][MP];
   __shared__ double swt[WPC][MP];
   __shared__ double sycar[WPC][MP];  // end trace of every mode at the previous chunk's last slab
+  extern __shared__ __align__(16) double stage[];  // [WPC][MP][32][NQ]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t NT = (int64_t)N * NQ;
   const int nch = (N + 31) / 32;
@@ -235,13 +236,27 @@ __global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, con
     for (int ch = 0; ch < nch; ++ch) {
       const int n = 32 * ch + lane;
       const bool valid = n < N;
+      // stage the weighted corrections [slot][slab][a] in shared memory, then one
+      // contiguous run of 32 NQ atomics per node (lanes on consecutive doubles: fewer
+      // L2 sectors per instruction than lane = slab with stride NQ)
+      double *stg = stage + (size_t)w * MP * 32 * NQ;
       sym_patch_chunk<K, NQ>(P, snode[w], sycar[w], n, valid, NT, r, lane, [&](int a, const double(&x)[MP]) {
-        if (valid) {
 #pragma unroll
-          for (int j = 0; j < MP; ++j)
-            atomicAdd(u + (int64_t)snode[w][j] * NT + (int64_t)n * NQ + a, swt[w][j] * x[j]);
-        }
+        for (int j = 0; j < MP; ++j) stg[(j * 32 + lane) * NQ + a] = swt[w][j] * x[j];
       });
+      __syncwarp();
+      const int64_t t0 = (int64_t)ch * 32 * NQ;
+      const int nv = (int)min((int64_t)32 * NQ, NT - t0);  // valid values of this chunk
+#pragma unroll 4
+      for (int j = 0; j < MP; ++j) {
+        double *dst = u + (int64_t)snode[w][j] * NT + t0;
+#pragma unroll
+        for (int e = 0; e < NQ; ++e) {
+          const int idx = lane + 32 * e;
+          if (idx < nv) atomicAdd(dst + idx, stg[j * 32 * NQ + idx]);
+        }
+      }
+      __syncwarp();
     }
   }
 }
@@ -335,8 +350,10 @@ void sym_launch(const Level &L, int N, const double *r, double *u, double omega,
   if (np > 0) {
     const int64_t nblk = (np + 3) / 4;
     const int grid = (int)std::min<int64_t>(nblk, (int64_t)6 * num_sms());
-    k_sweep_sym<K, NQ><<<grid, 128, 0, s>>>(N, np, L.ntile > 0 ? L.sym_single : nullptr, L.sym_nodes, L.symtab,
-                                            L.wnode, omega, r, u);
+    const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
+    smem_optin((const void *)k_sweep_sym<K, NQ>, smem);
+    k_sweep_sym<K, NQ><<<grid, 128, smem, s>>>(N, np, L.ntile > 0 ? L.sym_single : nullptr, L.sym_nodes, L.symtab,
+                                               L.wnode, omega, r, u);
     ++g_launches;
   }
 }
@@ -346,7 +363,9 @@ void sym_list_launch(const Level &L, int N, const double *r, double *u, double o
                      const int32_t *list) {
   if (np <= 0) return;
   const int grid = (int)std::min<int64_t>((np + 3) / 4, (int64_t)6 * num_sms());
-  k_sweep_sym<K, NQ><<<grid, 128, 0, s>>>(N, np, list, L.sym_nodes, L.symtab, L.wnode, omega, r, u);
+  const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
+  smem_optin((const void *)k_sweep_sym<K, NQ>, smem);
+  k_sweep_sym<K, NQ><<<grid, 128, smem, s>>>(N, np, list, L.sym_nodes, L.symtab, L.wnode, omega, r, u);
   ++g_launches;
 }
 

@@ -16,5 +16,7 @@ for _ in range(3):
     c.residual(u, b, r)
 for _ in range(2):
     c.smooth(u, b, 1, 1.0)
+x = c.empty()
+c.fgmres(b, x, restart=30, maxit=3, rtol=1e-12)
 torch.cuda.synchronize()
 print("ok")
