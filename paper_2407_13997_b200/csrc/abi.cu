@@ -83,6 +83,14 @@ T *dalloc(size_t n) {
   CK(cudaMalloc(&p, n * sizeof(T)));
   return (T *)p;
 }
+// Zero-initialised work vector (rows a kernel never writes -- e.g. a strip's
+// non-owned columns -- then read as 0 instead of a recycled allocation's bytes).
+template <class T>
+T *dzalloc(size_t n) {
+  T *p = dalloc<T>(n);
+  CK(cudaMemset(p, 0, (n ? n : 1) * sizeof(T)));
+  return p;
+}
 
 template <class T>
 T *dupload(const std::vector<T> &v, cudaStream_t s) {
@@ -327,10 +335,13 @@ void halo_reverse_add(wrmg_ctx *c, Level &L, double *v) {
   launch_cols(v, L.Lx, L.Ly, c->nt, S.sr0, S.nsr, L.hx[3], 2, s);
 }
 
+// Zero every column this rank does not own: the ghost columns and, on ranks > 0, the
+// local lattice's first column (one cell left of the left ghosts; never refreshed --
+// with Neumann boundaries it is a free row, so dot products must not see it).
 void zero_ghosts(wrmg_ctx *c, Level &L, double *v) {
   const StripInfo &S = L.st;
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.lg0, S.nlg, nullptr, 3, c->stream);
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.rg0, S.nrg, nullptr, 3, c->stream);
+  if (S.own0 > 0) launch_cols(v, L.Lx, L.Ly, c->nt, 0, S.own0, nullptr, 3, c->stream);
+  if (S.own1 + 1 < L.Lx) launch_cols(v, L.Lx, L.Ly, c->nt, S.own1 + 1, L.Lx - S.own1 - 1, nullptr, 3, c->stream);
 }
 
 // One additive sweep on a strip: owned patches add into owned and right-ghost
@@ -816,22 +827,25 @@ void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om);
 // lam_l: `steps` Arnoldi steps (CGS2) on B A from the seeded start vector, B one
 // undamped sweep from zero; the estimate is the largest |Ritz value| (PAPER.md:366-371:
 // "estimate the largest eigenvalue"; DESIGN.md R-cheb).
+void reduce_to_host(wrmg_ctx *c, const double *dev, int nv, double *host);
+
 double estimate_lambda(wrmg_ctx *c, int l) {
   cudaStream_t s = c->stream;
   Level &L = c->lv[l];
   const int64_t n = L.nnode * c->nt;
   const int steps = c->co.cheb_steps;
   std::vector<double *> V(steps + 1);
-  for (auto &v : V) v = dalloc<double>(n);
-  double *w = dalloc<double>(n), *t = dalloc<double>(n);
+  for (auto &v : V) v = dzalloc<double>(n);
+  double *w = dzalloc<double>(n), *t = dzalloc<double>(n);
+  // strips: the Krylov vectors keep zero ghost columns, so the dots count owned rows;
+  // every rank sums the all-gathered partial dots in rank order (reduce_to_host)
   auto dot = [&](const double *a, const double *b) {
     const int nb = multidot_blocks(n);
     const double *Vp[1] = {a};
     launch_multidot(Vp, 1, b, n, c->red + 64, nb, s);
     launch_reduce_partials(c->red + 64, nb, 1, c->red, s);
     double out = 0;
-    CK(cudaMemcpyAsync(&out, c->red, sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    reduce_to_host(c, c->red, 1, &out);
     return out;
   };
   // h = V[0..nv)^T w in chunks of 32 vectors
@@ -842,9 +856,8 @@ double estimate_lambda(wrmg_ctx *c, int l) {
       const int nb = multidot_blocks(n);
       launch_multidot(V.data() + c0, k2, w, n, c->red + 64, nb, s);
       launch_reduce_partials(c->red + 64, nb, k2, c->red, s);
-      CK(cudaMemcpyAsync(h.data() + c0, c->red, k2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      reduce_to_host(c, c->red, k2, h.data() + c0);
     }
-    CK(cudaStreamSynchronize(s));
   };
   auto subtract = [&](int nv, const std::vector<double> &h) {  // w -= V h
     for (int c0 = 0; c0 < nv; c0 += 32) {
@@ -853,14 +866,29 @@ double estimate_lambda(wrmg_ctx *c, int l) {
       launch_multiaxpy(w, V.data() + c0, c->red, k2, n, -1.0, s);
     }
   };
-  launch_fill_uniform(V[0], n, 0, c->co.cheb_seed, s);
+  if (!c->strip) {
+    launch_fill_uniform(V[0], n, 0, c->co.cheb_seed, s);
+  } else {  // R6 generator at the global canonical ids: local row J holds global columns G0 ..
+    const int64_t GLx = (int64_t)c->k * L.st.gnx + 1, rowlen = (int64_t)L.Lx * c->nt;
+    for (int J = 0; J < L.Ly; ++J)
+      launch_fill_uniform(V[0] + J * rowlen, rowlen, (uint64_t)((J * GLx + L.st.G0) * c->nt), c->co.cheb_seed, s);
+    zero_ghosts(c, L, V[0]);
+  }
   launch_ns_mask(L.nnode, c->nt, L.con, nullptr, V[0], V[0], s);  // constrained rows 0
   launch_scale(V[0], V[0], 1.0 / std::sqrt(dot(V[0], V[0])), n, s);
   std::vector<double> H((size_t)(steps + 1) * steps, 0.0), h, h2;
   for (int j = 0; j < steps; ++j) {
+    if (c->strip) halo_forward(c, L, V[j]);
     prof_residual(c, l, V[j], nullptr, t, false);  // t = A v_j
     CK(cudaMemsetAsync(w, 0, n * sizeof(double), s));
-    prof_sweep(c, l, t, w, 1.0);                    // w = B A v_j
+    if (c->strip) {
+      zero_ghosts(c, L, V[j]);
+      halo_forward(c, L, t);
+      sweep_strip(c, l, t, w, 1.0);                 // w = B A v_j
+      zero_ghosts(c, L, w);
+    } else {
+      prof_sweep(c, l, t, w, 1.0);                  // w = B A v_j
+    }
     multidot(j + 1, h);
     subtract(j + 1, h);
     multidot(j + 1, h2);
@@ -897,11 +925,16 @@ void cheb_smooth(wrmg_ctx *c, int l, const double *b, double *u, bool u_zero, in
   for (int k2 = 0; k2 < nu; ++k2) {
     const double *res = b;
     if (k2 > 0 || !u_zero) {
-      prof_residual(c, l, u, b, t, false);
+      prof_residual(c, l, u, b, t, false);  // strips: u's ghosts are current (see below)
       res = t;
     }
     CK(cudaMemsetAsync(br, 0, n * sizeof(double), s));
-    prof_sweep(c, l, res, br, 1.0);
+    if (c->strip) {
+      if (res != b) halo_forward(c, L, t);  // b's ghosts were refreshed by the caller
+      sweep_strip(c, l, res, br, 1.0);      // br valid on owned and ghost columns
+    } else {
+      prof_sweep(c, l, res, br, 1.0);
+    }
     double c1 = 0.0, c2 = 1.0 / theta;
     if (k2 > 0) {
       const double rn = 1.0 / (2.0 * sigma - rho);
@@ -950,13 +983,17 @@ void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
   const double om = c->co.omega_mg;
   halo_forward(c, L, const_cast<double *>(r));
   CK(cudaMemsetAsync(z, 0, nd * sizeof(double), s));
-  for (int it = 0; it < c->co.nu_pre; ++it) {
-    if (it == 0) {
-      sweep_strip(c, l, r, z, om);
-    } else {
-      prof_residual(c, l, z, r, t, false);
-      halo_forward(c, L, t);
-      sweep_strip(c, l, t, z, om);
+  if (c->cheb) {
+    cheb_smooth(c, l, r, z, true, c->co.nu_pre);
+  } else {
+    for (int it = 0; it < c->co.nu_pre; ++it) {
+      if (it == 0) {
+        sweep_strip(c, l, r, z, om);
+      } else {
+        prof_residual(c, l, z, r, t, false);
+        halo_forward(c, L, t);
+        sweep_strip(c, l, t, z, om);
+      }
     }
   }
   prof_residual(c, l, z, r, t, c->co.nu_pre == 0);
@@ -976,10 +1013,14 @@ void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
     }
   }
   halo_forward(c, L, z);
-  for (int it = 0; it < c->co.nu_post; ++it) {
-    prof_residual(c, l, z, r, t, false);
-    halo_forward(c, L, t);
-    sweep_strip(c, l, t, z, om);
+  if (c->cheb) {
+    cheb_smooth(c, l, r, z, false, c->co.nu_post);
+  } else {
+    for (int it = 0; it < c->co.nu_post; ++it) {
+      prof_residual(c, l, z, r, t, false);
+      halo_forward(c, L, t);
+      sweep_strip(c, l, t, z, om);
+    }
   }
   check_launch();
 }
@@ -1221,9 +1262,8 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       throw Err{WRMG_E_UNSUPPORTED, "problem must be WRMG_HEAT or WRMG_NAVIER_STOKES"};
     if (coeffs->problem == WRMG_HEAT && coeffs->bc != WRMG_BC_DIRICHLET0 && coeffs->bc != WRMG_BC_NEUMANN)
       throw Err{WRMG_E_UNSUPPORTED, "heat: bc must be WRMG_BC_DIRICHLET0 or WRMG_BC_NEUMANN"};
-    if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV &&
-        (coeffs->nranks > 1 || coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
-      throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: single rank, cheb_steps <= 63"};
+    if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV && (coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
+      throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: cheb_steps <= 63"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
     if (coeffs->nranks > 1 && coeffs->problem != WRMG_HEAT)
       throw Err{WRMG_E_UNSUPPORTED, "strip partitions are built for the heat operator only"};
@@ -1486,9 +1526,9 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         c->sweep_flops.push_back(fl * c->N);
       }
       if (l < nl - 1) {
-        L.vr = dalloc<double>(L.nnode * c->nt);
-        L.vz = dalloc<double>(L.nnode * c->nt);
-        L.vt = dalloc<double>(L.nnode * c->nt);
+        L.vr = dzalloc<double>(L.nnode * c->nt);
+        L.vz = dzalloc<double>(L.nnode * c->nt);
+        L.vt = dzalloc<double>(L.nnode * c->nt);
       }
       if (c->strip)
         for (int b = 0; b < 4; ++b) L.hx[b] = dalloc<double>((size_t)L.Ly * degree * c->nt);
@@ -1540,10 +1580,10 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       X.R.col = dupload(tci, s);
       X.R.val = dupload(tv, s);
       const int64_t ng = gc.nnode * c->nt;
-      c->sub_r = dalloc<double>(ng);
-      c->sub_z = dalloc<double>(ng);
-      c->sub_part = dalloc<double>(ng);
-      c->sub_all = dalloc<double>(ng * coeffs->nranks);
+      c->sub_r = dzalloc<double>(ng);
+      c->sub_z = dzalloc<double>(ng);
+      c->sub_part = dzalloc<double>(ng);
+      c->sub_all = dzalloc<double>(ng * coeffs->nranks);
       CK(cudaStreamSynchronize(s));
     }
     PlanLevel gplan;  // strips: the global coarsest level, replicated on every rank
@@ -1600,7 +1640,7 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
         C.ksig = dalloc<double>((size_t)C.mp);
       }
     }
-    c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
+    c->tmp = dzalloc<double>(c->lv.back().nnode * c->nt);
     c->red = dalloc<double>(64 + 64 * kDotBlocksMax);
     CK(cudaStreamSynchronize(s));
     factor_all(c);
@@ -1610,9 +1650,9 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       c->lam.assign(nl, 0.0);
       c->cd.assign(nl, nullptr);
       c->cbr.assign(nl, nullptr);
-      for (int l = 1; l < nl; ++l) {
-        c->cd[l] = dalloc<double>(c->lv[l].nnode * c->nt);
-        c->cbr[l] = dalloc<double>(c->lv[l].nnode * c->nt);
+      for (int l = c->sub ? 0 : 1; l < nl; ++l) {  // strips over a replicated sub-hierarchy: level 0 is smoothed
+        c->cd[l] = dzalloc<double>(c->lv[l].nnode * c->nt);
+        c->cbr[l] = dzalloc<double>(c->lv[l].nnode * c->nt);
         c->lam[l] = estimate_lambda(c, l);
       }
     }
@@ -1858,9 +1898,9 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
       c->V.clear();
       c->Z.clear();
       dfree(c->w);
-      for (int i = 0; i <= restart; ++i) c->V.push_back(dalloc<double>(n));
-      for (int i = 0; i < restart; ++i) c->Z.push_back(dalloc<double>(n));
-      c->w = dalloc<double>(n);
+      for (int i = 0; i <= restart; ++i) c->V.push_back(dzalloc<double>(n));
+      for (int i = 0; i < restart; ++i) c->Z.push_back(dzalloc<double>(n));
+      c->w = dzalloc<double>(n);
       c->restart_alloc = restart;
     }
     double *red = c->red;            // [0, 64): results / coefficients

@@ -11,7 +11,7 @@ namespace {
 __global__ void k_cheb_update(int64_t n, double c1, double c2, const double *__restrict__ br, double *__restrict__ d,
                               double *__restrict__ u) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = fma(c1, d[i], c2 * br[i]);
+    const double v = c1 != 0.0 ? fma(c1, d[i], c2 * br[i]) : c2 * br[i];  // first step: d not read
     d[i] = v;
     u[i] += v;
   }

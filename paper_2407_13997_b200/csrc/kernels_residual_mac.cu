@@ -542,7 +542,16 @@ bool launch_residual_mac(const Level &L, int k, int q, int N, const Temporal &tm
 #define WRMG_MAC(KK_, NQ_, MX_, R_) \
   if (k == KK_ && q + 1 == NQ_) ok = mac_launch<KK_, NQ_, MX_, R_>(L, N, P, u, b, r, apply, s);
     WRMG_MAC(1, 1, 16, 8) WRMG_MAC(1, 2, 16, 8) WRMG_MAC(1, 3, 16, 8) WRMG_MAC(1, 4, 16, 8)
-    WRMG_MAC(2, 1, 8, 5) WRMG_MAC(2, 2, 8, 5) WRMG_MAC(2, 3, 8, 5) WRMG_MAC(2, 4, 8, 4)
+    static const int k2mx = [] {  // WRMG_MAC_K2=16: P2 levels with 16 macro columns per CTA (A/B)
+      const char *e = getenv("WRMG_MAC_K2");
+      return e ? atoi(e) : 8;
+    }();
+    if (k2mx == 16) {
+      WRMG_MAC(2, 2, 16, 4)
+    }
+    if (!ok) {
+      WRMG_MAC(2, 1, 8, 5) WRMG_MAC(2, 2, 8, 5) WRMG_MAC(2, 3, 8, 5) WRMG_MAC(2, 4, 8, 4)
+    }
     WRMG_MAC(3, 1, 8, 4) WRMG_MAC(3, 2, 8, 4)
 #undef WRMG_MAC
   }
