@@ -464,10 +464,169 @@ __device__ int gj_invert_smem(double *A, int m, double tol, double *X, int *piv,
   return s_info;
 }
 
+// Same elimination (same pivots, same operations per entry) with the panel columns
+// factored by warp 0 alone in registers: lane l holds rows l, l + 32, ... (RPL rows)
+// of the GJB panel columns; the pivot search is a warp argmax (first maximum |a|,
+// lowest row on ties: R10), the pivot and displaced rows move by shuffles, the rank-1
+// panel updates are lane-local FMAs.  The row interchanges reach the other columns
+// afterwards (in pivot order, one thread per column), then the DMMA rank-GJB update
+// as in gj_invert_smem.  Three CTA barriers per panel instead of three per column.
+template <int RPL>
+__device__ int gj_invert_smem_wp(double *A, int m, double tol, double *X, int *piv, int *idx) {
+  __shared__ int s_info;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  if (tid == 0) s_info = 0;
+  __syncthreads();
+  for (int k0 = 0; k0 < m; k0 += GJB) {
+    const int nb = min(GJB, m - k0), k1 = k0 + nb;
+    if (wid == 0) {
+      double P[RPL][GJB];
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) {
+        const int r = lane + 32 * s;
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) P[s][t] = (r < m && t < nb) ? A[r * m + k0 + t] : 0.0;
+      }
+      int info = 0;
+#pragma unroll
+      for (int tc = 0; tc < GJB; ++tc) {
+        if (tc >= nb) break;
+        const int c = k0 + tc;
+        // (1) argmax |P[r][tc]| over rows r >= c: first maximum, lowest row
+        double bv = -1.0;
+        int bi = m;
+#pragma unroll
+        for (int s = 0; s < RPL; ++s) {
+          const int r = lane + 32 * s;
+          const double v = fabs(P[s][tc]);
+          if (r >= c && r < m && v > bv) {
+            bv = v;
+            bi = r;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        if (!(bv >= tol) && info == 0) info = c + 1;
+        // (2) pivot row and row c (the rows to interchange) to every lane
+        const int sp = bi >> 5, lp = bi & 31, sc = c >> 5, lc = c & 31;
+        double prow[GJB], crow[GJB];
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) {
+          double vp = 0.0, vc = 0.0;
+#pragma unroll
+          for (int s = 0; s < RPL; ++s) {
+            vp = (s == sp) ? P[s][t] : vp;
+            vc = (s == sc) ? P[s][t] : vc;
+          }
+          prow[t] = __shfl_sync(0xffffffffu, vp, lp);
+          crow[t] = __shfl_sync(0xffffffffu, vc, lc);
+        }
+        const double pv = prow[tc];
+        const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
+        double newc[GJB];  // pivot row after scaling (panel columns); column tc holds 1 / pivot
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) newc[t] = (t == tc) ? pinv : prow[t] * pinv;
+        // (3) interchange, scale, rank-1 update of the panel rows
+#pragma unroll
+        for (int s = 0; s < RPL; ++s) {
+          const int r = lane + 32 * s;
+          if (r == bi && bi != c) {
+#pragma unroll
+            for (int t = 0; t < GJB; ++t) P[s][t] = crow[t];
+          }
+          if (r == c) {
+#pragma unroll
+            for (int t = 0; t < GJB; ++t) P[s][t] = newc[t];
+          } else {
+            const double fr = P[s][tc];
+#pragma unroll
+            for (int t = 0; t < GJB; ++t)
+              if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
+            P[s][tc] = -fr * pinv;
+          }
+        }
+        if (lane == 0) piv[c] = bi;
+      }
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) {
+        const int r = lane + 32 * s;
+        if (r < m)
+#pragma unroll
+          for (int t = 0; t < GJB; ++t)
+            if (t < nb) A[r * m + k0 + t] = P[s][t];
+      }
+      if (lane == 0 && info && s_info == 0) s_info = info;
+    }
+    __syncthreads();
+    // the panel's row interchanges on the other columns (pivot order), then X = pivot rows
+    for (int j = tid; j < m; j += nth) {
+      if (j >= k0 && j < k1) continue;
+      for (int c = k0; c < k1; ++c) {
+        const int p = piv[c];
+        if (p != c) {
+          const double t1 = A[c * m + j];
+          A[c * m + j] = A[p * m + j];
+          A[p * m + j] = t1;
+        }
+      }
+      for (int t = 0; t < nb; ++t) X[t * m + j] = A[(k0 + t) * m + j];
+    }
+    for (int e = tid; e < nb * nb; e += nth) X[(e / nb) * m + k0 + (e % nb)] = 0.0;
+    __syncthreads();
+    {  // A[:, j] = [0 on pivot rows; A] + Panel X (columns outside the panel), DMMA 8 x 8 tiles
+      const int nt8 = (m + 7) / 8, pt = k0 / 8;
+      const int lr = lane >> 2, lc = lane & 3;
+      for (int it = wid; it < nt8 * nt8; it += nw) {
+        const int tr = it / nt8, tc = it - tr * nt8;
+        if (tc == pt) continue;
+        const int R = tr * 8 + lr;
+        const bool rok = R < m, rpiv = R >= k0 && R < k1;
+        double cc[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int J = tc * 8 + 2 * lc + e;
+          cc[e] = (rok && !rpiv && J < m) ? A[R * m + J] : 0.0;
+        }
+        const int Jb = tc * 8 + lr;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = 4 * h + lc;
+          const double a = (rok && t < nb) ? A[R * m + k0 + t] : 0.0;
+          const double bb = (t < nb && Jb < m) ? X[t * m + Jb] : 0.0;
+          dmma_ns(cc[0], cc[1], a, bb);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int J = tc * 8 + 2 * lc + e;
+          if (rok && J < m) A[R * m + J] = cc[e];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int c = 0; c < m; ++c) idx[c] = c;
+    for (int c = m - 1; c >= 0; --c) {
+      const int p = piv[c], t = idx[c];
+      idx[c] = idx[p];
+      idx[p] = t;
+    }
+  }
+  __syncthreads();
+  return s_info;
+}
+
 // One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
 // DoFs: identity rows), invert, write the row-major inverse to
 // out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
-template <int NQ, int NTH>
+template <int NQ, int NTH, int RPL>
 __global__ void __launch_bounds__(NTH) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
                                                    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
                                                    const double *__restrict__ Mv, const double *__restrict__ KGv,
@@ -550,7 +709,10 @@ __global__ void __launch_bounds__(NTH) k_ns_factor(int mp, int N, int64_t mstrid
   __syncthreads();
   double mx = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
-  const int st = gj_invert_smem(A, m, 1e-14 * mx, X, piv, idx);
+  static_assert(GJB == 8, "panel width");
+  int st;
+  if constexpr (RPL > 0) st = gj_invert_smem_wp<RPL>(A, m, 1e-14 * mx, X, piv, idx);  // m <= 32 RPL
+  else st = gj_invert_smem(A, m, 1e-14 * mx, X, piv, idx);
   double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
   for (int e = tid; e < m * m; e += blockDim.x) {
     const int sig = e / m, rho = e - sig * m;
@@ -1576,11 +1738,27 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
     ++g_launches;
     return;
   }
+  // warp-panel Gauss-Jordan (gj_invert_smem_wp) for m <= 192; WRMG_NS_FACTOR_WP=0: the
+  // column-at-a-time panels of gj_invert_smem (A/B)
+  static const bool wp = [] {
+    const char *e = getenv("WRMG_NS_FACTOR_WP");
+    return !(e && e[0] == '0');
+  }();
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
-    smem_optin((const void *)k_ns_factor<NQ, 256>, (int)sm);
-    k_ns_factor<NQ, 256><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu, vvptr,
-                                          conv, tm, out, info, ppos, pvv);
+    if (wp && m <= 96) {
+      smem_optin((const void *)k_ns_factor<NQ, 128, 3>, (int)sm);
+      k_ns_factor<NQ, 128, 3><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
+                                                    vvptr, conv, tm, out, info, ppos, pvv);
+    } else if (wp && m <= 192) {
+      smem_optin((const void *)k_ns_factor<NQ, 256, 6>, (int)sm);
+      k_ns_factor<NQ, 256, 6><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
+                                                    vvptr, conv, tm, out, info, ppos, pvv);
+    } else {
+      smem_optin((const void *)k_ns_factor<NQ, 256, 0>, (int)sm);
+      k_ns_factor<NQ, 256, 0><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
+                                                    vvptr, conv, tm, out, info, ppos, pvv);
+    }
   });
   ++g_launches;
 }

@@ -542,9 +542,9 @@ bool launch_residual_mac(const Level &L, int k, int q, int N, const Temporal &tm
 #define WRMG_MAC(KK_, NQ_, MX_, R_) \
   if (k == KK_ && q + 1 == NQ_) ok = mac_launch<KK_, NQ_, MX_, R_>(L, N, P, u, b, r, apply, s);
     WRMG_MAC(1, 1, 16, 8) WRMG_MAC(1, 2, 16, 8) WRMG_MAC(1, 3, 16, 8) WRMG_MAC(1, 4, 16, 8)
-    static const int k2mx = [] {  // WRMG_MAC_K2=16: P2 levels with 16 macro columns per CTA (A/B)
-      const char *e = getenv("WRMG_MAC_K2");
-      return e ? atoi(e) : 8;
+    static const int k2mx = [] {  // P2 levels: 16 macro columns per CTA (C5 L7 residual 2.5 vs 2.1 TB/s
+      const char *e = getenv("WRMG_MAC_K2");  // with 8); WRMG_MAC_K2=8 for the narrower form (A/B)
+      return e ? atoi(e) : 16;
     }();
     if (k2mx == 16) {
       WRMG_MAC(2, 2, 16, 4)
