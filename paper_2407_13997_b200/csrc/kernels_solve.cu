@@ -276,7 +276,62 @@ __global__ void k_spmv_nt1(int64_t nrow, int64_t NT, const int32_t *__restrict__
   }
 }
 
+// Same with each thread on TP pairs spaced NT2 / TP apart (NT2 % TP == 0): the row's
+// index and value loads are shared by TP gathers, TP 16-byte loads in flight per entry.
+template <bool ACC, int TP>
+__global__ void __launch_bounds__(256) k_spmv_nt_tp(int64_t nrow, int64_t NT2, const int32_t *__restrict__ rp,
+                                                    const int32_t *__restrict__ ci, const double *__restrict__ v,
+                                                    const double2 *__restrict__ x, double2 *__restrict__ y) {
+  const int64_t W = NT2 / TP;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= nrow * W) return;
+  const int64_t i = idx / W, t = idx - i * W;
+  const int e0 = __ldg(rp + i), e1 = __ldg(rp + i + 1);
+  if (ACC && e0 == e1) return;
+  double2 acc[TP];
+#pragma unroll
+  for (int p = 0; p < TP; ++p) acc[p] = make_double2(0.0, 0.0);
+#pragma unroll 2
+  for (int e = e0; e < e1; ++e) {
+    const double a = __ldg(v + e);
+    const double2 *xr = x + (int64_t)__ldg(ci + e) * NT2 + t;
+#pragma unroll
+    for (int p = 0; p < TP; ++p) {
+      const double2 xv = __ldg(xr + p * W);
+      acc[p].x = fma(a, xv.x, acc[p].x);
+      acc[p].y = fma(a, xv.y, acc[p].y);
+    }
+  }
+  double2 *yr = y + i * NT2 + t;
+#pragma unroll
+  for (int p = 0; p < TP; ++p) {
+    if (ACC) {
+      double2 o = yr[p * W];
+      o.x += acc[p].x;
+      o.y += acc[p].y;
+      yr[p * W] = o;
+    } else {
+      yr[p * W] = acc[p];
+    }
+  }
+}
+
 void spmv_nt(const DevCSR &A, int64_t NT, const double *x, double *y, bool acc, cudaStream_t s) {
+  static const int tp = [] {  // WRMG_SPMV_TP=1: one time pair per thread (A/B)
+    const char *e = getenv("WRMG_SPMV_TP");
+    return e ? atoi(e) : 4;
+  }();
+  if (NT % 2 == 0 && tp == 4 && (NT / 2) % 4 == 0) {
+    const int64_t n = A.nrow * (NT / 8);
+    if (acc)
+      k_spmv_nt_tp<true, 4><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val,
+                                                                         (const double2 *)x, (double2 *)y);
+    else
+      k_spmv_nt_tp<false, 4><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val,
+                                                                          (const double2 *)x, (double2 *)y);
+    ++g_launches;
+    return;
+  }
   if (NT % 2 == 0) {
     const int64_t n = A.nrow * (NT / 2);
     if (acc)
