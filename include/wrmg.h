@@ -270,6 +270,10 @@ void wrmg_loopback_destroy(void *hub);
 
 /* Number of kernels this library has launched in the process so far. */
 int64_t wrmg_launch_count(void);
+/* Host-only: allocations whose guard bands were found overwritten when they were freed.
+ * Guard bands (4 KB of 0xFF on both sides of every device allocation of the library) are
+ * enabled by the environment variable WRMG_GUARD=1 at the first allocation; 0 otherwise. */
+int64_t wrmg_guard_violations(void);
 
 /* Host-only planning query (no device needed): sizes of the finest level and
  * hierarchy for a configuration, for tests of the host setup logic (H3). */

@@ -13,6 +13,7 @@ from ._lib import (  # noqa: F401
     WrmgError,
     exported_symbols,
     launch_count,
+    guard_violations,
     lib,
     wrmg_batched_lu,
     wrmg_fill_uniform,

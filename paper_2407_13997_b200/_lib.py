@@ -71,6 +71,7 @@ _sig = {
     "wrmg_profile": (c_i32, [c_vp, c_i32]),
     "wrmg_kernel_stats": (c_i32, [c_vp, c_vp]),
     "wrmg_launch_count": (c_i64, []),
+    "wrmg_guard_violations": (c_i64, []),
     "wrmg_debug_fetch": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64]),
     "wrmg_nccl_unique_id": (c_i32, [c_vp]),
     "wrmg_hessenberg_eig": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
@@ -86,6 +87,11 @@ for _name, (_res, _args) in _sig.items():
 
 def launch_count():
     return lib.wrmg_launch_count()
+
+
+def guard_violations():
+    """Allocations whose guard bands were overwritten (WRMG_GUARD=1 runs)."""
+    return lib.wrmg_guard_violations()
 
 
 def exported_symbols():

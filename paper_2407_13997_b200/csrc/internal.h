@@ -231,6 +231,10 @@ struct wrmg_ctx {
   int64_t nt = 1;
   double dt = 0;
   cudaStream_t stream = nullptr;
+  // side stream + events: the boundary-class sweep kernels run concurrently with the
+  // symmetric-class one (both add into u with FP64 atomics)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   wrmg::RefElement ref;
   wrmg::Temporal tm;
   std::vector<wrmg::Level> lv;  // 0 = coarsest

@@ -381,7 +381,8 @@ __device__ __forceinline__ void mac_step(const MacArgs &P, double *ring, uint64_
         const double *p = gp[yl / K] + ((yl % K) * RWX + xl) * VPC;
         if constexpr (NQ == 2) return *reinterpret_cast<const double2 *>(p);
         else if constexpr (NQ == 1) return *p;
-        else return W::ld(p);
+        else if constexpr (NQ == 3) return V3{p[0], p[1], p[2]};  // shared memory: plain loads, not __ldg
+        else return V4{*reinterpret_cast<const double2 *>(p), *reinterpret_cast<const double2 *>(p + 2)};
       };
       V am[KK], ak[KK];
 #pragma unroll

@@ -207,9 +207,122 @@ __device__ __forceinline__ void sym_patch_chunk(const SymTab &P, const int *snod
   }
 }
 
+// The same chunk with y kept in the warp's shared-memory buffer buf[slot][lane][a]
+// instead of registers (fewer live registers -> more warps per SM); on return buf
+// holds the weighted corrections wt[slot] x[slot] for the contiguous atomics.
+template <int D, int B, int VO, int MODE0, int NQ>
+__device__ __forceinline__ void sym_block_s(const SymTab &P, double *yb, double *ycar, int lane) {
+  auto Y = [&](int j, int a) -> double & { return yb[j * 32 * NQ + a]; };
+  double t[NQ][D];
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double yv[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) yv[j] = Y(B + j, a);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(P.V[VO + j * D + i], yv[j], s);
+      t[a][i] = s;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const int md = MODE0 + i;
+    double gh[NQ];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) gh[a] = t[a][i];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 < NQ; ++b2) s = fma(P.S[md * 16 + a * NQ + b2], gh[b2], s);
+      t[a][i] = s;
+    }
+    const double sg = P.sig[md];
+    double v = t[NQ - 1][i], pp = sg;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, v, d);
+      v = fma(lane >= d ? pp : 0.0, o, v);
+      pp *= pp;
+    }
+    double pw = 1.0, bs = sg;
+#pragma unroll
+    for (int bit = 0; bit < 6; ++bit) {
+      pw *= (((lane + 1) >> bit) & 1) ? bs : 1.0;
+      bs *= bs;
+    }
+    const double yc = ycar[md];
+    const double yn = fma(pw, yc, v);
+    double yp = __shfl_up_sync(0xffffffffu, yn, 1);
+    if (lane == 0) yp = yc;
+#pragma unroll
+    for (int a = 0; a < NQ - 1; ++a) t[a][i] = fma(P.S[md * 16 + a * NQ + 0], yp, t[a][i]);
+    t[NQ - 1][i] = yn;
+    const double last = __shfl_sync(0xffffffffu, yn, 31);
+    __syncwarp();
+    if (lane == 0) ycar[md] = last;
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; ++a)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) s = fma(P.V[VO + j * D + i], t[a][i], s);
+      Y(B + j, a) = s;
+    }
+}
+
+template <int K, int NQ>
+__device__ __forceinline__ void sym_patch_chunk_s(const SymTab &P, const int *snode, const double *swt, double *ycar,
+                                                  int n, bool valid, int64_t NT, const double *__restrict__ r,
+                                                  int lane, double *buf) {
+  using S = Sh<K>;
+  constexpr int MP = S::MP;
+  double *yb = buf + lane * NQ;
+  {  // gather (slot order), y = U^T g into the buffer
+    double g[NQ][MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) {
+      const double *src = r + (int64_t)snode[j] * NT + (int64_t)n * NQ;
+      if constexpr (NQ == 2) {
+        const double2 v = valid ? __ldg(reinterpret_cast<const double2 *>(src)) : make_double2(0.0, 0.0);
+        g[0][j] = v.x;
+        g[1][j] = v.y;
+      } else {
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) g[a][j] = valid ? __ldg(src + a) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double y[MP];
+      sym_fwd<K>(g[a], y);
+#pragma unroll
+      for (int j = 0; j < MP; ++j) yb[j * 32 * NQ + a] = y[j];
+    }
+  }
+  sym_block_s<S::D0, S::B0, S::V0, S::B0, NQ>(P, yb, ycar, lane);
+  sym_block_s<S::D1, S::B1, S::V1, S::B1, NQ>(P, yb, ycar, lane);
+  sym_block_s<S::D2, S::B2, S::V2, S::B2, NQ>(P, yb, ycar, lane);
+  sym_block_s<S::D3, S::B3, S::V3, S::B3, NQ>(P, yb, ycar, lane);
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double y[MP], x[MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) y[j] = yb[j * 32 * NQ + a];
+    sym_bwd<K>(y, x);
+#pragma unroll
+    for (int j = 0; j < MP; ++j) yb[j * 32 * NQ + a] = swt[j] * x[j];
+  }
+}
+
 // Patches one per warp, FP64 atomics for the weighted additive scatter.
 template <int K, int NQ>
-__global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, const int32_t *__restrict__ list,
+__global__ void __launch_bounds__(128, 4) k_sweep_sym(int N, int64_t npatch, const int32_t *__restrict__ list,
                                                       const int32_t *__restrict__ pnodes,
                                                       const __grid_constant__ SymTab P,
                                                       const double *__restrict__ wnode, double omega,
@@ -240,10 +353,7 @@ __global__ void __launch_bounds__(128, 3) k_sweep_sym(int N, int64_t npatch, con
       // contiguous run of 32 NQ atomics per node (lanes on consecutive doubles: fewer
       // L2 sectors per instruction than lane = slab with stride NQ)
       double *stg = stage + (size_t)w * MP * 32 * NQ;
-      sym_patch_chunk<K, NQ>(P, snode[w], sycar[w], n, valid, NT, r, lane, [&](int a, const double(&x)[MP]) {
-#pragma unroll
-        for (int j = 0; j < MP; ++j) stg[(j * 32 + lane) * NQ + a] = swt[w][j] * x[j];
-      });
+      sym_patch_chunk_s<K, NQ>(P, snode[w], swt[w], sycar[w], n, valid, NT, r, lane, stg);
       __syncwarp();
       const int64_t t0 = (int64_t)ch * 32 * NQ;
       const int nv = (int)min((int64_t)32 * NQ, NT - t0);  // valid values of this chunk
@@ -349,7 +459,7 @@ void sym_launch(const Level &L, int N, const double *r, double *u, double omega,
   const int64_t np = L.ntile > 0 ? L.nsingle : L.nsym;
   if (np > 0) {
     const int64_t nblk = (np + 3) / 4;
-    const int grid = (int)std::min<int64_t>(nblk, (int64_t)6 * num_sms());
+    const int grid = (int)std::min<int64_t>(nblk, (int64_t)10 * num_sms());
     const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
     smem_optin((const void *)k_sweep_sym<K, NQ>, smem);
     k_sweep_sym<K, NQ><<<grid, 128, smem, s>>>(N, np, L.ntile > 0 ? L.sym_single : nullptr, L.sym_nodes, L.symtab,
@@ -362,7 +472,7 @@ template <int K, int NQ>
 void sym_list_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s, int64_t np,
                      const int32_t *list) {
   if (np <= 0) return;
-  const int grid = (int)std::min<int64_t>((np + 3) / 4, (int64_t)6 * num_sms());
+  const int grid = (int)std::min<int64_t>((np + 3) / 4, (int64_t)10 * num_sms());
   const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
   smem_optin((const void *)k_sweep_sym<K, NQ>, smem);
   k_sweep_sym<K, NQ><<<grid, 128, smem, s>>>(N, np, list, L.sym_nodes, L.symtab, L.wnode, omega, r, u);

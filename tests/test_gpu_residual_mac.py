@@ -1,10 +1,9 @@
 """GPU parity of the macro-block residual (kernels_residual_mac.cu), which runs on
-levels with >= 50 000 lattice nodes: full vectors against the oracle's explicit
+levels with >= 5000 lattice nodes: full vectors against the oracle's explicit
 space-time operator (r = b - A u, eq. heatfem, R1-R5) and y = A u, for P1 / P2 / P3
-in space, DG0 ... DG3 in time (NQ = 3 takes the 30-value chunk and the gather
-combination, the others the butterfly), slab counts that leave a ragged last
-time chunk, and Neumann boundaries (boundary rows go through the fix-up kernel
-k_residual_rows)."""
+in space, DG0 ... DG3 in time (the TMA form for P1 / P2 at every q and P3 at q <= 1,
+the L1 form for P3 x DG2 / DG3), slab counts that leave a ragged last 16-slab chunk,
+and Neumann boundaries (boundary rows go through the fix-up kernel k_residual_rows)."""
 import numpy as np
 import pytest
 
@@ -23,6 +22,14 @@ CASES = [  # n, k, q, N, bc
     (224, 1, 0, 40, "dirichlet0"),
     (224, 1, 1, 3, "neumann"),
     (80, 3, 1, 4, "neumann"),
+    # TMA form with 3 and 4 values per lane (P1 / P2 x DG2, DG3)
+    (112, 2, 2, 4, "dirichlet0"),
+    (112, 2, 3, 3, "neumann"),
+    (224, 1, 2, 5, "dirichlet0"),
+    (224, 1, 3, 3, "dirichlet0"),
+    # levels between 5000 and 50 000 nodes (the macro kernel runs from 5000)
+    (32, 3, 1, 9, "dirichlet0"),
+    (40, 2, 2, 6, "neumann"),
 ]
 
 
@@ -31,7 +38,7 @@ def test_macro_block_residual(n, k, q, N, bc):
     import paper_2407_13997_b200 as w
     from oracle import heat
     p = heat.unit_square_problem(n, k, q, N, 1.0 / N, bc="neumann" if bc == "neumann" else "dirichlet")
-    assert p.nnode >= 50000  # the macro-block kernel's level-size condition
+    assert p.nnode >= 5000  # the macro-block kernel's level-size condition
     c = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=1.0 / N, bc=bc)
     u = wi.spacetime_field(p.nnode, N, q, seed=11)
     b = wi.spacetime_field(p.nnode, N, q, seed=12)
