@@ -218,10 +218,12 @@ __device__ __forceinline__ void mac_accum_ld_part(int part, const LD &ld, const 
   if constexpr (K == 1) mac_accum_ld_k1(ld, C, am, ak);
   else if constexpr (K == 2) {
     if (part == 0) mac_accum_ld_k2_p0(ld, C, am, ak);
-    else mac_accum_ld_k2_p1(ld, C, am, ak);
+    else if (part == 1) mac_accum_ld_k2_p1(ld, C, am, ak);
+    else mac_accum_ld_k2(ld, C, am, ak);
   } else {
     if (part == 0) mac_accum_ld_k3_p0(ld, C, am, ak);
-    else mac_accum_ld_k3_p1(ld, C, am, ak);
+    else if (part == 1) mac_accum_ld_k3_p1(ld, C, am, ak);
+    else mac_accum_ld_k3(ld, C, am, ak);
   }
 }
 
@@ -353,7 +355,8 @@ __device__ __forceinline__ void mac_step(const MacArgs &P, double *ring, uint64_
   constexpr int RWX = K * MX + 2 * K;
   constexpr int GROUP = K * RWX * VPC;
   constexpr int KK = K * K;
-  constexpr int T0 = (K == 1 || PART == 0) ? 0 : K, T1 = (K == 1 || PART == 1) ? KK : K;
+  // PART 0: rows of line b = 0; 1: lines b >= 1; 2: every row of the macro
+  constexpr int T0 = (K == 1 || PART != 1) ? 0 : K, T1 = (K == 1 || PART != 0) ? KK : K;
   const int n = c * SPC + sl;
   const bool valid = n < N;
   const int64_t tg = (int64_t)(valid ? n : N - 1) * NQ;
@@ -419,8 +422,8 @@ __device__ __forceinline__ void mac_step(const MacArgs &P, double *ring, uint64_
     }
 }
 
-template <int K, int NQ, int MX, int R>
-__global__ void __launch_bounds__(16 * MX * (K > 1 ? 2 : 1)) k_residual_mac(const __grid_constant__ CUtensorMap umap,
+template <int K, int NQ, int MX, int R, bool SPLIT = true>
+__global__ void __launch_bounds__(16 * MX * (K > 1 && SPLIT ? 2 : 1)) k_residual_mac(const __grid_constant__ CUtensorMap umap,
                                                           const __grid_constant__ MacArgs P, int Lx, int Ly,
                                                           int64_t NT, int nstrips, int nmy, int JS,
                                                           const uint8_t *__restrict__ rcls,
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(16 * MX * (K > 1 ? 2 : 1)) k_residual_mac(cons
   extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[R];
   double *prevq = ring + R * GROUP;  // [2][MX][JS][KK]: (M u)_{last slab}[q] of the previous chunk (by parity)
-  constexpr int NPART = K > 1 ? 2 : 1;  // warps per macro pair: rows of line b = 0 / lines b >= 1
+  constexpr int NPART = K > 1 && SPLIT ? 2 : 1;  // warps per macro pair: rows of line b = 0 / lines b >= 1
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int part = w % NPART, pw = w / NPART;
   const int h = lane >> 4, sl = lane & 15;
@@ -474,7 +477,10 @@ __global__ void __launch_bounds__(16 * MX * (K > 1 ? 2 : 1)) k_residual_mac(cons
       const int hi = (st / ns) * ngrp + (st - (st / ns) * ns) + 2;
       while (issued <= hi && issued - R < lo) issue(issued++);
     }
-    if (part == 0)
+    if (NPART == 1 && K > 1)
+      mac_step<K, NQ, MX, R, 2>(P, ring, full, prevq, Lx, Ly, NT, JS, rcls, b, r, apply, c, jj, jm, lo, im, mloc, sl, N,
+                                active);
+    else if (part == 0)
       mac_step<K, NQ, MX, R, 0>(P, ring, full, prevq, Lx, Ly, NT, JS, rcls, b, r, apply, c, jj, jm, lo, im, mloc, sl, N,
                                 active);
     else
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(16 * MX * (K > 1 ? 2 : 1)) k_residual_mac(cons
   }
 }
 
-template <int K, int NQ, int MX, int R>
+template <int K, int NQ, int MX, int R, bool SPLIT = true>
 bool mac_launch(const Level &L, int N, const MacArgs &P, const double *u, const double *b, double *r, int apply,
                 cudaStream_t s) {
   constexpr int VPC = 16 * NQ;
@@ -501,8 +507,8 @@ bool mac_launch(const Level &L, int N, const MacArgs &P, const double *u, const 
   nseg = (nmy + JS - 1) / JS;
   const size_t smem = ((size_t)R * K * RWX * VPC + (size_t)2 * MX * JS * K * K) * sizeof(double);
   if (smem > 200 * 1024) return false;
-  smem_optin((const void *)k_residual_mac<K, NQ, MX, R>, (int)smem);
-  k_residual_mac<K, NQ, MX, R><<<nstrips * nseg, 16 * MX * (K > 1 ? 2 : 1), smem, s>>>(umap, P, L.Lx, L.Ly, NT, nstrips, nmy, JS,
+  smem_optin((const void *)k_residual_mac<K, NQ, MX, R, SPLIT>, (int)smem);
+  k_residual_mac<K, NQ, MX, R, SPLIT><<<nstrips * nseg, 16 * MX * (K > 1 && SPLIT ? 2 : 1), smem, s>>>(umap, P, L.Lx, L.Ly, NT, nstrips, nmy, JS,
                                                                         L.rcls, b, r, apply);
   ++g_launches;
   return true;
@@ -547,7 +553,12 @@ bool launch_residual_mac(const Level &L, int k, int q, int N, const Temporal &tm
       const char *e = getenv("WRMG_MAC_K2");  // with 8); WRMG_MAC_K2=8 for the narrower form (A/B)
       return e ? atoi(e) : 16;
     }();
-    if (k2mx == 16) {
+    static const bool k2split = [] {  // WRMG_MAC_K2_SPLIT=0: P2 macros without the two-warp row split (A/B)
+      const char *e = getenv("WRMG_MAC_K2_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    if (k == 2 && q == 1 && k2mx == 16 && !k2split) ok = mac_launch<2, 2, 16, 4, false>(L, N, P, u, b, r, apply, s);
+    if (!ok && k2mx == 16) {
       WRMG_MAC(2, 2, 16, 4)
     }
     if (!ok) {
