@@ -337,6 +337,10 @@ __device__ __forceinline__ double block_entry(const int32_t *__restrict__ rowptr
 // idx[c] = the column of A holding column c of the inverse.  Returns 0 or 1 + the
 // first column with |pivot| < tol.
 constexpr int GJB = 8;
+// doubles of shared memory per block in k_ns_factor_warp: A, X, and the int arrays (piv, idx, nodes)
+__host__ __device__ constexpr size_t ns_factor_warp_doubles(int m, int mp) {
+  return (size_t)m * m + (size_t)GJB * m + ((size_t)(2 * m + mp) + 1) / 2 + 2;
+}
 __device__ __forceinline__ void dmma_ns(double &c0, double &c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
@@ -621,6 +625,228 @@ __device__ int gj_invert_smem_wp(double *A, int m, double tol, double *X, int *p
   }
   __syncthreads();
   return s_info;
+}
+
+// Warp-per-block Gauss-Jordan (m <= 32 RPL): the same elimination as
+// gj_invert_smem_wp (identical pivots and operations per entry) carried out by one
+// warp on its own block -- panel in registers, interchanges and DMMA rank-GJB
+// updates by the same warp -- so blocks never wait at CTA barriers and a CTA keeps
+// several blocks in flight (one per warp).
+template <int RPL>
+__device__ int gj_invert_warp(double *A, int m, double tol, double *X, int *piv, int *idx, int lane) {
+  int info = 0;
+  for (int k0 = 0; k0 < m; k0 += GJB) {
+    const int nb = min(GJB, m - k0), k1 = k0 + nb;
+    double P[RPL][GJB];
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+#pragma unroll
+      for (int t = 0; t < GJB; ++t) P[s][t] = (r < m && t < nb) ? A[r * m + k0 + t] : 0.0;
+    }
+#pragma unroll
+    for (int tc = 0; tc < GJB; ++tc) {
+      if (tc >= nb) break;
+      const int c = k0 + tc;
+      double bv = -1.0;
+      int bi = m;
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) {
+        const int r = lane + 32 * s;
+        const double v = fabs(P[s][tc]);
+        if (r >= c && r < m && v > bv) {
+          bv = v;
+          bi = r;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (!(bv >= tol) && info == 0) info = c + 1;
+      const int sp = bi >> 5, lp = bi & 31, sc = c >> 5, lc = c & 31;
+      double prow[GJB], crow[GJB];
+#pragma unroll
+      for (int t = 0; t < GJB; ++t) {
+        double vp = 0.0, vc = 0.0;
+#pragma unroll
+        for (int s = 0; s < RPL; ++s) {
+          vp = (s == sp) ? P[s][t] : vp;
+          vc = (s == sc) ? P[s][t] : vc;
+        }
+        prow[t] = __shfl_sync(0xffffffffu, vp, lp);
+        crow[t] = __shfl_sync(0xffffffffu, vc, lc);
+      }
+      const double pv = prow[tc];
+      const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
+      double newc[GJB];
+#pragma unroll
+      for (int t = 0; t < GJB; ++t) newc[t] = (t == tc) ? pinv : prow[t] * pinv;
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) {
+        const int r = lane + 32 * s;
+        if (r == bi && bi != c) {
+#pragma unroll
+          for (int t = 0; t < GJB; ++t) P[s][t] = crow[t];
+        }
+        if (r == c) {
+#pragma unroll
+          for (int t = 0; t < GJB; ++t) P[s][t] = newc[t];
+        } else {
+          const double fr = P[s][tc];
+#pragma unroll
+          for (int t = 0; t < GJB; ++t)
+            if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
+          P[s][tc] = -fr * pinv;
+        }
+      }
+      if (lane == 0) piv[c] = bi;
+    }
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+      if (r < m)
+#pragma unroll
+        for (int t = 0; t < GJB; ++t)
+          if (t < nb) A[r * m + k0 + t] = P[s][t];
+    }
+    __syncwarp();
+    for (int j = lane; j < m; j += 32) {
+      if (j >= k0 && j < k1) continue;
+      for (int c = k0; c < k1; ++c) {
+        const int p = piv[c];
+        if (p != c) {
+          const double t1 = A[c * m + j];
+          A[c * m + j] = A[p * m + j];
+          A[p * m + j] = t1;
+        }
+      }
+      for (int t = 0; t < nb; ++t) X[t * m + j] = A[(k0 + t) * m + j];
+    }
+    for (int e = lane; e < nb * nb; e += 32) X[(e / nb) * m + k0 + (e % nb)] = 0.0;
+    __syncwarp();
+    {
+      const int nt8 = (m + 7) / 8, pt = k0 / 8;
+      const int lr = lane >> 2, lcc = lane & 3;
+      for (int it = 0; it < nt8 * nt8; ++it) {
+        const int tr = it / nt8, tcl = it - tr * nt8;
+        if (tcl == pt) continue;
+        const int R = tr * 8 + lr;
+        const bool rok = R < m, rpiv = R >= k0 && R < k1;
+        double cc[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int J = tcl * 8 + 2 * lcc + e;
+          cc[e] = (rok && !rpiv && J < m) ? A[R * m + J] : 0.0;
+        }
+        const int Jb = tcl * 8 + lr;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = 4 * h + lcc;
+          const double a = (rok && t < nb) ? A[R * m + k0 + t] : 0.0;
+          const double bb = (t < nb && Jb < m) ? X[t * m + Jb] : 0.0;
+          dmma_ns(cc[0], cc[1], a, bb);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int J = tcl * 8 + 2 * lcc + e;
+          if (rok && J < m) A[R * m + J] = cc[e];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    for (int c = 0; c < m; ++c) idx[c] = c;
+    for (int c = m - 1; c >= 0; --c) {
+      const int p = piv[c], t = idx[c];
+      idx[c] = idx[p];
+      idx[p] = t;
+    }
+  }
+  __syncwarp();
+  return info;
+}
+
+// One warp per (patch, slab) block, WPB blocks per CTA (shared memory: WPB private
+// m x m matrices), blocks b = blockIdx.x WPB + w over npatch N: assembly as in
+// k_ns_factor, warp-per-block Gauss-Jordan, column-major inverse out.
+template <int NQ, int WPB, int RPL>
+__global__ void __launch_bounds__(32 * WPB) k_ns_factor_warp(int mp, int N, int64_t nblk, int64_t mstride,
+                                                             const int32_t *__restrict__ pnodes,
+                                                             const double *__restrict__ Mv,
+                                                             const double *__restrict__ KGv,
+                                                             const double *__restrict__ conv, NSTime tm,
+                                                             double *__restrict__ out, int32_t *__restrict__ info,
+                                                             const int32_t *__restrict__ ppos,
+                                                             const int32_t *__restrict__ pvv) {
+  extern __shared__ __align__(16) double smem[];
+  const int m = NQ * mp;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t per = ns_factor_warp_doubles(m, mp);
+  double *A = smem + w * per, *X = A + (size_t)m * m;
+  int *piv = (int *)(X + GJB * m);
+  int *idx = piv + m;
+  int *nodes = idx + m;
+  const int64_t NT = (int64_t)N * NQ;
+  for (int64_t blk = (int64_t)blockIdx.x * WPB + w; blk < nblk; blk += (int64_t)gridDim.x * WPB) {
+    const int64_t p = blk / N;
+    const int n = (int)(blk - p * N);
+    for (int i = lane; i < mp; i += 32) nodes[i] = pnodes[p * mp + i];
+    __syncwarp();
+    const int npair = mp * mp;
+    for (int e = lane; e < npair; e += 32) {
+      const int ii = e / mp, jj = e - ii * mp;
+      const bool pad = nodes[ii] < 0 || nodes[jj] < 0;
+      const int64_t pe = (p * mp + ii) * mp + jj;
+      const int pos = pad ? -1 : __ldg(ppos + pe);
+      const int vv = pad ? -1 : __ldg(pvv + pe);
+      const double mv = pos >= 0 ? __ldg(Mv + pos) : 0.0, kg = pos >= 0 ? __ldg(KGv + pos) : 0.0;
+      double cv[NQ];
+      const double *cp = conv + (int64_t)(vv >= 0 ? vv : 0) * NT + (int64_t)n * NQ;
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) cv[c] = (pos >= 0 && vv >= 0) ? __ldg(cp + c) : 0.0;
+#pragma unroll
+      for (int a = 0; a < NQ; ++a)
+#pragma unroll
+        for (int bb = 0; bb < NQ; ++bb) {
+          const int rho = ii * NQ + a, sig = jj * NQ + bb;
+          double v;
+          if (pad) {
+            v = (rho == sig) ? 1.0 : 0.0;
+          } else if (pos < 0) {
+            v = 0.0;
+          } else {
+            v = tm.CE[a * NQ + bb] * mv + tm.Mt[a * NQ + bb] * kg;
+            if (vv >= 0)
+#pragma unroll
+              for (int c = 0; c < NQ; ++c) v = fma(tm.T[(a * NQ + bb) * NQ + c], cv[c], v);
+          }
+          A[rho * m + sig] = v;
+        }
+    }
+    __syncwarp();
+    double rn = 0.0;  // max row norm (R10 tolerance)
+    for (int r = lane; r < m; r += 32) {
+      double sum = 0.0;
+      for (int c = 0; c < m; ++c) sum += fabs(A[r * m + c]);
+      rn = fmax(rn, sum);
+    }
+    for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
+    const int st = gj_invert_warp<RPL>(A, m, 1e-14 * rn, X, piv, idx, lane);
+    double *o = out + blk * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+    for (int e = lane; e < m * m; e += 32) {
+      const int sig = e / m, rho = e - sig * m;
+      o[e] = A[rho * m + idx[sig]];
+    }
+    if (lane == 0) info[blk] = st;
+    __syncwarp();
+  }
 }
 
 // One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
@@ -1746,7 +1972,28 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
   }();
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
-    if (wp && m <= 96) {
+    // WRMG_NS_FACTOR_WARP=1: one warp per block, four blocks per CTA (measured slower:
+    // C3 factor@L4 134 vs 86 ms -- one warp per scheduler exposes every latency)
+    static const bool warp_blocks = [] {
+      const char *e = getenv("WRMG_NS_FACTOR_WARP");
+      return e && e[0] == '1';
+    }();
+    const size_t perw = ns_factor_warp_doubles(m, mp) * sizeof(double);
+    if (warp_blocks && wp && m <= 96 && perw <= 56 * 1024) {
+      const int wpb = (int)std::min<size_t>(4, (220 * 1024) / perw);
+      const int64_t nblk = npatch * N;
+      const int grid = (int)std::min<int64_t>((nblk + wpb - 1) / wpb, (int64_t)8 * num_sms());
+      const size_t smw = perw * wpb;
+      if (wpb == 4) {
+        smem_optin((const void *)k_ns_factor_warp<NQ, 4, 3>, (int)smw);
+        k_ns_factor_warp<NQ, 4, 3><<<grid, 128, smw, s>>>(mp, N, nblk, mstride, pnodes, A.val, A.val2, conv, tm, out,
+                                                          info, ppos, pvv);
+      } else {
+        smem_optin((const void *)k_ns_factor_warp<NQ, 1, 3>, (int)perw);
+        k_ns_factor_warp<NQ, 1, 3><<<grid, 32, perw, s>>>(mp, N, nblk, mstride, pnodes, A.val, A.val2, conv, tm, out,
+                                                         info, ppos, pvv);
+      }
+    } else if (wp && m <= 96) {
       smem_optin((const void *)k_ns_factor<NQ, 128, 3>, (int)sm);
       k_ns_factor<NQ, 128, 3><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
                                                     vvptr, conv, tm, out, info, ppos, pvv);
