@@ -196,6 +196,23 @@ wrmg_status wrmg_level_size(const wrmg_ctx *ctx, int32_t level, int64_t *nnode);
 wrmg_status wrmg_fgmres(wrmg_ctx *ctx, const double *b, double *x, int32_t restart, int32_t maxit,
                         double rtol, double atol, int32_t *iters, double *relres);
 
+/* ncycles stationary multigrid iterations u <- u + B (b - A u), B = one wrmg_vcycle (the C5
+ * protocol: 20 V(1,1) cycles from u = 0).  u, b: device vectors as for
+ * wrmg_residual (strips: u's ghost columns are refreshed).  Two scratch vectors are owned by
+ * the context (allocated at the first call). */
+wrmg_status wrmg_stationary(wrmg_ctx *ctx, const double *b, double *u, int32_t ncycles);
+
+/* Serving form of wrmg_fgmres on HOST buffers: solves A x_i = b_i for nrhs right-hand sides
+ * b_host[i] -> x_host[i] (each ndof doubles in the owned layout of wrmg_layout; page-locked
+ * memory recommended, pageable accepted).  The library owns two device input and two output
+ * buffers and a copy stream: the upload of b_{i+1} and the download of x_{i-1} run on the copy
+ * engines while right-hand side i is solved.  iters / relres (may be NULL) receive nrhs
+ * values.  Returns the first non-OK status of the solves (all are attempted); the host
+ * results are complete when the call returns. */
+wrmg_status wrmg_fgmres_host(wrmg_ctx *ctx, int32_t nrhs, const double *const *b_host, double *const *x_host,
+                             int32_t restart, int32_t maxit, double rtol, double atol, int32_t *iters,
+                             double *relres);
+
 /* Navier-Stokes Newton-FGMRES-WRMG (H14, R22): solves F(U) = 0
  * from U (constrained rows set to the boundary values), relinearising every
  * level and refactorising every (patch, slab) block at each step, FGMRES(30)

@@ -59,6 +59,8 @@ _sig = {
     "wrmg_prolong_add": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
     "wrmg_level_size": (c_i32, [c_vp, c_i32, _P(c_i64)]),
     "wrmg_fgmres": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_dbl, c_dbl, _P(c_i32), _P(c_dbl)]),
+    "wrmg_fgmres_host": (c_i32, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_dbl, c_dbl, _P(c_i32), _P(c_dbl)]),
+    "wrmg_stationary": (c_i32, [c_vp, c_vp, c_vp, c_i32]),
     "wrmg_newton": (c_i32, [c_vp, c_vp, c_dbl, c_i32, _P(c_i32), _P(c_i32)]),
     "wrmg_newton_rhs": (c_i32, [c_vp, c_vp, c_vp, c_dbl, c_i32, _P(c_i32), _P(c_i32)]),
     "wrmg_batched_lu": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp]),
@@ -304,6 +306,23 @@ class Context:
         if st not in (0, 5, 6):
             _check(st, self._h)
         return its.value, rel.value, STATUS[st]
+
+    def stationary(self, b, u, ncycles):
+        """wrmg_stationary: ncycles of u <- u + V(b - A u) (device vectors)."""
+        _check(lib.wrmg_stationary(self._h, _ptr(b), _ptr(u), int(ncycles)), self._h)
+
+    def fgmres_host(self, bs, xs, restart=30, maxit=200, rtol=1e-8, atol=0.0):
+        """wrmg_fgmres_host: solves for host (CPU, preferably pinned) float64 tensors bs[i] -> xs[i],
+        uploads / downloads pipelined inside the library.  Returns (iters, relres, status)."""
+        k = len(bs)
+        bp = (c_vp * k)(*[b.data_ptr() for b in bs])
+        xp = (c_vp * k)(*[x.data_ptr() for x in xs])
+        its, rel = (c_i32 * k)(), (c_dbl * k)()
+        st = lib.wrmg_fgmres_host(self._h, k, ctypes.cast(bp, c_vp), ctypes.cast(xp, c_vp), int(restart), int(maxit),
+                                  float(rtol), float(atol), its, rel)
+        if st not in (0, 5, 6):
+            _check(st, self._h)
+        return list(its), list(rel), STATUS[st]
 
     def newton(self, U, rtol=1e-8, maxit=20, rhs=None):
         its, lin = c_i32(), c_i32()

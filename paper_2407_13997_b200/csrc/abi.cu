@@ -2160,6 +2160,82 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
   }
 }
 
+wrmg_status wrmg_stationary(wrmg_ctx *c, const double *b, double *u, int32_t ncycles) {
+  if (!c || !b || !u || ncycles < 0) return WRMG_E_INVALID;
+  DevGuard dg_(c);
+  try {
+    const int top = (int)c->lv.size() - 1;
+    const int64_t n = c->lv.back().nnode * c->nt;
+    if (!c->st_r) {
+      c->st_r = dzalloc<double>(n);
+      c->st_z = dzalloc<double>(n);
+    }
+    for (int it = 0; it < ncycles; ++it) {
+      if (c->strip) halo_forward(c, c->lv.back(), u);
+      prof_residual(c, top, u, b, c->st_r, false);
+      if (c->ns) ns_project(c, c->lv.back(), c->st_r);
+      vcycle_level(c, top, c->st_r, c->st_z);
+      launch_axpy(n, 1.0, c->st_z, u, c->stream);  // strips: z valid on owned and ghost columns
+    }
+    check_launch();
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
+wrmg_status wrmg_fgmres_host(wrmg_ctx *c, int32_t nrhs, const double *const *b_host, double *const *x_host,
+                             int32_t restart, int32_t maxit, double rtol, double atol, int32_t *iters,
+                             double *relres) {
+  if (!c || nrhs < 0 || (nrhs > 0 && (!b_host || !x_host))) return WRMG_E_INVALID;
+  DevGuard dg_(c);
+  try {
+    const int64_t n = c->lv.back().nnode * c->nt;
+    const size_t bytes = (size_t)n * sizeof(double);
+    if (!c->copy) {
+      CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+      for (int j = 0; j < 2; ++j) {
+        c->hb[j] = dalloc<double>(n);
+        c->hx[j] = dalloc<double>(n);
+        CK(cudaEventCreateWithFlags(&c->ev_in[j], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_solved[j], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_out[j], cudaEventDisableTiming));
+      }
+    }
+    cudaStream_t s = c->stream, cs = c->copy;
+    wrmg_status first = WRMG_OK;
+    auto upload = [&](int i) {
+      const int j = i & 1;
+      if (i >= 2) CK(cudaStreamWaitEvent(cs, c->ev_solved[j], 0));  // solve i-2 no longer reads hb[j]
+      CK(cudaMemcpyAsync(c->hb[j], b_host[i], bytes, cudaMemcpyHostToDevice, cs));
+      CK(cudaEventRecord(c->ev_in[j], cs));
+    };
+    if (nrhs > 0) upload(0);
+    for (int i = 0; i < nrhs; ++i) {
+      const int j = i & 1;
+      if (i + 1 < nrhs) upload(i + 1);  // on the copy engines while i is solved
+      CK(cudaStreamWaitEvent(s, c->ev_in[j], 0));
+      if (i >= 2) CK(cudaStreamWaitEvent(s, c->ev_out[j], 0));  // x_{i-2} downloaded from hx[j]
+      int32_t it = 0;
+      double rr = 0.0;
+      const wrmg_status st = wrmg_fgmres(c, c->hb[j], c->hx[j], restart, maxit, rtol, atol, &it, &rr);
+      if (st != WRMG_OK && st != WRMG_E_NOT_CONVERGED && st != WRMG_E_BREAKDOWN) return st;
+      if (st != WRMG_OK && first == WRMG_OK) first = st;
+      if (iters) iters[i] = it;
+      if (relres) relres[i] = rr;
+      CK(cudaEventRecord(c->ev_solved[j], s));
+      CK(cudaStreamWaitEvent(cs, c->ev_solved[j], 0));
+      CK(cudaMemcpyAsync(x_host[i], c->hx[j], bytes, cudaMemcpyDeviceToHost, cs));
+      CK(cudaEventRecord(c->ev_out[j], cs));
+    }
+    CK(cudaStreamSynchronize(cs));
+    CK(cudaStreamSynchronize(s));
+    return first;
+  } catch (const Err &e) {
+    return fail(c, e);
+  }
+}
+
 wrmg_status wrmg_profile(wrmg_ctx *c, int32_t enable) {
   if (!c) return WRMG_E_INVALID;
   DevGuard dg_(c);
@@ -2392,6 +2468,19 @@ void wrmg_destroy(wrmg_ctx *c) {
   if (!c) return;
   DevGuard dg_(c);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  dfree(c->st_r);
+  dfree(c->st_z);
+  if (c->copy) {
+    cudaStreamSynchronize(c->copy);
+    cudaStreamDestroy(c->copy);
+    for (int j = 0; j < 2; ++j) {
+      dfree(c->hb[j]);
+      dfree(c->hx[j]);
+      cudaEventDestroy(c->ev_in[j]);
+      cudaEventDestroy(c->ev_solved[j]);
+      cudaEventDestroy(c->ev_out[j]);
+    }
+  }
   if (c->side) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);

@@ -245,6 +245,11 @@ struct wrmg_ctx {
   std::vector<double *> V, Z;
   double *w = nullptr, *red = nullptr, *red_host = nullptr;
   double *kry = nullptr;   // device-side CGS2 coefficients of the single-rank FGMRES (kernels_krylov.cu)
+  // wrmg_fgmres_host: double-buffered device copies of b / x, copy stream, events
+  double *hb[2] = {nullptr, nullptr}, *hx[2] = {nullptr, nullptr};
+  double *st_r = nullptr, *st_z = nullptr;  // wrmg_stationary scratch
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_solved[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   double *hmap = nullptr;  // mapped pinned host buffer (2 x hmap_cap doubles): small Krylov results without the copy engines
   int hmap_cap = 0;        // doubles per direction: max(1024, 64 nranks)
   double *gred = nullptr;  // strips: all ranks' reduction results (nranks x 64), for wrmg_fgmres
