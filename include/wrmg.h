@@ -111,6 +111,12 @@ typedef struct {
   int32_t own0, own1;   /* owned lattice columns [own0, own1] of the local lattice (0, lx-1 on one rank) */
   int32_t g0;           /* global lattice column of local column 0 */
   int64_t nfree_owned_st; /* free space-time DoFs owned by this rank */
+  /* Navier-Stokes (lx, ly, own0, own1, g0 above describe the velocity lattice; sids
+     u_x: [0, lu), u_y: [lu, 2 lu), p: [2 lu, 2 lu + lpx lpy)); 0 for the heat operator */
+  int64_t lu;             /* velocity lattice nodes lx * ly */
+  int32_t lpx, lpy;       /* pressure lattice nodes per direction */
+  int32_t own0p, own1p;   /* owned pressure lattice columns */
+  int32_t g0p;            /* global pressure lattice column of local column 0 */
 } wrmg_layout_t;
 
 /* Build the hierarchy on the device.  PAPER.md:351-360 (space-only coarsening),

@@ -33,7 +33,8 @@ class wrmg_layout_t(ctypes.Structure):
                 ("ly", c_i32), ("nlevels", c_i32), ("degree", c_i32), ("q", c_i32), ("nslabs", c_i32),
                 ("npatch", c_i64), ("mp_max", c_i32), ("npatch_types", c_i32),
                 ("smooth_dof_updates_per_vcycle", c_i64), ("own0", c_i32), ("own1", c_i32), ("g0", c_i32),
-                ("nfree_owned_st", c_i64)]
+                ("nfree_owned_st", c_i64), ("lu", c_i64), ("lpx", c_i32), ("lpy", c_i32), ("own0p", c_i32),
+                ("own1p", c_i32), ("g0p", c_i32)]
 
 
 class wrmg_kernel_stat(ctypes.Structure):

@@ -228,8 +228,20 @@ NSGeom geom(const wrmg_ctx *c, const Level &L) {
 }
 
 // Pressure mean removal per (slab, temporal node) of a level vector (H15, R19).
+// Strips: the column sums over the owned pressure columns, all-gathered and summed in
+// rank order (every rank subtracts bitwise the same mean).
+void comm_call(wrmg_ctx *c, const std::function<void()> &f);
 void ns_project(wrmg_ctx *c, const Level &L, double *v) {
-  launch_ns_project(v + 2 * L.Lu * c->nt, L.Lp, c->nt, c->proj, c->stream);
+  double *p = v + 2 * L.Lu * c->nt;
+  if (!c->strip) {
+    launch_ns_project(p, L.Lp, c->nt, c->proj, c->stream);
+    return;
+  }
+  const StripInfo &S = L.stp;
+  launch_ns_colsum_owned(p, L.Lpx, (int)(L.Lp / L.Lpx), S.own0, S.own1 - S.own0 + 1, c->nt, c->proj, c->pj_sums,
+                         c->stream);
+  comm_call(c, [&] { c->comm->allgather(c->pj_sums, c->pj_all, (size_t)c->nt, c->stream); });
+  launch_ns_sub_gathered_mean(p, L.Lp, c->nt, c->pj_all, c->comm->nranks, L.gLp, c->pj_sums, c->stream);
 }
 
 void prof_residual(wrmg_ctx *c, int l, const double *u, const double *b, double *r, bool uzero,
@@ -248,7 +260,7 @@ void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
   if (c->ns) {
     const Level &L = c->lv[l];
     launch_ns_sweep(c->q, c->N, L.mp, L.npatch, L.mstride, L.pnodes, L.wnode, L.A, L.nsinv, r, u, om, c->stream);
-    ns_project(c, L, u);
+    if (!c->strip) ns_project(c, L, u);
     return;
   }
   if (c->use_kron && c->lv[l].coloured) {  // one pass per vertex colour: one addition per value and pass
@@ -386,46 +398,127 @@ void comm_call(wrmg_ctx *c, const std::function<void()> &f) {
   }
 }
 
+// The lattice fields of a level vector: heat one lattice; Navier-Stokes u_x, u_y
+// (velocity lattice, degree k + 1) and p (pressure lattice, degree k), each with its
+// own column bookkeeping (ns.h: plan_ns_strip_level).
+struct FieldView {
+  int64_t off;  // first double of the field in the level vector
+  int Lx, Ly, k;
+  int64_t goff;  // global sid of the field's first node (canonical ids)
+  const StripInfo *S;
+};
+int level_fields(const wrmg_ctx *c, const Level &L, FieldView *f) {
+  if (!c->ns) {
+    f[0] = {0, L.Lx, L.Ly, c->k, 0, &L.st};
+    return 1;
+  }
+  const int ku = c->k + 1, kp = c->k;
+  const int Lpy = (int)(L.Lp / L.Lpx);
+  const int64_t GLu = (int64_t)(ku * L.st.gnx + 1) * L.Ly;
+  f[0] = {0, L.Lux, L.Ly, ku, 0, &L.st};
+  f[1] = {L.Lu * c->nt, L.Lux, L.Ly, ku, GLu, &L.st};
+  f[2] = {2 * L.Lu * c->nt, L.Lpx, Lpy, kp, 2 * GLu, &L.stp};
+  return 3;
+}
+// doubles of one halo buffer (k ghost columns of every field)
+int64_t halo_doubles(const wrmg_ctx *c, const Level &L) {
+  FieldView f[3];
+  const int nf = level_fields(c, L, f);
+  int64_t n = 0;
+  for (int i = 0; i < nf; ++i) n += (int64_t)f[i].Ly * f[i].k * c->nt;
+  return n;
+}
+
+// mode 0: pack the columns (c0, nc) of every field into buf; 1: unpack; 2: unpack-add
+size_t halo_cols(wrmg_ctx *c, Level &L, double *v, bool left_side, bool ghosts, double *buf, int mode) {
+  FieldView f[3];
+  const int nf = level_fields(c, L, f);
+  size_t o = 0;
+  for (int i = 0; i < nf; ++i) {
+    const StripInfo &S = *f[i].S;
+    const int c0 = ghosts ? (left_side ? S.lg0 : S.rg0) : (left_side ? S.sl0 : S.sr0);
+    const int nc = ghosts ? (left_side ? S.nlg : S.nrg) : (left_side ? S.nsl : S.nsr);
+    launch_cols(v + f[i].off, f[i].Lx, f[i].Ly, c->nt, c0, nc, buf + o, mode, c->stream);
+    o += (size_t)f[i].Ly * nc * c->nt;
+  }
+  return o;
+}
+
 // ghosts <- owners (both sides)
 void halo_forward(wrmg_ctx *c, Level &L, double *v) {
-  const StripInfo &S = L.st;
-  cudaStream_t s = c->stream;
-  const size_t cnt = (size_t)L.Ly * c->k * c->nt;
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.sl0, S.nsl, L.hx[0], 0, s);
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.sr0, S.nsr, L.hx[2], 0, s);
-  comm_call(c, [&] { c->comm->exchange(L.hx[0], L.hx[1], S.nsl ? cnt : 0, L.hx[2], L.hx[3], S.nsr ? cnt : 0, s); });
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.lg0, S.nlg, L.hx[1], 1, s);
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.rg0, S.nrg, L.hx[3], 1, s);
+  const size_t nL = halo_cols(c, L, v, true, false, L.hx[0], 0);
+  const size_t nR = halo_cols(c, L, v, false, false, L.hx[2], 0);
+  comm_call(c, [&] { c->comm->exchange(L.hx[0], L.hx[1], nL, L.hx[2], L.hx[3], nR, c->stream); });
+  halo_cols(c, L, v, true, true, L.hx[1], 1);
+  halo_cols(c, L, v, false, true, L.hx[3], 1);
 }
 
 // owners += ghosts of the neighbours (both sides)
 void halo_reverse_add(wrmg_ctx *c, Level &L, double *v) {
-  const StripInfo &S = L.st;
-  cudaStream_t s = c->stream;
-  const size_t cnt = (size_t)L.Ly * c->k * c->nt;
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.lg0, S.nlg, L.hx[0], 0, s);
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.rg0, S.nrg, L.hx[2], 0, s);
-  comm_call(c, [&] { c->comm->exchange(L.hx[0], L.hx[1], S.nlg ? cnt : 0, L.hx[2], L.hx[3], S.nrg ? cnt : 0, s); });
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.sl0, S.nsl, L.hx[1], 2, s);
-  launch_cols(v, L.Lx, L.Ly, c->nt, S.sr0, S.nsr, L.hx[3], 2, s);
+  const size_t nL = halo_cols(c, L, v, true, true, L.hx[0], 0);
+  const size_t nR = halo_cols(c, L, v, false, true, L.hx[2], 0);
+  comm_call(c, [&] { c->comm->exchange(L.hx[0], L.hx[1], nL, L.hx[2], L.hx[3], nR, c->stream); });
+  halo_cols(c, L, v, true, false, L.hx[1], 2);
+  halo_cols(c, L, v, false, false, L.hx[3], 2);
 }
 
 // Zero every column this rank does not own: the ghost columns and, on ranks > 0, the
 // local lattice's first column (one cell left of the left ghosts; never refreshed --
 // with Neumann boundaries it is a free row, so dot products must not see it).
 void zero_ghosts(wrmg_ctx *c, Level &L, double *v) {
-  const StripInfo &S = L.st;
-  if (S.own0 > 0) launch_cols(v, L.Lx, L.Ly, c->nt, 0, S.own0, nullptr, 3, c->stream);
-  if (S.own1 + 1 < L.Lx) launch_cols(v, L.Lx, L.Ly, c->nt, S.own1 + 1, L.Lx - S.own1 - 1, nullptr, 3, c->stream);
+  FieldView f[3];
+  const int nf = level_fields(c, L, f);
+  for (int i = 0; i < nf; ++i) {
+    const StripInfo &S = *f[i].S;
+    double *p = v + f[i].off;
+    if (S.own0 > 0) launch_cols(p, f[i].Lx, f[i].Ly, c->nt, 0, S.own0, nullptr, 3, c->stream);
+    if (S.own1 + 1 < f[i].Lx)
+      launch_cols(p, f[i].Lx, f[i].Ly, c->nt, S.own1 + 1, f[i].Lx - S.own1 - 1, nullptr, 3, c->stream);
+  }
+}
+
+// Navier-Stokes strips: every local column of v (owned, ghost and the overlap cells
+// beyond) rewritten from its owner -- all-gather of the owned columns.  The
+// linearisation state needs it: the Vanka blocks of the owned patches integrate over
+// cells up to two columns of cells beyond the owned ones (ns.h).
+void state_refresh(wrmg_ctx *c, Level &L, double *v) {
+  FieldView f[3];
+  const int nf = level_fields(c, L, f);
+  cudaStream_t s = c->stream;
+  size_t o = 0;
+  for (int i = 0; i < nf; ++i) {
+    const StripInfo &S = *f[i].S;
+    const int nown = S.own1 - S.own0 + 1;
+    launch_cols(v + f[i].off, f[i].Lx, f[i].Ly, c->nt, S.own0, nown, c->rf_send + o, 0, s);
+    o += (size_t)f[i].Ly * nown * c->nt;
+  }
+  if ((int64_t)o > c->rf_chunk) throw Err{WRMG_E_INVALID, "state refresh: chunk overflow"};
+  comm_call(c, [&] { c->comm->allgather(c->rf_send, c->rf_recv, (size_t)c->rf_chunk, s); });
+  for (int q = 0; q < c->comm->nranks; ++q) {
+    size_t oq = 0;
+    for (int i = 0; i < nf; ++i) {
+      const StripInfo &S = *f[i].S;
+      const int k = f[i].k, x0q = q * S.nx;
+      const int g0q = q == 0 ? 0 : k * x0q + 1, g1q = k * (x0q + S.nx), nq = g1q - g0q + 1;
+      const int ov0 = std::max(g0q, S.G0), ov1 = std::min(g1q, S.G0 + f[i].Lx - 1);
+      if (ov0 <= ov1)
+        launch_window(c->rf_recv + (int64_t)q * c->rf_chunk + oq, nq, ov0 - g0q, v + f[i].off, f[i].Lx, ov0 - S.G0,
+                      f[i].Ly, ov1 - ov0 + 1, c->nt, s);
+      oq += (size_t)f[i].Ly * nq * c->nt;
+    }
+  }
 }
 
 // One additive sweep on a strip: owned patches add into owned and right-ghost
 // columns; the ghost sums are returned to their owners, then ghosts refreshed.
+void ns_project(wrmg_ctx *c, const Level &L, double *v);
+
 void sweep_strip(wrmg_ctx *c, int l, const double *r, double *u, double om) {
   Level &L = c->lv[l];
   zero_ghosts(c, L, u);
   prof_sweep(c, l, r, u, om);
   halo_reverse_add(c, L, u);
+  if (c->ns) ns_project(c, L, u);  // the pressure mean of the summed update (every rank subtracts the same)
   halo_forward(c, L, u);
 }
 
@@ -657,20 +750,53 @@ double estimate_lambda(wrmg_ctx *c, int l);
 // Navier-Stokes linearisation at the finest-level state W (NULL = zero state):
 // inject W to every level (R13), assemble R N(W) (H1), invert every (patch, slab)
 // block (H4, H5) and the pinned coarse slab blocks (H11).  Synchronises.
+void state_refresh(wrmg_ctx *c, Level &L, double *v);
+
+// Singular (patch, slab) blocks of levels >= l0 -> WRMG_E_SINGULAR with the location.
+void check_ns_patch_info(wrmg_ctx *c, int l0) {
+  c->err_level = c->err_patch = c->err_slab = -1;
+  for (int l = l0; l < (int)c->lv.size(); ++l) {
+    Level &L = c->lv[l];
+    std::vector<int32_t> info((size_t)L.npatch * c->N);
+    CK(cudaMemcpy(info.data(), L.nsinfo, info.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (size_t e = 0; e < info.size(); ++e)
+      if (info[e]) {
+        c->err_level = l;
+        c->err_patch = (int)(e / c->N);
+        c->err_slab = (int)(e % c->N);
+        throw Err{WRMG_E_SINGULAR, "singular Vanka patch block (level " + std::to_string(l) + ", patch " +
+                                       std::to_string(c->err_patch) + ", slab " + std::to_string(c->err_slab) + ")"};
+      }
+  }
+}
+
 void factor_all_ns(wrmg_ctx *c, const double *W) {
   cudaStream_t s = c->stream;
   const int nl = (int)c->lv.size();
   const double *Wl = W;
+  if (c->strip && W) {  // strips: a copy of the state with every local column from its owner
+    Level &F = c->lv.back();
+    CK(cudaMemcpyAsync(F.state, W, F.nnode * c->nt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    state_refresh(c, F, F.state);
+    Wl = F.state;
+  }
   for (int l = nl - 1; l >= 0; --l) {
     Level &L = c->lv[l];
     if (l < nl - 1 && W) {
-      launch_ns_inject(geom(c, L), geom(c, c->lv[l + 1]), c->nt, Wl, L.state, s);
+      if (c->strip) {  // owned coarse columns from owned fine columns, then the refresh
+        const Level &F = c->lv[l + 1];
+        const NSInjMap m{2 * L.st.G0 - F.st.G0, 2 * L.stp.G0 - F.stp.G0, F.st.own0, F.st.own1, F.stp.own0, F.stp.own1};
+        launch_ns_inject(geom(c, L), geom(c, F), c->nt, Wl, L.state, s, &m);
+        state_refresh(c, L, L.state);
+      } else {
+        launch_ns_inject(geom(c, L), geom(c, c->lv[l + 1]), c->nt, Wl, L.state, s);
+      }
       Wl = L.state;
     }
     launch_ns_assemble_conv(geom(c, L), c->nt, c->co.reynolds, true, L.A, L.vvptr, W ? Wl : nullptr, L.conv,
                             c->th_T, s);
     check_launch();
-    if (l >= 1 || nl == 1) {
+    if (l >= 1 || nl == 1 || c->strip) {
       const double m = (double)c->nq * L.mp;
       PScope ps(c, WRMG_K_FACTOR, l, 8.0 * (double)L.npatch * c->N * L.mstride,
                 2.0 * m * m * m * (double)L.npatch * c->N);
@@ -678,6 +804,26 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
                        L.nsinv, L.nsinfo, L.ppos, L.pvv, s);
       check_launch();
     }
+  }
+  if (c->strip) {
+    // the replicated hierarchy (levels below the partitioned ones): its finest level's
+    // state by injection of the owned columns of level 0, summed over ranks in rank order
+    const double *Ws = nullptr;
+    if (W) {
+      const Level &T = c->sub->lv.back(), &L0 = c->lv[0];
+      const int64_t ng = T.nnode * c->nt;
+      const NSInjMap m{-L0.st.G0, -L0.stp.G0, L0.st.own0, L0.st.own1, L0.stp.own0, L0.stp.own1};
+      launch_ns_inject(geom(c->sub, T), geom(c, L0), c->nt, Wl, c->sub_part, s, &m);
+      comm_call(c, [&] { c->comm->allgather(c->sub_part, c->sub_all, (size_t)ng, s); });
+      launch_sum_chunks(c->sub_all, c->comm->nranks, ng, c->sub_w, s);
+      Ws = c->sub_w;
+    }
+    factor_all_ns(c->sub, Ws);
+    CK(cudaStreamSynchronize(s));
+    check_ns_patch_info(c, 0);
+    if (c->cheb)
+      for (int l = 0; l < nl; ++l) c->lam[l] = estimate_lambda(c, l);
+    return;
   }
   Coarse &C = c->coarse;
   Level &L0 = c->lv[0];
@@ -701,20 +847,7 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
   launch_ns_coarse_H(c->q, c->N, C.mp, C.pin, C.nodes, C.sid2c, L0.A, C.nsinvT, C.nsH, C.nsG, s);
   check_launch();
   CK(cudaStreamSynchronize(s));
-  c->err_level = c->err_patch = c->err_slab = -1;
-  for (int l = (nl == 1 ? 0 : 1); l < nl; ++l) {
-    Level &L = c->lv[l];
-    std::vector<int32_t> info((size_t)L.npatch * c->N);
-    CK(cudaMemcpy(info.data(), L.nsinfo, info.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    for (size_t e = 0; e < info.size(); ++e)
-      if (info[e]) {
-        c->err_level = l;
-        c->err_patch = (int)(e / c->N);
-        c->err_slab = (int)(e % c->N);
-        throw Err{WRMG_E_SINGULAR, "singular Vanka patch block (level " + std::to_string(l) + ", patch " +
-                                       std::to_string(c->err_patch) + ", slab " + std::to_string(c->err_slab) + ")"};
-      }
-  }
+  check_ns_patch_info(c, nl == 1 ? 0 : 1);
   std::vector<int32_t> ci(c->N);
   CK(cudaMemcpy(ci.data(), C.nsinfo, c->N * sizeof(int32_t), cudaMemcpyDeviceToHost));
   for (int n = 0; n < c->N; ++n)
@@ -725,6 +858,17 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
     }
   if (c->cheb)  // the relaxed operator changed: new Chebyshev intervals (R-cheb)
     for (int l = 1; l < nl; ++l) c->lam[l] = estimate_lambda(c, l);
+}
+
+// Uniform strips x0 = rank * nx: the transport.
+void make_strip_comm(wrmg_ctx *c) {
+  const int P = c->co.nranks, r = c->co.rank;
+  if (r < 0 || r >= P || c->mesh.nx * P != c->mesh.gnx || c->mesh.x0 != r * c->mesh.nx)
+    throw Err{WRMG_E_INVALID, "strips: need nx * nranks = gnx and x0 = rank * nx"};
+  std::string e;
+  c->comm = c->co.loopback_hub ? make_loop_comm(c->co.loopback_hub, r, P, e)
+                               : make_nccl_comm(c->co.nccl_unique_id, r, P, e);
+  if (!c->comm) throw Err{WRMG_E_NCCL, e};
 }
 
 // Hierarchy of Taylor-Hood levels (problem == WRMG_NAVIER_STOKES).
@@ -752,14 +896,57 @@ void setup_ns(wrmg_ctx *c) {
   }
   std::vector<int> nys;
   std::vector<int> nxs = level_sizes(c->mesh.gnx, c->mesh.gny, c->mesh.ncoarse, &nys);
+  // strips: the coarsest level -- the pinned-pressure direct
+  // solve -- and every level narrower than 2 cells per strip run replicated on every
+  // rank as a single-rank hierarchy (c->sub) below the partitioned levels
+  c->strip = c->co.nranks > 1;
+  if (c->strip) {
+    int lrep = 1;
+    for (int l = 0; l < (int)nxs.size(); ++l) {
+      const int f = c->mesh.gnx / nxs[l];
+      if (c->mesh.nx % f || c->mesh.nx / f < 2) lrep = std::max(lrep, l + 1);
+    }
+    if (lrep >= (int)nxs.size())
+      throw Err{WRMG_E_UNSUPPORTED, "strips: the finest level's strip is narrower than 2 cells"};
+    wrmg_mesh sm{};
+    sm.gnx = nxs[lrep - 1];
+    sm.gny = nys[lrep - 1];
+    sm.x0 = 0;
+    sm.nx = sm.gnx;
+    sm.h = c->mesh.h * (double)(c->mesh.gnx / nxs[lrep - 1]);
+    sm.ncoarse = c->mesh.ncoarse;
+    wrmg_coeffs sc = c->co;
+    sc.rank = 0;
+    sc.nranks = 1;
+    sc.loopback_hub = nullptr;
+    sc.nccl_unique_id = nullptr;
+    const wrmg_status st = wrmg_setup(&sm, c->k, c->q, c->N, c->dt, &sc, &c->sub);
+    if (st != WRMG_OK) throw Err{st, std::string("replicated coarse hierarchy: ") + wrmg_last_error(nullptr, 0, 0, 0)};
+    if ((int)c->sub->lv.size() != lrep) throw Err{WRMG_E_INVALID, "replicated coarse hierarchy: level count"};
+    nxs.erase(nxs.begin(), nxs.begin() + lrep);
+    nys.erase(nys.begin(), nys.begin() + lrep);
+    make_strip_comm(c);
+  } else if (c->mesh.x0 != 0 || c->mesh.nx != c->mesh.gnx) {
+    throw Err{WRMG_E_INVALID, "a partial strip needs nranks > 1"};
+  }
   const int nl = (int)nxs.size();
   std::vector<NSPlan> plans(nl);
   c->lv.resize(nl);
   for (int l = 0; l < nl; ++l) {
     const double h = c->mesh.h * (double)(c->mesh.gnx / nxs[l]);
-    plan_ns_level(nxs[l], nys[l], h, c->k, c->co.bc, c->co.lid_speed, &plans[l]);
-    NSPlan &P = plans[l];
     Level &L = c->lv[l];
+    if (c->strip) {
+      const int f = c->mesh.gnx / nxs[l];
+      try {
+        plan_ns_strip_level(nxs[l], nys[l], c->mesh.x0 / f, c->mesh.nx / f, h, c->k, c->co.bc, c->co.lid_speed,
+                            c->co.rank, c->co.nranks, &plans[l], &L.st, &L.stp);
+      } catch (const std::exception &e) {
+        throw Err{WRMG_E_INVALID, e.what()};
+      }
+    } else {
+      plan_ns_level(nxs[l], nys[l], h, c->k, c->co.bc, c->co.lid_speed, &plans[l]);
+    }
+    NSPlan &P = plans[l];
     L.nx = P.nx;
     L.ny = P.ny;
     L.h = h;
@@ -797,26 +984,45 @@ void setup_ns(wrmg_ctx *c) {
       throw Err{WRMG_E_UNSUPPORTED, "Vanka patch system of size " + std::to_string(m) +
                                         " exceeds one CTA (shared-memory block inverse): lower q or degree"};
     L.mstride = (m * m + 1) & ~(int64_t)1;
-    L.st.own1 = L.Lx - 1;  // NS: single rank, whole lattice
-    L.nfree_owned = L.nfree;
-    if (l >= 1 || nl == 1) {
+    L.gLp = (int64_t)(c->k * nxs[l] + 1) * (c->k * nys[l] + 1);
+    if (!c->strip) {  // single rank: the whole lattices
+      L.st = StripInfo{};
+      L.st.gnx = L.st.nx = L.st.nxl = nxs[l];
+      L.st.own1 = L.Lux - 1;
+      L.stp = L.st;
+      L.stp.own1 = L.Lpx - 1;
+      L.nfree_owned = L.nfree;
+    } else {
+      int64_t nfo = 0;
+      for (int J = 0; J < P.Luy; ++J)
+        for (int I = L.st.own0; I <= L.st.own1; ++I)
+          nfo += !P.con[(int64_t)J * P.Lux + I] + !P.con[P.Lu + (int64_t)J * P.Lux + I];
+      nfo += (int64_t)P.Lpy * (L.stp.own1 - L.stp.own0 + 1);
+      L.nfree_owned = nfo;
+      for (int b = 0; b < 4; ++b) L.hx[b] = dalloc<double>(halo_doubles(c, L));
+    }
+    if (l >= 1 || nl == 1 || c->strip) {
       L.nsinv = dalloc<double>((size_t)L.npatch * c->N * L.mstride);
       L.nsinfo = dalloc<int32_t>((size_t)L.npatch * c->N);
       L.ppos = dalloc<int32_t>((size_t)L.npatch * L.mp * L.mp);
       L.pvv = dalloc<int32_t>((size_t)L.npatch * L.mp * L.mp);
     }
     if (l < nl - 1) {
-      L.vr = dalloc<double>(L.nnode * c->nt);
-      L.vz = dalloc<double>(L.nnode * c->nt);
-      L.vt = dalloc<double>(L.nnode * c->nt);
-      L.state = dalloc<double>(L.nnode * c->nt);
+      L.vr = dzalloc<double>(L.nnode * c->nt);
+      L.vz = dzalloc<double>(L.nnode * c->nt);
+      L.vt = dzalloc<double>(L.nnode * c->nt);
     }
+    if (l < nl - 1 || c->strip) L.state = dzalloc<double>(L.nnode * c->nt);
     CK(cudaStreamSynchronize(s));
   }
   for (int l = 1; l < nl; ++l) {
     std::vector<int32_t> rp, ci, trp, tci;
     std::vector<double> v, tv;
-    plan_ns_interpolation(plans[l - 1], plans[l], rp, ci, v);
+    if (c->strip)
+      plan_ns_strip_interpolation(plans[l - 1], c->lv[l - 1].st, c->lv[l - 1].stp, plans[l], c->lv[l].st,
+                                  c->lv[l].stp, nys[l], rp, ci, v);
+    else
+      plan_ns_interpolation(plans[l - 1], plans[l], rp, ci, v);
     transpose_csr(plans[l].ns, plans[l - 1].ns, rp, ci, v, trp, tci, tv);
     Level &C = c->lv[l - 1];
     C.P.nrow = plans[l].ns;
@@ -831,7 +1037,44 @@ void setup_ns(wrmg_ctx *c) {
     C.R.val = dupload(tv, s);
     CK(cudaStreamSynchronize(s));
   }
-  {
+  if (c->strip) {  // hand-over between level 0 (owned rows) and the replicated hierarchy (global sids)
+    const Level &T = c->sub->lv.back();
+    NSPlan gc;
+    plan_ns_level(T.nx, T.ny, T.h, c->k, c->co.bc, c->co.lid_speed, &gc);
+    StripInfo wu{}, wp{};
+    wu.gnx = wu.nx = wu.nxl = T.nx;
+    wp = wu;
+    std::vector<int32_t> rp, ci, trp, tci;
+    std::vector<double> v, tv;
+    plan_ns_strip_interpolation(gc, wu, wp, plans[0], c->lv[0].st, c->lv[0].stp, nys[0], rp, ci, v);
+    transpose_csr(plans[0].ns, gc.ns, rp, ci, v, trp, tci, tv);
+    Level &X = c->xfer;
+    X.P.nrow = plans[0].ns;
+    X.P.nnz = (int64_t)ci.size();
+    X.P.rowptr = dupload(rp, s);
+    X.P.col = dupload(ci, s);
+    X.P.val = dupload(v, s);
+    X.R.nrow = gc.ns;
+    X.R.nnz = (int64_t)tci.size();
+    X.R.rowptr = dupload(trp, s);
+    X.R.col = dupload(tci, s);
+    X.R.val = dupload(tv, s);
+    const int64_t ng = gc.ns * c->nt;
+    c->sub_r = dzalloc<double>(ng);
+    c->sub_z = dzalloc<double>(ng);
+    c->sub_part = dzalloc<double>(ng);
+    c->sub_w = dzalloc<double>(ng);
+    c->sub_all = dzalloc<double>(ng * c->co.nranks);
+    // state refresh: the largest owned-column block of any rank (rank 0 owns one more column)
+    const Level &F = c->lv.back();
+    const int ku = c->k + 1, kp = c->k;
+    c->rf_chunk = ((int64_t)2 * F.Ly * (ku * F.st.nx + 1) + (int64_t)(F.Lp / F.Lpx) * (kp * F.stp.nx + 1)) * c->nt;
+    c->rf_send = dzalloc<double>(c->rf_chunk);
+    c->rf_recv = dzalloc<double>(c->rf_chunk * c->co.nranks);
+    c->pj_sums = dzalloc<double>(c->nt);
+    c->pj_all = dzalloc<double>(c->nt * c->co.nranks);
+    CK(cudaStreamSynchronize(s));
+  } else {
     Coarse &C = c->coarse;
     const NSPlan &P = plans[0];
     std::vector<int32_t> nodes;
@@ -862,7 +1105,10 @@ void setup_ns(wrmg_ctx *c) {
   }
   c->tmp = dalloc<double>(c->lv.back().nnode * c->nt);
   c->red = dalloc<double>(64 + 64 * kDotBlocksMax);
-  c->proj = dalloc<double>(ns_project_scratch(c->lv.back().Lp, c->nt));
+  {
+    const Level &F = c->lv.back();
+    c->proj = dalloc<double>(std::max<int64_t>(ns_project_scratch(F.Lp, c->nt), (F.Lp / F.Lpx + 1) * c->nt));
+  }
   c->bcg = dupload(plans[nl - 1].g, s);
   for (auto &L : c->lv) {
     launch_ns_assemble_linear(geom(c, L), L.A, c->th_ref, s);
@@ -876,9 +1122,9 @@ void setup_ns(wrmg_ctx *c) {
     c->lam.assign(nl, 0.0);
     c->cd.assign(nl, nullptr);
     c->cbr.assign(nl, nullptr);
-    for (int l = 1; l < nl; ++l) {
-      c->cd[l] = dalloc<double>(c->lv[l].nnode * c->nt);
-      c->cbr[l] = dalloc<double>(c->lv[l].nnode * c->nt);
+    for (int l = c->strip ? 0 : 1; l < nl; ++l) {
+      c->cd[l] = dzalloc<double>(c->lv[l].nnode * c->nt);
+      c->cbr[l] = dzalloc<double>(c->lv[l].nnode * c->nt);
     }
   }
   factor_all_ns(c, nullptr);
@@ -944,9 +1190,14 @@ double estimate_lambda(wrmg_ctx *c, int l) {
   if (!c->strip) {
     launch_fill_uniform(V[0], n, 0, c->co.cheb_seed, s);
   } else {  // R6 generator at the global canonical ids: local row J holds global columns G0 ..
-    const int64_t GLx = (int64_t)c->k * L.st.gnx + 1, rowlen = (int64_t)L.Lx * c->nt;
-    for (int J = 0; J < L.Ly; ++J)
-      launch_fill_uniform(V[0] + J * rowlen, rowlen, (uint64_t)((J * GLx + L.st.G0) * c->nt), c->co.cheb_seed, s);
+    FieldView f[3];
+    const int nf = level_fields(c, L, f);
+    for (int i = 0; i < nf; ++i) {
+      const int64_t GLx = (int64_t)f[i].k * f[i].S->gnx + 1, rowlen = (int64_t)f[i].Lx * c->nt;
+      for (int J = 0; J < f[i].Ly; ++J)
+        launch_fill_uniform(V[0] + f[i].off + J * rowlen, rowlen,
+                            (uint64_t)((f[i].goff + J * GLx + f[i].S->G0) * c->nt), c->co.cheb_seed, s);
+    }
     zero_ghosts(c, L, V[0]);
   }
   launch_ns_mask(L.nnode, c->nt, L.con, nullptr, V[0], V[0], s);  // constrained rows 0
@@ -1039,6 +1290,7 @@ void sub_cycle(wrmg_ctx *c, const double *t, double *z) {
   }
   comm_call(c, [&] { c->comm->allgather(c->sub_part, c->sub_all, (size_t)ng, s); });
   launch_sum_chunks(c->sub_all, c->comm->nranks, ng, c->sub_r, s);
+  if (c->ns) ns_project(S, T, c->sub_r);
   vcycle_level(S, (int)S->lv.size() - 1, c->sub_r, c->sub_z);
   {
     PScope ps(c, WRMG_K_PROLONG, 0, 8.0 * (2 * c->lv[0].nnode + T.nnode) * c->nt, 2.0 * c->xfer.P.nnz * c->nt);
@@ -1081,6 +1333,7 @@ void vcycle_strip(wrmg_ctx *c, int l, const double *r, double *z) {
       launch_restrict(C, c->nt, t, C.vr, s);  // R = P^T over owned fine rows
     }
     halo_reverse_add(c, C, C.vr);
+    if (c->ns) ns_project(c, C, C.vr);
     vcycle_strip(c, l - 1, C.vr, C.vz);
     {
       PScope ps(c, WRMG_K_PROLONG, l, 8.0 * (2 * L.nnode + C.nnode) * c->nt, 2.0 * C.P.nnz * c->nt);
@@ -1340,8 +1593,6 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV && (coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
       throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: cheb_steps <= 63"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
-    if (coeffs->nranks > 1 && coeffs->problem != WRMG_HEAT)
-      throw Err{WRMG_E_UNSUPPORTED, "strip partitions are built for the heat operator only"};
     c = new wrmg_ctx();
     c->mesh = *mesh;
     if (c->mesh.nx == 0) c->mesh.nx = mesh->gnx;
@@ -1417,14 +1668,8 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     const int nl = (int)nxs.size();
     std::vector<PlanLevel> plans(nl);
     c->lv.resize(nl);
-    if (c->strip) {  // uniform strips x0 = rank * nx
-      const int P = coeffs->nranks, r = coeffs->rank;
-      if (r < 0 || r >= P || c->mesh.nx * P != mesh->gnx || c->mesh.x0 != r * c->mesh.nx)
-        throw Err{WRMG_E_INVALID, "strips: need nx * nranks = gnx and x0 = rank * nx"};
-      std::string e;
-      c->comm = coeffs->loopback_hub ? make_loop_comm(coeffs->loopback_hub, r, P, e)
-                                     : make_nccl_comm(coeffs->nccl_unique_id, r, P, e);
-      if (!c->comm) throw Err{WRMG_E_NCCL, e};
+    if (c->strip) {
+      make_strip_comm(c);
     } else if (c->mesh.x0 != 0 || c->mesh.nx != mesh->gnx) {
       throw Err{WRMG_E_INVALID, "a partial strip needs nranks > 1"};
     }
@@ -1768,6 +2013,14 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
   out->own1 = L.st.own1;
   out->g0 = L.st.G0;
   out->nfree_owned_st = L.nfree_owned * c->nt;
+  if (c->ns) {
+    out->lu = L.Lu;
+    out->lpx = L.Lpx;
+    out->lpy = (int32_t)(L.Lp / L.Lpx);
+    out->own0p = L.stp.own0;
+    out->own1p = L.stp.own1;
+    out->g0p = L.stp.G0;
+  }
   if (c->strip) {  // owned rows; the replicated levels (c->sub) are counted once, on rank 0
     upd = 0;
     for (size_t l = c->sub ? 0 : 1; l < c->lv.size(); ++l)
@@ -1867,6 +2120,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
   DevGuard dg_(c);
   try {
     if (nonlinear) {
+      if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(u));
       ns_nonlinear_residual(c, u, b, r);
       check_launch();
       return WRMG_OK;
@@ -2374,7 +2628,9 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
     launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, U, U, s, c->bcg_st);
     launch_ns_mask(L.nnode, c->nt, L.con, c->bcg, rhs, c->nl_b, s, c->bcg_st);  // F(U) = rhs on free rows, U = g on constrained
     auto negF = [&]() {  // nl_r = -F(U)
+      if (c->strip) halo_forward(c, L, U);
       ns_nonlinear_residual(c, U, c->nl_b, c->nl_r);
+      if (c->strip) zero_ghosts(c, L, c->nl_r);  // norms over owned rows
       return std::sqrt(dot_host(c, c->nl_r, c->nl_r, n));
     };
     const double f0 = negF();
@@ -2492,7 +2748,9 @@ void wrmg_destroy(wrmg_ctx *c) {
   for (auto &L : c->lv) free_level(L);
   free_level(c->gco);
   free_level(c->xfer);
-  for (void *p : {(void *)c->sub_r, (void *)c->sub_z, (void *)c->sub_part, (void *)c->sub_all}) dfree(p);
+  for (void *p : {(void *)c->sub_r, (void *)c->sub_z, (void *)c->sub_part, (void *)c->sub_all, (void *)c->sub_w,
+                  (void *)c->rf_send, (void *)c->rf_recv, (void *)c->pj_sums, (void *)c->pj_all})
+    dfree(p);
   if (c->sub) wrmg_destroy(c->sub);
   for (double *p : c->cd) dfree(p);
   for (double *p : c->cbr) dfree(p);

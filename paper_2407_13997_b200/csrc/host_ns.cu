@@ -8,11 +8,13 @@
 //     components on the closure of each vertex star, pressure on the open star;
 //   * block-diagonal interpolation diag(Pu, Pu, Pp) (R12).
 #include <algorithm>
+#include <stdexcept>
 #include <vector>
 
 #include "lattice.h"
 #include "ns.h"
 #include "plan.h"
+#include "strip.h"
 
 namespace wrmg {
 
@@ -152,6 +154,7 @@ void plan_ns_level(int nx, int ny, double h, int k, int bc, double lid_speed, NS
     }
   std::vector<std::vector<int32_t>> pat;
   pat.reserve(nv);
+  P->pvert.clear();
   P->mu.assign(P->ns, 0);
   for (int vj = 0; vj <= ny; ++vj)
     for (int vi = 0; vi <= nx; ++vi) {
@@ -164,6 +167,7 @@ void plan_ns_level(int nx, int ny, double h, int k, int bc, double lid_speed, NS
       std::sort(pv.begin(), pv.end());
       for (int32_t j : pv) s.push_back((int32_t)(2 * Lu + j));
       if (s.empty()) continue;  // empty patches dropped (R8)
+      P->pvert.push_back(vj * (nx + 1) + vi);
       for (int32_t x : s) P->mu[x] += 1;
       P->mp = std::max<int>(P->mp, (int)s.size());
       pat.push_back(std::move(s));
@@ -204,6 +208,149 @@ void plan_ns_interpolation(const NSPlan &C, const NSPlan &F, std::vector<int32_t
     const std::vector<int32_t> &rp = vel ? urp : prp, &ci = vel ? uci : pci;
     const std::vector<double> &vv = vel ? uv : pv;
     const int64_t off = blk * C.Lu;  // coarse sid offset (pressure block starts at 2 C.Lu)
+    const int64_t nrow = vel ? F.Lu : F.Lp;
+    for (int64_t i = 0; i < nrow; ++i, ++r) {
+      for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+        col.push_back((int32_t)(off + ci[e]));
+        val.push_back(vv[e]);
+      }
+      rowptr[r + 1] = (int32_t)col.size();
+    }
+  }
+}
+
+namespace {
+
+// Column bookkeeping of one lattice (degree k) of a strip whose local mesh starts at cell cx0.
+void strip_columns(int k, int gnx, int x0, int nx, int cx0, int nxl, int rank, int nranks, StripInfo *S) {
+  StripInfo &s = *S;
+  s = StripInfo{};
+  s.rank = rank;
+  s.nranks = nranks;
+  s.gnx = gnx;
+  s.x0 = x0;
+  s.nx = nx;
+  s.cx0 = cx0;
+  s.nxl = nxl;
+  s.G0 = k * cx0;
+  s.own0 = (rank == 0 ? 0 : k * x0 + 1) - s.G0;
+  s.own1 = k * (x0 + nx) - s.G0;
+  if (rank > 0) {
+    s.nlg = k;
+    s.lg0 = k * x0 - k + 1 - s.G0;
+    s.nsl = k;
+    s.sl0 = k * x0 + 1 - s.G0;
+  }
+  if (rank < nranks - 1) {
+    s.nrg = k;
+    s.rg0 = k * (x0 + nx) + 1 - s.G0;
+    s.nsr = k;
+    s.sr0 = k * (x0 + nx) - k + 1 - s.G0;
+  }
+}
+
+// Scalar lattice view (Lx, Ly, nnode) of one NS field for plan_strip_interpolation.
+PlanLevel scalar_view(const NSPlan &Q, bool vel) {
+  PlanLevel S;
+  S.nx = Q.nx;
+  S.ny = Q.ny;
+  S.Lx = vel ? Q.Lux : Q.Lpx;
+  S.Ly = vel ? Q.Luy : Q.Lpy;
+  S.nnode = (int64_t)S.Lx * S.Ly;
+  return S;
+}
+
+}  // namespace
+
+void plan_ns_strip_level(int gnx, int gny, int x0, int nx, double h, int k, int bc, double lid_speed, int rank,
+                         int nranks, NSPlan *P, StripInfo *su, StripInfo *sp) {
+  NSPlan G;
+  plan_ns_level(gnx, gny, h, k, bc, lid_speed, &G);
+  const int cx0 = std::max(0, x0 - 1), cx1 = std::min(gnx, x0 + nx + 2), nxl = cx1 - cx0;
+  const int ku = k + 1, kp = k;
+  plan_ns_level(nxl, gny, h, k, bc, lid_speed, P);  // CSR pattern of the local mesh (edge rows truncated)
+  strip_columns(ku, gnx, x0, nx, cx0, nxl, rank, nranks, su);
+  strip_columns(kp, gnx, x0, nx, cx0, nxl, rank, nranks, sp);
+  const int G0u = su->G0, G0p = sp->G0;
+  // local sid of a global sid (-1 outside the local lattices)
+  auto loc = [&](int64_t g) -> int64_t {
+    if (g < 2 * G.Lu) {
+      const int64_t d = g / G.Lu, i = g - d * G.Lu;
+      const int I = (int)(i % G.Lux) - G0u, J = (int)(i / G.Lux);
+      if (I < 0 || I >= P->Lux) return -1;
+      return d * P->Lu + (int64_t)J * P->Lux + I;
+    }
+    const int64_t j = g - 2 * G.Lu;
+    const int I = (int)(j % G.Lpx) - G0p, J = (int)(j / G.Lpx);
+    if (I < 0 || I >= P->Lpx) return -1;
+    return 2 * P->Lu + (int64_t)J * P->Lpx + I;
+  };
+  // global sid of a local sid
+  auto glob = [&](int64_t l) -> int64_t {
+    if (l < 2 * P->Lu) {
+      const int64_t d = l / P->Lu, i = l - d * P->Lu;
+      const int I = (int)(i % P->Lux) + G0u, J = (int)(i / P->Lux);
+      return d * G.Lu + (int64_t)J * G.Lux + I;
+    }
+    const int64_t j = l - 2 * P->Lu;
+    const int I = (int)(j % P->Lpx) + G0p, J = (int)(j / P->Lpx);
+    return 2 * G.Lu + (int64_t)J * G.Lpx + I;
+  };
+  int64_t ncon = 0;
+  for (int64_t l = 0; l < P->ns; ++l) {
+    const int64_t g = glob(l);
+    P->con[l] = G.con[g];
+    P->g[l] = G.g[g];
+    P->mu[l] = G.mu[g];
+    ncon += P->con[l];
+  }
+  P->nfree = P->ns - ncon;
+  const int vlo = rank == 0 ? 0 : x0 + 1, vhi = x0 + nx;
+  std::vector<std::vector<int32_t>> pat;
+  std::vector<int32_t> pv;
+  int mp = 0;
+  for (int64_t p = 0; p < G.npatch; ++p) {
+    const int vi = G.pvert[p] % (gnx + 1);
+    if (vi < vlo || vi > vhi) continue;
+    std::vector<int32_t> s;
+    for (int e = 0; e < G.psize[p]; ++e) {
+      const int64_t l = loc(G.pnodes[p * G.mp + e]);
+      if (l < 0) throw std::runtime_error("plan_ns_strip_level: patch outside the local lattice");
+      s.push_back((int32_t)l);
+    }
+    mp = std::max<int>(mp, (int)s.size());
+    pv.push_back(G.pvert[p]);
+    pat.push_back(std::move(s));
+  }
+  P->mp = mp;
+  P->npatch = (int64_t)pat.size();
+  P->pvert.swap(pv);
+  P->pnodes.assign(P->npatch * P->mp, -1);
+  P->psize.resize(P->npatch);
+  for (int64_t p = 0; p < P->npatch; ++p) {
+    P->psize[p] = (int32_t)pat[p].size();
+    std::copy(pat[p].begin(), pat[p].end(), P->pnodes.begin() + p * P->mp);
+  }
+  (void)ku;
+  (void)kp;
+}
+
+void plan_ns_strip_interpolation(const NSPlan &C, const StripInfo &Scu, const StripInfo &Scp, const NSPlan &F,
+                                 const StripInfo &Sfu, const StripInfo &Sfp, int gny_f, std::vector<int32_t> &rowptr,
+                                 std::vector<int32_t> &col, std::vector<double> &val) {
+  std::vector<int32_t> urp, uci, prp, pci;
+  std::vector<double> uv, pv;
+  plan_strip_interpolation(scalar_view(C, true), Scu, scalar_view(F, true), Sfu, F.ku, gny_f, urp, uci, uv, false);
+  plan_strip_interpolation(scalar_view(C, false), Scp, scalar_view(F, false), Sfp, F.kp, gny_f, prp, pci, pv, true);
+  rowptr.assign(F.ns + 1, 0);
+  col.clear();
+  val.clear();
+  int64_t r = 0;
+  for (int blk = 0; blk < 3; ++blk) {
+    const bool vel = blk < 2;
+    const std::vector<int32_t> &rp = vel ? urp : prp, &ci = vel ? uci : pci;
+    const std::vector<double> &vv = vel ? uv : pv;
+    const int64_t off = blk * C.Lu;
     const int64_t nrow = vel ? F.Lu : F.Lp;
     for (int64_t i = 0; i < nrow; ++i, ++r) {
       for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {

@@ -193,7 +193,9 @@ struct Level {
   int32_t *ppos = nullptr, *pvv = nullptr;  // [npatch][mp][mp] CSR / convection index of each patch pair
   int64_t nsfree_patch_dofs = 0;    // sum of patch sizes (algorithmic accounting)
   // strip partition (nranks > 1)
-  StripInfo st;
+  StripInfo st;                     // heat: the lattice; Navier-Stokes: the velocity lattice
+  StripInfo stp;                    // Navier-Stokes: the pressure lattice
+  int64_t gLp = 0;                  // Navier-Stokes: global pressure nodes (strip projection)
   double *hx[4] = {nullptr, nullptr, nullptr, nullptr};  // halo send-left, recv-left, send-right, recv-right
   int64_t nfree_owned = 0;
 };
@@ -289,6 +291,11 @@ struct wrmg_ctx {
   double *sub_r = nullptr, *sub_z = nullptr, *sub_part = nullptr, *sub_all = nullptr;
   double *gr = nullptr, *gz = nullptr, *gsend = nullptr, *grecv = nullptr;
   int64_t gchunk = 0;
+  // Navier-Stokes strips: state refresh (all-gather of the owned columns, every local
+  // column rewritten from its owner), projection sums, the replicated hierarchy's state
+  double *rf_send = nullptr, *rf_recv = nullptr;
+  int64_t rf_chunk = 0;
+  double *pj_sums = nullptr, *pj_all = nullptr, *sub_w = nullptr;
   // Chebyshev-accelerated smoothing (WRMG_SMOOTH_CHEBYSHEV): lambda per level, direction / B r vectors
   bool cheb = false;
   std::vector<double> lam;

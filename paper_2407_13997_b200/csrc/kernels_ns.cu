@@ -166,22 +166,42 @@ __global__ void __launch_bounds__(256) k_ns_assemble_conv(NSGeom g, int64_t NT, 
 
 // State on the next coarser level by nodal sampling (R13): coarse node (I, J) is
 // fine node (2I, 2J) on both lattices.
-__global__ void k_ns_inject(NSGeom c, NSGeom f, int64_t NT, const double *__restrict__ Wf, double *__restrict__ Wc) {
+__global__ void k_ns_inject(NSGeom c, NSGeom f, int64_t NT, const double *__restrict__ Wf, double *__restrict__ Wc,
+                            NSInjMap m) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= c.ns * NT) return;
   const int64_t s = idx / NT, tt = idx - s * NT;
   int64_t fs;
+  int If;
+  bool ok;
   if (s < 2 * c.Lu) {
     const int d = (int)(s / c.Lu);
     const int64_t i = s - d * c.Lu;
     const int I = (int)(i % c.Lux), J = (int)(i / c.Lux);
-    fs = d * f.Lu + (int64_t)(2 * J) * f.Lux + 2 * I;
+    If = 2 * I + m.du;
+    ok = If >= m.fu0 && If <= m.fu1;
+    fs = d * f.Lu + (int64_t)(2 * J) * f.Lux + If;
   } else {
     const int64_t j = s - 2 * c.Lu;
     const int I = (int)(j % c.Lpx), J = (int)(j / c.Lpx);
-    fs = 2 * f.Lu + (int64_t)(2 * J) * f.Lpx + 2 * I;
+    If = 2 * I + m.dp;
+    ok = If >= m.fp0 && If <= m.fp1;
+    fs = 2 * f.Lu + (int64_t)(2 * J) * f.Lpx + If;
   }
-  Wc[idx] = Wf[fs * NT + tt];
+  Wc[idx] = ok ? Wf[fs * NT + tt] : 0.0;
+}
+
+// Column sums over the lattice columns [c0, c0 + nc) of a (Ly, Lx, NT) field: one
+// partial per block of lattice rows (strip pressure projection, owned columns).
+__global__ void k_colsum_cols(const double *__restrict__ P, int Lx, int Ly, int c0, int nc, int64_t NT, int rpb,
+                              double *__restrict__ partial) {
+  const int J0 = blockIdx.x * rpb, J1 = min(Ly, J0 + rpb);
+  for (int64_t t = threadIdx.x; t < NT; t += blockDim.x) {
+    double acc = 0.0;
+    for (int J = J0; J < J1; ++J)
+      for (int c = 0; c < nc; ++c) acc += P[((int64_t)J * Lx + c0 + c) * NT + t];
+    partial[blockIdx.x * NT + t] = acc;
+  }
 }
 
 // ------------------------------------------------------------------ H6 residual
@@ -1901,9 +1921,12 @@ void launch_ns_assemble_conv(const NSGeom &g, int64_t NT, double R, bool newton,
   ++g_launches;
 }
 
-void launch_ns_inject(const NSGeom &c, const NSGeom &f, int64_t NT, const double *Wf, double *Wc, cudaStream_t s) {
+void launch_ns_inject(const NSGeom &c, const NSGeom &f, int64_t NT, const double *Wf, double *Wc, cudaStream_t s,
+                      const NSInjMap *map) {
+  NSInjMap m{0, 0, 0, f.Lux - 1, 0, f.Lpx - 1};
+  if (map) m = *map;
   const int64_t n = c.ns * NT;
-  k_ns_inject<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, f, NT, Wf, Wc);
+  k_ns_inject<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c, f, NT, Wf, Wc, m);
   ++g_launches;
 }
 
@@ -2065,6 +2088,25 @@ void launch_ns_project(double *P, int64_t nrow, int64_t NT, double *scratch, cud
 int64_t ns_project_scratch(int64_t nrow, int64_t NT) {
   const int64_t rpb = std::max<int64_t>(16, (nrow + 295) / 296);
   return ((nrow + rpb - 1) / rpb + 1) * NT;
+}
+
+void launch_ns_colsum_owned(const double *P, int Lx, int Ly, int c0, int nc, int64_t NT, double *scratch, double *sums,
+                            cudaStream_t s) {
+  // scratch: >= nb * NT doubles, nb = ceil(Ly / rpb); sums: NT doubles
+  const int rpb = std::max(1, (Ly + 295) / 296);
+  const int nb = (Ly + rpb - 1) / rpb;
+  k_colsum_cols<<<nb, 256, 0, s>>>(P, Lx, Ly, c0, nc, NT, rpb, scratch);
+  k_colmean<<<(unsigned)((NT + 255) / 256), 256, 0, s>>>(scratch, nb, NT, 1, sums);
+  g_launches += 2;
+}
+
+void launch_ns_sub_gathered_mean(double *P, int64_t nrow, int64_t NT, const double *gathered, int nranks,
+                                 int64_t gnrow, double *mean, cudaStream_t s) {
+  // mean = (sum over ranks, in rank order, of the owned column sums) / gnrow; P -= mean
+  k_colmean<<<(unsigned)((NT + 255) / 256), 256, 0, s>>>(gathered, nranks, NT, gnrow, mean);
+  const int64_t n = nrow * NT;
+  k_colsub<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P, nrow, NT, mean);
+  g_launches += 2;
 }
 
 void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,

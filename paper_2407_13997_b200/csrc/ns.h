@@ -42,11 +42,32 @@ struct NSPlan {
   int mp = 0;                    // largest Vanka+star patch
   int64_t npatch = 0;
   std::vector<int32_t> pnodes, psize, mu;  // [npatch][mp] sids (-1 pad), sizes, multiplicity per sid
+  std::vector<int32_t> pvert;    // per patch: its mesh vertex vj (nx + 1) + vi
 };
 
 void plan_ns_level(int nx, int ny, double h, int k, int bc, double lid_speed, NSPlan *P);
 // Block-diagonal P_h = diag(Pu, Pu, Pp) in correction form (R5, R12).
 void plan_ns_interpolation(const NSPlan &C, const NSPlan &F, std::vector<int32_t> &rowptr,
                            std::vector<int32_t> &col, std::vector<double> &val);
+
+
+// Strip partition of a Navier-Stokes level.
+// Rank r owns the cell columns [x0, x0 + nx); its local mesh is the cells
+// [max(0, x0 - 1), min(gnx, x0 + nx + 2)): one cell of overlap on the left and two
+// on the right, so that every entry of the Vanka blocks of its owned patches (the
+// velocity closure of the star reaches one cell beyond the owned vertex columns,
+// and an entry between two nodes of that last column integrates over the cell to
+// its right) is assembled from complete cells.  su / sp: the column bookkeeping of
+// the velocity (degree k + 1) and pressure (degree k) lattices, the rules of
+// strip.h per lattice.  Constrained flags, boundary values and multiplicities come
+// from the global plan; the patches are those of the owned mesh vertices (columns
+// (x0, x0 + nx], rank 0 from 0), renumbered to local sids.
+void plan_ns_strip_level(int gnx, int gny, int x0, int nx, double h, int k, int bc, double lid_speed, int rank,
+                         int nranks, NSPlan *P, StripInfo *su, StripInfo *sp);
+// diag(Pu, Pu, Pp) with rows for the owned fine sids only; columns are local
+// coarse sids (Scu.G0 = Scp.G0 = 0 and C the global plan: global coarse sids).
+void plan_ns_strip_interpolation(const NSPlan &C, const StripInfo &Scu, const StripInfo &Scp, const NSPlan &F,
+                                 const StripInfo &Sfu, const StripInfo &Sfp, int gny_f, std::vector<int32_t> &rowptr,
+                                 std::vector<int32_t> &col, std::vector<double> &val);
 
 }  // namespace wrmg

@@ -25,7 +25,14 @@ int64_t ns_project_scratch(int64_t nrow, int64_t NT);
 void launch_ns_assemble_linear(const NSGeom &g, const DevCSR &A, const double *ref, cudaStream_t s);
 void launch_ns_assemble_conv(const NSGeom &g, int64_t NT, double R, bool newton, const DevCSR &A, const int32_t *vvptr,
                              const double *W, double *conv, const double *Th, cudaStream_t s);
-void launch_ns_inject(const NSGeom &c, const NSGeom &f, int64_t NT, const double *Wf, double *Wc, cudaStream_t s);
+// Injection fine -> coarse (R13): coarse local column I reads fine local column 2 I + du
+// (velocity) / 2 I + dp (pressure); outside [fu0, fu1] / [fp0, fp1] the coarse value is 0
+// (strips: only the owned fine columns are read; the rest is refreshed from the owners).
+struct NSInjMap {
+  int du, dp, fu0, fu1, fp0, fp1;
+};
+void launch_ns_inject(const NSGeom &c, const NSGeom &f, int64_t NT, const double *Wf, double *Wc, cudaStream_t s,
+                      const NSInjMap *map = nullptr);
 void launch_ns_residual(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                         const double *conv, const uint8_t *con, const double *u, const double *b, double *r,
                         cudaStream_t s);
@@ -37,6 +44,12 @@ void launch_ns_patch_pos(const NSGeom &g, const DevCSR &A, const int32_t *vvptr,
 void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
                      const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s);
 void launch_ns_project(double *P, int64_t nrow, int64_t NT, double *scratch, cudaStream_t s);
+// Strip form of the projection: column sums over the owned lattice columns (scratch >=
+// (Ly + 1) NT), then, from the all-gathered per-rank sums, P -= sum / gnrow.
+void launch_ns_colsum_owned(const double *P, int Lx, int Ly, int c0, int nc, int64_t NT, double *scratch, double *sums,
+                            cudaStream_t s);
+void launch_ns_sub_gathered_mean(double *P, int64_t nrow, int64_t NT, const double *gathered, int nranks,
+                                 int64_t gnrow, double *mean, cudaStream_t s);
 void launch_ns_coarse_blocks(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                              const double *conv, const int32_t *cnodes, int mc, int pin, double *D, cudaStream_t s);
 void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes, const DevCSR &A, const double *DinvT,
