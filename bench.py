@@ -355,32 +355,36 @@ def run_c3(args, ws, rank, local):
     n, k, q, N, R, T = 64, 1, 1, 64, 100.0, 1.0
     dt = T / N
     stream = torch.cuda.current_stream()
+    kw = strip_kwargs(ws, rank, local)
     t0 = time.time()
     ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
-                    omega_mg=0.8, device=local, stream=stream.cuda_stream)
+                    omega_mg=0.8, device=local, stream=stream.cuda_stream, **kw)
     setup_s = time.time() - t0
     lay = ctx.layout
-    W = torch.as_tensor(wi.wind_state(n, n, 1.0 / n, k, N, q, dt), device=f"cuda:{local}")
+    Wg = wi.wind_state(n, n, 1.0 / n, k, N, q, dt)
+    if ws > 1:  # this strip's window of the global state (the library refreshes non-owned columns itself)
+        Wg = ns_window(Wg, lay, (k + 1) * n + 1, (k + 1) * n + 1, k * n + 1, k * n + 1, lay["nt"])
+    W = torch.as_tensor(Wg, device=f"cuda:{local}")
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ctx.linearize(W)  # warm
     torch.cuda.synchronize()
     ctx.profile(True)
+    barrier(ws)
     ev[0].record(stream)
     ctx.linearize(W)
     ev[1].record(stream)
     torch.cuda.synchronize()
-    lin_ms = ev[0].elapsed_time(ev[1])
+    lin_ms = max_over_ranks(ev[0].elapsed_time(ev[1]), ws)
     lin_stats = {f"{a}@L{l}": {"ms": round(v["ms"], 3), "TFs": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 3)}
                  for (a, l), v in ctx.kernel_stats().items()}
     ctx.profile(False)
-    f = ctx.empty()
-    ctx.fill_uniform(f, 0, 0)
+    f = ns_fill_canonical(ctx, k, n)
     b = ctx.empty()
     ctx.rhs(f, b)
     x = ctx.empty()
     u, r, z = ctx.empty(), ctx.empty(), ctx.empty()
-    upd_vc = lay["smooth_dof_updates_per_vcycle"]
-    upd_sweep = lay["nfree_st"]
+    upd_vc = sum_over_ranks(lay["smooth_dof_updates_per_vcycle"], ws, local)
+    upd_sweep = sum_over_ranks(lay["nfree_owned_st"], ws, local)
 
     def solve():
         u.zero_()
@@ -430,12 +434,14 @@ def run_c3(args, ws, rank, local):
                                 "GBs": round(s["bytes"] / (s["ms"] / 1e3) / 1e9, 1) if s["ms"] > 0 else None,
                                 "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}
                   for (a, l), s in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
-    line = {"metric": METRIC, "value": ws * tot / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+    line = {"metric": METRIC, "value": tot / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C3 = BASELINE configs[2]: Oseen (Newton Jacobian at w = curl psi), P2-P1 x DG1, "
                                    "64x64, N=64, T=1, Re=100, lid; step = 10 sweeps + V(1,1) + 30 FGMRES(30) "
                                    "iterations, omega_mg 0.8",
+                       "parallelism": f"{ws} spatial strips, NCCL halos" if ws > 1 else "1 GPU",
                        "ndof": lay["ndof"], "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
                        "npatch": lay["npatch"], "mp_max": lay["mp_max"], "setup_s": round(setup_s, 2)},
             "fgmres_iterations": its_l[0], "fgmres_status_relres": st_l[0], "linearize_ms": lin_ms,
@@ -449,52 +455,111 @@ def run_c3(args, ws, rank, local):
     ctx.close()
 
 
+def strip_kwargs(ws, rank, local):
+    """Context kwargs of this rank's spatial strip (NCCL transport; rank 0 draws the id)."""
+    if ws == 1:
+        return {}
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_13997_b200 as w
+    idt = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(w.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    return dict(rank=rank, nranks=ws, nccl_id=bytes(idt.cpu().numpy().tobytes()))
+
+
+def sum_over_ranks(x, ws, local):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t)
+    return t.item()
+
+
+def ns_fill_canonical(ctx, k, n, seed=0):
+    """R6 draws of a Navier-Stokes vector at the GLOBAL canonical ids (sid NT + t): one
+    call on one rank; on a strip, per local lattice row of each field (u_x, u_y, p)."""
+    lay = ctx.layout
+    f = ctx.empty()
+    if lay["g0"] == 0 and lay["own1"] == lay["lx"] - 1:
+        ctx.fill_uniform(f, 0, seed)
+        return f
+    NT, Lx, Ly = lay["nt"], lay["lx"], lay["ly"]
+    GLux = (k + 1) * n + 1
+    GLu = GLux * Ly
+    fv = f.view(-1, NT)
+    for off, lx, ly, gx, gc0, goff in ((0, Lx, Ly, GLux, lay["g0"], 0), (lay["lu"], Lx, Ly, GLux, lay["g0"], GLu),
+                                       (2 * lay["lu"], lay["lpx"], lay["lpy"], k * n + 1, lay["g0p"], 2 * GLu)):
+        for J in range(ly):
+            ctx.fill_uniform(fv[off + J * lx:off + (J + 1) * lx].reshape(-1), (goff + J * gx + gc0) * NT, seed)
+    return f
+
+
+def ns_window(vg, lay, ly_g, lx_g, lpy_g, lpx_g, NT):
+    """This rank's local window (every local column) of a global NS vector (host numpy)."""
+    import numpy as np
+    lu_g = lx_g * ly_g
+    a = vg.reshape(-1, NT)
+    gu, gv = a[:lu_g].reshape(ly_g, lx_g, NT), a[lu_g:2 * lu_g].reshape(ly_g, lx_g, NT)
+    gp = a[2 * lu_g:].reshape(lpy_g, lpx_g, NT)
+    c0, c0p = lay["g0"], lay["g0p"]
+    return np.concatenate([gu[:, c0:c0 + lay["lx"]].reshape(-1), gv[:, c0:c0 + lay["lx"]].reshape(-1),
+                           gp[:, c0p:c0p + lay["lpx"]].reshape(-1)])
+
+
 def run_c4(args, ws, rank, local):
-    """BASELINE configs[3] (C4) shape on one B200: Navier-Stokes lid-driven cavity, P3-P2
-    Taylor-Hood x DG1, 128x128 mesh, dt = 1/128, Re = 1000, linearised at the zero state
-    + lid lift (the first Newton step, R26), N = args.c4_n slabs: the stored (patch, slab)
-    block inverses of the full 128-slab horizon are 447 GB, N = 32 is the
-    largest slab count whose ~150 GB fit one GPU.  Step = fixed work: 10 Vanka+star
-    sweeps (omega 1) + one residual + one V(1,1) on a seeded RHS (omega_mg 0.8); the
-    linearisation (assembly + batched block inversion on every level) is timed apart."""
+    """BASELINE configs[3] (C4): Navier-Stokes lid-driven cavity, P3-P2 Taylor-Hood x
+    DG1, 128x128 mesh, dt = 1/128, Re = 1000, linearised at the zero state + lid lift
+    (the first Newton step, R26).  The stored (patch, slab) block inverses of the full
+    128-slab horizon are 447 GB: one B200 holds N = 32 slabs; with ws > 1
+    the mesh is split into ws spatial strips (NCCL halos) and the
+    default horizon is N = min(128, 32 ws) -- the full C4 horizon from 4 GPUs on.
+    Step = fixed work: 10 Vanka+star sweeps (omega 1) + one residual + one V(1,1) on a
+    seeded RHS (omega_mg 0.8); the linearisation (assembly + batched block inversion on
+    every level) is timed apart."""
     import torch
 
     import paper_2407_13997_b200 as w
     torch.cuda.set_device(local)
-    n, k, q, N, R = 128, 2, 1, args.c4_n, 1000.0
+    n, k, q, R = 128, 2, 1, 1000.0
+    N = args.c4_n if args.c4_n else min(128, 32 * ws)
     dt = 1.0 / 128
     stream = torch.cuda.current_stream()
+    kw = strip_kwargs(ws, rank, local)
     t0 = time.time()
     ctx = w.Context(n, n, 1.0 / n, degree=k, q=q, nslabs=N, dt=dt, problem="ns", reynolds=R, bc="lid",
-                    omega_mg=0.8, device=local, stream=stream.cuda_stream)
+                    omega_mg=0.8, device=local, stream=stream.cuda_stream, **kw)
     setup_s = time.time() - t0
     lay = ctx.layout
     NT = lay["nt"]
-    ku = k + 1
-    Lux = ku * n + 1
-    Lu = Lux * Lux
+    Lx, Ly, g0 = lay["lx"], lay["ly"], lay["g0"]
+    GLux = (k + 1) * n + 1
     W = torch.zeros(lay["ndof"], dtype=torch.float64, device=f"cuda:{local}")
-    top = W.view(-1, NT)[(Lux - 1) * Lux + 1:(Lux - 1) * Lux + Lux - 1]  # u_x on the lid, corners excluded
-    top.fill_(1.0)
-    assert (Lux - 1) * Lux + Lux - 1 <= Lu
+    top = W.view(-1, NT)[(Ly - 1) * Lx:Ly * Lx]  # u_x on the lid row (local columns), corners excluded
+    lo, hi = max(0, 1 - g0), min(Lx, GLux - 1 - g0)
+    top[lo:hi].fill_(1.0)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ctx.profile(True)
+    barrier(ws)
     ev[0].record(stream)
     ctx.linearize(W)
     ev[1].record(stream)
     torch.cuda.synchronize()
-    lin_ms = ev[0].elapsed_time(ev[1])
+    lin_ms = max_over_ranks(ev[0].elapsed_time(ev[1]), ws)
     lin_stats = {f"{a}@L{l}": {"ms": round(v["ms"], 3), "TFs": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 3)}
                  for (a, l), v in ctx.kernel_stats().items()}
     ctx.profile(False)
-    f = ctx.empty()
-    ctx.fill_uniform(f, 0, 0)
+    f = ns_fill_canonical(ctx, k, n)
     b = ctx.empty()
     ctx.rhs(f, b)
     del f
     u, r, z = ctx.empty(), ctx.empty(), ctx.empty()
-    upd_vc = lay["smooth_dof_updates_per_vcycle"]
-    upd_sweep = lay["nfree_st"]
+    upd_vc = sum_over_ranks(lay["smooth_dof_updates_per_vcycle"], ws, local)
+    upd_sweep = sum_over_ranks(lay["nfree_owned_st"], ws, local)
 
     def step():
         u.zero_()
@@ -510,13 +575,16 @@ def run_c4(args, ws, rank, local):
     time.sleep(0.3)
     ctx.profile(True)
     l0 = w.launch_count()
+    barrier(ws)
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
     stats = ctx.kernel_stats()
     ctx.profile(False)
     clk = clocks.stop()
@@ -525,12 +593,17 @@ def run_c4(args, ws, rank, local):
                                 "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}
                   for (a, l), s in sorted(stats.items(), key=lambda kv: -kv[1]["ms"])}
     tot = args.steps * (10 * upd_sweep + upd_vc)
-    line = {"metric": METRIC, "value": tot / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C4 shape = BASELINE configs[3] at full mesh: NS cavity P3-P2 x DG1, 128x128, "
-                                   f"dt=1/128, Re=1000, linearised at the lid lift; N={N} slabs (C4's 128 slabs "
-                                   f"need 447 GB of stored block inverses); step = 10 sweeps + residual + V(1,1)",
+    full = N == 128
+    line = {"metric": METRIC, "value": tot / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if N == 32 * ws else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"C4 = BASELINE configs[3]: NS cavity P3-P2 x DG1, 128x128, dt=1/128, Re=1000, "
+                                   f"linearised at the lid lift; N={N} slabs"
+                                   + (" (the full horizon [0, 1])" if full else
+                                      " (the 128-slab horizon needs 447 GB of stored block inverses: >= 4 GPUs)")
+                                   + "; step = 10 sweeps + residual + V(1,1)",
+                       "parallelism": f"{ws} spatial strips, NCCL halos" if ws > 1 else "1 GPU",
                        "ndof": lay["ndof"], "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
                        "npatch": lay["npatch"], "mp_max": lay["mp_max"], "setup_s": round(setup_s, 2)},
             "linearize_ms": lin_ms, "linearize_kernels": lin_stats,
@@ -732,7 +805,8 @@ def main():
     ap.add_argument("--impl", default="wrmg", choices=["wrmg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
-    ap.add_argument("--c4-n", type=int, default=32, help="C4 slabs on one GPU (32: largest whose inverses fit)")
+    ap.add_argument("--c4-n", type=int, default=0,
+                    help="C4 slabs (0: min(128, 32 x GPUs); one GPU holds the inverses of 32)")
     ap.add_argument("--c5-n", type=int, default=1024, help="C5 cells per side per GPU (1024 = the config)")
     ap.add_argument("--scatter", default="atomic", choices=["atomic", "colour"],
                     help="weighted additive scatter of the heat sweep (H8): FP64 atomics or coloured passes")

@@ -322,6 +322,15 @@ wrmg_status wrmg_hessenberg_eig(const double *H, int32_t n, double *wr, double *
 wrmg_status wrmg_plan_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank, int32_t nranks, int32_t *info,
                             int32_t *patch_vertex, int64_t *npatch);
 
+/* Host-only: the Navier-Stokes strip plan of one rank (Taylor-Hood P_{degree+1} -
+ * P_degree; the lid-cavity boundary).  info[32] = the 16
+ * entries of wrmg_plan_strip for the velocity lattice, then for the pressure
+ * lattice.  *npatch, *mp: owned Vanka+star patches and the largest size; when
+ * patch_vertex / patch_sids are not NULL they receive each patch's global vertex
+ * id and its sids as GLOBAL sids ([npatch][mp], -1 padded). */
+wrmg_status wrmg_plan_ns_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank, int32_t nranks, int32_t *info,
+                               int32_t *patch_vertex, int32_t *patch_sids, int64_t *npatch, int32_t *mp);
+
 #ifdef __cplusplus
 }
 #endif

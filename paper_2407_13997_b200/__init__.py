@@ -20,4 +20,5 @@ from ._lib import (  # noqa: F401
     wrmg_plan,
     wrmg_plan_patches,
     wrmg_plan_strip,
+    wrmg_plan_ns_strip,
 )

@@ -79,6 +79,7 @@ _sig = {
     "wrmg_nccl_unique_id": (c_i32, [c_vp]),
     "wrmg_hessenberg_eig": (c_i32, [c_vp, c_i32, c_vp, c_vp]),
     "wrmg_plan_strip": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, c_vp, c_vp, _P(c_i64)]),
+    "wrmg_plan_ns_strip": (c_i32, [_P(wrmg_mesh), c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, _P(c_i64), _P(c_i32)]),
     "wrmg_loopback_create": (c_i32, [c_i32, _P(c_vp)]),
     "wrmg_loopback_destroy": (None, [c_vp]),
 }
@@ -145,6 +146,27 @@ def wrmg_plan_strip(gnx, gny, h, degree, rank, nranks):
     _check(lib.wrmg_plan_strip(ctypes.byref(m), int(degree), int(rank), int(nranks), info.ctypes.data_as(c_vp),
                                pv.ctypes.data_as(c_vp), ctypes.byref(n)))
     return dict(zip(STRIP_INFO, (int(x) for x in info))), pv[:n.value]
+
+
+def wrmg_plan_ns_strip(gnx, gny, h, degree, rank, nranks):
+    """Host-only Navier-Stokes strip plan of one rank (lid cavity): (velocity info,
+    pressure info, global vertex ids of its patches, their global sids [npatch][mp])."""
+    if gnx % nranks:
+        raise ValueError("gnx must be divisible by nranks")
+    snx = gnx // nranks
+    m = _mesh(gnx, gny, h, 4, rank * snx, snx)
+    info = np.zeros(32, dtype=np.int32)
+    n, mp = c_i64(), c_i32()
+    _check(lib.wrmg_plan_ns_strip(ctypes.byref(m), int(degree), int(rank), int(nranks), info.ctypes.data_as(c_vp),
+                                  None, None, ctypes.byref(n), ctypes.byref(mp)))
+    pv = np.zeros(max(n.value, 1), dtype=np.int32)
+    ps = np.zeros((max(n.value, 1), max(mp.value, 1)), dtype=np.int32)
+    _check(lib.wrmg_plan_ns_strip(ctypes.byref(m), int(degree), int(rank), int(nranks), info.ctypes.data_as(c_vp),
+                                  pv.ctypes.data_as(c_vp), ps.ctypes.data_as(c_vp), ctypes.byref(n),
+                                  ctypes.byref(mp)))
+    iu = dict(zip(STRIP_INFO, (int(x) for x in info[:16])))
+    ip = dict(zip(STRIP_INFO, (int(x) for x in info[16:32])))
+    return iu, ip, pv[:n.value], ps[:n.value]
 
 
 def nccl_unique_id():

@@ -1577,6 +1577,51 @@ wrmg_status wrmg_plan_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank,
   }
 }
 
+wrmg_status wrmg_plan_ns_strip(const wrmg_mesh *mesh, int32_t degree, int32_t rank, int32_t nranks, int32_t *info,
+                               int32_t *patch_vertex, int32_t *patch_sids, int64_t *npatch, int32_t *mp) {
+  try {
+    validate(mesh, degree + 1, 0, 1, 1.0);
+    if (!info || nranks < 1 || rank < 0 || rank >= nranks || degree < 1 || degree > 2)
+      throw Err{WRMG_E_INVALID, "bad strip query"};
+    NSPlan P;
+    StripInfo Su, Sp;
+    try {
+      plan_ns_strip_level(mesh->gnx, mesh->gny, mesh->x0, mesh->nx, mesh->h, degree, WRMG_BC_LID, 1.0, rank, nranks,
+                          &P, &Su, &Sp);
+    } catch (const std::exception &e) {
+      throw Err{WRMG_E_INVALID, e.what()};
+    }
+    const int Lpy = P.Lpy;
+    const int32_t v[32] = {Su.G0, Su.own0, Su.own1, Su.lg0, Su.nlg, Su.rg0, Su.nrg, Su.sl0, Su.nsl, Su.sr0, Su.nsr,
+                           P.Lux, P.Luy, Su.cx0, Su.nxl, 0,
+                           Sp.G0, Sp.own0, Sp.own1, Sp.lg0, Sp.nlg, Sp.rg0, Sp.nrg, Sp.sl0, Sp.nsl, Sp.sr0, Sp.nsr,
+                           P.Lpx, Lpy, Sp.cx0, Sp.nxl, 0};
+    std::memcpy(info, v, sizeof(v));
+    if (npatch) *npatch = P.npatch;
+    if (mp) *mp = P.mp;
+    const int64_t GLux = (int64_t)(degree + 1) * mesh->gnx + 1, GLu = GLux * P.Luy, GLpx = (int64_t)degree * mesh->gnx + 1;
+    for (int64_t p = 0; p < P.npatch; ++p) {
+      if (patch_vertex) patch_vertex[p] = P.pvert[p];
+      if (patch_sids)
+        for (int e = 0; e < P.mp; ++e) {
+          const int32_t l = P.pnodes[p * P.mp + e];
+          int64_t g = -1;
+          if (l >= 0 && l < 2 * P.Lu) {
+            const int64_t d = l / P.Lu, i = l - d * P.Lu;
+            g = d * GLu + (i / P.Lux) * GLux + (i % P.Lux) + Su.G0;
+          } else if (l >= 0) {
+            const int64_t j = l - 2 * P.Lu;
+            g = 2 * GLu + (j / P.Lpx) * GLpx + (j % P.Lpx) + Sp.G0;
+          }
+          patch_sids[p * P.mp + e] = (int32_t)g;
+        }
+    }
+    return WRMG_OK;
+  } catch (const Err &e) {
+    return fail(nullptr, e);
+  }
+}
+
 wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, double dt,
                        const wrmg_coeffs *coeffs, wrmg_ctx **out) {
   wrmg_ctx *c = nullptr;

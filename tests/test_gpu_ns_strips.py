@@ -224,3 +224,36 @@ def test_ns_strips_newton_cavity(P, k, cheb):
         assert o["st"] == "WRMG_OK" and o["its"] == its_g and o["lin"] == lin_g, (o["its"], o["lin"], its_g, lin_g)
     e = _rel(_assemble(outs, "U", gl), ref)
     assert e <= 1e-8, f"U: rel {e:.3e}"
+
+
+def test_ns_strip_canonical_fill_and_window():
+    """bench.py's per-rank inputs of the NS strips: the R6 draws at global canonical
+    ids (ns_fill_canonical) and the host window of a global vector (ns_window) equal
+    the global vector's columns on every local column of every field."""
+    import torch
+    import paper_2407_13997_b200 as w
+    import bench
+    P, n, k, q, N = 2, 8, 2, 1, 2
+    kw = dict(degree=k, q=q, nslabs=N, dt=0.1, ncoarse=2, problem="ns", reynolds=10.0, bc="lid")
+    g = w.Context(n, n, 1.0 / n, **kw)
+    gl = g.layout
+    fg = bench.ns_fill_canonical(g, k, n).cpu().numpy()
+    g.close()
+    hub = w.LoopbackHub(P)
+
+    def rank_fn(r):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            c = w.Context(n, n, 1.0 / n, rank=r, nranks=P, hub=hub, stream=st.cuda_stream, **kw)
+            lay = c.layout
+            fl = bench.ns_fill_canonical(c, k, n)
+            st.synchronize()
+            got = fl.cpu().numpy()
+            win = bench.ns_window(fg, lay, gl["ly"], gl["lx"], gl["lpy"], gl["lpx"], gl["nt"])
+            c.close()
+            return got, _window(fg, gl, lay), win
+
+    outs = _run_ranks(P, rank_fn)
+    hub.close()
+    for got, ref, win in outs:
+        assert np.array_equal(got, ref) and np.array_equal(win, ref)

@@ -98,3 +98,85 @@ def test_nccl_transport_loads_and_creates_unique_ids():
     import paper_2407_13997_b200 as w
     a, b = w.nccl_unique_id(), w.nccl_unique_id()
     assert len(a) == 128 and len(b) == 128 and a != b and any(a)
+
+
+def _ns_worker(rank, world, port, gnx, gny, k, out):
+    import torch
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2407_13997_b200 as w
+        iu, ip, pv, ps = w.wrmg_plan_ns_strip(gnx, gny, 1.0 / gny, k, rank, world)
+        plans = [None] * world
+        dist.all_gather_object(plans, (iu, ip, pv.tolist(), ps.tolist()))
+        # halo forward of each lattice with gloo: every column carries its global id
+        ghosts = []
+        for info in (iu, ip):
+            Lx = info["Lx"]
+            v = np.full(Lx, -1.0)
+            v[info["own0"]:info["own1"] + 1] = info["G0"] + np.arange(info["own0"], info["own1"] + 1)
+            reqs, bufs = [], {}
+            if info["nsl"]:
+                reqs.append(dist.isend(torch.tensor(v[info["sl0"]:info["sl0"] + info["nsl"]]), rank - 1))
+                bufs["L"] = torch.zeros(info["nlg"], dtype=torch.float64)
+                reqs.append(dist.irecv(bufs["L"], rank - 1))
+            if info["nsr"]:
+                reqs.append(dist.isend(torch.tensor(v[info["sr0"]:info["sr0"] + info["nsr"]]), rank + 1))
+                bufs["R"] = torch.zeros(info["nrg"], dtype=torch.float64)
+                reqs.append(dist.irecv(bufs["R"], rank + 1))
+            for r in reqs:
+                r.wait()
+            if "L" in bufs:
+                v[info["lg0"]:info["lg0"] + info["nlg"]] = bufs["L"].numpy()
+            if "R" in bufs:
+                v[info["rg0"]:info["rg0"] + info["nrg"]] = bufs["R"].numpy()
+            ghosts.append([(c, v[c]) for c in list(range(info["lg0"], info["lg0"] + info["nlg"]))
+                           + list(range(info["rg0"], info["rg0"] + info["nrg"]))])
+        halo = [None] * world
+        dist.all_gather_object(halo, ghosts)
+        if rank == 0:
+            out.put((plans, halo))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,snx,gny,k", [(2, 4, 5, 1), (3, 3, 4, 2), (2, 2, 3, 2)])
+def test_ns_strip_plans_and_halo_over_gloo(world, snx, gny, k):
+    """Navier-Stokes strips: the owned columns of the velocity
+    (degree k + 1) and pressure (degree k) lattices tile the global lattices, the
+    gloo halo fills k + 1 / k ghost columns per side with the owners' columns, and
+    the owned Vanka+star patches -- mapped back to global sids -- are exactly the
+    oracle's patches (Fig. patches right), each on one rank."""
+    from oracle import mesh, ns
+    gnx = world * snx
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ns_worker, args=(r, world, port, gnx, gny, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    plans, halo = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for f, kk in ((0, k + 1), (1, k)):
+        owned = []
+        for pl in plans:
+            info = pl[f]
+            owned += list(range(info["G0"] + info["own0"], info["G0"] + info["own1"] + 1))
+        assert owned == list(range(kk * gnx + 1))
+        for r, gh in enumerate(halo):
+            info = plans[r][f]
+            for c, val in gh[f]:
+                assert val == info["G0"] + c
+            assert len(gh[f]) == kk * ((r > 0) + (r < world - 1))
+    prob = ns.NSProblem(mesh.Mesh(gnx, gny, 1.0 / gny), k, 0, 1, 1.0, 1.0, bc="lid")
+    pats, verts = ns.vanka_star_patches(prob)
+    ref = {int(v): p.tolist() for v, p in zip(verts, pats)}
+    got = {}
+    for _, _, pv, ps in plans:
+        for v, sids in zip(pv, ps):
+            assert v not in got
+            got[v] = [s for s in sids if s >= 0]
+    assert got == ref
