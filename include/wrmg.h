@@ -91,9 +91,13 @@ typedef struct {
                            value unspecified) | WRMG_SCATTER_COLOUR (three passes, one per vertex colour
                            (i - j) mod 3 -- patches of one colour share no DoF -- so every value receives one
                            addition per pass in a fixed order: bitwise reproducible) */
+  int32_t orth;         /* Arnoldi orthogonalisation of wrmg_fgmres (R16): WRMG_ORTH_CGS (default;
+                           classical Gram-Schmidt, one pass -- the default of the PETSc FGMRES that the
+                           paper's Firedrake runs use) | WRMG_ORTH_CGS2 (applied twice) */
 } wrmg_coeffs;
 enum { WRMG_SMOOTH_DAMPED = 0, WRMG_SMOOTH_CHEBYSHEV = 1 };
 enum { WRMG_SCATTER_ATOMIC = 0, WRMG_SCATTER_COLOUR = 1 };
+enum { WRMG_ORTH_CGS = 0, WRMG_ORTH_CGS2 = 1 };
 
 typedef struct {
   int64_t nnode;        /* lattice nodes of the finest level owned by this rank */

@@ -4,15 +4,17 @@
 where we use FGMRES ... because it explicitly stores the preconditioned Arnoldi
 vectors and, thus, can reassemble the final solution without the additional
 application of the preconditioner."  DESIGN.md R16: x0 = 0, restart 30, classical
-Gram-Schmidt applied twice (CGS2), Givens rotations, stop when the implicit
-residual |g_{j+1}| <= max(rtol ||b||, atol); true residual recomputed at each
-restart; breakdown when h_{j+1,j} < 1e-30 (reported separately).
+Gram-Schmidt (one pass, orth="cgs": the default orthogonalisation of the PETSc
+FGMRES behind the paper's Firedrake runs; orth="cgs2" applies it
+twice), Givens rotations, stop when the implicit residual |g_{j+1}| <= max(rtol
+||b||, atol); true residual recomputed at each restart; breakdown when h_{j+1,j} <
+1e-30 (reported separately).
 Textbook algorithm (Saad, FGMRES), written out step by step.
 """
 import numpy as np
 
 
-def fgmres(A, M, b, restart=30, maxit=200, rtol=1e-8, atol=0.0, x0=None):
+def fgmres(A, M, b, restart=30, maxit=200, rtol=1e-8, atol=0.0, x0=None, orth="cgs"):
     """Returns (x, iterations, history, status) with status in
     {'converged', 'breakdown', 'maxit'}; history holds |g_{j+1}| per iteration
     (history[0] = initial residual norm)."""
@@ -42,9 +44,12 @@ def fgmres(A, M, b, restart=30, maxit=200, rtol=1e-8, atol=0.0, x0=None):
             Vm = np.array(V)  # (j+1, n)
             h = Vm @ w
             w = w - Vm.T @ h
-            h2 = Vm @ w
-            w = w - Vm.T @ h2
-            h = h + h2
+            if orth == "cgs2":
+                h2 = Vm @ w
+                w = w - Vm.T @ h2
+                h = h + h2
+            elif orth != "cgs":
+                raise ValueError(orth)
             hn = np.linalg.norm(w)
             col = np.zeros(restart + 1)
             col[:j + 1] = h

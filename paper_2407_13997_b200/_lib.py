@@ -25,7 +25,7 @@ class wrmg_coeffs(ctypes.Structure):
                 ("weights", c_i32), ("omega_mg", c_dbl), ("nu_pre", c_i32), ("nu_post", c_i32),
                 ("factor_mode", c_i32), ("device", c_i32), ("stream", c_vp), ("rank", c_i32), ("nranks", c_i32),
                 ("nccl_unique_id", c_vp), ("loopback_hub", c_vp), ("smoother", c_i32), ("cheb_steps", c_i32),
-                ("cheb_seed", ctypes.c_uint64), ("scatter", c_i32)]
+                ("cheb_seed", ctypes.c_uint64), ("scatter", c_i32), ("orth", c_i32)]
 
 
 class wrmg_layout_t(ctypes.Structure):
@@ -227,7 +227,7 @@ class Context:
     def __init__(self, nx, ny=None, h=None, degree=1, q=0, nslabs=1, dt=1.0, kappa=1.0, omega_mg=1.0,
                  nu_pre=1, nu_post=1, weights="pou", ncoarse=4, device=0, stream=None, factor_mode="auto",
                  problem="heat", reynolds=1.0, bc=None, lid_speed=1.0, rank=0, nranks=1, nccl_id=None,
-                 hub=None, smoother="damped", cheb_steps=50, cheb_seed=7, scatter="atomic"):
+                 hub=None, smoother="damped", cheb_steps=50, cheb_seed=7, scatter="atomic", orth="cgs"):
         import torch
         ny = nx if ny is None else ny
         h = 1.0 / ny if h is None else h
@@ -259,6 +259,7 @@ class Context:
         co.cheb_steps, co.cheb_seed = int(cheb_steps), int(cheb_seed)
         co.factor_mode = {"auto": 0, "lu": 1}[factor_mode]
         co.scatter = {"atomic": 0, "colour": 1}[scatter]
+        co.orth = {"cgs": 0, "cgs2": 1}[orth]
         self._co = co
         h_ = c_vp()
         _check(lib.wrmg_setup(ctypes.byref(self._mesh), int(degree), int(q), int(nslabs), float(dt),

@@ -1638,6 +1638,8 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
     if (coeffs->smoother == WRMG_SMOOTH_CHEBYSHEV && (coeffs->cheb_steps < 0 || coeffs->cheb_steps > 63))
       throw Err{WRMG_E_UNSUPPORTED, "Chebyshev smoothing: cheb_steps <= 63"};
     if (coeffs->problem == WRMG_HEAT && !(coeffs->kappa > 0)) throw Err{WRMG_E_INVALID, "kappa must be > 0"};
+    if (coeffs->orth != WRMG_ORTH_CGS && coeffs->orth != WRMG_ORTH_CGS2)
+      throw Err{WRMG_E_INVALID, "orth must be WRMG_ORTH_CGS or WRMG_ORTH_CGS2"};
     c = new wrmg_ctx();
     c->mesh = *mesh;
     if (c->mesh.nx == 0) c->mesh.nx = mesh->gnx;
@@ -2265,6 +2267,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
     cudaStream_t s = c->stream;
     Level &L = c->lv.back();
     const bool strip = c->strip;
+    const bool cgs2 = c->co.orth == WRMG_ORTH_CGS2;
     const int64_t n = L.nnode * c->nt;
     if (c->restart_alloc < restart) {
       for (double *p : c->V) dfree(p);
@@ -2329,6 +2332,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
         // w = A Z_j (residual kernel in apply mode)
         prof_residual(c, (int)c->lv.size() - 1, c->Z[j], nullptr, c->w, false);
         if (strip) zero_ghosts(c, L, c->w);
+        // CGS (R16), fused: h = V^T w;  w -= V h & |w|^2.
         // CGS2, fused: h = V^T w;  w -= V h & h2 = V^T w;  w -= V h2 & |w|^2
         // (w' = A Z_j', the true w = sc_j w': h_i = sc_i sc_j <V_i', w'>, and
         // w -= sum h_i V_i  <=>  w' -= sum sc_i^2 <V_i', w'> V_i')
@@ -2342,15 +2346,17 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
             launch_reduce_partials(part, nb, j + 1, c->kry + 32, s);
           }
           launch_cgs_step(c->kry, j, 0, s);
-          {
-            PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 4.0 * (j + 1) * n);
-            launch_cgs_update_dot(c->V.data(), j + 1, c->w, c->kry + 64, n, part, nb, s);
-            launch_reduce_partials(part, nb, j + 1, c->kry + 96, s);
+          if (cgs2) {
+            {
+              PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 4.0 * (j + 1) * n);
+              launch_cgs_update_dot(c->V.data(), j + 1, c->w, c->kry + 64, n, part, nb, s);
+              launch_reduce_partials(part, nb, j + 1, c->kry + 96, s);
+            }
+            launch_cgs_step(c->kry, j, 1, s);
           }
-          launch_cgs_step(c->kry, j, 1, s);
-          {
+          {  // CGS: w -= V coef_A and |w|^2 in one pass (CGS2: coef_B)
             PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
-            launch_cgs_update_norm(c->V.data(), j + 1, c->w, c->kry + 128, n, part, nb, s);
+            launch_cgs_update_norm(c->V.data(), j + 1, c->w, c->kry + (cgs2 ? 128 : 64), n, part, nb, s);
             launch_reduce_partials(part, nb, 1, c->kry + 192, s);
           }
           launch_cgs_step(c->kry, j, 2, s);
@@ -2364,6 +2370,9 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           coef[i] = sc[i] * sc[i] * h[i];
           h[i] *= sc[i] * sc[j];
         }
+        if (!cgs2) {  // CGS: w -= V coef and |w|^2 in one pass
+          small_h2d(c, coef.data(), red + 32, j + 1);
+        } else {
         small_h2d(c, coef.data(), red, j + 1);
         {
           PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 4.0 * (j + 1) * n);
@@ -2378,6 +2387,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
           h[i] += sc[i] * sc[j] * h2[i];
         }
         small_h2d(c, coef.data(), red + 32, j + 1);
+        }
         {
           PScope ps(c, WRMG_K_KRYLOV, (int)c->lv.size() - 1, 8.0 * (j + 3) * n, 2.0 * (j + 2) * n);
           const int nb = multidot_blocks(n);
