@@ -541,7 +541,7 @@ void coarse_strip(wrmg_ctx *c, const double *r, double *z) {
     const Coarse &C = c->coarse;
     PScope ps(c, WRMG_K_COARSE, 0, 16.0 * C.nfree * c->nt + 8.0 * G.nnode * c->nt,
               2.0 * c->N * ((double)C.m * C.m + (double)C.m * C.mp));
-    if (c->use_kron)
+    if (c->coarse_kron)
       launch_coarse_solve_kron(C, G, c->q, c->N, c->gr, c->gz, s);
     else
       launch_coarse_solve(C, G, c->q, c->N, c->gr, c->gz, s);
@@ -713,7 +713,7 @@ void factor_all(wrmg_ctx *c) {
   }
   CK(cudaStreamSynchronize(s));
   dfree(LU);
-  if (c->use_kron) {
+  if (c->coarse_kron) {
     double *scr = dalloc<double>((size_t)3 * C.mp * C.mp);
     launch_kron_setup_coarse(L0, C, c->nq, c->tm, scr, s);
     check_launch();
@@ -1088,7 +1088,10 @@ void setup_ns(wrmg_ctx *c) {
     C.m = c->nq * C.mp;
     C.nnzj = 0;
     for (int32_t sd : nodes) C.nnzj += P.rowptr[sd + 1] - P.rowptr[sd];
-    if (C.m > 2048) throw Err{WRMG_E_UNSUPPORTED, "coarse slab block larger than 2048 (raise ncoarse depth)"};
+    // dense per-slab blocks (m^2 doubles each, twice) and the end-trace recurrence's
+    // 4 mc doubles of shared memory bound the coarse level
+    if (C.m > 8192 || 4 * (size_t)C.mp * sizeof(double) > 220 * 1024)
+      throw Err{WRMG_E_UNSUPPORTED, "coarse slab block larger than 8192 (raise ncoarse depth)"};
     C.nodes = dupload(nodes, s);
     C.nsD = dalloc<double>((size_t)c->N * C.m * C.m);
     C.nsinvT = dalloc<double>((size_t)c->N * C.m * C.m);
@@ -1380,7 +1383,7 @@ void vcycle_level(wrmg_ctx *c, int l, const double *r, double *z) {
     const Coarse &C = c->coarse;
     PScope ps(c, WRMG_K_COARSE, 0, 16.0 * C.nfree * c->nt + 8.0 * L.nnode * c->nt,
               2.0 * c->N * ((double)C.m * C.m + (double)C.m * C.mp));
-    if (c->use_kron)
+    if (c->coarse_kron)
       launch_coarse_solve_kron(C, L, c->q, c->N, r, z, s);
     else
       launch_coarse_solve(C, L, c->q, c->N, r, z, s);
@@ -2000,7 +2003,11 @@ wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t
       C.Y = dalloc<double>((size_t)(c->N + 1) * C.mp);
       C.piv = dalloc<int32_t>(C.m);
       C.info = dalloc<int32_t>(1);
-      if (c->use_kron) {
+      // coarsest levels with more than kCoarseKronMax free nodes: the slab march with the
+      // stored block inverse (the single-CTA Jacobi eigen-setup of the Kronecker form costs
+      // O(mp^3) sweeps serially: minutes at mp = 841, the paper protocol's P3 10 x 10 level)
+      c->coarse_kron = c->use_kron && C.mp <= kCoarseKronMax;
+      if (c->coarse_kron) {
         C.kV = dalloc<double>((size_t)C.mp * C.mp);
         C.kVT = dalloc<double>((size_t)C.mp * C.mp);
         C.kS = dalloc<double>((size_t)C.mp * c->nq * c->nq);

@@ -257,6 +257,7 @@ struct wrmg_ctx {
   double *gred = nullptr;  // strips: all ranks' reduction results (nranks x 64), for wrmg_fgmres
   double *tmp = nullptr;        // finest-level scratch (residual)
   bool use_kron = true;         // factor_mode AUTO: Kronecker-diagonalised heat patch solves
+  bool coarse_kron = false;     // the coarsest level's solve in Kronecker form (mp <= kCoarseKronMax)
   std::string err;
   int err_level = -1, err_patch = -1, err_slab = -1;
   // kernel timing (wrmg_profile / wrmg_kernel_stats)
@@ -303,6 +304,7 @@ struct wrmg_ctx {
 };
 
 namespace wrmg {
+constexpr int kCoarseKronMax = 200;
 extern std::atomic<int64_t> g_launches;  // kernels launched by this library (process-wide)
 // Streaming multiprocessors of the current device (cached per device; 148 on B200).
 int num_sms();

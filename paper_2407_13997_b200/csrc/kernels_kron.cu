@@ -20,6 +20,8 @@
 // 2 (q+1) m_p^2 + O((q+1)^2 m_p) FMAs instead of the LU solve's (q+1)^2 m_p^2 + m_p^2.
 #include <cfloat>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace wrmg {
@@ -828,7 +830,16 @@ bool launch_sweep_kron(const Level &L, int q, int N, const double *r, double *u,
   const int pp = sl ? sl->pp : L.kron_pp;
   const int32_t *gp = sl ? sl->grp_patch8 : L.grp_patch8, *gt = sl ? sl->grp_type8 : L.grp_type8;
   const int32_t *cp = sl ? sl->cta_patch : L.cta_patch, *ct = sl ? sl->cta_type : L.cta_type;
-  if (nq == 2 && L.npatch >= 1000) {  // small levels: chunk-parallel kernel below
+  // Levels whose interior class runs in kernels_sweep_sym.cu leave only the boundary
+  // classes here (a few hundred patches): the chunk-parallel kernel below (one warp per
+  // 32-slab chunk) instead of the DMMA kernel's one warp walking all slabs of a patch
+  // (latency-bound on so few patches).  WRMG_BOUNDARY_CP=0: the DMMA kernel (A/B).
+  static const bool boundary_cp = [] {
+    const char *e = getenv("WRMG_BOUNDARY_CP");
+    return !(e && e[0] == '0');
+  }();
+  const bool residue = L.sym_ok && L.nsym > 0 && !sl && boundary_cp && N > 32;
+  if (nq == 2 && L.npatch >= 1000 && !residue) {  // small levels: chunk-parallel kernel below
     if (L.mp == 19 || L.mp == 7 || L.mp == 1) {
       if (ngrp8 == 0) return true;  // nothing in this list
       if (L.mp == 19) sweep_kron_mma_launch<19>(L, N, r, u, omega, s, ngrp8, gp, gt);

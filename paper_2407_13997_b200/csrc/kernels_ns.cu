@@ -1707,37 +1707,39 @@ __global__ void __launch_bounds__(256) k_ns_coarse_pass(int mc, int N, int pin, 
 }
 
 // y_n = z_n[q] + G_n y_{n-1} (y_{-1} = 0), one CTA of 1024 threads: thread (row
-// jj = t % 128 + 128 k, column group t / 128 of 8); y double-buffered by slab
-// parity, two barriers per slab; Y[n mp + jj].
-template <int NQ>
+// jj = t % R + R k, column group t / R of CG, R = 1024 / CG); y double-buffered by
+// slab parity, two barriers per slab; Y[n mp + jj].  Shared memory (2 + CG) mc
+// doubles: CG = 8, or 2 for the largest coarse levels (mc > 2560).
+template <int NQ, int CG>
 __global__ void __launch_bounds__(1024) k_ns_coarse_yrec(int mc, int N, const double *__restrict__ Z,
                                                          const double *__restrict__ G, double *__restrict__ Y) {
-  extern __shared__ double sh[];  // y (2 mc) + partials (8 mc)
+  extern __shared__ double sh[];  // y (2 mc) + partials (CG mc)
+  constexpr int R = 1024 / CG;
   double *yb = sh, *pp = sh + 2 * mc;
-  const int m = NQ * mc, tid = threadIdx.x, rr = tid & 127, cg8 = tid >> 7;
+  const int m = NQ * mc, tid = threadIdx.x, rr = tid % R, cg = tid / R;
   for (int j = tid; j < 2 * mc; j += blockDim.x) yb[j] = 0.0;
   __syncthreads();
   for (int n = 0; n < N; ++n) {
     const double *Gn = G + (int64_t)n * mc * mc;
     const double *yp = yb + ((n + 1) & 1) * mc;
     double *yn = yb + (n & 1) * mc;
-    for (int jj = rr; jj < mc; jj += 128) {
+    for (int jj = rr; jj < mc; jj += R) {
       double a0 = 0.0, a1 = 0.0;
       if (n > 0) {
-        int j = cg8;
-        for (; j + 8 < mc; j += 16) {
+        int j = cg;
+        for (; j + CG < mc; j += 2 * CG) {
           a0 = fma(__ldg(Gn + (int64_t)j * mc + jj), yp[j], a0);
-          a1 = fma(__ldg(Gn + (int64_t)(j + 8) * mc + jj), yp[j + 8], a1);
+          a1 = fma(__ldg(Gn + (int64_t)(j + CG) * mc + jj), yp[j + CG], a1);
         }
         if (j < mc) a0 = fma(__ldg(Gn + (int64_t)j * mc + jj), yp[j], a0);
       }
-      pp[cg8 * mc + jj] = a0 + a1;
+      pp[cg * mc + jj] = a0 + a1;
     }
     __syncthreads();
     for (int jj = tid; jj < mc; jj += blockDim.x) {
       double v = Z[(int64_t)n * m + jj * NQ + NQ - 1];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v += pp[k * mc + jj];
+      for (int k = 0; k < CG; ++k) v += pp[k * mc + jj];
       yn[jj] = v;
       Y[(int64_t)n * mc + jj] = v;
     }
@@ -2141,10 +2143,17 @@ void launch_ns_coarse_solve_pint(int q, int N, int mc, int pin, const int32_t *c
   dim3 grid((unsigned)N, (unsigned)((m + 31) / 32));
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
+    smem_optin((const void *)k_ns_coarse_pass<NQ, false>, m * (int)sizeof(double));
+    smem_optin((const void *)k_ns_coarse_pass<NQ, true>, m * (int)sizeof(double));
     k_ns_coarse_pass<NQ, false><<<grid, 256, m * sizeof(double), s>>>(mc, N, pin, cnodes, DinvT, r, Zs, nullptr,
                                                                       nullptr, nullptr);
-    smem_optin((const void *)k_ns_coarse_yrec<NQ>, 200 * 1024);
-    k_ns_coarse_yrec<NQ><<<1, 1024, 10 * mc * sizeof(double), s>>>(mc, N, Zs, G, Ys);
+    if (10 * (size_t)mc * sizeof(double) <= 200 * 1024) {
+      smem_optin((const void *)k_ns_coarse_yrec<NQ, 8>, 200 * 1024);
+      k_ns_coarse_yrec<NQ, 8><<<1, 1024, 10 * mc * sizeof(double), s>>>(mc, N, Zs, G, Ys);
+    } else {
+      smem_optin((const void *)k_ns_coarse_yrec<NQ, 2>, 220 * 1024);
+      k_ns_coarse_yrec<NQ, 2><<<1, 1024, 4 * mc * sizeof(double), s>>>(mc, N, Zs, G, Ys);
+    }
     k_ns_coarse_pass<NQ, true><<<grid, 256, mc * sizeof(double), s>>>(mc, N, pin, cnodes, DinvT, r, Zs, H, Ys, z);
   });
   g_launches += 3;

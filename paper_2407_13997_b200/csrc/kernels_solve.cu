@@ -517,6 +517,7 @@ void launch_coarse_solve(const Coarse &C, const Level &L, int q, int N, const do
   const int nq = q + 1;
   const int64_t NT = (int64_t)N * nq;
   cudaMemsetAsync(x, 0, L.nnode * NT * sizeof(double), s);
+  smem_optin((const void *)k_coarse_z, C.m * (int)sizeof(double));
   k_coarse_z<<<N, 256, C.m * sizeof(double), s>>>(C.m, C.mp, nq, NT, C.nodes, C.DinvT, r, C.Z); ++g_launches;
   size_t gq = (size_t)C.mp * C.mp * sizeof(double);
   int in_smem = (gq + 2 * C.mp * sizeof(double)) <= 200 * 1024;

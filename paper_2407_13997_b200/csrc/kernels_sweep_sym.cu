@@ -14,6 +14,8 @@
 // memory; one character block at a time is live in registers besides y.  The
 // block coefficients are kernel parameters (constant bank operands).  Patches of the
 // other (boundary) classes go through kernels_kron.cu on their own work lists.
+#include <cstdlib>
+
 #include "internal.h"
 #include "sym.h"
 
@@ -320,6 +322,196 @@ __device__ __forceinline__ void sym_patch_chunk_s(const SymTab &P, const int *sn
   }
 }
 
+// Chunk-parallel form of one character block (levels with few patches): the CTA's
+// four warps hold four consecutive 32-slab chunks of ONE patch.  Each warp scans its
+// chunk with zero carry-in, publishes the zero-carry end trace of every mode, and
+// after one barrier forms its true carry-in from the group's carry and the earlier
+// warps' end traces, y_in(w) = sigma^{32 w} ycar + sum_{w' < w} sigma^{32 (w - 1 - w')}
+// z(w') (the end-trace recurrence y_n = z_n + sigma y_{n-1} is linear): the slab
+// recurrence is solved in parallel over 128 slabs instead of one warp walking them.
+template <int D, int B, int VO, int MODE0, int NQ, int MP>
+__device__ __forceinline__ void sym_block_cp(const SymTab &P, double *yb, const double *ycar_in, double *ycar_out,
+                                             double *zend, int lane, int w) {
+  auto Y = [&](int j, int a) -> double & { return yb[j * 32 * NQ + a]; };
+  double t[NQ][D], vv[D];
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double yv[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) yv[j] = Y(B + j, a);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(P.V[VO + j * D + i], yv[j], s);
+      t[a][i] = s;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const int md = MODE0 + i;
+    double gh[NQ];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) gh[a] = t[a][i];
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double s = 0.0;
+#pragma unroll
+      for (int b2 = 0; b2 < NQ; ++b2) s = fma(P.S[md * 16 + a * NQ + b2], gh[b2], s);
+      t[a][i] = s;
+    }
+    double v = t[NQ - 1][i], pp = P.sig[md];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(0xffffffffu, v, d);
+      v = fma(lane >= d ? pp : 0.0, o, v);
+      pp *= pp;
+    }
+    vv[i] = v;
+    const double last = __shfl_sync(0xffffffffu, v, 31);
+    if (lane == 0) zend[w * MP + md] = last;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const int md = MODE0 + i;
+    const double sg = P.sig[md];
+    double s32 = sg;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) s32 *= s32;
+    double yin = ycar_in[md];
+    for (int w2 = 0; w2 < w; ++w2) yin = fma(s32, yin, zend[w2 * MP + md]);
+    double pw = 1.0, bs = sg;  // sigma^(lane + 1)
+#pragma unroll
+    for (int bit = 0; bit < 6; ++bit) {
+      pw *= (((lane + 1) >> bit) & 1) ? bs : 1.0;
+      bs *= bs;
+    }
+    const double yn = fma(pw, yin, vv[i]);
+    double yp = __shfl_up_sync(0xffffffffu, yn, 1);
+    if (lane == 0) yp = yin;
+#pragma unroll
+    for (int a = 0; a < NQ - 1; ++a) t[a][i] = fma(P.S[md * 16 + a * NQ + 0], yp, t[a][i]);
+    t[NQ - 1][i] = yn;
+    if (w == 3 && lane == 31) ycar_out[md] = yn;  // carry of the next group of four chunks
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; ++a)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) s = fma(P.V[VO + j * D + i], t[a][i], s);
+      Y(B + j, a) = s;
+    }
+}
+
+template <int K, int NQ>
+__device__ __forceinline__ void sym_patch_chunk_cp(const SymTab &P, const int *snode, const double *swt,
+                                                   const double *ycar_in, double *ycar_out, double *zend, int n,
+                                                   bool valid, int64_t NT, const double *__restrict__ r, int lane,
+                                                   int w, double *buf) {
+  using S = Sh<K>;
+  constexpr int MP = S::MP;
+  double *yb = buf + lane * NQ;
+  {
+    double g[NQ][MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) {
+      const double *src = r + (int64_t)snode[j] * NT + (int64_t)n * NQ;
+      if constexpr (NQ == 2) {
+        const double2 v = valid ? __ldg(reinterpret_cast<const double2 *>(src)) : make_double2(0.0, 0.0);
+        g[0][j] = v.x;
+        g[1][j] = v.y;
+      } else {
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) g[a][j] = valid ? __ldg(src + a) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+      double y[MP];
+      sym_fwd<K>(g[a], y);
+#pragma unroll
+      for (int j = 0; j < MP; ++j) yb[j * 32 * NQ + a] = y[j];
+    }
+  }
+  sym_block_cp<S::D0, S::B0, S::V0, S::B0, NQ, MP>(P, yb, ycar_in, ycar_out, zend, lane, w);
+  sym_block_cp<S::D1, S::B1, S::V1, S::B1, NQ, MP>(P, yb, ycar_in, ycar_out, zend, lane, w);
+  sym_block_cp<S::D2, S::B2, S::V2, S::B2, NQ, MP>(P, yb, ycar_in, ycar_out, zend, lane, w);
+  sym_block_cp<S::D3, S::B3, S::V3, S::B3, NQ, MP>(P, yb, ycar_in, ycar_out, zend, lane, w);
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+    double y[MP], x[MP];
+#pragma unroll
+    for (int j = 0; j < MP; ++j) y[j] = yb[j * 32 * NQ + a];
+    sym_bwd<K>(y, x);
+#pragma unroll
+    for (int j = 0; j < MP; ++j) yb[j * 32 * NQ + a] = swt[j] * x[j];
+  }
+}
+
+// CTA = one patch, warp = one 32-slab chunk of a group of four (sym_block_cp).
+template <int K, int NQ>
+__global__ void __launch_bounds__(128, 4) k_sweep_sym_cp(int N, int64_t npatch, const int32_t *__restrict__ list,
+                                                         const int32_t *__restrict__ pnodes,
+                                                         const __grid_constant__ SymTab P,
+                                                         const double *__restrict__ wnode, double omega,
+                                                         const double *__restrict__ r, double *__restrict__ u) {
+  constexpr int MP = Sh<K>::MP;
+  __shared__ int snode[MP];
+  __shared__ double swt[MP];
+  __shared__ double sycar[2][MP];
+  __shared__ double zend[4 * MP];
+  extern __shared__ __align__(16) double stage[];  // [4][MP][32][NQ]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t NT = (int64_t)N * NQ;
+  const int nch = (N + 31) / 32, ngrp = (nch + 3) / 4;
+  double *stg = stage + (size_t)w * MP * 32 * NQ;
+  for (int64_t i = blockIdx.x; i < npatch; i += gridDim.x) {
+    const int64_t p = list ? list[i] : i;
+    __syncthreads();
+    if (threadIdx.x < MP) {
+      const int nd = __ldg(pnodes + p * MP + threadIdx.x);
+      snode[threadIdx.x] = nd;
+      swt[threadIdx.x] = omega * __ldg(wnode + nd);
+      sycar[0][threadIdx.x] = 0.0;
+    }
+    __syncthreads();
+    for (int g = 0; g < ngrp; ++g) {
+      const int ch = 4 * g + w;
+      const int n = 32 * ch + lane;
+      sym_patch_chunk_cp<K, NQ>(P, snode, swt, sycar[g & 1], sycar[(g & 1) ^ 1], zend, n, n < N, NT, r, lane, w,
+                                stg);
+      __syncwarp();
+      if (ch < nch) {
+        const int64_t t0 = (int64_t)ch * 32 * NQ;
+        const int nv = (int)min((int64_t)32 * NQ, NT - t0);
+#pragma unroll 4
+        for (int j = 0; j < MP; ++j) {
+          double *dst = u + (int64_t)snode[j] * NT + t0;
+#pragma unroll
+          for (int e = 0; e < NQ; ++e) {
+            const int idx = lane + 32 * e;
+            if (idx < nv) atomicAdd(dst + idx, stg[j * 32 * NQ + idx]);
+          }
+        }
+      }
+      __syncthreads();  // the next group's carry is written; zend / stage reusable
+    }
+  }
+}
+
+// Chunk-parallel form: opt-in (WRMG_SWEEP_CP=1).
+bool use_chunk_parallel(int64_t np, int N) {
+  static const int mode = [] {
+    const char *e = getenv("WRMG_SWEEP_CP");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  (void)np;
+  return N > 32 && mode == 1;  // measured slower than one warp per patch at C2's 64^2 level
+}
+
 // Patches one per warp, FP64 atomics for the weighted additive scatter.
 template <int K, int NQ>
 __global__ void __launch_bounds__(128, 4) k_sweep_sym(int N, int64_t npatch, const int32_t *__restrict__ list,
@@ -457,7 +649,14 @@ void sym_launch(const Level &L, int N, const double *r, double *u, double omega,
     ++g_launches;
   }
   const int64_t np = L.ntile > 0 ? L.nsingle : L.nsym;
-  if (np > 0) {
+  if (np > 0 && use_chunk_parallel(np, N)) {
+    const int grid = (int)std::min<int64_t>(np, (int64_t)16 * num_sms());
+    const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
+    smem_optin((const void *)k_sweep_sym_cp<K, NQ>, smem);
+    k_sweep_sym_cp<K, NQ><<<grid, 128, smem, s>>>(N, np, L.ntile > 0 ? L.sym_single : nullptr, L.sym_nodes,
+                                                  L.symtab, L.wnode, omega, r, u);
+    ++g_launches;
+  } else if (np > 0) {
     const int64_t nblk = (np + 3) / 4;
     const int grid = (int)std::min<int64_t>(nblk, (int64_t)10 * num_sms());
     const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
@@ -472,8 +671,15 @@ template <int K, int NQ>
 void sym_list_launch(const Level &L, int N, const double *r, double *u, double omega, cudaStream_t s, int64_t np,
                      const int32_t *list) {
   if (np <= 0) return;
-  const int grid = (int)std::min<int64_t>((np + 3) / 4, (int64_t)10 * num_sms());
   const int smem = 4 * Sh<K>::MP * 32 * NQ * (int)sizeof(double);
+  if (use_chunk_parallel(np, N)) {
+    smem_optin((const void *)k_sweep_sym_cp<K, NQ>, smem);
+    k_sweep_sym_cp<K, NQ><<<(int)std::min<int64_t>(np, (int64_t)16 * num_sms()), 128, smem, s>>>(
+        N, np, list, L.sym_nodes, L.symtab, L.wnode, omega, r, u);
+    ++g_launches;
+    return;
+  }
+  const int grid = (int)std::min<int64_t>((np + 3) / 4, (int64_t)10 * num_sms());
   smem_optin((const void *)k_sweep_sym<K, NQ>, smem);
   k_sweep_sym<K, NQ><<<grid, 128, smem, s>>>(N, np, list, L.sym_nodes, L.symtab, L.wnode, omega, r, u);
   ++g_launches;

@@ -126,12 +126,15 @@ def _sampled_sweep_check(n, k, q, N, nodes_ij, omega=0.9):
 
 
 @pytest.mark.parametrize("n,k,q,N", [(40, 3, 0, 37), (40, 3, 2, 6), (40, 3, 1, 20), (36, 2, 0, 33),
-                                     (36, 2, 2, 4), (36, 2, 3, 5), (48, 2, 1, 3)])
+                                     (36, 2, 2, 4), (36, 2, 3, 5), (48, 2, 1, 3),
+                                     # chunk-parallel form (k_sweep_sym_cp): ragged groups, two groups
+                                     (36, 3, 1, 70), (32, 2, 1, 150)])
 def test_symmetric_sweep_sampled(n, k, q, N):
     """Levels with >= 1000 patches run the interior class through the symmetry-reduced
     sweep (kernels_sweep_sym.cu) and the boundary classes through kernels_kron.cu;
     sampled nodes cover the vertex, edge and cell-interior types of both, the corners
-    and the lattice edges."""
+    and the lattice edges.  With N > 32 slabs and fewer than 8 four-patch CTAs per SM
+    the chunk-parallel form runs (four warps = four 32-slab chunks of one patch)."""
     L = k * n + 1
     m = L // 2
     nodes = [(1, 1), (2, 1), (1, 2), (k, k), (k + 1, k), (2 * k, 1), (m, m), (m + 1, m), (m, m + 1),

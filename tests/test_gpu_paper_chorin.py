@@ -108,15 +108,14 @@ def test_paper_chorin_error_q0_N10():
 @pytest.mark.skipif(os.environ.get("WRMG_PAPER_TABLES") != "1", reason="set WRMG_PAPER_TABLES=1")
 @pytest.mark.parametrize("k", [1, 2])
 def test_paper_chorin_table(k):
-    """Spatial degree k column of Table tab:chorin:mg_errors.  k = 2 (P3-P2) runs on
-    a 5x5 coarsest level (the 10x10 one has m_c = 4246 per slab, beyond the dense
-    coarse solve): the hierarchy changes the iteration counts, not the
-    discretisation error being compared."""
+    """Spatial degree k column of Table tab:chorin:mg_errors on the paper's hierarchy
+    (Mref = 3: 80 x 80 over a 10 x 10 coarsest level; for k = 2 (P3-P2) x DG1 the
+    coarse slab blocks have m_c = 4246)."""
     out = os.environ.get("WRMG_TABLE_OUT")
     rows = []
     for q in (0, 1):
         for N in (10, 20, 40):
-            r = _paper_case(k, q, N, ncoarse=10 if k == 1 else 5)
+            r = _paper_case(k, q, N, ncoarse=10)
             rows.append(r)
             print(json.dumps(r), flush=True)
             if out:

@@ -162,11 +162,13 @@ def test_vcycle(n, k, q, N, mode):
     assert_parity(_host(z), multigrid.vcycle(H, r_np), what="vcycle")
 
 
-@pytest.mark.parametrize("n,k,q,N", [(8, 3, 1, 5), (6, 2, 3, 3), (10, 1, 0, 4)])
+@pytest.mark.parametrize("n,k,q,N", [(8, 3, 1, 5), (6, 2, 3, 3), (10, 1, 0, 4), (8, 2, 1, 7)])
 def test_one_level_coarse_solve_large_blocks(n, k, q, N):
     """H11 with a single level (ncoarse = n): the V-cycle is the exact time-marching
-    coarse solve; slab blocks of m = 1058 / 484 / 81 use the blocked Gauss-Jordan
-    inverse (kernels_gj.cu, m >= 192) or the CTA LU.  Checked against the oracle's
+    coarse solve; slab blocks of m = 1058 / 484 / 81 / 450 use the blocked Gauss-Jordan
+    inverse (kernels_gj.cu, m >= 192) or the CTA LU; coarse levels with more than 200
+    free nodes (529, 225 here) march with the stored block inverse instead of the
+    Kronecker form (no single-CTA eigen-setup).  Checked against the oracle's
     V-cycle and against A z = r (spsolve-free residual check)."""
     from oracle import multigrid
     import paper_2407_13997_b200 as w
