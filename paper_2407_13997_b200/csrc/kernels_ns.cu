@@ -647,6 +647,190 @@ __device__ int gj_invert_smem_wp(double *A, int m, double tol, double *X, int *p
   return s_info;
 }
 
+// ---- look-ahead form of gj_invert_smem_wp (same pivots, same operations per entry)
+// Panel k's update is split: first the next panel's tile column (all warps), then
+// warp 0 factors panel k + 1 in registers WHILE the other warps apply panel k to the
+// remaining tile columns -- the panel's serial shuffle chain overlaps the bulk DMMA
+// update instead of every other warp waiting for it at a barrier.  Two barriers per
+// panel plus one between the phases.
+
+// Warp 0: Gauss-Jordan on the panel columns [k0, k0 + nb) (registers, lane l holds
+// rows l, l + 32, ...), pivots into piv, the factored panel written back to A.
+template <int RPL>
+__device__ __forceinline__ void gj_wp_panel(double *A, int m, int k0, int nb, double tol, int *piv, int *s_info,
+                                            int lane) {
+  double P[RPL][GJB];
+#pragma unroll
+  for (int s = 0; s < RPL; ++s) {
+    const int r = lane + 32 * s;
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) P[s][t] = (r < m && t < nb) ? A[r * m + k0 + t] : 0.0;
+  }
+  int info = 0;
+#pragma unroll
+  for (int tc = 0; tc < GJB; ++tc) {
+    if (tc >= nb) break;
+    const int c = k0 + tc;
+    double bv = -1.0;
+    int bi = m;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+      const double v = fabs(P[s][tc]);
+      if (r >= c && r < m && v > bv) {
+        bv = v;
+        bi = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (!(bv >= tol) && info == 0) info = c + 1;
+    const int sp = bi >> 5, lp = bi & 31, sc = c >> 5, lc = c & 31;
+    double prow[GJB], crow[GJB];
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) {
+      double vp = 0.0, vc = 0.0;
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) {
+        vp = (s == sp) ? P[s][t] : vp;
+        vc = (s == sc) ? P[s][t] : vc;
+      }
+      prow[t] = __shfl_sync(0xffffffffu, vp, lp);
+      crow[t] = __shfl_sync(0xffffffffu, vc, lc);
+    }
+    const double pv = prow[tc];
+    const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
+    double newc[GJB];
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) newc[t] = (t == tc) ? pinv : prow[t] * pinv;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+      if (r == bi && bi != c) {
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) P[s][t] = crow[t];
+      }
+      if (r == c) {
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) P[s][t] = newc[t];
+      } else {
+        const double fr = P[s][tc];
+#pragma unroll
+        for (int t = 0; t < GJB; ++t)
+          if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
+        P[s][tc] = -fr * pinv;
+      }
+    }
+    if (lane == 0) piv[c] = bi;
+  }
+#pragma unroll
+  for (int s = 0; s < RPL; ++s) {
+    const int r = lane + 32 * s;
+    if (r < m)
+#pragma unroll
+      for (int t = 0; t < GJB; ++t)
+        if (t < nb) A[r * m + k0 + t] = P[s][t];
+  }
+  if (lane == 0 && info && *s_info == 0) *s_info = info;
+}
+
+// DMMA rank-nb update A[:, j] = [0 on pivot rows; A] + Panel X over the 8 x 8 tiles of
+// the selected tile columns: mode 0 every column but the panel's (pt), 1 only pt + 1,
+// 2 every column but pt and pt + 1.  Warps wslot, wslot + nws, ... walk the tiles.
+__device__ __forceinline__ void gj_tile_update(double *A, const double *X, int m, int k0, int nb, int mode,
+                                               int wslot, int nws, int lane) {
+  const int k1 = k0 + nb, nt8 = (m + 7) / 8, pt = k0 / 8;
+  const int nsel = mode == 0 ? nt8 - 1 : (mode == 1 ? 1 : nt8 - 2);
+  const int lr = lane >> 2, lc = lane & 3;
+  int tr = wslot, tci = 0;
+  for (;;) {
+    while (tr >= nt8) {
+      tr -= nt8;
+      ++tci;
+    }
+    if (tci >= nsel) break;
+    const int tc = mode == 1 ? pt + 1 : (tci < pt ? tci : tci + (mode == 0 ? 1 : 2));
+    const int R = tr * 8 + lr;
+    const bool rok = R < m, rpiv = R >= k0 && R < k1;
+    double cc[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int J = tc * 8 + 2 * lc + e;
+      cc[e] = (rok && !rpiv && J < m) ? A[R * m + J] : 0.0;
+    }
+    const int Jb = tc * 8 + lr;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = 4 * h + lc;
+      const double a = (rok && t < nb) ? A[R * m + k0 + t] : 0.0;
+      const double bb = (t < nb && Jb < m) ? X[t * m + Jb] : 0.0;
+      dmma_ns(cc[0], cc[1], a, bb);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int J = tc * 8 + 2 * lc + e;
+      if (rok && J < m) A[R * m + J] = cc[e];
+    }
+    tr += nws;
+  }
+}
+
+template <int RPL>
+__device__ int gj_invert_smem_la(double *A, int m, double tol, double *X, int *piv, int *idx) {
+  __shared__ int s_info;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  if (tid == 0) s_info = 0;
+  __syncthreads();
+  if (wid == 0) gj_wp_panel<RPL>(A, m, 0, min(GJB, m), tol, piv, &s_info, lane);
+  __syncthreads();
+  for (int k0 = 0; k0 < m; k0 += GJB) {
+    const int nb = min(GJB, m - k0), k1 = k0 + nb;
+    // the panel's row interchanges on the other columns (pivot order), X = pivot rows
+    for (int j = tid; j < m; j += nth) {
+      if (j >= k0 && j < k1) continue;
+      for (int c = k0; c < k1; ++c) {
+        const int p = piv[c];
+        if (p != c) {
+          const double t1 = A[c * m + j];
+          A[c * m + j] = A[p * m + j];
+          A[p * m + j] = t1;
+        }
+      }
+      for (int t = 0; t < nb; ++t) X[t * m + j] = A[(k0 + t) * m + j];
+    }
+    for (int e = tid; e < nb * nb; e += nth) X[(e / nb) * m + k0 + (e % nb)] = 0.0;
+    __syncthreads();
+    if (k1 < m) {
+      gj_tile_update(A, X, m, k0, nb, 1, wid, nw, lane);  // the next panel's columns first
+      __syncthreads();
+      if (wid == 0)
+        gj_wp_panel<RPL>(A, m, k1, min(GJB, m - k1), tol, piv, &s_info, lane);
+      else
+        gj_tile_update(A, X, m, k0, nb, 2, wid - 1, nw - 1, lane);
+    } else {
+      gj_tile_update(A, X, m, k0, nb, 0, wid, nw, lane);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    for (int c = 0; c < m; ++c) idx[c] = c;
+    for (int c = m - 1; c >= 0; --c) {
+      const int p = piv[c], t = idx[c];
+      idx[c] = idx[p];
+      idx[p] = t;
+    }
+  }
+  __syncthreads();
+  return s_info;
+}
+
 // Warp-per-block Gauss-Jordan (m <= 32 RPL): the same elimination as
 // gj_invert_smem_wp (identical pivots and operations per entry) carried out by one
 // warp on its own block -- panel in registers, interchanges and DMMA rank-GJB
@@ -872,8 +1056,8 @@ __global__ void __launch_bounds__(32 * WPB) k_ns_factor_warp(int mp, int N, int6
 // One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
 // DoFs: identity rows), invert, write the row-major inverse to
 // out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
-template <int NQ, int NTH, int RPL>
-__global__ void __launch_bounds__(NTH) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
+template <int NQ, int NTH, int RPL, bool LA = false>
+__global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
                                                    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
                                                    const double *__restrict__ Mv, const double *__restrict__ KGv,
                                                    int64_t nvrow, const int32_t *__restrict__ vvptr,
@@ -957,7 +1141,8 @@ __global__ void __launch_bounds__(NTH) k_ns_factor(int mp, int N, int64_t mstrid
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
   static_assert(GJB == 8, "panel width");
   int st;
-  if constexpr (RPL > 0) st = gj_invert_smem_wp<RPL>(A, m, 1e-14 * mx, X, piv, idx);  // m <= 32 RPL
+  if constexpr (RPL > 0 && LA) st = gj_invert_smem_la<RPL>(A, m, 1e-14 * mx, X, piv, idx);  // m <= 32 RPL
+  else if constexpr (RPL > 0) st = gj_invert_smem_wp<RPL>(A, m, 1e-14 * mx, X, piv, idx);
   else st = gj_invert_smem(A, m, 1e-14 * mx, X, piv, idx);
   double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
   for (int e = tid; e < m * m; e += blockDim.x) {
@@ -1995,6 +2180,11 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
     const char *e = getenv("WRMG_NS_FACTOR_WP");
     return !(e && e[0] == '0');
   }();
+  // look-ahead panels (gj_invert_smem_la); WRMG_NS_FACTOR_LA=0: without (A/B)
+  static const bool la = [] {
+    const char *e = getenv("WRMG_NS_FACTOR_LA");
+    return !(e && e[0] == '0');
+  }();
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
     // WRMG_NS_FACTOR_WARP=1: one warp per block, four blocks per CTA (measured slower:
@@ -2018,6 +2208,14 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
         k_ns_factor_warp<NQ, 1, 3><<<grid, 32, perw, s>>>(mp, N, nblk, mstride, pnodes, A.val, A.val2, conv, tm, out,
                                                          info, ppos, pvv);
       }
+    } else if (wp && la && m <= 96) {
+      smem_optin((const void *)k_ns_factor<NQ, 128, 3, true>, (int)sm);
+      k_ns_factor<NQ, 128, 3, true><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
+                                                          2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+    } else if (wp && la && m <= 192) {
+      smem_optin((const void *)k_ns_factor<NQ, 256, 6, true>, (int)sm);
+      k_ns_factor<NQ, 256, 6, true><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
+                                                          2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
     } else if (wp && m <= 96) {
       smem_optin((const void *)k_ns_factor<NQ, 128, 3>, (int)sm);
       k_ns_factor<NQ, 128, 3><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
