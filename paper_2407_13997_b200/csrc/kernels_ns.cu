@@ -831,6 +831,189 @@ __device__ int gj_invert_smem_la(double *A, int m, double tol, double *X, int *p
   return s_info;
 }
 
+// ---- look-ahead form without row interchanges (gj_invert_smem_lr)
+// The pivot rows stay where they are: column c eliminates with the unused row of
+// largest |a| (lowest row on ties -- on exact ties a different, equally valid pivot
+// than dgetrf's position order; the inverse agrees to rounding), recorded in
+// prow_of[c]; X copies the panel's pivot rows, the update zeroes them, and the row
+// order of the result is restored once at the end by replaying the equivalent
+// interchanges (the inverse of P A, then the column permutation as before).  No
+// interchange pass over the matrix per panel, no displaced-row shuffles in the panel.
+template <int RPL>
+__device__ __forceinline__ void gj_lr_panel(double *A, int m, int k0, int nb, double tol, int *prow_of,
+                                            int8_t *used_in, int *s_info, int lane) {
+  double P[RPL][GJB];
+  bool used[RPL];
+#pragma unroll
+  for (int s = 0; s < RPL; ++s) {
+    const int r = lane + 32 * s;
+    used[s] = r >= m || used_in[r] >= 0;
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) P[s][t] = (r < m && t < nb) ? A[r * m + k0 + t] : 0.0;
+  }
+  int info = 0;
+  const int pt = k0 / GJB;
+#pragma unroll
+  for (int tc = 0; tc < GJB; ++tc) {
+    if (tc >= nb) break;
+    const int c = k0 + tc;
+    double bv = -1.0;
+    int bi = m;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const double v = fabs(P[s][tc]);
+      if (!used[s] && v > bv) {
+        bv = v;
+        bi = lane + 32 * s;
+      }
+    }
+    double mv = bv;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
+    bi = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == mv ? bi : m));
+    if (!(mv >= tol) && info == 0) info = c + 1;
+    const int sp = bi >> 5, lp = bi & 31;
+    double prow[GJB];
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) {
+      double vp = 0.0;
+#pragma unroll
+      for (int s = 0; s < RPL; ++s) vp = (s == sp) ? P[s][t] : vp;
+      prow[t] = __shfl_sync(0xffffffffu, vp, lp);
+    }
+    const double pv = prow[tc];
+    const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
+    double newc[GJB];
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) newc[t] = (t == tc) ? pinv : prow[t] * pinv;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const int r = lane + 32 * s;
+      if (r == bi) {
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) P[s][t] = newc[t];
+        used[s] = true;
+      } else {
+        const double fr = P[s][tc];
+#pragma unroll
+        for (int t = 0; t < GJB; ++t)
+          if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
+        P[s][tc] = -fr * pinv;
+      }
+    }
+    if (lane == 0) {
+      prow_of[c] = bi < m ? bi : c;
+      if (bi < m) used_in[bi] = (int8_t)(pt & 127);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < RPL; ++s) {
+    const int r = lane + 32 * s;
+    if (r < m)
+#pragma unroll
+      for (int t = 0; t < GJB; ++t)
+        if (t < nb) A[r * m + k0 + t] = P[s][t];
+  }
+  if (lane == 0 && info && *s_info == 0) *s_info = info;
+}
+
+// gj_tile_update with the panel's pivot rows marked in used_in (== pt & 127).
+__device__ __forceinline__ void gj_lr_tile_update(double *A, const double *X, const int8_t *used_in, int m, int k0,
+                                                  int nb, int mode, int wslot, int nws, int lane) {
+  const int nt8 = (m + 7) / 8, pt = k0 / 8;
+  const int nsel = mode == 0 ? nt8 - 1 : (mode == 1 ? 1 : nt8 - 2);
+  const int lr = lane >> 2, lc = lane & 3;
+  const int8_t mark = (int8_t)(pt & 127);
+  int tr = wslot, tci = 0;
+  for (;;) {
+    while (tr >= nt8) {
+      tr -= nt8;
+      ++tci;
+    }
+    if (tci >= nsel) break;
+    const int tc = mode == 1 ? pt + 1 : (tci < pt ? tci : tci + (mode == 0 ? 1 : 2));
+    const int R = tr * 8 + lr;
+    const bool rok = R < m, rpiv = rok && used_in[R] == mark;
+    double cc[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int J = tc * 8 + 2 * lc + e;
+      cc[e] = (rok && !rpiv && J < m) ? A[R * m + J] : 0.0;
+    }
+    const int Jb = tc * 8 + lr;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = 4 * h + lc;
+      const double a = (rok && t < nb) ? A[R * m + k0 + t] : 0.0;
+      const double bb = (t < nb && Jb < m) ? X[t * m + Jb] : 0.0;
+      dmma_ns(cc[0], cc[1], a, bb);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int J = tc * 8 + 2 * lc + e;
+      if (rok && J < m) A[R * m + J] = cc[e];
+    }
+    tr += nws;
+  }
+}
+
+// On return rowmap[c] = the physical row of A holding row c of (P A)^{-1} and idx the
+// column permutation as in gj_invert_smem: D^{-1}[rho][sig] = A[rowmap[rho]][idx[sig]].
+// Shared scratch: piv, idx, rowmap, tmp (m ints each), used_in (m bytes).
+template <int RPL>
+__device__ int gj_invert_smem_lr(double *A, int m, double tol, double *X, int *piv, int *idx, int8_t *used_in,
+                                 int *rowmap, int *tmp) {
+  __shared__ int s_info;
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  if (tid == 0) s_info = 0;
+  for (int r = tid; r < m; r += nth) used_in[r] = -1;
+  __syncthreads();
+  int *prow_of = rowmap;  // the pivot row of every column during the elimination
+  if (wid == 0) gj_lr_panel<RPL>(A, m, 0, min(GJB, m), tol, prow_of, used_in, &s_info, lane);
+  __syncthreads();
+  for (int k0 = 0; k0 < m; k0 += GJB) {
+    const int nb = min(GJB, m - k0), k1 = k0 + nb;
+    for (int j = tid; j < m; j += nth) {  // X = the panel's pivot rows (other columns)
+      const bool inp = j >= k0 && j < k1;
+      for (int t = 0; t < nb; ++t) X[t * m + j] = inp ? 0.0 : A[prow_of[k0 + t] * m + j];
+    }
+    __syncthreads();
+    if (k1 < m) {
+      gj_lr_tile_update(A, X, used_in, m, k0, nb, 1, wid, nw, lane);
+      __syncthreads();
+      if (wid == 0)
+        gj_lr_panel<RPL>(A, m, k1, min(GJB, m - k1), tol, prow_of, used_in, &s_info, lane);
+      else
+        gj_lr_tile_update(A, X, used_in, m, k0, nb, 2, wid - 1, nw - 1, lane);
+    } else {
+      gj_lr_tile_update(A, X, used_in, m, k0, nb, 0, wid, nw, lane);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    // replay the equivalent interchanges: position c receives row prow_of[c]
+    int *pos2row = tmp, *row2pos = piv;
+    for (int c = 0; c < m; ++c) pos2row[c] = row2pos[c] = c;
+    for (int c = 0; c < m; ++c) {
+      const int pr = rowmap[c], pp = row2pos[pr], rc = pos2row[c];
+      pos2row[c] = pr;
+      pos2row[pp] = rc;
+      row2pos[pr] = c;
+      row2pos[rc] = pp;
+      rowmap[c] = pp;  // the dgetrf-style pivot position of column c
+    }
+    for (int c = 0; c < m; ++c) idx[c] = c;
+    for (int c = m - 1; c >= 0; --c) {
+      const int p = rowmap[c], t = idx[c];
+      idx[c] = idx[p];
+      idx[p] = t;
+    }
+    for (int c = 0; c < m; ++c) rowmap[c] = pos2row[c];
+  }
+  __syncthreads();
+  return s_info;
+}
+
 // Warp-per-block Gauss-Jordan (m <= 32 RPL): the same elimination as
 // gj_invert_smem_wp (identical pivots and operations per entry) carried out by one
 // warp on its own block -- panel in registers, interchanges and DMMA rank-GJB
@@ -1056,7 +1239,7 @@ __global__ void __launch_bounds__(32 * WPB) k_ns_factor_warp(int mp, int N, int6
 // One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
 // DoFs: identity rows), invert, write the row-major inverse to
 // out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
-template <int NQ, int NTH, int RPL, bool LA = false>
+template <int NQ, int NTH, int RPL, int LA = 0>  // LA: 0 gj_invert_smem_wp, 1 _la, 2 _lr
 __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
                                                    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
                                                    const double *__restrict__ Mv, const double *__restrict__ KGv,
@@ -1070,6 +1253,8 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
   int *piv = (int *)(X + GJB * m);
   int *idx = piv + m;
   int *nodes = idx + m;
+  int *rowmap = nodes + mp, *tmp = rowmap + m;  // LA == 2 only (ns_factor_smem_lr)
+  int8_t *used_in = (int8_t *)(tmp + m);
   __shared__ double s_red[32];
   const int64_t p = blockIdx.x;
   const int n = blockIdx.y;
@@ -1141,13 +1326,14 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_red[w]);
   static_assert(GJB == 8, "panel width");
   int st;
-  if constexpr (RPL > 0 && LA) st = gj_invert_smem_la<RPL>(A, m, 1e-14 * mx, X, piv, idx);  // m <= 32 RPL
+  if constexpr (RPL > 0 && LA == 2) st = gj_invert_smem_lr<RPL>(A, m, 1e-14 * mx, X, piv, idx, used_in, rowmap, tmp);
+  else if constexpr (RPL > 0 && LA == 1) st = gj_invert_smem_la<RPL>(A, m, 1e-14 * mx, X, piv, idx);  // m <= 32 RPL
   else if constexpr (RPL > 0) st = gj_invert_smem_wp<RPL>(A, m, 1e-14 * mx, X, piv, idx);
   else st = gj_invert_smem(A, m, 1e-14 * mx, X, piv, idx);
   double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
   for (int e = tid; e < m * m; e += blockDim.x) {
     const int sig = e / m, rho = e - sig * m;
-    o[e] = A[rho * m + idx[sig]];
+    o[e] = A[(LA == 2 ? rowmap[rho] : rho) * m + idx[sig]];
   }
   if (tid == 0) info[p * N + n] = st;
 }
@@ -2143,6 +2329,7 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
   const NSTime tm = make_nstime(T);
   const int m = (q + 1) * mp;
   const size_t sm = ns_factor_smem(m, mp);
+  const size_t sml = sm + (size_t)2 * m * sizeof(int) + (size_t)m + 8;  // + rowmap, tmp, used_in
   dim3 grid((unsigned)npatch, (unsigned)N);
   // row-per-thread register Gauss-Jordan, fully unrolled (instantiated for DG0 / DG1 patch sizes only:
   // each instance is ~7k straight-line DFMAs)
@@ -2180,10 +2367,11 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
     const char *e = getenv("WRMG_NS_FACTOR_WP");
     return !(e && e[0] == '0');
   }();
-  // look-ahead panels (gj_invert_smem_la); WRMG_NS_FACTOR_LA=0: without (A/B)
-  static const bool la = [] {
+  // look-ahead panels without row interchanges (gj_invert_smem_lr, default); WRMG_NS_FACTOR_LA=1:
+  // look-ahead with interchanges (gj_invert_smem_la), 0: neither (A/B)
+  static const int la = [] {
     const char *e = getenv("WRMG_NS_FACTOR_LA");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2) : 2;
   }();
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
@@ -2208,14 +2396,22 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
         k_ns_factor_warp<NQ, 1, 3><<<grid, 32, perw, s>>>(mp, N, nblk, mstride, pnodes, A.val, A.val2, conv, tm, out,
                                                          info, ppos, pvv);
       }
-    } else if (wp && la && m <= 96) {
-      smem_optin((const void *)k_ns_factor<NQ, 128, 3, true>, (int)sm);
-      k_ns_factor<NQ, 128, 3, true><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
-                                                          2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
-    } else if (wp && la && m <= 192) {
-      smem_optin((const void *)k_ns_factor<NQ, 256, 6, true>, (int)sm);
-      k_ns_factor<NQ, 256, 6, true><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
-                                                          2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+    } else if (wp && la == 2 && m <= 96) {
+      smem_optin((const void *)k_ns_factor<NQ, 128, 3, 2>, (int)sml);
+      k_ns_factor<NQ, 128, 3, 2><<<grid, 128, sml, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
+                                                        2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+    } else if (wp && la == 2 && m <= 192) {
+      smem_optin((const void *)k_ns_factor<NQ, 256, 6, 2>, (int)sml);
+      k_ns_factor<NQ, 256, 6, 2><<<grid, 256, sml, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
+                                                        2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+    } else if (wp && la == 1 && m <= 96) {
+      smem_optin((const void *)k_ns_factor<NQ, 128, 3, 1>, (int)sm);
+      k_ns_factor<NQ, 128, 3, 1><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
+                                                       2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+    } else if (wp && la == 1 && m <= 192) {
+      smem_optin((const void *)k_ns_factor<NQ, 256, 6, 1>, (int)sm);
+      k_ns_factor<NQ, 256, 6, 1><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
+                                                       2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
     } else if (wp && m <= 96) {
       smem_optin((const void *)k_ns_factor<NQ, 128, 3>, (int)sm);
       k_ns_factor<NQ, 128, 3><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
