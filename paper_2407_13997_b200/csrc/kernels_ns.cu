@@ -1236,30 +1236,16 @@ __global__ void __launch_bounds__(32 * WPB) k_ns_factor_warp(int mp, int N, int6
   }
 }
 
-// One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
-// DoFs: identity rows), invert, write the row-major inverse to
-// out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
-template <int NQ, int NTH, int RPL, int LA = 0>  // LA: 0 gj_invert_smem_wp, 1 _la, 2 _lr
-__global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
-                                                   const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
-                                                   const double *__restrict__ Mv, const double *__restrict__ KGv,
-                                                   int64_t nvrow, const int32_t *__restrict__ vvptr,
-                                                   const double *__restrict__ conv, NSTime tm,
-                                                   double *__restrict__ out, int32_t *__restrict__ info,
-                                                   const int32_t *__restrict__ ppos, const int32_t *__restrict__ pvv) {
-  extern __shared__ __align__(16) double smem[];
-  const int m = NQ * mp;
-  double *A = smem, *X = smem + (int64_t)m * m;  // X: GJB x m
-  int *piv = (int *)(X + GJB * m);
-  int *idx = piv + m;
-  int *nodes = idx + m;
-  int *rowmap = nodes + mp, *tmp = rowmap + m;  // LA == 2 only (ns_factor_smem_lr)
-  int8_t *used_in = (int8_t *)(tmp + m);
-  __shared__ double s_red[32];
-  const int64_t p = blockIdx.x;
-  const int n = blockIdx.y;
+// H4: D_{p,n} = R_p A_nn R_p^T (R9) assembled row-major (stride m) into shared A from the
+// per-patch pair tables; pad DoFs (node < 0) get identity rows.  The caller syncs after.
+template <int NQ>
+__device__ __forceinline__ void ns_assemble_block(double *A, int *nodes, int mp, int64_t p, int n, int N,
+                                                  const int32_t *__restrict__ pnodes, const double *__restrict__ Mv,
+                                                  const double *__restrict__ KGv, const double *__restrict__ conv,
+                                                  const NSTime &tm, const int32_t *__restrict__ ppos,
+                                                  const int32_t *__restrict__ pvv) {
+  const int m = NQ * mp, tid = threadIdx.x;
   const int64_t NT = (int64_t)N * NQ;
-  const int tid = threadIdx.x;
   for (int i = tid; i < mp; i += blockDim.x) nodes[i] = pnodes[p * mp + i];
   __syncthreads();
   // thread per node pair (i, j): the pair's CSR position, mass / stiffness values
@@ -1312,6 +1298,33 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
         }
     }
   }
+}
+
+// One CTA per (patch p = blockIdx.x, slab n = blockIdx.y): assemble D_{p,n} (pad
+// DoFs: identity rows), invert, write the row-major inverse to
+// out[(p N + n) mstride ...].  info[p N + n] = 0 or 1 + singular column.
+template <int NQ, int NTH, int RPL, int LA = 0>  // LA: 0 gj_invert_smem_wp, 1 _la, 2 _lr
+__global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes,
+                                                   const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                                                   const double *__restrict__ Mv, const double *__restrict__ KGv,
+                                                   int64_t nvrow, const int32_t *__restrict__ vvptr,
+                                                   const double *__restrict__ conv, NSTime tm,
+                                                   double *__restrict__ out, int32_t *__restrict__ info,
+                                                   const int32_t *__restrict__ ppos, const int32_t *__restrict__ pvv) {
+  extern __shared__ __align__(16) double smem[];
+  const int m = NQ * mp;
+  double *A = smem, *X = smem + (int64_t)m * m;  // X: GJB x m
+  int *piv = (int *)(X + GJB * m);
+  int *idx = piv + m;
+  int *nodes = idx + m;
+  int *rowmap = nodes + mp, *tmp = rowmap + m;  // LA == 2 only (ns_factor_smem_lr)
+  int8_t *used_in = (int8_t *)(tmp + m);
+  __shared__ double s_red[32];
+  const int64_t p = blockIdx.x;
+  const int n = blockIdx.y;
+  const int64_t NT = (int64_t)N * NQ;
+  const int tid = threadIdx.x;
+  ns_assemble_block<NQ>(A, nodes, mp, p, n, N, pnodes, Mv, KGv, conv, tm, ppos, pvv);
   __syncthreads();
   double rn = 0.0;  // max row norm (R10 tolerance)
   for (int r = tid; r < m; r += blockDim.x) {
@@ -1336,6 +1349,368 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
     o[e] = A[(LA == 2 ? rowmap[rho] : rho) * m + idx[sig]];
   }
   if (tid == 0) info[p * N + n] = st;
+}
+
+// ---- H5 register-tiled Gauss-Jordan (k_ns_factor_rt, m <= 96; round 2)
+// The block lives in DMMA accumulator fragments for the whole elimination: tile
+// column J (8 columns, M = 8 NT padded; pad rows / columns = identity) belongs to
+// accumulator warp J mod W, two tile columns per warp, so the rank-8 update of every
+// panel reads only the factored panel (A fragments) and the pivot rows (B fragments)
+// from shared memory -- the m^2 matrix itself is never re-read or re-written (the
+// shared-memory kernel moves the whole matrix through shared memory once per panel:
+// 83 % L1 busy, 56-66 % bank conflicts, ncu round 2).  A dedicated panel warp
+// factors panel K+1 (columns in registers, no row interchanges as in
+// gj_invert_smem_lr) while the accumulator warps apply panel K: the owner of tile
+// column K+1 updates it first, hands it over through shared memory (named barrier
+// 1), and the panel warp's pivot search is one redux.sync over a 32-bit key
+// (|a| rounded to 16 mantissa bits, ties and near-ties to the lowest row -- a
+// partial pivot within 2^-16 of the column maximum, R10) overlapped with each
+// lane's speculative reciprocal of its own best candidate.  The result rows are the
+// pivot rows of the unpermuted elimination: D^{-1}[rho][sig] = A[prow[rho]][q[sig]]
+// with q the inverse of prow (DESIGN R10).
+constexpr int RT_PS = 9;  // row stride of the panel hand-over buffer (odd: conflict-free row reads)
+
+__device__ __forceinline__ double rt_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  e = fma(e, e, e);  // r (1 + e + e^2): cubic step
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  return x != 0.0 ? r : 0.0;
+}
+
+// Panel K (columns k0 .. k0+nb) from Pin (M x RT_PS, current values) -> Pf (A-fragment
+// order [I][h][lane]) and the pivot records prow / used / tpos; one warp.  Row r is
+// slot s = r / 32 of lane r % 32; the pivot's slot is warp-uniform (from the redux), so
+// its broadcast is one uniform branch; every lane's reciprocals are computed
+// speculatively while the redux is in flight.
+template <int M>
+__device__ __forceinline__ void rt_panel(const double *Pin, double *Pf, int m, int K, int nb, double tol, int *prow,
+                                         int8_t *used, int8_t *tpos, int *s_info, unsigned *pmask, int lane) {
+  constexpr int RPL = (M + 31) / 32;
+  const int k0 = 8 * K;
+  double P[RPL][8];
+  unsigned elig = 0;
+#pragma unroll
+  for (int s = 0; s < RPL; ++s) {
+    const int r = lane + 32 * s;
+    if (r < m && used[r] < 0) elig |= 1u << s;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) P[s][t] = (r < M) ? Pin[r * RT_PS + t] : 0.0;
+  }
+  int mybi = 0, sing = 0;
+#pragma unroll
+  for (int tc = 0; tc < 8; ++tc) {
+    if (tc >= nb) break;
+    unsigned key = 0;
+    double rc[RPL];
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const double v = P[s][tc];
+      rc[s] = rt_rcp(v);
+      const unsigned k = ((elig >> s) & 1u)
+                             ? ((__float_as_uint((float)fabs(v)) & 0xFFFFFF00u) | (unsigned)(255 - (lane + 32 * s)))
+                             : 0u;
+      key = max(key, k);
+    }
+    const unsigned gk = __reduce_max_sync(0xffffffffu, key);
+    const int bi = 255 - (int)(gk & 255u), lp = bi & 31, sp = bi >> 5;
+    double prow_v[8], pinv = 0.0;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s)
+      if (s == sp) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) prow_v[t] = __shfl_sync(0xffffffffu, P[s][t], lp);
+        pinv = __shfl_sync(0xffffffffu, rc[s], lp);
+      }
+    const double pv = prow_v[tc];
+    double newc[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) newc[t] = (t == tc) ? pinv : prow_v[t] * pinv;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {
+      const double fr = P[s][tc];
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
+      P[s][tc] = -fr * pinv;
+    }
+    if (lane == lp) {
+#pragma unroll
+      for (int s = 0; s < RPL; ++s)
+        if (s == sp) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) P[s][t] = newc[t];
+        }
+      elig &= ~(1u << sp);
+    }
+    if (lane == tc) mybi = bi;
+    if (!(fabs(pv) >= tol) && sing == 0) sing = k0 + tc + 1;
+  }
+#pragma unroll
+  for (int s = 0; s < RPL; ++s) {
+    const int r = lane + 32 * s;
+    if (r < M)
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        Pf[((r >> 3) * 2 + (t >> 2)) * 32 + (((r & 7) << 2) | (t & 3))] = (t < nb) ? P[s][t] : 0.0;
+  }
+  // the pivot rows of this panel as per-lane-row masks: bit I of pmask[lr] = row 8 I + lr pivoted
+  unsigned pmk = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int bt = __shfl_sync(0xffffffffu, mybi, t);
+    if (t < nb && (bt & 7) == lane) pmk |= 1u << (bt >> 3);
+  }
+  if (lane < 8) pmask[(K & 1) * 8 + lane] = pmk;
+  if (lane < nb) {
+    prow[k0 + lane] = mybi;
+    used[mybi] = (int8_t)K;
+    tpos[mybi] = (int8_t)lane;
+  }
+  if (lane == 0 && sing && *s_info == 0) *s_info = sing;
+}
+
+// Rank-8 update of one (TWO = false) or two owned tile columns with panel K: acc += Pf X
+// (the pivot rows of panel K were reset to zero when their X rows were written).
+template <int NT, bool TWO>
+__device__ __forceinline__ void rt_update(double (&acc0)[NT][2], double (&acc1)[NT][2], const double *Pf,
+                                          const double *X, int J0, int J1, unsigned pm, int lane) {
+  const double b00 = X[(J0 * 2) * 32 + lane], b01 = X[(J0 * 2 + 1) * 32 + lane];
+  double b10 = 0.0, b11 = 0.0;
+  if (TWO) {
+    b10 = X[(J1 * 2) * 32 + lane];
+    b11 = X[(J1 * 2 + 1) * 32 + lane];
+  }
+#pragma unroll
+  for (int I = 0; I < NT; ++I) {
+    const double a0 = Pf[(I * 2) * 32 + lane], a1 = Pf[(I * 2 + 1) * 32 + lane];
+    dmma_ns(acc0[I][0], acc0[I][1], a0, b00);
+    dmma_ns(acc0[I][0], acc0[I][1], a1, b01);
+    if (TWO) {
+      dmma_ns(acc1[I][0], acc1[I][1], a0, b10);
+      dmma_ns(acc1[I][0], acc1[I][1], a1, b11);
+    }
+  }
+}
+
+template <int NT>
+__host__ __device__ constexpr size_t ns_factor_rt_buf_doubles(int m) {
+  // max(assembly / output matrix m x m, panel hand-over M x RT_PS + two Pf (8 M each) + X (8 M))
+  return (size_t)m * m > (size_t)(RT_PS + 24) * 8 * NT ? (size_t)m * m : (size_t)(RT_PS + 24) * 8 * NT;
+}
+template <int NT>
+__host__ __device__ constexpr size_t ns_factor_rt_smem(int m, int mp) {
+  return ns_factor_rt_buf_doubles<NT>(m) * sizeof(double) + (size_t)(2 * 8 * NT + mp) * sizeof(int) + 2 * 8 * NT + 16;
+}
+
+// phase timers of k_ns_factor_rt<..., PROF = true> (clock64 sums over all blocks; tools only)
+__device__ unsigned long long g_rtprof[16];
+#define RT_T0(v) \
+  long long v = 0;   \
+  if constexpr (PROF) v = clock64();
+#define RT_ACC(slot, v) \
+  if constexpr (PROF) \
+    if (lane == 0) atomicAdd(&g_rtprof[slot], (unsigned long long)(clock64() - v));
+
+template <int NQ, int NT, int MINB, bool PROF = false>
+__global__ void __launch_bounds__(32 * ((NT + 1) / 2 + 1), MINB)
+    k_ns_factor_rt(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes, const double *__restrict__ Mv,
+                   const double *__restrict__ KGv, const double *__restrict__ conv, NSTime tm,
+                   double *__restrict__ out, int32_t *__restrict__ info, const int32_t *__restrict__ ppos,
+                   const int32_t *__restrict__ pvv) {
+  constexpr int W = (NT + 1) / 2, M = 8 * NT;  // W accumulator warps + the panel warp (warp W)
+  extern __shared__ __align__(16) double smem[];
+  const int m = NQ * mp;
+  double *A = smem;
+  int *prow = (int *)(smem + ns_factor_rt_buf_doubles<NT>(m));
+  int *qinv = prow + M;
+  int *nodes = qinv + M;
+  int8_t *used = (int8_t *)(nodes + mp);
+  int8_t *tpos = used + M;
+  __shared__ double s_red[W + 1];
+  __shared__ int s_info;
+  __shared__ unsigned s_pmask[16];
+  const int64_t p = blockIdx.x;
+  const int n = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, lr = lane >> 2, lc = lane & 3;
+  RT_T0(t_start)
+  ns_assemble_block<NQ>(A, nodes, mp, p, n, N, pnodes, Mv, KGv, conv, tm, ppos, pvv);
+  for (int r = tid; r < M; r += blockDim.x) used[r] = -1;
+  if (tid == 0) s_info = 0;
+  __syncthreads();
+  double rn = 0.0;  // max row norm (R10 tolerance); rotated columns (no bank conflicts), 4 sums in flight
+  for (int r = tid; r < m; r += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const double *row = A + r * m;
+    int c = r, j = 0;
+    auto nx = [&](int x) { return x + 1 == m ? 0 : x + 1; };
+    for (; j + 4 <= m; j += 4) {
+      const int c1 = nx(c), c2 = nx(c1), c3 = nx(c2);
+      s0 += fabs(row[c]);
+      s1 += fabs(row[c1]);
+      s2 += fabs(row[c2]);
+      s3 += fabs(row[c3]);
+      c = nx(c3);
+    }
+    for (; j < m; ++j, c = nx(c)) s0 += fabs(row[c]);
+    rn = fmax(rn, (s0 + s1) + (s2 + s3));
+  }
+  for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
+  if (lane == 0) s_red[w] = rn;
+  double *Pin = A, *Pfb = A + RT_PS * M, *X = Pfb + 16 * M;
+  const int npan = (m + 7) / 8;
+  // Two role loops with the same CTA barriers: the accumulators are live only in the
+  // accumulator warps' loop (one shared loop would keep them live in the panel warp too).
+  if (w < W) {
+    double acc[2][NT][2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int J = w + W * c;
+#pragma unroll
+      for (int I = 0; I < NT; ++I)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int R = I * 8 + lr, C = J * 8 + 2 * lc + e;
+          acc[c][I][e] = (J < NT) ? ((R < m && C < m) ? A[R * m + C] : (R == C ? 1.0 : 0.0)) : 0.0;
+        }
+    }
+    __syncthreads();  // (1) A is free: the hand-over buffers alias it
+    RT_ACC(0, t_start)
+    RT_T0(t_elim)
+    if (w == 0) {     // panel 0: tile column 0 handed over
+#pragma unroll
+      for (int I = 0; I < NT; ++I)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Pin[(I * 8 + lr) * RT_PS + 2 * lc + e] = acc[0][I][e];
+      __syncwarp();
+      asm volatile("bar.arrive 1, %0;" ::"r"(64) : "memory");
+    }
+    __syncthreads();  // (2) panel 0 factored
+    for (int K = 0; K < npan; ++K) {
+      RT_T0(t_a)
+      const double *Pf = Pfb + (K & 1) * 8 * M;
+      const bool next = K + 1 < npan;
+      const unsigned pm = s_pmask[(K & 1) * 8 + lr];
+      const int J0 = w, J1 = w + W;
+      const bool v1 = J1 < NT;
+      // X: the pivot rows' current values in tile column J (B-fragment order [J][h][lane]);
+      // the pivot rows restart from zero (GJ: row = Pf X)
+      auto xw = [&](double(&ac)[NT][2], int J) {
+#pragma unroll
+        for (int I = 0; I < NT; ++I)
+          if ((pm >> I) & 1u) {
+            const int t = tpos[I * 8 + lr];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              X[(J * 2 + (t >> 2)) * 32 + (((2 * lc + e) << 2) | (t & 3))] = ac[I][e];
+              ac[I][e] = 0.0;
+            }
+          }
+        __syncwarp();
+      };
+      RT_ACC(1, t_a)
+      RT_T0(t_b)
+      auto take_panel = [&](double(&ac)[NT][2]) {  // the factored panel itself
+#pragma unroll
+        for (int I = 0; I < NT; ++I)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int t = 2 * lc + e;
+            ac[I][e] = Pf[(I * 2 + (t >> 2)) * 32 + ((lr << 2) | (t & 3))];
+          }
+      };
+      auto hand_over = [&](double(&ac)[NT][2]) {  // look-ahead column to the panel warp
+#pragma unroll
+        for (int I = 0; I < NT; ++I)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) Pin[(I * 8 + lr) * RT_PS + 2 * lc + e] = ac[I][e];
+        __syncwarp();
+        asm volatile("bar.arrive 1, %0;" ::"r"(64) : "memory");
+        RT_ACC(3, t_a)
+      };
+      if (J0 != K) xw(acc[0], J0);
+      if (v1 && J1 != K) xw(acc[1], J1);
+      if (J0 == K) {
+        take_panel(acc[0]);
+        if (v1) {
+          rt_update<NT, false>(acc[1], acc[1], Pf, X, J1, J1, pm, lane);
+          if (next && J1 == K + 1) hand_over(acc[1]);
+        }
+      } else if (v1 && J1 == K) {
+        take_panel(acc[1]);
+        rt_update<NT, false>(acc[0], acc[0], Pf, X, J0, J0, pm, lane);
+        if (next && J0 == K + 1) hand_over(acc[0]);
+      } else if (next && J0 == K + 1) {
+        rt_update<NT, false>(acc[0], acc[0], Pf, X, J0, J0, pm, lane);
+        hand_over(acc[0]);
+        if (v1) rt_update<NT, false>(acc[1], acc[1], Pf, X, J1, J1, pm, lane);
+      } else if (next && v1 && J1 == K + 1) {
+        rt_update<NT, false>(acc[1], acc[1], Pf, X, J1, J1, pm, lane);
+        hand_over(acc[1]);
+        rt_update<NT, false>(acc[0], acc[0], Pf, X, J0, J0, pm, lane);
+      } else if (v1) {
+        rt_update<NT, true>(acc[0], acc[1], Pf, X, J0, J1, pm, lane);
+      } else {
+        rt_update<NT, false>(acc[0], acc[0], Pf, X, J0, J0, pm, lane);
+      }
+      RT_ACC(2, t_b)
+      RT_T0(t_c)
+      __syncthreads();
+      RT_ACC(4, t_c)
+    }
+    RT_ACC(5, t_elim)
+    // result rows to shared memory (the hand-over buffers are dead after the last barrier)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int J = w + W * c;
+#pragma unroll
+      for (int I = 0; I < NT; ++I)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int R = I * 8 + lr, C = J * 8 + 2 * lc + e;
+          if (J < NT && R < m && C < m) A[R * m + C] = acc[c][I][e];
+        }
+    }
+  } else {
+    __syncthreads();  // (1)
+    double tol = 0.0;
+#pragma unroll
+    for (int i = 0; i <= W; ++i) tol = fmax(tol, s_red[i]);
+    tol *= 1e-14;
+    asm volatile("bar.sync 1, %0;" ::"r"(64) : "memory");
+    rt_panel<M>(Pin, Pfb, m, 0, min(8, m), tol, prow, used, tpos, &s_info, s_pmask, lane);
+    __syncthreads();  // (2)
+    for (int K = 0; K < npan; ++K) {
+      if (K + 1 < npan) {
+        RT_T0(t_w)
+        asm volatile("bar.sync 1, %0;" ::"r"(64) : "memory");
+        RT_ACC(8, t_w)
+        RT_T0(t_f)
+        rt_panel<M>(Pin, Pfb + ((K + 1) & 1) * 8 * M, m, K + 1, min(8, m - 8 * (K + 1)), tol, prow, used, tpos,
+                    &s_info, s_pmask, lane);
+        RT_ACC(9, t_f)
+      }
+      RT_T0(t_g)
+      __syncthreads();
+      RT_ACC(10, t_g)
+    }
+  }
+  RT_T0(t_o)
+  __syncthreads();
+  for (int c = tid; c < m; c += blockDim.x) qinv[prow[c]] = c;
+  __syncthreads();
+  double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+  for (int sig = w; sig < m; sig += W + 1) {
+    const int qs = qinv[sig];
+    for (int rho = lane; rho < m; rho += 32) o[(int64_t)sig * m + rho] = A[prow[rho] * m + qs];
+  }
+  if (tid == 0) info[p * N + n] = s_info;
+  RT_ACC(12, t_o)
+  if constexpr (PROF)
+    if (tid == 0) atomicAdd(&g_rtprof[15], 1ull);
 }
 
 // Register-tiled variant (m <= 80): thread t owns the TR x TC tile (t / NTC, t % NTC)
@@ -2373,6 +2748,33 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
     const char *e = getenv("WRMG_NS_FACTOR_LA");
     return e ? (e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2) : 2;
   }();
+  // register-tiled Gauss-Jordan (k_ns_factor_rt) for the Vanka block sizes m <= 96 of the
+  // Taylor-Hood levels (P2-P1: m = 39 (DG0), 78 (DG1); P3-P2: m = 81 (DG0));
+  // WRMG_NS_FACTOR_RT=0 selects the shared-memory kernels below (A/B), =9 the phase-timer
+  // build read by tools/rt_prof.py
+  static const int rt = [] {
+    const char *e = getenv("WRMG_NS_FACTOR_RT");
+    return e ? e[0] - '0' : 1;
+  }();
+  if (rt && force_smem) {
+    auto go = [&](auto kern, int nt) {
+      const int thr = 32 * ((nt + 1) / 2 + 1);
+      static const size_t pad = [] {  // experiments: WRMG_RT_SMEM_PAD=<KB> lowers the CTAs per SM
+        const char *e = getenv("WRMG_RT_SMEM_PAD");
+        return e ? (size_t)atoi(e) * 1024 : 0;
+      }();
+      const size_t smr = pad + std::max(ns_factor_rt_smem<5>(m, mp), std::max(ns_factor_rt_smem<10>(m, mp),
+                                                                             ns_factor_rt_smem<11>(m, mp)));
+      smem_optin((const void *)kern, (int)smr);
+      kern<<<grid, thr, smr, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos, pvv);
+      ++g_launches;
+    };
+    const int nt = (m + 7) / 8;
+    if (q == 0 && nt == 5) return go(k_ns_factor_rt<1, 5, 3>, 5);
+    if (q == 1 && nt == 10 && rt == 9) return go(k_ns_factor_rt<2, 10, 3, true>, 10);
+    if (q == 1 && nt == 10) return go(k_ns_factor_rt<2, 10, 3>, 10);
+    if (q == 0 && nt == 11) return go(k_ns_factor_rt<1, 11, 2>, 11);
+  }
   by_nq(q + 1, [&](auto NQc) {
     constexpr int NQ = decltype(NQc)::value;
     // WRMG_NS_FACTOR_WARP=1: one warp per block, four blocks per CTA (measured slower:
@@ -2574,3 +2976,11 @@ void launch_ns_coarse_solve(int q, int N, int mc, int pin, const int32_t *cnodes
 }
 
 }  // namespace wrmg
+
+// Tools only (not in include/wrmg.h): read and clear the k_ns_factor_rt phase timers
+// (WRMG_NS_FACTOR_RT=9 builds them); out[16] = clock64 sums, out[15] = blocks.
+extern "C" int wrmg_debug_rt_prof(unsigned long long *out) {
+  if (cudaMemcpyFromSymbol(out, wrmg::g_rtprof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(wrmg::g_rtprof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
