@@ -600,8 +600,10 @@ def run_c4(args, ws, rank, local):
             "data": "synthetic",
             "config": {"workload": f"C4 = BASELINE configs[3]: NS cavity P3-P2 x DG1, 128x128, dt=1/128, Re=1000, "
                                    f"linearised at the lid lift; N={N} slabs"
-                                   + (" (the full horizon [0, 1])" if full else
-                                      " (the 128-slab horizon needs 447 GB of stored block inverses: >= 4 GPUs)")
+                                   + ((" (the full horizon [0, 1]; 447 GB of block inverses: levels whose store "
+                                       "does not fit keep a slab window and recompute it in every sweep)")
+                                      if full and 32 * ws < 128 else " (the full horizon [0, 1])" if full else
+                                      " (--c4-n 128: the full horizon, windowed inverses on one GPU)")
                                    + "; step = 10 sweeps + residual + V(1,1)",
                        "parallelism": f"{ws} spatial strips, NCCL halos" if ws > 1 else "1 GPU",
                        "ndof": lay["ndof"], "nfree_st": lay["nfree_st"], "levels": lay["nlevels"],
@@ -810,7 +812,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--c4-n", type=int, default=0,
-                    help="C4 slabs (0: min(128, 32 x GPUs); one GPU holds the inverses of 32)")
+                    help="C4 slabs (0: min(128, 32 x GPUs); one GPU stores the inverses of 32, more slabs "
+                         "recompute windows of them in every sweep)")
     ap.add_argument("--c5-n", type=int, default=1024, help="C5 cells per side per GPU (1024 = the config)")
     ap.add_argument("--scatter", default="atomic", choices=["atomic", "colour"],
                     help="weighted additive scatter of the heat sweep (H8): FP64 atomics or coloured passes")

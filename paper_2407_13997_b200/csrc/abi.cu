@@ -256,6 +256,25 @@ void prof_residual(wrmg_ctx *c, int l, const double *u, const double *b, double 
 }
 
 void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
+  if (c->ns && c->lv[l].nswin < c->N) {  // slab windows: recompute each window's inverses, then sweep it
+    const Level &L = c->lv[l];
+    const double m = (double)c->nq * L.mp;
+    for (int n0 = 0; n0 < c->N; n0 += L.nswin) {
+      const int nw = std::min(L.nswin, c->N - n0);
+      const double fr = (double)nw / c->N;
+      {
+        PScope pf(c, WRMG_K_FACTOR, l, 8.0 * (double)L.npatch * nw * L.mstride,
+                  2.0 * m * m * m * (double)L.npatch * nw);
+        launch_ns_factor(geom(c, L), c->q, c->N, c->tm, L.A, L.vvptr, L.conv, L.pnodes, L.npatch, L.mp, L.mstride,
+                         L.nsinv, L.nsinfo, L.ppos, L.pvv, c->stream, n0, nw);
+      }
+      PScope ps(c, WRMG_K_SWEEP, l, sweep_bytes(c, l) * fr, c->sweep_flops[l] * fr);
+      launch_ns_sweep(c->q, c->N, L.mp, L.npatch, L.mstride, L.pnodes, L.wnode, L.A, L.nsinv, r, u, om, c->stream,
+                      n0, nw, L.nsxs);
+    }
+    if (!c->strip) ns_project(c, L, u);
+    return;
+  }
   PScope ps(c, WRMG_K_SWEEP, l, sweep_bytes(c, l), c->sweep_flops[l]);
   if (c->ns) {
     const Level &L = c->lv[l];
@@ -311,7 +330,7 @@ void free_level(Level &L) {
                   (void *)L.vt, (void *)L.kV, (void *)L.kVT, (void *)L.kS, (void *)L.ksig, (void *)L.cta_patch,
                   (void *)L.cta_type, (void *)L.rcls, (void *)L.cta_patch1, (void *)L.cta_type1,
                   (void *)L.goff, (void *)L.grp_patch8, (void *)L.grp_type8, (void *)L.vvptr, (void *)L.conv,
-                  (void *)L.state, (void *)L.nsinv, (void *)L.nsinfo, (void *)L.ppos, (void *)L.pvv, (void *)L.hx[0],
+                  (void *)L.state, (void *)L.nsinv, (void *)L.nsxs, (void *)L.nsinfo, (void *)L.ppos, (void *)L.pvv, (void *)L.hx[0],
                   (void *)L.hx[1],
                   (void *)L.hx[2], (void *)L.hx[3], (void *)L.gen_rows, (void *)L.sym_nodes,
                   (void *)L.tile_patch, (void *)L.sym_single, (void *)L.tgeo_dev})
@@ -800,8 +819,11 @@ void factor_all_ns(wrmg_ctx *c, const double *W) {
       const double m = (double)c->nq * L.mp;
       PScope ps(c, WRMG_K_FACTOR, l, 8.0 * (double)L.npatch * c->N * L.mstride,
                 2.0 * m * m * m * (double)L.npatch * c->N);
-      launch_ns_factor(geom(c, L), c->q, c->N, c->tm, L.A, L.vvptr, L.conv, L.pnodes, L.npatch, L.mp, L.mstride,
-                       L.nsinv, L.nsinfo, L.ppos, L.pvv, s);
+      // slab windows: every window factored once here for the singularity check (the sweeps
+      // recompute them); a stored level is one window
+      for (int n0 = 0; n0 < c->N; n0 += L.nswin)
+        launch_ns_factor(geom(c, L), c->q, c->N, c->tm, L.A, L.vvptr, L.conv, L.pnodes, L.npatch, L.mp, L.mstride,
+                         L.nsinv, L.nsinfo, L.ppos, L.pvv, s, n0, std::min(L.nswin, c->N - n0));
       check_launch();
     }
   }
@@ -872,6 +894,46 @@ void make_strip_comm(wrmg_ctx *c) {
 }
 
 // Hierarchy of Taylor-Hood levels (problem == WRMG_NAVIER_STOKES).
+// Stored Vanka inverses (m^2 doubles per (patch, slab)): levels whose store does not fit
+// the memory budget keep a window of W slabs only and recompute it inside every sweep
+// ("slab windows"): the budget is 85 % of the free device memory less the
+// FGMRES(30) basis a later solve allocates; while the stores exceed it, the level with the
+// largest store halves its window.  WRMG_NS_WINDOW=<W> windows every stored level at W
+// slabs (tests), WRMG_NS_STORE_GB=<GB> sets the budget.
+void ns_slab_windows(wrmg_ctx *c) {
+  std::vector<Level *> ls;
+  for (auto &L : c->lv)
+    if (L.nsinfo) ls.push_back(&L);
+  for (Level *L : ls) L->nswin = c->N;
+  auto per_slab = [&](const Level *L) { return 8.0 * (double)L->npatch * (double)L->mstride; };
+  if (const char *e = getenv("WRMG_NS_WINDOW")) {
+    const int w = atoi(e);
+    if (w > 0)
+      for (Level *L : ls) L->nswin = std::min(w, c->N);
+  } else {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    double budget = 0.85 * (double)fr - 62.0 * 8.0 * (double)c->lv.back().nnode * (double)c->nt;
+    if (const char *e = getenv("WRMG_NS_STORE_GB")) budget = atof(e) * 1e9;
+    auto total = [&] {
+      double t = 0.0;
+      for (Level *L : ls) t += per_slab(L) * L->nswin;
+      return t;
+    };
+    while (total() > budget) {
+      Level *big = nullptr;
+      for (Level *L : ls)
+        if (L->nswin > 1 && (!big || per_slab(L) * L->nswin > per_slab(big) * big->nswin)) big = L;
+      if (!big) throw Err{WRMG_E_OOM, "Vanka inverses: one slab per level does not fit the device"};
+      big->nswin = (big->nswin + 1) / 2;
+    }
+  }
+  for (Level *L : ls) {
+    L->nsinv = dalloc<double>((size_t)L->npatch * L->nswin * L->mstride);
+    if (L->nswin < c->N) L->nsxs = dzalloc<double>((size_t)L->npatch * c->nq * L->mp);
+  }
+}
+
 void setup_ns(wrmg_ctx *c) {
   cudaStream_t s = c->stream;
   if (c->k > 2) throw Err{WRMG_E_UNSUPPORTED, "Navier-Stokes: degree must be 1 (P2-P1) or 2 (P3-P2)"};
@@ -1001,8 +1063,7 @@ void setup_ns(wrmg_ctx *c) {
       L.nfree_owned = nfo;
       for (int b = 0; b < 4; ++b) L.hx[b] = dalloc<double>(halo_doubles(c, L));
     }
-    if (l >= 1 || nl == 1 || c->strip) {
-      L.nsinv = dalloc<double>((size_t)L.npatch * c->N * L.mstride);
+    if (l >= 1 || nl == 1 || c->strip) {  // the stored inverses are allocated after the slab windows are set
       L.nsinfo = dalloc<int32_t>((size_t)L.npatch * c->N);
       L.ppos = dalloc<int32_t>((size_t)L.npatch * L.mp * L.mp);
       L.pvv = dalloc<int32_t>((size_t)L.npatch * L.mp * L.mp);
@@ -1130,6 +1191,7 @@ void setup_ns(wrmg_ctx *c) {
       c->cbr[l] = dzalloc<double>(c->lv[l].nnode * c->nt);
     }
   }
+  ns_slab_windows(c);
   factor_all_ns(c, nullptr);
 }
 

@@ -188,7 +188,9 @@ struct Level {
   double *conv = nullptr;           // [nvv][NT]: R N(w_{n,c}) of the current linearisation
   double *state = nullptr;          // injected linearisation state (levels below the finest)
   int64_t mstride = 0;              // doubles per stored (patch, slab) inverse
-  double *nsinv = nullptr;          // [npatch][N][mstride] row-major D_{p,n}^{-1}
+  double *nsinv = nullptr;          // [npatch][nswin][mstride] column-major D_{p,n}^{-1}
+  int nswin = 0;                    // stored slabs per patch: N, or a window recomputed in every sweep
+  double *nsxs = nullptr;           // windows: [npatch][m] patch solution at the end of the previous window
   int32_t *nsinfo = nullptr;        // [npatch][N]
   int32_t *ppos = nullptr, *pvv = nullptr;  // [npatch][mp][mp] CSR / convection index of each patch pair
   int64_t nsfree_patch_dofs = 0;    // sum of patch sizes (algorithmic accounting)

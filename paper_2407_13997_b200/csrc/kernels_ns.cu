@@ -1310,7 +1310,8 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
                                                    int64_t nvrow, const int32_t *__restrict__ vvptr,
                                                    const double *__restrict__ conv, NSTime tm,
                                                    double *__restrict__ out, int32_t *__restrict__ info,
-                                                   const int32_t *__restrict__ ppos, const int32_t *__restrict__ pvv) {
+                                                   const int32_t *__restrict__ ppos, const int32_t *__restrict__ pvv,
+                                                   int n0, int nwin) {
   extern __shared__ __align__(16) double smem[];
   const int m = NQ * mp;
   double *A = smem, *X = smem + (int64_t)m * m;  // X: GJB x m
@@ -1321,7 +1322,7 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
   int8_t *used_in = (int8_t *)(tmp + m);
   __shared__ double s_red[32];
   const int64_t p = blockIdx.x;
-  const int n = blockIdx.y;
+  const int n = n0 + blockIdx.y;  // slab window [n0, n0 + nwin)
   const int64_t NT = (int64_t)N * NQ;
   const int tid = threadIdx.x;
   ns_assemble_block<NQ>(A, nodes, mp, p, n, N, pnodes, Mv, KGv, conv, tm, ppos, pvv);
@@ -1343,7 +1344,7 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
   else if constexpr (RPL > 0 && LA == 1) st = gj_invert_smem_la<RPL>(A, m, 1e-14 * mx, X, piv, idx);  // m <= 32 RPL
   else if constexpr (RPL > 0) st = gj_invert_smem_wp<RPL>(A, m, 1e-14 * mx, X, piv, idx);
   else st = gj_invert_smem(A, m, 1e-14 * mx, X, piv, idx);
-  double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+  double *o = out + (p * nwin + blockIdx.y) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
   for (int e = tid; e < m * m; e += blockDim.x) {
     const int sig = e / m, rho = e - sig * m;
     o[e] = A[(LA == 2 ? rowmap[rho] : rho) * m + idx[sig]];
@@ -1520,7 +1521,7 @@ __global__ void __launch_bounds__(32 * ((NT + 1) / 2 + 1), MINB)
     k_ns_factor_rt(int mp, int N, int64_t mstride, const int32_t *__restrict__ pnodes, const double *__restrict__ Mv,
                    const double *__restrict__ KGv, const double *__restrict__ conv, NSTime tm,
                    double *__restrict__ out, int32_t *__restrict__ info, const int32_t *__restrict__ ppos,
-                   const int32_t *__restrict__ pvv) {
+                   const int32_t *__restrict__ pvv, int n0, int nwin) {
   constexpr int W = (NT + 1) / 2, M = 8 * NT;  // W accumulator warps + the panel warp (warp W)
   extern __shared__ __align__(16) double smem[];
   const int m = NQ * mp;
@@ -1534,7 +1535,7 @@ __global__ void __launch_bounds__(32 * ((NT + 1) / 2 + 1), MINB)
   __shared__ int s_info;
   __shared__ unsigned s_pmask[16];
   const int64_t p = blockIdx.x;
-  const int n = blockIdx.y;
+  const int n = n0 + blockIdx.y;  // slab window [n0, n0 + nwin)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, lr = lane >> 2, lc = lane & 3;
   RT_T0(t_start)
   ns_assemble_block<NQ>(A, nodes, mp, p, n, N, pnodes, Mv, KGv, conv, tm, ppos, pvv);
@@ -1702,7 +1703,7 @@ __global__ void __launch_bounds__(32 * ((NT + 1) / 2 + 1), MINB)
   __syncthreads();
   for (int c = tid; c < m; c += blockDim.x) qinv[prow[c]] = c;
   __syncthreads();
-  double *o = out + (p * N + n) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
+  double *o = out + (p * nwin + blockIdx.y) * mstride;  // column-major: o[sig m + rho] = D^{-1}[rho][sig]
   for (int sig = w; sig < m; sig += W + 1) {
     const int qs = qinv[sig];
     for (int rho = lane; rho < m; rho += 32) o[(int64_t)sig * m + rho] = A[prow[rho] * m + qs];
@@ -2099,7 +2100,8 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
                                                   const double *__restrict__ wnode, const int32_t *__restrict__ rowptr,
                                                   const int32_t *__restrict__ col, const double *__restrict__ Mv,
                                                   const double *__restrict__ Dinv, const double *__restrict__ r,
-                                                  double *__restrict__ u, double omega) {
+                                                  double *__restrict__ u, double omega, int n0, int nwin,
+                                                  double *__restrict__ xs) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bar[2];
   const int m = NQ * mp;
@@ -2111,7 +2113,9 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
   const int64_t p = blockIdx.x;
   const int64_t NT = (int64_t)N * NQ;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  const double *Dp = Dinv + p * N * mstride;
+  // slab window [n0, n0 + nwin): Dinv holds the window's inverses, xs (windows after the
+  // first) the patch solution of slab n0 - 1 for the jump
+  const double *Dp = Dinv + p * nwin * mstride;
   const unsigned bytes = (unsigned)(m * m * sizeof(double) + 15) & ~15u;
   if (STAGED && tid == 0) {
     mbar_init_ns(&bar[0], 1);
@@ -2125,6 +2129,7 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
     wn[i] = s >= 0 ? omega * wnode[s] : 0.0;
     xq[i] = 0.0;
   }
+  for (int i = tid; i < m; i += blockDim.x) x[i] = (n0 > 0 && xs) ? xs[p * m + i] : 0.0;
   __syncthreads();
   for (int e = tid; e < mp * mp; e += blockDim.x) {
     const int i = e / mp, j = e - i * mp;
@@ -2141,13 +2146,15 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
   const int i_me = tid / NQ, a_me = tid - (tid / NQ) * NQ;
   const bool own = tid < m && nodes[i_me < mp ? i_me : 0] >= 0 && i_me < mp;
   const int64_t rbase = own ? (int64_t)nodes[i_me] * NT + a_me : 0;
-  double rcur = own ? __ldg(r + rbase) : 0.0;
-  for (int n = 0; n < N; ++n) {
-    if (STAGED && tid == 0 && n + 1 < N) {
+  const int n1 = n0 + nwin;
+  double rcur = own ? __ldg(r + rbase + (int64_t)n0 * NQ) : 0.0;
+  for (int n = n0; n < n1; ++n) {
+    const int ln = n - n0;  // slab within the window
+    if (STAGED && tid == 0 && n + 1 < n1) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      bulk_load(buf + ((n + 1) & 1) * mstride, Dp + (int64_t)(n + 1) * mstride, bytes, &bar[(n + 1) & 1]);
+      bulk_load(buf + ((ln + 1) & 1) * mstride, Dp + (int64_t)(ln + 1) * mstride, bytes, &bar[(ln + 1) & 1]);
     }
-    const double rnext = (own && n + 1 < N) ? __ldg(r + rbase + (int64_t)(n + 1) * NQ) : 0.0;
+    const double rnext = (own && n + 1 < n1) ? __ldg(r + rbase + (int64_t)(n + 1) * NQ) : 0.0;
     if (tid < m) {
       double v = rcur;
       if (own && a_me == 0 && n > 0)  // jump: M_p x_{n-1}[q] (x still holds slab n-1)
@@ -2158,10 +2165,10 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
     __syncthreads();
     const double *D;
     if (STAGED) {
-      mbar_wait_ns(&bar[n & 1], (n >> 1) & 1);
-      D = buf + (n & 1) * mstride;
+      mbar_wait_ns(&bar[ln & 1], (ln >> 1) & 1);
+      D = buf + (ln & 1) * mstride;
     } else {
-      D = Dp + (int64_t)n * mstride;
+      D = Dp + (int64_t)ln * mstride;
     }
     // x = D^{-1} g with D^{-1} column-major: thread (rho, grp) sums columns
     // sig = grp, grp + G, ... (consecutive rho -> consecutive banks), partials in smem
@@ -2182,6 +2189,8 @@ __global__ void __launch_bounds__(256) k_ns_sweep(int mp, int N, int64_t mstride
     }
     __syncthreads();
   }
+  if (xs && n1 < N)
+    for (int i = tid; i < m; i += blockDim.x) xs[p * m + i] = x[i];
 }
 
 // Large blocks (m x m too big for a shared double buffer, e.g. P3-P2 x DG1,
@@ -2197,7 +2206,8 @@ __global__ void __launch_bounds__(256) k_ns_sweep_chunked(int mp, int N, int64_t
                                                           const int32_t *__restrict__ col,
                                                           const double *__restrict__ Mv,
                                                           const double *__restrict__ Dinv, const double *__restrict__ r,
-                                                          double *__restrict__ u, double omega) {
+                                                          double *__restrict__ u, double omega, int n0, int nwin,
+                                                          double *__restrict__ xs) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bar[8];
   const int m = NQ * mp;
@@ -2209,9 +2219,9 @@ __global__ void __launch_bounds__(256) k_ns_sweep_chunked(int mp, int N, int64_t
   const int64_t p = blockIdx.x;
   const int64_t NT = (int64_t)N * NQ;
   const int tid = threadIdx.x;
-  const double *Dp = Dinv + p * N * mstride;
+  const double *Dp = Dinv + p * nwin * mstride;  // the window [n0, n0 + nwin) (k_ns_sweep)
   const int nch = (m + CW - 1) / CW;
-  const int64_t total = (int64_t)N * nch;
+  const int64_t total = (int64_t)nwin * nch;
   auto issue = [&](int64_t t) {  // chunk t = (slab n, chunk c) into slot t % R
     const int64_t n = t / nch;
     const int c = (int)(t - n * nch);
@@ -2239,14 +2249,15 @@ __global__ void __launch_bounds__(256) k_ns_sweep_chunked(int mp, int N, int64_t
     }
     Mp[e] = v;
   }
-  for (int i = tid; i < m; i += blockDim.x) x[i] = 0.0;
+  for (int i = tid; i < m; i += blockDim.x) x[i] = (n0 > 0 && xs) ? xs[p * m + i] : 0.0;
   __syncthreads();
   const int i_me = tid / NQ, a_me = tid - (tid / NQ) * NQ;
   const bool own = tid < m && i_me < mp && nodes[i_me] >= 0;
   const int64_t rbase = own ? (int64_t)nodes[i_me] * NT + a_me : 0;
-  double rcur = own ? __ldg(r + rbase) : 0.0;
-  for (int n = 0; n < N; ++n) {
-    const double rnext = (own && n + 1 < N) ? __ldg(r + rbase + (int64_t)(n + 1) * NQ) : 0.0;
+  const int n1 = n0 + nwin;
+  double rcur = own ? __ldg(r + rbase + (int64_t)n0 * NQ) : 0.0;
+  for (int n = n0; n < n1; ++n) {
+    const double rnext = (own && n + 1 < n1) ? __ldg(r + rbase + (int64_t)(n + 1) * NQ) : 0.0;
     if (tid < m) {
       double v = rcur;
       if (own && a_me == 0 && n > 0)  // jump: M_p x_{n-1}[q]
@@ -2257,7 +2268,7 @@ __global__ void __launch_bounds__(256) k_ns_sweep_chunked(int mp, int N, int64_t
     __syncthreads();
     double acc = 0.0;
     for (int c = 0; c < nch; ++c) {
-      const int64_t t = (int64_t)n * nch + c;
+      const int64_t t = (int64_t)(n - n0) * nch + c;
       mbar_wait_ns(&bar[t % R], (unsigned)((t / R) & 1));
       const double *D = ring + (t % R) * slot;
       const int cols = min(CW, m - c * CW);
@@ -2277,6 +2288,8 @@ __global__ void __launch_bounds__(256) k_ns_sweep_chunked(int mp, int N, int64_t
     }
     __syncthreads();
   }
+  if (xs && n1 < N)
+    for (int i = tid; i < m; i += blockDim.x) xs[p * m + i] = x[i];
 }
 
 // --------------------------------------------------------------- H15 projection
@@ -2700,12 +2713,14 @@ void launch_ns_patch_pos(const NSGeom &g, const DevCSR &A, const int32_t *vvptr,
 
 void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                       const double *conv, const int32_t *pnodes, int64_t npatch, int mp, int64_t mstride, double *out,
-                      int32_t *info, const int32_t *ppos, const int32_t *pvv, cudaStream_t s) {
+                      int32_t *info, const int32_t *ppos, const int32_t *pvv, cudaStream_t s,
+                      int n0, int nwin) {
   const NSTime tm = make_nstime(T);
   const int m = (q + 1) * mp;
+  if (nwin <= 0) nwin = N;  // slab window [n0, n0 + nwin): out holds npatch x nwin inverses
   const size_t sm = ns_factor_smem(m, mp);
   const size_t sml = sm + (size_t)2 * m * sizeof(int) + (size_t)m + 8;  // + rowmap, tmp, used_in
-  dim3 grid((unsigned)npatch, (unsigned)N);
+  dim3 grid((unsigned)npatch, (unsigned)nwin);
   // row-per-thread register Gauss-Jordan, fully unrolled (instantiated for DG0 / DG1 patch sizes only:
   // each instance is ~7k straight-line DFMAs)
   // The shared-memory blocked kernel (gj_invert_smem: DMMA tile updates, 2.5 TF/s at
@@ -2715,19 +2730,19 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
     const char *e = getenv("WRMG_NS_FACTOR_REG");
     return !(e && e[0] == '1');
   }();
-  if (!force_smem && q == 0 && m <= 64) {
+  if (!force_smem && nwin == N && q == 0 && m <= 64) {
     k_ns_factor_row<1, 64, 64><<<grid, 64, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos,
                                                    pvv);
     ++g_launches;
     return;
   }
-  if (!force_smem && q == 1 && m <= 80) {
+  if (!force_smem && nwin == N && q == 1 && m <= 80) {
     k_ns_factor_row<2, 80, 96><<<grid, 96, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos,
                                                    pvv);
     ++g_launches;
     return;
   }
-  if (!force_smem && m <= 80) {  // register-tiled Gauss-Jordan (4 x 8 tiles, 20 x 10 threads)
+  if (!force_smem && nwin == N && m <= 80) {  // register-tiled Gauss-Jordan (4 x 8 tiles, 20 x 10 threads)
     by_nq(q + 1, [&](auto NQc) {
       constexpr int NQ = decltype(NQc)::value;
       k_ns_factor_reg<NQ, 4, 8, 20, 10><<<grid, 256, 0, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out,
@@ -2766,7 +2781,7 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
       const size_t smr = pad + std::max(ns_factor_rt_smem<5>(m, mp), std::max(ns_factor_rt_smem<10>(m, mp),
                                                                              ns_factor_rt_smem<11>(m, mp)));
       smem_optin((const void *)kern, (int)smr);
-      kern<<<grid, thr, smr, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos, pvv);
+      kern<<<grid, thr, smr, s>>>(mp, N, mstride, pnodes, A.val, A.val2, conv, tm, out, info, ppos, pvv, n0, nwin);
       ++g_launches;
     };
     const int nt = (m + 7) / 8;
@@ -2784,7 +2799,7 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
       return e && e[0] == '1';
     }();
     const size_t perw = ns_factor_warp_doubles(m, mp) * sizeof(double);
-    if (warp_blocks && wp && m <= 96 && perw <= 56 * 1024) {
+    if (warp_blocks && nwin == N && wp && m <= 96 && perw <= 56 * 1024) {
       const int wpb = (int)std::min<size_t>(4, (220 * 1024) / perw);
       const int64_t nblk = npatch * N;
       const int grid = (int)std::min<int64_t>((nblk + wpb - 1) / wpb, (int64_t)8 * num_sms());
@@ -2801,39 +2816,41 @@ void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const De
     } else if (wp && la == 2 && m <= 96) {
       smem_optin((const void *)k_ns_factor<NQ, 128, 3, 2>, (int)sml);
       k_ns_factor<NQ, 128, 3, 2><<<grid, 128, sml, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
-                                                        2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+                                                        2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     } else if (wp && la == 2 && m <= 192) {
       smem_optin((const void *)k_ns_factor<NQ, 256, 6, 2>, (int)sml);
       k_ns_factor<NQ, 256, 6, 2><<<grid, 256, sml, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
-                                                        2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+                                                        2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     } else if (wp && la == 1 && m <= 96) {
       smem_optin((const void *)k_ns_factor<NQ, 128, 3, 1>, (int)sm);
       k_ns_factor<NQ, 128, 3, 1><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
-                                                       2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+                                                       2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     } else if (wp && la == 1 && m <= 192) {
       smem_optin((const void *)k_ns_factor<NQ, 256, 6, 1>, (int)sm);
       k_ns_factor<NQ, 256, 6, 1><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2,
-                                                       2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv);
+                                                       2 * g.Lu, vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     } else if (wp && m <= 96) {
       smem_optin((const void *)k_ns_factor<NQ, 128, 3>, (int)sm);
       k_ns_factor<NQ, 128, 3><<<grid, 128, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
-                                                    vvptr, conv, tm, out, info, ppos, pvv);
+                                                    vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     } else if (wp && m <= 192) {
       smem_optin((const void *)k_ns_factor<NQ, 256, 6>, (int)sm);
       k_ns_factor<NQ, 256, 6><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
-                                                    vvptr, conv, tm, out, info, ppos, pvv);
+                                                    vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     } else {
       smem_optin((const void *)k_ns_factor<NQ, 256, 0>, (int)sm);
       k_ns_factor<NQ, 256, 0><<<grid, 256, sm, s>>>(mp, N, mstride, pnodes, A.rowptr, A.col, A.val, A.val2, 2 * g.Lu,
-                                                    vvptr, conv, tm, out, info, ppos, pvv);
+                                                    vvptr, conv, tm, out, info, ppos, pvv, n0, nwin);
     }
   });
   ++g_launches;
 }
 
 void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
-                     const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s) {
+                     const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s,
+                     int n0, int nwin, double *xs) {
   const int m = (q + 1) * mp;
+  if (nwin <= 0) nwin = N;
   // m <= 256 (one thread per patch row) is enforced by setup_ns
   const bool staged = ns_sweep_smem(m, mp, mstride, true) <= 200 * 1024;
   const size_t sm = ns_sweep_smem(m, mp, mstride, staged);
@@ -2851,7 +2868,8 @@ void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, cons
       constexpr int NQ = decltype(NQc)::value;
       smem_optin((const void *)k_ns_sweep_chunked<NQ>, (int)smc);
       k_ns_sweep_chunked<NQ><<<(unsigned)npatch, 256, smc, s>>>(mp, N, mstride, CW, R, pnodes, wnode, A.rowptr,
-                                                                A.col, A.val, Dinv, r, u, omega);
+                                                                A.col, A.val, Dinv, r, u, omega, n0, nwin,
+                                                                xs);
     });
     ++g_launches;
     return;
@@ -2861,11 +2879,11 @@ void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, cons
     if (staged) {
       smem_optin((const void *)k_ns_sweep<NQ, true>, (int)sm);
       k_ns_sweep<NQ, true><<<(unsigned)npatch, 256, sm, s>>>(mp, N, mstride, pnodes, wnode, A.rowptr, A.col, A.val,
-                                                             Dinv, r, u, omega);
+                                                             Dinv, r, u, omega, n0, nwin, xs);
     } else {
       smem_optin((const void *)k_ns_sweep<NQ, false>, (int)sm);
       k_ns_sweep<NQ, false><<<(unsigned)npatch, 256, sm, s>>>(mp, N, mstride, pnodes, wnode, A.rowptr, A.col, A.val,
-                                                              Dinv, r, u, omega);
+                                                              Dinv, r, u, omega, n0, nwin, xs);
     }
   });
   ++g_launches;

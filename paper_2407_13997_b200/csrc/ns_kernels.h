@@ -38,11 +38,13 @@ void launch_ns_residual(const NSGeom &g, int q, int N, const Temporal &T, const 
                         cudaStream_t s);
 void launch_ns_factor(const NSGeom &g, int q, int N, const Temporal &T, const DevCSR &A, const int32_t *vvptr,
                       const double *conv, const int32_t *pnodes, int64_t npatch, int mp, int64_t mstride, double *out,
-                      int32_t *info, const int32_t *ppos, const int32_t *pvv, cudaStream_t s);
+                      int32_t *info, const int32_t *ppos, const int32_t *pvv, cudaStream_t s, int n0 = 0,
+                      int nwin = 0);
 void launch_ns_patch_pos(const NSGeom &g, const DevCSR &A, const int32_t *vvptr, const int32_t *pnodes, int64_t npatch,
                          int mp, int32_t *ppos, int32_t *pvv, cudaStream_t s);
 void launch_ns_sweep(int q, int N, int mp, int64_t npatch, int64_t mstride, const int32_t *pnodes, const double *wnode,
-                     const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s);
+                     const DevCSR &A, const double *Dinv, const double *r, double *u, double omega, cudaStream_t s,
+                     int n0 = 0, int nwin = 0, double *xs = nullptr);
 void launch_ns_project(double *P, int64_t nrow, int64_t NT, double *scratch, cudaStream_t s);
 // Strip form of the projection: column sums over the owned lattice columns (scratch >=
 // (Ly + 1) NT), then, from the all-gathered per-rank sums, P -= sum / gnrow.
