@@ -357,6 +357,10 @@ __device__ __forceinline__ double block_entry(const int32_t *__restrict__ rowptr
 // idx[c] = the column of A holding column c of the inverse.  Returns 0 or 1 + the
 // first column with |pivot| < tol.
 constexpr int GJB = 8;
+// X: GJB x m (or, gj_invert_smem_lr, the pivot rows in B-fragment order: 64 per tile column)
+__host__ __device__ constexpr size_t ns_factor_xdoubles(int m) {
+  return (size_t)GJB * m > (size_t)64 * ((m + 7) / 8) ? (size_t)GJB * m : (size_t)64 * ((m + 7) / 8);
+}
 // doubles of shared memory per block in k_ns_factor_warp: A, X, and the int arrays (piv, idx, nodes)
 __host__ __device__ constexpr size_t ns_factor_warp_doubles(int m, int mp) {
   return (size_t)m * m + (size_t)GJB * m + ((size_t)(2 * m + mp) + 1) / 2 + 2;
@@ -957,6 +961,61 @@ __device__ __forceinline__ void gj_lr_tile_update(double *A, const double *X, co
   }
 }
 
+// Column-strip form of gj_lr_tile_update (round 2): a warp takes whole tile columns J
+// (mode 1, the single look-ahead column: its row tiles split across the warps), so the
+// B fragments (the pivot rows, kept in fragment order XF[J][h][lane]) are loaded once per
+// column; C moves as one 16-byte access per lane (m even: conflict-free, row stride m / 2
+// 16-byte words); the rows that pivoted in this panel are masked by the per-lane-row bit
+// masks pm[lr] (bit I: row 8 I + lr).  Reads past row m stay inside the buffer (A is
+// followed by >= 8 m doubles of X) and are discarded; only stores are predicated.
+template <bool EVEN>
+__device__ __forceinline__ void gj_lr_strip_update(double *A, const double *XF, const unsigned *pm, int m, int k0,
+                                                   int nb, int mode, int wslot, int nws, int lane) {
+  const int nt8 = (m + 7) / 8, pt = k0 / 8;
+  const int ncol = mode == 0 ? nt8 - 1 : (mode == 1 ? 1 : nt8 - 2);
+  const int lr = lane >> 2, lc = lane & 3;
+  const unsigned pmk = pm[lr];
+  const bool ua0 = lc < nb, ua1 = 4 + lc < nb;
+  const int cstep = mode == 1 ? 1 : nws, istep = mode == 1 ? nws : 1;
+  for (int ci = mode == 1 ? 0 : wslot; ci < ncol; ci += cstep) {
+    const int J = mode == 1 ? pt + 1 : (ci < pt ? ci : ci + (mode == 0 ? 1 : 2));
+    const double b0 = XF[(J * 2) * 32 + lane], b1 = XF[(J * 2 + 1) * 32 + lane];
+    const int C0 = J * 8 + 2 * lc;
+    const bool cok = C0 < m, cok1 = C0 + 1 < m;
+    const double *ap = A + lr * m + k0 + lc;
+    double *cp = A + lr * m + C0;
+#pragma unroll 3
+    for (int I = mode == 1 ? wslot : 0; I < nt8; I += istep) {
+      const int off = I * 8 * m;
+      double a0 = ap[off], a1 = ap[off + 4];
+      a0 = ua0 ? a0 : 0.0;
+      a1 = ua1 ? a1 : 0.0;
+      double c0, c1;
+      if (EVEN) {
+        const double2 v = *reinterpret_cast<const double2 *>(cp + off);
+        c0 = v.x;
+        c1 = v.y;
+      } else {
+        c0 = cp[off];
+        c1 = cp[off + 1];
+      }
+      const bool z = (pmk >> I) & 1u;
+      c0 = z ? 0.0 : c0;
+      c1 = z ? 0.0 : c1;
+      dmma_ns(c0, c1, a0, b0);
+      dmma_ns(c0, c1, a1, b1);
+      if (I * 8 + lr < m) {
+        if (EVEN) {
+          if (cok) *reinterpret_cast<double2 *>(cp + off) = make_double2(c0, c1);
+        } else {
+          if (cok) cp[off] = c0;
+          if (cok1) cp[off + 1] = c1;
+        }
+      }
+    }
+  }
+}
+
 // On return rowmap[c] = the physical row of A holding row c of (P A)^{-1} and idx the
 // column permutation as in gj_invert_smem: D^{-1}[rho][sig] = A[rowmap[rho]][idx[sig]].
 // Shared scratch: piv, idx, rowmap, tmp (m ints each), used_in (m bytes).
@@ -971,22 +1030,39 @@ __device__ int gj_invert_smem_lr(double *A, int m, double tol, double *X, int *p
   int *prow_of = rowmap;  // the pivot row of every column during the elimination
   if (wid == 0) gj_lr_panel<RPL>(A, m, 0, min(GJB, m), tol, prow_of, used_in, &s_info, lane);
   __syncthreads();
+  __shared__ unsigned s_pm[8];
+  const bool even = (m & 1) == 0;
+  const int nt8 = (m + 7) / 8;
   for (int k0 = 0; k0 < m; k0 += GJB) {
     const int nb = min(GJB, m - k0), k1 = k0 + nb;
-    for (int j = tid; j < m; j += nth) {  // X = the panel's pivot rows (other columns)
+    // XF = the panel's pivot rows (other columns) in B-fragment order [J][h][lane]
+    for (int e = tid; e < nt8 * 64; e += nth) {
+      const int J = e >> 6, h = (e >> 5) & 1, ln = e & 31, t = 4 * h + (ln & 3), j = J * 8 + (ln >> 2);
       const bool inp = j >= k0 && j < k1;
-      for (int t = 0; t < nb; ++t) X[t * m + j] = inp ? 0.0 : A[prow_of[k0 + t] * m + j];
+      X[e] = (t < nb && j < m && !inp) ? A[prow_of[k0 + t] * m + j] : 0.0;
+    }
+    if (tid < 8) {
+      unsigned mk = 0;
+      for (int t = 0; t < nb; ++t) {
+        const int r = prow_of[k0 + t];
+        if ((r & 7) == tid) mk |= 1u << (r >> 3);
+      }
+      s_pm[tid] = mk;
     }
     __syncthreads();
     if (k1 < m) {
-      gj_lr_tile_update(A, X, used_in, m, k0, nb, 1, wid, nw, lane);
+      if (even) gj_lr_strip_update<true>(A, X, s_pm, m, k0, nb, 1, wid, nw, lane);
+      else gj_lr_strip_update<false>(A, X, s_pm, m, k0, nb, 1, wid, nw, lane);
       __syncthreads();
       if (wid == 0)
         gj_lr_panel<RPL>(A, m, k1, min(GJB, m - k1), tol, prow_of, used_in, &s_info, lane);
+      else if (even)
+        gj_lr_strip_update<true>(A, X, s_pm, m, k0, nb, 2, wid - 1, nw - 1, lane);
       else
-        gj_lr_tile_update(A, X, used_in, m, k0, nb, 2, wid - 1, nw - 1, lane);
+        gj_lr_strip_update<false>(A, X, s_pm, m, k0, nb, 2, wid - 1, nw - 1, lane);
     } else {
-      gj_lr_tile_update(A, X, used_in, m, k0, nb, 0, wid, nw, lane);
+      if (even) gj_lr_strip_update<true>(A, X, s_pm, m, k0, nb, 0, wid, nw, lane);
+      else gj_lr_strip_update<false>(A, X, s_pm, m, k0, nb, 0, wid, nw, lane);
     }
     __syncthreads();
   }
@@ -1314,8 +1390,8 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
                                                    int n0, int nwin) {
   extern __shared__ __align__(16) double smem[];
   const int m = NQ * mp;
-  double *A = smem, *X = smem + (int64_t)m * m;  // X: GJB x m
-  int *piv = (int *)(X + GJB * m);
+  double *A = smem, *X = smem + (int64_t)m * m;  // X: ns_factor_xdoubles(m)
+  int *piv = (int *)(X + ns_factor_xdoubles(m));
   int *idx = piv + m;
   int *nodes = idx + m;
   int *rowmap = nodes + mp, *tmp = rowmap + m;  // LA == 2 only (ns_factor_smem_lr)
@@ -2660,7 +2736,7 @@ void launch_axpy(int64_t n, double a, const double *x, double *y, cudaStream_t s
 }
 
 size_t ns_factor_smem(int m, int mp) {
-  return ((size_t)m * m + (size_t)GJB * m) * sizeof(double) + (size_t)(2 * m + mp) * sizeof(int) + 16;
+  return ((size_t)m * m + ns_factor_xdoubles(m)) * sizeof(double) + (size_t)(2 * m + mp) * sizeof(int) + 16;
 }
 
 size_t ns_sweep_smem(int m, int mp, int64_t mstride, bool staged) {
