@@ -755,9 +755,13 @@ def run_gpu(args, ws, rank, local):
     # right-hand sides held in pinned host memory, each uploaded, solved and downloaded by the
     # library (the upload of rhs i+1 and the download of x i-1 on its copy stream during solve i);
     # the timed region spans every copy.
-    e2e_steps = max(2, args.steps)
-    hb = [b.detach().cpu().pin_memory() for _ in range(e2e_steps)]
-    hx = [torch.empty_like(hb[0]).pin_memory() for _ in range(e2e_steps)]
+    # a serving loop of max(20, steps) solves over 4 pinned RHS / solution buffers used in turn (the
+    # pipeline's fill and drain -- one unhidden upload and download -- amortised over the loop)
+    e2e_steps = max(20, args.steps)
+    hb4 = [b.detach().cpu().pin_memory() for _ in range(4)]
+    hx4 = [torch.empty_like(hb4[0]).pin_memory() for _ in range(4)]
+    hb = [hb4[i % 4] for i in range(e2e_steps)]
+    hx = [hx4[i % 4] for i in range(e2e_steps)]
     barrier(ws)
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
