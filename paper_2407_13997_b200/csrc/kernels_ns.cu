@@ -843,15 +843,29 @@ __device__ int gj_invert_smem_la(double *A, int m, double tol, double *X, int *p
 // order of the result is restored once at the end by replaying the equivalent
 // interchanges (the inverse of P A, then the column permutation as before).  No
 // interchange pass over the matrix per panel, no displaced-row shuffles in the panel.
+// reciprocal: rcp.approx + a cubic and a Newton step (correct to the last bit or two; 0 -> 0)
+__device__ __forceinline__ double rt_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  e = fma(e, e, e);  // r (1 + e + e^2): cubic step
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  return x != 0.0 ? r : 0.0;
+}
+
 template <int RPL>
 __device__ __forceinline__ void gj_lr_panel(double *A, int m, int k0, int nb, double tol, int *prow_of,
-                                            int8_t *used_in, int *s_info, int lane) {
-  double P[RPL][GJB];
-  bool used[RPL];
+                                            int8_t *used_in, int *s_info, double *bc, int lane) {
+  // the pivot search and broadcast of rt_panel (redux.sync over a high-word key, speculative
+  // reciprocals, pivot row through shared memory bc[9]; ties and near-ties to the lowest row)
+  double P[RPL][8];
+  unsigned elig = 0;
 #pragma unroll
   for (int s = 0; s < RPL; ++s) {
     const int r = lane + 32 * s;
-    used[s] = r >= m || used_in[r] >= 0;
+    if (r < m && used_in[r] < 0) elig |= 1u << s;
 #pragma unroll
     for (int t = 0; t < GJB; ++t) P[s][t] = (r < m && t < nb) ? A[r * m + k0 + t] : 0.0;
   }
@@ -861,53 +875,57 @@ __device__ __forceinline__ void gj_lr_panel(double *A, int m, int k0, int nb, do
   for (int tc = 0; tc < GJB; ++tc) {
     if (tc >= nb) break;
     const int c = k0 + tc;
-    double bv = -1.0;
-    int bi = m;
+    unsigned key = 0;
+    double rc[RPL];
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {
-      const double v = fabs(P[s][tc]);
-      if (!used[s] && v > bv) {
-        bv = v;
-        bi = lane + 32 * s;
-      }
+      const double v = P[s][tc];
+      rc[s] = rt_rcp(v);
+      const unsigned k = ((elig >> s) & 1u)
+                             ? (((unsigned)__double2hiint(v) & 0x7FFFFF00u) | (unsigned)(255 - (lane + 32 * s)))
+                             : 0u;
+      key = max(key, k);
     }
-    double mv = bv;
+    const unsigned gk = __reduce_max_sync(0xffffffffu, key);
+    const int bi = 255 - (int)(gk & 255u), lp = bi & 31, sp = bi >> 5;
+    const bool isl = lane == lp;
+    if (isl) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mv = fmax(mv, __shfl_xor_sync(0xffffffffu, mv, o));
-    bi = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == mv ? bi : m));
-    if (!(mv >= tol) && info == 0) info = c + 1;
-    const int sp = bi >> 5, lp = bi & 31;
-    double prow[GJB];
+      for (int s = 0; s < RPL; ++s)
+        if (s == sp) {
 #pragma unroll
-    for (int t = 0; t < GJB; ++t) {
-      double vp = 0.0;
-#pragma unroll
-      for (int s = 0; s < RPL; ++s) vp = (s == sp) ? P[s][t] : vp;
-      prow[t] = __shfl_sync(0xffffffffu, vp, lp);
+          for (int t = 0; t < GJB; ++t) bc[t] = P[s][t];
+          bc[8] = rc[s];
+        }
     }
-    const double pv = prow[tc];
-    const double pinv = pv != 0.0 ? 1.0 / pv : 0.0;
-    double newc[GJB];
+    __syncwarp();
+    double prow_v[GJB];
 #pragma unroll
-    for (int t = 0; t < GJB; ++t) newc[t] = (t == tc) ? pinv : prow[t] * pinv;
+    for (int t = 0; t < GJB; ++t) prow_v[t] = bc[t];
+    const double pinv = bc[8];
+    __syncwarp();
+    if (!(fabs(prow_v[tc]) >= tol) && info == 0) info = c + 1;
 #pragma unroll
     for (int s = 0; s < RPL; ++s) {
-      const int r = lane + 32 * s;
-      if (r == bi) {
+      const double frp = P[s][tc] * pinv;
 #pragma unroll
-        for (int t = 0; t < GJB; ++t) P[s][t] = newc[t];
-        used[s] = true;
-      } else {
-        const double fr = P[s][tc];
-#pragma unroll
-        for (int t = 0; t < GJB; ++t)
-          if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
-        P[s][tc] = -fr * pinv;
-      }
+      for (int t = 0; t < GJB; ++t)
+        if (t != tc) P[s][t] = fma(-frp, prow_v[t], P[s][t]);
+      P[s][tc] = -frp;
     }
+    double keep[GJB];
+#pragma unroll
+    for (int t = 0; t < GJB; ++t) keep[t] = (t == tc) ? pinv : prow_v[t] * pinv;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s)
+      if (s == sp) {
+#pragma unroll
+        for (int t = 0; t < GJB; ++t) P[s][t] = isl ? keep[t] : P[s][t];
+      }
+    if (isl) elig &= ~(1u << sp);
     if (lane == 0) {
-      prow_of[c] = bi < m ? bi : c;
-      if (bi < m) used_in[bi] = (int8_t)(pt & 127);
+      prow_of[c] = bi;
+      used_in[bi] = (int8_t)(pt & 127);
     }
   }
 #pragma unroll
@@ -1028,7 +1046,8 @@ __device__ int gj_invert_smem_lr(double *A, int m, double tol, double *X, int *p
   for (int r = tid; r < m; r += nth) used_in[r] = -1;
   __syncthreads();
   int *prow_of = rowmap;  // the pivot row of every column during the elimination
-  if (wid == 0) gj_lr_panel<RPL>(A, m, 0, min(GJB, m), tol, prow_of, used_in, &s_info, lane);
+  __shared__ double s_bc[16];
+  if (wid == 0) gj_lr_panel<RPL>(A, m, 0, min(GJB, m), tol, prow_of, used_in, &s_info, s_bc, lane);
   __syncthreads();
   __shared__ unsigned s_pm[8];
   const bool even = (m & 1) == 0;
@@ -1055,7 +1074,7 @@ __device__ int gj_invert_smem_lr(double *A, int m, double tol, double *X, int *p
       else gj_lr_strip_update<false>(A, X, s_pm, m, k0, nb, 1, wid, nw, lane);
       __syncthreads();
       if (wid == 0)
-        gj_lr_panel<RPL>(A, m, k1, min(GJB, m - k1), tol, prow_of, used_in, &s_info, lane);
+        gj_lr_panel<RPL>(A, m, k1, min(GJB, m - k1), tol, prow_of, used_in, &s_info, s_bc, lane);
       else if (even)
         gj_lr_strip_update<true>(A, X, s_pm, m, k0, nb, 2, wid - 1, nw - 1, lane);
       else
@@ -1447,25 +1466,17 @@ __global__ void __launch_bounds__(NTH, (LA && NTH == 128) ? 4 : 1) k_ns_factor(i
 // with q the inverse of prow (DESIGN R10).
 constexpr int RT_PS = 9;  // row stride of the panel hand-over buffer (odd: conflict-free row reads)
 
-__device__ __forceinline__ double rt_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  e = fma(e, e, e);  // r (1 + e + e^2): cubic step
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  return x != 0.0 ? r : 0.0;
-}
 
 // Panel K (columns k0 .. k0+nb) from Pin (M x RT_PS, current values) -> Pf (A-fragment
 // order [I][h][lane]) and the pivot records prow / used / tpos; one warp.  Row r is
-// slot s = r / 32 of lane r % 32; the pivot's slot is warp-uniform (from the redux), so
-// its broadcast is one uniform branch; every lane's reciprocals are computed
-// speculatively while the redux is in flight.
+// slot s = r / 32 of lane r % 32; the pivot is chosen by one redux.sync, every lane's
+// reciprocals computed speculatively while it is in flight, and the pivot row and its
+// reciprocal reach all lanes through shared memory (bc: 9 doubles; tools/panel_bench.cu:
+// 378 cycles per column standalone against 442 with shuffles and an F2F key).
 template <int M>
 __device__ __forceinline__ void rt_panel(const double *Pin, double *Pf, int m, int K, int nb, double tol, int *prow,
-                                         int8_t *used, int8_t *tpos, int *s_info, unsigned *pmask, int lane) {
+                                         int8_t *used, int8_t *tpos, int *s_info, unsigned *pmask, double *bc,
+                                         int lane) {
   constexpr int RPL = (M + 31) / 32;
   const int k0 = 8 * K;
   double P[RPL][8];
@@ -1481,6 +1492,7 @@ __device__ __forceinline__ void rt_panel(const double *Pin, double *Pf, int m, i
 #pragma unroll
   for (int tc = 0; tc < 8; ++tc) {
     if (tc >= nb) break;
+    // key = high word of |a| (13 mantissa bits) | (255 - row); every lane's reciprocals speculatively
     unsigned key = 0;
     double rc[RPL];
 #pragma unroll
@@ -1488,41 +1500,48 @@ __device__ __forceinline__ void rt_panel(const double *Pin, double *Pf, int m, i
       const double v = P[s][tc];
       rc[s] = rt_rcp(v);
       const unsigned k = ((elig >> s) & 1u)
-                             ? ((__float_as_uint((float)fabs(v)) & 0xFFFFFF00u) | (unsigned)(255 - (lane + 32 * s)))
+                             ? (((unsigned)__double2hiint(v) & 0x7FFFFF80u) | (unsigned)(255 - (lane + 32 * s)))
                              : 0u;
       key = max(key, k);
     }
     const unsigned gk = __reduce_max_sync(0xffffffffu, key);
     const int bi = 255 - (int)(gk & 255u), lp = bi & 31, sp = bi >> 5;
-    double prow_v[8], pinv = 0.0;
-#pragma unroll
-    for (int s = 0; s < RPL; ++s)
-      if (s == sp) {
-#pragma unroll
-        for (int t = 0; t < 8; ++t) prow_v[t] = __shfl_sync(0xffffffffu, P[s][t], lp);
-        pinv = __shfl_sync(0xffffffffu, rc[s], lp);
-      }
-    const double pv = prow_v[tc];
-    double newc[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) newc[t] = (t == tc) ? pinv : prow_v[t] * pinv;
-#pragma unroll
-    for (int s = 0; s < RPL; ++s) {
-      const double fr = P[s][tc];
-#pragma unroll
-      for (int t = 0; t < 8; ++t)
-        if (t != tc) P[s][t] = fma(-fr, newc[t], P[s][t]);
-      P[s][tc] = -fr * pinv;
-    }
-    if (lane == lp) {
+    const bool isl = lane == lp;
+    // the pivot row and its reciprocal through shared memory (one store set, broadcast loads)
+    if (isl) {
 #pragma unroll
       for (int s = 0; s < RPL; ++s)
         if (s == sp) {
 #pragma unroll
-          for (int t = 0; t < 8; ++t) P[s][t] = newc[t];
+          for (int t = 0; t < 8; ++t) bc[t] = P[s][t];
+          bc[8] = rc[s];
         }
-      elig &= ~(1u << sp);
     }
+    __syncwarp();
+    double prow_v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) prow_v[t] = bc[t];
+    const double pinv = bc[8];
+    __syncwarp();
+    const double pv = prow_v[tc];
+#pragma unroll
+    for (int s = 0; s < RPL; ++s) {  // rows -= (a_r,c / pivot) x pivot row
+      const double frp = P[s][tc] * pinv;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t != tc) P[s][t] = fma(-frp, prow_v[t], P[s][t]);
+      P[s][tc] = -frp;
+    }
+    double keep[8];  // the pivot row: scaled by 1 / pivot, its column entry = 1 / pivot
+#pragma unroll
+    for (int t = 0; t < 8; ++t) keep[t] = (t == tc) ? pinv : prow_v[t] * pinv;
+#pragma unroll
+    for (int s = 0; s < RPL; ++s)
+      if (s == sp) {  // warp-uniform
+#pragma unroll
+        for (int t = 0; t < 8; ++t) P[s][t] = isl ? keep[t] : P[s][t];
+      }
+    if (isl) elig &= ~(1u << sp);
     if (lane == tc) mybi = bi;
     if (!(fabs(pv) >= tol) && sing == 0) sing = k0 + tc + 1;
   }
@@ -1575,8 +1594,9 @@ __device__ __forceinline__ void rt_update(double (&acc0)[NT][2], double (&acc1)[
 
 template <int NT>
 __host__ __device__ constexpr size_t ns_factor_rt_buf_doubles(int m) {
-  // max(assembly / output matrix m x m, panel hand-over M x RT_PS + two Pf (8 M each) + X (8 M))
-  return (size_t)m * m > (size_t)(RT_PS + 24) * 8 * NT ? (size_t)m * m : (size_t)(RT_PS + 24) * 8 * NT;
+  // max(assembly / output matrix m x m, panel hand-over M x RT_PS + two Pf (8 M each) + X (8 M)
+  // + 16 doubles of pivot-row broadcast scratch)
+  return (size_t)m * m > (size_t)(RT_PS + 24) * 8 * NT + 16 ? (size_t)m * m : (size_t)(RT_PS + 24) * 8 * NT + 16;
 }
 template <int NT>
 __host__ __device__ constexpr size_t ns_factor_rt_smem(int m, int mp) {
@@ -1758,7 +1778,7 @@ __global__ void __launch_bounds__(32 * ((NT + 1) / 2 + 1), MINB)
     for (int i = 0; i <= W; ++i) tol = fmax(tol, s_red[i]);
     tol *= 1e-14;
     asm volatile("bar.sync 1, %0;" ::"r"(64) : "memory");
-    rt_panel<M>(Pin, Pfb, m, 0, min(8, m), tol, prow, used, tpos, &s_info, s_pmask, lane);
+    rt_panel<M>(Pin, Pfb, m, 0, min(8, m), tol, prow, used, tpos, &s_info, s_pmask, X + 8 * M, lane);
     __syncthreads();  // (2)
     for (int K = 0; K < npan; ++K) {
       if (K + 1 < npan) {
@@ -1767,7 +1787,7 @@ __global__ void __launch_bounds__(32 * ((NT + 1) / 2 + 1), MINB)
         RT_ACC(8, t_w)
         RT_T0(t_f)
         rt_panel<M>(Pin, Pfb + ((K + 1) & 1) * 8 * M, m, K + 1, min(8, m - 8 * (K + 1)), tol, prow, used, tpos,
-                    &s_info, s_pmask, lane);
+                    &s_info, s_pmask, X + 8 * M, lane);
         RT_ACC(9, t_f)
       }
       RT_T0(t_g)
