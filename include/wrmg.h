@@ -139,8 +139,8 @@ wrmg_status wrmg_layout(const wrmg_ctx *ctx, wrmg_layout_t *out);
  * `state` (device vector, NULL for the linear heat operator).  Heat: recomputes
  * H1/H4/H5 on the device.  Synchronises; WRMG_E_SINGULAR on a failed pivot.
  * Navier-Stokes: the Vanka inverses (m^2 doubles per (patch, slab)) of a level
- * whose store does not fit the device (85 % of the free memory at setup less a
- * FGMRES(30) basis) are kept for a window of W slabs only: this call factors every
+ * whose store does not fit the device (92 % of the free memory at setup less
+ * 8 GB) are kept for a window of W slabs only: this call factors every
  * window once for the singularity check, and every sweep of that level
  * re-factors each window before sweeping it (PAPER.md:390 fixes the patch solve,
  * not its storage; DESIGN.md 1b "slab windows").  Environment: WRMG_NS_WINDOW=W

@@ -896,9 +896,10 @@ void make_strip_comm(wrmg_ctx *c) {
 // Hierarchy of Taylor-Hood levels (problem == WRMG_NAVIER_STOKES).
 // Stored Vanka inverses (m^2 doubles per (patch, slab)): levels whose store does not fit
 // the memory budget keep a window of W slabs only and recompute it inside every sweep
-// ("slab windows"): the budget is 85 % of the free device memory less the
-// FGMRES(30) basis a later solve allocates; while the stores exceed it, the level with the
-// largest store halves its window.  WRMG_NS_WINDOW=<W> windows every stored level at W
+// ("slab windows"): the budget is 92 % of the free device memory less 8 GB
+// (a later FGMRES(30) allocates 62 more vectors; lower the budget with WRMG_NS_STORE_GB
+// when they must fit beside a large store); while the stores exceed it, the level with
+// the largest store halves its window.  WRMG_NS_WINDOW=<W> windows every stored level at W
 // slabs (tests), WRMG_NS_STORE_GB=<GB> sets the budget.
 void ns_slab_windows(wrmg_ctx *c) {
   std::vector<Level *> ls;
@@ -913,7 +914,7 @@ void ns_slab_windows(wrmg_ctx *c) {
   } else {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
-    double budget = 0.85 * (double)fr - 62.0 * 8.0 * (double)c->lv.back().nnode * (double)c->nt;
+    double budget = 0.92 * (double)fr - 8e9;
     if (const char *e = getenv("WRMG_NS_STORE_GB")) budget = atof(e) * 1e9;
     auto total = [&] {
       double t = 0.0;
