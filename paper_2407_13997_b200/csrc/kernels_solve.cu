@@ -316,12 +316,69 @@ __global__ void __launch_bounds__(256) k_spmv_nt_tp(int64_t nrow, int64_t NT2, c
   }
 }
 
+// Small levels (few (row, time-pair) items): the S warps of a CTA share 32 consecutive items
+// of one row (NT2 % 32 == 0) and split the row's entries (warp w: entries w, w + S, ...); the
+// partial sums meet in shared memory.  Keeps every SM busy where one thread per item would fill
+// a fraction of them (C2: restriction to levels 0 / 1 25 -> a few us).
+template <bool ACC, int S>
+__global__ void __launch_bounds__(32 * S) k_spmv_nt_split(int64_t nrow, int64_t NT2, const int32_t *__restrict__ rp,
+                                                           const int32_t *__restrict__ ci,
+                                                           const double *__restrict__ v,
+                                                           const double2 *__restrict__ x, double2 *__restrict__ y) {
+  __shared__ double2 part[S][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t idx = blockIdx.x * 32ll + lane;  // the 32 items of a CTA lie in one row
+  const int64_t i = (blockIdx.x * 32ll) / NT2, t = idx - i * NT2;
+  const int e0 = __ldg(rp + i), e1 = __ldg(rp + i + 1);
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+  for (int e = e0 + w; e < e1; e += S) {
+    const double a = __ldg(v + e);
+    const double2 xv = __ldg(x + (int64_t)__ldg(ci + e) * NT2 + t);
+    acc.x = fma(a, xv.x, acc.x);
+    acc.y = fma(a, xv.y, acc.y);
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int k = 1; k < S; ++k) {
+      acc.x += part[k][lane].x;
+      acc.y += part[k][lane].y;
+    }
+    if (ACC) {
+      if (e0 == e1) return;
+      double2 o = y[idx];
+      o.x += acc.x;
+      o.y += acc.y;
+      y[idx] = o;
+    } else {
+      y[idx] = acc;
+    }
+  }
+}
+
 void spmv_nt(const DevCSR &A, int64_t NT, const double *x, double *y, bool acc, cudaStream_t s) {
   static const int tp = [] {  // WRMG_SPMV_TP=1: one time pair per thread (A/B)
     const char *e = getenv("WRMG_SPMV_TP");
     return e ? atoi(e) : 4;
   }();
-  if (NT % 2 == 0 && tp == 4 && (NT / 2) % 4 == 0) {
+  // launch shape by level size: four time pairs per thread only where the items still fill the
+  // GPU twice over, one pair per thread in between, entry-split CTAs on the small levels
+  const int64_t items = A.nrow * (NT / 2);
+  const int64_t fill = (int64_t)num_sms() * 2048;
+  if (NT % 2 == 0 && (NT / 2) % 32 == 0 && items < fill / 2 && tp != 1) {
+    const unsigned nb = (unsigned)(items / 32);
+    if (acc)
+      k_spmv_nt_split<true, 8><<<nb, 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val, (const double2 *)x,
+                                                   (double2 *)y);
+    else
+      k_spmv_nt_split<false, 8><<<nb, 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val, (const double2 *)x,
+                                                    (double2 *)y);
+    ++g_launches;
+    return;
+  }
+  if (NT % 2 == 0 && tp == 4 && (NT / 2) % 4 == 0 && items / 4 >= fill / 3) {
     const int64_t n = A.nrow * (NT / 8);
     if (acc)
       k_spmv_nt_tp<true, 4><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(A.nrow, NT / 2, A.rowptr, A.col, A.val,

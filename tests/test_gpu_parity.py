@@ -129,7 +129,10 @@ def test_C1_protocol():
     assert_parity(_host(u), u_ref, what="C1 V-cycle")
 
 
-@pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 5), (8, 3, 1, 35), (16, 2, 1, 3), (8, 2, 2, 4)])
+# (16, 3, 1, 32), (32, 3, 1, 64): 32 | N (q + 1) / 2 -- the entry-split (small levels) and
+# one-pair-per-thread launch shapes of the transfer SpMV
+@pytest.mark.parametrize("n,k,q,N", [(16, 1, 0, 5), (8, 3, 1, 35), (16, 2, 1, 3), (8, 2, 2, 4), (16, 3, 1, 32),
+                                     (32, 3, 1, 64)])
 def test_transfers(n, k, q, N):
     from oracle import multigrid, transfer
     H = multigrid.Hierarchy(n, n, 1.0 / n, k, q, N, 1.0 / N)
