@@ -727,6 +727,19 @@ def run_gpu(args, ws, rank, local):
                          "peak": fp64 if alu else hbm, "frac": (tfs / fp64) if alu else (gbs / hbm),
                          "share_of_kernel_time": st["ms"] / tot_ms if tot_ms else None})
     roof["top_kernels"] = roof_top
+    # the heat sweep's binding resource is the L2's FP64 atomic rate of its weighted additive
+    # scatter: one update per (patch DoF, time value), against the rate
+    # tools/atomic_probe.cu measured for contiguous lanes on this B200 (profiles/r02_atomic_probe.txt)
+    if args.scatter == "atomic" and ws == 1:
+        _, psz = w.wrmg_plan_patches(n, n, 1.0 / n, k)
+        upd = float(psz.sum()) * (q + 1) * N
+        sw = stats.get(("sweep", lay["nlevels"] - 1))
+        if sw and sw["launches"]:
+            t_l = sw["ms"] / sw["launches"] / 1e3
+            roof["sweep_l2_atomic"] = {"kernel": f"sweep@L{lay['nlevels'] - 1}", "bound": "l2_fp64_atomics",
+                                       "updates_per_launch": upd, "achieved": upd / t_l / 1e9, "peak": 320.3,
+                                       "unit": "G element-updates/s", "frac": upd / t_l / 1e9 / 320.3,
+                                       "peak_source": "measured: tools/atomic_probe.cu, contiguous red.global.add.f64"}
     per_kernel = {f"{a}@L{l}": {"launches": s["launches"], "ms": round(s["ms"], 4),
                                 "GBs": round(s["bytes"] / (s["ms"] / 1e3) / 1e9, 1) if s["ms"] > 0 else None,
                                 "TFs": round(s["flops"] / (s["ms"] / 1e3) / 1e12, 3) if s["ms"] > 0 else None}

@@ -26,6 +26,10 @@
  * (level, patch, slab) of the failing pivot (wrmg_last_error).  On error the
  * output buffers are unspecified.  Kernel-side failures are reported at the next
  * synchronising call.  No call falls back to a CPU implementation.
+ *
+ * Device vectors (every double * argument of the solver calls) must be 16-byte
+ * aligned -- cudaMalloc and torch allocations are; a view at an odd double offset
+ * is rejected with WRMG_E_INVALID (the kernels move 16-byte pairs and TMA boxes).
  */
 #ifndef WRMG_H
 #define WRMG_H
@@ -40,7 +44,7 @@ typedef struct wrmg_ctx wrmg_ctx; /* opaque; owned by the library, freed by wrmg
 
 typedef enum {
   WRMG_OK = 0,
-  WRMG_E_INVALID = 1,       /* bad argument (null pointer, size, R <= 0, ...) */
+  WRMG_E_INVALID = 1,       /* bad argument (null / misaligned pointer, size, R <= 0, ...) */
   WRMG_E_UNSUPPORTED = 2,   /* degree / problem / configuration not built */
   WRMG_E_OOM = 3,           /* device allocation failed */
   WRMG_E_SINGULAR = 4,      /* |pivot| < 1e-14 * max row norm in a patch or coarse block (R10) */

@@ -1569,6 +1569,14 @@ struct DevGuard {
 
 }  // namespace
 
+// Device vectors must be 16-byte aligned (the kernels move 16-byte pairs and TMA boxes;
+// cudaMalloc and torch allocations are): a view at an odd double offset is rejected.
+static bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+template <class... T>
+static bool al16(const void *p, T... rest) {
+  return al16(p) && al16(rest...);
+}
+
 extern "C" {
 
 wrmg_status wrmg_plan(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, wrmg_layout_t *out) {
@@ -2156,7 +2164,7 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
 }
 
 wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
-  if (!c) return WRMG_E_INVALID;
+  if (!c || (state && !al16(state))) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     if (c->ns) {
@@ -2172,7 +2180,7 @@ wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
 }
 
 wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
-  if (!c || !fhat || !b) return WRMG_E_INVALID;
+  if (!c || !fhat || !b || !al16(fhat, b)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     if (c->ns) {  // R6 (C3): b = drawn values on free rows, 0 on constrained rows, pressure mean-projected
@@ -2191,7 +2199,7 @@ wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
 }
 
 wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
-  if (!c || !u0 || !b) return WRMG_E_INVALID;
+  if (!c || !u0 || !b || !al16(u0, b)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     launch_rhs_initial(c->lv.back(), c->nq, c->nt, c->tm.phi0, u0, b, c->stream);
@@ -2203,7 +2211,7 @@ wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
 }
 
 wrmg_status wrmg_set_boundary_values(wrmg_ctx *c, const double *g) {
-  if (!c) return WRMG_E_INVALID;
+  if (!c || (g && !al16(g))) return WRMG_E_INVALID;
   if (!c->ns) {
     c->err = "wrmg_set_boundary_values: Navier-Stokes contexts only";
     return WRMG_E_UNSUPPORTED;
@@ -2232,7 +2240,7 @@ wrmg_status wrmg_cheb_lambda(const wrmg_ctx *c, int32_t level, double *lam) {
 }
 
 wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double *r, int32_t nonlinear) {
-  if (!c || !u || !b || !r) return WRMG_E_INVALID;
+  if (!c || !u || !b || !r || !al16(u, b, r)) return WRMG_E_INVALID;
   if (nonlinear && !c->ns) return WRMG_E_UNSUPPORTED;
   DevGuard dg_(c);
   try {
@@ -2252,7 +2260,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
 }
 
 wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
-  if (!c || !x || !y) return WRMG_E_INVALID;
+  if (!c || !x || !y || !al16(x, y)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(x));
@@ -2265,7 +2273,7 @@ wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
 }
 
 wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps, double omega) {
-  if (!c || !u || !b || nsweeps < 0) return WRMG_E_INVALID;
+  if (!c || !u || !b || nsweeps < 0 || !al16(u, b)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     const int l = (int)c->lv.size() - 1;
@@ -2288,7 +2296,7 @@ wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps
 }
 
 wrmg_status wrmg_vcycle(wrmg_ctx *c, const double *r, double *z) {
-  if (!c || !r || !z) return WRMG_E_INVALID;
+  if (!c || !r || !z || !al16(r, z)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     vcycle_level(c, (int)c->lv.size() - 1, r, z);
@@ -2306,7 +2314,7 @@ wrmg_status wrmg_level_size(const wrmg_ctx *c, int32_t level, int64_t *nnode) {
 }
 
 wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *rc) {
-  if (!c || !rf || !rc || level < 1 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  if (!c || !rf || !rc || level < 1 || level >= (int)c->lv.size() || !al16(rf, rc)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     launch_restrict(c->lv[level - 1], c->nt, rf, rc, c->stream);
@@ -2318,7 +2326,7 @@ wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *
 }
 
 wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, double *uf) {
-  if (!c || !ec || !uf || level < 1 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
+  if (!c || !ec || !uf || level < 1 || level >= (int)c->lv.size() || !al16(ec, uf)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     launch_prolong_add(c->lv[level - 1], c->nt, ec, uf, c->stream);
@@ -2331,7 +2339,7 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, doubl
 
 wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
                         double atol, int32_t *iters, double *relres) {
-  if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1) return WRMG_E_INVALID;
+  if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1 || !al16(b, x)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     cudaStream_t s = c->stream;
@@ -2540,7 +2548,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
 }
 
 wrmg_status wrmg_stationary(wrmg_ctx *c, const double *b, double *u, int32_t ncycles) {
-  if (!c || !b || !u || ncycles < 0) return WRMG_E_INVALID;
+  if (!c || !b || !u || ncycles < 0 || !al16(b, u)) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     const int top = (int)c->lv.size() - 1;
@@ -2739,6 +2747,7 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
     c->err = "wrmg_newton: the heat operator is linear";
     return WRMG_E_UNSUPPORTED;
   }
+  if (!al16(U) || (rhs && !al16(rhs))) return WRMG_E_INVALID;
   DevGuard dg_(c);
   try {
     cudaStream_t s = c->stream;

@@ -21,7 +21,7 @@ struct Ptrs {
 // MODE 1: w <- w - sum_k c_k V_k;  part[k] = sum_i V_k[i] w_new[i]
 // MODE 2: w <- w - sum_k c_k V_k;  part[0] = sum_i w_new[i]^2
 // MODE 3: w <- w + sgn sum_k c_k V_k  (MODEs 1, 2 subtract: sgn = -1)
-template <int NV, int MODE>
+template <int NV, int MODE, bool VEC = true>
 __global__ void __launch_bounds__(256) k_krylov(Ptrs V, int nv, double *__restrict__ w, const double *__restrict__ coef,
                                                 int64_t n, double *__restrict__ partials, int stride, double sgn) {
   double acc[NV];
@@ -31,27 +31,46 @@ __global__ void __launch_bounds__(256) k_krylov(Ptrs V, int nv, double *__restri
     acc[k] = 0.0;
     c[k] = (MODE != 0 && k < nv) ? sgn * coef[k] : 0.0;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double wi = w[i];
+  // element i (scalar tail) or the pair (2 i, 2 i + 1) of 16-byte loads: twice the bytes in
+  // flight per thread of the scalar form (the early Arnoldi steps stream only 1-3 vectors)
+  // VEC = false (a vector not 16-byte aligned): one element per iteration
+  const int64_t n2 = VEC ? n >> 1 : 0;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nit = VEC ? n2 + (n & 1) : n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nit; i += gstride) {
+    const bool pair = VEC && i < n2;
+    const int64_t is = VEC ? 2 * i : i;  // the scalar element
+    double2 wv = pair ? reinterpret_cast<const double2 *>(w)[i] : make_double2(w[is], 0.0);
     if (MODE != 0) {
-      double v[NV];
+      double2 v[NV];
 #pragma unroll
-      for (int k = 0; k < NV; ++k) v[k] = k < nv ? __ldg(V.p[k] + i) : 0.0;
-      double s = wi;
+      for (int k = 0; k < NV; ++k)
+        v[k] = k < nv ? (pair ? __ldg(reinterpret_cast<const double2 *>(V.p[k]) + i)
+                              : make_double2(__ldg(V.p[k] + is), 0.0))
+                      : make_double2(0.0, 0.0);
+      double2 sv = wv;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) s = fma(c[k], v[k], s);
-      wi = s;
-      w[i] = wi;
+      for (int k = 0; k < NV; ++k) {
+        sv.x = fma(c[k], v[k].x, sv.x);
+        sv.y = fma(c[k], v[k].y, sv.y);
+      }
+      wv = sv;
+      if (pair) reinterpret_cast<double2 *>(w)[i] = wv;
+      else w[is] = wv.x;
       if (MODE == 1) {
 #pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] = fma(v[k], wi, acc[k]);
+        for (int k = 0; k < NV; ++k) acc[k] = fma(v[k].y, wv.y, fma(v[k].x, wv.x, acc[k]));
       } else if (MODE == 2) {
-        acc[0] = fma(wi, wi, acc[0]);
+        acc[0] = fma(wv.y, wv.y, fma(wv.x, wv.x, acc[0]));
       }
     } else {
 #pragma unroll
       for (int k = 0; k < NV; ++k)
-        if (k < nv) acc[k] = fma(__ldg(V.p[k] + i), wi, acc[k]);
+        if (k < nv) {
+          const double2 vk = pair ? __ldg(reinterpret_cast<const double2 *>(V.p[k]) + i)
+                                  : make_double2(__ldg(V.p[k] + is), 0.0);
+          acc[k] = fma(vk.y, wv.y, fma(vk.x, wv.x, acc[k]));
+        }
     }
   }
   if (MODE == 3) return;
@@ -118,8 +137,17 @@ template <int MODE>
 void krylov_launch(const double *const *V, int nv, double *w, const double *coef, int64_t n, double *partials,
                    int nblk, cudaStream_t s, double sgn = -1.0) {
   Ptrs P{};
-  for (int k = 0; k < nv; ++k) P.p[k] = V[k];
+  uintptr_t al = (uintptr_t)w;
+  for (int k = 0; k < nv; ++k) {
+    P.p[k] = V[k];
+    al |= (uintptr_t)V[k];
+  }
   const int stride = (MODE == 2) ? 1 : nv;
+  if (al & 15) {  // a vector not 16-byte aligned (e.g. a user's tensor view): the scalar form
+    k_krylov<32, MODE, false><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
+    ++g_launches;
+    return;
+  }
   if (nv <= 4) k_krylov<4, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
   else if (nv <= 8) k_krylov<8, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);
   else if (nv <= 16) k_krylov<16, MODE><<<nblk, 256, 0, s>>>(P, nv, w, coef, n, partials, stride, sgn);

@@ -139,3 +139,30 @@ def test_large_level_residual_ragged_chunks(n, k, q, N):
         refy = -p.residual_node(i, u, zero)
         assert np.max(np.abs(yg[i] - refy)) <= 1e-10 * max(np.max(np.abs(refy)), 1e-300), (I, J)
     ctx.close()
+
+
+def test_misaligned_vectors_rejected():
+    """Device vectors must be 16-byte aligned (include/wrmg.h): a view at an odd double
+    offset fails loudly with WRMG_E_INVALID instead of faulting a kernel."""
+    import torch
+
+    import paper_2407_13997_b200 as w
+    from paper_2407_13997_b200._lib import WrmgError
+    c = w.Context(8, 8, 1.0 / 8, degree=2, q=1, nslabs=4, dt=0.25)
+    n = c.layout["ndof"]
+    f = c.empty()
+    c.fill_uniform(f, 0, 3)
+    b = c.empty()
+    c.rhs(f, b)
+    bb = torch.zeros(n + 1, dtype=torch.float64, device="cuda:0")
+    xb = torch.zeros(n + 1, dtype=torch.float64, device="cuda:0")
+    bb[1:].copy_(b)
+    for call in (lambda: c.fgmres(bb[1:], xb[1:]), lambda: c.residual(xb[1:], bb[1:], c.empty()),
+                 lambda: c.smooth(xb[1:], b, 1, 1.0), lambda: c.vcycle(bb[1:], c.empty())):
+        with pytest.raises(WrmgError) as ei:
+            call()
+        assert "INVALID" in str(ei.value)
+    x = c.empty()  # the aligned call still works after the rejections
+    its, rel, st = c.fgmres(b, x)
+    assert st == "WRMG_OK" and its > 0
+    c.close()
