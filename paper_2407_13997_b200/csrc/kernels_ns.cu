@@ -249,13 +249,25 @@ __global__ void __launch_bounds__(256) k_ns_residual(int64_t ns, int N, const in
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
+        if constexpr (NQ == 2) {  // DG1: the slab's two values as one 16-byte load (NT even, offsets even)
+          const double2 uv = __ldg(reinterpret_cast<const double2 *>(u + cb[k]));
+          ub[k][0] = uv.x;
+          ub[k][1 % NQ] = uv.y;
+        } else {
 #pragma unroll
-        for (int bb = 0; bb < NQ; ++bb) ub[k][bb] = __ldg(u + cb[k] + bb);
+          for (int bb = 0; bb < NQ; ++bb) ub[k][bb] = __ldg(u + cb[k] + bb);
+        }
         um[k] = n > 0 ? __ldg(u + cb[k] - 1) : 0.0;
         if (hasconv) {
           const double *cv = conv + (int64_t)(vb + (k < cnt ? e + k : e) - e0) * NT + (int64_t)n * NQ;
+          if constexpr (NQ == 2) {
+            const double2 cw = k < cnt ? __ldg(reinterpret_cast<const double2 *>(cv)) : make_double2(0.0, 0.0);
+            w[k][0] = cw.x;
+            w[k][1 % NQ] = cw.y;
+          } else {
 #pragma unroll
-          for (int c = 0; c < NQ; ++c) w[k][c] = k < cnt ? __ldg(cv + c) : 0.0;
+            for (int c = 0; c < NQ; ++c) w[k][c] = k < cnt ? __ldg(cv + c) : 0.0;
+          }
         }
       }
 #pragma unroll
@@ -281,8 +293,17 @@ __global__ void __launch_bounds__(256) k_ns_residual(int64_t ns, int N, const in
     const int ev1 = e0 + nvv;
     for (int e = e0; e < ev1; e += U) batch(e, min(U, ev1 - e), true);
     for (int e = ev1; e < e1; e += U) batch(e, min(U, e1 - e), false);
+    if constexpr (NQ == 2) {
+      double2 o = make_double2(acc[0], acc[1 % NQ]);
+      if (b) {
+        const double2 bv = *reinterpret_cast<const double2 *>(b + base);
+        o = make_double2(bv.x - o.x, bv.y - o.y);
+      }
+      *reinterpret_cast<double2 *>(r + base) = o;
+    } else {
 #pragma unroll
-    for (int a = 0; a < NQ; ++a) r[base + a] = b ? b[base + a] - acc[a] : acc[a];
+      for (int a = 0; a < NQ; ++a) r[base + a] = b ? b[base + a] - acc[a] : acc[a];
+    }
   }
 }
 
