@@ -6,7 +6,8 @@ import torch
 sys.path.insert(0, ".")
 import paper_2407_13997_b200 as w  # noqa: E402
 
-c = w.Context(128, 128, 1.0 / 128, degree=3, q=1, nslabs=128, dt=1.0 / 128, kappa=1.0)
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+c = w.Context(n, n, 1.0 / n, degree=3, q=1, nslabs=128, dt=1.0 / 128, kappa=1.0)
 u, b, r = c.empty(), c.empty(), c.empty()
 c.fill_uniform(u, 0, 1)
 c.fill_uniform(b, 0, 2)
@@ -20,4 +21,5 @@ for _ in range(20):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 20
-print(f"residual {ms * 1e3:.1f} us  {911.0e6 / (ms / 1e3) / 1e9:.0f} GB/s")
+nb = 24.0 * c.layout["ndof"]
+print(f"n={n} residual {ms * 1e3:.1f} us  {nb / (ms / 1e3) / 1e9:.0f} GB/s")
