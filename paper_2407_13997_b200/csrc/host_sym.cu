@@ -280,6 +280,11 @@ bool sym_factor(int k, const double *Mp, const double *Kp, const Temporal &tm, S
       }
       for (int e = 0; e < nq * nq; ++e) out->S[mode * 16 + e] = inv[e];
       out->sig[mode] = inv[(nq - 1) * nq + 0];
+      double pp = out->sig[mode];  // the squarings the scan would form in-kernel, bit for bit
+      for (int k2 = 0; k2 < 5; ++k2) {
+        out->sig2[k2][mode] = pp;
+        pp *= pp;
+      }
     }
   }
   return true;

@@ -73,6 +73,7 @@ struct SymTab {
   double V[7 * 7 + 3 * 3 + 4 * 4 + 5 * 5];
   double S[kSymMaxMP * 16];
   double sig[kSymMaxMP];
+  double sig2[5][kSymMaxMP];  // sig^(2^k), the shuffle-scan coefficients (host_sym.cu)
 };
 
 // 2 x 2 vertex tiles of the symmetric class (kernels_sweep_sym.cu, tiled form): the

@@ -213,7 +213,7 @@ __device__ __forceinline__ void sym_patch_chunk(const SymTab &P, const int *snod
 // instead of registers (fewer live registers -> more warps per SM); on return buf
 // holds the weighted corrections wt[slot] x[slot] for the contiguous atomics.
 template <int D, int B, int VO, int MODE0, int NQ>
-__device__ __forceinline__ void sym_block_s(const SymTab &P, double *yb, double *ycar, int lane) {
+__device__ __forceinline__ void sym_block_s(const SymTab &P, const double *spw, double *yb, double *ycar, int lane) {
   auto Y = [&](int j, int a) -> double & { return yb[j * 32 * NQ + a]; };
   double t[NQ][D];
 #pragma unroll
@@ -242,20 +242,16 @@ __device__ __forceinline__ void sym_block_s(const SymTab &P, double *yb, double 
       for (int b2 = 0; b2 < NQ; ++b2) s = fma(P.S[md * 16 + a * NQ + b2], gh[b2], s);
       t[a][i] = s;
     }
-    const double sg = P.sig[md];
-    double v = t[NQ - 1][i], pp = sg;
+    // inclusive scan of the end-trace recurrence over the warp's 32 slabs: predicated
+    // DFMAs with the constant-bank sig^(2^k) (lanes below the distance keep v exactly,
+    // as fma(0, o, v) would), and sig^(lane + 1) from the CTA's table
+    double v = t[NQ - 1][i];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double o = __shfl_up_sync(0xffffffffu, v, d);
-      v = fma(lane >= d ? pp : 0.0, o, v);
-      pp *= pp;
+    for (int k2 = 0; k2 < 5; ++k2) {
+      const double o = __shfl_up_sync(0xffffffffu, v, 1 << k2);
+      if (lane >= (1 << k2)) v = fma(P.sig2[k2][md], o, v);
     }
-    double pw = 1.0, bs = sg;
-#pragma unroll
-    for (int bit = 0; bit < 6; ++bit) {
-      pw *= (((lane + 1) >> bit) & 1) ? bs : 1.0;
-      bs *= bs;
-    }
+    const double pw = spw[md * 32 + lane];
     const double yc = ycar[md];
     const double yn = fma(pw, yc, v);
     double yp = __shfl_up_sync(0xffffffffu, yn, 1);
@@ -279,7 +275,8 @@ __device__ __forceinline__ void sym_block_s(const SymTab &P, double *yb, double 
 }
 
 template <int K, int NQ>
-__device__ __forceinline__ void sym_patch_chunk_s(const SymTab &P, const int *snode, const double *swt, double *ycar,
+__device__ __forceinline__ void sym_patch_chunk_s(const SymTab &P, const double *spw, const int *snode, const double *swt,
+                                                  double *ycar,
                                                   int n, bool valid, int64_t NT, const double *__restrict__ r,
                                                   int lane, double *buf) {
   using S = Sh<K>;
@@ -307,10 +304,10 @@ __device__ __forceinline__ void sym_patch_chunk_s(const SymTab &P, const int *sn
       for (int j = 0; j < MP; ++j) yb[j * 32 * NQ + a] = y[j];
     }
   }
-  sym_block_s<S::D0, S::B0, S::V0, S::B0, NQ>(P, yb, ycar, lane);
-  sym_block_s<S::D1, S::B1, S::V1, S::B1, NQ>(P, yb, ycar, lane);
-  sym_block_s<S::D2, S::B2, S::V2, S::B2, NQ>(P, yb, ycar, lane);
-  sym_block_s<S::D3, S::B3, S::V3, S::B3, NQ>(P, yb, ycar, lane);
+  sym_block_s<S::D0, S::B0, S::V0, S::B0, NQ>(P, spw, yb, ycar, lane);
+  sym_block_s<S::D1, S::B1, S::V1, S::B1, NQ>(P, spw, yb, ycar, lane);
+  sym_block_s<S::D2, S::B2, S::V2, S::B2, NQ>(P, spw, yb, ycar, lane);
+  sym_block_s<S::D3, S::B3, S::V3, S::B3, NQ>(P, spw, yb, ycar, lane);
 #pragma unroll
   for (int a = 0; a < NQ; ++a) {
     double y[MP], x[MP];
@@ -524,10 +521,21 @@ __global__ void __launch_bounds__(128, 4) k_sweep_sym(int N, int64_t npatch, con
   __shared__ int snode[WPC][MP];
   __shared__ double swt[WPC][MP];
   __shared__ double sycar[WPC][MP];  // end trace of every mode at the previous chunk's last slab
+  __shared__ double spw[MP * 32];     // sig_mode^(lane + 1): the carry's weight in the scan
   extern __shared__ __align__(16) double stage[];  // [WPC][MP][32][NQ]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t NT = (int64_t)N * NQ;
   const int nch = (N + 31) / 32;
+  for (int e = threadIdx.x; e < MP * 32; e += blockDim.x) {
+    const int l = e & 31;
+    double pw = 1.0, bs = P.sig[e >> 5];  // binary powering, as the in-warp form formed it
+    for (int bit = 0; bit < 6; ++bit) {
+      pw *= (((l + 1) >> bit) & 1) ? bs : 1.0;
+      bs *= bs;
+    }
+    spw[e] = pw;
+  }
+  __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * WPC + w; i < npatch; i += (int64_t)gridDim.x * WPC) {
     const int64_t p = list ? list[i] : i;
     __syncwarp();
@@ -545,7 +553,7 @@ __global__ void __launch_bounds__(128, 4) k_sweep_sym(int N, int64_t npatch, con
       // contiguous run of 32 NQ atomics per node (lanes on consecutive doubles: fewer
       // L2 sectors per instruction than lane = slab with stride NQ)
       double *stg = stage + (size_t)w * MP * 32 * NQ;
-      sym_patch_chunk_s<K, NQ>(P, snode[w], swt[w], sycar[w], n, valid, NT, r, lane, stg);
+      sym_patch_chunk_s<K, NQ>(P, spw, snode[w], swt[w], sycar[w], n, valid, NT, r, lane, stg);
       __syncwarp();
       const int64_t t0 = (int64_t)ch * 32 * NQ;
       const int nv = (int)min((int64_t)32 * NQ, NT - t0);  // valid values of this chunk
