@@ -278,6 +278,25 @@ __global__ void __launch_bounds__(256, 2) k_sweep_kron(int N, int C, int PP, con
   }
   for (int e = tid; e < MP * NQ * NQ; e += blockDim.x) sS[e] = Sg[(size_t)ty * MP * NQ * NQ + e];
   for (int e = tid; e < MP; e += blockDim.x) ssig[e] = sigg[(size_t)ty * MP + e];
+  // scan coefficients: sig_i^(2^k) and sig_i^(lane + 1), formed once per CTA by the
+  // squarings / binary powering each warp formed per mode before (bit-identical)
+  __shared__ double ssig2[5][MP];
+  __shared__ double spw[MP * 32];
+  for (int e = tid; e < MP * 32; e += blockDim.x) {
+    const double sg = sigg[(size_t)ty * MP + (e >> 5)];
+    const int ex = (e & 31) + 1;
+    double pw = 1.0, bs = sg;
+    for (int bit = 0; bit < 6; ++bit) {
+      pw *= ((ex >> bit) & 1) ? bs : 1.0;
+      bs *= bs;
+    }
+    spw[e] = pw;
+    if ((e & 31) < 5) {
+      double p = sg;
+      for (int k = 0; k < (e & 31); ++k) p *= p;
+      ssig2[e & 31][e >> 5] = p;
+    }
+  }
   for (int e = tid; e < PP * MP; e += blockDim.x) {
     const int pp = e / MP, j = e % MP;
     const int p = cta_patch[(size_t)cta * PP + pp];
@@ -328,12 +347,11 @@ __global__ void __launch_bounds__(256, 2) k_sweep_kron(int N, int C, int PP, con
       for (int b2 = 0; b2 < NQ; ++b2) s = fma(sS[(i * NQ + a) * NQ + b2], gh[b2], s);
       t[a][i] = s;
     }
-    double v = t[NQ - 1][i], p = ssig[i];
+    double v = t[NQ - 1][i];
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double o = __shfl_up_sync(0xffffffffu, v, d);
-      v = fma(lane >= d ? p : 0.0, o, v);
-      p *= p;
+    for (int k = 0; k < 5; ++k) {
+      const double o = __shfl_up_sync(0xffffffffu, v, 1 << k);
+      if (lane >= (1 << k)) v = fma(ssig2[k][i], o, v);
     }
     t[NQ - 1][i] = v;
     if (lane == 31) scar[(pp * C + c) * MP + i] = v;
@@ -348,13 +366,7 @@ __global__ void __launch_bounds__(256, 2) k_sweep_kron(int N, int C, int PP, con
     for (int d = 0; d < 5; ++d) s32 *= s32;
     double Y = 0.0;
     for (int c2 = 0; c2 < c; ++c2) Y = fma(s32, Y, scar[(pp * C + c2) * MP + i]);
-    double pw = 1.0, bs = sg;
-    const int e = lane + 1;
-#pragma unroll
-    for (int bit = 0; bit < 6; ++bit) {
-      pw *= ((e >> bit) & 1) ? bs : 1.0;
-      bs *= bs;
-    }
+    const double pw = spw[i * 32 + lane];
     const double y = fma(pw, Y, t[NQ - 1][i]);
     double yp = __shfl_up_sync(0xffffffffu, y, 1);
     if (lane == 0) yp = Y;
