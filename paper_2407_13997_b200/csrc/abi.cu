@@ -294,11 +294,11 @@ void prof_sweep(wrmg_ctx *c, int l, const double *r, double *u, double om) {
   if (c->use_kron) {
     const Level &L = c->lv[l];
     // WRMG_SWEEP_SIDE=1: boundary classes on a side stream, concurrently with the symmetric
-    // class (C2: finest level 0.4 ms per solve faster, coarser levels slower: off by default)
-    static const bool side = [] {
-      const char *e = getenv("WRMG_SWEEP_SIDE");
-      return e && e[0] == '1';
-    }();
+    // class (C2, finest level only or every level: within noise of the serial order, 23.84-24.00
+    // vs 23.90-23.91 ms per solve; coarser levels alone slower: off by default).  Read per
+    // launch: the parity tests switch it.
+    const char *se = getenv("WRMG_SWEEP_SIDE");
+    const bool side = se && se[0] == '1';
     if (side && L.sym_ok && L.nsym > 0 && (L.kron_ngrp8 > 0 || L.kron_ncta > 0)) {
       // fork: the boundary classes on the side stream while the symmetric class runs
       if (!c->side) {

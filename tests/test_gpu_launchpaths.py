@@ -140,3 +140,12 @@ def test_symmetric_sweep_sampled(n, k, q, N):
     nodes = [(1, 1), (2, 1), (1, 2), (k, k), (k + 1, k), (2 * k, 1), (m, m), (m + 1, m), (m, m + 1),
              (m + 1, m + 2), (m + 2, m + 2), (L - 2, L - 2), (L - 2, m), (m, 1), (3 * k + 1, 2 * k + 2)]
     assert _sampled_sweep_check(n, k, q, N, nodes) <= 1e-10
+
+
+@pytest.mark.parametrize("side", ["1", "0"])
+def test_side_stream_boundary_sweep(monkeypatch, side):
+    """WRMG_SWEEP_SIDE=1: the boundary classes' Kronecker sweep runs on a side stream
+    concurrently with the symmetric class (opt-in); =0, the default, serialises them.  Both: full vectors of three
+    sweeps, one V(1,1) and the FGMRES count against the oracle (P3 x DG1, 40 x 40)."""
+    monkeypatch.setenv("WRMG_SWEEP_SIDE", side)
+    test_dmma_sweep_vcycle_fgmres(40, 3, 20, 5, 19)
