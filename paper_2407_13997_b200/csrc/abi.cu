@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <functional>
 #include <mutex>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges per API call and kernel phase
 #include <map>
 #include <utility>
 #include <cstring>
@@ -177,6 +179,20 @@ cudaEvent_t get_event(wrmg_ctx *c) {
 
 // Records a CUDA event pair around the launches issued in its scope (on the
 // context's stream) when profiling is on, with the launches' algorithmic cost.
+// NVTX range names of the kernel phases, "<class>_L<level>" (built once; no formatting per call)
+const char *phase_name(int cls, int lvl) {
+  static const char *kCls[] = {"residual", "sweep", "restrict", "prolong", "coarse", "krylov", "factor"};
+  constexpr int kNc = (int)(sizeof(kCls) / sizeof(kCls[0])), kNl = 32;
+  static const std::vector<std::string> names = [] {
+    std::vector<std::string> v;
+    for (int c2 = 0; c2 < kNc; ++c2)
+      for (int l = 0; l < kNl; ++l) v.push_back(std::string(kCls[c2]) + "_L" + std::to_string(l));
+    return v;
+  }();
+  if (cls < 0 || cls >= kNc || lvl < 0 || lvl >= kNl) return "phase";
+  return names[(size_t)cls * kNl + lvl].c_str();
+}
+
 struct PScope {
   wrmg_ctx *c;
   int cls, lvl;
@@ -184,6 +200,7 @@ struct PScope {
   cudaEvent_t a = nullptr, b = nullptr;
   PScope(wrmg_ctx *c_, int cls_, int lvl_, double bytes_, double flops_)
       : c(c_), cls(cls_), lvl(lvl_), bytes(bytes_), flops(flops_) {
+    nvtxRangePushA(phase_name(cls, lvl));
     if (c->prof_on) {
       a = get_event(c);
       b = get_event(c);
@@ -195,6 +212,7 @@ struct PScope {
       cudaEventRecord(b, c->stream);
       c->prof_recs.push_back({cls, lvl, a, b, bytes, flops});
     }
+    nvtxRangePop();
   }
 };
 
@@ -1552,18 +1570,26 @@ double dot_host(wrmg_ctx *c, const double *a, const double *b, int64_t n) {
 // Every exported entry point runs on the context's device and restores the
 // caller's current device on return (wrmg_setup used to leave the
 // calling thread on coeffs.device and later calls used whatever was current).
+// Entry-point guard: the context's device for the call (the caller's restored after), and
+// an NVTX range named after the entry point.
 struct DevGuard {
   int prev = -1, dev = -1;
-  explicit DevGuard(int d) : dev(d) {
+  bool named = false;
+  explicit DevGuard(int d, const char *name = nullptr) : dev(d) {
+    if (name) {
+      nvtxRangePushA(name);
+      named = true;
+    }
     if (dev < 0 || cudaGetDevice(&prev) != cudaSuccess) {
       dev = -1;
       return;
     }
     if (prev != dev) cudaSetDevice(dev);
   }
-  explicit DevGuard(const wrmg_ctx *c) : DevGuard(c ? c->co.device : -1) {}
+  explicit DevGuard(const wrmg_ctx *c, const char *name = nullptr) : DevGuard(c ? c->co.device : -1, name) {}
   ~DevGuard() {
     if (dev >= 0 && prev != dev) cudaSetDevice(prev);
+    if (named) nvtxRangePop();
   }
 };
 
@@ -1699,7 +1725,7 @@ wrmg_status wrmg_plan_ns_strip(const wrmg_mesh *mesh, int32_t degree, int32_t ra
 wrmg_status wrmg_setup(const wrmg_mesh *mesh, int32_t degree, int32_t q, int32_t nslabs, double dt,
                        const wrmg_coeffs *coeffs, wrmg_ctx **out) {
   wrmg_ctx *c = nullptr;
-  DevGuard dg_(coeffs ? coeffs->device : -1);
+  DevGuard dg_(coeffs ? coeffs->device : -1, "wrmg_setup");
   try {
     if (!out) throw Err{WRMG_E_INVALID, "out is NULL"};
     *out = nullptr;
@@ -2165,7 +2191,7 @@ wrmg_status wrmg_layout(const wrmg_ctx *c, wrmg_layout_t *out) {
 
 wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
   if (!c || (state && !al16(state))) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     if (c->ns) {
       factor_all_ns(c, state);
@@ -2181,7 +2207,7 @@ wrmg_status wrmg_linearize(wrmg_ctx *c, const double *state) {
 
 wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
   if (!c || !fhat || !b || !al16(fhat, b)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     if (c->ns) {  // R6 (C3): b = drawn values on free rows, 0 on constrained rows, pressure mean-projected
       const Level &L = c->lv.back();
@@ -2200,7 +2226,7 @@ wrmg_status wrmg_rhs(wrmg_ctx *c, const double *fhat, double *b) {
 
 wrmg_status wrmg_rhs_initial(wrmg_ctx *c, const double *u0, double *b) {
   if (!c || !u0 || !b || !al16(u0, b)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     launch_rhs_initial(c->lv.back(), c->nq, c->nt, c->tm.phi0, u0, b, c->stream);
     check_launch();
@@ -2216,7 +2242,7 @@ wrmg_status wrmg_set_boundary_values(wrmg_ctx *c, const double *g) {
     c->err = "wrmg_set_boundary_values: Navier-Stokes contexts only";
     return WRMG_E_UNSUPPORTED;
   }
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     const int64_t n = c->lv.back().nnode * c->nt;
     if (!g) {
@@ -2242,7 +2268,7 @@ wrmg_status wrmg_cheb_lambda(const wrmg_ctx *c, int32_t level, double *lam) {
 wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double *r, int32_t nonlinear) {
   if (!c || !u || !b || !r || !al16(u, b, r)) return WRMG_E_INVALID;
   if (nonlinear && !c->ns) return WRMG_E_UNSUPPORTED;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     if (nonlinear) {
       if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(u));
@@ -2261,7 +2287,7 @@ wrmg_status wrmg_residual(wrmg_ctx *c, const double *u, const double *b, double 
 
 wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
   if (!c || !x || !y || !al16(x, y)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     if (c->strip) halo_forward(c, c->lv.back(), const_cast<double *>(x));
     prof_residual(c, (int)c->lv.size() - 1, x, nullptr, y, false);  // b = NULL: y = A x
@@ -2274,7 +2300,7 @@ wrmg_status wrmg_apply(wrmg_ctx *c, const double *x, double *y) {
 
 wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps, double omega) {
   if (!c || !u || !b || nsweeps < 0 || !al16(u, b)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     const int l = (int)c->lv.size() - 1;
     for (int s = 0; s < nsweeps; ++s) {
@@ -2297,7 +2323,7 @@ wrmg_status wrmg_smooth(wrmg_ctx *c, double *u, const double *b, int32_t nsweeps
 
 wrmg_status wrmg_vcycle(wrmg_ctx *c, const double *r, double *z) {
   if (!c || !r || !z || !al16(r, z)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     vcycle_level(c, (int)c->lv.size() - 1, r, z);
     check_launch();
@@ -2315,7 +2341,7 @@ wrmg_status wrmg_level_size(const wrmg_ctx *c, int32_t level, int64_t *nnode) {
 
 wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *rc) {
   if (!c || !rf || !rc || level < 1 || level >= (int)c->lv.size() || !al16(rf, rc)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     launch_restrict(c->lv[level - 1], c->nt, rf, rc, c->stream);
     check_launch();
@@ -2327,7 +2353,7 @@ wrmg_status wrmg_restrict(wrmg_ctx *c, int32_t level, const double *rf, double *
 
 wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, double *uf) {
   if (!c || !ec || !uf || level < 1 || level >= (int)c->lv.size() || !al16(ec, uf)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     launch_prolong_add(c->lv[level - 1], c->nt, ec, uf, c->stream);
     check_launch();
@@ -2340,7 +2366,7 @@ wrmg_status wrmg_prolong_add(wrmg_ctx *c, int32_t level, const double *ec, doubl
 wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart, int32_t maxit, double rtol,
                         double atol, int32_t *iters, double *relres) {
   if (!c || !b || !x || restart < 1 || restart > 31 || maxit < 1 || !al16(b, x)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     cudaStream_t s = c->stream;
     Level &L = c->lv.back();
@@ -2549,7 +2575,7 @@ wrmg_status wrmg_fgmres(wrmg_ctx *c, const double *b, double *x, int32_t restart
 
 wrmg_status wrmg_stationary(wrmg_ctx *c, const double *b, double *u, int32_t ncycles) {
   if (!c || !b || !u || ncycles < 0 || !al16(b, u)) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     const int top = (int)c->lv.size() - 1;
     const int64_t n = c->lv.back().nnode * c->nt;
@@ -2575,7 +2601,7 @@ wrmg_status wrmg_fgmres_host(wrmg_ctx *c, int32_t nrhs, const double *const *b_h
                              int32_t restart, int32_t maxit, double rtol, double atol, int32_t *iters,
                              double *relres) {
   if (!c || nrhs < 0 || (nrhs > 0 && (!b_host || !x_host))) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     const int64_t n = c->lv.back().nnode * c->nt;
     const size_t bytes = (size_t)n * sizeof(double);
@@ -2625,7 +2651,7 @@ wrmg_status wrmg_fgmres_host(wrmg_ctx *c, int32_t nrhs, const double *const *b_h
 
 wrmg_status wrmg_profile(wrmg_ctx *c, int32_t enable) {
   if (!c) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     CK(cudaStreamSynchronize(c->stream));
     for (auto &r : c->prof_recs) {
@@ -2643,7 +2669,7 @@ wrmg_status wrmg_profile(wrmg_ctx *c, int32_t enable) {
 
 wrmg_status wrmg_kernel_stats(wrmg_ctx *c, wrmg_kernel_stat *out) {
   if (!c || !out) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     CK(cudaStreamSynchronize(c->stream));
     for (auto &r : c->prof_recs) {
@@ -2700,7 +2726,7 @@ void wrmg_loopback_destroy(void *hub) { loop_hub_destroy(hub); }
 
 wrmg_status wrmg_debug_fetch(wrmg_ctx *c, int32_t level, int32_t which, void *host_dst, int64_t count) {
   if (!c || !host_dst || count < 0 || level < 0 || level >= (int)c->lv.size()) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     const Level &L = c->lv[level];
     const void *src = nullptr;
@@ -2748,7 +2774,7 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
     return WRMG_E_UNSUPPORTED;
   }
   if (!al16(U) || (rhs && !al16(rhs))) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     cudaStream_t s = c->stream;
     Level &L = c->lv.back();
@@ -2803,7 +2829,7 @@ wrmg_status wrmg_newton_rhs(wrmg_ctx *c, double *U, const double *rhs, double rt
 
 wrmg_status wrmg_batched_lu(const wrmg_ctx *c, double *A, int32_t m, int32_t batch, int32_t *piv, int32_t *info) {
   if (!A || !piv || !info || m < 1 || batch < 0) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     cudaStream_t s = c ? c->stream : nullptr;
     launch_batched_lu(A, m, batch, piv, info, s);
@@ -2824,7 +2850,7 @@ wrmg_status wrmg_batched_lu(const wrmg_ctx *c, double *A, int32_t m, int32_t bat
 
 wrmg_status wrmg_fill_uniform(const wrmg_ctx *c, double *out, int64_t count, uint64_t first_id, uint64_t seed) {
   if (!out || count < 0) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     launch_fill_uniform(out, count, first_id, seed, c ? c->stream : nullptr);
     check_launch();
@@ -2836,7 +2862,7 @@ wrmg_status wrmg_fill_uniform(const wrmg_ctx *c, double *out, int64_t count, uin
 
 wrmg_status wrmg_sync(wrmg_ctx *c) {
   if (!c) return WRMG_E_INVALID;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   try {
     CK(cudaStreamSynchronize(c->stream));
     check_launch();
@@ -2856,7 +2882,7 @@ const char *wrmg_last_error(const wrmg_ctx *c, int32_t *level, int32_t *patch, i
 
 void wrmg_destroy(wrmg_ctx *c) {
   if (!c) return;
-  DevGuard dg_(c);
+  DevGuard dg_(c, __func__);
   if (c->stream) cudaStreamSynchronize(c->stream);
   dfree(c->st_r);
   dfree(c->st_z);
