@@ -4,7 +4,7 @@ Holds none of the method's arithmetic: only the counter-based generator of
 DESIGN.md R6 and the canonical-index helpers needed to call it.  Both
 ``oracle/`` and the tests/bench use it to draw the SAME inputs; the CUDA library
 carries its own independent implementation of the same generator
-(csrc/kernels_misc.cu, ``wrmg_fill_uniform``), checked equal by tests.
+(csrc/kernels_solve.cu ``k_fill_uniform``, exported as ``wrmg_fill_uniform``), checked equal by tests.
 
 splitmix64 finaliser at canonical id g (uint64, mod 2^64):
     z = g + (seed + 1) * 0x9E3779B97F4A7C15
