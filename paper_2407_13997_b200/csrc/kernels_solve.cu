@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(256) k_spmv_nt(int64_t nrow, int64_t NT2, cons
   const int e0 = rp[i], e1 = rp[i + 1];
   if (ACC && e0 == e1) return;
   double2 acc = make_double2(0.0, 0.0);
+  double2 o = ACC ? y[idx] : make_double2(0.0, 0.0);  // loaded ahead of the gather loop
 #pragma unroll 4
   for (int e = e0; e < e1; ++e) {
     const double a = __ldg(v + e);
@@ -252,7 +253,6 @@ __global__ void __launch_bounds__(256) k_spmv_nt(int64_t nrow, int64_t NT2, cons
     acc.y = fma(a, xv.y, acc.y);
   }
   if (ACC) {
-    double2 o = y[idx];
     o.x += acc.x;
     o.y += acc.y;
     y[idx] = o;
@@ -291,6 +291,10 @@ __global__ void __launch_bounds__(256) k_spmv_nt_tp(int64_t nrow, int64_t NT2, c
   double2 acc[TP];
 #pragma unroll
   for (int p = 0; p < TP; ++p) acc[p] = make_double2(0.0, 0.0);
+  double2 *yr = y + i * NT2 + t;
+  double2 yo[TP];  // ACC: the row's old values, loaded ahead of the gather loop
+#pragma unroll
+  for (int p = 0; p < TP; ++p) yo[p] = ACC ? yr[p * W] : make_double2(0.0, 0.0);
 #pragma unroll 2
   for (int e = e0; e < e1; ++e) {
     const double a = __ldg(v + e);
@@ -302,11 +306,10 @@ __global__ void __launch_bounds__(256) k_spmv_nt_tp(int64_t nrow, int64_t NT2, c
       acc[p].y = fma(a, xv.y, acc[p].y);
     }
   }
-  double2 *yr = y + i * NT2 + t;
 #pragma unroll
   for (int p = 0; p < TP; ++p) {
     if (ACC) {
-      double2 o = yr[p * W];
+      double2 o = yo[p];
       o.x += acc[p].x;
       o.y += acc[p].y;
       yr[p * W] = o;
