@@ -106,6 +106,7 @@ T *dalloc(size_t n) {
   const size_t bytes = n * sizeof(T);
   CK(cudaMalloc(&p, bytes + 2 * kGuard));
   CK(cudaMemset(p, 0xFF, bytes + 2 * kGuard));
+  CK(cudaStreamSynchronize(cudaStreamLegacy));  // the fill runs on the legacy stream: contexts on non-blocking streams are not ordered after it
   char *u = (char *)p + kGuard;
   std::lock_guard<std::mutex> lk(g_guard_mu);
   g_guard_sizes[u] = bytes;
@@ -117,6 +118,7 @@ template <class T>
 T *dzalloc(size_t n) {
   T *p = dalloc<T>(n);
   CK(cudaMemset(p, 0, (n ? n : 1) * sizeof(T)));
+  CK(cudaStreamSynchronize(cudaStreamLegacy));  // as above: the zeros must be in place before the context's stream uses p
   return p;
 }
 

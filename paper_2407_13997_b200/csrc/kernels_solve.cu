@@ -278,8 +278,11 @@ __global__ void k_spmv_nt1(int64_t nrow, int64_t NT, const int32_t *__restrict__
 
 // Same with each thread on TP pairs spaced NT2 / TP apart (NT2 % TP == 0): the row's
 // index and value loads are shared by TP gathers, TP 16-byte loads in flight per entry.
+// The kernel is latency-bound, so registers are capped for occupancy (measured on C2's finest
+// level): prolongation (ACC) 4 CTAs/SM with the entry loop unrolled twice,
+// restriction 5 CTAs/SM without unrolling.
 template <bool ACC, int TP>
-__global__ void __launch_bounds__(256) k_spmv_nt_tp(int64_t nrow, int64_t NT2, const int32_t *__restrict__ rp,
+__global__ void __launch_bounds__(256, ACC ? 4 : 5) k_spmv_nt_tp(int64_t nrow, int64_t NT2, const int32_t *__restrict__ rp,
                                                     const int32_t *__restrict__ ci, const double *__restrict__ v,
                                                     const double2 *__restrict__ x, double2 *__restrict__ y) {
   const int64_t W = NT2 / TP;
@@ -295,7 +298,8 @@ __global__ void __launch_bounds__(256) k_spmv_nt_tp(int64_t nrow, int64_t NT2, c
   double2 yo[TP];  // ACC: the row's old values, loaded ahead of the gather loop
 #pragma unroll
   for (int p = 0; p < TP; ++p) yo[p] = ACC ? yr[p * W] : make_double2(0.0, 0.0);
-#pragma unroll 2
+  constexpr int kTpUnroll = ACC ? 2 : 1;
+#pragma unroll kTpUnroll
   for (int e = e0; e < e1; ++e) {
     const double a = __ldg(v + e);
     const double2 *xr = x + (int64_t)__ldg(ci + e) * NT2 + t;
